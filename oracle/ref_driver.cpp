@@ -1,0 +1,142 @@
+// Test infrastructure (oracle side) — NOT product code.
+//
+// Thin command-line driver over the UNMODIFIED reference engine (linked from
+// oracle/_ref/libpystachio_ref.a, built by oracle/build_ref.sh from /root/reference/proj/src).
+// It only calls the reference's public API:
+//   gen  -> pystachio::gen_workload            (/root/reference/proj/src/bench.cpp:85-114)
+//   run  -> pystachio::run_socket_pipeline      (/root/reference/proj/src/pipeline_harness.cpp:81-109)
+//           pystachio::run_sim_pipeline         (/root/reference/proj/src/pipeline_harness.cpp:23-79)
+// and prints one JSON line with result checksums (rowhash = sum over rows of FNV-1a64 of the
+// row's little-endian words) plus wall time, optionally dumping the raw rows.
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iostream>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "pystachio/bench.hpp"
+#include "pystachio/hashing.hpp"
+#include "pystachio/pipeline_harness.hpp"
+#include "pystachio/psto.hpp"
+
+using namespace pystachio;
+
+namespace {
+
+std::string arg(int argc, char** argv, const std::string& key, const std::string& dflt) {
+  for (int i = 1; i + 1 < argc; ++i)
+    if (key == argv[i]) return argv[i + 1];
+  return dflt;
+}
+
+std::string read_file(const std::string& p) {
+  std::ifstream in(p);
+  if (!in) throw std::runtime_error("cannot open " + p);
+  std::stringstream ss;
+  ss << in.rdbuf();
+  return ss.str();
+}
+
+void summarize(const std::vector<std::vector<std::uint64_t>>& rows, std::size_t ncols, double secs,
+               const std::vector<std::size_t>& per_node, const std::string& dump) {
+  std::uint64_t rowhash = 0;
+  std::vector<std::uint64_t> colsum(ncols, 0);
+  for (const auto& r : rows) {
+    rowhash += fnv1a64(r.data(), r.size() * 8);
+    for (std::size_t c = 0; c < r.size() && c < ncols; ++c) colsum[c] += r[c];
+  }
+  std::printf("{\"rows\": %zu, \"ncols\": %zu, \"rowhash\": \"%016llx\", \"colsums\": [", rows.size(),
+              ncols, static_cast<unsigned long long>(rowhash));
+  for (std::size_t c = 0; c < ncols; ++c)
+    std::printf("%s\"%llu\"", c ? ", " : "", static_cast<unsigned long long>(colsum[c]));
+  std::printf("], \"per_node_rows\": [");
+  for (std::size_t i = 0; i < per_node.size(); ++i) std::printf("%s%zu", i ? ", " : "", per_node[i]);
+  std::printf("], \"seconds\": %.6f}\n", secs);
+  if (!dump.empty()) {
+    std::ofstream out(dump, std::ios::binary);
+    std::uint64_t n = rows.size(), k = ncols;
+    out.write(reinterpret_cast<const char*>(&n), 8);
+    out.write(reinterpret_cast<const char*>(&k), 8);
+    for (const auto& r : rows) out.write(reinterpret_cast<const char*>(r.data()), r.size() * 8);
+  }
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+  if (argc < 2) {
+    std::fprintf(stderr, "usage: ref_driver gen|run [options]\n");
+    return 2;
+  }
+  const std::string cmd = argv[1];
+  try {
+    if (cmd == "gen") {
+      GenWorkloadSpec spec;
+      spec.kind = arg(argc, argv, "--kind", "tpch") == "tpch" ? WorkloadKind::TpchAnalog
+                                                               : WorkloadKind::SyntheticJoin;
+      spec.out_dir = arg(argc, argv, "--out", "data");
+      spec.scale = std::stod(arg(argc, argv, "--scale", "0.01"));
+      spec.nodes = std::stoi(arg(argc, argv, "--nodes", "1"));
+      spec.devices = std::stoi(arg(argc, argv, "--devices", std::to_string(spec.nodes)));
+      spec.seed = std::stoull(arg(argc, argv, "--seed", "42"));
+      spec.codec = codec_from_string(arg(argc, argv, "--codec", "identity"));
+      spec.row_group_bytes = std::stoull(arg(argc, argv, "--rg-bytes", "1048576"));
+      const auto t0 = std::chrono::steady_clock::now();
+      const std::string manifest = gen_workload(spec);
+      const double s =
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      std::printf("{\"manifest\": \"%s\", \"seconds\": %.3f}\n", manifest.c_str(), s);
+      return 0;
+    }
+    if (cmd == "run") {
+      std::string plan = arg(argc, argv, "--plan-json", "");
+      if (plan.empty()) plan = read_file(arg(argc, argv, "--plan", "plan.json"));
+      const std::string data = arg(argc, argv, "--data", "data");
+      const ExecMode mode = exec_mode_from_string(arg(argc, argv, "--mode", "overlapped"));
+      const std::string backend = arg(argc, argv, "--backend", "socket");
+      const int nodes = std::stoi(arg(argc, argv, "--nodes", "1"));
+      const int repeat = std::stoi(arg(argc, argv, "--repeat", "1"));
+      const std::string dump = arg(argc, argv, "--dump", "");
+      for (int it = 0; it < repeat; ++it) {
+        std::vector<std::vector<std::uint64_t>> rows;
+        std::vector<std::size_t> per_node;
+        std::size_t ncols = 0;
+        const auto t0 = std::chrono::steady_clock::now();
+        if (backend == "sim") {
+          SimPipelineOptions opts;
+          opts.plan_json = plan;
+          opts.data_root = data;
+          opts.nodes = nodes;
+          opts.mode = mode;
+          auto outcome = run_sim_pipeline(opts);
+          for (const auto& r : outcome.per_node) {
+            per_node.push_back(r.rows.size());
+            ncols = std::max(ncols, r.schema.column_count());
+            rows.insert(rows.end(), r.rows.begin(), r.rows.end());
+          }
+        } else {
+          const std::uint16_t port =
+              static_cast<std::uint16_t>(std::stoi(arg(argc, argv, "--port", "47011")));
+          ClusterConfig cluster = ClusterConfig::loopback(1, port);
+          auto r = run_socket_pipeline(plan, data, cluster, 0, mode);
+          per_node.push_back(r.rows.size());
+          ncols = r.schema.column_count();
+          rows = std::move(r.rows);
+        }
+        const double s =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        summarize(rows, ncols, s, per_node, it == 0 ? dump : std::string());
+        std::fflush(stdout);
+      }
+      return 0;
+    }
+    std::fprintf(stderr, "unknown command %s\n", cmd.c_str());
+    return 2;
+  } catch (const std::exception& e) {
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return 1;
+  }
+}
