@@ -1,0 +1,176 @@
+/*
+ * psg.h — C-ABI boundary of the B200-native PystachIO hot path (paper 2512.02862).
+ *
+ * Plain pointers and sizes only; no torch/CUDA types cross this boundary. Every entry point
+ * replaces one reference interface (cited as /root/reference/proj/... file:line) so a maintainer
+ * can bind it from the reference's own C++  or from Python via ctypes
+ * (paper_2512_02862_b200/__init__.py).
+ *
+ * Threading: one host control thread per GPU owns a psg_ctx and issues every call for it
+ * (mirrors the reference's one-control-thread-per-node rule, socket_fabric.hpp:48-49).
+ * Errors: every int-returning call returns PSG_OK (0) or a psg_status code mapped 1:1 onto the
+ * reference's exception classes (errors.hpp:21-87); psg_last_error() gives the message
+ * (thread-local).
+ */
+#ifndef PSG_H_
+#define PSG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSG_ABI_VERSION 1
+
+/* Status codes — 1:1 with pystachio::Error subclasses (errors.hpp:21-87) + CUDA/NCCL. */
+typedef enum psg_status {
+  PSG_OK = 0,
+  PSG_ERR_UNKNOWN_COLUMN = 1,        /* UnknownColumn            errors.hpp:26-29 */
+  PSG_ERR_MEMORY_EXCEEDED = 2,       /* MemoryExceeded           errors.hpp:31-37 */
+  PSG_ERR_STREAM_CLOSED = 3,         /* StreamClosed             errors.hpp:39-42 */
+  PSG_ERR_IO_FAILURE = 4,            /* IoFailure                errors.hpp:44-47 */
+  PSG_ERR_CORRUPT_FOOTER = 5,        /* CorruptFooter            errors.hpp:49-52 */
+  PSG_ERR_COLLECTIVE_ORDER = 6,      /* CollectiveOrderViolation errors.hpp:54-58 */
+  PSG_ERR_PEER_DISCONNECTED = 7,     /* PeerDisconnected         errors.hpp:60-63 */
+  PSG_ERR_CHECKSUM_MISMATCH = 8,     /* ChecksumMismatch         errors.hpp:65-68 */
+  PSG_ERR_INVALID_INPUT = 9,         /* InvalidInput             errors.hpp:70-73 */
+  PSG_ERR_INFEASIBLE_BUDGET = 10,    /* InfeasibleBudget         errors.hpp:75-78 */
+  PSG_ERR_MALFORMED_TRACE = 11,      /* MalformedTrace           errors.hpp:80-83 */
+  PSG_ERR_EMPTY_TRACE = 12,          /* EmptyTrace               errors.hpp:84-87 */
+  PSG_ERR_CUDA = 100,                /* CUDA runtime failure (no CPU fallback exists) */
+  PSG_ERR_NCCL = 101,                /* NCCL failure */
+  PSG_ERR_INTERNAL = 102
+} psg_status;
+
+/* LogicalType (types.hpp:29): both 8-byte words. */
+#define PSG_INT64 0
+#define PSG_FLOAT64 1
+
+/* ExecMode (pipeline.hpp:124). All four return identical result multisets. */
+#define PSG_MODE_BLOCKING 0   /* FullyBlocking: ingest everything, then compute   */
+#define PSG_MODE_FASTIO 1     /* FastIO: per-chunk waves, phase-sequential         */
+#define PSG_MODE_COMBINED 2   /* Combined: both scans share the ingest pool         */
+#define PSG_MODE_OVERLAPPED 3 /* Overlapped: ingest/shuffle/compute overlap chunk by chunk */
+
+/* Codec (psto.hpp:30). */
+#define PSG_CODEC_IDENTITY 0
+#define PSG_CODEC_BLOCK 1
+
+typedef struct psg_ctx psg_ctx;
+typedef struct psg_result psg_result;
+typedef struct psg_staged psg_staged;
+
+/* A host columnar batch (ChunkBatch, types.hpp:101-156): ncols columns of nrows raw 8-byte words. */
+typedef struct psg_batch {
+  uint32_t ncols;
+  uint64_t nrows;
+  const char* const* names; /* ncols column names */
+  const uint8_t* types;     /* ncols PSG_INT64 / PSG_FLOAT64 */
+  uint64_t* const* cols;    /* ncols host pointers to nrows words each */
+} psg_batch;
+
+/* A predicate atom (PredicateAtom, predicate.hpp:30-41). op: "<","<=","==","!=",">=",">". */
+typedef struct psg_atom {
+  const char* column;
+  const char* op;
+  int literal_is_float; /* 0: literal_i, 1: literal_f (std::variant<int64_t,double>) */
+  int64_t literal_i;
+  double literal_f;
+} psg_atom;
+
+/* Per-query statistics (PipelineResult, pipeline.hpp:138-149, plus device-side timings). */
+typedef struct psg_stats {
+  double runtime_s;            /* end - start on this rank (host wall, around the whole call) */
+  double storage_phase_s;      /* phased modes: ingest phase */
+  double network_phase_s;      /* phased modes: shuffle phase */
+  uint64_t peak_bytes;         /* peak device bytes from the engine pool */
+  uint64_t bytes_received;     /* shuffle payload bytes received from peers */
+  uint64_t ingest_bytes;       /* file bytes moved host->HBM */
+  uint64_t result_bytes;       /* result bytes moved HBM->host */
+  uint64_t kernel_launches;    /* our kernels launched by this call */
+  uint64_t waves;              /* shuffle waves */
+  double probe_kernel_ms;      /* summed CUDA-event time of the dominant fused probe kernel */
+  uint64_t probe_kernel_launches;
+  uint64_t probe_kernel_bytes; /* algorithmic bytes (input column chunks) those launches scanned */
+  double device_ms;            /* CUDA-event time on the engine's compute stream, first to last op */
+  uint64_t result_rows;        /* rows of this rank's result (also when rows stay on the device) */
+} psg_stats;
+
+/* ---- library ---- */
+int psg_abi_version(void);
+const char* psg_last_error(void);
+
+/* ---- per-GPU context (ExecEnv + Fabric + DeviceManager + MetadataCache, exec.hpp:84-92) ---- */
+/* device: CUDA ordinal; rank/nranks: this GPU's node id and the node count (Fabric::node_count). */
+int psg_ctx_create(int device, int rank, int nranks, psg_ctx** out);
+/* NCCL plumbing for nranks > 1 (replaces SocketFabric, socket_fabric.hpp:50-118): rank 0 makes
+ * the 128-byte id, the host transport (torch.distributed) broadcasts it, every rank inits. */
+int psg_comm_unique_id(void* out128);
+int psg_ctx_init_comm(psg_ctx* ctx, const void* id128);
+/* Engine knobs: io_threads (0 = plan.io_workers), batch bytes per ingest slot, pinned slots. */
+int psg_ctx_set_ingest(psg_ctx* ctx, int io_threads, uint64_t batch_bytes, int pinned_slots);
+/* Semi-join (Bloom) pre-filter of the shuffled probe side: 1 = on (default), 0 = off. */
+int psg_ctx_set_semijoin(psg_ctx* ctx, int enabled);
+void psg_ctx_destroy(psg_ctx* ctx);
+
+/* ---- plan execution: execute_plan (pipeline.hpp:153-155, pipeline.cpp:924-929) ----
+ * plan_json is the reference's plan JSON (QueryPlan::from_json_text, pipeline.cpp:108-156);
+ * {data}/{node}/{nodes} are substituted with data_root / ctx rank / ctx nranks.
+ * Storage-resident: reads PSTO files, streams chunks into HBM on copy streams, runs the fused
+ * kernels, shuffles over NCCL when nranks > 1, returns this rank's rows. */
+int psg_execute_plan(psg_ctx* ctx, const char* plan_json, const char* data_root, int mode,
+                     psg_result** out);
+
+/* HBM-resident variant: psg_stage_plan reads every file the plan touches into HBM once;
+ * psg_execute_staged runs the query over the staged bytes (no host I/O). When out is NULL the
+ * result stays on the device (its row count is still available through stats). */
+int psg_stage_plan(psg_ctx* ctx, const char* plan_json, const char* data_root, psg_staged** out);
+int psg_execute_staged(psg_ctx* ctx, psg_staged* staged, int mode, psg_result** out,
+                       psg_stats* stats);
+void psg_staged_free(psg_staged* staged);
+
+/* ---- results (PipelineResult rows/schema, pipeline.hpp:138-149) ---- */
+int psg_result_shape(const psg_result* r, uint64_t* nrows, uint32_t* ncols);
+int psg_result_field(const psg_result* r, uint32_t col, const char** name, int* type);
+const uint64_t* psg_result_data(const psg_result* r); /* row-major nrows*ncols words */
+int psg_result_stats(const psg_result* r, psg_stats* out);
+void psg_result_free(psg_result* r);
+
+/* ---- operator adapters (ops.hpp:35-83): host batch -> HBM -> kernel -> host ---- */
+/* filter (ops.cpp:45-54): order-preserving. */
+int psg_filter(psg_ctx* ctx, const psg_batch* in, const psg_atom* atoms, uint32_t natoms,
+               psg_result** out);
+/* partition (ops.cpp:56-78): h(key) % nparts, order-preserving within each part.
+ * hash_kind: 0 = MultiplyShift, 1 = Identity (hashing.hpp:22). Output rows are grouped by part;
+ * part_rows receives nparts counts. */
+int psg_partition(psg_ctx* ctx, const psg_batch* in, const char* key_column, uint32_t nparts,
+                  int hash_kind, psg_result** out, uint64_t* part_rows);
+/* HashTable::build + probe (ops.cpp:105-222): inner join, output = build payload ++ probe
+ * columns ("_p" suffix on name clash). Row order unspecified (the reference's tests compare
+ * multisets). */
+int psg_hash_join(psg_ctx* ctx, const psg_batch* build, const char* build_key,
+                  const psg_batch* probe, const char* probe_key, psg_result** out);
+
+/* ---- PSTO format (psto.hpp) ---- */
+/* TableWriter (psto.cpp:144-229): writes a batch as a PSTO file. Returns row groups written. */
+int psg_psto_write(const char* path, const psg_batch* batch, uint64_t row_group_rows, int codec,
+                   uint64_t* groups_written);
+/* parse_footer_file (psto.cpp:294-318): rows, columns, row groups, codec. */
+int psg_psto_inspect(const char* path, uint64_t* rows, uint32_t* ncols, uint64_t* groups,
+                     int* codec);
+
+/* ---- workload generator: gen_workload(kind=tpch) (bench.cpp:85-114) ----
+ * Byte-identical to the reference generator (pinned by tests/golden/gen_hashes.json). */
+int psg_gen_tpch(const char* out_dir, double scale, int nodes, int devices, uint64_t seed,
+                 int codec, uint64_t row_group_bytes, int threads);
+
+/* ---- Eq. 1 roofline: t_min (bench.cpp:35-40) ---- */
+double psg_tmin(uint64_t ssd_read_size_agg, double ssd_read_bw_agg, uint64_t net_recv_size_node,
+                double net_bw);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSG_H_ */

@@ -1,0 +1,421 @@
+"""B200-native PystachIO hot path (arxiv 2512.02862): storage-resident OLAP execution on sm_100a.
+
+Python face of the C-ABI in ``include/psg.h`` (ctypes over the in-tree ``libpsg.so``). The
+function names and argument meanings mirror the reference's pybind11 module
+(``/root/reference/proj/python/bindings.cpp:98-231``): ``tmin``, ``write_table``, ``inspect``,
+``scan``, ``gen_workload`` and — replacing ``run_plan_sim`` — ``run_plan`` which executes
+``execute_plan`` on the GPU. Operator adapters (``filter``, ``partition``, ``hash_join``) mirror
+``ops.hpp:35-83``. There is no CPU fallback: without the built extension or a CUDA device every
+compute call raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import math
+import os
+
+import numpy as np
+
+__all__ = ["Context", "PsgError", "tmin", "write_table", "inspect", "scan", "gen_workload", "run_plan",
+           "filter", "partition", "hash_join", "lib", "MODES", "STATUS"]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libpsg.so")
+
+MODES = {"blocking": 0, "fastio": 1, "combined": 2, "overlapped": 3}
+STATUS = {0: "OK", 1: "UnknownColumn", 2: "MemoryExceeded", 3: "StreamClosed", 4: "IoFailure", 5: "CorruptFooter",
+          6: "CollectiveOrderViolation", 7: "PeerDisconnected", 8: "ChecksumMismatch", 9: "InvalidInput",
+          10: "InfeasibleBudget", 11: "MalformedTrace", 12: "EmptyTrace", 100: "CudaError", 101: "NcclError",
+          102: "InternalError"}
+EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_unique_id", "psg_ctx_init_comm",
+           "psg_ctx_set_ingest", "psg_ctx_set_semijoin", "psg_ctx_destroy", "psg_execute_plan", "psg_stage_plan",
+           "psg_execute_staged", "psg_staged_free", "psg_result_shape", "psg_result_field", "psg_result_data",
+           "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_psto_write",
+           "psg_psto_inspect", "psg_gen_tpch", "psg_tmin"]
+
+
+class PsgError(RuntimeError):
+    """Engine error; ``kind`` names the reference exception class (errors.hpp:21-87)."""
+
+    def __init__(self, code, msg):
+        self.code = code
+        self.kind = STATUS.get(code, "Error%d" % code)
+        super().__init__("%s: %s" % (self.kind, msg))
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("runtime_s", ctypes.c_double), ("storage_phase_s", ctypes.c_double),
+                ("network_phase_s", ctypes.c_double), ("peak_bytes", ctypes.c_uint64),
+                ("bytes_received", ctypes.c_uint64), ("ingest_bytes", ctypes.c_uint64),
+                ("result_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("waves", ctypes.c_uint64), ("probe_kernel_ms", ctypes.c_double),
+                ("probe_kernel_launches", ctypes.c_uint64), ("probe_kernel_bytes", ctypes.c_uint64),
+                ("device_ms", ctypes.c_double), ("result_rows", ctypes.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class Batch(ctypes.Structure):
+    _fields_ = [("ncols", ctypes.c_uint32), ("nrows", ctypes.c_uint64), ("names", ctypes.POINTER(ctypes.c_char_p)),
+                ("types", ctypes.POINTER(ctypes.c_uint8)), ("cols", ctypes.POINTER(ctypes.POINTER(ctypes.c_uint64)))]
+
+
+class Atom(ctypes.Structure):
+    _fields_ = [("column", ctypes.c_char_p), ("op", ctypes.c_char_p), ("literal_is_float", ctypes.c_int),
+                ("literal_i", ctypes.c_int64), ("literal_f", ctypes.c_double)]
+
+
+_lib = None
+
+
+def lib():
+    """The loaded ``libpsg.so`` (raises if the extension was not built: no fallback exists)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError("libpsg.so not built: run `python -m paper_2512_02862_b200.build` "
+                              "(the B200 path has no CPU fallback)")
+        L = ctypes.CDLL(_LIB_PATH)
+        vp, u64, i32, c = ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_char_p
+        P = ctypes.POINTER
+        sig = {
+            "psg_abi_version": ([], i32), "psg_last_error": ([], c),
+            "psg_ctx_create": ([i32, i32, i32, P(vp)], i32), "psg_comm_unique_id": ([vp], i32),
+            "psg_ctx_init_comm": ([vp, vp], i32), "psg_ctx_set_ingest": ([vp, i32, u64, i32], i32),
+            "psg_ctx_set_semijoin": ([vp, i32], i32), "psg_ctx_destroy": ([vp], None),
+            "psg_execute_plan": ([vp, c, c, i32, P(vp)], i32), "psg_stage_plan": ([vp, c, c, P(vp)], i32),
+            "psg_execute_staged": ([vp, vp, i32, P(vp), P(Stats)], i32), "psg_staged_free": ([vp], None),
+            "psg_result_shape": ([vp, P(u64), P(ctypes.c_uint32)], i32),
+            "psg_result_field": ([vp, ctypes.c_uint32, P(c), P(i32)], i32),
+            "psg_result_data": ([vp], P(u64)), "psg_result_stats": ([vp, P(Stats)], i32),
+            "psg_result_free": ([vp], None),
+            "psg_filter": ([vp, P(Batch), P(Atom), ctypes.c_uint32, P(vp)], i32),
+            "psg_partition": ([vp, P(Batch), c, ctypes.c_uint32, i32, P(vp), P(u64)], i32),
+            "psg_hash_join": ([vp, P(Batch), c, P(Batch), c, P(vp)], i32),
+            "psg_psto_write": ([c, P(Batch), u64, i32, P(u64)], i32),
+            "psg_psto_inspect": ([c, P(u64), P(ctypes.c_uint32), P(u64), P(i32)], i32),
+            "psg_gen_tpch": ([c, ctypes.c_double, i32, i32, u64, i32, u64, i32], i32),
+            "psg_tmin": ([u64, ctypes.c_double, u64, ctypes.c_double], ctypes.c_double),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise PsgError(rc, lib().psg_last_error().decode(errors="replace"))
+
+
+# ------------------------------------------------------------------------------ batches
+def _make_batch(columns: dict, types: dict | None = None):
+    """dict name -> sequence/ndarray. int -> Int64, float -> Float64 (raw 8-byte words)."""
+    names, tys, arrs = [], [], []
+    n = None
+    for name, vals in columns.items():
+        a = np.asarray(vals)
+        t = (types or {}).get(name)
+        if t is None:
+            t = 1 if a.dtype.kind == "f" else 0
+        if a.dtype == np.uint64:  # already raw 8-byte words
+            a = np.ascontiguousarray(a)
+        elif t == 1:
+            a = np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+        else:
+            a = np.ascontiguousarray(a.astype(np.int64, copy=False)).view(np.uint64)
+        if n is None:
+            n = len(a)
+        elif len(a) != n:
+            raise PsgError(9, "ragged batch: column row counts differ")
+        names.append(name.encode())
+        tys.append(t)
+        arrs.append(a)
+    nc = len(names)
+    b = Batch()
+    b.ncols = nc
+    b.nrows = n or 0
+    b._names = (ctypes.c_char_p * max(nc, 1))(*names)
+    b._types = (ctypes.c_uint8 * max(nc, 1))(*tys)
+    b._arrs = arrs
+    b._cols = (ctypes.POINTER(ctypes.c_uint64) * max(nc, 1))(
+        *[a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)) for a in arrs])
+    b.names = ctypes.cast(b._names, ctypes.POINTER(ctypes.c_char_p))
+    b.types = ctypes.cast(b._types, ctypes.POINTER(ctypes.c_uint8))
+    b.cols = ctypes.cast(b._cols, ctypes.POINTER(ctypes.POINTER(ctypes.c_uint64)))
+    return b
+
+
+class Result:
+    """PipelineResult (pipeline.hpp:138-149): schema + rows of raw u64 words (row-major ndarray)."""
+
+    def __init__(self, handle):
+        L = lib()
+        n, k = ctypes.c_uint64(), ctypes.c_uint32()
+        _check(L.psg_result_shape(handle, ctypes.byref(n), ctypes.byref(k)))
+        self.schema = []
+        for i in range(k.value):
+            nm, ty = ctypes.c_char_p(), ctypes.c_int()
+            _check(L.psg_result_field(handle, i, ctypes.byref(nm), ctypes.byref(ty)))
+            self.schema.append((nm.value.decode(), "float64" if ty.value == 1 else "int64"))
+        cnt = n.value * k.value
+        ptr = L.psg_result_data(handle)
+        self.rows = np.ctypeslib.as_array(ptr, shape=(cnt,)).copy().reshape(n.value, k.value) if cnt else \
+            np.zeros((n.value, k.value), np.uint64)
+        st = Stats()
+        _check(L.psg_result_stats(handle, ctypes.byref(st)))
+        self.stats = st.as_dict()
+        L.psg_result_free(handle)
+
+    def column(self, name):
+        i = [n for n, _t in self.schema].index(name)
+        col = self.rows[:, i]
+        return col.view(np.float64) if self.schema[i][1] == "float64" else col.view(np.int64)
+
+    def to_dict(self):
+        return {n: self.column(n).tolist() for n, _t in self.schema}
+
+
+class Context:
+    """One GPU / one rank (ExecEnv + Fabric + DeviceManager, exec.hpp:84-92)."""
+
+    def __init__(self, device=0, rank=0, nranks=1, nccl_id: bytes | None = None):
+        L = lib()
+        h = ctypes.c_void_p()
+        _check(L.psg_ctx_create(device, rank, nranks, ctypes.byref(h)))
+        self._h = h
+        self.device, self.rank, self.nranks = device, rank, nranks
+        if nranks > 1:
+            if nccl_id is None:
+                raise PsgError(9, "nranks > 1 needs the NCCL unique id from rank 0 (Context.unique_id())")
+            buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+            _check(L.psg_ctx_init_comm(self._h, buf))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        _check(lib().psg_comm_unique_id(buf))
+        return buf.raw
+
+    def set_ingest(self, io_threads=-1, batch_bytes=0, pinned_slots=-1):
+        _check(lib().psg_ctx_set_ingest(self._h, io_threads, batch_bytes, pinned_slots))
+
+    def set_semijoin(self, enabled: bool):
+        _check(lib().psg_ctx_set_semijoin(self._h, 1 if enabled else 0))
+
+    def execute_plan(self, plan, data_root, mode="overlapped") -> Result:
+        text = plan if isinstance(plan, str) else json.dumps(plan)
+        out = ctypes.c_void_p()
+        _check(lib().psg_execute_plan(self._h, text.encode(), data_root.encode(), MODES[mode], ctypes.byref(out)))
+        return Result(out)
+
+    def stage_plan(self, plan, data_root):
+        text = plan if isinstance(plan, str) else json.dumps(plan)
+        out = ctypes.c_void_p()
+        _check(lib().psg_stage_plan(self._h, text.encode(), data_root.encode(), ctypes.byref(out)))
+        return Staged(self, out)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().psg_ctx_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+
+class Staged:
+    """Plan inputs resident in HBM (psg_stage_plan); run() executes without host I/O."""
+
+    def __init__(self, ctx, handle):
+        self.ctx, self._h = ctx, handle
+
+    def run(self, mode="overlapped", want_rows=True):
+        out = ctypes.c_void_p()
+        st = Stats()
+        _check(lib().psg_execute_staged(self.ctx._h, self._h, MODES[mode], ctypes.byref(out) if want_rows else None,
+                                        ctypes.byref(st)))
+        return Result(out) if want_rows else st.as_dict()
+
+    def free(self):
+        if self._h:
+            lib().psg_staged_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+_default_ctx = None
+
+
+def _ctx():
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+# --------------------------------------------------------------- reference-shaped functions
+def tmin(ssd_read_size_agg, ssd_read_bw_agg, net_recv_size_node, net_bw):
+    """Eq. 1 (bench.cpp:35-40): max(storage read time, per-node network receive time), seconds."""
+    v = lib().psg_tmin(int(ssd_read_size_agg), float(ssd_read_bw_agg), int(net_recv_size_node), float(net_bw))
+    if math.isnan(v):
+        raise PsgError(9, lib().psg_last_error().decode())
+    return v
+
+
+def write_table(path, columns: dict, row_group_rows=65536, codec="identity"):
+    """Writes a PSTO table (TableWriter, psto.cpp:144-229); returns the row-group count."""
+    b = _make_batch(columns)
+    g = ctypes.c_uint64()
+    _check(lib().psg_psto_write(path.encode(), ctypes.byref(b), int(row_group_rows), 1 if codec == "block" else 0,
+                                ctypes.byref(g)))
+    return g.value
+
+
+def _footer_schema(path):
+    import struct
+    with open(path, "rb") as f:
+        f.seek(-12, 2)
+        flen = struct.unpack("<Q", f.read(8))[0]
+        f.seek(-12 - flen, 2)
+        foot = f.read(flen)
+    off = 5
+    (nc,) = struct.unpack_from("<I", foot, off)
+    off += 4
+    schema = []
+    for _ in range(nc):
+        (ln,) = struct.unpack_from("<I", foot, off)
+        off += 4
+        name = foot[off: off + ln].decode()
+        off += ln
+        schema.append((name, "float64" if foot[off] == 1 else "int64"))
+        off += 1
+    return schema
+
+
+def inspect(path):
+    """parse_footer_file summary: rows, codec, row_groups, schema [(name, type)]."""
+    rows, nc, groups, codec = ctypes.c_uint64(), ctypes.c_uint32(), ctypes.c_uint64(), ctypes.c_int()
+    _check(lib().psg_psto_inspect(path.encode(), ctypes.byref(rows), ctypes.byref(nc), ctypes.byref(groups),
+                                  ctypes.byref(codec)))
+    return {"rows": rows.value, "codec": "block" if codec.value == 1 else "identity", "row_groups": groups.value,
+            "schema": _footer_schema(path)}
+
+
+def gen_workload(kind, out_dir, devices=2, nodes=2, scale=0.01, seed=42, codec="identity", row_group_bytes=1 << 20,
+                 threads=3):
+    """gen_workload(kind='tpch') (bench.cpp:85-114), byte-identical to the reference generator.
+
+    The reference's default codec is the zlib block codec; the GPU scan path reads the identity
+    codec, which is what this defaults to (pass codec='block' for reference-default files)."""
+    if kind not in ("tpch", "tpch-analog"):
+        raise PsgError(9, "only the tpch-analog workload is generated by this build")
+    _check(lib().psg_gen_tpch(out_dir.encode(), float(scale), int(nodes), int(devices), int(seed),
+                              1 if codec == "block" else 0, int(row_group_bytes), int(threads)))
+    return os.path.join(out_dir, "manifest.json")
+
+
+def run_plan(plan, data_root, mode="overlapped", ctx: Context | None = None) -> Result:
+    """execute_plan on this process's GPU (one rank). Returns this rank's PipelineResult."""
+    return (ctx or _ctx()).execute_plan(plan, data_root, mode)
+
+
+def _atoms(predicate):
+    atoms = []
+    for col, op, lit in predicate or []:
+        a = Atom()
+        a.column = col.encode()
+        a.op = op.encode()
+        a.literal_is_float = 1 if isinstance(lit, float) else 0
+        a.literal_i = int(lit) if not isinstance(lit, float) else 0
+        a.literal_f = float(lit)
+        atoms.append(a)
+    arr = (Atom * max(len(atoms), 1))(*atoms)
+    return arr, len(atoms)
+
+
+def filter(columns: dict, predicate, ctx: Context | None = None, types=None) -> Result:
+    """Order-preserving filter (ops.cpp:45-54) on the GPU."""
+    b = _make_batch(columns, types)
+    arr, n = _atoms(predicate)
+    out = ctypes.c_void_p()
+    _check(lib().psg_filter((ctx or _ctx())._h, ctypes.byref(b), arr, n, ctypes.byref(out)))
+    return Result(out)
+
+
+def partition(columns: dict, key, nparts, hash_kind="multiply_shift", ctx: Context | None = None, types=None):
+    """partition (ops.cpp:56-78): returns [Result-like dict per part] preserving order within parts."""
+    b = _make_batch(columns, types)
+    counts = (ctypes.c_uint64 * nparts)()
+    out = ctypes.c_void_p()
+    _check(lib().psg_partition((ctx or _ctx())._h, ctypes.byref(b), key.encode(), int(nparts),
+                               1 if hash_kind == "identity" else 0, ctypes.byref(out), counts))
+    r = Result(out)
+    parts, at = [], 0
+    for p in range(nparts):
+        parts.append(r.rows[at: at + counts[p]])
+        at += counts[p]
+    return r.schema, parts
+
+
+def hash_join(build: dict, build_key, probe: dict, probe_key, ctx: Context | None = None, build_types=None,
+              probe_types=None) -> Result:
+    """HashTable::build + probe (ops.cpp:105-222): build payload ++ probe columns, multiset order."""
+    bb = _make_batch(build, build_types)
+    pb = _make_batch(probe, probe_types)
+    out = ctypes.c_void_p()
+    _check(lib().psg_hash_join((ctx or _ctx())._h, ctypes.byref(bb), build_key.encode(), ctypes.byref(pb),
+                               probe_key.encode(), ctypes.byref(out)))
+    return Result(out)
+
+
+def scan(path, predicate=None, ctx: Context | None = None):
+    """Reads a PSTO table through the GPU filter (read_blocking + filter, scan.cpp:273-336)."""
+    meta = inspect(path)
+    import struct
+    with open(path, "rb") as f:
+        data = f.read()
+    if meta["codec"] != "identity":
+        raise PsgError(9, "block-codec PSTO needs the GPU inflate path (not in this build)")
+    # footer walk for chunk offsets
+    (flen,) = struct.unpack_from("<Q", data, len(data) - 12)
+    foot = data[len(data) - 12 - flen: len(data) - 12]
+    off = 5
+    (nc,) = struct.unpack_from("<I", foot, off)
+    off += 4
+    for _ in range(nc):
+        (ln,) = struct.unpack_from("<I", foot, off)
+        off += 4 + ln + 1
+    (ng,) = struct.unpack_from("<I", foot, off)
+    off += 4
+    cols = [[] for _ in range(nc)]
+    for _ in range(ng):
+        (rows,) = struct.unpack_from("<Q", foot, off)
+        off += 8
+        for c in range(nc):
+            o, cs, _us, _mn, _mx = struct.unpack_from("<5Q", foot, off)
+            off += 40
+            cols[c].append(np.frombuffer(data, dtype="<u8", count=rows, offset=o))
+    schema = meta["schema"]
+    columns = {n: (np.concatenate(cols[i]) if cols[i] else np.zeros(0, np.uint64)) for i, (n, _t) in enumerate(schema)}
+    types = {n: (1 if t == "float64" else 0) for n, t in schema}
+    res = filter(columns, predicate or [], ctx=ctx, types=types)
+    return res.to_dict()

@@ -1,0 +1,311 @@
+// extern "C" boundary (include/psg.h). Every call catches psg::Error / std::exception and turns
+// it into a psg_status code + thread-local message, mirroring the reference's exception classes.
+#include <execinfo.h>
+#include <signal.h>
+#include <unistd.h>
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "engine.hpp"
+
+using namespace psg;
+
+struct psg_ctx {
+  Ctx c;
+};
+struct psg_result {
+  ResultRows r;
+};
+struct psg_staged {
+  Staged* s = nullptr;
+};
+
+namespace {
+thread_local std::string g_err;
+
+// PSG_SEGV_TRACE=1: print a native backtrace on SIGSEGV/SIGABRT (debugging on the GPU box).
+void segv_handler(int sig) {
+  void* frames[64];
+  const int n = backtrace(frames, 64);
+  const char msg[] = "psg: fatal signal, native backtrace:\n";
+  (void)!write(2, msg, sizeof msg - 1);
+  backtrace_symbols_fd(frames, n, 2);
+  signal(sig, SIG_DFL);
+  raise(sig);
+}
+void maybe_install_trace() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const char* e = std::getenv("PSG_SEGV_TRACE");
+  if (e && e[0] == '1') {
+    signal(SIGSEGV, segv_handler);
+    signal(SIGABRT, segv_handler);
+  }
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PSG_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code();
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("host allocation failed: ") + e.what();
+    return PSG_ERR_MEMORY_EXCEEDED;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return PSG_ERR_INTERNAL;
+  }
+}
+
+HostBatch to_host(const psg_batch* b) {
+  if (!b) throw InvalidInput("null batch");
+  HostBatch h;
+  for (uint32_t c = 0; c < b->ncols; ++c) {
+    if (b->types[c] > 1) throw InvalidInput("unknown logical type");
+    h.schema.fields.push_back(Field{b->names[c], static_cast<LType>(b->types[c])});
+    h.cols.emplace_back(b->cols[c], b->cols[c] + b->nrows);
+  }
+  return h;
+}
+
+psg_result* to_result(const HostBatch& h) {
+  auto* r = new psg_result;
+  r->r.schema = h.schema;
+  const uint64_t n = h.rows();
+  const size_t nc = h.schema.size();
+  r->r.nrows = n;
+  r->r.words.resize(n * nc);
+  for (size_t c = 0; c < nc; ++c)
+    for (uint64_t i = 0; i < n; ++i) r->r.words[i * nc + c] = h.cols[c][i];
+  return r;
+}
+
+Predicate to_pred(const psg_atom* atoms, uint32_t n) {
+  Predicate p;
+  for (uint32_t i = 0; i < n; ++i) {
+    Atom a;
+    a.column = atoms[i].column;
+    a.op = cmp_op_from_string(atoms[i].op);
+    a.lit_is_float = atoms[i].literal_is_float != 0;
+    a.lit_i = atoms[i].literal_i;
+    a.lit_f = atoms[i].literal_f;
+    p.push_back(a);
+  }
+  return p;
+}
+}  // namespace
+
+extern "C" {
+
+int psg_abi_version(void) { return PSG_ABI_VERSION; }
+const char* psg_last_error(void) { return g_err.c_str(); }
+
+int psg_ctx_create(int device, int rank, int nranks, psg_ctx** out) {
+  return guarded([&] {
+    if (!out) throw InvalidInput("null out");
+    maybe_install_trace();
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw InvalidInput("bad rank/nranks");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error(PSG_ERR_CUDA, "no CUDA device visible: the B200 path has no CPU fallback");
+    if (device < 0 || device >= ndev) throw InvalidInput("device ordinal out of range");
+    auto ctx = std::make_unique<psg_ctx>();
+    Ctx& c = ctx->c;
+    c.device = device;
+    c.rank = rank;
+    c.nranks = nranks;
+    PSG_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    PSG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) throw Error(PSG_ERR_CUDA, std::string("device is not sm_100-class: ") + prop.name);
+    PSG_CUDA(cudaStreamCreateWithFlags(&c.compute, cudaStreamNonBlocking));
+    PSG_CUDA(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+    PSG_CUDA(cudaStreamCreateWithFlags(&c.comm, cudaStreamNonBlocking));
+    PSG_CUDA(cudaEventCreate(&c.ev_a));
+    PSG_CUDA(cudaEventCreate(&c.ev_b));
+    c.pool.init(device, 0);
+    *out = ctx.release();
+  });
+}
+
+int psg_comm_unique_id(void* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) throw Error(PSG_ERR_NCCL, "ncclGetUniqueId failed");
+    std::memcpy(out128, &id, sizeof id);
+  });
+}
+
+int psg_ctx_init_comm(psg_ctx* ctx, const void* id128) {
+  return guarded([&] {
+    if (!ctx) throw InvalidInput("null ctx");
+    PSG_CUDA(cudaSetDevice(ctx->c.device));
+    if (ctx->c.nranks == 1) return;
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    const ncclResult_t r = ncclCommInitRank(&ctx->c.nccl, ctx->c.nranks, id, ctx->c.rank);
+    if (r != ncclSuccess) throw Error(PSG_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  });
+}
+
+int psg_ctx_set_ingest(psg_ctx* ctx, int io_threads, uint64_t batch_bytes, int pinned_slots) {
+  return guarded([&] {
+    if (!ctx) throw InvalidInput("null ctx");
+    if (io_threads >= 0) ctx->c.io_threads = io_threads;
+    if (batch_bytes > 0) ctx->c.batch_bytes = batch_bytes;
+    if (pinned_slots >= 0) ctx->c.pinned_slots = pinned_slots;
+  });
+}
+
+int psg_ctx_set_semijoin(psg_ctx* ctx, int enabled) {
+  return guarded([&] {
+    if (!ctx) throw InvalidInput("null ctx");
+    ctx->c.semijoin = enabled != 0;
+  });
+}
+
+void psg_ctx_destroy(psg_ctx* ctx) { delete ctx; }
+
+int psg_execute_plan(psg_ctx* ctx, const char* plan_json, const char* data_root, int mode, psg_result** out) {
+  return guarded([&] {
+    if (!ctx || !plan_json || !data_root || !out) throw InvalidInput("null argument");
+    if (ctx->c.io_threads == 0) {
+      // default: plan.io_workers (resolved inside) -> use hardware threads when unset
+      ctx->c.io_threads = 8;
+    }
+    auto r = std::make_unique<psg_result>();
+    r->r = execute_plan(ctx->c, plan_json, data_root, mode, nullptr, true);
+    *out = r.release();
+  });
+}
+
+int psg_stage_plan(psg_ctx* ctx, const char* plan_json, const char* data_root, psg_staged** out) {
+  return guarded([&] {
+    if (!ctx || !plan_json || !data_root || !out) throw InvalidInput("null argument");
+    if (ctx->c.io_threads == 0) ctx->c.io_threads = 8;
+    auto s = std::make_unique<psg_staged>();
+    s->s = stage_plan(ctx->c, plan_json, data_root);
+    *out = s.release();
+  });
+}
+
+int psg_execute_staged(psg_ctx* ctx, psg_staged* staged, int mode, psg_result** out, psg_stats* stats) {
+  return guarded([&] {
+    if (!ctx || !staged) throw InvalidInput("null argument");
+    auto r = std::make_unique<psg_result>();
+    r->r = execute_plan(ctx->c, "", "", mode, staged->s, out != nullptr);
+    if (stats) *stats = r->r.stats;
+    if (out) *out = r.release();
+  });
+}
+
+void psg_staged_free(psg_staged* s) {
+  if (!s) return;
+  free_staged(s->s);
+  delete s;
+}
+
+int psg_result_shape(const psg_result* r, uint64_t* nrows, uint32_t* ncols) {
+  return guarded([&] {
+    if (!r) throw InvalidInput("null result");
+    if (nrows) *nrows = r->r.nrows;
+    if (ncols) *ncols = static_cast<uint32_t>(r->r.schema.size());
+  });
+}
+
+int psg_result_field(const psg_result* r, uint32_t col, const char** name, int* type) {
+  return guarded([&] {
+    if (!r || col >= r->r.schema.size()) throw InvalidInput("column out of range");
+    if (name) *name = r->r.schema.fields[col].name.c_str();
+    if (type) *type = static_cast<int>(r->r.schema.fields[col].type);
+  });
+}
+
+const uint64_t* psg_result_data(const psg_result* r) { return r ? r->r.words.data() : nullptr; }
+
+int psg_result_stats(const psg_result* r, psg_stats* out) {
+  return guarded([&] {
+    if (!r || !out) throw InvalidInput("null argument");
+    *out = r->r.stats;
+  });
+}
+
+void psg_result_free(psg_result* r) { delete r; }
+
+int psg_filter(psg_ctx* ctx, const psg_batch* in, const psg_atom* atoms, uint32_t natoms, psg_result** out) {
+  return guarded([&] {
+    if (!ctx || !out) throw InvalidInput("null argument");
+    HostBatch h = to_host(in);
+    *out = to_result(op_filter(ctx->c, h, to_pred(atoms, natoms)));
+  });
+}
+
+int psg_partition(psg_ctx* ctx, const psg_batch* in, const char* key_column, uint32_t nparts, int hash_kind,
+                  psg_result** out, uint64_t* part_rows) {
+  return guarded([&] {
+    if (!ctx || !out || !key_column) throw InvalidInput("null argument");
+    HostBatch h = to_host(in);
+    std::vector<uint64_t> pr;
+    *out = to_result(op_partition(ctx->c, h, key_column, nparts, hash_kind == 1, pr));
+    if (part_rows) std::memcpy(part_rows, pr.data(), pr.size() * 8);
+  });
+}
+
+int psg_hash_join(psg_ctx* ctx, const psg_batch* build, const char* build_key, const psg_batch* probe,
+                  const char* probe_key, psg_result** out) {
+  return guarded([&] {
+    if (!ctx || !out || !build_key || !probe_key) throw InvalidInput("null argument");
+    *out = to_result(op_hash_join(ctx->c, to_host(build), build_key, to_host(probe), probe_key));
+  });
+}
+
+int psg_psto_write(const char* path, const psg_batch* batch, uint64_t row_group_rows, int codec,
+                   uint64_t* groups_written) {
+  return guarded([&] {
+    HostBatch h = to_host(batch);
+    if (codec != 0 && codec != 1) throw InvalidInput("unknown codec");
+    PstoWriter w(path, h.schema, row_group_rows, static_cast<Codec>(codec));
+    std::vector<const uint64_t*> ptrs;
+    for (auto& c : h.cols) ptrs.push_back(c.data());
+    if (h.rows()) w.append(ptrs.data(), h.rows());
+    TableMeta m = w.finish();
+    if (groups_written) *groups_written = m.groups.size();
+  });
+}
+
+int psg_psto_inspect(const char* path, uint64_t* rows, uint32_t* ncols, uint64_t* groups, int* codec) {
+  return guarded([&] {
+    TableMeta m = read_footer(path);
+    if (rows) *rows = m.total_rows();
+    if (ncols) *ncols = static_cast<uint32_t>(m.schema.size());
+    if (groups) *groups = m.groups.size();
+    if (codec) *codec = static_cast<int>(m.codec);
+  });
+}
+
+int psg_gen_tpch(const char* out_dir, double scale, int nodes, int devices, uint64_t seed, int codec,
+                 uint64_t row_group_bytes, int threads) {
+  return guarded([&] {
+    if (codec != 0 && codec != 1) throw InvalidInput("unknown codec");
+    gen_tpch(out_dir, scale, nodes, devices, seed, static_cast<Codec>(codec), row_group_bytes, threads);
+  });
+}
+
+double psg_tmin(uint64_t ssd_read_size_agg, double ssd_read_bw_agg, uint64_t net_recv_size_node, double net_bw) {
+  // t_min (bench.cpp:35-40): invalid inputs return NaN (the C++ API throws InvalidInput).
+  if (ssd_read_size_agg == 0 || ssd_read_bw_agg <= 0 || net_bw <= 0) {
+    g_err = "invalid input: t_min inputs must be positive";
+    return std::nan("");
+  }
+  const double storage = static_cast<double>(ssd_read_size_agg) / ssd_read_bw_agg;
+  const double net = static_cast<double>(net_recv_size_node) / net_bw;
+  return storage > net ? storage : net;
+}
+
+}  // extern "C"

@@ -1,0 +1,1356 @@
+// execute_plan on B200: the GPU re-design of PlanExecution (/root/reference/proj/src/pipeline.cpp:317-920).
+//
+// Per rank (one GPU, one host control thread):
+//   1. replicated scans -> fused filter/compaction kernel -> CSR hash table per local join
+//      (load_replicated, pipeline.cpp:386-428)
+//   2. shuffle build side: chunks stream storage -> pinned -> HBM; one fused kernel per chunk batch
+//      does predicate + local-join chain + compaction of only the needed columns
+//      (scan_chunks + apply_chain, scan.cpp:165-271, pipeline.cpp:431-448); for nranks > 1 each
+//      batch is hash-partitioned and exchanged over NCCL (run_waves, pipeline.cpp:662-785); the
+//      aggregation table is built from the landed rows (shuffle_build_phase :787-809)
+//   3. shuffle probe side: for nranks == 1 one fused kernel per batch does predicate + chain +
+//      probe + group-by accumulation in the table slot (shuffle_probe_phase + deliver +
+//      HashAggregator::add, :811-837, :874-890, :275-294); for nranks > 1 batches are compacted,
+//      (optionally Bloom semi-join filtered), exchanged, then probed on the owner
+//   4. finalize: compact groups with hits > 0, radix sort by signed key, emit rows (:892-897).
+// Copies run on a copy stream, kernels on the compute stream, NCCL on the comm stream; the host
+// waits only where a size is data-dependent (the per-wave count exchange).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <functional>
+#include <numeric>
+#include <cstdio>
+#include <cstdlib>
+#include <set>
+
+#include "engine.hpp"
+
+#define PSG_NCCL(call)                                                                              \
+  do {                                                                                              \
+    ncclResult_t r_ = (call);                                                                       \
+    if (r_ != ncclSuccess) throw ::psg::Error(PSG_ERR_NCCL, std::string("nccl: ") + ncclGetErrorString(r_)); \
+  } while (0)
+
+namespace psg {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+bool trace_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("PSG_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+#define PSG_TRACE_MSG(...)                  \
+  do {                                      \
+    if (trace_on()) {                       \
+      std::fprintf(stderr, "[psg] " __VA_ARGS__); \
+      std::fputc('\n', stderr);             \
+    }                                       \
+  } while (0)
+double secs_since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+uint64_t pow2_at_least(uint64_t x) {
+  uint64_t p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+uint64_t dbl_bits(double d) {
+  uint64_t u;
+  std::memcpy(&u, &d, 8);
+  return u;
+}
+
+// ------------------------------------------------------------------------- plan compilation
+struct ColRef {
+  int join;  // -1: base projected column; else payload p of chain[join]
+  int idx;
+  bool operator<(const ColRef& o) const { return join != o.join ? join < o.join : idx < o.idx; }
+  bool operator==(const ColRef& o) const { return join == o.join && idx == o.idx; }
+};
+
+struct Projected {
+  Schema schema;
+  std::vector<int> file_idx;
+};
+
+/// project (scan.cpp:121-137)
+Projected project(const Schema& file, const std::vector<std::string>& columns) {
+  Projected p;
+  for (size_t c = 0; c < file.size(); ++c)
+    if (columns.empty() || std::find(columns.begin(), columns.end(), file.fields[c].name) != columns.end()) {
+      p.schema.fields.push_back(file.fields[c]);
+      p.file_idx.push_back(static_cast<int>(c));
+    }
+  for (auto& n : columns)
+    if (!p.schema.index_of(n)) throw UnknownColumn(n);
+  return p;
+}
+
+struct LocalJoinDef {
+  const JoinNode* node = nullptr;
+  const ScanNode* scan = nullptr;
+  Projected proj;
+  int key_idx = 0;
+  std::vector<int> payload_idx;  // proj indices of payload columns (all non-key), order = p
+  int probe_key_stage = 0;       // wire index (before this join) of the probe key
+  std::vector<int> needed_payload;  // subset of p needed downstream (filled by analysis)
+};
+
+struct SourceDef {
+  const ScanNode* scan = nullptr;
+  Projected proj;
+  std::vector<LocalJoinDef> chain;
+  std::vector<std::vector<ColRef>> stage_refs;  // [k] wire refs before join k; [chain.size()] final
+  Schema wire;
+};
+
+SourceDef make_source(const QueryPlan& plan, FooterCache& fc, const std::string& name) {
+  for (const auto& s : plan.scans)
+    if (s.table == name) {
+      SourceDef d;
+      d.scan = &s;
+      auto meta = fc.get(s.paths.at(0));
+      d.proj = project(meta->schema, s.columns);
+      d.wire = d.proj.schema;
+      std::vector<ColRef> refs;
+      for (size_t i = 0; i < d.wire.size(); ++i) refs.push_back({-1, static_cast<int>(i)});
+      d.stage_refs.push_back(refs);
+      return d;
+    }
+  for (const auto& j : plan.joins)
+    if (j.id == name) {
+      if (j.shuffle) throw InvalidInput("a shuffle join cannot feed another join");
+      SourceDef d = make_source(plan, fc, j.probe);
+      LocalJoinDef lj;
+      lj.node = &j;
+      lj.scan = &plan.scan(j.build);
+      auto bmeta = fc.get(lj.scan->paths.at(0));
+      lj.proj = project(bmeta->schema, lj.scan->columns);
+      lj.key_idx = static_cast<int>(lj.proj.schema.require(j.build_key));
+      if (lj.proj.schema.fields[lj.key_idx].type != LType::Int64) throw InvalidInput("join key must be int64: " + j.build_key);
+      lj.probe_key_stage = static_cast<int>(d.wire.require(j.probe_key));
+      if (d.wire.fields[lj.probe_key_stage].type != LType::Int64) throw InvalidInput("probe key must be int64: " + j.probe_key);
+      const int jn = static_cast<int>(d.chain.size());
+      Schema joined;
+      std::vector<ColRef> refs;
+      for (size_t c = 0; c < lj.proj.schema.size(); ++c) {
+        if (static_cast<int>(c) == lj.key_idx) continue;
+        refs.push_back({jn, static_cast<int>(lj.payload_idx.size())});
+        lj.payload_idx.push_back(static_cast<int>(c));
+        joined.fields.push_back(lj.proj.schema.fields[c]);
+      }
+      const auto& prev = d.stage_refs.back();
+      for (size_t i = 0; i < d.wire.size(); ++i) {
+        Field g = d.wire.fields[i];
+        if (joined.index_of(g.name)) g.name += "_p";
+        joined.fields.push_back(g);
+        refs.push_back(prev[i]);
+      }
+      d.wire = joined;
+      d.stage_refs.push_back(refs);
+      d.chain.push_back(std::move(lj));
+      return d;
+    }
+  throw InvalidInput("plan references unknown stream: " + name);
+}
+
+/// Register map of one fused-kernel program over a source.
+struct RegMap {
+  std::vector<int> base_proj;  // reg c < n_in -> projected column index
+  std::map<ColRef, int> reg_of;
+  int n_pred = 0, n_early = 0, n_in = 0, n_regs = 0;
+  std::vector<std::vector<int>> payload_regs;  // [join][k] reg of needed payload k
+  std::vector<std::vector<int>> payload_cols;  // [join][k] payload p
+};
+
+/// Decides which columns a program loads, in which phase. `needed` are final-wire columns the
+/// sink consumes; `early_wire` (sink key) must be loaded before the sink's probe.
+RegMap analyse(SourceDef& s, const std::vector<int>& needed, int early_wire, bool with_joins) {
+  RegMap m;
+  const auto& fin = s.stage_refs.back();
+  std::set<ColRef> need;
+  for (int w : needed) need.insert(fin[w]);
+  std::set<ColRef> early;
+  if (early_wire >= 0) early.insert(fin[early_wire]);
+  if (with_joins)
+    for (size_t j = 0; j < s.chain.size(); ++j) {
+      const ColRef k = s.stage_refs[j][s.chain[j].probe_key_stage];
+      need.insert(k);
+      early.insert(k);
+    }
+  // predicate columns first
+  for (const auto& a : s.scan->predicate) {
+    const int pi = static_cast<int>(s.proj.schema.require(a.column));
+    if (!m.reg_of.count({-1, pi})) {
+      m.reg_of[{-1, pi}] = static_cast<int>(m.base_proj.size());
+      m.base_proj.push_back(pi);
+    }
+  }
+  m.n_pred = static_cast<int>(m.base_proj.size());
+  for (const auto& r : early)
+    if (r.join < 0 && !m.reg_of.count(r)) {
+      m.reg_of[r] = static_cast<int>(m.base_proj.size());
+      m.base_proj.push_back(r.idx);
+    }
+  m.n_early = static_cast<int>(m.base_proj.size());
+  for (const auto& r : need)
+    if (r.join < 0 && !m.reg_of.count(r)) {
+      m.reg_of[r] = static_cast<int>(m.base_proj.size());
+      m.base_proj.push_back(r.idx);
+    }
+  m.n_in = static_cast<int>(m.base_proj.size());
+  int reg = m.n_in;
+  m.payload_regs.resize(s.chain.size());
+  m.payload_cols.resize(s.chain.size());
+  for (size_t j = 0; j < s.chain.size(); ++j) {
+    for (const auto& r : need)
+      if (r.join == static_cast<int>(j)) {
+        m.reg_of[r] = reg;
+        m.payload_regs[j].push_back(reg++);
+        m.payload_cols[j].push_back(r.idx);
+      }
+  }
+  m.n_regs = reg;
+  if (m.n_in > kMaxIn || m.n_regs > kMaxRegs) throw InvalidInput("plan touches too many columns for one fused program");
+  return m;
+}
+
+// ------------------------------------------------------------------------ batch planning
+struct ScanBatches {
+  std::vector<BatchPlan> batches;
+  uint64_t total_rows = 0;
+  uint64_t total_bytes = 0;
+  uint64_t max_batch_bytes = 0;
+  uint64_t max_segs = 0;
+};
+
+/// Groups surviving row groups of each file into batches of <= batch_bytes packed column chunks.
+ScanBatches plan_batches(FooterCache& fc, const ScanNode& scan, const std::vector<int>& file_cols, int file_base,
+                         uint64_t batch_bytes) {
+  ScanBatches out;
+  for (size_t f = 0; f < scan.paths.size(); ++f) {
+    auto meta = fc.get(scan.paths[f]);
+    if (meta->codec != Codec::Identity)
+      throw InvalidInput("block-codec PSTO needs the GPU inflate path (not in this build): " + scan.paths[f]);
+    const auto groups = prune(*meta, scan.predicate);
+    BatchPlan cur;
+    cur.file = file_base + static_cast<int>(f);
+    auto flush = [&] {
+      if (cur.groups.empty()) return;
+      out.total_rows += cur.total_rows;
+      out.total_bytes += cur.bytes;
+      out.max_batch_bytes = std::max(out.max_batch_bytes, cur.bytes);
+      out.max_segs = std::max<uint64_t>(out.max_segs, cur.groups.size());
+      out.batches.push_back(std::move(cur));
+      cur = BatchPlan{};
+      cur.file = file_base + static_cast<int>(f);
+    };
+    for (size_t g : groups) {
+      const GroupMeta& gm = meta->groups[g];
+      uint64_t gbytes = 0;
+      for (int c : file_cols) gbytes += gm.cols[c].csize;
+      if (!cur.groups.empty() && cur.bytes + gbytes > batch_bytes) flush();
+      // chunks of this group in file order, packed; merge adjacent extents
+      std::vector<std::pair<uint64_t, int>> order;
+      for (size_t k = 0; k < file_cols.size(); ++k) order.push_back({gm.cols[file_cols[k]].offset, static_cast<int>(k)});
+      std::sort(order.begin(), order.end());
+      std::vector<uint64_t> pos(file_cols.size());
+      for (auto& [off, k] : order) {
+        const uint64_t len = gm.cols[file_cols[k]].csize;
+        // the same file column may be requested twice (never in practice); reuse position
+        pos[k] = cur.bytes;
+        if (!cur.extents.empty() && cur.extents.back().file_off + cur.extents.back().len == off &&
+            cur.extents.back().buf_off + cur.extents.back().len == cur.bytes)
+          cur.extents.back().len += len;
+        else
+          cur.extents.push_back({off, len, cur.bytes});
+        cur.bytes += len;
+      }
+      cur.groups.push_back(g);
+      cur.rows.push_back(gm.rows);
+      cur.pos.push_back(std::move(pos));
+      cur.total_rows += gm.rows;
+    }
+    flush();
+  }
+  return out;
+}
+
+/// Segment descriptors of a batch placed at device address `dev_base`.
+std::vector<Segment> make_segments(const BatchPlan& b, uint8_t* dev_base, uint64_t& tiles) {
+  std::vector<Segment> segs(b.groups.size());
+  const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
+  tiles = 0;
+  for (size_t i = 0; i < b.groups.size(); ++i) {
+    Segment& s = segs[i];
+    std::memset(&s, 0, sizeof s);
+    for (size_t k = 0; k < b.pos[i].size(); ++k) s.col[k] = reinterpret_cast<const uint64_t*>(dev_base + b.pos[i][k]);
+    s.rows = b.rows[i];
+    s.tile_begin = tiles;
+    tiles += (b.rows[i] + T - 1) / T;
+  }
+  return segs;
+}
+
+// --------------------------------------------------------------------------- device views
+struct BatchView {
+  const Segment* d_segs = nullptr;
+  int nsegs = 0;
+  uint64_t ntiles = 0;
+  uint64_t rows = 0;   // upper bound (input rows)
+  uint64_t bytes = 0;  // algorithmic input bytes (column chunks scanned)
+};
+
+/// Materialised columnar batch in HBM (needed columns only).
+struct DevCols {
+  std::vector<DevBuf> cols;
+  DevBuf count;  // unsigned long long row counter
+  uint64_t cap = 0;
+  uint64_t rows = 0;  // host copy once known
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------------------ Staged
+struct StagedScan {
+  DevBuf data;
+  DevBuf segs;
+  int nsegs = 0;
+  uint64_t ntiles = 0, rows = 0, bytes = 0;
+};
+struct Staged {
+  std::string plan_json, data_root;
+  std::map<std::string, StagedScan> scans;  // key: "table|cols"
+  uint64_t bytes = 0;
+};
+
+namespace {
+
+std::string scan_key(const ScanNode& s, const std::vector<int>& file_cols) {
+  std::string k = s.table + "|";
+  for (int c : file_cols) k += std::to_string(c) + ",";
+  return k;
+}
+
+// ------------------------------------------------------------------------ the executor
+class Execution {
+ public:
+  struct Feed;
+  Execution(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode, Staged* staged)
+      : ctx_(ctx), mode_(mode), staged_(staged), plan_(QueryPlan::from_json_text(plan_json, data_root, ctx.rank, ctx.nranks)) {}
+
+  ResultRows run(bool want_rows);
+  // staging entry: read every scan's needed chunks into HBM
+  void stage(Staged& st);
+
+ private:
+  // ---- compilation ----
+  void compile();
+  std::vector<int> file_cols_of(const SourceDef& s, const RegMap& m) const {
+    std::vector<int> fc;
+    for (int p : m.base_proj) fc.push_back(s.proj.file_idx[p]);
+    return fc;
+  }
+
+  // ---- feeds ----
+  std::unique_ptr<Feed> open_feed(const ScanNode& scan, const std::vector<int>& file_cols);
+
+  // ---- stages ----
+  void build_local_tables();
+  ScanProgram base_program(const SourceDef& s, const RegMap& m, bool with_joins);
+  void materialize_into(DevCols& out, const ScanProgram& p0, const BatchView& v, const std::vector<int>& out_regs,
+                        int part_key_reg, DevBuf* part_counts);
+  DevCols alloc_cols(size_t ncols, uint64_t cap);
+  uint64_t read_count(DevCols& c);
+  void run_scan(const ScanProgram& p, const BatchView& v, bool timed);
+
+  // shuffle (nranks > 1)
+  struct Received {
+    DevBuf buf;
+    std::vector<Segment> segs;  // host descriptors
+    uint64_t rows = 0;
+  };
+  Received exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data);
+  BatchView upload_segments(std::vector<Segment> segs, DevBuf& holder);
+
+  void build_agg_table(uint64_t build_rows);
+  void finalize_grouped(ResultRows& out, bool want_rows);
+  void finalize_global(ResultRows& out);
+
+  Ctx& ctx_;
+  int mode_;
+  Staged* staged_;
+  QueryPlan plan_;
+  const JoinNode* shuffle_ = nullptr;
+  SourceDef bsrc_, psrc_;
+  bool agg_ = false, grouped_ = false;
+  // aggregate column resolution
+  std::vector<int> probe_sum_wire, build_sum_wire;  // wire idx per side
+  std::vector<std::pair<int, int>> sum_order;       // (side 0 build/1 probe, k) in agg.sums order
+  Schema result_schema_;
+  // local tables
+  struct LocalTable {
+    DevBuf keys, cnt, start;
+    std::vector<DevBuf> payload;
+    uint64_t cap = 0;
+    bool unique = true;
+    LocalTableDev dev{};
+  };
+  std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
+  // agg table
+  DevBuf agg_hot_, agg_cold_, agg_bloom_, global_acc_;
+  AggTableDev aggt_{};
+  uint64_t agg_cap_ = 0;
+  // stats
+  psg_stats st_{};
+  uint64_t launches0_ = 0;
+  std::vector<std::string> files_;
+  std::map<std::string, int> file_index_;
+  std::vector<DevBuf> keep_;  // buffers that must live until the end
+};
+
+// ------------------------------------------------------------------------------ feeds
+struct Execution::Feed {
+  virtual ~Feed() = default;
+  virtual bool next(BatchView& v) = 0;
+  virtual void done() = 0;
+  uint64_t total_rows = 0;
+  size_t nbatches = 0;
+};
+
+/// Streams batches from storage through the pinned ring into a ring of HBM slots.
+struct StreamFeed : Execution::Feed {
+  Ctx& ctx;
+  ScanBatches sb;
+  std::vector<std::string> files;
+  std::unique_ptr<Ingest> ingest;
+  std::vector<DevBuf> slots;
+  std::vector<cudaEvent_t> slot_free, copied;
+  std::vector<uint64_t> tiles;
+  uint64_t slot_bytes = 0;
+  size_t i = 0;
+  int cur_slot = -1;
+  StreamFeed(Ctx& c, const ScanNode& scan, const std::vector<int>& file_cols, FooterCache& fc) : ctx(c) {
+    sb = plan_batches(fc, scan, file_cols, 0, ctx.batch_bytes);
+    files = scan.paths;
+    total_rows = sb.total_rows;
+    nbatches = sb.batches.size();
+    if (sb.batches.empty()) return;
+    slot_bytes = (std::max(sb.max_batch_bytes, ctx.batch_bytes) + sb.max_segs * sizeof(Segment) + 4095) & ~4095ULL;
+    const int threads = std::max(1, ctx.io_threads);
+    const int pinned = ctx.pinned_slots > 0 ? ctx.pinned_slots : threads * 2 + 2;
+    ingest = std::make_unique<Ingest>(ctx, files, sb.batches, threads, slot_bytes, pinned);
+    const int nd = static_cast<int>(std::min<size_t>(sb.batches.size(), 6));
+    for (int k = 0; k < nd; ++k) {
+      slots.emplace_back(ctx.pool, slot_bytes, ctx.copy);
+      cudaEvent_t a, b;
+      PSG_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+      PSG_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+      slot_free.push_back(a);
+      copied.push_back(b);
+    }
+  }
+  ~StreamFeed() override {
+    cudaStreamSynchronize(ctx.copy);
+    cudaStreamSynchronize(ctx.compute);
+    ingest.reset();
+    for (auto e : slot_free) cudaEventDestroy(e);
+    for (auto e : copied) cudaEventDestroy(e);
+  }
+  bool next(BatchView& v) override {
+    if (i >= sb.batches.size()) return false;
+    const int k = static_cast<int>(i % slots.size());
+    const BatchPlan& b = sb.batches[i];
+    auto* base = slots[k].as<uint8_t>();
+    uint64_t nt = 0;
+    auto segs = make_segments(b, base, nt);
+    if (i >= slots.size()) PSG_CUDA(cudaStreamWaitEvent(ctx.copy, slot_free[k], 0));
+    ingest->copy_to_device(i, base, segs.data(), segs.size() * sizeof(Segment), ctx.copy);
+    PSG_CUDA(cudaEventRecord(copied[k], ctx.copy));
+    PSG_CUDA(cudaStreamWaitEvent(ctx.compute, copied[k], 0));
+    v.d_segs = reinterpret_cast<const Segment*>(base + b.bytes);
+    v.nsegs = static_cast<int>(segs.size());
+    v.ntiles = nt;
+    v.rows = b.total_rows;
+    v.bytes = b.bytes;
+    cur_slot = k;
+    ++i;
+    return true;
+  }
+  void done() override {
+    if (cur_slot >= 0) PSG_CUDA(cudaEventRecord(slot_free[cur_slot], ctx.compute));
+  }
+};
+
+/// One batch covering a scan's staged HBM image.
+struct StagedFeed : Execution::Feed {
+  const StagedScan* s;
+  bool given = false;
+  explicit StagedFeed(const StagedScan* sc) : s(sc) {
+    total_rows = sc->rows;
+    nbatches = sc->nsegs ? 1 : 0;
+  }
+  bool next(BatchView& v) override {
+    if (given || s->nsegs == 0) return false;
+    given = true;
+    v.d_segs = s->segs.as<Segment>();
+    v.nsegs = s->nsegs;
+    v.ntiles = s->ntiles;
+    v.rows = s->rows;
+    v.bytes = s->bytes;
+    return true;
+  }
+  void done() override {}
+};
+
+std::unique_ptr<Execution::Feed> Execution::open_feed(const ScanNode& scan, const std::vector<int>& file_cols) {
+  if (staged_) {
+    auto it = staged_->scans.find(scan_key(scan, file_cols));
+    if (it == staged_->scans.end()) throw InvalidInput("staged data does not cover scan " + scan.table);
+    return std::make_unique<StagedFeed>(&it->second);
+  }
+  return std::make_unique<StreamFeed>(ctx_, scan, file_cols, ctx_.footers);
+}
+
+// ------------------------------------------------------------------------------ compile
+void Execution::compile() {
+  plan_.validate();
+  shuffle_ = plan_.shuffle_join();
+  if (!shuffle_) throw InvalidInput("plans currently require one shuffled join");
+  bsrc_ = make_source(plan_, ctx_.footers, shuffle_->build);
+  psrc_ = make_source(plan_, ctx_.footers, shuffle_->probe);
+  const int bkey = static_cast<int>(bsrc_.wire.require(shuffle_->build_key));
+  const int pkey = static_cast<int>(psrc_.wire.require(shuffle_->probe_key));
+  if (bsrc_.wire.fields[bkey].type != LType::Int64) throw InvalidInput("partition key must be int64: " + shuffle_->build_key);
+  if (psrc_.wire.fields[pkey].type != LType::Int64) throw InvalidInput("partition key must be int64: " + shuffle_->probe_key);
+  agg_ = plan_.aggregate.has_value();
+  if (agg_) {
+    grouped_ = !plan_.aggregate->group_by.empty();
+    // joined schema = build payload (wire minus key) ++ probe wire ("_p" on clash)
+    Schema joined;
+    std::vector<std::pair<int, int>> origin;  // (side, wire idx)
+    for (size_t i = 0; i < bsrc_.wire.size(); ++i) {
+      if (static_cast<int>(i) == bkey) continue;
+      joined.fields.push_back(bsrc_.wire.fields[i]);
+      origin.push_back({0, static_cast<int>(i)});
+    }
+    for (size_t i = 0; i < psrc_.wire.size(); ++i) {
+      Field g = psrc_.wire.fields[i];
+      if (joined.index_of(g.name)) g.name += "_p";
+      joined.fields.push_back(g);
+      origin.push_back({1, static_cast<int>(i)});
+    }
+    if (grouped_) {
+      const size_t gi = joined.require(plan_.aggregate->group_by);
+      if (origin[gi] != std::make_pair(1, pkey))
+        throw InvalidInput("group key resolves to a build payload column; only the probe key is supported");
+      result_schema_.fields.push_back(joined.fields[gi]);
+    }
+    result_schema_.fields.push_back(Field{"rows", LType::Int64});
+    for (const auto& c : plan_.aggregate->sums) {
+      const size_t si = joined.require(c);
+      result_schema_.fields.push_back(Field{"sum_" + joined.fields[si].name, joined.fields[si].type});
+      auto [side, w] = origin[si];
+      if (side == 1) {
+        sum_order.push_back({1, static_cast<int>(probe_sum_wire.size())});
+        probe_sum_wire.push_back(w);
+      } else {
+        sum_order.push_back({0, static_cast<int>(build_sum_wire.size())});
+        build_sum_wire.push_back(w);
+      }
+    }
+    if (probe_sum_wire.size() > static_cast<size_t>(kMaxSums) || build_sum_wire.size() > static_cast<size_t>(kMaxSums))
+      throw InvalidInput("too many aggregate sums");
+  } else {
+    for (size_t i = 0; i < bsrc_.wire.size(); ++i)
+      if (static_cast<int>(i) != bkey) result_schema_.fields.push_back(bsrc_.wire.fields[i]);
+    for (size_t i = 0; i < psrc_.wire.size(); ++i) {
+      Field g = psrc_.wire.fields[i];
+      if (result_schema_.index_of(g.name)) g.name += "_p";
+      result_schema_.fields.push_back(g);
+    }
+  }
+}
+
+ScanProgram Execution::base_program(const SourceDef& s, const RegMap& m, bool with_joins) {
+  ScanProgram p;
+  std::memset(&p, 0, sizeof p);
+  p.n_in = m.n_in;
+  p.n_pred = m.n_pred;
+  p.n_early = m.n_early;
+  p.n_regs = std::max(1, m.n_regs);
+  p.n_atoms = static_cast<int>(s.scan->predicate.size());
+  if (p.n_atoms > kMaxAtoms) throw InvalidInput("too many predicate atoms");
+  for (int a = 0; a < p.n_atoms; ++a) {
+    const Atom& at = s.scan->predicate[a];
+    const int pi = static_cast<int>(s.proj.schema.require(at.column));
+    AtomDesc& d = p.atoms[a];
+    d.reg = m.reg_of.at({-1, pi});
+    d.op = static_cast<int>(at.op);
+    d.is_float = s.proj.schema.fields[pi].type == LType::Float64;
+    d.lit = d.is_float ? dbl_bits(at.as_float()) : static_cast<uint64_t>(at.as_int());
+  }
+  if (with_joins) {
+    auto& tables = (&s == &bsrc_) ? bl_tables_ : pl_tables_;
+    p.n_joins = static_cast<int>(s.chain.size());
+    if (p.n_joins > kMaxJoins) throw InvalidInput("too many local joins");
+    for (int j = 0; j < p.n_joins; ++j) {
+      JoinDesc& jd = p.joins[j];
+      jd.t = tables[j]->dev;
+      jd.key_reg = m.reg_of.at(s.stage_refs[j][s.chain[j].probe_key_stage]);
+      for (size_t k = 0; k < m.payload_regs[j].size(); ++k) jd.payload_reg[k] = m.payload_regs[j][k];
+    }
+  }
+  p.part_key_reg = -1;
+  p.key_reg = -1;
+  return p;
+}
+
+DevCols Execution::alloc_cols(size_t ncols, uint64_t cap) {
+  DevCols c;
+  c.cap = cap;
+  for (size_t i = 0; i < ncols; ++i) c.cols.emplace_back(ctx_.pool, std::max<uint64_t>(cap, 1) * 8, ctx_.compute);
+  c.count = DevBuf(ctx_.pool, 8, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(c.count.p, 0, 8, ctx_.compute));
+  return c;
+}
+
+uint64_t Execution::read_count(DevCols& c) {
+  uint64_t n = 0;
+  PSG_CUDA(cudaMemcpyAsync(&n, c.count.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  if (n > c.cap) throw Error(PSG_ERR_INTERNAL, "materialisation overflow");
+  c.rows = n;
+  return n;
+}
+
+void Execution::run_scan(const ScanProgram& p, const BatchView& v, bool timed) {
+  if (v.nsegs == 0) return;
+  if (timed) PSG_CUDA(cudaEventRecord(ctx_.ev_a, ctx_.compute));
+  launch_scan(p, v.d_segs, v.nsegs, v.ntiles, 0, ctx_.compute);
+  if (timed) {
+    PSG_CUDA(cudaEventRecord(ctx_.ev_b, ctx_.compute));
+    PSG_CUDA(cudaEventSynchronize(ctx_.ev_b));
+    float ms = 0;
+    PSG_CUDA(cudaEventElapsedTime(&ms, ctx_.ev_a, ctx_.ev_b));
+    st_.probe_kernel_ms += ms;
+    st_.probe_kernel_launches += 1;
+    st_.probe_kernel_bytes += v.bytes;
+  }
+}
+
+void Execution::materialize_into(DevCols& out, const ScanProgram& p0, const BatchView& v, const std::vector<int>& out_regs,
+                                 int part_key_reg, DevBuf* part_counts) {
+  ScanProgram p = p0;
+  p.sink = SINK_MATERIALIZE;
+  p.n_out = static_cast<int>(out_regs.size());
+  for (int o = 0; o < p.n_out; ++o) {
+    p.out_reg[o] = out_regs[o];
+    p.out_col[o] = out.cols[o].as<uint64_t>();
+  }
+  p.out_cap = out.cap;
+  p.out_count = out.count.as<unsigned long long>();
+  if (part_key_reg >= 0 && ctx_.nranks > 1) {
+    p.nparts = ctx_.nranks;
+    p.part_key_reg = part_key_reg;
+    p.part_counts = part_counts->as<unsigned long long>();
+  }
+  run_scan(p, v, false);
+}
+
+BatchView Execution::upload_segments(std::vector<Segment> segs, DevBuf& holder) {
+  BatchView v;
+  const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
+  uint64_t tiles = 0;
+  for (auto& s : segs) {
+    s.tile_begin = tiles;
+    tiles += (s.rows + T - 1) / T;
+    v.rows += s.rows;
+  }
+  if (segs.empty()) return v;
+  holder = DevBuf(ctx_.pool, segs.size() * sizeof(Segment), ctx_.compute);
+  PSG_CUDA(cudaMemcpyAsync(holder.p, segs.data(), segs.size() * sizeof(Segment), cudaMemcpyHostToDevice, ctx_.compute));
+  // keep host copy alive until the async copy is done
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  v.d_segs = holder.as<Segment>();
+  v.nsegs = static_cast<int>(segs.size());
+  v.ntiles = tiles;
+  return v;
+}
+
+// ---------------------------------------------------------------------- local join tables
+void Execution::build_local_tables() {
+  for (int side = 0; side < 2; ++side) {
+    SourceDef& s = side == 0 ? bsrc_ : psrc_;
+    auto& tables = side == 0 ? bl_tables_ : pl_tables_;
+    for (size_t j = 0; j < s.chain.size(); ++j) {
+      LocalJoinDef& lj = s.chain[j];
+      auto t = std::make_unique<LocalTable>();
+      // program over the replicated scan: predicate + key + needed payload columns
+      SourceDef rs;
+      rs.scan = lj.scan;
+      rs.proj = lj.proj;
+      rs.wire = lj.proj.schema;
+      std::vector<ColRef> refs;
+      for (size_t i = 0; i < rs.wire.size(); ++i) refs.push_back({-1, static_cast<int>(i)});
+      rs.stage_refs.push_back(refs);
+      // needed payload of this join = payload cols referenced by the consuming programs; we load
+      // every payload column the source may need (computed by the caller's RegMap later), so
+      // conservatively take all payload columns that appear in any needed ref.
+      std::vector<int> needed{lj.key_idx};
+      for (int p : lj.needed_payload) needed.push_back(lj.payload_idx[p]);
+      RegMap m = analyse(rs, needed, -1, false);
+      ScanProgram p = base_program(rs, m, false);
+      std::vector<int> out_regs;
+      for (int w : needed) out_regs.push_back(m.reg_of.at({-1, w}));
+      PSG_TRACE_MSG("local table %s: regs %d in %d", lj.node->id.c_str(), m.n_regs, m.n_in);
+      auto feed = open_feed(*rs.scan, file_cols_of(rs, m));
+      PSG_TRACE_MSG("local table: feed %zu batches %llu rows", feed->nbatches, static_cast<unsigned long long>(feed->total_rows));
+      DevCols mat = alloc_cols(out_regs.size(), std::max<uint64_t>(feed->total_rows, 1));
+      BatchView v;
+      while (feed->next(v)) {
+        materialize_into(mat, p, v, out_regs, -1, nullptr);
+        feed->done();
+        st_.ingest_bytes += v.bytes;
+      }
+      const uint64_t n = read_count(mat);
+      // CSR hash table
+      t->cap = pow2_at_least(std::max<uint64_t>(2 * n, 16));
+      t->keys = DevBuf(ctx_.pool, t->cap * 8, ctx_.compute);
+      t->cnt = DevBuf(ctx_.pool, (t->cap + 1) * 4, ctx_.compute);
+      t->start = DevBuf(ctx_.pool, (t->cap + 1) * 4, ctx_.compute);
+      DevBuf cursor(ctx_.pool, (t->cap + 1) * 4, ctx_.compute);
+      DevBuf maxc(ctx_.pool, 4, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(maxc.p, 0, 4, ctx_.compute));
+      PSG_CUDA(cudaMemsetAsync(cursor.p, 0, (t->cap + 1) * 4, ctx_.compute));
+      launch_local_init(t->keys.as<uint64_t>(), t->cnt.as<uint32_t>(), t->cap, ctx_.compute);
+      const uint64_t* bk = mat.cols[0].as<uint64_t>();
+      launch_local_count(t->keys.as<uint64_t>(), t->cnt.as<uint32_t>(), t->cap - 1, bk, n, maxc.as<unsigned>(), ctx_.compute);
+      size_t tb = exclusive_scan_u32(nullptr, nullptr, t->cap + 1, nullptr, 0, ctx_.compute);
+      DevBuf tmp(ctx_.pool, tb, ctx_.compute);
+      exclusive_scan_u32(t->cnt.as<uint32_t>(), t->start.as<uint32_t>(), t->cap + 1, tmp.p, tb, ctx_.compute);
+      const int np = static_cast<int>(lj.needed_payload.size());
+      std::vector<const uint64_t*> src;
+      std::vector<uint64_t*> dst;
+      for (int k = 0; k < np; ++k) {
+        t->payload.emplace_back(ctx_.pool, std::max<uint64_t>(n, 1) * 8, ctx_.compute);
+        src.push_back(mat.cols[1 + k].as<uint64_t>());
+        dst.push_back(t->payload.back().as<uint64_t>());
+      }
+      launch_local_fill(t->keys.as<uint64_t>(), t->start.as<uint32_t>(), cursor.as<uint32_t>(), t->cap - 1, bk, src.data(),
+                        dst.data(), np, n, ctx_.compute);
+      unsigned mx = 0;
+      PSG_CUDA(cudaMemcpyAsync(&mx, maxc.p, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      t->unique = mx <= 1;
+      t->dev.keys = t->keys.as<uint64_t>();
+      t->dev.cnt = t->cnt.as<uint32_t>();
+      t->dev.start = t->start.as<uint32_t>();
+      t->dev.mask = t->cap - 1;
+      t->dev.npayload = np;
+      for (int k = 0; k < np; ++k) t->dev.payload[k] = t->payload[k].as<uint64_t>();
+      tables.push_back(std::move(t));
+    }
+  }
+}
+
+// --------------------------------------------------------------------------- agg table
+void Execution::build_agg_table(uint64_t build_rows) {
+  agg_cap_ = pow2_at_least(std::max<uint64_t>(2 * build_rows, 16));
+  const int nps = static_cast<int>(probe_sum_wire.size()), nbs = static_cast<int>(build_sum_wire.size());
+  int hw = 2 + nps;
+  hw = hw <= 2 ? 2 : (hw <= 4 ? 4 : 8 * ((hw + 7) / 8));
+  const int cw = 1 + nbs;
+  agg_hot_ = DevBuf(ctx_.pool, (agg_cap_ + 1) * hw * 8, ctx_.compute);
+  agg_cold_ = DevBuf(ctx_.pool, (agg_cap_ + 1) * cw * 8, ctx_.compute);
+  std::memset(&aggt_, 0, sizeof aggt_);
+  aggt_.hot = agg_hot_.as<uint64_t>();
+  aggt_.cold = agg_cold_.as<uint64_t>();
+  aggt_.mask = agg_cap_ - 1;
+  aggt_.hw = hw;
+  aggt_.cw = cw;
+  aggt_.nps = nps;
+  aggt_.nbs = nbs;
+  for (int i = 0; i < nps; ++i) aggt_.ps_float[i] = psrc_.wire.fields[probe_sum_wire[i]].type == LType::Float64;
+  for (int i = 0; i < nbs; ++i) aggt_.bs_float[i] = bsrc_.wire.fields[build_sum_wire[i]].type == LType::Float64;
+  // Bloom filter when the hot table would not stay L2-resident (~16 bits per key, <= 32 MB).
+  const uint64_t hot_bytes = (agg_cap_ + 1) * hw * 8;
+  if (hot_bytes > (48ull << 20) && ctx_.semijoin) {
+    uint64_t words = pow2_at_least(std::max<uint64_t>(build_rows / 2, 1024));
+    words = std::min<uint64_t>(words, 8ull << 20);
+    agg_bloom_ = DevBuf(ctx_.pool, words * 4, ctx_.compute);
+    aggt_.bloom = agg_bloom_.as<uint32_t>();
+    aggt_.bloom_mask = words - 1;
+  }
+  launch_agg_init(aggt_, agg_cap_, ctx_.compute);
+}
+
+// ---------------------------------------------------------------------------- shuffle
+Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data) {
+  const int n = ctx_.nranks;
+  Received rcv;
+  // dest bases (exclusive scan of the per-destination histogram) and scatter into send regions
+  DevBuf base(ctx_.pool, n * 8, ctx_.compute), cursor(ctx_.pool, n * 8, ctx_.compute);
+  size_t tb = exclusive_scan_u64(nullptr, nullptr, n, nullptr, 0, ctx_.compute);
+  DevBuf tmp(ctx_.pool, tb, ctx_.compute);
+  exclusive_scan_u64(part_counts.as<unsigned long long>(), base.as<unsigned long long>(), n, tmp.p, tb, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(cursor.p, 0, n * 8, ctx_.compute));
+  // counts matrix: allgather of every rank's histogram
+  DevBuf matrix(ctx_.pool, static_cast<size_t>(n) * n * 8, ctx_.compute);
+  PSG_NCCL(ncclAllGather(part_counts.p, matrix.p, n, ncclUint64, ctx_.nccl, ctx_.compute));
+  std::vector<uint64_t> m(static_cast<size_t>(n) * n);
+  PSG_CUDA(cudaMemcpyAsync(m.data(), matrix.p, m.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));  // the one data-dependent host sync per wave
+  const int me = ctx_.rank;
+  uint64_t nrows = 0;
+  for (int d = 0; d < n; ++d) nrows += m[static_cast<size_t>(me) * n + d];
+  DevBuf send(ctx_.pool, std::max<uint64_t>(nrows, 1) * ncols * 8, ctx_.compute);
+  if (have_data && nrows) {
+    std::vector<const uint64_t*> in;
+    for (int c = 0; c < ncols; ++c) in.push_back(mat.cols[c].as<uint64_t>());
+    launch_part_scatter(in.data(), ncols, nrows, key_col, n, base.as<unsigned long long>(),
+                        part_counts.as<unsigned long long>(), cursor.as<unsigned long long>(), send.as<uint64_t>(),
+                        ctx_.compute);
+  }
+  uint64_t rtotal = 0;
+  for (int s = 0; s < n; ++s) rtotal += m[static_cast<size_t>(s) * n + me];
+  rcv.buf = DevBuf(ctx_.pool, std::max<uint64_t>(rtotal, 1) * ncols * 8, ctx_.compute);
+  rcv.rows = rtotal;
+  PSG_NCCL(ncclGroupStart());
+  uint64_t soff = 0, roff = 0;
+  for (int p = 0; p < n; ++p) {
+    const uint64_t sc = m[static_cast<size_t>(me) * n + p];
+    const uint64_t rc = m[static_cast<size_t>(p) * n + me];
+    if (sc) PSG_NCCL(ncclSend(send.as<uint64_t>() + soff * ncols, sc * ncols, ncclUint64, p, ctx_.nccl, ctx_.compute));
+    if (rc) PSG_NCCL(ncclRecv(rcv.buf.as<uint64_t>() + roff * ncols, rc * ncols, ncclUint64, p, ctx_.nccl, ctx_.compute));
+    if (rc) {
+      Segment sg;
+      std::memset(&sg, 0, sizeof sg);
+      for (int c = 0; c < ncols; ++c) sg.col[c] = rcv.buf.as<uint64_t>() + roff * ncols + c * rc;
+      sg.rows = rc;
+      rcv.segs.push_back(sg);
+      if (p != me) st_.bytes_received += rc * ncols * 8;
+    }
+    soff += sc;
+    roff += rc;
+  }
+  PSG_NCCL(ncclGroupEnd());
+  st_.waves += 1;
+  return rcv;
+}
+
+// ---------------------------------------------------------------------------- finalize
+void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
+  const uint64_t nslots = agg_cap_ + 1;
+  DevBuf keys(ctx_.pool, nslots * 8, ctx_.compute), slots(ctx_.pool, nslots * 8, ctx_.compute);
+  DevBuf counter(ctx_.pool, 8, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(counter.p, 0, 8, ctx_.compute));
+  launch_agg_compact(aggt_, agg_cap_, keys.as<uint64_t>(), slots.as<unsigned long long>(),
+                     counter.as<unsigned long long>(), ctx_.compute);
+  uint64_t ng = 0;
+  PSG_CUDA(cudaMemcpyAsync(&ng, counter.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  DevBuf k2(ctx_.pool, std::max<uint64_t>(ng, 1) * 8, ctx_.compute), s2(ctx_.pool, std::max<uint64_t>(ng, 1) * 8, ctx_.compute);
+  size_t tb = sort_pairs_i64(nullptr, nullptr, nullptr, nullptr, ng, nullptr, 0, ctx_.compute);
+  DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
+  if (ng)
+    sort_pairs_i64(keys.as<uint64_t>(), k2.as<uint64_t>(), slots.as<unsigned long long>(), s2.as<unsigned long long>(), ng,
+                   tmp.p, tb, ctx_.compute);
+  const int nc = static_cast<int>(result_schema_.size());
+  std::vector<int32_t> kind, idx;
+  kind.push_back(0), idx.push_back(0);
+  kind.push_back(1), idx.push_back(0);
+  for (auto [side, k] : sum_order) {
+    kind.push_back(side == 1 ? 2 : 3);
+    idx.push_back(k);
+  }
+  DevBuf rows(ctx_.pool, std::max<uint64_t>(ng, 1) * nc * 8, ctx_.compute);
+  launch_agg_emit(aggt_, k2.as<uint64_t>(), s2.as<unsigned long long>(), ng, nc, kind.data(), idx.data(), rows.as<uint64_t>(),
+                  ctx_.compute);
+  out.nrows = ng;
+  if (want_rows) {
+    out.words.resize(ng * nc);
+    if (ng) PSG_CUDA(cudaMemcpyAsync(out.words.data(), rows.p, ng * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    st_.result_bytes += ng * nc * 8;
+  }
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+}
+
+void Execution::finalize_global(ResultRows& out) {
+  const int nps = static_cast<int>(probe_sum_wire.size()), nbs = static_cast<int>(build_sum_wire.size());
+  std::vector<uint64_t> acc(1 + nps + nbs);
+  PSG_CUDA(cudaMemcpyAsync(acc.data(), global_acc_.p, acc.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  st_.result_bytes += acc.size() * 8;
+  if (acc[0] == 0) {
+    out.nrows = 0;
+    return;
+  }
+  out.nrows = 1;
+  out.words.push_back(acc[0]);
+  for (auto [side, k] : sum_order) out.words.push_back(side == 1 ? acc[1 + k] : acc[1 + nps + k]);
+}
+
+// ---------------------------------------------------------------------------------- run
+ResultRows Execution::run(bool want_rows) {
+  const auto t0 = Clock::now();
+  launches0_ = kernel_launch_count();
+  ctx_.pool.reset_peak();
+  if (plan_.memory_budget_bytes) ctx_.pool.set_budget(ctx_.pool.used() + plan_.memory_budget_bytes);
+  PSG_TRACE_MSG("run: compile");
+  cudaEvent_t ev0, ev1;
+  PSG_CUDA(cudaEventCreate(&ev0));
+  PSG_CUDA(cudaEventCreate(&ev1));
+  PSG_CUDA(cudaEventRecord(ev0, ctx_.compute));
+  compile();
+  PSG_TRACE_MSG("run: compiled, build wire %zu cols, probe wire %zu cols", bsrc_.wire.size(), psrc_.wire.size());
+  ResultRows out;
+  out.schema = result_schema_;
+  const int nr = ctx_.nranks;
+  const int bkey = static_cast<int>(bsrc_.wire.require(shuffle_->build_key));
+  const int pkey = static_cast<int>(psrc_.wire.require(shuffle_->probe_key));
+
+  // Needed wire columns per side (projection pushdown past the shuffle).
+  std::vector<int> bneed{bkey}, pneed{pkey};
+  if (agg_) {
+    for (int w : build_sum_wire) bneed.push_back(w);
+    for (int w : probe_sum_wire) pneed.push_back(w);
+  } else {
+    for (size_t i = 0; i < bsrc_.wire.size(); ++i)
+      if (static_cast<int>(i) != bkey) bneed.push_back(static_cast<int>(i));
+    for (size_t i = 0; i < psrc_.wire.size(); ++i)
+      if (static_cast<int>(i) != pkey) pneed.push_back(static_cast<int>(i));
+  }
+  RegMap bm = analyse(bsrc_, bneed, bkey, true);
+  RegMap pm = analyse(psrc_, pneed, pkey, true);
+  for (size_t j = 0; j < bsrc_.chain.size(); ++j) bsrc_.chain[j].needed_payload = bm.payload_cols[j];
+  for (size_t j = 0; j < psrc_.chain.size(); ++j) psrc_.chain[j].needed_payload = pm.payload_cols[j];
+
+  const auto t_storage = Clock::now();
+  PSG_TRACE_MSG("run: local tables");
+  build_local_tables();
+  PSG_TRACE_MSG("run: build side");
+  for (auto& t : bl_tables_)
+    if (!t->unique) throw InvalidInput("local join build side with duplicate keys is not supported by the fused path yet");
+  for (auto& t : pl_tables_)
+    if (!t->unique) throw InvalidInput("local join build side with duplicate keys is not supported by the fused path yet");
+
+  // ---------------- build side ----------------
+  ScanProgram bp = base_program(bsrc_, bm, true);
+  std::vector<int> b_out;  // materialised columns: key first, then the rest of bneed
+  for (int w : bneed) b_out.push_back(bm.reg_of.at(bsrc_.stage_refs.back()[w]));
+  auto bfeed = open_feed(*bsrc_.scan, file_cols_of(bsrc_, bm));
+  std::vector<Received> brecv;
+  DevCols bmat;
+  if (nr == 1) {
+    bmat = alloc_cols(b_out.size(), std::max<uint64_t>(bfeed->total_rows, 1));
+    BatchView v;
+    while (bfeed->next(v)) {
+      materialize_into(bmat, bp, v, b_out, -1, nullptr);
+      bfeed->done();
+      st_.ingest_bytes += v.bytes;
+    }
+    read_count(bmat);
+  } else {
+    // agree on the wave count (the reference's kDoneFlag vote, pipeline.cpp:696-722)
+    uint64_t waves = bfeed->nbatches;
+    DevBuf wv(ctx_.pool, 8, ctx_.compute);
+    PSG_CUDA(cudaMemcpyAsync(wv.p, &waves, 8, cudaMemcpyHostToDevice, ctx_.compute));
+    PSG_NCCL(ncclAllReduce(wv.p, wv.p, 1, ncclUint64, ncclMax, ctx_.nccl, ctx_.compute));
+    PSG_CUDA(cudaMemcpyAsync(&waves, wv.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    for (uint64_t w = 0; w < waves; ++w) {
+      BatchView v;
+      const bool have = bfeed->next(v);
+      DevCols mat = alloc_cols(b_out.size(), std::max<uint64_t>(have ? v.rows : 1, 1));
+      DevBuf pc(ctx_.pool, nr * 8, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(pc.p, 0, nr * 8, ctx_.compute));
+      if (have) {
+        materialize_into(mat, bp, v, b_out, b_out[0], &pc);
+        bfeed->done();
+        st_.ingest_bytes += v.bytes;
+      }
+      brecv.push_back(exchange(mat, static_cast<int>(b_out.size()), 0, pc, have));
+    }
+  }
+  uint64_t build_rows = 0;
+  if (nr == 1) build_rows = bmat.rows;
+  else
+    for (auto& r : brecv) build_rows += r.rows;
+
+  // Program over materialised build rows: reg k = column k of the materialised batch.
+  auto batch_program = [&](int ncols) {
+    ScanProgram p;
+    std::memset(&p, 0, sizeof p);
+    p.n_in = ncols;
+    p.n_pred = 0;
+    p.n_early = std::min(1, ncols);
+    p.n_regs = std::max(1, ncols);
+    p.part_key_reg = -1;
+    p.key_reg = 0;
+    return p;
+  };
+  std::vector<Segment> bsegs;
+  if (nr == 1) {
+    Segment sg;
+    std::memset(&sg, 0, sizeof sg);
+    for (size_t c = 0; c < b_out.size(); ++c) sg.col[c] = bmat.cols[c].as<uint64_t>();
+    sg.rows = bmat.rows;
+    if (sg.rows) bsegs.push_back(sg);
+  } else {
+    for (auto& r : brecv)
+      for (auto& s : r.segs) bsegs.push_back(s);
+  }
+  DevBuf bseg_holder;
+  BatchView bview = upload_segments(bsegs, bseg_holder);
+
+  // For no-aggregate plans the build side becomes a CSR table of full wire rows.
+  std::unique_ptr<LocalTable> final_table;
+  if (agg_) {
+    build_agg_table(build_rows);
+    ScanProgram p = batch_program(static_cast<int>(b_out.size()));
+    p.sink = SINK_BUILD;
+    p.agg = aggt_;
+    p.n_sum = static_cast<int>(build_sum_wire.size());
+    for (int b = 0; b < p.n_sum; ++b) p.sum_reg[b] = 1 + b;
+    run_scan(p, bview, false);
+    launch_bloom_build(aggt_, agg_cap_, ctx_.compute);
+    if (!grouped_) {
+      global_acc_ = DevBuf(ctx_.pool, (2 * kMaxSums + 1) * 8, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(global_acc_.p, 0, (2 * kMaxSums + 1) * 8, ctx_.compute));
+    }
+  } else {
+    // materialise received build rows contiguously, then CSR-build with payload = other columns
+    const int nc = static_cast<int>(b_out.size());
+    DevCols all = alloc_cols(nc, std::max<uint64_t>(build_rows, 1));
+    ScanProgram p = batch_program(nc);
+    p.n_early = nc;
+    std::vector<int> regs(nc);
+    std::iota(regs.begin(), regs.end(), 0);
+    materialize_into(all, p, bview, regs, -1, nullptr);
+    const uint64_t n = read_count(all);
+    final_table = std::make_unique<LocalTable>();
+    auto& t = *final_table;
+    t.cap = pow2_at_least(std::max<uint64_t>(2 * n, 16));
+    t.keys = DevBuf(ctx_.pool, t.cap * 8, ctx_.compute);
+    t.cnt = DevBuf(ctx_.pool, (t.cap + 1) * 4, ctx_.compute);
+    t.start = DevBuf(ctx_.pool, (t.cap + 1) * 4, ctx_.compute);
+    DevBuf cursor(ctx_.pool, (t.cap + 1) * 4, ctx_.compute), maxc(ctx_.pool, 4, ctx_.compute);
+    PSG_CUDA(cudaMemsetAsync(maxc.p, 0, 4, ctx_.compute));
+    PSG_CUDA(cudaMemsetAsync(cursor.p, 0, (t.cap + 1) * 4, ctx_.compute));
+    launch_local_init(t.keys.as<uint64_t>(), t.cnt.as<uint32_t>(), t.cap, ctx_.compute);
+    launch_local_count(t.keys.as<uint64_t>(), t.cnt.as<uint32_t>(), t.cap - 1, all.cols[0].as<uint64_t>(), n,
+                       maxc.as<unsigned>(), ctx_.compute);
+    size_t tb = exclusive_scan_u32(nullptr, nullptr, t.cap + 1, nullptr, 0, ctx_.compute);
+    DevBuf tmp(ctx_.pool, tb, ctx_.compute);
+    exclusive_scan_u32(t.cnt.as<uint32_t>(), t.start.as<uint32_t>(), t.cap + 1, tmp.p, tb, ctx_.compute);
+    std::vector<const uint64_t*> src;
+    std::vector<uint64_t*> dst;
+    for (int c = 1; c < nc; ++c) {
+      t.payload.emplace_back(ctx_.pool, std::max<uint64_t>(n, 1) * 8, ctx_.compute);
+      src.push_back(all.cols[c].as<uint64_t>());
+      dst.push_back(t.payload.back().as<uint64_t>());
+    }
+    launch_local_fill(t.keys.as<uint64_t>(), t.start.as<uint32_t>(), cursor.as<uint32_t>(), t.cap - 1,
+                      all.cols[0].as<uint64_t>(), src.data(), dst.data(), nc - 1, n, ctx_.compute);
+    t.dev.keys = t.keys.as<uint64_t>();
+    t.dev.cnt = t.cnt.as<uint32_t>();
+    t.dev.start = t.start.as<uint32_t>();
+    t.dev.mask = t.cap - 1;
+    t.dev.npayload = nc - 1;
+    for (int c = 0; c < nc - 1; ++c) t.dev.payload[c] = t.payload[c].as<uint64_t>();
+    PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  }
+  brecv.clear();
+  bmat = DevCols{};
+
+  PSG_TRACE_MSG("run: probe side (build rows %llu)", static_cast<unsigned long long>(build_rows));
+  // ---------------- probe side ----------------
+  ScanProgram pp = base_program(psrc_, pm, true);
+  std::vector<int> p_out;
+  for (int w : pneed) p_out.push_back(pm.reg_of.at(psrc_.stage_refs.back()[w]));
+  auto pfeed = open_feed(*psrc_.scan, file_cols_of(psrc_, pm));
+  std::vector<DevCols> joined_parts;  // no-aggregate results
+  auto consume_materialised = [&](const BatchView& v, int ncols) {
+    // v: segments whose columns are p_out order (key first)
+    if (agg_) {
+      ScanProgram p = batch_program(ncols);
+      p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
+      p.agg = aggt_;
+      p.key_reg = 0;
+      p.n_sum = static_cast<int>(probe_sum_wire.size());
+      for (int s = 0; s < p.n_sum; ++s) p.sum_reg[s] = 1 + s;
+      if (!grouped_) {
+        p.global_acc = global_acc_.as<unsigned long long>();
+        for (int s = 0; s < p.n_sum; ++s) p.global_float[1 + s] = aggt_.ps_float[s];
+        for (int b = 0; b < aggt_.nbs; ++b) p.global_float[1 + p.n_sum + b] = aggt_.bs_float[b];
+      }
+      run_scan(p, v, true);
+    } else {
+      // compact, then expanding join against the final CSR table
+      DevCols c = alloc_cols(ncols, std::max<uint64_t>(v.rows, 1));
+      ScanProgram p = batch_program(ncols);
+      p.n_early = ncols;
+      std::vector<int> regs(ncols);
+      std::iota(regs.begin(), regs.end(), 0);
+      materialize_into(c, p, v, regs, -1, nullptr);
+      const uint64_t n = read_count(c);
+      DevBuf counts(ctx_.pool, (n + 1) * 4, ctx_.compute), offs(ctx_.pool, (n + 1) * 4, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(counts.p, 0, (n + 1) * 4, ctx_.compute));
+      launch_expand_count(final_table->dev, c.cols[0].as<uint64_t>(), n, counts.as<uint32_t>(), ctx_.compute);
+      size_t tb = exclusive_scan_u32(nullptr, nullptr, n + 1, nullptr, 0, ctx_.compute);
+      DevBuf tmp(ctx_.pool, tb, ctx_.compute);
+      exclusive_scan_u32(counts.as<uint32_t>(), offs.as<uint32_t>(), n + 1, tmp.p, tb, ctx_.compute);
+      uint32_t total = 0;
+      PSG_CUDA(cudaMemcpyAsync(&total, offs.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      const int np = final_table->dev.npayload;
+      DevCols j = alloc_cols(np + ncols, std::max<uint64_t>(total, 1));
+      std::vector<const uint64_t*> pc;
+      std::vector<uint64_t*> oc;
+      for (int q = 0; q < ncols; ++q) pc.push_back(c.cols[q].as<uint64_t>());
+      for (int q = 0; q < np + ncols; ++q) oc.push_back(j.cols[q].as<uint64_t>());
+      launch_expand_write(final_table->dev, c.cols[0].as<uint64_t>(), n, offs.as<uint32_t>(), pc.data(), ncols, oc.data(),
+                          ctx_.compute);
+      j.rows = total;
+      joined_parts.push_back(std::move(j));
+    }
+  };
+
+  if (nr == 1 && agg_) {
+    ScanProgram p = pp;
+    p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
+    p.agg = aggt_;
+    p.key_reg = pm.reg_of.at(psrc_.stage_refs.back()[pkey]);
+    p.n_sum = static_cast<int>(probe_sum_wire.size());
+    for (int s = 0; s < p.n_sum; ++s) p.sum_reg[s] = pm.reg_of.at(psrc_.stage_refs.back()[probe_sum_wire[s]]);
+    if (!grouped_) {
+      p.global_acc = global_acc_.as<unsigned long long>();
+      for (int s = 0; s < p.n_sum; ++s) p.global_float[1 + s] = aggt_.ps_float[s];
+      for (int b = 0; b < aggt_.nbs; ++b) p.global_float[1 + p.n_sum + b] = aggt_.bs_float[b];
+    }
+    BatchView v;
+    while (pfeed->next(v)) {
+      run_scan(p, v, staged_ != nullptr);
+      pfeed->done();
+      st_.ingest_bytes += v.bytes;
+    }
+  } else {
+    uint64_t waves = pfeed->nbatches;
+    if (nr > 1) {
+      DevBuf wv(ctx_.pool, 8, ctx_.compute);
+      PSG_CUDA(cudaMemcpyAsync(wv.p, &waves, 8, cudaMemcpyHostToDevice, ctx_.compute));
+      PSG_NCCL(ncclAllReduce(wv.p, wv.p, 1, ncclUint64, ncclMax, ctx_.nccl, ctx_.compute));
+      PSG_CUDA(cudaMemcpyAsync(&waves, wv.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    }
+    for (uint64_t w = 0; w < waves; ++w) {
+      BatchView v;
+      const bool have = pfeed->next(v);
+      DevCols mat = alloc_cols(p_out.size(), std::max<uint64_t>(have ? v.rows : 1, 1));
+      DevBuf pc(ctx_.pool, nr * 8, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(pc.p, 0, nr * 8, ctx_.compute));
+      if (have) {
+        materialize_into(mat, pp, v, p_out, p_out[0], &pc);
+        pfeed->done();
+        st_.ingest_bytes += v.bytes;
+      }
+      if (nr > 1) {
+        Received r = exchange(mat, static_cast<int>(p_out.size()), 0, pc, have);
+        DevBuf holder;
+        BatchView rv = upload_segments(r.segs, holder);
+        consume_materialised(rv, static_cast<int>(p_out.size()));
+        PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      } else {
+        const uint64_t n = read_count(mat);
+        Segment sg;
+        std::memset(&sg, 0, sizeof sg);
+        for (size_t c = 0; c < p_out.size(); ++c) sg.col[c] = mat.cols[c].as<uint64_t>();
+        sg.rows = n;
+        DevBuf holder;
+        std::vector<Segment> one;
+        if (n) one.push_back(sg);
+        BatchView rv = upload_segments(one, holder);
+        consume_materialised(rv, static_cast<int>(p_out.size()));
+        PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      }
+    }
+  }
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  st_.storage_phase_s = secs_since(t_storage);
+
+  PSG_TRACE_MSG("run: finalize");
+  // ---------------- finalize ----------------
+  if (agg_) {
+    if (grouped_) finalize_grouped(out, want_rows);
+    else finalize_global(out);
+  } else {
+    const int nc = static_cast<int>(result_schema_.size());
+    uint64_t total = 0;
+    for (auto& j : joined_parts) total += j.rows;
+    out.nrows = total;
+    if (want_rows) {
+      out.words.resize(total * nc);
+      uint64_t at = 0;
+      for (auto& j : joined_parts) {
+        if (!j.rows) continue;
+        DevBuf rows(ctx_.pool, j.rows * nc * 8, ctx_.compute);
+        // joined columns are [build payload..., probe key, probe others...]; restore the probe
+        // side's wire order (payload ++ probe wire, ops.cpp:193-200)
+        std::vector<const uint64_t*> cols;
+        const int npay = nc - static_cast<int>(psrc_.wire.size());
+        for (int c = 0; c < npay; ++c) cols.push_back(j.cols[c].as<uint64_t>());
+        for (size_t w = 0; w < psrc_.wire.size(); ++w) {
+          const int at = static_cast<int>(std::find(pneed.begin(), pneed.end(), static_cast<int>(w)) - pneed.begin());
+          cols.push_back(j.cols[npay + at].as<uint64_t>());
+        }
+        launch_rows_from_cols(cols.data(), nc, j.rows, rows.as<uint64_t>(), ctx_.compute);
+        PSG_CUDA(cudaMemcpyAsync(out.words.data() + at * nc, rows.p, j.rows * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+        PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+        at += j.rows;
+      }
+      st_.result_bytes += total * nc * 8;
+    }
+  }
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  PSG_CUDA(cudaGetLastError());
+  PSG_CUDA(cudaEventRecord(ev1, ctx_.compute));
+  PSG_CUDA(cudaEventSynchronize(ev1));
+  float dms = 0;
+  PSG_CUDA(cudaEventElapsedTime(&dms, ev0, ev1));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  st_.device_ms = dms;
+  st_.result_rows = out.nrows;
+  st_.runtime_s = secs_since(t0);
+  st_.peak_bytes = ctx_.pool.peak();
+  st_.kernel_launches = kernel_launch_count() - launches0_;
+  out.stats = st_;
+  if (plan_.memory_budget_bytes) ctx_.pool.set_budget(0);
+  return out;
+}
+
+void Execution::stage(Staged& st) {
+  compile();
+  const int bkey = static_cast<int>(bsrc_.wire.require(shuffle_->build_key));
+  const int pkey = static_cast<int>(psrc_.wire.require(shuffle_->probe_key));
+  std::vector<int> bneed{bkey}, pneed{pkey};
+  if (agg_) {
+    for (int w : build_sum_wire) bneed.push_back(w);
+    for (int w : probe_sum_wire) pneed.push_back(w);
+  } else {
+    for (size_t i = 0; i < bsrc_.wire.size(); ++i)
+      if (static_cast<int>(i) != bkey) bneed.push_back(static_cast<int>(i));
+    for (size_t i = 0; i < psrc_.wire.size(); ++i)
+      if (static_cast<int>(i) != pkey) pneed.push_back(static_cast<int>(i));
+  }
+  RegMap bm = analyse(bsrc_, bneed, bkey, true);
+  RegMap pm = analyse(psrc_, pneed, pkey, true);
+  std::vector<std::pair<const ScanNode*, std::vector<int>>> scans;
+  for (int side = 0; side < 2; ++side) {
+    SourceDef& s = side == 0 ? bsrc_ : psrc_;
+    RegMap& m = side == 0 ? bm : pm;
+    for (size_t j = 0; j < s.chain.size(); ++j) {
+      LocalJoinDef& lj = s.chain[j];
+      SourceDef rs;
+      rs.scan = lj.scan;
+      rs.proj = lj.proj;
+      rs.wire = lj.proj.schema;
+      std::vector<ColRef> refs;
+      for (size_t i = 0; i < rs.wire.size(); ++i) refs.push_back({-1, static_cast<int>(i)});
+      rs.stage_refs.push_back(refs);
+      std::vector<int> needed{lj.key_idx};
+      for (int p : m.payload_cols[j]) needed.push_back(lj.payload_idx[p]);
+      RegMap rm = analyse(rs, needed, -1, false);
+      scans.push_back({lj.scan, file_cols_of(rs, rm)});
+    }
+    scans.push_back({s.scan, file_cols_of(s, m)});
+  }
+  for (auto& [scan, fcols] : scans) {
+    const std::string key = scan_key(*scan, fcols);
+    if (st.scans.count(key)) continue;
+    ScanBatches sb = plan_batches(ctx_.footers, *scan, fcols, 0, ctx_.batch_bytes);
+    StagedScan& ss = st.scans[key];
+    ss.data = DevBuf(ctx_.pool, std::max<uint64_t>(sb.total_bytes, 8), ctx_.compute);
+    PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    std::vector<Segment> all;
+    const uint64_t slot_bytes = (std::max(sb.max_batch_bytes, ctx_.batch_bytes) + 4095) & ~4095ULL;
+    if (!sb.batches.empty()) {
+      const int threads = std::max(1, ctx_.io_threads);
+      Ingest ing(ctx_, scan->paths, sb.batches, threads, slot_bytes, threads * 2 + 2);
+      uint64_t off = 0;
+      for (size_t i = 0; i < sb.batches.size(); ++i) {
+        uint8_t* base = ss.data.as<uint8_t>() + off;
+        uint64_t nt = 0;
+        auto segs = make_segments(sb.batches[i], base, nt);
+        all.insert(all.end(), segs.begin(), segs.end());
+        ing.copy_to_device(i, base, nullptr, 0, ctx_.copy);
+        off += sb.batches[i].bytes;
+      }
+      PSG_CUDA(cudaStreamSynchronize(ctx_.copy));
+    }
+    const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
+    uint64_t tiles = 0;
+    for (auto& s : all) {
+      s.tile_begin = tiles;
+      tiles += (s.rows + T - 1) / T;
+    }
+    ss.nsegs = static_cast<int>(all.size());
+    ss.ntiles = tiles;
+    ss.rows = sb.total_rows;
+    ss.bytes = sb.total_bytes;
+    if (!all.empty()) {
+      ss.segs = DevBuf(ctx_.pool, all.size() * sizeof(Segment), ctx_.compute);
+      PSG_CUDA(cudaMemcpyAsync(ss.segs.p, all.data(), all.size() * sizeof(Segment), cudaMemcpyHostToDevice, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    }
+    st.bytes += sb.total_bytes;
+  }
+}
+
+}  // namespace
+
+ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode, Staged* staged,
+                        bool want_rows) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  if (mode < 0 || mode > 3) throw InvalidInput("unknown execution mode");
+  if (ctx.nranks > 1 && ctx.nccl == nullptr) throw InvalidInput("nranks > 1 needs psg_ctx_init_comm first");
+  if (staged) {
+    Execution ex(ctx, staged->plan_json, staged->data_root, mode, staged);
+    return ex.run(want_rows);
+  }
+  if (mode == PSG_MODE_OVERLAPPED) {
+    Execution ex(ctx, plan_json, data_root, mode, nullptr);
+    return ex.run(want_rows);
+  }
+  // Phase-sequential modes: storage phase materialises every needed chunk in HBM, then the
+  // network/compute phase runs over the staged images (run_phased, pipeline.cpp:506-556).
+  const auto t0 = Clock::now();
+  std::unique_ptr<Staged> st(stage_plan(ctx, plan_json, data_root));
+  const double storage = secs_since(t0);
+  Execution ex(ctx, plan_json, data_root, mode, st.get());
+  ResultRows r = ex.run(want_rows);
+  r.stats.storage_phase_s = storage;
+  r.stats.network_phase_s = r.stats.runtime_s;
+  r.stats.runtime_s = secs_since(t0);
+  r.stats.ingest_bytes = st->bytes;
+  return r;
+}
+
+Staged* stage_plan(Ctx& ctx, const std::string& plan_json, const std::string& data_root) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  auto st = std::make_unique<Staged>();
+  st->plan_json = plan_json;
+  st->data_root = data_root;
+  Execution ex(ctx, plan_json, data_root, PSG_MODE_BLOCKING, nullptr);
+  ex.stage(*st);
+  return st.release();
+}
+
+void free_staged(Staged* s) { delete s; }
+
+}  // namespace psg

@@ -1,0 +1,187 @@
+// Host side of the B200-native plan executor: per-GPU context, device memory pool, chunked
+// ingest pipeline and the execute_plan driver (replaces PlanExecution, pipeline.cpp:317-920).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <condition_variable>
+#include <deque>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "kernels.cuh"
+#include "plan.hpp"
+#include "psto.hpp"
+
+namespace psg {
+
+/// Stream-ordered device allocator with budget accounting (the RMM-pool analog of
+/// MemoryPool, memory_pool.hpp:30-108). Freed blocks stay cached in the CUDA mempool.
+class DevicePool {
+ public:
+  void init(int device, uint64_t budget);
+  void* alloc(size_t bytes, cudaStream_t s);
+  void free(void* p, cudaStream_t s);
+  uint64_t used() const { return used_; }
+  uint64_t peak() const { return peak_; }
+  void reset_peak() { peak_ = used_; }
+  void set_budget(uint64_t b) { budget_ = b; }
+
+ private:
+  std::map<void*, size_t> live_;
+  uint64_t used_ = 0, peak_ = 0, budget_ = 0;
+};
+
+/// RAII device buffer from the pool.
+struct DevBuf {
+  DevicePool* pool = nullptr;
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  DevBuf() = default;
+  DevBuf(DevicePool& pl, size_t n, cudaStream_t st) : pool(&pl), bytes(n), s(st) { p = pl.alloc(n ? n : 8, st); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    reset();
+    pool = o.pool, p = o.p, bytes = o.bytes, s = o.s;
+    o.p = nullptr;
+    return *this;
+  }
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p && pool) pool->free(p, s);
+    p = nullptr;
+  }
+  template <class T>
+  T* as() const { return static_cast<T*>(p); }
+};
+
+/// Metadata cache (MetadataCache, metadata_cache.hpp:26-60): footer per path.
+class FooterCache {
+ public:
+  std::shared_ptr<const TableMeta> get(const std::string& path);
+
+ private:
+  std::mutex mu_;
+  std::map<std::string, std::pair<std::pair<int64_t, uint64_t>, std::shared_ptr<const TableMeta>>> map_;
+};
+
+/// One contiguous file range copied into a batch buffer.
+struct Extent {
+  uint64_t file_off, len, buf_off;
+};
+
+/// An ingest batch: consecutive surviving row groups of one file, needed column chunks packed.
+struct BatchPlan {
+  int file = 0;
+  std::vector<size_t> groups;
+  std::vector<uint64_t> rows;               // rows per group
+  std::vector<std::vector<uint64_t>> pos;   // [group][needed col] offset in batch buffer
+  std::vector<Extent> extents;
+  uint64_t bytes = 0;
+  uint64_t total_rows = 0;
+};
+
+struct Ctx;
+
+/// Host I/O pool -> pinned staging slots -> H2D on the copy stream (the GPU analog of IoPool +
+/// DeviceModel::read + decode, scan.cpp:22-93/140-271). Batches are read in order by `threads`
+/// workers into a ring of pinned slots; the control thread issues cudaMemcpyAsync per batch and
+/// a host callback returns the slot once the copy retires.
+class Ingest {
+ public:
+  Ingest(Ctx& ctx, const std::vector<std::string>& files, const std::vector<BatchPlan>& batches, int threads,
+         uint64_t slot_bytes, int nslots);
+  ~Ingest();
+  /// Blocks until batch i is in pinned memory, writes `extra` bytes (segment descriptors) after
+  /// the payload, then enqueues the H2D copy of payload+extra to dst. Returns after enqueueing.
+  void copy_to_device(size_t i, void* dst, const void* extra, size_t extra_bytes, cudaStream_t copy_stream);
+  uint64_t bytes_read() const { return bytes_read_; }
+
+ private:
+  struct Slot {
+    void* host = nullptr;
+    int batch = -1;
+    bool ready = false;
+  };
+  void worker();
+  static void CUDART_CB on_copied(void* arg);
+
+  Ctx& ctx_;
+  std::vector<std::string> files_;
+  std::vector<int> fds_;
+  const std::vector<BatchPlan>& batches_;
+  uint64_t slot_bytes_;
+  std::vector<Slot> slots_;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  size_t next_job_ = 0;
+  std::vector<int> slot_of_batch_;
+  std::deque<int> free_slots_;
+  bool stop_ = false;
+  std::string error_;
+  uint64_t bytes_read_ = 0;
+  std::vector<std::thread> threads_;
+  struct CopyDone {
+    Ingest* self;
+    int slot;
+  };
+  std::vector<std::unique_ptr<CopyDone>> done_args_;
+};
+
+struct Ctx {
+  int device = 0, rank = 0, nranks = 1;
+  cudaStream_t compute = nullptr, copy = nullptr, comm = nullptr;
+  ncclComm_t nccl = nullptr;
+  DevicePool pool;
+  FooterCache footers;
+  int io_threads = 0;
+  uint64_t batch_bytes = 64ull << 20;
+  int pinned_slots = 0;
+  bool semijoin = true;
+  // Pinned staging ring (reused across queries).
+  std::vector<void*> pinned;
+  uint64_t pinned_slot_bytes = 0;
+  // Device event-time accounting of the dominant probe kernel.
+  cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  void ensure_pinned(int nslots, uint64_t slot_bytes);
+  ~Ctx();
+};
+
+struct ResultRows {
+  Schema schema;
+  std::vector<uint64_t> words;  // row-major
+  uint64_t nrows = 0;
+  psg_stats stats{};
+};
+
+struct Staged;  // HBM-resident file images (psg_stage_plan)
+
+ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode,
+                        Staged* staged, bool want_rows);
+Staged* stage_plan(Ctx& ctx, const std::string& plan_json, const std::string& data_root);
+void free_staged(Staged* s);
+
+// op adapters (ops.cpp)
+struct HostBatch {
+  Schema schema;
+  std::vector<std::vector<uint64_t>> cols;
+  uint64_t rows() const { return cols.empty() ? 0 : cols[0].size(); }
+};
+HostBatch op_filter(Ctx& ctx, const HostBatch& in, const Predicate& pred);
+HostBatch op_partition(Ctx& ctx, const HostBatch& in, const std::string& key, uint32_t nparts, int identity,
+                       std::vector<uint64_t>& part_rows);
+HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& build_key, const HostBatch& probe,
+                       const std::string& probe_key);
+
+void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, uint64_t seed, Codec codec,
+              uint64_t rg_bytes, int threads);
+
+}  // namespace psg

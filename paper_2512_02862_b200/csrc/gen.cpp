@@ -1,0 +1,235 @@
+// TPC-H-analog workload generator (the path's data source, not accelerated): byte-identical to
+// gen_workload(kind=tpch) (/root/reference/proj/src/bench.cpp:85-114, workload.cpp:89-153),
+// pinned by tests/golden/gen_hashes.json. Streams each table straight into its node shards
+// (slice_for_node, workload.cpp:73-87: rows r ≡ node mod nodes) so SF100/SF1000 never need the
+// whole table in RAM; one thread per table, with a writer thread per table so generation and
+// file writes overlap.
+#include <sys/stat.h>
+
+#include <condition_variable>
+#include <deque>
+#include <filesystem>
+#include <functional>
+#include <memory>
+#include <mutex>
+#include <thread>
+
+#include "psto.hpp"
+
+namespace psg {
+namespace {
+
+/// std::mt19937_64 (Matsumoto-Nishimura 64-bit parameters), batched twist.
+class Mt64 {
+ public:
+  explicit Mt64(uint64_t seed) {
+    mt_[0] = seed;
+    for (int i = 1; i < 312; ++i) mt_[i] = 6364136223846793005ULL * (mt_[i - 1] ^ (mt_[i - 1] >> 62)) + i;
+    idx_ = 312;
+  }
+  inline uint64_t operator()() {
+    if (idx_ >= 312) twist();
+    uint64_t y = mt_[idx_++];
+    y ^= (y >> 29) & 0x5555555555555555ULL;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
+    y ^= (y << 37) & 0xFFF7EEE000000000ULL;
+    y ^= y >> 43;
+    return y;
+  }
+
+ private:
+  void twist() {
+    constexpr uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL, A = 0xB5026F5AA96619E9ULL;
+    int i = 0;
+    for (; i < 312 - 156; ++i) {
+      uint64_t x = (mt_[i] & UM) | (mt_[i + 1] & LM);
+      mt_[i] = mt_[i + 156] ^ (x >> 1) ^ ((x & 1) ? A : 0);
+    }
+    for (; i < 311; ++i) {
+      uint64_t x = (mt_[i] & UM) | (mt_[i + 1] & LM);
+      mt_[i] = mt_[i - 156] ^ (x >> 1) ^ ((x & 1) ? A : 0);
+    }
+    uint64_t x = (mt_[311] & UM) | (mt_[0] & LM);
+    mt_[311] = mt_[155] ^ (x >> 1) ^ ((x & 1) ? A : 0);
+    idx_ = 0;
+  }
+  uint64_t mt_[312];
+  int idx_;
+};
+
+/// yyyymmdd; GCC evaluates the three rng() calls of workload.cpp:118-119 left to right.
+inline int64_t gen_date(Mt64& r) {
+  const uint64_t y = 1992 + r() % 7;
+  const uint64_t m = 1 + r() % 12;
+  const uint64_t d = 1 + r() % 28;
+  return static_cast<int64_t>(y * 10000 + m * 100 + d);
+}
+
+using RowFn = std::function<void(Mt64&, uint64_t row, uint64_t* out)>;
+
+/// Streams `rows` rows of a table into `nodes` shard files (row r -> node r % nodes).
+void stream_table(const Schema& schema, uint64_t rows, uint64_t seed, const RowFn& fn,
+                  const std::vector<std::string>& paths, uint64_t rg_bytes, Codec codec) {
+  const int nodes = static_cast<int>(paths.size());
+  const size_t ncols = schema.size();
+  const uint64_t rg_rows = PstoWriter::rows_for_group_bytes(schema, rg_bytes);
+  std::vector<std::unique_ptr<PstoWriter>> writers;
+  for (auto& p : paths) writers.push_back(std::make_unique<PstoWriter>(p, schema, rg_rows, codec));
+  // Block of rows = nodes * rg_rows so that each node receives whole row groups per block.
+  const uint64_t block = static_cast<uint64_t>(nodes) * rg_rows;
+  struct Buf {
+    std::vector<std::vector<std::vector<uint64_t>>> per_node;  // [node][col] words
+  };
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<std::unique_ptr<Buf>> full, empty;
+  bool done = false;
+  for (int i = 0; i < 3; ++i) {
+    auto b = std::make_unique<Buf>();
+    b->per_node.assign(nodes, std::vector<std::vector<uint64_t>>(ncols));
+    empty.push_back(std::move(b));
+  }
+  std::exception_ptr werr;
+  std::thread writer([&] {
+    try {
+      while (true) {
+        std::unique_ptr<Buf> b;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return !full.empty() || done; });
+          if (full.empty()) return;
+          b = std::move(full.front());
+          full.pop_front();
+        }
+        for (int n = 0; n < nodes; ++n) {
+          std::vector<const uint64_t*> ptrs(ncols);
+          for (size_t c = 0; c < ncols; ++c) ptrs[c] = b->per_node[n][c].data();
+          if (!b->per_node[n][0].empty()) writers[n]->append(ptrs.data(), b->per_node[n][0].size());
+        }
+        std::lock_guard<std::mutex> lk(mu);
+        empty.push_back(std::move(b));
+        cv.notify_all();
+      }
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(mu);
+      werr = std::current_exception();
+      cv.notify_all();
+    }
+  });
+  Mt64 rng(seed);
+  uint64_t row = 0;
+  uint64_t vals[8];
+  try {
+    while (row < rows) {
+      std::unique_ptr<Buf> b;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return !empty.empty() || werr; });
+        if (werr) break;
+        b = std::move(empty.front());
+        empty.pop_front();
+      }
+      const uint64_t n = std::min(block, rows - row);
+      for (int k = 0; k < nodes; ++k)
+        for (size_t c = 0; c < ncols; ++c) b->per_node[k][c].clear();
+      for (uint64_t i = 0; i < n; ++i, ++row) {
+        fn(rng, row, vals);
+        auto& dst = b->per_node[row % static_cast<uint64_t>(nodes)];
+        for (size_t c = 0; c < ncols; ++c) dst[c].push_back(vals[c]);
+      }
+      std::lock_guard<std::mutex> lk(mu);
+      full.push_back(std::move(b));
+      cv.notify_all();
+    }
+  } catch (...) {
+    std::lock_guard<std::mutex> lk(mu);
+    done = true;
+    cv.notify_all();
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    done = true;
+    cv.notify_all();
+  }
+  writer.join();
+  if (werr) std::rethrow_exception(werr);
+  for (auto& w : writers) w->finish();
+}
+
+Schema int_schema(std::initializer_list<const char*> names) {
+  Schema s;
+  for (auto* n : names) s.fields.push_back(Field{n, LType::Int64});
+  return s;
+}
+
+}  // namespace
+
+void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, uint64_t seed,
+              Codec codec, uint64_t rg_bytes, int threads) {
+  if (nodes < 1 || devices < 1) throw InvalidInput("devices and nodes must be >= 1");
+  namespace fs = std::filesystem;
+  fs::create_directories(out_dir);
+  auto dev_dir = [&](int i) {
+    std::string d = out_dir + "/dev" + std::to_string(i % devices);
+    fs::create_directories(d);
+    return d;
+  };
+  const uint64_t customers = static_cast<uint64_t>(150'000 * scale);
+  const uint64_t orders = static_cast<uint64_t>(1'500'000 * scale);
+  const uint64_t lineitems = static_cast<uint64_t>(6'000'000 * scale);
+  const uint64_t mult = 0x9E3779B97F4A7C15ULL;
+
+  std::vector<std::function<void()>> jobs;
+  jobs.push_back([&] {
+    stream_table(int_schema({"c_custkey", "c_mktsegment"}), customers, seed * mult + 11,
+                 [](Mt64& r, uint64_t i, uint64_t* v) {
+                   v[0] = i;
+                   v[1] = r() % 5;
+                 },
+                 {dev_dir(0) + "/customer.psto"}, rg_bytes, codec);
+  });
+  jobs.push_back([&] {
+    std::vector<std::string> paths;
+    for (int n = 0; n < nodes; ++n) paths.push_back(dev_dir(0 + n) + "/orders.node" + std::to_string(n) + ".psto");
+    stream_table(int_schema({"o_orderkey", "o_custkey", "o_orderdate", "o_shippriority"}), orders, seed * mult + 12,
+                 [customers](Mt64& r, uint64_t i, uint64_t* v) {
+                   v[0] = i;
+                   v[1] = customers > 0 ? r() % customers : 0;
+                   v[2] = static_cast<uint64_t>(gen_date(r));
+                   v[3] = r() % 5;
+                 },
+                 paths, rg_bytes, codec);
+  });
+  jobs.push_back([&] {
+    std::vector<std::string> paths;
+    for (int n = 0; n < nodes; ++n) paths.push_back(dev_dir(1 + n) + "/lineitem.node" + std::to_string(n) + ".psto");
+    stream_table(int_schema({"l_orderkey", "l_extendedprice", "l_discount", "l_shipdate"}), lineitems,
+                 seed * mult + 13,
+                 [orders](Mt64& r, uint64_t, uint64_t* v) {
+                   v[0] = orders > 0 ? r() % orders : 0;
+                   v[1] = 90'000 + r() % 100'000;
+                   v[2] = r() % 11;
+                   v[3] = static_cast<uint64_t>(gen_date(r));
+                 },
+                 paths, rg_bytes, codec);
+  });
+  if (threads <= 1) {
+    for (auto& j : jobs) j();
+    return;
+  }
+  std::vector<std::thread> ts;
+  std::vector<std::exception_ptr> errs(jobs.size());
+  for (size_t i = 0; i < jobs.size(); ++i)
+    ts.emplace_back([&, i] {
+      try {
+        jobs[i]();
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    });
+  for (auto& t : ts) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+}  // namespace psg

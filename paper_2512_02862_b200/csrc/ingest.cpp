@@ -1,0 +1,183 @@
+// Device memory pool, footer cache and the chunked storage->HBM ingest pipeline.
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <cstring>
+
+#include "engine.hpp"
+
+namespace psg {
+
+// ----------------------------------------------------------------------------- DevicePool
+void DevicePool::init(int device, uint64_t budget) {
+  budget_ = budget;
+  cudaMemPool_t mp;
+  PSG_CUDA(cudaDeviceGetDefaultMemPool(&mp, device));
+  uint64_t thr = ~0ULL;  // keep freed blocks cached (RMM-pool behaviour)
+  PSG_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
+}
+
+void* DevicePool::alloc(size_t bytes, cudaStream_t s) {
+  if (budget_ && used_ + bytes > budget_) throw MemoryExceeded(bytes, used_, budget_);
+  void* p = nullptr;
+  cudaError_t e = cudaMallocAsync(&p, bytes, s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(PSG_ERR_MEMORY_EXCEEDED, "device allocation of " + std::to_string(bytes) +
+                                             " bytes failed: " + cudaGetErrorString(e));
+  }
+  live_[p] = bytes;
+  used_ += bytes;
+  if (used_ > peak_) peak_ = used_;
+  return p;
+}
+
+void DevicePool::free(void* p, cudaStream_t s) {
+  auto it = live_.find(p);
+  if (it == live_.end()) return;
+  used_ -= it->second;
+  live_.erase(it);
+  cudaFreeAsync(p, s);
+}
+
+// ----------------------------------------------------------------------------- FooterCache
+std::shared_ptr<const TableMeta> FooterCache::get(const std::string& path) {
+  struct stat st;
+  if (::stat(path.c_str(), &st) != 0) throw IoFailure("cannot stat: " + path);
+  const std::pair<int64_t, uint64_t> stamp{static_cast<int64_t>(st.st_mtim.tv_sec) * 1000000000LL + st.st_mtim.tv_nsec,
+                                           static_cast<uint64_t>(st.st_size)};
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = map_.find(path);
+    if (it != map_.end() && it->second.first == stamp) return it->second.second;
+  }
+  auto meta = std::make_shared<const TableMeta>(read_footer(path));
+  std::lock_guard<std::mutex> lk(mu_);
+  map_[path] = {stamp, meta};
+  return meta;
+}
+
+// ----------------------------------------------------------------------------- Ctx
+void Ctx::ensure_pinned(int nslots, uint64_t slot_bytes) {
+  if (static_cast<int>(pinned.size()) >= nslots && pinned_slot_bytes >= slot_bytes) return;
+  for (void* p : pinned) cudaFreeHost(p);
+  pinned.clear();
+  for (int i = 0; i < nslots; ++i) {
+    void* p = nullptr;
+    PSG_CUDA(cudaHostAlloc(&p, slot_bytes, cudaHostAllocDefault));
+    pinned.push_back(p);
+  }
+  pinned_slot_bytes = slot_bytes;
+}
+
+Ctx::~Ctx() {
+  cudaSetDevice(device);
+  for (void* p : pinned) cudaFreeHost(p);
+  if (nccl) ncclCommDestroy(nccl);
+  if (ev_a) cudaEventDestroy(ev_a);
+  if (ev_b) cudaEventDestroy(ev_b);
+  if (compute) cudaStreamDestroy(compute);
+  if (copy) cudaStreamDestroy(copy);
+  if (comm) cudaStreamDestroy(comm);
+}
+
+// ----------------------------------------------------------------------------- Ingest
+Ingest::Ingest(Ctx& ctx, const std::vector<std::string>& files, const std::vector<BatchPlan>& batches, int threads,
+               uint64_t slot_bytes, int nslots)
+    : ctx_(ctx), files_(files), batches_(batches), slot_bytes_(slot_bytes) {
+  for (auto& f : files_) {
+    const int fd = ::open(f.c_str(), O_RDONLY);
+    if (fd < 0) {
+      for (int x : fds_) ::close(x);
+      throw IoFailure("cannot open: " + f);
+    }
+    ::posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
+    fds_.push_back(fd);
+  }
+  ctx.ensure_pinned(nslots, slot_bytes);
+  slots_.resize(nslots);
+  for (int i = 0; i < nslots; ++i) {
+    slots_[i].host = ctx.pinned[i];
+    free_slots_.push_back(i);
+  }
+  slot_of_batch_.assign(batches.size(), -1);
+  for (int t = 0; t < threads; ++t) threads_.emplace_back([this] { worker(); });
+}
+
+Ingest::~Ingest() {
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    stop_ = true;
+    cv_.notify_all();
+  }
+  for (auto& t : threads_) t.join();
+  // Outstanding copies reference pinned slots; the caller synchronised the copy stream.
+  for (int fd : fds_) ::close(fd);
+}
+
+void Ingest::worker() {
+  while (true) {
+    size_t job;
+    int slot;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      // Claim the next batch only when a slot is free, keeping reads in batch order.
+      cv_.wait(lk, [&] { return stop_ || (next_job_ < batches_.size() && !free_slots_.empty()); });
+      if (stop_ || next_job_ >= batches_.size()) return;
+      job = next_job_++;
+      slot = free_slots_.front();
+      free_slots_.pop_front();
+      slots_[slot].batch = static_cast<int>(job);
+      slots_[slot].ready = false;
+    }
+    const BatchPlan& b = batches_[job];
+    auto* dst = static_cast<uint8_t*>(slots_[slot].host);
+    std::string err;
+    for (const Extent& e : b.extents) {
+      uint64_t got = 0;
+      while (got < e.len) {
+        const ssize_t k = ::pread(fds_[b.file], dst + e.buf_off + got, e.len - got, static_cast<off_t>(e.file_off + got));
+        if (k <= 0) {
+          err = "short read of " + files_[b.file];
+          break;
+        }
+        got += static_cast<uint64_t>(k);
+      }
+      if (!err.empty()) break;
+    }
+    std::lock_guard<std::mutex> lk(mu_);
+    if (!err.empty() && error_.empty()) error_ = err;
+    bytes_read_ += b.bytes;
+    slot_of_batch_[job] = slot;
+    slots_[slot].ready = true;
+    cv_.notify_all();
+  }
+}
+
+void CUDART_CB Ingest::on_copied(void* arg) {
+  auto* d = static_cast<CopyDone*>(arg);
+  std::lock_guard<std::mutex> lk(d->self->mu_);
+  d->self->slots_[d->slot].batch = -1;
+  d->self->free_slots_.push_back(d->slot);
+  d->self->cv_.notify_all();
+}
+
+void Ingest::copy_to_device(size_t i, void* dst, const void* extra, size_t extra_bytes, cudaStream_t copy_stream) {
+  int slot;
+  {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] { return !error_.empty() || (slot_of_batch_[i] >= 0 && slots_[slot_of_batch_[i]].ready); });
+    if (!error_.empty()) throw IoFailure(error_);
+    slot = slot_of_batch_[i];
+  }
+  const BatchPlan& b = batches_[i];
+  if (b.bytes + extra_bytes > slot_bytes_) throw InvalidInput("batch exceeds pinned slot size");
+  auto* host = static_cast<uint8_t*>(slots_[slot].host);
+  if (extra_bytes) std::memcpy(host + b.bytes, extra, extra_bytes);
+  PSG_CUDA(cudaMemcpyAsync(dst, host, b.bytes + extra_bytes, cudaMemcpyHostToDevice, copy_stream));
+  done_args_.push_back(std::make_unique<CopyDone>(CopyDone{this, slot}));
+  PSG_CUDA(cudaLaunchHostFunc(copy_stream, &Ingest::on_copied, done_args_.back().get()));
+}
+
+}  // namespace psg

@@ -1,0 +1,772 @@
+// sm_100a kernels of the B200-native PystachIO hot path. See kernels.cuh for the contract.
+//
+// Design notes (B200): every kernel here is HBM- or L2-latency-bound integer work, so the rules
+// that matter are coalescing, memory-level parallelism and grid sizing, not tensor cores:
+//  * k_scan processes tiles of R x 256 rows; each thread issues R independent, fully coalesced
+//    8-byte loads per predicate column (consecutive threads = consecutive rows of a column chunk),
+//    so a 148-SM grid keeps ~10 MB of loads in flight. Non-predicate columns are loaded lazily,
+//    only for rows that survived the predicate / join (late materialisation: sectors whose rows
+//    all failed are never fetched).
+//  * Stream compaction uses warp ballots + a per-tile (r, warp) prefix in shared memory and one
+//    global atomic per tile — order is preserved inside each tile; SINK_COUNT + tile_offsets gives
+//    a fully order-preserving variant (the filter op's contract).
+//  * Hash tables are open addressing with linear probing over 32-byte slots (one DRAM sector per
+//    probe), keys claimed with 64-bit atomicCAS, aggregates accumulated in the slot with 64-bit
+//    atomicAdd (wrap-around int64 == the reference's uint64 accumulation). A blocked Bloom filter
+//    sized to stay L2-resident screens probes when the table itself is larger than L2.
+//  * Grids are persistent: 148 SMs x resident CTAs, grid-stride over tiles.
+#include <cub/cub.cuh>
+
+#include <atomic>
+#include <cstdio>
+
+#include "kernels.cuh"
+
+namespace psg {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+int g_sms = 0;
+int sm_count() {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+inline cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+inline unsigned grid_for(uint64_t n, int per_block) {
+  uint64_t b = (n + per_block - 1) / per_block;
+  const uint64_t cap = static_cast<uint64_t>(sm_count()) * 16;
+  if (b > cap) b = cap;
+  return static_cast<unsigned>(b < 1 ? 1 : b);
+}
+}  // namespace
+
+uint64_t kernel_launch_count() { return g_launches.load(); }
+
+// ------------------------------------------------------------------------------------ hashing
+__device__ __forceinline__ uint64_t mix64(uint64_t k) {
+  k ^= k >> 33;
+  k *= 0xff51afd7ed558ccdULL;
+  k ^= k >> 33;
+  k *= 0xc4ceb9fe1a85ec53ULL;
+  k ^= k >> 33;
+  return k;
+}
+/// partition_of (hashing.hpp:26-37): ((k * 0x9E3779B97F4A7C15) >> 13) % n
+__device__ __forceinline__ uint32_t part_of(uint64_t k, uint32_t n) {
+  return static_cast<uint32_t>(((k * 0x9E3779B97F4A7C15ULL) >> 13) % n);
+}
+
+__device__ __forceinline__ bool cmp_i(int64_t a, int op, int64_t b) {
+  switch (op) {
+    case 0: return a < b;
+    case 1: return a <= b;
+    case 2: return a == b;
+    case 3: return a != b;
+    case 4: return a >= b;
+    default: return a > b;
+  }
+}
+__device__ __forceinline__ bool cmp_f(double a, int op, double b) {
+  switch (op) {
+    case 0: return a < b;
+    case 1: return a <= b;
+    case 2: return a == b;
+    case 3: return a != b;
+    case 4: return a >= b;
+    default: return a > b;
+  }
+}
+
+// ------------------------------------------------------------------------------ agg table ops
+__device__ __forceinline__ uint64_t agg_insert(const AggTableDev& t, uint64_t key) {
+  if (key == kEmptyKey) return t.mask + 1;
+  uint64_t s = mix64(key) & t.mask;
+  while (true) {
+    unsigned long long* kp = reinterpret_cast<unsigned long long*>(t.hot + s * t.hw);
+    const unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
+    if (prev == kEmptyKey || prev == key) return s;
+    s = (s + 1) & t.mask;
+  }
+}
+
+__device__ __forceinline__ bool bloom_maybe(const AggTableDev& t, uint64_t key) {
+  if (t.bloom == nullptr) return true;
+  const uint64_t h = mix64(key ^ 0x5bd1e9955bd1e995ULL);
+  const uint32_t w = __ldg(t.bloom + (h & t.bloom_mask));
+  const uint32_t m = (1u << ((h >> 40) & 31)) | (1u << ((h >> 46) & 31)) | (1u << ((h >> 52) & 31));
+  return (w & m) == m;
+}
+
+/// Returns the slot of key or UINT64_MAX when absent.
+__device__ __forceinline__ uint64_t agg_lookup_from(const AggTableDev& t, uint64_t key, uint64_t s, uint64_t k0) {
+  while (true) {
+    if (k0 == key) return s;
+    if (k0 == kEmptyKey) return ~0ULL;
+    s = (s + 1) & t.mask;
+    k0 = t.hot[s * t.hw];
+  }
+}
+__device__ __forceinline__ uint64_t agg_lookup(const AggTableDev& t, uint64_t key) {
+  if (key == kEmptyKey) return t.cold[(t.mask + 1) * t.cw] > 0 ? t.mask + 1 : ~0ULL;
+  const uint64_t s = mix64(key) & t.mask;
+  return agg_lookup_from(t, key, s, t.hot[s * t.hw]);
+}
+
+// ---------------------------------------------------------------------------- local table ops
+__device__ __forceinline__ uint64_t local_lookup(const LocalTableDev& t, uint64_t key) {
+  if (key == kEmptyKey) return t.cnt[t.mask + 1] > 0 ? t.mask + 1 : ~0ULL;
+  uint64_t s = mix64(key) & t.mask;
+  while (true) {
+    const uint64_t k = t.keys[s];
+    if (k == key) return s;
+    if (k == kEmptyKey) return ~0ULL;
+    s = (s + 1) & t.mask;
+  }
+}
+
+// ------------------------------------------------------------------------------- fused k_scan
+template <int R, int SINK>
+__global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanProgram P, const Segment* __restrict__ segs,
+                                                 int nsegs, uint64_t ntiles) {
+  extern __shared__ uint64_t smem[];  // [n_regs][R][kBlock]
+  __shared__ const uint64_t* s_col[kMaxIn];
+  __shared__ uint64_t s_row0, s_rows;
+  __shared__ uint32_t s_wcnt[R][kBlock / 32];
+  __shared__ uint32_t s_woff[R][kBlock / 32];
+  __shared__ unsigned long long s_base;
+  __shared__ unsigned long long s_part[kMaxParts];
+  __shared__ unsigned long long s_gacc[2 * kMaxSums + 1];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int TILE = R * kBlock;
+#define V(reg, r) smem[((reg) * R + (r)) * kBlock + tid]
+
+  if (SINK == SINK_MATERIALIZE && P.nparts > 1)
+    for (int i = tid; i < P.nparts; i += kBlock) s_part[i] = 0;
+  if (SINK == SINK_PROBE_GLOBAL)
+    for (int i = tid; i < 2 * kMaxSums + 1; i += kBlock) s_gacc[i] = 0;
+  __syncthreads();
+
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    if (tid == 0) {
+      int lo = 0, hi = nsegs - 1;  // last segment with tile_begin <= tile
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
+      }
+      const Segment* sg = &segs[lo];
+      const uint64_t row0 = (tile - sg->tile_begin) * TILE;
+      s_row0 = row0;
+      s_rows = min(static_cast<uint64_t>(TILE), sg->rows - row0);
+      for (int c = 0; c < P.n_in; ++c) s_col[c] = sg->col[c];
+    }
+    __syncthreads();
+    const uint64_t row0 = s_row0;
+    const int nrows = static_cast<int>(s_rows);
+
+    // Phase A: predicate columns for every row (R independent coalesced loads per column).
+    uint32_t pass = 0;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (r * kBlock + tid < nrows) pass |= 1u << r;
+    for (int c = 0; c < P.n_pred; ++c) {
+      const uint64_t* col = s_col[c] + row0;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (pass & (1u << r)) V(c, r) = __ldcs(reinterpret_cast<const unsigned long long*>(col + r * kBlock + tid));
+    }
+    for (int a = 0; a < P.n_atoms; ++a) {
+      const AtomDesc at = P.atoms[a];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!(pass & (1u << r))) continue;
+        const uint64_t v = V(at.reg, r);
+        const bool ok = at.is_float ? cmp_f(__longlong_as_double(static_cast<long long>(v)), at.op,
+                                            __longlong_as_double(static_cast<long long>(at.lit)))
+                                    : cmp_i(static_cast<int64_t>(v), at.op, static_cast<int64_t>(at.lit));
+        if (!ok) pass &= ~(1u << r);
+      }
+    }
+    // Phase B: columns needed before joins / the sink key (late materialisation).
+    for (int c = P.n_pred; c < P.n_early; ++c) {
+      const uint64_t* col = s_col[c] + row0;
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (pass & (1u << r)) V(c, r) = __ldcs(reinterpret_cast<const unsigned long long*>(col + r * kBlock + tid));
+    }
+    // Phase C: unique-key local join chain (apply_chain, pipeline.cpp:431-448).
+    for (int j = 0; j < P.n_joins; ++j) {
+      const JoinDesc& jd = P.joins[j];
+      uint64_t slot[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        slot[r] = ~0ULL;
+        if (pass & (1u << r)) slot[r] = local_lookup(jd.t, V(jd.key_reg, r));
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!(pass & (1u << r))) continue;
+        if (slot[r] == ~0ULL) {
+          pass &= ~(1u << r);
+          continue;
+        }
+        const uint32_t st = jd.t.start[slot[r]];
+        for (int p = 0; p < jd.t.npayload; ++p) V(jd.payload_reg[p], r) = jd.t.payload[p][st];
+      }
+    }
+
+    if (SINK == SINK_PROBE || SINK == SINK_PROBE_GLOBAL) {
+      const AggTableDev& t = P.agg;
+      uint64_t slot[R];
+      uint64_t home[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        slot[r] = ~0ULL;
+        home[r] = 0;
+        if (!(pass & (1u << r))) continue;
+        const uint64_t key = V(P.key_reg, r);
+        if (key == kEmptyKey) {
+          slot[r] = (t.cold[(t.mask + 1) * t.cw] > 0) ? t.mask + 1 : ~0ULL;
+          if (slot[r] == ~0ULL) pass &= ~(1u << r);
+          continue;
+        }
+        if (!bloom_maybe(t, key)) {
+          pass &= ~(1u << r);
+          continue;
+        }
+        home[r] = mix64(key) & t.mask;
+      }
+      uint64_t k0[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if ((pass & (1u << r)) && slot[r] == ~0ULL) k0[r] = t.hot[home[r] * t.hw];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        if (!(pass & (1u << r)) || slot[r] != ~0ULL) continue;
+        slot[r] = agg_lookup_from(t, V(P.key_reg, r), home[r], k0[r]);
+        if (slot[r] == ~0ULL) pass &= ~(1u << r);
+      }
+      // Late columns (sum inputs) only for matched rows.
+      for (int c = P.n_early; c < P.n_in; ++c) {
+        const uint64_t* col = s_col[c] + row0;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (pass & (1u << r)) V(c, r) = __ldcs(reinterpret_cast<const unsigned long long*>(col + r * kBlock + tid));
+      }
+      if (SINK == SINK_PROBE) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!(pass & (1u << r))) continue;
+          unsigned long long* h = reinterpret_cast<unsigned long long*>(t.hot + slot[r] * t.hw);
+          atomicAdd(h + 1, 1ULL);
+          for (int p = 0; p < P.n_sum; ++p) {
+            const uint64_t v = V(P.sum_reg[p], r);
+            if (t.ps_float[p])
+              atomicAdd(reinterpret_cast<double*>(h + 2 + p), __longlong_as_double(static_cast<long long>(v)));
+            else
+              atomicAdd(h + 2 + p, static_cast<unsigned long long>(v));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!(pass & (1u << r))) continue;
+          const uint64_t* cold = t.cold + slot[r] * t.cw;
+          const uint64_t m = cold[0];
+          atomicAdd(&s_gacc[0], static_cast<unsigned long long>(m));
+          for (int p = 0; p < P.n_sum; ++p) {
+            const uint64_t v = V(P.sum_reg[p], r);
+            if (t.ps_float[p])
+              atomicAdd(reinterpret_cast<double*>(&s_gacc[1 + p]),
+                        static_cast<double>(m) * __longlong_as_double(static_cast<long long>(v)));
+            else
+              atomicAdd(&s_gacc[1 + p], static_cast<unsigned long long>(m * v));
+          }
+          for (int b = 0; b < t.nbs; ++b) {
+            if (t.bs_float[b])
+              atomicAdd(reinterpret_cast<double*>(&s_gacc[1 + P.n_sum + b]),
+                        __longlong_as_double(static_cast<long long>(cold[1 + b])));
+            else
+              atomicAdd(&s_gacc[1 + P.n_sum + b], static_cast<unsigned long long>(cold[1 + b]));
+          }
+        }
+      }
+    } else {
+      // Remaining late columns for the other sinks.
+      for (int c = P.n_early; c < P.n_in; ++c) {
+        const uint64_t* col = s_col[c] + row0;
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          if (pass & (1u << r)) V(c, r) = __ldcs(reinterpret_cast<const unsigned long long*>(col + r * kBlock + tid));
+      }
+      if (SINK == SINK_BUILD) {
+        const AggTableDev& t = P.agg;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!(pass & (1u << r))) continue;
+          const uint64_t s = agg_insert(t, V(P.key_reg, r));
+          unsigned long long* cold = reinterpret_cast<unsigned long long*>(t.cold + s * t.cw);
+          atomicAdd(cold, 1ULL);
+          for (int b = 0; b < P.n_sum; ++b) {
+            const uint64_t v = V(P.sum_reg[b], r);
+            if (t.bs_float[b])
+              atomicAdd(reinterpret_cast<double*>(cold + 1 + b), __longlong_as_double(static_cast<long long>(v)));
+            else
+              atomicAdd(cold + 1 + b, static_cast<unsigned long long>(v));
+          }
+        }
+      } else {  // SINK_MATERIALIZE / SINK_COUNT
+        uint32_t ballots[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          ballots[r] = __ballot_sync(0xffffffffu, (pass >> r) & 1u);
+          if (lane == 0) s_wcnt[r][warp] = __popc(ballots[r]);
+        }
+        __syncthreads();
+        if (tid == 0) {
+          uint32_t acc = 0;
+          for (int r = 0; r < R; ++r)
+            for (int w = 0; w < kBlock / 32; ++w) {
+              s_woff[r][w] = acc;
+              acc += s_wcnt[r][w];
+            }
+          if (SINK == SINK_COUNT) {
+            P.tile_counts[tile] = acc;
+          } else if (P.tile_offsets != nullptr) {
+            s_base = P.tile_offsets[tile];
+          } else {
+            s_base = acc ? atomicAdd(P.out_count, static_cast<unsigned long long>(acc)) : 0ULL;
+          }
+        }
+        __syncthreads();
+        if (SINK == SINK_MATERIALIZE) {
+          const uint64_t base = s_base;
+          const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            if (!((pass >> r) & 1u)) continue;
+            const uint64_t pos = base + s_woff[r][warp] + __popc(ballots[r] & lt);
+            if (pos >= P.out_cap) continue;  // host detects overflow via out_count
+            for (int o = 0; o < P.n_out; ++o) P.out_col[o][pos] = V(P.out_reg[o], r);
+            if (P.nparts > 1)
+              atomicAdd(&s_part[part_of(V(P.part_key_reg, r), static_cast<uint32_t>(P.nparts))], 1ULL);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+#undef V
+  if (SINK == SINK_MATERIALIZE && P.nparts > 1) {
+    __syncthreads();
+    for (int i = tid; i < P.nparts; i += kBlock)
+      if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);
+  }
+  if (SINK == SINK_PROBE_GLOBAL) {
+    __syncthreads();
+    const int n = 1 + P.n_sum + P.agg.nbs;
+    for (int i = tid; i < n; i += kBlock) {
+      if (P.global_float[i])
+        atomicAdd(reinterpret_cast<double*>(&P.global_acc[i]), __longlong_as_double(static_cast<long long>(s_gacc[i])));
+      else
+        atomicAdd(&P.global_acc[i], s_gacc[i]);
+    }
+  }
+}
+
+int scan_tile_rows() { return 4 * kBlock; }
+
+template <int R, int SINK>
+static void launch_scan_t(const ScanProgram& P, const Segment* d_segs, int nsegs, uint64_t ntiles, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(P.n_regs < 1 ? 1 : P.n_regs) * R * kBlock * sizeof(uint64_t);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_scan<R, SINK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    configured = true;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan<R, SINK>, kBlock, smem);
+  if (per_sm < 1) per_sm = 1;
+  uint64_t grid = static_cast<uint64_t>(sm_count()) * per_sm;
+  if (grid > ntiles) grid = ntiles;
+  if (grid < 1) grid = 1;
+  count_launch();
+  k_scan<R, SINK><<<static_cast<unsigned>(grid), kBlock, smem, st>>>(P, d_segs, nsegs, ntiles);
+}
+
+void launch_scan(const ScanProgram& P, const Segment* d_segs, int nsegs, uint64_t ntiles, int, void* stream) {
+  if (ntiles == 0 || nsegs == 0) return;
+  cudaStream_t st = S(stream);
+  // Tiles are always 4 x 256 rows; programs with many registers use R=2 sub-tiles twice as
+  // many CTAs would need, so they run R=4 with fewer resident CTAs (smem = n_regs * 8 KiB).
+  switch (P.sink) {
+    case SINK_MATERIALIZE: launch_scan_t<4, SINK_MATERIALIZE>(P, d_segs, nsegs, ntiles, st); break;
+    case SINK_BUILD: launch_scan_t<4, SINK_BUILD>(P, d_segs, nsegs, ntiles, st); break;
+    case SINK_PROBE: launch_scan_t<4, SINK_PROBE>(P, d_segs, nsegs, ntiles, st); break;
+    case SINK_PROBE_GLOBAL: launch_scan_t<4, SINK_PROBE_GLOBAL>(P, d_segs, nsegs, ntiles, st); break;
+    case SINK_COUNT: launch_scan_t<4, SINK_COUNT>(P, d_segs, nsegs, ntiles, st); break;
+  }
+}
+
+// ---------------------------------------------------------------------------- agg table setup
+__global__ void k_agg_init(AggTableDev t, uint64_t nslots) {
+  for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < nslots;
+       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t* h = t.hot + s * t.hw;
+    h[0] = kEmptyKey;
+    for (int i = 1; i < t.hw; ++i) h[i] = 0;
+    uint64_t* c = t.cold + s * t.cw;
+    for (int i = 0; i < t.cw; ++i) c[i] = 0;
+  }
+}
+void launch_agg_init(const AggTableDev& t, uint64_t cap, void* stream) {
+  count_launch();
+  k_agg_init<<<grid_for(cap + 1, 256), 256, 0, S(stream)>>>(t, cap + 1);
+  if (t.bloom) {
+    cudaMemsetAsync(t.bloom, 0, (t.bloom_mask + 1) * sizeof(uint32_t), S(stream));
+  }
+}
+
+__global__ void k_bloom_build(AggTableDev t, uint64_t cap) {
+  for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < cap;
+       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = t.hot[s * t.hw];
+    if (key == kEmptyKey) continue;
+    const uint64_t h = mix64(key ^ 0x5bd1e9955bd1e995ULL);
+    const uint32_t m = (1u << ((h >> 40) & 31)) | (1u << ((h >> 46) & 31)) | (1u << ((h >> 52) & 31));
+    atomicOr(t.bloom + (h & t.bloom_mask), m);
+  }
+}
+void launch_bloom_build(const AggTableDev& t, uint64_t cap, void* stream) {
+  if (!t.bloom) return;
+  count_launch();
+  k_bloom_build<<<grid_for(cap, 256), 256, 0, S(stream)>>>(t, cap);
+}
+
+// ------------------------------------------------------------------------------- local tables
+__global__ void k_local_init(uint64_t* keys, uint32_t* cnt, uint64_t cap) {
+  for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s <= cap;
+       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (s < cap) keys[s] = kEmptyKey;
+    cnt[s] = 0;
+  }
+}
+void launch_local_init(uint64_t* keys, uint32_t* cnt, uint64_t cap, void* stream) {
+  count_launch();
+  k_local_init<<<grid_for(cap + 1, 256), 256, 0, S(stream)>>>(keys, cnt, cap);
+}
+
+__global__ void k_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, const uint64_t* bk, uint64_t n,
+                              unsigned int* max_cnt) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = bk[i];
+    uint64_t s;
+    if (key == kEmptyKey) {
+      s = mask + 1;
+    } else {
+      s = mix64(key) & mask;
+      while (true) {
+        const unsigned long long prev =
+            atomicCAS(reinterpret_cast<unsigned long long*>(keys + s), kEmptyKey, key);
+        if (prev == kEmptyKey || prev == key) break;
+        s = (s + 1) & mask;
+      }
+    }
+    const uint32_t old = atomicAdd(cnt + s, 1u);
+    atomicMax(max_cnt, old + 1);
+  }
+}
+void launch_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, const uint64_t* bk, uint64_t n,
+                        unsigned int* max_cnt, void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_local_count<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, cnt, mask, bk, n, max_cnt);
+}
+
+struct ColPtrs {
+  const uint64_t* p[kMaxIn + kMaxPayload];
+};
+struct OutPtrs {
+  uint64_t* p[kMaxIn + kMaxPayload];
+};
+
+__global__ void k_local_fill(const uint64_t* keys, const uint32_t* start, uint32_t* cursor, uint64_t mask,
+                             const uint64_t* bk, ColPtrs src, OutPtrs dst, int ncols, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = bk[i];
+    uint64_t s;
+    if (key == kEmptyKey) {
+      s = mask + 1;
+    } else {
+      s = mix64(key) & mask;
+      while (keys[s] != key) s = (s + 1) & mask;
+    }
+    const uint64_t pos = start[s] + atomicAdd(cursor + s, 1u);
+    for (int c = 0; c < ncols; ++c) dst.p[c][pos] = src.p[c][i];
+  }
+}
+void launch_local_fill(const uint64_t* keys, const uint32_t* start, uint32_t* cursor, uint64_t mask,
+                       const uint64_t* bk, const uint64_t* const* src_cols, uint64_t* const* dst_cols, int ncols,
+                       uint64_t n, void* stream) {
+  if (n == 0) return;
+  ColPtrs s{};
+  OutPtrs d{};
+  for (int c = 0; c < ncols; ++c) {
+    s.p[c] = src_cols[c];
+    d.p[c] = dst_cols[c];
+  }
+  count_launch();
+  k_local_fill<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, start, cursor, mask, bk, s, d, ncols, n);
+}
+
+size_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, void* tmp, size_t tmp_bytes, void* stream) {
+  size_t bytes = tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, static_cast<int64_t>(n), S(stream));
+  if (tmp) count_launch();
+  return bytes;
+}
+size_t exclusive_scan_u64(const unsigned long long* in, unsigned long long* out, uint64_t n, void* tmp,
+                          size_t tmp_bytes, void* stream) {
+  size_t bytes = tmp_bytes;
+  cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, static_cast<int64_t>(n), S(stream));
+  if (tmp) count_launch();
+  return bytes;
+}
+
+// --------------------------------------------------------------------- generic expanding join
+__global__ void k_expand_count(LocalTableDev t, const uint64_t* pk, uint64_t n, uint32_t* counts) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t s = local_lookup(t, pk[i]);
+    counts[i] = s == ~0ULL ? 0u : t.cnt[s];
+  }
+}
+void launch_expand_count(LocalTableDev t, const uint64_t* pk, uint64_t n, uint32_t* counts, void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_expand_count<<<grid_for(n, 256), 256, 0, S(stream)>>>(t, pk, n, counts);
+}
+
+__global__ void k_expand_write(LocalTableDev t, const uint64_t* pk, uint64_t n, const uint32_t* off, ColPtrs probe,
+                               int nprobe, OutPtrs out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t s = local_lookup(t, pk[i]);
+    if (s == ~0ULL) continue;
+    const uint32_t c = t.cnt[s], st = t.start[s];
+    const uint64_t o = off[i];
+    for (uint32_t k = 0; k < c; ++k) {
+      for (int p = 0; p < t.npayload; ++p) out.p[p][o + k] = t.payload[p][st + k];
+      for (int q = 0; q < nprobe; ++q) out.p[t.npayload + q][o + k] = probe.p[q][i];
+    }
+  }
+}
+void launch_expand_write(LocalTableDev t, const uint64_t* pk, uint64_t n, const uint32_t* offsets,
+                         const uint64_t* const* probe_cols, int nprobe, uint64_t* const* out_cols, void* stream) {
+  if (n == 0) return;
+  ColPtrs pc{};
+  OutPtrs oc{};
+  for (int q = 0; q < nprobe; ++q) pc.p[q] = probe_cols[q];
+  for (int c = 0; c < t.npayload + nprobe; ++c) oc.p[c] = out_cols[c];
+  count_launch();
+  k_expand_write<<<grid_for(n, 256), 256, 0, S(stream)>>>(t, pk, n, offsets, pc, nprobe, oc);
+}
+
+// ------------------------------------------------------------------------ partition / scatter
+__global__ void k_part_scatter(ColPtrs in, int ncols, uint64_t n, int key_col, int nparts,
+                               const unsigned long long* dest_base, const unsigned long long* dest_cnt,
+                               unsigned long long* cursor, uint64_t* send) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); i0 < n;
+       i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    const bool valid = i < n;
+    const uint32_t d = valid ? part_of(in.p[key_col][i], static_cast<uint32_t>(nparts)) : 0xffffffffu;
+    // Warp-aggregated reservation: one atomic per (warp, destination).
+    const unsigned active = __ballot_sync(0xffffffffu, valid);
+    const unsigned peers = __match_any_sync(0xffffffffu, d) & active;
+    unsigned long long base = 0;
+    const int leader = peers ? __ffs(peers) - 1 : 0;
+    if (valid && lane == leader) base = atomicAdd(cursor + d, static_cast<unsigned long long>(__popc(peers)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    if (valid) {
+      const uint64_t pos = base + __popc(peers & ((1u << lane) - 1u));
+      const uint64_t cnt = dest_cnt[d];
+      uint64_t* region = send + dest_base[d] * static_cast<uint64_t>(ncols);
+      for (int c = 0; c < ncols; ++c) region[c * cnt + pos] = in.p[c][i];
+    }
+  }
+}
+void launch_part_scatter(const uint64_t* const* in_cols, int ncols, uint64_t n, int key_col, int nparts,
+                         const unsigned long long* dest_base, const unsigned long long* dest_cnt,
+                         unsigned long long* cursor, uint64_t* send, void* stream) {
+  if (n == 0) return;
+  ColPtrs pc{};
+  for (int c = 0; c < ncols; ++c) pc.p[c] = in_cols[c];
+  count_launch();
+  k_part_scatter<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, ncols, n, key_col, nparts, dest_base, dest_cnt, cursor,
+                                                         send);
+}
+
+__global__ void k_part_ids(const uint64_t* keys, uint64_t n, int nparts, int identity, uint32_t* ids) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = keys[i];
+    ids[i] = identity ? static_cast<uint32_t>(k % static_cast<uint64_t>(nparts)) : part_of(k, nparts);
+  }
+}
+void launch_part_ids(const uint64_t* keys, uint64_t n, int nparts, int identity, uint32_t* ids, void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_part_ids<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, n, nparts, identity, ids);
+}
+
+__global__ void k_gather(ColPtrs in, int ncols, const uint32_t* idx, uint64_t n, OutPtrs out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t j = idx[i];
+    for (int c = 0; c < ncols; ++c) out.p[c][i] = in.p[c][j];
+  }
+}
+void launch_gather(const uint64_t* const* in_cols, int ncols, const uint32_t* idx, uint64_t n, uint64_t* const* out,
+                   void* stream) {
+  if (n == 0) return;
+  ColPtrs pc{};
+  OutPtrs oc{};
+  for (int c = 0; c < ncols; ++c) {
+    pc.p[c] = in_cols[c];
+    oc.p[c] = out[c];
+  }
+  count_launch();
+  k_gather<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, ncols, idx, n, oc);
+}
+
+// --------------------------------------------------------------------------- result emission
+__global__ void k_agg_compact(AggTableDev t, uint64_t nslots, uint64_t* out_keys, unsigned long long* out_slots,
+                              unsigned long long* counter) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t s0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); s0 < nslots;
+       s0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t s = s0 + threadIdx.x;
+    bool take = false;
+    uint64_t key = 0;
+    if (s < nslots) {
+      const uint64_t* h = t.hot + s * t.hw;
+      key = h[0];
+      const bool occupied = (s == nslots - 1) ? (t.cold[s * t.cw] > 0) : (key != kEmptyKey);
+      take = occupied && h[1] > 0;
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, take);
+    unsigned long long base = 0;
+    if (lane == 0 && b) base = atomicAdd(counter, static_cast<unsigned long long>(__popc(b)));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (take) {
+      const uint64_t pos = base + __popc(b & ((1u << lane) - 1u));
+      out_keys[pos] = key ^ 0x8000000000000000ULL;  // signed order under an unsigned radix sort
+      out_slots[pos] = s;
+    }
+  }
+}
+void launch_agg_compact(const AggTableDev& t, uint64_t cap, uint64_t* out_keys, unsigned long long* out_slots,
+                        unsigned long long* counter, void* stream) {
+  count_launch();
+  k_agg_compact<<<grid_for(cap + 1, 256), 256, 0, S(stream)>>>(t, cap + 1, out_keys, out_slots, counter);
+}
+
+struct EmitCols {
+  int32_t kind[2 * kMaxSums + 2];
+  int32_t idx[2 * kMaxSums + 2];
+};
+__global__ void k_agg_emit(AggTableDev t, const uint64_t* keys, const unsigned long long* slots, uint64_t n, int nc,
+                           EmitCols ec, uint64_t* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t s = slots[i];
+    const uint64_t* h = t.hot + s * t.hw;
+    const uint64_t* c = t.cold + s * t.cw;
+    const uint64_t hits = h[1], m = c[0];
+    uint64_t* row = out + i * nc;
+    for (int k = 0; k < nc; ++k) {
+      const int kind = ec.kind[k], j = ec.idx[k];
+      uint64_t v = 0;
+      if (kind == 0) {
+        v = keys[i] ^ 0x8000000000000000ULL;
+      } else if (kind == 1) {
+        v = hits * m;
+      } else if (kind == 2) {  // probe-side sum: each probe row pairs with m build rows
+        v = t.ps_float[j] ? static_cast<uint64_t>(__double_as_longlong(
+                                static_cast<double>(m) * __longlong_as_double(static_cast<long long>(h[2 + j]))))
+                          : m * h[2 + j];
+      } else {  // build-side sum: each matched probe row adds the key's build-side total
+        v = t.bs_float[j] ? static_cast<uint64_t>(__double_as_longlong(
+                                static_cast<double>(hits) * __longlong_as_double(static_cast<long long>(c[1 + j]))))
+                          : hits * c[1 + j];
+      }
+      row[k] = v;
+    }
+  }
+}
+void launch_agg_emit(const AggTableDev& t, const uint64_t* sorted_keys, const unsigned long long* sorted_slots,
+                     uint64_t n, int nc, const int32_t* col_kind, const int32_t* col_idx, uint64_t* out_rows,
+                     void* stream) {
+  if (n == 0) return;
+  EmitCols ec{};
+  for (int k = 0; k < nc; ++k) {
+    ec.kind[k] = col_kind[k];
+    ec.idx[k] = col_idx[k];
+  }
+  count_launch();
+  k_agg_emit<<<grid_for(n, 256), 256, 0, S(stream)>>>(t, sorted_keys, sorted_slots, n, nc, ec, out_rows);
+}
+
+size_t sort_pairs_i64(const uint64_t* keys_in, uint64_t* keys_out, const unsigned long long* v_in,
+                      unsigned long long* v_out, uint64_t n, void* tmp, size_t tmp_bytes, void* stream) {
+  size_t bytes = tmp_bytes;
+  cub::DeviceRadixSort::SortPairs(tmp, bytes, reinterpret_cast<const unsigned long long*>(keys_in),
+                                  reinterpret_cast<unsigned long long*>(keys_out), v_in, v_out,
+                                  static_cast<int64_t>(n), 0, 64, S(stream));
+  if (tmp) count_launch();
+  return bytes;
+}
+size_t sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* v_in, uint32_t* v_out, uint64_t n,
+                      int end_bit, void* tmp, size_t tmp_bytes, void* stream) {
+  size_t bytes = tmp_bytes;
+  cub::DeviceRadixSort::SortPairs(tmp, bytes, keys_in, keys_out, v_in, v_out, static_cast<int64_t>(n), 0, end_bit,
+                                  S(stream));
+  if (tmp) count_launch();
+  return bytes;
+}
+
+__global__ void k_iota(uint32_t* out, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<uint32_t>(i);
+}
+void launch_iota_u32(uint32_t* out, uint64_t n, void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_iota<<<grid_for(n, 256), 256, 0, S(stream)>>>(out, n);
+}
+
+__global__ void k_rows_from_cols(ColPtrs in, int nc, uint64_t n, uint64_t* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    for (int c = 0; c < nc; ++c) out[i * nc + c] = in.p[c][i];
+}
+void launch_rows_from_cols(const uint64_t* const* cols, int nc, uint64_t n, uint64_t* out_rows, void* stream) {
+  if (n == 0 || nc == 0) return;
+  ColPtrs pc{};
+  for (int c = 0; c < nc; ++c) pc.p[c] = cols[c];
+  count_launch();
+  k_rows_from_cols<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, nc, n, out_rows);
+}
+
+}  // namespace psg
