@@ -363,7 +363,7 @@ class Execution {
   void build_local_tables();
   ScanProgram base_program(const SourceDef& s, const RegMap& m, bool with_joins);
   void materialize_into(DevCols& out, const ScanProgram& p0, const BatchView& v, const std::vector<int>& out_regs,
-                        int part_key_reg, DevBuf* part_counts);
+                        int part_key_reg, DevBuf* part_counts, bool timed = false);
   DevCols alloc_cols(size_t ncols, uint64_t cap);
   uint64_t read_count(DevCols& c);
   void run_scan(const ScanProgram& p, const BatchView& v, bool timed);
@@ -644,7 +644,7 @@ void Execution::run_scan(const ScanProgram& p, const BatchView& v, bool timed) {
 }
 
 void Execution::materialize_into(DevCols& out, const ScanProgram& p0, const BatchView& v, const std::vector<int>& out_regs,
-                                 int part_key_reg, DevBuf* part_counts) {
+                                 int part_key_reg, DevBuf* part_counts, bool timed) {
   ScanProgram p = p0;
   p.sink = SINK_MATERIALIZE;
   p.n_out = static_cast<int>(out_regs.size());
@@ -659,7 +659,7 @@ void Execution::materialize_into(DevCols& out, const ScanProgram& p0, const Batc
     p.part_key_reg = part_key_reg;
     p.part_counts = part_counts->as<unsigned long long>();
   }
-  run_scan(p, v, false);
+  run_scan(p, v, timed);
 }
 
 BatchView Execution::upload_segments(std::vector<Segment> segs, DevBuf& holder) {
@@ -1089,7 +1089,7 @@ ResultRows Execution::run(bool want_rows) {
         for (int s = 0; s < p.n_sum; ++s) p.global_float[1 + s] = aggt_.ps_float[s];
         for (int b = 0; b < aggt_.nbs; ++b) p.global_float[1 + p.n_sum + b] = aggt_.bs_float[b];
       }
-      run_scan(p, v, true);
+      run_scan(p, v, false);
     } else {
       // compact, then expanding join against the final CSR table
       DevCols c = alloc_cols(ncols, std::max<uint64_t>(v.rows, 1));
@@ -1155,7 +1155,7 @@ ResultRows Execution::run(bool want_rows) {
       DevBuf pc(ctx_.pool, nr * 8, ctx_.compute);
       PSG_CUDA(cudaMemsetAsync(pc.p, 0, nr * 8, ctx_.compute));
       if (have) {
-        materialize_into(mat, pp, v, p_out, p_out[0], &pc);
+        materialize_into(mat, pp, v, p_out, p_out[0], &pc, staged_ != nullptr);
         pfeed->done();
         st_.ingest_bytes += v.bytes;
       }
