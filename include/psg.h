@@ -166,6 +166,11 @@ int psg_psto_inspect(const char* path, uint64_t* rows, uint32_t* ncols, uint64_t
 int psg_gen_tpch(const char* out_dir, double scale, int nodes, int devices, uint64_t seed,
                  int codec, uint64_t row_group_bytes, int threads);
 
+/* ---- query compiler self-test: NVRTC-compiles representative fused-scan programs for sm_100a
+ * (no GPU needed). Returns the number of failing programs (0 = ok), -1 on error; log gets NVRTC
+ * output for failures. */
+int psg_jit_selftest(char* log, size_t cap);
+
 /* ---- Eq. 1 roofline: t_min (bench.cpp:35-40) ---- */
 double psg_tmin(uint64_t ssd_read_size_agg, double ssd_read_bw_agg, uint64_t net_recv_size_node,
                 double net_bw);

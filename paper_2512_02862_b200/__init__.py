@@ -32,7 +32,7 @@ EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_uniq
            "psg_ctx_set_ingest", "psg_ctx_set_semijoin", "psg_ctx_destroy", "psg_execute_plan", "psg_stage_plan",
            "psg_execute_staged", "psg_staged_free", "psg_result_shape", "psg_result_field", "psg_result_data",
            "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_psto_write",
-           "psg_psto_inspect", "psg_gen_tpch", "psg_tmin"]
+           "psg_psto_inspect", "psg_gen_tpch", "psg_jit_selftest", "psg_tmin"]
 
 
 class PsgError(RuntimeError):
@@ -98,6 +98,7 @@ def lib():
             "psg_psto_inspect": ([c, P(u64), P(ctypes.c_uint32), P(u64), P(i32)], i32),
             "psg_gen_tpch": ([c, ctypes.c_double, i32, i32, u64, i32, u64, i32], i32),
             "psg_tmin": ([u64, ctypes.c_double, u64, ctypes.c_double], ctypes.c_double),
+            "psg_jit_selftest": ([ctypes.c_char_p, ctypes.c_size_t], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -273,6 +274,13 @@ def _ctx():
 
 
 # --------------------------------------------------------------- reference-shaped functions
+def jit_selftest():
+    """NVRTC-compile representative fused-scan programs for sm_100a (no GPU needed)."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    n = lib().psg_jit_selftest(buf, len(buf))
+    return n, buf.value.decode(errors="replace")
+
+
 def tmin(ssd_read_size_agg, ssd_read_bw_agg, net_recv_size_node, net_bw):
     """Eq. 1 (bench.cpp:35-40): max(storage read time, per-node network receive time), seconds."""
     v = lib().psg_tmin(int(ssd_read_size_agg), float(ssd_read_bw_agg), int(net_recv_size_node), float(net_bw))

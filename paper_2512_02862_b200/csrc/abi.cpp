@@ -9,6 +9,7 @@
 #include <cstring>
 
 #include "engine.hpp"
+#include "jit.hpp"
 
 using namespace psg;
 
@@ -295,6 +296,17 @@ int psg_gen_tpch(const char* out_dir, double scale, int nodes, int devices, uint
     if (codec != 0 && codec != 1) throw InvalidInput("unknown codec");
     gen_tpch(out_dir, scale, nodes, devices, seed, static_cast<Codec>(codec), row_group_bytes, threads);
   });
+}
+
+int psg_jit_selftest(char* log, size_t cap) {
+  std::string l;
+  int f = 0;
+  const int rc = guarded([&] { f = jit_selftest(l); });
+  if (log && cap) {
+    std::strncpy(log, l.c_str(), cap - 1);
+    log[cap - 1] = '\0';
+  }
+  return rc != PSG_OK ? -1 : f;
 }
 
 double psg_tmin(uint64_t ssd_read_size_agg, double ssd_read_bw_agg, uint64_t net_recv_size_node, double net_bw) {

@@ -1,0 +1,194 @@
+// Device data structures + hash-table primitives shared by the nvcc-compiled kernels (kernels.cu)
+// and the NVRTC-compiled per-plan kernels (jit.cpp embeds this file verbatim), so both agree on
+// layout and hashing bit for bit.
+#pragma once
+
+#ifdef __CUDACC_RTC__
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+#else
+#include <cstdint>
+#endif
+
+namespace psg {
+
+constexpr uint64_t kEmptyKey = 0x8000000000000000ULL;  // INT64_MIN; real INT64_MIN keys use the spill slot
+constexpr int kMaxIn = 16;
+constexpr int kMaxAtoms = 8;
+constexpr int kMaxJoins = 4;
+constexpr int kMaxPayload = 8;
+constexpr int kMaxRegs = 26;  // interpreter smem = n_regs * 4 rows * 256 threads * 8 B <= 208 KiB
+constexpr int kMaxOut = 16;
+constexpr int kMaxSums = 8;
+constexpr int kMaxParts = 64;
+constexpr int kBlock = 256;
+constexpr int kRowsPerThread = 4;
+constexpr uint64_t kSlotMul = 0xD6E8FEB86659FD93ULL;   // table slot = (k * kSlotMul) >> shift
+constexpr uint64_t kBloomMul = 0xA24BAED4963EE407ULL;  // bloom word/bits from (k * kBloomMul)
+constexpr uint64_t kPartMul = 0x9E3779B97F4A7C15ULL;   // partition_of, hashing.hpp:26-28
+
+enum SinkKind : int { SINK_MATERIALIZE = 0, SINK_BUILD = 1, SINK_PROBE = 2, SINK_PROBE_GLOBAL = 3, SINK_COUNT = 4 };
+
+/// One row group (or one received/materialised run): rows + a device pointer per input column.
+struct Segment {
+  const uint64_t* col[kMaxIn];
+  uint64_t rows;
+  uint64_t tile_begin;  // first tile index of this segment (prefix over segments)
+};
+
+struct AtomDesc {
+  int32_t reg;
+  int32_t op;        // CmpOp: 0 <, 1 <=, 2 ==, 3 !=, 4 >=, 5 >
+  int32_t is_float;  // compare as double (column type Float64)
+  int32_t pad;
+  uint64_t lit;      // int64 literal or double bits (already cast per literal_as<T>)
+};
+
+/// CSR hash table of a replicated build side (local join). Slots [0,cap) linear-probed by key;
+/// slot cap is the spill slot for key == kEmptyKey.
+struct LocalTableDev {
+  uint64_t* keys;
+  uint32_t* cnt;
+  uint32_t* start;
+  uint64_t mask;
+  const uint64_t* payload[kMaxPayload];  // CSR-ordered payload columns (needed ones only)
+  int32_t npayload;
+  int32_t shift;  // 64 - log2(cap)
+};
+
+struct JoinDesc {
+  LocalTableDev t;
+  int32_t key_reg;
+  int32_t payload_reg[kMaxPayload];  // destination register of each payload column
+};
+
+/// Shuffle-join aggregation table (group key == join key, pipeline.cpp:191-195):
+///   hot[slot*hw + 0] = key, +1 = probe hits, +2.. = probe-side sums
+///   cold[slot*cw + 0] = build multiplicity m, +1.. = build-side sums
+/// slot == cap is the spill slot of key == kEmptyKey (occupied iff m > 0).
+struct AggTableDev {
+  uint64_t* hot;
+  uint64_t* cold;
+  uint32_t* bloom;   // optional blocked Bloom filter over the keys (nullptr = none)
+  uint64_t mask;
+  uint64_t bloom_mask;  // number of 32-bit words - 1
+  int32_t hw, cw;
+  int32_t nps, nbs;  // probe-side / build-side sums
+  int32_t ps_float[kMaxSums];
+  int32_t bs_float[kMaxSums];
+  int32_t shift;        // 64 - log2(cap)
+  int32_t bloom_shift;  // 64 - log2(bloom words)
+};
+
+struct ScanProgram {
+  int32_t n_in;        // regs [0,n_in) load from Segment::col
+  int32_t n_pred;      // regs [0,n_pred) are loaded for every row (predicate columns)
+  int32_t n_early;     // regs [n_pred,n_early) load after the predicate, before joins/probe
+  int32_t n_regs;      // total registers (inputs + join payloads)
+  int32_t n_atoms;
+  int32_t n_joins;
+  AtomDesc atoms[kMaxAtoms];
+  JoinDesc joins[kMaxJoins];
+  int32_t sink;
+  // SINK_MATERIALIZE / SINK_COUNT
+  int32_t n_out;
+  int32_t out_reg[kMaxOut];
+  uint64_t* out_col[kMaxOut];
+  uint64_t out_cap;
+  unsigned long long* out_count;        // atomic reservation counter (unordered tiles)
+  const uint64_t* tile_offsets;         // ordered mode: exclusive prefix of tile counts
+  unsigned long long* tile_counts;      // SINK_COUNT output
+  int32_t nparts;                       // >1: histogram of partition_of(reg[part_key_reg])
+  int32_t part_key_reg;
+  unsigned long long* part_counts;
+  // SINK_BUILD / SINK_PROBE / SINK_PROBE_GLOBAL
+  int32_t key_reg;
+  int32_t n_sum;
+  int32_t sum_reg[kMaxSums];            // probe: probe-side sums; build: build-side sums
+  AggTableDev agg;
+  unsigned long long* global_acc;       // SINK_PROBE_GLOBAL: [rows, probe sums..., build sums...]
+  int32_t global_float[2 * kMaxSums + 1];
+};
+
+#if defined(__CUDACC__) || defined(__CUDACC_RTC__)
+/// partition_of (hashing.hpp:26-37): ((k * 0x9E3779B97F4A7C15) >> 13) % n
+__device__ __forceinline__ uint32_t part_of(uint64_t k, uint32_t n) {
+  return static_cast<uint32_t>(((k * kPartMul) >> 13) % n);
+}
+__device__ __forceinline__ uint64_t slot_of(uint64_t key, int shift) { return (key * kSlotMul) >> shift; }
+
+__device__ __forceinline__ bool cmp_i(int64_t a, int op, int64_t b) {
+  switch (op) {
+    case 0: return a < b;
+    case 1: return a <= b;
+    case 2: return a == b;
+    case 3: return a != b;
+    case 4: return a >= b;
+    default: return a > b;
+  }
+}
+__device__ __forceinline__ bool cmp_f(double a, int op, double b) {
+  switch (op) {  // IEEE semantics (NaN compares false except !=)
+    case 0: return a < b;
+    case 1: return a <= b;
+    case 2: return a == b;
+    case 3: return a != b;
+    case 4: return a >= b;
+    default: return a > b;
+  }
+}
+
+__device__ __forceinline__ uint32_t bloom_bits(uint64_t h2, int bshift) {
+  return (1u << ((h2 >> (bshift - 5)) & 31)) | (1u << ((h2 >> (bshift - 10)) & 31)) |
+         (1u << ((h2 >> (bshift - 15)) & 31));
+}
+__device__ __forceinline__ bool bloom_maybe(const AggTableDev& t, uint64_t key) {
+  if (t.bloom == nullptr) return true;
+  const uint64_t h2 = key * kBloomMul;
+  const uint32_t m = bloom_bits(h2, t.bloom_shift);
+  const uint32_t w = __ldg(t.bloom + (h2 >> t.bloom_shift));
+  return (w & m) == m;
+}
+
+__device__ __forceinline__ uint64_t agg_insert_from(const AggTableDev& t, uint64_t key, uint64_t s) {
+  while (true) {
+    unsigned long long* kp = reinterpret_cast<unsigned long long*>(t.hot + s * t.hw);
+    const unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
+    if (prev == kEmptyKey || prev == key) return s;
+    s = (s + 1) & t.mask;
+  }
+}
+__device__ __forceinline__ uint64_t agg_insert(const AggTableDev& t, uint64_t key) {
+  if (key == kEmptyKey) return t.mask + 1;
+  return agg_insert_from(t, key, slot_of(key, t.shift));
+}
+/// Linear probe from slot s whose key k0 was already loaded; UINT64_MAX when absent.
+__device__ __forceinline__ uint64_t agg_lookup_from(const AggTableDev& t, uint64_t key, uint64_t s, uint64_t k0) {
+  while (true) {
+    if (k0 == key) return s;
+    if (k0 == kEmptyKey) return ~0ULL;
+    s = (s + 1) & t.mask;
+    k0 = t.hot[s * t.hw];
+  }
+}
+__device__ __forceinline__ uint64_t agg_lookup(const AggTableDev& t, uint64_t key) {
+  if (key == kEmptyKey) return t.cold[(t.mask + 1) * t.cw] > 0 ? t.mask + 1 : ~0ULL;
+  const uint64_t s = slot_of(key, t.shift);
+  return agg_lookup_from(t, key, s, t.hot[s * t.hw]);
+}
+
+__device__ __forceinline__ uint64_t local_lookup(const LocalTableDev& t, uint64_t key) {
+  if (key == kEmptyKey) return t.cnt[t.mask + 1] > 0 ? t.mask + 1 : ~0ULL;
+  uint64_t s = slot_of(key, t.shift);
+  while (true) {
+    const uint64_t k = t.keys[s];
+    if (k == key) return s;
+    if (k == kEmptyKey) return ~0ULL;
+    s = (s + 1) & t.mask;
+  }
+}
+#endif
+
+}  // namespace psg

@@ -25,6 +25,7 @@
 #include <set>
 
 #include "engine.hpp"
+#include "jit.hpp"
 
 #define PSG_NCCL(call)                                                                              \
   do {                                                                                              \
@@ -57,6 +58,11 @@ uint64_t pow2_at_least(uint64_t x) {
   uint64_t p = 1;
   while (p < x) p <<= 1;
   return p;
+}
+int shift_of(uint64_t pow2) {
+  int l = 0;
+  while ((1ULL << l) < pow2) ++l;
+  return 64 - l;
 }
 uint64_t dbl_bits(double d) {
   uint64_t u;
@@ -296,9 +302,31 @@ std::vector<Segment> make_segments(const BatchPlan& b, uint8_t* dev_base, uint64
   return segs;
 }
 
+/// tile -> segment index table for k_scan (segments must have tile_begin set).
+std::vector<uint32_t> tile_table(const std::vector<Segment>& segs) {
+  const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
+  std::vector<uint32_t> t;
+  for (size_t i = 0; i < segs.size(); ++i) {
+    const uint64_t n = (segs[i].rows + T - 1) / T;
+    t.insert(t.end(), n, static_cast<uint32_t>(i));
+  }
+  return t;
+}
+
+/// Segment array followed by its tile table, as one host blob (8-byte aligned).
+std::vector<uint8_t> pack_view(const std::vector<Segment>& segs, size_t& tile_off) {
+  auto tt = tile_table(segs);
+  tile_off = segs.size() * sizeof(Segment);
+  std::vector<uint8_t> blob(tile_off + ((tt.size() * 4 + 7) & ~size_t(7)));
+  std::memcpy(blob.data(), segs.data(), tile_off);
+  std::memcpy(blob.data() + tile_off, tt.data(), tt.size() * 4);
+  return blob;
+}
+
 // --------------------------------------------------------------------------- device views
 struct BatchView {
   const Segment* d_segs = nullptr;
+  const uint32_t* d_tile_seg = nullptr;
   int nsegs = 0;
   uint64_t ntiles = 0;
   uint64_t rows = 0;   // upper bound (input rows)
@@ -318,7 +346,8 @@ struct DevCols {
 // ------------------------------------------------------------------------------ Staged
 struct StagedScan {
   DevBuf data;
-  DevBuf segs;
+  DevBuf segs;  // segment array + tile table at tile_off
+  size_t tile_off = 0;
   int nsegs = 0;
   uint64_t ntiles = 0, rows = 0, bytes = 0;
 };
@@ -440,7 +469,10 @@ struct StreamFeed : Execution::Feed {
     total_rows = sb.total_rows;
     nbatches = sb.batches.size();
     if (sb.batches.empty()) return;
-    slot_bytes = (std::max(sb.max_batch_bytes, ctx.batch_bytes) + sb.max_segs * sizeof(Segment) + 4095) & ~4095ULL;
+    const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
+    const uint64_t max_tiles = std::max(sb.max_batch_bytes, ctx.batch_bytes) / 8 / T + sb.max_segs + 1;
+    slot_bytes = (std::max(sb.max_batch_bytes, ctx.batch_bytes) + sb.max_segs * sizeof(Segment) + max_tiles * 4 + 4096 +
+                  4095) & ~4095ULL;
     const int threads = std::max(1, ctx.io_threads);
     const int pinned = ctx.pinned_slots > 0 ? ctx.pinned_slots : threads * 2 + 2;
     ingest = std::make_unique<Ingest>(ctx, files, sb.batches, threads, slot_bytes, pinned);
@@ -469,10 +501,13 @@ struct StreamFeed : Execution::Feed {
     uint64_t nt = 0;
     auto segs = make_segments(b, base, nt);
     if (i >= slots.size()) PSG_CUDA(cudaStreamWaitEvent(ctx.copy, slot_free[k], 0));
-    ingest->copy_to_device(i, base, segs.data(), segs.size() * sizeof(Segment), ctx.copy);
+    size_t toff = 0;
+    auto blob = pack_view(segs, toff);
+    ingest->copy_to_device(i, base, blob.data(), blob.size(), ctx.copy);
     PSG_CUDA(cudaEventRecord(copied[k], ctx.copy));
     PSG_CUDA(cudaStreamWaitEvent(ctx.compute, copied[k], 0));
     v.d_segs = reinterpret_cast<const Segment*>(base + b.bytes);
+    v.d_tile_seg = reinterpret_cast<const uint32_t*>(base + b.bytes + toff);
     v.nsegs = static_cast<int>(segs.size());
     v.ntiles = nt;
     v.rows = b.total_rows;
@@ -498,6 +533,7 @@ struct StagedFeed : Execution::Feed {
     if (given || s->nsegs == 0) return false;
     given = true;
     v.d_segs = s->segs.as<Segment>();
+    v.d_tile_seg = reinterpret_cast<const uint32_t*>(s->segs.as<uint8_t>() + s->tile_off);
     v.nsegs = s->nsegs;
     v.ntiles = s->ntiles;
     v.rows = s->rows;
@@ -631,7 +667,7 @@ uint64_t Execution::read_count(DevCols& c) {
 void Execution::run_scan(const ScanProgram& p, const BatchView& v, bool timed) {
   if (v.nsegs == 0) return;
   if (timed) PSG_CUDA(cudaEventRecord(ctx_.ev_a, ctx_.compute));
-  launch_scan(p, v.d_segs, v.nsegs, v.ntiles, 0, ctx_.compute);
+  fused_scan(p, v.d_segs, v.d_tile_seg, v.nsegs, v.ntiles, ctx_.compute);
   if (timed) {
     PSG_CUDA(cudaEventRecord(ctx_.ev_b, ctx_.compute));
     PSG_CUDA(cudaEventSynchronize(ctx_.ev_b));
@@ -672,11 +708,14 @@ BatchView Execution::upload_segments(std::vector<Segment> segs, DevBuf& holder) 
     v.rows += s.rows;
   }
   if (segs.empty()) return v;
-  holder = DevBuf(ctx_.pool, segs.size() * sizeof(Segment), ctx_.compute);
-  PSG_CUDA(cudaMemcpyAsync(holder.p, segs.data(), segs.size() * sizeof(Segment), cudaMemcpyHostToDevice, ctx_.compute));
+  size_t toff = 0;
+  auto blob = pack_view(segs, toff);
+  holder = DevBuf(ctx_.pool, blob.size(), ctx_.compute);
+  PSG_CUDA(cudaMemcpyAsync(holder.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, ctx_.compute));
   // keep host copy alive until the async copy is done
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   v.d_segs = holder.as<Segment>();
+  v.d_tile_seg = reinterpret_cast<const uint32_t*>(holder.as<uint8_t>() + toff);
   v.nsegs = static_cast<int>(segs.size());
   v.ntiles = tiles;
   return v;
@@ -729,7 +768,8 @@ void Execution::build_local_tables() {
       PSG_CUDA(cudaMemsetAsync(cursor.p, 0, (t->cap + 1) * 4, ctx_.compute));
       launch_local_init(t->keys.as<uint64_t>(), t->cnt.as<uint32_t>(), t->cap, ctx_.compute);
       const uint64_t* bk = mat.cols[0].as<uint64_t>();
-      launch_local_count(t->keys.as<uint64_t>(), t->cnt.as<uint32_t>(), t->cap - 1, bk, n, maxc.as<unsigned>(), ctx_.compute);
+      launch_local_count(t->keys.as<uint64_t>(), t->cnt.as<uint32_t>(), t->cap - 1, shift_of(t->cap), bk, n, maxc.as<unsigned>(),
+                         ctx_.compute);
       size_t tb = exclusive_scan_u32(nullptr, nullptr, t->cap + 1, nullptr, 0, ctx_.compute);
       DevBuf tmp(ctx_.pool, tb, ctx_.compute);
       exclusive_scan_u32(t->cnt.as<uint32_t>(), t->start.as<uint32_t>(), t->cap + 1, tmp.p, tb, ctx_.compute);
@@ -741,7 +781,8 @@ void Execution::build_local_tables() {
         src.push_back(mat.cols[1 + k].as<uint64_t>());
         dst.push_back(t->payload.back().as<uint64_t>());
       }
-      launch_local_fill(t->keys.as<uint64_t>(), t->start.as<uint32_t>(), cursor.as<uint32_t>(), t->cap - 1, bk, src.data(),
+      launch_local_fill(t->keys.as<uint64_t>(), t->start.as<uint32_t>(), cursor.as<uint32_t>(), t->cap - 1, shift_of(t->cap), bk,
+                        src.data(),
                         dst.data(), np, n, ctx_.compute);
       unsigned mx = 0;
       PSG_CUDA(cudaMemcpyAsync(&mx, maxc.p, 4, cudaMemcpyDeviceToHost, ctx_.compute));
@@ -751,6 +792,7 @@ void Execution::build_local_tables() {
       t->dev.cnt = t->cnt.as<uint32_t>();
       t->dev.start = t->start.as<uint32_t>();
       t->dev.mask = t->cap - 1;
+      t->dev.shift = shift_of(t->cap);
       t->dev.npayload = np;
       for (int k = 0; k < np; ++k) t->dev.payload[k] = t->payload[k].as<uint64_t>();
       tables.push_back(std::move(t));
@@ -771,6 +813,7 @@ void Execution::build_agg_table(uint64_t build_rows) {
   aggt_.hot = agg_hot_.as<uint64_t>();
   aggt_.cold = agg_cold_.as<uint64_t>();
   aggt_.mask = agg_cap_ - 1;
+  aggt_.shift = shift_of(agg_cap_);
   aggt_.hw = hw;
   aggt_.cw = cw;
   aggt_.nps = nps;
@@ -785,6 +828,7 @@ void Execution::build_agg_table(uint64_t build_rows) {
     agg_bloom_ = DevBuf(ctx_.pool, words * 4, ctx_.compute);
     aggt_.bloom = agg_bloom_.as<uint32_t>();
     aggt_.bloom_mask = words - 1;
+    aggt_.bloom_shift = shift_of(words);
   }
   launch_agg_init(aggt_, agg_cap_, ctx_.compute);
 }
@@ -1043,7 +1087,7 @@ ResultRows Execution::run(bool want_rows) {
     PSG_CUDA(cudaMemsetAsync(maxc.p, 0, 4, ctx_.compute));
     PSG_CUDA(cudaMemsetAsync(cursor.p, 0, (t.cap + 1) * 4, ctx_.compute));
     launch_local_init(t.keys.as<uint64_t>(), t.cnt.as<uint32_t>(), t.cap, ctx_.compute);
-    launch_local_count(t.keys.as<uint64_t>(), t.cnt.as<uint32_t>(), t.cap - 1, all.cols[0].as<uint64_t>(), n,
+    launch_local_count(t.keys.as<uint64_t>(), t.cnt.as<uint32_t>(), t.cap - 1, shift_of(t.cap), all.cols[0].as<uint64_t>(), n,
                        maxc.as<unsigned>(), ctx_.compute);
     size_t tb = exclusive_scan_u32(nullptr, nullptr, t.cap + 1, nullptr, 0, ctx_.compute);
     DevBuf tmp(ctx_.pool, tb, ctx_.compute);
@@ -1055,12 +1099,13 @@ ResultRows Execution::run(bool want_rows) {
       src.push_back(all.cols[c].as<uint64_t>());
       dst.push_back(t.payload.back().as<uint64_t>());
     }
-    launch_local_fill(t.keys.as<uint64_t>(), t.start.as<uint32_t>(), cursor.as<uint32_t>(), t.cap - 1,
+    launch_local_fill(t.keys.as<uint64_t>(), t.start.as<uint32_t>(), cursor.as<uint32_t>(), t.cap - 1, shift_of(t.cap),
                       all.cols[0].as<uint64_t>(), src.data(), dst.data(), nc - 1, n, ctx_.compute);
     t.dev.keys = t.keys.as<uint64_t>();
     t.dev.cnt = t.cnt.as<uint32_t>();
     t.dev.start = t.start.as<uint32_t>();
     t.dev.mask = t.cap - 1;
+    t.dev.shift = shift_of(t.cap);
     t.dev.npayload = nc - 1;
     for (int c = 0; c < nc - 1; ++c) t.dev.payload[c] = t.payload[c].as<uint64_t>();
     PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
@@ -1304,8 +1349,9 @@ void Execution::stage(Staged& st) {
     ss.rows = sb.total_rows;
     ss.bytes = sb.total_bytes;
     if (!all.empty()) {
-      ss.segs = DevBuf(ctx_.pool, all.size() * sizeof(Segment), ctx_.compute);
-      PSG_CUDA(cudaMemcpyAsync(ss.segs.p, all.data(), all.size() * sizeof(Segment), cudaMemcpyHostToDevice, ctx_.compute));
+      auto blob = pack_view(all, ss.tile_off);
+      ss.segs = DevBuf(ctx_.pool, blob.size(), ctx_.compute);
+      PSG_CUDA(cudaMemcpyAsync(ss.segs.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, ctx_.compute));
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
     }
     st.bytes += sb.total_bytes;

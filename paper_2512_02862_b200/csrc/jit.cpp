@@ -1,0 +1,435 @@
+// Query compilation: the fused scan kernel specialised per plan program with NVRTC for sm_100a.
+//
+// k_scan (kernels.cu) interprets a ScanProgram at run time: register indices, atom operators,
+// join chains and sinks are data, which costs ~250 warp instructions per row (ncu, profiles/).
+// Here the same program is emitted as straight-line CUDA C++ — every column lives in named
+// registers, operators are inlined, loops over columns/atoms/sums disappear — and compiled once
+// per distinct program *structure* (literals, table pointers and outputs stay in the kernel's
+// __grid_constant__ ScanProgram, so the cache hits across literal changes and queries). The
+// generated kernel shares device_common.cuh (layout + hashing) with the nvcc-built kernels.
+// Fallback when NVRTC is unavailable: the interpreter k_scan (still GPU; there is no CPU path).
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "jit.hpp"
+#include "kernels.cuh"
+
+namespace psg {
+
+namespace {
+#include "_gen_device_common.inc"  // kDeviceCommonSrc: device_common.cuh verbatim (build.py)
+
+struct Compiled {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  int per_sm = 1;
+  bool ok = false;
+};
+
+std::mutex g_mu;
+std::map<std::pair<int, std::string>, Compiled> g_cache;
+double g_compile_s = 0;
+uint64_t g_compiles = 0;
+
+bool jit_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PSG_JIT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+std::string V(int reg) { return "v" + std::to_string(reg); }
+
+const char* op_str(int op) {
+  switch (op) {
+    case 0: return "<";
+    case 1: return "<=";
+    case 2: return "==";
+    case 3: return "!=";
+    case 4: return ">=";
+    default: return ">";
+  }
+}
+
+/// Emits `for r: if (pass & bit) vC[r] = load(col c of the tile)` for columns [lo, hi).
+void emit_loads(std::ostringstream& s, int lo, int hi) {
+  for (int c = lo; c < hi; ++c) {
+    s << "    { const uint64_t* col = s_col[b][" << c << "] + row0 + tid;\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (pass & (1u << r)) " << V(c)
+      << "[r] = __ldcs(reinterpret_cast<const unsigned long long*>(col + r * 256));\n    }\n";
+  }
+}
+
+}  // namespace
+
+std::string jit_source(const ScanProgram& P) {
+  std::ostringstream s;
+  const int nin = P.n_in, nregs = std::max(1, P.n_regs);
+  const bool mat = P.sink == SINK_MATERIALIZE || P.sink == SINK_COUNT;
+  const bool probe = P.sink == SINK_PROBE || P.sink == SINK_PROBE_GLOBAL;
+  const bool part = P.sink == SINK_MATERIALIZE && P.nparts > 1;
+  const bool glob = P.sink == SINK_PROBE_GLOBAL;
+  const int nglob = glob ? 1 + P.n_sum + P.agg.nbs : 0;
+  s << "using namespace psg;\n#define R 4\n"
+    << "extern \"C\" __global__ void __launch_bounds__(256) psg_jit_scan(const __grid_constant__ ScanProgram P, "
+       "const Segment* __restrict__ segs, const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {\n"
+    << "  __shared__ const uint64_t* s_col[2][" << std::max(1, nin) << "];\n"
+    << "  __shared__ uint64_t s_row0[2], s_rows[2];\n";
+  if (mat) s << "  __shared__ uint32_t s_wcnt[R][8], s_woff[R][8];\n  __shared__ unsigned long long s_base;\n";
+  if (part) s << "  __shared__ unsigned long long s_part[" << kMaxParts << "];\n";
+  if (glob) s << "  __shared__ unsigned long long s_gacc[" << nglob << "];\n";
+  s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  (void)lane; (void)warp;\n";
+  if (part) s << "  for (int i = tid; i < " << kMaxParts << "; i += 256) s_part[i] = 0;\n";
+  if (glob) {
+    s << "  for (int i = tid; i < " << nglob << "; i += 256) s_gacc[i] = 0;\n";
+    for (int i = 0; i < nglob; ++i)
+      s << "  " << (P.global_float[i] ? "double" : "unsigned long long") << " g" << i << " = 0;\n";
+  }
+  // tile descriptors: double-buffered, next tile prefetched into registers
+  s << "  auto fetch = [&](uint64_t t, const uint64_t*& col, uint64_t& r0, uint64_t& rows) {\n"
+    << "    const uint32_t si = __ldg(tile_seg + t);\n"
+    << "    if (tid < " << nin << ") { col = segs[si].col[tid]; }\n"
+    << "    else if (tid == " << kMaxIn << ") { const uint64_t tb = segs[si].tile_begin; r0 = (t - tb) * 1024ULL;"
+       " rows = min(1024ULL, segs[si].rows - r0); }\n  };\n"
+    << "  if (blockIdx.x < ntiles) { const uint64_t* c = nullptr; uint64_t r0 = 0, rows = 0;"
+       " fetch(blockIdx.x, c, r0, rows);\n"
+    << "    if (tid < " << nin << ") s_col[0][tid] = c;\n"
+    << "    if (tid == " << kMaxIn << ") { s_row0[0] = r0; s_rows[0] = rows; } }\n  __syncthreads();\n"
+    << "  int it = 0;\n"
+    << "  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {\n"
+    << "    const int b = it & 1;\n    const uint64_t next = tile + gridDim.x;\n"
+    << "    const uint64_t* pf_col = nullptr; uint64_t pf_r0 = 0, pf_rows = 0;\n"
+    << "    if (next < ntiles) fetch(next, pf_col, pf_r0, pf_rows);\n"
+    << "    const uint64_t row0 = s_row0[b];\n    const int nrows = static_cast<int>(s_rows[b]);\n"
+    << "    uint32_t pass = 0;\n#pragma unroll\n    for (int r = 0; r < R; ++r) if (r * 256 + tid < nrows) pass |= 1u << r;\n";
+  for (int r = 0; r < nregs; ++r) s << "    uint64_t " << V(r) << "[R] = {0, 0, 0, 0};\n";
+  // Phase A: predicate columns + atoms
+  emit_loads(s, 0, P.n_pred);
+  for (int a = 0; a < P.n_atoms; ++a) {
+    const AtomDesc& at = P.atoms[a];
+    if (at.is_float) {
+      s << "    { const double lit = __longlong_as_double(static_cast<long long>(P.atoms[" << a << "].lit));\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!(__longlong_as_double(static_cast<long long>(" << V(at.reg)
+        << "[r])) " << op_str(at.op) << " lit)) pass &= ~(1u << r);\n    }\n";
+    } else {
+      s << "    { const long long lit = static_cast<long long>(P.atoms[" << a << "].lit);\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!(static_cast<long long>(" << V(at.reg) << "[r]) "
+        << op_str(at.op) << " lit)) pass &= ~(1u << r);\n    }\n";
+    }
+  }
+  // Phase B: early columns
+  emit_loads(s, P.n_pred, P.n_early);
+  // Phase C: unique-key local joins (two-stage probe: home-slot loads for all rows first)
+  for (int j = 0; j < P.n_joins; ++j) {
+    const JoinDesc& jd = P.joins[j];
+    s << "    { const LocalTableDev& T = P.joins[" << j << "].t;\n      uint64_t sl[R], k0[R];\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = ~0ULL; k0[r] = 0; if (pass & (1u << r)) {\n"
+      << "        const uint64_t key = " << V(jd.key_reg) << "[r];\n"
+      << "        if (key == kEmptyKey) { if (T.cnt[T.mask + 1] == 0) pass &= ~(1u << r); else { sl[r] = T.mask + 1; k0[r] = key; } }\n"
+      << "        else { sl[r] = slot_of(key, T.shift); k0[r] = T.keys[sl[r]]; } } }\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+      << "        const uint64_t key = " << V(jd.key_reg) << "[r]; uint64_t sx = sl[r], kk = k0[r];\n"
+      << "        if (sx != T.mask + 1) { while (kk != key && kk != kEmptyKey) { sx = (sx + 1) & T.mask; kk = T.keys[sx]; }\n"
+      << "          if (kk != key) { pass &= ~(1u << r); continue; } }\n";
+    if (jd.t.npayload > 0) {
+      s << "        const uint32_t st = T.start[sx];\n";
+      for (int p = 0; p < jd.t.npayload; ++p)
+        s << "        " << V(jd.payload_reg[p]) << "[r] = T.payload[" << p << "][st];\n";
+    }
+    s << "      }\n    }\n";
+  }
+  if (probe) {
+    const bool bloom = P.agg.bloom != nullptr;
+    s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R], k0[R];\n";
+    if (bloom) {
+      s << "      uint32_t bw[R], bm[R];\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bm[r] = 0; if ((pass & (1u << r)) && " << V(P.key_reg)
+        << "[r] != kEmptyKey) {\n        const uint64_t h2 = " << V(P.key_reg) << "[r] * kBloomMul;\n"
+        << "        bm[r] = bloom_bits(h2, T.bloom_shift); bw[r] = __ldg(T.bloom + (h2 >> T.bloom_shift)); } }\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && " << V(P.key_reg)
+        << "[r] != kEmptyKey && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n";
+    }
+    s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = ~0ULL; k0[r] = 0; if (pass & (1u << r)) {\n"
+      << "        const uint64_t key = " << V(P.key_reg) << "[r];\n"
+      << "        if (key == kEmptyKey) { if (T.cold[(T.mask + 1) * T.cw] == 0) pass &= ~(1u << r); else sl[r] = T.mask + 1; }\n"
+      << "        else { sl[r] = slot_of(key, T.shift); k0[r] = T.hot[sl[r] * " << P.agg.hw << "]; } } }\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r)) || sl[r] == T.mask + 1) continue;\n"
+      << "        const uint64_t key = " << V(P.key_reg) << "[r]; uint64_t sx = sl[r], kk = k0[r];\n"
+      << "        while (kk != key && kk != kEmptyKey) { sx = (sx + 1) & T.mask; kk = T.hot[sx * " << P.agg.hw << "]; }\n"
+      << "        if (kk != key) pass &= ~(1u << r); else sl[r] = sx; }\n";
+    emit_loads(s, P.n_early, P.n_in);
+    if (P.sink == SINK_PROBE) {
+      s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+        << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n"
+        << "        atomicAdd(h + 1, 1ULL);\n";
+      for (int p = 0; p < P.n_sum; ++p) {
+        if (P.agg.ps_float[p])
+          s << "        atomicAdd(reinterpret_cast<double*>(h + " << 2 + p << "), __longlong_as_double(static_cast<long long>("
+            << V(P.sum_reg[p]) << "[r])));\n";
+        else
+          s << "        atomicAdd(h + " << 2 + p << ", static_cast<unsigned long long>(" << V(P.sum_reg[p]) << "[r]));\n";
+      }
+      s << "      }\n";
+    } else {
+      s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+        << "        const uint64_t* cold = T.cold + sl[r] * " << P.agg.cw << ";\n        const uint64_t m = cold[0];\n"
+        << "        g0 += m;\n";
+      for (int p = 0; p < P.n_sum; ++p) {
+        if (P.agg.ps_float[p])
+          s << "        g" << 1 + p << " += static_cast<double>(m) * __longlong_as_double(static_cast<long long>("
+            << V(P.sum_reg[p]) << "[r]));\n";
+        else
+          s << "        g" << 1 + p << " += m * " << V(P.sum_reg[p]) << "[r];\n";
+      }
+      for (int bb = 0; bb < P.agg.nbs; ++bb) {
+        if (P.agg.bs_float[bb])
+          s << "        g" << 1 + P.n_sum + bb << " += __longlong_as_double(static_cast<long long>(cold[" << 1 + bb << "]));\n";
+        else
+          s << "        g" << 1 + P.n_sum + bb << " += cold[" << 1 + bb << "];\n";
+      }
+      s << "      }\n";
+    }
+    s << "    }\n";
+  } else {
+    emit_loads(s, P.n_early, P.n_in);
+    if (P.sink == SINK_BUILD) {
+      s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R]; unsigned long long pv[R];\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0; pv[r] = kEmptyKey; if (!(pass & (1u << r))) continue;\n"
+        << "        const uint64_t key = " << V(P.key_reg) << "[r];\n"
+        << "        if (key == kEmptyKey) { sl[r] = T.mask + 1; continue; }\n"
+        << "        sl[r] = slot_of(key, T.shift);\n"
+        << "        pv[r] = atomicCAS(reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << "), kEmptyKey, key); }\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+        << "        const uint64_t key = " << V(P.key_reg) << "[r]; uint64_t sx = sl[r];\n"
+        << "        if (pv[r] != kEmptyKey && pv[r] != key) sx = agg_insert_from(T, key, (sx + 1) & T.mask);\n"
+        << "        unsigned long long* cold = reinterpret_cast<unsigned long long*>(T.cold + sx * " << P.agg.cw << ");\n"
+        << "        atomicAdd(cold, 1ULL);\n";
+      for (int bb = 0; bb < P.n_sum; ++bb) {
+        if (P.agg.bs_float[bb])
+          s << "        atomicAdd(reinterpret_cast<double*>(cold + " << 1 + bb << "), __longlong_as_double(static_cast<long long>("
+            << V(P.sum_reg[bb]) << "[r])));\n";
+        else
+          s << "        atomicAdd(cold + " << 1 + bb << ", static_cast<unsigned long long>(" << V(P.sum_reg[bb]) << "[r]));\n";
+      }
+      s << "      }\n    }\n";
+    } else {  // MATERIALIZE / COUNT
+      s << "    uint32_t ballots[R];\n#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
+        << "      ballots[r] = __ballot_sync(0xffffffffu, (pass >> r) & 1u);\n"
+        << "      if (lane == 0) s_wcnt[r][warp] = __popc(ballots[r]); }\n    __syncthreads();\n"
+        << "    if (tid == 0) { uint32_t acc = 0;\n      for (int r = 0; r < R; ++r) for (int w = 0; w < 8; ++w) { s_woff[r][w] = acc; acc += s_wcnt[r][w]; }\n";
+      if (P.sink == SINK_COUNT)
+        s << "      P.tile_counts[tile] = acc;\n";
+      else if (P.tile_offsets)
+        s << "      s_base = P.tile_offsets[tile];\n";
+      else
+        s << "      s_base = acc ? atomicAdd(P.out_count, static_cast<unsigned long long>(acc)) : 0ULL;\n";
+      s << "    }\n    __syncthreads();\n";
+      if (P.sink == SINK_MATERIALIZE) {
+        s << "    { const uint64_t base = s_base; const uint32_t lt = (1u << lane) - 1u;\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!((pass >> r) & 1u)) continue;\n"
+          << "        const uint64_t pos = base + s_woff[r][warp] + __popc(ballots[r] & lt);\n"
+          << "        if (pos >= P.out_cap) continue;\n";
+        for (int o = 0; o < P.n_out; ++o) s << "        P.out_col[" << o << "][pos] = " << V(P.out_reg[o]) << "[r];\n";
+        if (part)
+          s << "        atomicAdd(&s_part[part_of(" << V(P.part_key_reg) << "[r], static_cast<uint32_t>(P.nparts))], 1ULL);\n";
+        s << "      }\n    }\n";
+      }
+    }
+  }
+  s << "    if (next < ntiles) { if (tid < " << nin << ") s_col[b ^ 1][tid] = pf_col;\n"
+    << "      if (tid == " << kMaxIn << ") { s_row0[b ^ 1] = pf_r0; s_rows[b ^ 1] = pf_rows; } }\n"
+    << "    __syncthreads();\n  }\n";
+  if (part)
+    s << "  __syncthreads();\n  for (int i = tid; i < P.nparts; i += 256) if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
+  if (glob) {
+    for (int i = 0; i < nglob; ++i) {
+      if (P.global_float[i])
+        s << "  atomicAdd(reinterpret_cast<double*>(&s_gacc[" << i << "]), g" << i << ");\n";
+      else
+        s << "  atomicAdd(&s_gacc[" << i << "], g" << i << ");\n";
+    }
+    s << "  __syncthreads();\n  for (int i = tid; i < " << nglob << "; i += 256) {\n"
+      << "    if (P.global_float[i]) atomicAdd(reinterpret_cast<double*>(&P.global_acc[i]), "
+         "__longlong_as_double(static_cast<long long>(s_gacc[i])));\n"
+      << "    else atomicAdd(&P.global_acc[i], s_gacc[i]); }\n";
+  }
+  s << "}\n";
+  return s.str();
+}
+
+namespace {
+
+/// NVRTC: CUDA C++ -> sm_100a cubin. Returns false (with the log) on failure.
+bool nvrtc_cubin(const std::string& body, std::string& cubin, std::string& log) {
+  const std::string src = std::string(kDeviceCommonSrc) + "\n" + body;
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, src.c_str(), "psg_jit_scan.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    log = "nvrtcCreateProgram failed";
+    return false;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "--restrict"};
+  const nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  size_t n = 0;
+  nvrtcGetProgramLogSize(prog, &n);
+  log.assign(n, '\0');
+  if (n) nvrtcGetProgramLog(prog, log.data());
+  if (r != NVRTC_SUCCESS) {
+    nvrtcDestroyProgram(&prog);
+    return false;
+  }
+  nvrtcGetCUBINSize(prog, &n);
+  cubin.assign(n, '\0');
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  return true;
+}
+
+Compiled compile(const std::string& body, int device) {
+  Compiled c;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::string cubin, log;
+  if (!nvrtc_cubin(body, cubin, log)) {
+    std::fprintf(stderr, "[psg] NVRTC compile failed (falling back to the interpreter kernel):\n%s\n", log.c_str());
+    return c;
+  }
+  if (cudaLibraryLoadData(&c.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return c;
+  }
+  if (cudaLibraryGetKernel(&c.kern, c.lib, "psg_jit_scan") != cudaSuccess) {
+    cudaGetLastError();
+    return c;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(c.kern), kBlock, 0) !=
+          cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 4;
+  }
+  c.per_sm = per_sm;
+  c.ok = true;
+  g_compile_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  ++g_compiles;
+  (void)device;
+  return c;
+}
+
+}  // namespace
+
+void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_tile_seg, int nsegs, uint64_t ntiles,
+                cudaStream_t stream) {
+  if (ntiles == 0 || nsegs == 0) return;
+  if (jit_enabled()) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const std::string body = jit_source(P);
+    Compiled c;
+    {
+      std::lock_guard<std::mutex> lk(g_mu);
+      auto key = std::make_pair(dev, body);
+      auto it = g_cache.find(key);
+      if (it == g_cache.end()) it = g_cache.emplace(key, compile(body, dev)).first;
+      c = it->second;
+    }
+    if (c.ok) {
+      int sms = 148;
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      uint64_t grid = static_cast<uint64_t>(sms) * c.per_sm;
+      if (grid > ntiles) grid = ntiles;
+      void* args[] = {const_cast<ScanProgram*>(&P), const_cast<Segment**>(&d_segs), const_cast<uint32_t**>(&d_tile_seg),
+                      &ntiles};
+      count_external_launch();
+      PSG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(c.kern), dim3(static_cast<unsigned>(grid)), dim3(kBlock),
+                                args, 0, stream));
+      return;
+    }
+  }
+  launch_scan(P, d_segs, d_tile_seg, nsegs, ntiles, stream);
+}
+
+int jit_selftest(std::string& log) {
+  // Representative program structures: every sink, int/float atoms, a local join with payload,
+  // Bloom-screened probe, partition histogram, ordered compaction, global aggregate.
+  std::vector<ScanProgram> progs;
+  auto base = [] {
+    ScanProgram p;
+    std::memset(&p, 0, sizeof p);
+    p.n_in = 4;
+    p.n_pred = 1;
+    p.n_early = 2;
+    p.n_regs = 4;
+    p.n_atoms = 2;
+    p.atoms[0] = AtomDesc{0, 5, 0, 0, 19950315};
+    p.atoms[1] = AtomDesc{0, 3, 0, 0, 7};
+    p.key_reg = 1;
+    p.part_key_reg = -1;
+    return p;
+  };
+  for (int sink : {SINK_MATERIALIZE, SINK_BUILD, SINK_PROBE, SINK_PROBE_GLOBAL, SINK_COUNT}) {
+    ScanProgram p = base();
+    p.sink = sink;
+    p.n_sum = 2;
+    p.sum_reg[0] = 2;
+    p.sum_reg[1] = 3;
+    p.agg.hw = 4;
+    p.agg.cw = 2;
+    p.agg.nbs = 1;
+    p.agg.ps_float[1] = 1;
+    p.agg.bs_float[0] = 1;
+    p.global_float[2] = 1;
+    p.global_float[3] = 1;
+    p.n_out = 3;
+    p.out_reg[0] = 1, p.out_reg[1] = 2, p.out_reg[2] = 3;
+    if (sink == SINK_PROBE) p.agg.bloom = reinterpret_cast<uint32_t*>(16);
+    if (sink == SINK_MATERIALIZE) {
+      p.nparts = 4;
+      p.part_key_reg = 1;
+    }
+    progs.push_back(p);
+  }
+  {
+    ScanProgram p = base();  // orders-like: filter, local join with payload, materialise
+    p.sink = SINK_MATERIALIZE;
+    p.n_in = 3;
+    p.n_regs = 5;
+    p.n_joins = 1;
+    p.joins[0].key_reg = 1;
+    p.joins[0].t.npayload = 2;
+    p.joins[0].payload_reg[0] = 3;
+    p.joins[0].payload_reg[1] = 4;
+    p.atoms[1] = AtomDesc{0, 1, 1, 0, 0};
+    p.n_out = 2;
+    p.out_reg[0] = 2, p.out_reg[1] = 4;
+    p.tile_offsets = reinterpret_cast<const uint64_t*>(16);
+    progs.push_back(p);
+  }
+  int failures = 0;
+  for (auto& p : progs) {
+    std::string cubin, l;
+    if (!nvrtc_cubin(jit_source(p), cubin, l) || cubin.empty()) {
+      ++failures;
+      log += "sink " + std::to_string(p.sink) + ": " + l + "\n";
+    }
+  }
+  return failures;
+}
+
+JitStats jit_stats() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  return JitStats{g_compiles, g_compile_s, jit_enabled()};
+}
+
+}  // namespace psg

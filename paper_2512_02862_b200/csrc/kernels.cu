@@ -47,96 +47,17 @@ inline unsigned grid_for(uint64_t n, int per_block) {
 }  // namespace
 
 uint64_t kernel_launch_count() { return g_launches.load(); }
-
-// ------------------------------------------------------------------------------------ hashing
-__device__ __forceinline__ uint64_t mix64(uint64_t k) {
-  k ^= k >> 33;
-  k *= 0xff51afd7ed558ccdULL;
-  k ^= k >> 33;
-  k *= 0xc4ceb9fe1a85ec53ULL;
-  k ^= k >> 33;
-  return k;
-}
-/// partition_of (hashing.hpp:26-37): ((k * 0x9E3779B97F4A7C15) >> 13) % n
-__device__ __forceinline__ uint32_t part_of(uint64_t k, uint32_t n) {
-  return static_cast<uint32_t>(((k * 0x9E3779B97F4A7C15ULL) >> 13) % n);
-}
-
-__device__ __forceinline__ bool cmp_i(int64_t a, int op, int64_t b) {
-  switch (op) {
-    case 0: return a < b;
-    case 1: return a <= b;
-    case 2: return a == b;
-    case 3: return a != b;
-    case 4: return a >= b;
-    default: return a > b;
-  }
-}
-__device__ __forceinline__ bool cmp_f(double a, int op, double b) {
-  switch (op) {
-    case 0: return a < b;
-    case 1: return a <= b;
-    case 2: return a == b;
-    case 3: return a != b;
-    case 4: return a >= b;
-    default: return a > b;
-  }
-}
-
-// ------------------------------------------------------------------------------ agg table ops
-__device__ __forceinline__ uint64_t agg_insert(const AggTableDev& t, uint64_t key) {
-  if (key == kEmptyKey) return t.mask + 1;
-  uint64_t s = mix64(key) & t.mask;
-  while (true) {
-    unsigned long long* kp = reinterpret_cast<unsigned long long*>(t.hot + s * t.hw);
-    const unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
-    if (prev == kEmptyKey || prev == key) return s;
-    s = (s + 1) & t.mask;
-  }
-}
-
-__device__ __forceinline__ bool bloom_maybe(const AggTableDev& t, uint64_t key) {
-  if (t.bloom == nullptr) return true;
-  const uint64_t h = mix64(key ^ 0x5bd1e9955bd1e995ULL);
-  const uint32_t w = __ldg(t.bloom + (h & t.bloom_mask));
-  const uint32_t m = (1u << ((h >> 40) & 31)) | (1u << ((h >> 46) & 31)) | (1u << ((h >> 52) & 31));
-  return (w & m) == m;
-}
-
-/// Returns the slot of key or UINT64_MAX when absent.
-__device__ __forceinline__ uint64_t agg_lookup_from(const AggTableDev& t, uint64_t key, uint64_t s, uint64_t k0) {
-  while (true) {
-    if (k0 == key) return s;
-    if (k0 == kEmptyKey) return ~0ULL;
-    s = (s + 1) & t.mask;
-    k0 = t.hot[s * t.hw];
-  }
-}
-__device__ __forceinline__ uint64_t agg_lookup(const AggTableDev& t, uint64_t key) {
-  if (key == kEmptyKey) return t.cold[(t.mask + 1) * t.cw] > 0 ? t.mask + 1 : ~0ULL;
-  const uint64_t s = mix64(key) & t.mask;
-  return agg_lookup_from(t, key, s, t.hot[s * t.hw]);
-}
-
-// ---------------------------------------------------------------------------- local table ops
-__device__ __forceinline__ uint64_t local_lookup(const LocalTableDev& t, uint64_t key) {
-  if (key == kEmptyKey) return t.cnt[t.mask + 1] > 0 ? t.mask + 1 : ~0ULL;
-  uint64_t s = mix64(key) & t.mask;
-  while (true) {
-    const uint64_t k = t.keys[s];
-    if (k == key) return s;
-    if (k == kEmptyKey) return ~0ULL;
-    s = (s + 1) & t.mask;
-  }
-}
+void count_external_launch() { count_launch(); }
 
 // ------------------------------------------------------------------------------- fused k_scan
 template <int R, int SINK>
 __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanProgram P, const Segment* __restrict__ segs,
-                                                 int nsegs, uint64_t ntiles) {
+                                                 const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {
   extern __shared__ uint64_t smem[];  // [n_regs][R][kBlock]
-  __shared__ const uint64_t* s_col[kMaxIn];
-  __shared__ uint64_t s_row0, s_rows;
+  // Double-buffered tile descriptors: the next tile's segment/column pointers are fetched into
+  // registers while the current tile computes (two dependent loads hidden behind the tile).
+  __shared__ const uint64_t* s_col[2][kMaxIn];
+  __shared__ uint64_t s_row0[2], s_rows[2];
   __shared__ uint32_t s_wcnt[R][kBlock / 32];
   __shared__ uint32_t s_woff[R][kBlock / 32];
   __shared__ unsigned long long s_base;
@@ -151,24 +72,36 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
     for (int i = tid; i < P.nparts; i += kBlock) s_part[i] = 0;
   if (SINK == SINK_PROBE_GLOBAL)
     for (int i = tid; i < 2 * kMaxSums + 1; i += kBlock) s_gacc[i] = 0;
+  auto fetch = [&](uint64_t t, const uint64_t*& col, uint64_t& r0, uint64_t& rows) {
+    const uint32_t si = __ldg(tile_seg + t);
+    if (tid < P.n_in) {
+      col = segs[si].col[tid];
+    } else if (tid == kMaxIn) {
+      const uint64_t tb = segs[si].tile_begin;
+      r0 = (t - tb) * TILE;
+      rows = min(static_cast<uint64_t>(TILE), segs[si].rows - r0);
+    }
+  };
+  if (blockIdx.x < ntiles) {
+    const uint64_t* c = nullptr;
+    uint64_t r0 = 0, rows = 0;
+    fetch(blockIdx.x, c, r0, rows);
+    if (tid < P.n_in) s_col[0][tid] = c;
+    if (tid == kMaxIn) s_row0[0] = r0, s_rows[0] = rows;
+  }
   __syncthreads();
 
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    if (tid == 0) {
-      int lo = 0, hi = nsegs - 1;  // last segment with tile_begin <= tile
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (segs[mid].tile_begin <= tile) lo = mid; else hi = mid - 1;
-      }
-      const Segment* sg = &segs[lo];
-      const uint64_t row0 = (tile - sg->tile_begin) * TILE;
-      s_row0 = row0;
-      s_rows = min(static_cast<uint64_t>(TILE), sg->rows - row0);
-      for (int c = 0; c < P.n_in; ++c) s_col[c] = sg->col[c];
-    }
-    __syncthreads();
-    const uint64_t row0 = s_row0;
-    const int nrows = static_cast<int>(s_rows);
+  int it = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int b = it & 1;
+    const uint64_t next = tile + gridDim.x;
+    const uint64_t* pf_col = nullptr;
+    uint64_t pf_r0 = 0, pf_rows = 0;
+    if (next < ntiles) fetch(next, pf_col, pf_r0, pf_rows);
+    const uint64_t* const* s_colb = s_col[b];
+    const uint64_t row0 = s_row0[b];
+    const int nrows = static_cast<int>(s_rows[b]);
+#define s_col s_colb
 
     // Phase A: predicate columns for every row (R independent coalesced loads per column).
     uint32_t pass = 0;
@@ -240,7 +173,7 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
           pass &= ~(1u << r);
           continue;
         }
-        home[r] = mix64(key) & t.mask;
+        home[r] = slot_of(key, t.shift);
       }
       uint64_t k0[R];
 #pragma unroll
@@ -307,10 +240,28 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
       }
       if (SINK == SINK_BUILD) {
         const AggTableDev& t = P.agg;
+        // Claim the home slots of all R rows first (R CASes in flight), then resolve collisions.
+        uint64_t slot[R];
+        unsigned long long prev[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          slot[r] = ~0ULL;
+          if (!(pass & (1u << r))) continue;
+          const uint64_t key = V(P.key_reg, r);
+          if (key == kEmptyKey) {
+            slot[r] = t.mask + 1;
+            prev[r] = kEmptyKey;
+            continue;
+          }
+          slot[r] = slot_of(key, t.shift);
+          prev[r] = atomicCAS(reinterpret_cast<unsigned long long*>(t.hot + slot[r] * t.hw), kEmptyKey, key);
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           if (!(pass & (1u << r))) continue;
-          const uint64_t s = agg_insert(t, V(P.key_reg, r));
+          const uint64_t key = V(P.key_reg, r);
+          uint64_t s = slot[r];
+          if (prev[r] != kEmptyKey && prev[r] != key) s = agg_insert_from(t, key, (s + 1) & t.mask);
           unsigned long long* cold = reinterpret_cast<unsigned long long*>(t.cold + s * t.cw);
           atomicAdd(cold, 1ULL);
           for (int b = 0; b < P.n_sum; ++b) {
@@ -360,6 +311,11 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
         }
       }
     }
+#undef s_col
+    if (next < ntiles) {
+      if (tid < P.n_in) s_col[b ^ 1][tid] = pf_col;
+      if (tid == kMaxIn) s_row0[b ^ 1] = pf_r0, s_rows[b ^ 1] = pf_rows;
+    }
     __syncthreads();
   }
 #undef V
@@ -383,7 +339,8 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
 int scan_tile_rows() { return 4 * kBlock; }
 
 template <int R, int SINK>
-static void launch_scan_t(const ScanProgram& P, const Segment* d_segs, int nsegs, uint64_t ntiles, cudaStream_t st) {
+static void launch_scan_t(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_tile_seg, uint64_t ntiles,
+                          cudaStream_t st) {
   const size_t smem = static_cast<size_t>(P.n_regs < 1 ? 1 : P.n_regs) * R * kBlock * sizeof(uint64_t);
   static bool configured = false;
   if (!configured) {
@@ -397,20 +354,21 @@ static void launch_scan_t(const ScanProgram& P, const Segment* d_segs, int nsegs
   if (grid > ntiles) grid = ntiles;
   if (grid < 1) grid = 1;
   count_launch();
-  k_scan<R, SINK><<<static_cast<unsigned>(grid), kBlock, smem, st>>>(P, d_segs, nsegs, ntiles);
+  k_scan<R, SINK><<<static_cast<unsigned>(grid), kBlock, smem, st>>>(P, d_segs, d_tile_seg, ntiles);
 }
 
-void launch_scan(const ScanProgram& P, const Segment* d_segs, int nsegs, uint64_t ntiles, int, void* stream) {
+void launch_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_tile_seg, int nsegs, uint64_t ntiles,
+                 void* stream) {
   if (ntiles == 0 || nsegs == 0) return;
   cudaStream_t st = S(stream);
   // Tiles are always 4 x 256 rows; programs with many registers use R=2 sub-tiles twice as
   // many CTAs would need, so they run R=4 with fewer resident CTAs (smem = n_regs * 8 KiB).
   switch (P.sink) {
-    case SINK_MATERIALIZE: launch_scan_t<4, SINK_MATERIALIZE>(P, d_segs, nsegs, ntiles, st); break;
-    case SINK_BUILD: launch_scan_t<4, SINK_BUILD>(P, d_segs, nsegs, ntiles, st); break;
-    case SINK_PROBE: launch_scan_t<4, SINK_PROBE>(P, d_segs, nsegs, ntiles, st); break;
-    case SINK_PROBE_GLOBAL: launch_scan_t<4, SINK_PROBE_GLOBAL>(P, d_segs, nsegs, ntiles, st); break;
-    case SINK_COUNT: launch_scan_t<4, SINK_COUNT>(P, d_segs, nsegs, ntiles, st); break;
+    case SINK_MATERIALIZE: launch_scan_t<4, SINK_MATERIALIZE>(P, d_segs, d_tile_seg, ntiles, st); break;
+    case SINK_BUILD: launch_scan_t<4, SINK_BUILD>(P, d_segs, d_tile_seg, ntiles, st); break;
+    case SINK_PROBE: launch_scan_t<4, SINK_PROBE>(P, d_segs, d_tile_seg, ntiles, st); break;
+    case SINK_PROBE_GLOBAL: launch_scan_t<4, SINK_PROBE_GLOBAL>(P, d_segs, d_tile_seg, ntiles, st); break;
+    case SINK_COUNT: launch_scan_t<4, SINK_COUNT>(P, d_segs, d_tile_seg, ntiles, st); break;
   }
 }
 
@@ -438,9 +396,8 @@ __global__ void k_bloom_build(AggTableDev t, uint64_t cap) {
        s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t key = t.hot[s * t.hw];
     if (key == kEmptyKey) continue;
-    const uint64_t h = mix64(key ^ 0x5bd1e9955bd1e995ULL);
-    const uint32_t m = (1u << ((h >> 40) & 31)) | (1u << ((h >> 46) & 31)) | (1u << ((h >> 52) & 31));
-    atomicOr(t.bloom + (h & t.bloom_mask), m);
+    const uint64_t h2 = key * kBloomMul;
+    atomicOr(t.bloom + (h2 >> t.bloom_shift), bloom_bits(h2, t.bloom_shift));
   }
 }
 void launch_bloom_build(const AggTableDev& t, uint64_t cap, void* stream) {
@@ -462,7 +419,7 @@ void launch_local_init(uint64_t* keys, uint32_t* cnt, uint64_t cap, void* stream
   k_local_init<<<grid_for(cap + 1, 256), 256, 0, S(stream)>>>(keys, cnt, cap);
 }
 
-__global__ void k_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, const uint64_t* bk, uint64_t n,
+__global__ void k_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, int shift, const uint64_t* bk, uint64_t n,
                               unsigned int* max_cnt) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -471,7 +428,7 @@ __global__ void k_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, cons
     if (key == kEmptyKey) {
       s = mask + 1;
     } else {
-      s = mix64(key) & mask;
+      s = slot_of(key, shift);
       while (true) {
         const unsigned long long prev =
             atomicCAS(reinterpret_cast<unsigned long long*>(keys + s), kEmptyKey, key);
@@ -483,11 +440,11 @@ __global__ void k_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, cons
     atomicMax(max_cnt, old + 1);
   }
 }
-void launch_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, const uint64_t* bk, uint64_t n,
+void launch_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, int shift, const uint64_t* bk, uint64_t n,
                         unsigned int* max_cnt, void* stream) {
   if (n == 0) return;
   count_launch();
-  k_local_count<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, cnt, mask, bk, n, max_cnt);
+  k_local_count<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, cnt, mask, shift, bk, n, max_cnt);
 }
 
 struct ColPtrs {
@@ -497,7 +454,7 @@ struct OutPtrs {
   uint64_t* p[kMaxIn + kMaxPayload];
 };
 
-__global__ void k_local_fill(const uint64_t* keys, const uint32_t* start, uint32_t* cursor, uint64_t mask,
+__global__ void k_local_fill(const uint64_t* keys, const uint32_t* start, uint32_t* cursor, uint64_t mask, int shift,
                              const uint64_t* bk, ColPtrs src, OutPtrs dst, int ncols, uint64_t n) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -506,14 +463,14 @@ __global__ void k_local_fill(const uint64_t* keys, const uint32_t* start, uint32
     if (key == kEmptyKey) {
       s = mask + 1;
     } else {
-      s = mix64(key) & mask;
+      s = slot_of(key, shift);
       while (keys[s] != key) s = (s + 1) & mask;
     }
     const uint64_t pos = start[s] + atomicAdd(cursor + s, 1u);
     for (int c = 0; c < ncols; ++c) dst.p[c][pos] = src.p[c][i];
   }
 }
-void launch_local_fill(const uint64_t* keys, const uint32_t* start, uint32_t* cursor, uint64_t mask,
+void launch_local_fill(const uint64_t* keys, const uint32_t* start, uint32_t* cursor, uint64_t mask, int shift,
                        const uint64_t* bk, const uint64_t* const* src_cols, uint64_t* const* dst_cols, int ncols,
                        uint64_t n, void* stream) {
   if (n == 0) return;
@@ -524,7 +481,7 @@ void launch_local_fill(const uint64_t* keys, const uint32_t* start, uint32_t* cu
     d.p[c] = dst_cols[c];
   }
   count_launch();
-  k_local_fill<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, start, cursor, mask, bk, s, d, ncols, n);
+  k_local_fill<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, start, cursor, mask, shift, bk, s, d, ncols, n);
 }
 
 size_t exclusive_scan_u32(const uint32_t* in, uint32_t* out, uint64_t n, void* tmp, size_t tmp_bytes, void* stream) {

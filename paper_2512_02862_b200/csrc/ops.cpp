@@ -4,6 +4,7 @@
 #include <numeric>
 
 #include "engine.hpp"
+#include "jit.hpp"
 
 namespace psg {
 
@@ -72,8 +73,9 @@ HostBatch op_filter(Ctx& ctx, const HostBatch& in, const Predicate& pred) {
   sg.tile_begin = 0;
   const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
   const uint64_t ntiles = (n + T - 1) / T;
-  DevBuf dseg(ctx.pool, sizeof(Segment), ctx.compute);
+  DevBuf dseg(ctx.pool, sizeof(Segment), ctx.compute), dtile(ctx.pool, ntiles * 4, ctx.compute);
   PSG_CUDA(cudaMemcpyAsync(dseg.p, &sg, sizeof sg, cudaMemcpyHostToDevice, ctx.compute));
+  PSG_CUDA(cudaMemsetAsync(dtile.p, 0, ntiles * 4, ctx.compute));  // single segment
   ScanProgram p;
   std::memset(&p, 0, sizeof p);
   p.n_in = nc;
@@ -102,7 +104,7 @@ HostBatch op_filter(Ctx& ctx, const HostBatch& in, const Predicate& pred) {
   ScanProgram pc = p;
   pc.sink = SINK_COUNT;
   pc.tile_counts = counts.as<unsigned long long>();
-  launch_scan(pc, dseg.as<Segment>(), 1, ntiles, 0, ctx.compute);
+  fused_scan(pc, dseg.as<Segment>(), dtile.as<uint32_t>(), 1, ntiles, ctx.compute);
   size_t tb = exclusive_scan_u64(nullptr, nullptr, ntiles + 1, nullptr, 0, ctx.compute);
   DevBuf tmp(ctx.pool, tb, ctx.compute);
   exclusive_scan_u64(counts.as<unsigned long long>(), offs.as<unsigned long long>(), ntiles + 1, tmp.p, tb, ctx.compute);
@@ -122,7 +124,7 @@ HostBatch op_filter(Ctx& ctx, const HostBatch& in, const Predicate& pred) {
   pm.tile_offsets = offs.as<uint64_t>();
   DevBuf cnt(ctx.pool, 8, ctx.compute);
   pm.out_count = cnt.as<unsigned long long>();
-  launch_scan(pm, dseg.as<Segment>(), 1, ntiles, 0, ctx.compute);
+  fused_scan(pm, dseg.as<Segment>(), dtile.as<uint32_t>(), 1, ntiles, ctx.compute);
   for (int c = 0; c < nc; ++c) out.cols[c] = download(ctx, oc[c], total);
   PSG_CUDA(cudaStreamSynchronize(ctx.compute));
   return out;
@@ -204,7 +206,9 @@ HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& buil
   PSG_CUDA(cudaMemsetAsync(cursor.p, 0, (cap + 1) * 4, ctx.compute));
   PSG_CUDA(cudaMemsetAsync(maxc.p, 0, 4, ctx.compute));
   launch_local_init(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap, ctx.compute);
-  launch_local_count(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap - 1, ub.cols[bk].as<uint64_t>(), nb, maxc.as<unsigned>(),
+  int shift = 64;
+  for (uint64_t c = cap; c > 1; c >>= 1) --shift;
+  launch_local_count(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap - 1, shift, ub.cols[bk].as<uint64_t>(), nb, maxc.as<unsigned>(),
                      ctx.compute);
   size_t tb = exclusive_scan_u32(nullptr, nullptr, cap + 1, nullptr, 0, ctx.compute);
   DevBuf tmp(ctx.pool, tb, ctx.compute);
@@ -218,13 +222,14 @@ HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& buil
     src.push_back(ub.cols[c].as<uint64_t>());
     dst.push_back(payload.back().as<uint64_t>());
   }
-  launch_local_fill(keys.as<uint64_t>(), start.as<uint32_t>(), cursor.as<uint32_t>(), cap - 1, ub.cols[bk].as<uint64_t>(),
+  launch_local_fill(keys.as<uint64_t>(), start.as<uint32_t>(), cursor.as<uint32_t>(), cap - 1, shift, ub.cols[bk].as<uint64_t>(),
                     src.data(), dst.data(), np, nb, ctx.compute);
   LocalTableDev t{};
   t.keys = keys.as<uint64_t>();
   t.cnt = cnt.as<uint32_t>();
   t.start = start.as<uint32_t>();
   t.mask = cap - 1;
+  t.shift = shift;
   t.npayload = np;
   for (int k = 0; k < np; ++k) t.payload[k] = payload[k].as<uint64_t>();
   DevBuf counts(ctx.pool, (npr + 1) * 4, ctx.compute), offs(ctx.pool, (npr + 1) * 4, ctx.compute);

@@ -81,3 +81,9 @@ def test_corrupt_footer_raises(tmp_path):
     with pytest.raises(psg.PsgError) as e:
         psg.inspect(str(tmp_path / "missing.psto"))
     assert e.value.kind == "IoFailure"
+
+
+def test_query_compiler_builds_every_sink_for_sm100a():
+    """NVRTC specialisation of the fused scan (jit.cpp) compiles for sm_100a without a GPU."""
+    failures, log = psg.jit_selftest()
+    assert failures == 0, log
