@@ -279,11 +279,13 @@ def main():
     sync_all()
     e2e_t, h2d, d2h = [], 0, 0
     e2e_rows = 0
+    io_wait = []
     for _ in range(e2e_steps):
         t = time.time()
         res = ctx.execute_plan(plan, data_root)
         e2e_t.append(time.time() - t)
         h2d, d2h = res.stats["ingest_bytes"], res.stats["result_bytes"]
+        io_wait.append(res.stats["io_wait_s"])
         e2e_rows = res.rows.shape[0]
     sync_all()
     e2e_s = max_over_ranks(statistics.mean(e2e_t)) if e2e_t else None
@@ -335,6 +337,8 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_s, 4) if e2e_s else None, "unit": "s", "h2d_bytes_per_step": int(h2d_all),
                     "d2h_bytes_per_step": int(d2h_all), "steps": e2e_steps, "groups": int(e2e_groups),
+                    "io_wait_s": round(statistics.mean(io_wait), 4) if io_wait else None,
+                    "ingest_gbs": round(h2d_all / 1e9 / e2e_s, 2) if e2e_s else None,
                     "path": "psg_execute_plan: PSTO files (warm page cache) -> pinned -> HBM -> rows to host"},
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -96,6 +96,8 @@ typedef struct psg_stats {
   uint64_t probe_kernel_bytes; /* algorithmic bytes (input column chunks) those launches scanned */
   double device_ms;            /* CUDA-event time on the engine's compute stream, first to last op */
   uint64_t result_rows;        /* rows of this rank's result (also when rows stay on the device) */
+  double io_wait_s;            /* host time the control thread waited for storage reads */
+  uint64_t jit_compiles;       /* NVRTC kernel compilations during this call (cached afterwards) */
 } psg_stats;
 
 /* ---- library ---- */

@@ -51,7 +51,8 @@ class Stats(ctypes.Structure):
                 ("result_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
                 ("waves", ctypes.c_uint64), ("probe_kernel_ms", ctypes.c_double),
                 ("probe_kernel_launches", ctypes.c_uint64), ("probe_kernel_bytes", ctypes.c_uint64),
-                ("device_ms", ctypes.c_double), ("result_rows", ctypes.c_uint64)]
+                ("device_ms", ctypes.c_double), ("result_rows", ctypes.c_uint64), ("io_wait_s", ctypes.c_double),
+                ("jit_compiles", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -151,6 +152,15 @@ def _make_batch(columns: dict, types: dict | None = None):
     return b
 
 
+class _View:
+    """Array-interface wrapper whose lifetime pins the owning Result (numpy keeps it as .base)."""
+
+    def __init__(self, owner, ptr, n):
+        self._owner = owner
+        self.__array_interface__ = {"shape": (n,), "typestr": "<u8", "version": 3,
+                                    "data": (ctypes.cast(ptr, ctypes.c_void_p).value, False)}
+
+
 class Result:
     """PipelineResult (pipeline.hpp:138-149): schema + rows of raw u64 words (row-major ndarray)."""
 
@@ -165,12 +175,25 @@ class Result:
             self.schema.append((nm.value.decode(), "float64" if ty.value == 1 else "int64"))
         cnt = n.value * k.value
         ptr = L.psg_result_data(handle)
-        self.rows = np.ctypeslib.as_array(ptr, shape=(cnt,)).copy().reshape(n.value, k.value) if cnt else \
-            np.zeros((n.value, k.value), np.uint64)
         st = Stats()
         _check(L.psg_result_stats(handle, ctypes.byref(st)))
         self.stats = st.as_dict()
-        L.psg_result_free(handle)
+        if cnt:
+            # zero-copy view of the engine's (pinned) result rows; freed with this object
+            self._h = handle
+            self.rows = np.asarray(_View(self, ptr, cnt)).reshape(n.value, k.value)
+        else:
+            self.rows = np.zeros((n.value, k.value), np.uint64)
+            self._h = None
+            L.psg_result_free(handle)
+
+    def __del__(self):
+        try:
+            if self._h is not None:
+                lib().psg_result_free(self._h)
+                self._h = None
+        except Exception:
+            pass
 
     def column(self, name):
         i = [n for n, _t in self.schema].index(name)

@@ -228,7 +228,7 @@ int psg_result_field(const psg_result* r, uint32_t col, const char** name, int* 
   });
 }
 
-const uint64_t* psg_result_data(const psg_result* r) { return r ? r->r.words.data() : nullptr; }
+const uint64_t* psg_result_data(const psg_result* r) { return r ? r->r.data() : nullptr; }
 
 int psg_result_stats(const psg_result* r, psg_stats* out) {
   return guarded([&] {

@@ -152,17 +152,32 @@ __device__ __forceinline__ bool bloom_maybe(const AggTableDev& t, uint64_t key) 
   return (w & m) == m;
 }
 
-__device__ __forceinline__ uint64_t agg_insert_from(const AggTableDev& t, uint64_t key, uint64_t s) {
+/// Claims key's slot from s on; `dup` = the key was already present (another build row).
+__device__ __forceinline__ uint64_t agg_insert_from(const AggTableDev& t, uint64_t key, uint64_t s, bool& dup) {
   while (true) {
     unsigned long long* kp = reinterpret_cast<unsigned long long*>(t.hot + s * t.hw);
     const unsigned long long prev = atomicCAS(kp, kEmptyKey, key);
-    if (prev == kEmptyKey || prev == key) return s;
+    if (prev == kEmptyKey || prev == key) {
+      dup = prev == key;
+      return s;
+    }
     s = (s + 1) & t.mask;
   }
 }
-__device__ __forceinline__ uint64_t agg_insert(const AggTableDev& t, uint64_t key) {
-  if (key == kEmptyKey) return t.mask + 1;
-  return agg_insert_from(t, key, slot_of(key, t.shift));
+/// Build multiplicity m of an occupied slot: cold[0] counts duplicates (m - 1) so unique build
+/// keys never touch the cold array; the kEmptyKey spill slot counts m directly.
+__device__ __forceinline__ uint64_t agg_mult(const AggTableDev& t, uint64_t slot) {
+  const uint64_t c = t.cold[slot * t.cw];
+  return slot == t.mask + 1 ? c : c + 1;
+}
+/// Records one build row of key in slot (after agg_insert_from): duplicate count + Bloom bits.
+__device__ __forceinline__ void agg_count_build(const AggTableDev& t, uint64_t key, uint64_t slot, bool dup) {
+  if (slot == t.mask + 1 || dup) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(t.cold + slot * t.cw), 1ULL);
+  } else if (t.bloom != nullptr) {
+    const uint64_t h2 = key * kBloomMul;
+    atomicOr(t.bloom + (h2 >> t.bloom_shift), bloom_bits(h2, t.bloom_shift));
+  }
 }
 /// Linear probe from slot s whose key k0 was already loaded; UINT64_MAX when absent.
 __device__ __forceinline__ uint64_t agg_lookup_from(const AggTableDev& t, uint64_t key, uint64_t s, uint64_t k0) {

@@ -22,6 +22,7 @@
 #include <numeric>
 #include <cstdio>
 #include <cstdlib>
+#include <deque>
 #include <set>
 
 #include "engine.hpp"
@@ -52,6 +53,18 @@ bool trace_on() {
       std::fputc('\n', stderr);             \
     }                                       \
   } while (0)
+struct PhaseTimer {
+  Clock::time_point t0 = Clock::now(), last = t0;
+  void mark(const char* what, cudaStream_t s) {
+    if (!trace_on()) return;
+    cudaStreamSynchronize(s);
+    const auto now = Clock::now();
+    std::fprintf(stderr, "[psg] %-28s %8.3f ms (total %8.3f)\n", what,
+                 std::chrono::duration<double, std::milli>(now - last).count(),
+                 std::chrono::duration<double, std::milli>(now - t0).count());
+    last = now;
+  }
+};
 double secs_since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
 
 uint64_t pow2_at_least(uint64_t x) {
@@ -366,6 +379,7 @@ std::string scan_key(const ScanNode& s, const std::vector<int>& file_cols) {
 }
 
 // ------------------------------------------------------------------------ the executor
+struct StreamSession;
 class Execution {
  public:
   struct Feed;
@@ -436,10 +450,15 @@ class Execution {
   uint64_t agg_cap_ = 0;
   // stats
   psg_stats st_{};
-  uint64_t launches0_ = 0;
+  uint64_t launches0_ = 0, jit0_ = 0;
   std::vector<std::string> files_;
   std::map<std::string, int> file_index_;
   std::vector<DevBuf> keep_;  // buffers that must live until the end
+  std::vector<std::vector<uint8_t>> host_keep_;  // host sources of in-flight async copies
+  std::unique_ptr<StreamSession> session_;
+  /// (scan, file columns) of every scan in consumption order: replicated scans of the build
+  /// chain, of the probe chain, then the shuffle build and probe sources.
+  std::vector<std::pair<const ScanNode*, std::vector<int>>> scan_list(const RegMap& bm, const RegMap& pm);
 };
 
 // ------------------------------------------------------------------------------ feeds
@@ -451,52 +470,84 @@ struct Execution::Feed {
   size_t nbatches = 0;
 };
 
-/// Streams batches from storage through the pinned ring into a ring of HBM slots.
-struct StreamFeed : Execution::Feed {
+/// One ingest session per query: every batch of every scan the query streams (in consumption
+/// order: replicated scans, shuffle build side, probe side) goes through one I/O pool, one pinned
+/// ring and one ring of HBM slots, so reads of the next scan overlap the processing of the
+/// current one (the reference's reader combining, scan.cpp:22-93, without phase bubbles).
+struct StreamSession {
   Ctx& ctx;
-  ScanBatches sb;
   std::vector<std::string> files;
+  std::map<std::string, int> file_index;
+  std::vector<BatchPlan> batches;
+  struct Range {
+    size_t begin = 0, end = 0;
+    uint64_t rows = 0;
+  };
+  std::map<std::string, std::deque<Range>> ranges;  // scan_key -> batch ranges in consumption order
   std::unique_ptr<Ingest> ingest;
   std::vector<DevBuf> slots;
   std::vector<cudaEvent_t> slot_free, copied;
-  std::vector<uint64_t> tiles;
   uint64_t slot_bytes = 0;
-  size_t i = 0;
+  size_t cursor = 0;  // next batch to consume (global order)
   int cur_slot = -1;
-  StreamFeed(Ctx& c, const ScanNode& scan, const std::vector<int>& file_cols, FooterCache& fc) : ctx(c) {
-    sb = plan_batches(fc, scan, file_cols, 0, ctx.batch_bytes);
-    files = scan.paths;
-    total_rows = sb.total_rows;
-    nbatches = sb.batches.size();
-    if (sb.batches.empty()) return;
+
+  StreamSession(Ctx& c, const std::vector<std::pair<const ScanNode*, std::vector<int>>>& scans) : ctx(c) {
+    uint64_t max_bytes = 0, max_segs = 0;
+    for (auto& [scan, fcols] : scans) {
+      const std::string key = scan_key(*scan, fcols);
+      // union file list; plan this scan's batches against it
+      std::vector<int> idx;
+      for (auto& path : scan->paths) {
+        auto it = file_index.find(path);
+        if (it == file_index.end()) {
+          it = file_index.emplace(path, static_cast<int>(files.size())).first;
+          files.push_back(path);
+        }
+        idx.push_back(it->second);
+      }
+      ScanBatches sb = plan_batches(ctx.footers, *scan, fcols, 0, ctx.batch_bytes);
+      Range r;
+      r.begin = batches.size();
+      for (auto& bp : sb.batches) {
+        bp.file = idx[bp.file];
+        batches.push_back(std::move(bp));
+      }
+      r.end = batches.size();
+      r.rows = sb.total_rows;
+      ranges[key].push_back(r);
+      max_bytes = std::max(max_bytes, sb.max_batch_bytes);
+      max_segs = std::max(max_segs, sb.max_segs);
+    }
+    if (batches.empty()) return;
     const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
-    const uint64_t max_tiles = std::max(sb.max_batch_bytes, ctx.batch_bytes) / 8 / T + sb.max_segs + 1;
-    slot_bytes = (std::max(sb.max_batch_bytes, ctx.batch_bytes) + sb.max_segs * sizeof(Segment) + max_tiles * 4 + 4096 +
-                  4095) & ~4095ULL;
+    const uint64_t cap = std::max(max_bytes, ctx.batch_bytes);
+    const uint64_t max_tiles = cap / 8 / T + max_segs + 1;
+    slot_bytes = (cap + max_segs * sizeof(Segment) + max_tiles * 4 + 4096 + 4095) & ~4095ULL;
     const int threads = std::max(1, ctx.io_threads);
     const int pinned = ctx.pinned_slots > 0 ? ctx.pinned_slots : threads * 2 + 2;
-    ingest = std::make_unique<Ingest>(ctx, files, sb.batches, threads, slot_bytes, pinned);
-    const int nd = static_cast<int>(std::min<size_t>(sb.batches.size(), 6));
+    ingest = std::make_unique<Ingest>(ctx, files, batches, threads, slot_bytes, pinned);
+    const int nd = static_cast<int>(std::min<size_t>(batches.size(), 8));
     for (int k = 0; k < nd; ++k) {
       slots.emplace_back(ctx.pool, slot_bytes, ctx.copy);
-      cudaEvent_t a, b;
-      PSG_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
-      PSG_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
-      slot_free.push_back(a);
-      copied.push_back(b);
+      cudaEvent_t x, y;
+      PSG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+      PSG_CUDA(cudaEventCreateWithFlags(&y, cudaEventDisableTiming));
+      slot_free.push_back(x);
+      copied.push_back(y);
     }
   }
-  ~StreamFeed() override {
+  ~StreamSession() {
     cudaStreamSynchronize(ctx.copy);
     cudaStreamSynchronize(ctx.compute);
     ingest.reset();
-    for (auto e : slot_free) cudaEventDestroy(e);
-    for (auto e : copied) cudaEventDestroy(e);
+    for (auto x : slot_free) cudaEventDestroy(x);
+    for (auto x : copied) cudaEventDestroy(x);
   }
-  bool next(BatchView& v) override {
-    if (i >= sb.batches.size()) return false;
+  /// Stages batch i (must be the next in consumption order) into its HBM ring slot.
+  void stage(size_t i, BatchView& v) {
+    if (i != cursor) throw Error(PSG_ERR_INTERNAL, "ingest batches consumed out of order");
     const int k = static_cast<int>(i % slots.size());
-    const BatchPlan& b = sb.batches[i];
+    const BatchPlan& b = batches[i];
     auto* base = slots[k].as<uint8_t>();
     uint64_t nt = 0;
     auto segs = make_segments(b, base, nt);
@@ -513,12 +564,26 @@ struct StreamFeed : Execution::Feed {
     v.rows = b.total_rows;
     v.bytes = b.bytes;
     cur_slot = k;
-    ++i;
-    return true;
+    ++cursor;
   }
-  void done() override {
+  void release() {
     if (cur_slot >= 0) PSG_CUDA(cudaEventRecord(slot_free[cur_slot], ctx.compute));
   }
+};
+
+struct SessionFeed : Execution::Feed {
+  StreamSession& ss;
+  size_t i, end;
+  SessionFeed(StreamSession& s, const StreamSession::Range& r) : ss(s), i(r.begin), end(r.end) {
+    total_rows = r.rows;
+    nbatches = r.end - r.begin;
+  }
+  bool next(BatchView& v) override {
+    if (i >= end) return false;
+    ss.stage(i++, v);
+    return true;
+  }
+  void done() override { ss.release(); }
 };
 
 /// One batch covering a scan's staged HBM image.
@@ -549,7 +614,13 @@ std::unique_ptr<Execution::Feed> Execution::open_feed(const ScanNode& scan, cons
     if (it == staged_->scans.end()) throw InvalidInput("staged data does not cover scan " + scan.table);
     return std::make_unique<StagedFeed>(&it->second);
   }
-  return std::make_unique<StreamFeed>(ctx_, scan, file_cols, ctx_.footers);
+  if (!session_) throw Error(PSG_ERR_INTERNAL, "no ingest session");
+  auto it = session_->ranges.find(scan_key(scan, file_cols));
+  if (it == session_->ranges.end() || it->second.empty())
+    throw Error(PSG_ERR_INTERNAL, "scan not planned in the ingest session");
+  auto r = it->second.front();
+  it->second.pop_front();
+  return std::make_unique<SessionFeed>(*session_, r);
 }
 
 // ------------------------------------------------------------------------------ compile
@@ -712,8 +783,7 @@ BatchView Execution::upload_segments(std::vector<Segment> segs, DevBuf& holder) 
   auto blob = pack_view(segs, toff);
   holder = DevBuf(ctx_.pool, blob.size(), ctx_.compute);
   PSG_CUDA(cudaMemcpyAsync(holder.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, ctx_.compute));
-  // keep host copy alive until the async copy is done
-  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  host_keep_.push_back(std::move(blob));  // pageable source must outlive the async copy
   v.d_segs = holder.as<Segment>();
   v.d_tile_seg = reinterpret_cast<const uint32_t*>(holder.as<uint8_t>() + toff);
   v.nsegs = static_cast<int>(segs.size());
@@ -891,19 +961,24 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
 void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
   const uint64_t nslots = agg_cap_ + 1;
   DevBuf keys(ctx_.pool, nslots * 8, ctx_.compute), slots(ctx_.pool, nslots * 8, ctx_.compute);
-  DevBuf counter(ctx_.pool, 8, ctx_.compute);
-  PSG_CUDA(cudaMemsetAsync(counter.p, 0, 8, ctx_.compute));
+  DevBuf counter(ctx_.pool, 24, ctx_.compute);
+  const uint64_t init[3] = {0, ~0ULL, 0};
+  PSG_CUDA(cudaMemcpyAsync(counter.p, init, 24, cudaMemcpyHostToDevice, ctx_.compute));
   launch_agg_compact(aggt_, agg_cap_, keys.as<uint64_t>(), slots.as<unsigned long long>(),
                      counter.as<unsigned long long>(), ctx_.compute);
-  uint64_t ng = 0;
-  PSG_CUDA(cudaMemcpyAsync(&ng, counter.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
+  uint64_t cnt[3] = {0, 0, 0};
+  PSG_CUDA(cudaMemcpyAsync(cnt, counter.p, 24, cudaMemcpyDeviceToHost, ctx_.compute));
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  const uint64_t ng = cnt[0];
+  // radix-sort only the key bits that vary: every key lies in [min, max] and shares their prefix
+  int end_bit = 1;
+  if (ng > 1 && cnt[1] != cnt[2]) end_bit = 64 - __builtin_clzll(cnt[1] ^ cnt[2]);
   DevBuf k2(ctx_.pool, std::max<uint64_t>(ng, 1) * 8, ctx_.compute), s2(ctx_.pool, std::max<uint64_t>(ng, 1) * 8, ctx_.compute);
-  size_t tb = sort_pairs_i64(nullptr, nullptr, nullptr, nullptr, ng, nullptr, 0, ctx_.compute);
+  size_t tb = sort_pairs_i64(nullptr, nullptr, nullptr, nullptr, ng, end_bit, nullptr, 0, ctx_.compute);
   DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
   if (ng)
     sort_pairs_i64(keys.as<uint64_t>(), k2.as<uint64_t>(), slots.as<unsigned long long>(), s2.as<unsigned long long>(), ng,
-                   tmp.p, tb, ctx_.compute);
+                   end_bit, tmp.p, tb, ctx_.compute);
   const int nc = static_cast<int>(result_schema_.size());
   std::vector<int32_t> kind, idx;
   kind.push_back(0), idx.push_back(0);
@@ -917,8 +992,8 @@ void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
                   ctx_.compute);
   out.nrows = ng;
   if (want_rows) {
-    out.words.resize(ng * nc);
-    if (ng) PSG_CUDA(cudaMemcpyAsync(out.words.data(), rows.p, ng * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    uint64_t* dst = out.mutable_rows(ng * nc);
+    if (ng) PSG_CUDA(cudaMemcpyAsync(dst, rows.p, ng * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
     st_.result_bytes += ng * nc * 8;
   }
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
@@ -943,6 +1018,7 @@ void Execution::finalize_global(ResultRows& out) {
 ResultRows Execution::run(bool want_rows) {
   const auto t0 = Clock::now();
   launches0_ = kernel_launch_count();
+  jit0_ = jit_stats().compiles;
   ctx_.pool.reset_peak();
   if (plan_.memory_budget_bytes) ctx_.pool.set_budget(ctx_.pool.used() + plan_.memory_budget_bytes);
   PSG_TRACE_MSG("run: compile");
@@ -974,10 +1050,12 @@ ResultRows Execution::run(bool want_rows) {
   for (size_t j = 0; j < bsrc_.chain.size(); ++j) bsrc_.chain[j].needed_payload = bm.payload_cols[j];
   for (size_t j = 0; j < psrc_.chain.size(); ++j) psrc_.chain[j].needed_payload = pm.payload_cols[j];
 
+  if (!staged_) session_ = std::make_unique<StreamSession>(ctx_, scan_list(bm, pm));
   const auto t_storage = Clock::now();
-  PSG_TRACE_MSG("run: local tables");
+  PhaseTimer pt;
+  pt.mark("compile", ctx_.compute);
   build_local_tables();
-  PSG_TRACE_MSG("run: build side");
+  pt.mark("local tables", ctx_.compute);
   for (auto& t : bl_tables_)
     if (!t->unique) throw InvalidInput("local join build side with duplicate keys is not supported by the fused path yet");
   for (auto& t : pl_tables_)
@@ -1021,6 +1099,7 @@ ResultRows Execution::run(bool want_rows) {
       brecv.push_back(exchange(mat, static_cast<int>(b_out.size()), 0, pc, have));
     }
   }
+  pt.mark("build side scan", ctx_.compute);
   uint64_t build_rows = 0;
   if (nr == 1) build_rows = bmat.rows;
   else
@@ -1061,8 +1140,7 @@ ResultRows Execution::run(bool want_rows) {
     p.agg = aggt_;
     p.n_sum = static_cast<int>(build_sum_wire.size());
     for (int b = 0; b < p.n_sum; ++b) p.sum_reg[b] = 1 + b;
-    run_scan(p, bview, false);
-    launch_bloom_build(aggt_, agg_cap_, ctx_.compute);
+    run_scan(p, bview, false);  // also sets the Bloom bits of every inserted key
     if (!grouped_) {
       global_acc_ = DevBuf(ctx_.pool, (2 * kMaxSums + 1) * 8, ctx_.compute);
       PSG_CUDA(cudaMemsetAsync(global_acc_.p, 0, (2 * kMaxSums + 1) * 8, ctx_.compute));
@@ -1113,7 +1191,7 @@ ResultRows Execution::run(bool want_rows) {
   brecv.clear();
   bmat = DevCols{};
 
-  PSG_TRACE_MSG("run: probe side (build rows %llu)", static_cast<unsigned long long>(build_rows));
+  pt.mark("build table", ctx_.compute);
   // ---------------- probe side ----------------
   ScanProgram pp = base_program(psrc_, pm, true);
   std::vector<int> p_out;
@@ -1228,7 +1306,7 @@ ResultRows Execution::run(bool want_rows) {
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   st_.storage_phase_s = secs_since(t_storage);
 
-  PSG_TRACE_MSG("run: finalize");
+  pt.mark("probe side", ctx_.compute);
   // ---------------- finalize ----------------
   if (agg_) {
     if (grouped_) finalize_grouped(out, want_rows);
@@ -1239,7 +1317,7 @@ ResultRows Execution::run(bool want_rows) {
     for (auto& j : joined_parts) total += j.rows;
     out.nrows = total;
     if (want_rows) {
-      out.words.resize(total * nc);
+      uint64_t* dst = out.mutable_rows(total * nc);
       uint64_t at = 0;
       for (auto& j : joined_parts) {
         if (!j.rows) continue;
@@ -1254,7 +1332,7 @@ ResultRows Execution::run(bool want_rows) {
           cols.push_back(j.cols[npay + at].as<uint64_t>());
         }
         launch_rows_from_cols(cols.data(), nc, j.rows, rows.as<uint64_t>(), ctx_.compute);
-        PSG_CUDA(cudaMemcpyAsync(out.words.data() + at * nc, rows.p, j.rows * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+        PSG_CUDA(cudaMemcpyAsync(dst + at * nc, rows.p, j.rows * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
         PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
         at += j.rows;
       }
@@ -1263,6 +1341,7 @@ ResultRows Execution::run(bool want_rows) {
   }
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   PSG_CUDA(cudaGetLastError());
+  pt.mark("finalize", ctx_.compute);
   PSG_CUDA(cudaEventRecord(ev1, ctx_.compute));
   PSG_CUDA(cudaEventSynchronize(ev1));
   float dms = 0;
@@ -1270,6 +1349,8 @@ ResultRows Execution::run(bool want_rows) {
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   st_.device_ms = dms;
+  if (session_ && session_->ingest) st_.io_wait_s = session_->ingest->wait_s();
+  st_.jit_compiles = jit_stats().compiles - jit0_;
   st_.result_rows = out.nrows;
   st_.runtime_s = secs_since(t0);
   st_.peak_bytes = ctx_.pool.peak();
@@ -1277,6 +1358,31 @@ ResultRows Execution::run(bool want_rows) {
   out.stats = st_;
   if (plan_.memory_budget_bytes) ctx_.pool.set_budget(0);
   return out;
+}
+
+std::vector<std::pair<const ScanNode*, std::vector<int>>> Execution::scan_list(const RegMap& bm, const RegMap& pm) {
+  std::vector<std::pair<const ScanNode*, std::vector<int>>> scans;
+  for (int side = 0; side < 2; ++side) {
+    SourceDef& s = side == 0 ? bsrc_ : psrc_;
+    const RegMap& m = side == 0 ? bm : pm;
+    for (size_t j = 0; j < s.chain.size(); ++j) {
+      LocalJoinDef& lj = s.chain[j];
+      SourceDef rs;
+      rs.scan = lj.scan;
+      rs.proj = lj.proj;
+      rs.wire = lj.proj.schema;
+      std::vector<ColRef> refs;
+      for (size_t i = 0; i < rs.wire.size(); ++i) refs.push_back({-1, static_cast<int>(i)});
+      rs.stage_refs.push_back(refs);
+      std::vector<int> needed{lj.key_idx};
+      for (int p : m.payload_cols[j]) needed.push_back(lj.payload_idx[p]);
+      RegMap rm = analyse(rs, needed, -1, false);
+      scans.push_back({lj.scan, file_cols_of(rs, rm)});
+    }
+  }
+  scans.push_back({bsrc_.scan, file_cols_of(bsrc_, bm)});
+  scans.push_back({psrc_.scan, file_cols_of(psrc_, pm)});
+  return scans;
 }
 
 void Execution::stage(Staged& st) {
@@ -1295,26 +1401,7 @@ void Execution::stage(Staged& st) {
   }
   RegMap bm = analyse(bsrc_, bneed, bkey, true);
   RegMap pm = analyse(psrc_, pneed, pkey, true);
-  std::vector<std::pair<const ScanNode*, std::vector<int>>> scans;
-  for (int side = 0; side < 2; ++side) {
-    SourceDef& s = side == 0 ? bsrc_ : psrc_;
-    RegMap& m = side == 0 ? bm : pm;
-    for (size_t j = 0; j < s.chain.size(); ++j) {
-      LocalJoinDef& lj = s.chain[j];
-      SourceDef rs;
-      rs.scan = lj.scan;
-      rs.proj = lj.proj;
-      rs.wire = lj.proj.schema;
-      std::vector<ColRef> refs;
-      for (size_t i = 0; i < rs.wire.size(); ++i) refs.push_back({-1, static_cast<int>(i)});
-      rs.stage_refs.push_back(refs);
-      std::vector<int> needed{lj.key_idx};
-      for (int p : m.payload_cols[j]) needed.push_back(lj.payload_idx[p]);
-      RegMap rm = analyse(rs, needed, -1, false);
-      scans.push_back({lj.scan, file_cols_of(rs, rm)});
-    }
-    scans.push_back({s.scan, file_cols_of(s, m)});
-  }
+  const auto scans = scan_list(bm, pm);
   for (auto& [scan, fcols] : scans) {
     const std::string key = scan_key(*scan, fcols);
     if (st.scans.count(key)) continue;

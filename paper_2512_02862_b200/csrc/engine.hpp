@@ -104,6 +104,7 @@ class Ingest {
   /// the payload, then enqueues the H2D copy of payload+extra to dst. Returns after enqueueing.
   void copy_to_device(size_t i, void* dst, const void* extra, size_t extra_bytes, cudaStream_t copy_stream);
   uint64_t bytes_read() const { return bytes_read_; }
+  double wait_s() const { return wait_s_; }
 
  private:
   struct Slot {
@@ -128,6 +129,7 @@ class Ingest {
   bool stop_ = false;
   std::string error_;
   uint64_t bytes_read_ = 0;
+  double wait_s_ = 0;
   std::vector<std::thread> threads_;
   struct CopyDone {
     Ingest* self;
@@ -155,11 +157,35 @@ struct Ctx {
   ~Ctx();
 };
 
+/// Process-wide cache of pinned host blocks for result rows: D2H at full PCIe speed without
+/// re-pinning (cudaHostAlloc of ~400 MB costs more than the copy) and without zero-filling.
+class PinnedBlock {
+ public:
+  static std::shared_ptr<PinnedBlock> get(size_t bytes);
+  ~PinnedBlock();
+  void* data() const { return p_; }
+  size_t bytes() const { return n_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t n_ = 0;
+};
+
 struct ResultRows {
   Schema schema;
-  std::vector<uint64_t> words;  // row-major
+  std::vector<uint64_t> words;          // row-major (small results)
+  std::shared_ptr<PinnedBlock> pinned;  // row-major (large results), takes precedence
   uint64_t nrows = 0;
   psg_stats stats{};
+  uint64_t* mutable_rows(uint64_t nwords) {
+    if (nwords * 8 >= (1u << 20)) {
+      pinned = PinnedBlock::get(nwords * 8);
+      return static_cast<uint64_t*>(pinned->data());
+    }
+    words.resize(nwords);
+    return words.data();
+  }
+  const uint64_t* data() const { return pinned ? static_cast<const uint64_t*>(pinned->data()) : words.data(); }
 };
 
 struct Staged;  // HBM-resident file images (psg_stage_plan)

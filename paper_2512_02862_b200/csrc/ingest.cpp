@@ -3,6 +3,8 @@
 #include <sys/stat.h>
 #include <unistd.h>
 
+#include <chrono>
+#include <map>
 #include <cstring>
 
 #include "engine.hpp"
@@ -39,6 +41,44 @@ void DevicePool::free(void* p, cudaStream_t s) {
   used_ -= it->second;
   live_.erase(it);
   cudaFreeAsync(p, s);
+}
+
+// ----------------------------------------------------------------------------- PinnedBlock
+namespace {
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;  // cached blocks by size
+size_t g_pin_cached = 0;
+constexpr size_t kPinCacheMax = 8ull << 30;
+}  // namespace
+
+std::shared_ptr<PinnedBlock> PinnedBlock::get(size_t bytes) {
+  bytes = (bytes + (1u << 20) - 1) & ~size_t((1u << 20) - 1);
+  auto b = std::shared_ptr<PinnedBlock>(new PinnedBlock());
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.lower_bound(bytes);
+    if (it != g_pin_free.end() && it->first <= 2 * bytes) {
+      b->n_ = it->first;
+      b->p_ = it->second;
+      g_pin_cached -= it->first;
+      g_pin_free.erase(it);
+      return b;
+    }
+  }
+  PSG_CUDA(cudaHostAlloc(&b->p_, bytes, cudaHostAllocDefault));
+  b->n_ = bytes;
+  return b;
+}
+
+PinnedBlock::~PinnedBlock() {
+  if (!p_) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (g_pin_cached + n_ <= kPinCacheMax) {
+    g_pin_free.emplace(n_, p_);
+    g_pin_cached += n_;
+  } else {
+    cudaFreeHost(p_);
+  }
 }
 
 // ----------------------------------------------------------------------------- FooterCache
@@ -166,8 +206,10 @@ void CUDART_CB Ingest::on_copied(void* arg) {
 void Ingest::copy_to_device(size_t i, void* dst, const void* extra, size_t extra_bytes, cudaStream_t copy_stream) {
   int slot;
   {
+    const auto t0 = std::chrono::steady_clock::now();
     std::unique_lock<std::mutex> lk(mu_);
     cv_.wait(lk, [&] { return !error_.empty() || (slot_of_batch_[i] >= 0 && slots_[slot_of_batch_[i]].ready); });
+    wait_s_ += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (!error_.empty()) throw IoFailure(error_);
     slot = slot_of_batch_[i];
   }

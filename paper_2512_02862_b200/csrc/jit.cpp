@@ -66,9 +66,10 @@ const char* op_str(int op) {
 /// Emits `for r: if (pass & bit) vC[r] = load(col c of the tile)` for columns [lo, hi).
 void emit_loads(std::ostringstream& s, int lo, int hi) {
   for (int c = lo; c < hi; ++c) {
-    s << "    { const uint64_t* col = s_col[b][" << c << "] + row0 + tid;\n"
+    s << "    { const uint64_t* col = reinterpret_cast<const uint64_t*>(__shfl_sync(0xffffffffu, "
+         "reinterpret_cast<unsigned long long>(cur_col), " << c << ")) + row0 + wrow;\n"
       << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (pass & (1u << r)) " << V(c)
-      << "[r] = __ldcs(reinterpret_cast<const unsigned long long*>(col + r * 256));\n    }\n";
+      << "[r] = __ldcs(reinterpret_cast<const unsigned long long*>(col + r * 32));\n    }\n";
   }
 }
 
@@ -82,38 +83,39 @@ std::string jit_source(const ScanProgram& P) {
   const bool part = P.sink == SINK_MATERIALIZE && P.nparts > 1;
   const bool glob = P.sink == SINK_PROBE_GLOBAL;
   const int nglob = glob ? 1 + P.n_sum + P.agg.nbs : 0;
+  // Block tiles of 1024 rows; warp w owns rows [128w, 128w+128) of the tile, lane-contiguous per
+  // r (each warp load = 256 contiguous bytes), so row order inside a tile is (warp, r, lane).
+  // Tile descriptors are fetched per warp into registers (lane c holds column c's pointer) and
+  // the next tile's descriptor is prefetched while the current one computes: no block barrier
+  // except the compaction prefix of the materialising sinks.
   s << "using namespace psg;\n#define R 4\n"
-    << "extern \"C\" __global__ void __launch_bounds__(256) psg_jit_scan(const __grid_constant__ ScanProgram P, "
-       "const Segment* __restrict__ segs, const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {\n"
-    << "  __shared__ const uint64_t* s_col[2][" << std::max(1, nin) << "];\n"
-    << "  __shared__ uint64_t s_row0[2], s_rows[2];\n";
-  if (mat) s << "  __shared__ uint32_t s_wcnt[R][8], s_woff[R][8];\n  __shared__ unsigned long long s_base;\n";
+    << "extern \"C\" __global__ void __launch_bounds__(256, " << (P.sink == SINK_MATERIALIZE || P.sink == SINK_COUNT ? 6 : 8)
+    << ") psg_jit_scan(const __grid_constant__ ScanProgram P, "
+       "const Segment* __restrict__ segs, const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {\n";
+  if (mat) s << "  __shared__ uint32_t s_wcnt[8][R], s_woff[8][R];\n  __shared__ unsigned long long s_base;\n";
   if (part) s << "  __shared__ unsigned long long s_part[" << kMaxParts << "];\n";
   if (glob) s << "  __shared__ unsigned long long s_gacc[" << nglob << "];\n";
-  s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  (void)lane; (void)warp;\n";
+  s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  const int wrow = warp * 128 + lane;\n";
   if (part) s << "  for (int i = tid; i < " << kMaxParts << "; i += 256) s_part[i] = 0;\n";
   if (glob) {
     s << "  for (int i = tid; i < " << nglob << "; i += 256) s_gacc[i] = 0;\n";
     for (int i = 0; i < nglob; ++i)
       s << "  " << (P.global_float[i] ? "double" : "unsigned long long") << " g" << i << " = 0;\n";
   }
-  // tile descriptors: double-buffered, next tile prefetched into registers
-  s << "  auto fetch = [&](uint64_t t, const uint64_t*& col, uint64_t& r0, uint64_t& rows) {\n"
-    << "    const uint32_t si = __ldg(tile_seg + t);\n"
-    << "    if (tid < " << nin << ") { col = segs[si].col[tid]; }\n"
-    << "    else if (tid == " << kMaxIn << ") { const uint64_t tb = segs[si].tile_begin; r0 = (t - tb) * 1024ULL;"
-       " rows = min(1024ULL, segs[si].rows - r0); }\n  };\n"
-    << "  if (blockIdx.x < ntiles) { const uint64_t* c = nullptr; uint64_t r0 = 0, rows = 0;"
-       " fetch(blockIdx.x, c, r0, rows);\n"
-    << "    if (tid < " << nin << ") s_col[0][tid] = c;\n"
-    << "    if (tid == " << kMaxIn << ") { s_row0[0] = r0; s_rows[0] = rows; } }\n  __syncthreads();\n"
-    << "  int it = 0;\n"
-    << "  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {\n"
-    << "    const int b = it & 1;\n    const uint64_t next = tile + gridDim.x;\n"
-    << "    const uint64_t* pf_col = nullptr; uint64_t pf_r0 = 0, pf_rows = 0;\n"
+  if (part || glob) s << "  __syncthreads();\n";
+  s << "  auto fetch = [&](uint64_t t, const uint64_t*& col, uint64_t& r0, int& rows) {\n"
+    << "    const Segment* sg = segs + __ldg(tile_seg + t);\n"
+    << "    col = lane < " << nin << " ? sg->col[lane] : nullptr;\n"
+    << "    r0 = (t - sg->tile_begin) * 1024ULL;\n"
+    << "    rows = static_cast<int>(min(1024ULL, sg->rows - r0));\n  };\n"
+    << "  const uint64_t* cur_col = nullptr; uint64_t cur_r0 = 0; int cur_rows = 0;\n"
+    << "  if (blockIdx.x < ntiles) fetch(blockIdx.x, cur_col, cur_r0, cur_rows);\n"
+    << "  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
+    << "    const uint64_t next = tile + gridDim.x;\n"
+    << "    const uint64_t* pf_col = nullptr; uint64_t pf_r0 = 0; int pf_rows = 0;\n"
     << "    if (next < ntiles) fetch(next, pf_col, pf_r0, pf_rows);\n"
-    << "    const uint64_t row0 = s_row0[b];\n    const int nrows = static_cast<int>(s_rows[b]);\n"
-    << "    uint32_t pass = 0;\n#pragma unroll\n    for (int r = 0; r < R; ++r) if (r * 256 + tid < nrows) pass |= 1u << r;\n";
+    << "    const uint64_t row0 = cur_r0;\n    const int nrows = cur_rows - warp * 128;\n"
+    << "    uint32_t pass = 0;\n#pragma unroll\n    for (int r = 0; r < R; ++r) if (r * 32 + lane < nrows) pass |= 1u << r;\n";
   for (int r = 0; r < nregs; ++r) s << "    uint64_t " << V(r) << "[R] = {0, 0, 0, 0};\n";
   // Phase A: predicate columns + atoms
   emit_loads(s, 0, P.n_pred);
@@ -184,7 +186,7 @@ std::string jit_source(const ScanProgram& P) {
       s << "      }\n";
     } else {
       s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
-        << "        const uint64_t* cold = T.cold + sl[r] * " << P.agg.cw << ";\n        const uint64_t m = cold[0];\n"
+        << "        const uint64_t* cold = T.cold + sl[r] * " << P.agg.cw << ";\n        const uint64_t m = agg_mult(T, sl[r]);\n"
         << "        g0 += m;\n";
       for (int p = 0; p < P.n_sum; ++p) {
         if (P.agg.ps_float[p])
@@ -212,10 +214,10 @@ std::string jit_source(const ScanProgram& P) {
         << "        sl[r] = slot_of(key, T.shift);\n"
         << "        pv[r] = atomicCAS(reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << "), kEmptyKey, key); }\n"
         << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
-        << "        const uint64_t key = " << V(P.key_reg) << "[r]; uint64_t sx = sl[r];\n"
-        << "        if (pv[r] != kEmptyKey && pv[r] != key) sx = agg_insert_from(T, key, (sx + 1) & T.mask);\n"
-        << "        unsigned long long* cold = reinterpret_cast<unsigned long long*>(T.cold + sx * " << P.agg.cw << ");\n"
-        << "        atomicAdd(cold, 1ULL);\n";
+        << "        const uint64_t key = " << V(P.key_reg) << "[r]; uint64_t sx = sl[r]; bool dup = pv[r] == key;\n"
+        << "        if (pv[r] != kEmptyKey && pv[r] != key) sx = agg_insert_from(T, key, (sx + 1) & T.mask, dup);\n"
+        << "        agg_count_build(T, key, sx, dup);\n"
+        << "        unsigned long long* cold = reinterpret_cast<unsigned long long*>(T.cold + sx * " << P.agg.cw << ");\n";
       for (int bb = 0; bb < P.n_sum; ++bb) {
         if (P.agg.bs_float[bb])
           s << "        atomicAdd(reinterpret_cast<double*>(cold + " << 1 + bb << "), __longlong_as_double(static_cast<long long>("
@@ -227,8 +229,8 @@ std::string jit_source(const ScanProgram& P) {
     } else {  // MATERIALIZE / COUNT
       s << "    uint32_t ballots[R];\n#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
         << "      ballots[r] = __ballot_sync(0xffffffffu, (pass >> r) & 1u);\n"
-        << "      if (lane == 0) s_wcnt[r][warp] = __popc(ballots[r]); }\n    __syncthreads();\n"
-        << "    if (tid == 0) { uint32_t acc = 0;\n      for (int r = 0; r < R; ++r) for (int w = 0; w < 8; ++w) { s_woff[r][w] = acc; acc += s_wcnt[r][w]; }\n";
+        << "      if (lane == 0) s_wcnt[warp][r] = __popc(ballots[r]); }\n    __syncthreads();\n"
+        << "    if (tid == 0) { uint32_t acc = 0;\n      for (int w = 0; w < 8; ++w) for (int r = 0; r < R; ++r) { s_woff[w][r] = acc; acc += s_wcnt[w][r]; }\n";
       if (P.sink == SINK_COUNT)
         s << "      P.tile_counts[tile] = acc;\n";
       else if (P.tile_offsets)
@@ -239,7 +241,7 @@ std::string jit_source(const ScanProgram& P) {
       if (P.sink == SINK_MATERIALIZE) {
         s << "    { const uint64_t base = s_base; const uint32_t lt = (1u << lane) - 1u;\n"
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!((pass >> r) & 1u)) continue;\n"
-          << "        const uint64_t pos = base + s_woff[r][warp] + __popc(ballots[r] & lt);\n"
+          << "        const uint64_t pos = base + s_woff[warp][r] + __popc(ballots[r] & lt);\n"
           << "        if (pos >= P.out_cap) continue;\n";
         for (int o = 0; o < P.n_out; ++o) s << "        P.out_col[" << o << "][pos] = " << V(P.out_reg[o]) << "[r];\n";
         if (part)
@@ -248,9 +250,8 @@ std::string jit_source(const ScanProgram& P) {
       }
     }
   }
-  s << "    if (next < ntiles) { if (tid < " << nin << ") s_col[b ^ 1][tid] = pf_col;\n"
-    << "      if (tid == " << kMaxIn << ") { s_row0[b ^ 1] = pf_r0; s_rows[b ^ 1] = pf_rows; } }\n"
-    << "    __syncthreads();\n  }\n";
+  if (mat) s << "    __syncthreads();\n";  // s_base / s_woff reuse by the next tile
+  s << "    cur_col = pf_col; cur_r0 = pf_r0; cur_rows = pf_rows;\n  }\n";
   if (part)
     s << "  __syncthreads();\n  for (int i = tid; i < P.nparts; i += 256) if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
   if (glob) {

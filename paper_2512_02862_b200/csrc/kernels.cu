@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
         for (int r = 0; r < R; ++r) {
           if (!(pass & (1u << r))) continue;
           const uint64_t* cold = t.cold + slot[r] * t.cw;
-          const uint64_t m = cold[0];
+          const uint64_t m = agg_mult(t, slot[r]);
           atomicAdd(&s_gacc[0], static_cast<unsigned long long>(m));
           for (int p = 0; p < P.n_sum; ++p) {
             const uint64_t v = V(P.sum_reg[p], r);
@@ -261,9 +261,10 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
           if (!(pass & (1u << r))) continue;
           const uint64_t key = V(P.key_reg, r);
           uint64_t s = slot[r];
-          if (prev[r] != kEmptyKey && prev[r] != key) s = agg_insert_from(t, key, (s + 1) & t.mask);
+          bool dup = prev[r] == key;
+          if (prev[r] != kEmptyKey && prev[r] != key) s = agg_insert_from(t, key, (s + 1) & t.mask, dup);
+          agg_count_build(t, key, s, dup);
           unsigned long long* cold = reinterpret_cast<unsigned long long*>(t.cold + s * t.cw);
-          atomicAdd(cold, 1ULL);
           for (int b = 0; b < P.n_sum; ++b) {
             const uint64_t v = V(P.sum_reg[b], r);
             if (t.bs_float[b])
@@ -437,7 +438,7 @@ __global__ void k_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, int 
       }
     }
     const uint32_t old = atomicAdd(cnt + s, 1u);
-    atomicMax(max_cnt, old + 1);
+    if (old > 0) atomicMax(max_cnt, old + 1);  // only duplicates contend
   }
 }
 void launch_local_count(uint64_t* keys, uint32_t* cnt, uint64_t mask, int shift, const uint64_t* bk, uint64_t n,
@@ -607,9 +608,12 @@ void launch_gather(const uint64_t* const* in_cols, int ncols, const uint32_t* id
 }
 
 // --------------------------------------------------------------------------- result emission
+/// counter[0] = groups, counter[1] = min, counter[2] = max of the sign-flipped keys (the sort
+/// then only needs the bits where min and max differ: all keys share the bits above).
 __global__ void k_agg_compact(AggTableDev t, uint64_t nslots, uint64_t* out_keys, unsigned long long* out_slots,
                               unsigned long long* counter) {
   const int lane = threadIdx.x & 31;
+  unsigned long long lo = ~0ULL, hi = 0;
   for (uint64_t s0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); s0 < nslots;
        s0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t s = s0 + threadIdx.x;
@@ -627,9 +631,20 @@ __global__ void k_agg_compact(AggTableDev t, uint64_t nslots, uint64_t* out_keys
     base = __shfl_sync(0xffffffffu, base, 0);
     if (take) {
       const uint64_t pos = base + __popc(b & ((1u << lane) - 1u));
-      out_keys[pos] = key ^ 0x8000000000000000ULL;  // signed order under an unsigned radix sort
+      const uint64_t fk = key ^ 0x8000000000000000ULL;  // signed order under an unsigned radix sort
+      out_keys[pos] = fk;
       out_slots[pos] = s;
+      lo = min(lo, static_cast<unsigned long long>(fk));
+      hi = max(hi, static_cast<unsigned long long>(fk));
     }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if (lane == 0 && hi >= lo) {
+    atomicMin(counter + 1, lo);
+    atomicMax(counter + 2, hi);
   }
 }
 void launch_agg_compact(const AggTableDev& t, uint64_t cap, uint64_t* out_keys, unsigned long long* out_slots,
@@ -649,7 +664,7 @@ __global__ void k_agg_emit(AggTableDev t, const uint64_t* keys, const unsigned l
     const uint64_t s = slots[i];
     const uint64_t* h = t.hot + s * t.hw;
     const uint64_t* c = t.cold + s * t.cw;
-    const uint64_t hits = h[1], m = c[0];
+    const uint64_t hits = h[1], m = agg_mult(t, s);
     uint64_t* row = out + i * nc;
     for (int k = 0; k < nc; ++k) {
       const int kind = ec.kind[k], j = ec.idx[k];
@@ -685,11 +700,11 @@ void launch_agg_emit(const AggTableDev& t, const uint64_t* sorted_keys, const un
 }
 
 size_t sort_pairs_i64(const uint64_t* keys_in, uint64_t* keys_out, const unsigned long long* v_in,
-                      unsigned long long* v_out, uint64_t n, void* tmp, size_t tmp_bytes, void* stream) {
+                      unsigned long long* v_out, uint64_t n, int end_bit, void* tmp, size_t tmp_bytes, void* stream) {
   size_t bytes = tmp_bytes;
   cub::DeviceRadixSort::SortPairs(tmp, bytes, reinterpret_cast<const unsigned long long*>(keys_in),
                                   reinterpret_cast<unsigned long long*>(keys_out), v_in, v_out,
-                                  static_cast<int64_t>(n), 0, 64, S(stream));
+                                  static_cast<int64_t>(n), 0, end_bit, S(stream));
   if (tmp) count_launch();
   return bytes;
 }

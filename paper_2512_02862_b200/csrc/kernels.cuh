@@ -62,7 +62,7 @@ void launch_agg_emit(const AggTableDev& t, const uint64_t* sorted_keys, const un
                      uint64_t n, int ncols_out, const int32_t* col_kind, const int32_t* col_idx, uint64_t* out_rows,
                      void* stream);
 size_t sort_pairs_i64(const uint64_t* keys_in, uint64_t* keys_out, const unsigned long long* v_in,
-                      unsigned long long* v_out, uint64_t n, void* tmp, size_t tmp_bytes, void* stream);
+                      unsigned long long* v_out, uint64_t n, int end_bit, void* tmp, size_t tmp_bytes, void* stream);
 size_t sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* v_in, uint32_t* v_out, uint64_t n,
                       int end_bit, void* tmp, size_t tmp_bytes, void* stream);
 void launch_iota_u32(uint32_t* out, uint64_t n, void* stream);
