@@ -1,0 +1,106 @@
+"""Multi-GPU parity check (one rank per GPU, NCCL shuffle): run under torchrun.
+
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 scripts/mgpu_check.py [--scale S]
+
+Data is generated with nodes=N (the reference's layout), every rank executes the plan through
+psg_execute_plan, and rank 0 checks each rank's rows against the reference's per-node results
+(tests/golden/results.json where a case with nodes=N exists) and against the oracle otherwise.
+Exit code 0 = all checks passed.
+"""
+import argparse
+import json
+import os
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import paper_2512_02862_b200 as psg  # noqa: E402
+from oracle import plan_oracle as po  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--scale", type=float, default=0.1)
+    ap.add_argument("--modes", default="overlapped,blocking")
+    a = ap.parse_args()
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    golden = json.load(open(os.path.join(ROOT, "tests", "golden", "results.json")))
+    base = tempfile.mkdtemp(prefix="mgpu_") if rank == 0 else None
+    obj = [base]
+    dist.broadcast_object_list(obj, src=0)
+    base = obj[0]
+    obj = [psg.Context.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx = psg.Context(local, rank, world, obj[0])
+    ctx.set_ingest(io_threads=4, batch_bytes=2 << 20)
+    failures = []
+    datasets = {}
+
+    def data(scale, seed=42, rg=1 << 20, devices=None):
+        key = (scale, seed, rg, devices)
+        if key not in datasets:
+            d = os.path.join(base, "d%d" % len(datasets))
+            if rank == 0:
+                psg.gen_workload("tpch", d, devices=devices or world, nodes=world, scale=scale, seed=seed,
+                                 row_group_bytes=rg)
+            dist.barrier()
+            datasets[key] = d
+        return datasets[key]
+
+    cases = [("canonical", a.scale, 42, 1 << 20), ("acceptance", 0.02, 42, 256 << 10),
+             ("projection_buildsums", 0.01, 42, 1 << 20), ("multi_atom", 0.1, 42, 1 << 20),
+             ("global_agg", 0.01, 42, 1 << 20), ("empty", 0.002, 42, 1 << 20),
+             ("no_aggregate", 0.002, 42, 64 << 10), ("smoke_py", 0.002, 11, 1 << 20),
+             ("pipeline_test", 0.004, 42, 64 << 10)]
+    for semijoin in (True, False):
+        ctx.set_semijoin(semijoin)
+        for pname, scale, seed, rg in cases:
+            d = data(scale, seed, rg)
+            plan = golden["plans"][pname]
+            for mode in a.modes.split(","):
+                try:
+                    res = ctx.execute_plan(plan, d, mode)
+                    mine = (res.schema, res.rows.copy())
+                except psg.PsgError as e:
+                    mine = ("error", str(e))
+                allres = [None] * world
+                dist.all_gather_object(allres, mine)
+                if rank == 0:
+                    if any(x[0] == "error" for x in allres):
+                        failures.append((pname, mode, semijoin, [x for x in allres if x[0] == "error"]))
+                        continue
+                    got = po.summary(allres)
+                    g = [r for r in golden["results"] if r["plan"] == pname and r["nodes"] == world
+                         and r["scale"] == scale and r["seed"] == seed and r["rg_bytes"] == rg]
+                    if g:
+                        want = {k: g[0][k] for k in ("rows", "rowhash", "colsums", "per_node_rows")}
+                        src = "reference"
+                    else:
+                        want = po.summary(po.execute(json.dumps(plan), d, world))
+                        src = "oracle"
+                    ok = all(got[k] == want[k] for k in ("rows", "rowhash", "colsums", "per_node_rows"))
+                    print("%-22s %-10s semijoin=%d %-9s %s rows=%d per_node=%s" % (
+                        pname, mode, semijoin, src, "OK " if ok else "BAD", got["rows"], got["per_node_rows"]),
+                        flush=True)
+                    if not ok:
+                        failures.append((pname, mode, semijoin, got, want))
+    if rank == 0:
+        print("FAILURES", len(failures))
+        for f in failures:
+            print(f)
+    ok = torch.tensor([0 if failures else 1], device="cuda")
+    dist.broadcast(ok, src=0)
+    ctx.close()
+    dist.destroy_process_group()
+    sys.exit(0 if ok.item() else 1)
+
+
+if __name__ == "__main__":
+    main()
