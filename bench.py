@@ -253,12 +253,14 @@ def main():
     for _ in range(args.warmup):
         staged.run(want_rows=False)
     sync_all()
-    dev_ms, wall0 = [], time.time()
+    dev_ms = []
     launches = 0
     probe_ms = probe_bytes = probe_launches = 0
     rows = 0
     with Clocks(local) as clk:
+        wall0 = time.time()
         for _ in range(args.steps):
+            sync_all()  # every step starts aligned across ranks (the barrier is outside the engine's events)
             st = staged.run(want_rows=False)
             dev_ms.append(st["device_ms"])
             launches += st["kernel_launches"]
@@ -274,13 +276,14 @@ def main():
 
     # ---------------- e2e: storage-resident, through psg_execute_plan ----------------
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
-    for _ in range(min(args.warmup, 1)):
-        ctx.execute_plan(plan, data_root)
+    warm = [ctx.execute_plan(plan, data_root) for _ in range(min(args.warmup, 2))]  # pinned result blocks
+    del warm
     sync_all()
     e2e_t, h2d, d2h = [], 0, 0
     e2e_rows = 0
     io_wait = []
     for _ in range(e2e_steps):
+        sync_all()
         t = time.time()
         res = ctx.execute_plan(plan, data_root)
         e2e_t.append(time.time() - t)

@@ -110,6 +110,13 @@ struct ScanProgram {
   AggTableDev agg;
   unsigned long long* global_acc;       // SINK_PROBE_GLOBAL: [rows, probe sums..., build sums...]
   int32_t global_float[2 * kMaxSums + 1];
+  // Semi-join pre-filter of a partitioned probe side (MATERIALIZE with nparts > 1): nparts
+  // concatenated Bloom filters, filter d over the build keys owned by rank d. A row whose key is
+  // certainly absent on its owner is dropped before it is shuffled.
+  const uint32_t* semi_bloom;
+  uint64_t semi_words;
+  int32_t semi_shift;
+  int32_t semi_key_reg;
 };
 
 #if defined(__CUDACC__) || defined(__CUDACC_RTC__)
@@ -153,6 +160,16 @@ __device__ __forceinline__ bool bloom_maybe(const AggTableDev& t, uint64_t key) 
 }
 
 /// Claims key's slot from s on; `dup` = the key was already present (another build row).
+/// Semi-join test: false only when key is certainly not a build key of its owner rank.
+__device__ __forceinline__ bool semi_maybe(const ScanProgram& P, uint64_t key) {
+  if (key == kEmptyKey) return true;  // the spill key is never in the filters
+  const uint64_t h2 = key * kBloomMul;
+  const uint32_t d = part_of(key, static_cast<uint32_t>(P.nparts));
+  const uint32_t w = __ldg(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift));
+  const uint32_t m = bloom_bits(h2, P.semi_shift);
+  return (w & m) == m;
+}
+
 __device__ __forceinline__ uint64_t agg_insert_from(const AggTableDev& t, uint64_t key, uint64_t s, bool& dup) {
   while (true) {
     unsigned long long* kp = reinterpret_cast<unsigned long long*>(t.hot + s * t.hw);

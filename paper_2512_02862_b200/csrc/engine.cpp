@@ -420,7 +420,7 @@ class Execution {
   Received exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data);
   BatchView upload_segments(std::vector<Segment> segs, DevBuf& holder);
 
-  void build_agg_table(uint64_t build_rows);
+  void build_agg_table(uint64_t build_rows, uint64_t bloom_words);
   void finalize_grouped(ResultRows& out, bool want_rows);
   void finalize_global(ResultRows& out);
 
@@ -871,7 +871,7 @@ void Execution::build_local_tables() {
 }
 
 // --------------------------------------------------------------------------- agg table
-void Execution::build_agg_table(uint64_t build_rows) {
+void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words) {
   agg_cap_ = pow2_at_least(std::max<uint64_t>(2 * build_rows, 16));
   const int nps = static_cast<int>(probe_sum_wire.size()), nbs = static_cast<int>(build_sum_wire.size());
   int hw = 2 + nps;
@@ -890,15 +890,11 @@ void Execution::build_agg_table(uint64_t build_rows) {
   aggt_.nbs = nbs;
   for (int i = 0; i < nps; ++i) aggt_.ps_float[i] = psrc_.wire.fields[probe_sum_wire[i]].type == LType::Float64;
   for (int i = 0; i < nbs; ++i) aggt_.bs_float[i] = bsrc_.wire.fields[build_sum_wire[i]].type == LType::Float64;
-  // Bloom filter when the hot table would not stay L2-resident (~16 bits per key, <= 32 MB).
-  const uint64_t hot_bytes = (agg_cap_ + 1) * hw * 8;
-  if (hot_bytes > (48ull << 20) && ctx_.semijoin) {
-    uint64_t words = pow2_at_least(std::max<uint64_t>(build_rows / 2, 1024));
-    words = std::min<uint64_t>(words, 8ull << 20);
-    agg_bloom_ = DevBuf(ctx_.pool, words * 4, ctx_.compute);
+  if (bloom_words) {
+    agg_bloom_ = DevBuf(ctx_.pool, bloom_words * 4, ctx_.compute);
     aggt_.bloom = agg_bloom_.as<uint32_t>();
-    aggt_.bloom_mask = words - 1;
-    aggt_.bloom_shift = shift_of(words);
+    aggt_.bloom_mask = bloom_words - 1;
+    aggt_.bloom_shift = shift_of(bloom_words);
   }
   launch_agg_init(aggt_, agg_cap_, ctx_.compute);
 }
@@ -919,6 +915,7 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
   std::vector<uint64_t> m(static_cast<size_t>(n) * n);
   PSG_CUDA(cudaMemcpyAsync(m.data(), matrix.p, m.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));  // the one data-dependent host sync per wave
+  PhaseTimer xt;
   const int me = ctx_.rank;
   uint64_t nrows = 0;
   for (int d = 0; d < n; ++d) nrows += m[static_cast<size_t>(me) * n + d];
@@ -953,6 +950,7 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
     roff += rc;
   }
   PSG_NCCL(ncclGroupEnd());
+  xt.mark("  exchange payload", ctx_.compute);
   st_.waves += 1;
   return rcv;
 }
@@ -1133,14 +1131,39 @@ ResultRows Execution::run(bool want_rows) {
 
   // For no-aggregate plans the build side becomes a CSR table of full wire rows.
   std::unique_ptr<LocalTable> final_table;
+  // Bloom filter over the build keys: at one GPU it screens probes when the hot table would not
+  // stay L2-resident; at N GPUs every rank's filter is all-gathered so the probe side can drop
+  // rows whose key is absent on its owner before the shuffle (semi-join reduction). All ranks
+  // size the filter from the largest build side so the filters line up.
+  DevBuf semi_all;
+  uint64_t bloom_words = 0;
+  const bool semi = agg_ && nr > 1 && ctx_.semijoin;
   if (agg_) {
-    build_agg_table(build_rows);
+    uint64_t sized_rows = build_rows;
+    if (semi) {
+      DevBuf mv(ctx_.pool, 8, ctx_.compute);
+      PSG_CUDA(cudaMemcpyAsync(mv.p, &sized_rows, 8, cudaMemcpyHostToDevice, ctx_.compute));
+      PSG_NCCL(ncclAllReduce(mv.p, mv.p, 1, ncclUint64, ncclMax, ctx_.nccl, ctx_.compute));
+      PSG_CUDA(cudaMemcpyAsync(&sized_rows, mv.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    }
+    const uint64_t cap = pow2_at_least(std::max<uint64_t>(2 * build_rows, 16));
+    const int hw_est = 2 + static_cast<int>(probe_sum_wire.size()) <= 4 ? 4 : 8;
+    if (semi || ((cap + 1) * hw_est * 8 > (48ull << 20) && ctx_.semijoin))
+      bloom_words = std::min<uint64_t>(pow2_at_least(std::max<uint64_t>(sized_rows / 2, 1024)), 8ull << 20);
+  }
+  if (agg_) {
+    build_agg_table(build_rows, bloom_words);
     ScanProgram p = batch_program(static_cast<int>(b_out.size()));
     p.sink = SINK_BUILD;
     p.agg = aggt_;
     p.n_sum = static_cast<int>(build_sum_wire.size());
     for (int b = 0; b < p.n_sum; ++b) p.sum_reg[b] = 1 + b;
     run_scan(p, bview, false);  // also sets the Bloom bits of every inserted key
+    if (semi) {
+      semi_all = DevBuf(ctx_.pool, static_cast<size_t>(nr) * bloom_words * 4, ctx_.compute);
+      PSG_NCCL(ncclAllGather(agg_bloom_.p, semi_all.p, bloom_words * 4, ncclUint8, ctx_.nccl, ctx_.compute));
+    }
     if (!grouped_) {
       global_acc_ = DevBuf(ctx_.pool, (2 * kMaxSums + 1) * 8, ctx_.compute);
       PSG_CUDA(cudaMemsetAsync(global_acc_.p, 0, (2 * kMaxSums + 1) * 8, ctx_.compute));
@@ -1196,6 +1219,12 @@ ResultRows Execution::run(bool want_rows) {
   ScanProgram pp = base_program(psrc_, pm, true);
   std::vector<int> p_out;
   for (int w : pneed) p_out.push_back(pm.reg_of.at(psrc_.stage_refs.back()[w]));
+  if (semi) {
+    pp.semi_bloom = semi_all.as<uint32_t>();
+    pp.semi_words = bloom_words;
+    pp.semi_shift = aggt_.bloom_shift;
+    pp.semi_key_reg = p_out[0];
+  }
   auto pfeed = open_feed(*psrc_.scan, file_cols_of(psrc_, pm));
   std::vector<DevCols> joined_parts;  // no-aggregate results
   auto consume_materialised = [&](const BatchView& v, int ncols) {
@@ -1204,6 +1233,7 @@ ResultRows Execution::run(bool want_rows) {
       ScanProgram p = batch_program(ncols);
       p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
       p.agg = aggt_;
+      if (semi) p.agg.bloom = nullptr;  // received rows already passed the owner's filter
       p.key_reg = 0;
       p.n_sum = static_cast<int>(probe_sum_wire.size());
       for (int s = 0; s < p.n_sum; ++s) p.sum_reg[s] = 1 + s;
@@ -1282,12 +1312,15 @@ ResultRows Execution::run(bool want_rows) {
         pfeed->done();
         st_.ingest_bytes += v.bytes;
       }
+      pt.mark("  probe materialize", ctx_.compute);
       if (nr > 1) {
         Received r = exchange(mat, static_cast<int>(p_out.size()), 0, pc, have);
         DevBuf holder;
         BatchView rv = upload_segments(r.segs, holder);
+        pt.mark("  probe exchange", ctx_.compute);
         consume_materialised(rv, static_cast<int>(p_out.size()));
         PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+        pt.mark("  probe consume", ctx_.compute);
       } else {
         const uint64_t n = read_count(mat);
         Segment sg;

@@ -227,6 +227,14 @@ std::string jit_source(const ScanProgram& P) {
       }
       s << "      }\n    }\n";
     } else {  // MATERIALIZE / COUNT
+      if (P.sink == SINK_MATERIALIZE && P.semi_bloom != nullptr) {
+        s << "    { uint32_t bw[R], bm[R];\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = bm[r] = 0; const uint64_t key = " << V(P.semi_key_reg)
+          << "[r];\n        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t h2 = key * kBloomMul;\n"
+          << "          const uint32_t d = part_of(key, static_cast<uint32_t>(P.nparts));\n"
+          << "          bm[r] = bloom_bits(h2, P.semi_shift); bw[r] = __ldg(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift)); } }\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n    }\n";
+      }
       s << "    uint32_t ballots[R];\n#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
         << "      ballots[r] = __ballot_sync(0xffffffffu, (pass >> r) & 1u);\n"
         << "      if (lane == 0) s_wcnt[warp][r] = __popc(ballots[r]); }\n    __syncthreads();\n"
@@ -244,9 +252,13 @@ std::string jit_source(const ScanProgram& P) {
           << "        const uint64_t pos = base + s_woff[warp][r] + __popc(ballots[r] & lt);\n"
           << "        if (pos >= P.out_cap) continue;\n";
         for (int o = 0; o < P.n_out; ++o) s << "        P.out_col[" << o << "][pos] = " << V(P.out_reg[o]) << "[r];\n";
-        if (part)
-          s << "        atomicAdd(&s_part[part_of(" << V(P.part_key_reg) << "[r], static_cast<uint32_t>(P.nparts))], 1ULL);\n";
         s << "      }\n    }\n";
+        if (part)  // warp-aggregated destination histogram: one shared atomic per (warp, dest)
+          s << "#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
+            << "      const bool on = (pass >> r) & 1u;\n"
+            << "      const uint32_t d = on ? part_of(" << V(P.part_key_reg) << "[r], static_cast<uint32_t>(P.nparts)) : 0xffffffffu;\n"
+            << "      const unsigned peers = __match_any_sync(0xffffffffu, d);\n"
+            << "      if (on && lane == __ffs(peers) - 1) atomicAdd(&s_part[d], static_cast<unsigned long long>(__popc(peers)));\n    }\n";
       }
     }
   }
@@ -398,6 +410,8 @@ int jit_selftest(std::string& log) {
     if (sink == SINK_MATERIALIZE) {
       p.nparts = 4;
       p.part_key_reg = 1;
+      p.semi_bloom = reinterpret_cast<const uint32_t*>(16);
+      p.semi_key_reg = 1;
     }
     progs.push_back(p);
   }
