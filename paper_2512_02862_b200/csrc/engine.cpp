@@ -39,13 +39,14 @@ namespace psg {
 namespace {
 
 using Clock = std::chrono::steady_clock;
-bool trace_on() {
-  static const bool on = [] {
+int trace_level() {
+  static const int lvl = [] {
     const char* e = std::getenv("PSG_TRACE");
-    return e && e[0] == '1';
+    return e ? std::atoi(e) : 0;
   }();
-  return on;
+  return lvl;
 }
+bool trace_on() { return trace_level() > 0; }
 #define PSG_TRACE_MSG(...)                  \
   do {                                      \
     if (trace_on()) {                       \
@@ -57,7 +58,7 @@ struct PhaseTimer {
   Clock::time_point t0 = Clock::now(), last = t0;
   void mark(const char* what, cudaStream_t s) {
     if (!trace_on()) return;
-    cudaStreamSynchronize(s);
+    if (trace_level() == 1) cudaStreamSynchronize(s);  // level 2: host timestamps only
     const auto now = Clock::now();
     std::fprintf(stderr, "[psg] %-28s %8.3f ms (total %8.3f)\n", what,
                  std::chrono::duration<double, std::milli>(now - last).count(),
@@ -1153,7 +1154,9 @@ ResultRows Execution::run(bool want_rows) {
       bloom_words = std::min<uint64_t>(pow2_at_least(std::max<uint64_t>(sized_rows / 2, 1024)), 8ull << 20);
   }
   if (agg_) {
+    pt.mark("  pre agg alloc", ctx_.compute);
     build_agg_table(build_rows, bloom_words);
+    pt.mark("  agg alloc+init", ctx_.compute);
     ScanProgram p = batch_program(static_cast<int>(b_out.size()));
     p.sink = SINK_BUILD;
     p.agg = aggt_;
@@ -1342,6 +1345,7 @@ ResultRows Execution::run(bool want_rows) {
   pt.mark("probe side", ctx_.compute);
   // ---------------- finalize ----------------
   if (agg_) {
+    pt.mark("  pre finalize", ctx_.compute);
     if (grouped_) finalize_grouped(out, want_rows);
     else finalize_global(out);
   } else {

@@ -20,8 +20,11 @@
 
 namespace psg {
 
-/// Stream-ordered device allocator with budget accounting (the RMM-pool analog of
-/// MemoryPool, memory_pool.hpp:30-108). Freed blocks stay cached in the CUDA mempool.
+/// Caching device allocator with budget accounting (the RMM-pool analog of MemoryPool,
+/// memory_pool.hpp:30-108). Blocks are cudaMalloc'ed once and recycled per stream: a block freed
+/// on stream s is only handed out again to work on s, so stream order makes reuse safe without
+/// host syncs (cudaMallocAsync's pool grew and re-mapped memory under in-flight work, which cost
+/// milliseconds per query).
 class DevicePool {
  public:
   void init(int device, uint64_t budget);
@@ -29,12 +32,16 @@ class DevicePool {
   void free(void* p, cudaStream_t s);
   uint64_t used() const { return used_; }
   uint64_t peak() const { return peak_; }
+  uint64_t cached() const { return cached_; }
   void reset_peak() { peak_ = used_; }
   void set_budget(uint64_t b) { budget_ = b; }
+  void release_cache();
+  ~DevicePool() { release_cache(); }
 
  private:
   std::map<void*, size_t> live_;
-  uint64_t used_ = 0, peak_ = 0, budget_ = 0;
+  std::map<std::pair<cudaStream_t, size_t>, std::vector<void*>> free_;  // (stream, size) -> blocks
+  uint64_t used_ = 0, peak_ = 0, budget_ = 0, cached_ = 0;
 };
 
 /// RAII device buffer from the pool.

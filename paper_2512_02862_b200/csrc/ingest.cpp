@@ -12,25 +12,48 @@
 namespace psg {
 
 // ----------------------------------------------------------------------------- DevicePool
+namespace {
+constexpr uint64_t kPoolCacheMax = 120ull << 30;  // keep at most this much idle device memory
+size_t round_block(size_t b) {
+  // 2 MiB granularity above 64 MiB, 64 KiB below, so repeated queries hit identical sizes
+  const size_t g = b >= (64u << 20) ? (2u << 20) : (64u << 10);
+  return (b + g - 1) / g * g;
+}
+}  // namespace
+
 void DevicePool::init(int device, uint64_t budget) {
+  (void)device;
   budget_ = budget;
-  cudaMemPool_t mp;
-  PSG_CUDA(cudaDeviceGetDefaultMemPool(&mp, device));
-  uint64_t thr = ~0ULL;  // keep freed blocks cached (RMM-pool behaviour)
-  PSG_CUDA(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
 }
 
 void* DevicePool::alloc(size_t bytes, cudaStream_t s) {
-  if (budget_ && used_ + bytes > budget_) throw MemoryExceeded(bytes, used_, budget_);
+  const size_t rb = round_block(bytes ? bytes : 8);
+  if (budget_ && used_ + rb > budget_) throw MemoryExceeded(rb, used_, budget_);
   void* p = nullptr;
-  cudaError_t e = cudaMallocAsync(&p, bytes, s);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    throw Error(PSG_ERR_MEMORY_EXCEEDED, "device allocation of " + std::to_string(bytes) +
-                                             " bytes failed: " + cudaGetErrorString(e));
+  size_t got = rb;
+  // best fit among this stream's idle blocks of size [rb, 2 rb]
+  auto it = free_.lower_bound({s, rb});
+  if (it != free_.end() && it->first.first == s && it->first.second <= 2 * rb && !it->second.empty()) {
+    got = it->first.second;
+    p = it->second.back();
+    it->second.pop_back();
+    cached_ -= got;
+    if (it->second.empty()) free_.erase(it);
+  } else {
+    cudaError_t e = cudaMalloc(&p, rb);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      release_cache();  // give idle blocks back and retry once
+      e = cudaMalloc(&p, rb);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw Error(PSG_ERR_MEMORY_EXCEEDED,
+                    "device allocation of " + std::to_string(rb) + " bytes failed: " + cudaGetErrorString(e));
+      }
+    }
   }
-  live_[p] = bytes;
-  used_ += bytes;
+  live_[p] = got;
+  used_ += got;
   if (used_ > peak_) peak_ = used_;
   return p;
 }
@@ -38,9 +61,25 @@ void* DevicePool::alloc(size_t bytes, cudaStream_t s) {
 void DevicePool::free(void* p, cudaStream_t s) {
   auto it = live_.find(p);
   if (it == live_.end()) return;
-  used_ -= it->second;
+  const size_t n = it->second;
+  used_ -= n;
   live_.erase(it);
-  cudaFreeAsync(p, s);
+  if (cached_ + n > kPoolCacheMax) {
+    cudaStreamSynchronize(s);
+    cudaFree(p);
+    return;
+  }
+  free_[{s, n}].push_back(p);
+  cached_ += n;
+}
+
+void DevicePool::release_cache() {
+  if (free_.empty()) return;
+  cudaDeviceSynchronize();
+  for (auto& [k, v] : free_)
+    for (void* p : v) cudaFree(p);
+  free_.clear();
+  cached_ = 0;
 }
 
 // ----------------------------------------------------------------------------- PinnedBlock

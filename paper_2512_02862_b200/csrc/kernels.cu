@@ -379,22 +379,24 @@ void launch_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_
 }
 
 // ---------------------------------------------------------------------------- agg table setup
-__global__ void k_agg_init(AggTableDev t, uint64_t nslots) {
-  for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < nslots;
-       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    uint64_t* h = t.hot + s * t.hw;
-    h[0] = kEmptyKey;
-    for (int i = 1; i < t.hw; ++i) h[i] = 0;
-    uint64_t* c = t.cold + s * t.cw;
-    for (int i = 0; i < t.cw; ++i) c[i] = 0;
+/// Hot slots initialised with 16-byte stores ({kEmptyKey, 0} then {0, 0}); cold is memset.
+__global__ void k_agg_init(AggTableDev t, uint64_t nwords16) {
+  ulonglong2* h = reinterpret_cast<ulonglong2*>(t.hot);
+  const int per_slot = t.hw / 2;  // hw is even (2, 4, 8k)
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nwords16;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    ulonglong2 v;
+    v.x = (i % per_slot) == 0 ? kEmptyKey : 0ULL;
+    v.y = 0ULL;
+    h[i] = v;
   }
 }
 void launch_agg_init(const AggTableDev& t, uint64_t cap, void* stream) {
   count_launch();
-  k_agg_init<<<grid_for(cap + 1, 256), 256, 0, S(stream)>>>(t, cap + 1);
-  if (t.bloom) {
-    cudaMemsetAsync(t.bloom, 0, (t.bloom_mask + 1) * sizeof(uint32_t), S(stream));
-  }
+  const uint64_t n16 = (cap + 1) * t.hw / 2;
+  k_agg_init<<<grid_for(n16, 256), 256, 0, S(stream)>>>(t, n16);
+  cudaMemsetAsync(t.cold, 0, (cap + 1) * t.cw * sizeof(uint64_t), S(stream));
+  if (t.bloom) cudaMemsetAsync(t.bloom, 0, (t.bloom_mask + 1) * sizeof(uint32_t), S(stream));
 }
 
 __global__ void k_bloom_build(AggTableDev t, uint64_t cap) {
@@ -614,34 +616,71 @@ void launch_gather(const uint64_t* const* in_cols, int ncols, const uint32_t* id
 
 // --------------------------------------------------------------------------- result emission
 /// counter[0] = groups, counter[1] = min, counter[2] = max of the sign-flipped keys (the sort
-/// then only needs the bits where min and max differ: all keys share the bits above).
-__global__ void k_agg_compact(AggTableDev t, uint64_t nslots, uint64_t* out_keys, unsigned long long* out_slots,
-                              unsigned long long* counter) {
-  const int lane = threadIdx.x & 31;
+/// then only needs the bits where min and max differ: all keys share the bits above). Each block
+/// compacts a contiguous range of 4096 slots with one global atomic (block prefix in smem).
+constexpr int kCompactSpan = 4096;
+__global__ void __launch_bounds__(256) k_agg_compact(AggTableDev t, uint64_t nslots, uint64_t* out_keys,
+                                                     unsigned long long* out_slots, unsigned long long* counter) {
+  __shared__ uint32_t s_cnt[kCompactSpan / 32];
+  __shared__ unsigned long long s_base;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   unsigned long long lo = ~0ULL, hi = 0;
-  for (uint64_t s0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); s0 < nslots;
-       s0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t s = s0 + threadIdx.x;
-    bool take = false;
-    uint64_t key = 0;
-    if (s < nslots) {
-      const uint64_t* h = t.hot + s * t.hw;
-      key = h[0];
-      const bool occupied = (s == nslots - 1) ? (t.cold[s * t.cw] > 0) : (key != kEmptyKey);
-      take = occupied && h[1] > 0;
+  for (uint64_t span = blockIdx.x * static_cast<uint64_t>(kCompactSpan); span < nslots;
+       span += static_cast<uint64_t>(gridDim.x) * kCompactSpan) {
+    constexpr int PER = kCompactSpan / 256;  // slots per thread, warp-strided
+    bool take[PER];
+    uint64_t key[PER];
+    unsigned bal[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const uint64_t s = span + (warp * PER + k) * 32 + lane;
+      take[k] = false;
+      key[k] = 0;
+      if (s < nslots) {
+        const ulonglong2 kh = *reinterpret_cast<const ulonglong2*>(t.hot + s * t.hw);  // {key, hits}
+        key[k] = kh.x;
+        const bool occupied = (s == nslots - 1) ? (t.cold[s * t.cw] > 0) : (kh.x != kEmptyKey);
+        take[k] = occupied && kh.y > 0;
+      }
+      bal[k] = __ballot_sync(0xffffffffu, take[k]);
+      if (lane == 0) s_cnt[warp * PER + k] = __popc(bal[k]);
     }
-    const unsigned b = __ballot_sync(0xffffffffu, take);
-    unsigned long long base = 0;
-    if (lane == 0 && b) base = atomicAdd(counter, static_cast<unsigned long long>(__popc(b)));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (take) {
-      const uint64_t pos = base + __popc(b & ((1u << lane) - 1u));
-      const uint64_t fk = key ^ 0x8000000000000000ULL;  // signed order under an unsigned radix sort
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 128 per-(warp,k) counts, 4 per lane
+      uint32_t c[4], sum = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        c[q] = s_cnt[lane * 4 + q];
+        sum += c[q];
+      }
+      uint32_t incl = sum;
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      uint32_t run = incl - sum;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t x = c[q];
+        s_cnt[lane * 4 + q] = run;
+        run += x;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      if (lane == 31) s_base = total ? atomicAdd(counter, static_cast<unsigned long long>(total)) : 0ULL;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      if (!take[k]) continue;
+      const uint64_t s = span + (warp * PER + k) * 32 + lane;
+      const uint64_t pos = s_base + s_cnt[warp * PER + k] + __popc(bal[k] & ((1u << lane) - 1u));
+      const uint64_t fk = key[k] ^ 0x8000000000000000ULL;  // signed order under an unsigned radix sort
       out_keys[pos] = fk;
       out_slots[pos] = s;
       lo = min(lo, static_cast<unsigned long long>(fk));
       hi = max(hi, static_cast<unsigned long long>(fk));
     }
+    __syncthreads();
   }
   for (int o = 16; o > 0; o >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -655,7 +694,10 @@ __global__ void k_agg_compact(AggTableDev t, uint64_t nslots, uint64_t* out_keys
 void launch_agg_compact(const AggTableDev& t, uint64_t cap, uint64_t* out_keys, unsigned long long* out_slots,
                         unsigned long long* counter, void* stream) {
   count_launch();
-  k_agg_compact<<<grid_for(cap + 1, 256), 256, 0, S(stream)>>>(t, cap + 1, out_keys, out_slots, counter);
+  uint64_t blocks = (cap + 1 + kCompactSpan - 1) / kCompactSpan;
+  const uint64_t maxb = static_cast<uint64_t>(sm_count()) * 8;
+  if (blocks > maxb) blocks = maxb;
+  k_agg_compact<<<static_cast<unsigned>(blocks), 256, 0, S(stream)>>>(t, cap + 1, out_keys, out_slots, counter);
 }
 
 struct EmitCols {
