@@ -244,6 +244,7 @@ struct ScanBatches {
   std::vector<BatchPlan> batches;
   uint64_t total_rows = 0;
   uint64_t total_bytes = 0;
+  uint64_t total_payload = 0;
   uint64_t max_batch_bytes = 0;
   uint64_t max_segs = 0;
 };
@@ -261,8 +262,10 @@ ScanBatches plan_batches(FooterCache& fc, const ScanNode& scan, const std::vecto
     cur.file = file_base + static_cast<int>(f);
     auto flush = [&] {
       if (cur.groups.empty()) return;
+      cur.bytes += 16;  // tail padding: 16-byte async copies may read 8 bytes past the last chunk
       out.total_rows += cur.total_rows;
       out.total_bytes += cur.bytes;
+      out.total_payload += cur.payload_bytes;
       out.max_batch_bytes = std::max(out.max_batch_bytes, cur.bytes);
       out.max_segs = std::max<uint64_t>(out.max_segs, cur.groups.size());
       out.batches.push_back(std::move(cur));
@@ -281,8 +284,10 @@ ScanBatches plan_batches(FooterCache& fc, const ScanNode& scan, const std::vecto
       std::vector<uint64_t> pos(file_cols.size());
       for (auto& [off, k] : order) {
         const uint64_t len = gm.cols[file_cols[k]].csize;
-        // the same file column may be requested twice (never in practice); reuse position
+        // 16-byte aligned chunk positions (cp.async in the fused kernel); padding breaks an extent
+        cur.bytes = (cur.bytes + 15) & ~15ULL;
         pos[k] = cur.bytes;
+        cur.payload_bytes += len;
         if (!cur.extents.empty() && cur.extents.back().file_off + cur.extents.back().len == off &&
             cur.extents.back().buf_off + cur.extents.back().len == cur.bytes)
           cur.extents.back().len += len;
@@ -292,6 +297,7 @@ ScanBatches plan_batches(FooterCache& fc, const ScanNode& scan, const std::vecto
       }
       cur.groups.push_back(g);
       cur.rows.push_back(gm.rows);
+      cur.bytes = (cur.bytes + 15) & ~15ULL;
       cur.pos.push_back(std::move(pos));
       cur.total_rows += gm.rows;
     }
@@ -359,6 +365,7 @@ struct DevCols {
 
 // ------------------------------------------------------------------------------ Staged
 struct StagedScan {
+  uint64_t payload = 0;
   DevBuf data;
   DevBuf segs;  // segment array + tile table at tile_off
   size_t tile_off = 0;
@@ -563,7 +570,7 @@ struct StreamSession {
     v.nsegs = static_cast<int>(segs.size());
     v.ntiles = nt;
     v.rows = b.total_rows;
-    v.bytes = b.bytes;
+    v.bytes = b.payload_bytes;
     cur_slot = k;
     ++cursor;
   }
@@ -603,7 +610,7 @@ struct StagedFeed : Execution::Feed {
     v.nsegs = s->nsegs;
     v.ntiles = s->ntiles;
     v.rows = s->rows;
-    v.bytes = s->bytes;
+    v.bytes = s->payload;
     return true;
   }
   void done() override {}
@@ -721,7 +728,7 @@ ScanProgram Execution::base_program(const SourceDef& s, const RegMap& m, bool wi
 DevCols Execution::alloc_cols(size_t ncols, uint64_t cap) {
   DevCols c;
   c.cap = cap;
-  for (size_t i = 0; i < ncols; ++i) c.cols.emplace_back(ctx_.pool, std::max<uint64_t>(cap, 1) * 8, ctx_.compute);
+  for (size_t i = 0; i < ncols; ++i) c.cols.emplace_back(ctx_.pool, std::max<uint64_t>(cap, 1) * 8 + 16, ctx_.compute);
   c.count = DevBuf(ctx_.pool, 8, ctx_.compute);
   PSG_CUDA(cudaMemsetAsync(c.count.p, 0, 8, ctx_.compute));
   return c;
@@ -930,7 +937,7 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
   }
   uint64_t rtotal = 0;
   for (int s = 0; s < n; ++s) rtotal += m[static_cast<size_t>(s) * n + me];
-  rcv.buf = DevBuf(ctx_.pool, std::max<uint64_t>(rtotal, 1) * ncols * 8, ctx_.compute);
+  rcv.buf = DevBuf(ctx_.pool, std::max<uint64_t>(rtotal, 1) * ncols * 8 + 16, ctx_.compute);
   rcv.rows = rtotal;
   PSG_NCCL(ncclGroupStart());
   uint64_t soff = 0, roff = 0;
@@ -1472,13 +1479,14 @@ void Execution::stage(Staged& st) {
     ss.ntiles = tiles;
     ss.rows = sb.total_rows;
     ss.bytes = sb.total_bytes;
+    ss.payload = sb.total_payload;
     if (!all.empty()) {
       auto blob = pack_view(all, ss.tile_off);
       ss.segs = DevBuf(ctx_.pool, blob.size(), ctx_.compute);
       PSG_CUDA(cudaMemcpyAsync(ss.segs.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, ctx_.compute));
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
     }
-    st.bytes += sb.total_bytes;
+    st.bytes += sb.total_payload;
   }
 }
 

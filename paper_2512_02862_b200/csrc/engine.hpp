@@ -92,7 +92,8 @@ struct BatchPlan {
   std::vector<uint64_t> rows;               // rows per group
   std::vector<std::vector<uint64_t>> pos;   // [group][needed col] offset in batch buffer
   std::vector<Extent> extents;
-  uint64_t bytes = 0;
+  uint64_t bytes = 0;          // buffer footprint (16-byte aligned chunks + tail padding)
+  uint64_t payload_bytes = 0;  // column-chunk bytes read from the file (algorithmic bytes)
   uint64_t total_rows = 0;
 };
 

@@ -95,7 +95,8 @@ std::string jit_source(const ScanProgram& P) {
   if (mat) s << "  __shared__ uint32_t s_wcnt[8][R], s_woff[8][R];\n  __shared__ unsigned long long s_base;\n";
   if (part) s << "  __shared__ unsigned long long s_part[" << kMaxParts << "];\n";
   if (glob) s << "  __shared__ unsigned long long s_gacc[" << nglob << "];\n";
-  s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  const int wrow = warp * 128 + lane;\n";
+  s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  const int wrow = warp * 128 + lane;\n"
+    << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep; (void)wrow;\n";
   if (part) s << "  for (int i = tid; i < " << kMaxParts << "; i += 256) s_part[i] = 0;\n";
   if (glob) {
     s << "  for (int i = tid; i < " << nglob << "; i += 256) s_gacc[i] = 0;\n";
@@ -159,7 +160,7 @@ std::string jit_source(const ScanProgram& P) {
       s << "      uint32_t bw[R], bm[R];\n"
         << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bm[r] = 0; if ((pass & (1u << r)) && " << V(P.key_reg)
         << "[r] != kEmptyKey) {\n        const uint64_t h2 = " << V(P.key_reg) << "[r] * kBloomMul;\n"
-        << "        bm[r] = bloom_bits(h2, T.bloom_shift); bw[r] = __ldg(T.bloom + (h2 >> T.bloom_shift)); } }\n"
+        << "        bm[r] = bloom_bits(h2, T.bloom_shift); bw[r] = ldg_keep_u32(T.bloom + (h2 >> T.bloom_shift), pol_keep); } }\n"
         << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && " << V(P.key_reg)
         << "[r] != kEmptyKey && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n";
     }
@@ -232,7 +233,7 @@ std::string jit_source(const ScanProgram& P) {
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = bm[r] = 0; const uint64_t key = " << V(P.semi_key_reg)
           << "[r];\n        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t h2 = key * kBloomMul;\n"
           << "          const uint32_t d = part_of(key, static_cast<uint32_t>(P.nparts));\n"
-          << "          bm[r] = bloom_bits(h2, P.semi_shift); bw[r] = __ldg(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift)); } }\n"
+          << "          bm[r] = bloom_bits(h2, P.semi_shift); bw[r] = ldg_keep_u32(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift), pol_keep); } }\n"
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n    }\n";
       }
       s << "    uint32_t ballots[R];\n#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"

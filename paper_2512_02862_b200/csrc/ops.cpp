@@ -18,7 +18,7 @@ Uploaded upload(Ctx& ctx, const HostBatch& b) {
   Uploaded u;
   const uint64_t n = b.rows();
   for (auto& c : b.cols) {
-    u.cols.emplace_back(ctx.pool, std::max<uint64_t>(n, 1) * 8, ctx.compute);
+    u.cols.emplace_back(ctx.pool, std::max<uint64_t>(n, 1) * 8 + 16, ctx.compute);
     if (n) PSG_CUDA(cudaMemcpyAsync(u.cols.back().p, c.data(), n * 8, cudaMemcpyHostToDevice, ctx.compute));
   }
   return u;

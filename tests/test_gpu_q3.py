@@ -200,3 +200,15 @@ def test_errors_are_reference_classes(ctx, pdata, golden):
     with pytest.raises(psg.PsgError) as e:
         ctx.execute_plan(golden["plans"]["canonical"], "/nonexistent")
     assert e.value.kind == "IoFailure"
+
+
+SF10_GOLDEN = (1218662, "2979547", "417235545352", "14897482", "661bdb187378204d")
+
+
+@pytest.mark.parametrize("staged", [False, True])
+def test_sf10_matches_reference_golden(ctx, pdata, golden, staged):
+    d = pdata(10.0)
+    plan = golden["plans"]["canonical"]
+    res = ctx.stage_plan(plan, d).run() if staged else ctx.execute_plan(plan, d)
+    s = summarize(res)
+    assert (s["rows"], s["colsums"][1], s["colsums"][2], s["colsums"][3], s["rowhash"]) == SF10_GOLDEN
