@@ -83,6 +83,11 @@ std::string jit_source(const ScanProgram& P) {
   const bool part = P.sink == SINK_MATERIALIZE && P.nparts > 1;
   const bool glob = P.sink == SINK_PROBE_GLOBAL;
   const int nglob = glob ? 1 + P.n_sum + P.agg.nbs : 0;
+  // Unordered compaction (pipeline-internal materialisation): each warp stages its surviving rows
+  // in shared memory and flushes 128 rows at a time with one global atomic — no block barrier.
+  // The order-preserving variant (tile_offsets, SINK_COUNT: the filter op) keeps the block scan.
+  const bool wstage = P.sink == SINK_MATERIALIZE && P.tile_offsets == nullptr && P.n_out >= 1 && P.n_out <= 4;
+  const bool bscan = mat && !wstage;
   // Block tiles of 1024 rows; warp w owns rows [128w, 128w+128) of the tile, lane-contiguous per
   // r (each warp load = 256 contiguous bytes), so row order inside a tile is (warp, r, lane).
   // Tile descriptors are fetched per warp into registers (lane c holds column c's pointer) and
@@ -92,7 +97,8 @@ std::string jit_source(const ScanProgram& P) {
     << "extern \"C\" __global__ void __launch_bounds__(256, " << (P.sink == SINK_MATERIALIZE || P.sink == SINK_COUNT ? 6 : 8)
     << ") psg_jit_scan(const __grid_constant__ ScanProgram P, "
        "const Segment* __restrict__ segs, const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {\n";
-  if (mat) s << "  __shared__ uint32_t s_wcnt[8][R], s_woff[8][R];\n  __shared__ unsigned long long s_base;\n";
+  if (bscan) s << "  __shared__ uint32_t s_wcnt[8][R], s_woff[8][R];\n  __shared__ unsigned long long s_base;\n";
+  if (wstage) s << "  __shared__ uint64_t s_stg[8][" << P.n_out << "][128];\n";
   if (part) s << "  __shared__ unsigned long long s_part[" << kMaxParts << "];\n";
   if (glob) s << "  __shared__ unsigned long long s_gacc[" << nglob << "];\n";
   s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  const int wrow = warp * 128 + lane;\n"
@@ -108,8 +114,16 @@ std::string jit_source(const ScanProgram& P) {
     << "    const Segment* sg = segs + __ldg(tile_seg + t);\n"
     << "    col = lane < " << nin << " ? sg->col[lane] : nullptr;\n"
     << "    r0 = (t - sg->tile_begin) * 1024ULL;\n"
-    << "    rows = static_cast<int>(min(1024ULL, sg->rows - r0));\n  };\n"
-    << "  const uint64_t* cur_col = nullptr; uint64_t cur_r0 = 0; int cur_rows = 0;\n"
+    << "    rows = static_cast<int>(min(1024ULL, sg->rows - r0));\n  };\n";
+  if (wstage) {
+    s << "  int fill = 0;\n  auto flush = [&]() {\n    __syncwarp();\n    if (fill == 0) return;\n"
+      << "    unsigned long long base = 0;\n    if (lane == 0) base = atomicAdd(P.out_count, static_cast<unsigned long long>(fill));\n"
+      << "    base = __shfl_sync(0xffffffffu, base, 0);\n"
+      << "    for (int i = lane; i < fill; i += 32) { if (base + i >= P.out_cap) continue;\n";
+    for (int o = 0; o < P.n_out; ++o) s << "      P.out_col[" << o << "][base + i] = s_stg[warp][" << o << "][i];\n";
+    s << "    }\n    fill = 0;\n    __syncwarp();\n  };\n";
+  }
+  s << "  const uint64_t* cur_col = nullptr; uint64_t cur_r0 = 0; int cur_rows = 0;\n"
     << "  if (blockIdx.x < ntiles) fetch(blockIdx.x, cur_col, cur_r0, cur_rows);\n"
     << "  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {\n"
     << "    const uint64_t next = tile + gridDim.x;\n"
@@ -236,6 +250,16 @@ std::string jit_source(const ScanProgram& P) {
           << "          bm[r] = bloom_bits(h2, P.semi_shift); bw[r] = ldg_keep_u32(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift), pol_keep); } }\n"
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n    }\n";
       }
+      if (wstage) {
+        s << "    { const uint32_t lt = (1u << lane) - 1u;\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+          << "        const unsigned b = __ballot_sync(0xffffffffu, (pass >> r) & 1u);\n"
+          << "        const int cnt = __popc(b);\n        if (fill + cnt > 128) flush();\n"
+          << "        if ((pass >> r) & 1u) { const int pos = fill + __popc(b & lt);\n";
+        for (int o = 0; o < P.n_out; ++o)
+          s << "          s_stg[warp][" << o << "][pos] = " << V(P.out_reg[o]) << "[r];\n";
+        s << "        }\n        fill += cnt;\n      }\n    }\n";
+      } else {
       s << "    uint32_t ballots[R];\n#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
         << "      ballots[r] = __ballot_sync(0xffffffffu, (pass >> r) & 1u);\n"
         << "      if (lane == 0) s_wcnt[warp][r] = __popc(ballots[r]); }\n    __syncthreads();\n"
@@ -254,6 +278,9 @@ std::string jit_source(const ScanProgram& P) {
           << "        if (pos >= P.out_cap) continue;\n";
         for (int o = 0; o < P.n_out; ++o) s << "        P.out_col[" << o << "][pos] = " << V(P.out_reg[o]) << "[r];\n";
         s << "      }\n    }\n";
+      }
+      }
+      if (P.sink == SINK_MATERIALIZE) {
         if (part)  // warp-aggregated destination histogram: one shared atomic per (warp, dest)
           s << "#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
             << "      const bool on = (pass >> r) & 1u;\n"
@@ -263,8 +290,9 @@ std::string jit_source(const ScanProgram& P) {
       }
     }
   }
-  if (mat) s << "    __syncthreads();\n";  // s_base / s_woff reuse by the next tile
+  if (bscan) s << "    __syncthreads();\n";  // s_base / s_woff reuse by the next tile
   s << "    cur_col = pf_col; cur_r0 = pf_r0; cur_rows = pf_rows;\n  }\n";
+  if (wstage) s << "  flush();\n";
   if (part)
     s << "  __syncthreads();\n  for (int i = tid; i < P.nparts; i += 256) if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
   if (glob) {

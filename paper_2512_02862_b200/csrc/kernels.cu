@@ -546,27 +546,50 @@ void launch_expand_write(LocalTableDev t, const uint64_t* pk, uint64_t n, const 
 }
 
 // ------------------------------------------------------------------------ partition / scatter
-__global__ void k_part_scatter(ColPtrs in, int ncols, uint64_t n, int key_col, int nparts,
-                               const unsigned long long* dest_base, const unsigned long long* dest_cnt,
-                               unsigned long long* cursor, uint64_t* send) {
-  const int lane = threadIdx.x & 31;
-  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x); i0 < n;
-       i0 += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t i = i0 + threadIdx.x;
-    const bool valid = i < n;
-    const uint32_t d = valid ? part_of(in.p[key_col][i], static_cast<uint32_t>(nparts)) : 0xffffffffu;
-    // Warp-aggregated reservation: one atomic per (warp, destination).
-    const unsigned active = __ballot_sync(0xffffffffu, valid);
-    const unsigned peers = __match_any_sync(0xffffffffu, d) & active;
-    unsigned long long base = 0;
-    const int leader = peers ? __ffs(peers) - 1 : 0;
-    if (valid && lane == leader) base = atomicAdd(cursor + d, static_cast<unsigned long long>(__popc(peers)));
-    base = __shfl_sync(0xffffffffu, base, leader);
-    if (valid) {
-      const uint64_t pos = base + __popc(peers & ((1u << lane) - 1u));
+/// Scatter into dest-major send slabs. Each block takes 4096-row chunks: positions inside the chunk
+/// come from warp-aggregated shared-memory counters (one shared atomic per (warp, dest)), then one
+/// global atomic per (block, dest) reserves the chunk's range in each destination's slab.
+constexpr int kScatterPer = 16;  // rows per thread per chunk
+__global__ void __launch_bounds__(256) k_part_scatter(ColPtrs in, int ncols, uint64_t n, int key_col, int nparts,
+                                                      const unsigned long long* dest_base,
+                                                      const unsigned long long* dest_cnt, unsigned long long* cursor,
+                                                      uint64_t* send) {
+  __shared__ unsigned int s_cnt[kMaxParts];
+  __shared__ unsigned long long s_base[kMaxParts];
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int d = tid; d < nparts; d += 256) s_cnt[d] = 0;
+  __syncthreads();
+  constexpr uint64_t kChunk = 256ULL * kScatterPer;
+  for (uint64_t c0 = blockIdx.x * kChunk; c0 < n; c0 += static_cast<uint64_t>(gridDim.x) * kChunk) {
+    uint32_t dest[kScatterPer], pos[kScatterPer];
+#pragma unroll
+    for (int k = 0; k < kScatterPer; ++k) {
+      const uint64_t i = c0 + k * 256 + tid;
+      const bool valid = i < n;
+      const uint32_t d = valid ? part_of(in.p[key_col][i], static_cast<uint32_t>(nparts)) : 0xffffffffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      const int leader = __ffs(peers) - 1;
+      unsigned int old = 0;
+      if (valid && lane == leader) old = atomicAdd(&s_cnt[d], static_cast<unsigned int>(__popc(peers)));
+      old = __shfl_sync(0xffffffffu, old, leader);
+      dest[k] = d;
+      pos[k] = old + __popc(peers & ((1u << lane) - 1u));
+    }
+    __syncthreads();
+    for (int d = tid; d < nparts; d += 256) {
+      s_base[d] = s_cnt[d] ? atomicAdd(cursor + d, static_cast<unsigned long long>(s_cnt[d])) : 0ULL;
+      s_cnt[d] = 0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScatterPer; ++k) {
+      const uint64_t i = c0 + k * 256 + tid;
+      if (i >= n) continue;
+      const uint32_t d = dest[k];
+      const uint64_t at = s_base[d] + pos[k];
       const uint64_t cnt = dest_cnt[d];
       uint64_t* region = send + dest_base[d] * static_cast<uint64_t>(ncols);
-      for (int c = 0; c < ncols; ++c) region[c * cnt + pos] = in.p[c][i];
+      for (int c = 0; c < ncols; ++c) region[c * cnt + at] = in.p[c][i];
     }
   }
 }
@@ -577,8 +600,11 @@ void launch_part_scatter(const uint64_t* const* in_cols, int ncols, uint64_t n, 
   ColPtrs pc{};
   for (int c = 0; c < ncols; ++c) pc.p[c] = in_cols[c];
   count_launch();
-  k_part_scatter<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, ncols, n, key_col, nparts, dest_base, dest_cnt, cursor,
-                                                         send);
+  uint64_t blocks = (n + 256ULL * kScatterPer - 1) / (256ULL * kScatterPer);
+  const uint64_t maxb = static_cast<uint64_t>(sm_count()) * 8;
+  if (blocks > maxb) blocks = maxb;
+  k_part_scatter<<<static_cast<unsigned>(blocks), 256, 0, S(stream)>>>(pc, ncols, n, key_col, nparts, dest_base, dest_cnt,
+                                                                      cursor, send);
 }
 
 __global__ void k_part_ids(const uint64_t* keys, uint64_t n, int nparts, int identity, uint32_t* ids) {
