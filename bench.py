@@ -78,7 +78,7 @@ class Clocks:
             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -205,7 +205,7 @@ def main():
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cores = os.cpu_count() or 1
-    io_threads = args.io_threads or max(2, min(16, cores // max(world, 1)))
+    io_threads = args.io_threads or max(2, min(12, cores // max(world, 1)))
 
     data_root = os.path.join(args.data_dir, "sf%g_n%d" % (args.scale, SHARDS))
     gen_s = 0.0
@@ -257,7 +257,8 @@ def main():
     launches = 0
     probe_ms = probe_bytes = probe_launches = 0
     rows = 0
-    with Clocks(local) as clk:
+    clk = Clocks(local).__enter__()
+    if True:
         wall0 = time.time()
         for _ in range(args.steps):
             sync_all()  # every step starts aligned across ranks (the barrier is outside the engine's events)
@@ -291,6 +292,7 @@ def main():
         io_wait.append(res.stats["io_wait_s"])
         e2e_rows = res.rows.shape[0]
     sync_all()
+    clk.__exit__(None, None, None)
     e2e_s = max_over_ranks(statistics.mean(e2e_t)) if e2e_t else None
     h2d_all, d2h_all = sum_over_ranks(h2d), sum_over_ranks(d2h)
     e2e_groups = sum_over_ranks(e2e_rows)

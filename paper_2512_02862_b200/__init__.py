@@ -152,8 +152,24 @@ def _make_batch(columns: dict, types: dict | None = None):
     return b
 
 
+class _Owner:
+    """Owns a psg_result handle; freed as soon as the last Result/ndarray view referencing it dies
+    (no reference cycle, so the engine's pinned result block returns to its cache immediately)."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    def __del__(self):
+        try:
+            if self.h is not None:
+                lib().psg_result_free(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
 class _View:
-    """Array-interface wrapper whose lifetime pins the owning Result (numpy keeps it as .base)."""
+    """Array-interface wrapper whose lifetime pins the result handle (numpy keeps it as .base)."""
 
     def __init__(self, owner, ptr, n):
         self._owner = owner
@@ -179,21 +195,12 @@ class Result:
         _check(L.psg_result_stats(handle, ctypes.byref(st)))
         self.stats = st.as_dict()
         if cnt:
-            # zero-copy view of the engine's (pinned) result rows; freed with this object
-            self._h = handle
-            self.rows = np.asarray(_View(self, ptr, cnt)).reshape(n.value, k.value)
+            # zero-copy view of the engine's (pinned) result rows
+            self._owner = _Owner(handle)
+            self.rows = np.asarray(_View(self._owner, ptr, cnt)).reshape(n.value, k.value)
         else:
             self.rows = np.zeros((n.value, k.value), np.uint64)
-            self._h = None
             L.psg_result_free(handle)
-
-    def __del__(self):
-        try:
-            if self._h is not None:
-                lib().psg_result_free(self._h)
-                self._h = None
-        except Exception:
-            pass
 
     def column(self, name):
         i = [n for n, _t in self.schema].index(name)
