@@ -115,6 +115,11 @@ int psg_ctx_init_comm(psg_ctx* ctx, const void* id128);
 int psg_ctx_set_ingest(psg_ctx* ctx, int io_threads, uint64_t batch_bytes, int pinned_slots);
 /* Semi-join (Bloom) pre-filter of the shuffled probe side: 1 = on (default), 0 = off. */
 int psg_ctx_set_semijoin(psg_ctx* ctx, int enabled);
+/* Fused NVLink shuffle for grouped aggregates (nranks > 1): build inserts and probe+aggregate go
+ * straight into the owner rank's hash table through CUDA-IPC-mapped peer memory (system-scope
+ * atomics), replacing partition -> count exchange -> ncclSend/Recv -> consume. 1 = on (default
+ * when the symmetric heap could be mapped), 0 = the NCCL path. */
+int psg_ctx_set_fused_shuffle(psg_ctx* ctx, int enabled);
 void psg_ctx_destroy(psg_ctx* ctx);
 
 /* ---- plan execution: execute_plan (pipeline.hpp:153-155, pipeline.cpp:924-929) ----

@@ -29,7 +29,7 @@ STATUS = {0: "OK", 1: "UnknownColumn", 2: "MemoryExceeded", 3: "StreamClosed", 4
           10: "InfeasibleBudget", 11: "MalformedTrace", 12: "EmptyTrace", 100: "CudaError", 101: "NcclError",
           102: "InternalError"}
 EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_unique_id", "psg_ctx_init_comm",
-           "psg_ctx_set_ingest", "psg_ctx_set_semijoin", "psg_ctx_destroy", "psg_execute_plan", "psg_stage_plan",
+           "psg_ctx_set_ingest", "psg_ctx_set_semijoin", "psg_ctx_set_fused_shuffle", "psg_ctx_destroy", "psg_execute_plan", "psg_stage_plan",
            "psg_execute_staged", "psg_staged_free", "psg_result_shape", "psg_result_field", "psg_result_data",
            "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_psto_write",
            "psg_psto_inspect", "psg_gen_tpch", "psg_jit_selftest", "psg_tmin"]
@@ -85,7 +85,8 @@ def lib():
             "psg_abi_version": ([], i32), "psg_last_error": ([], c),
             "psg_ctx_create": ([i32, i32, i32, P(vp)], i32), "psg_comm_unique_id": ([vp], i32),
             "psg_ctx_init_comm": ([vp, vp], i32), "psg_ctx_set_ingest": ([vp, i32, u64, i32], i32),
-            "psg_ctx_set_semijoin": ([vp, i32], i32), "psg_ctx_destroy": ([vp], None),
+            "psg_ctx_set_semijoin": ([vp, i32], i32), "psg_ctx_set_fused_shuffle": ([vp, i32], i32),
+            "psg_ctx_destroy": ([vp], None),
             "psg_execute_plan": ([vp, c, c, i32, P(vp)], i32), "psg_stage_plan": ([vp, c, c, P(vp)], i32),
             "psg_execute_staged": ([vp, vp, i32, P(vp), P(Stats)], i32), "psg_staged_free": ([vp], None),
             "psg_result_shape": ([vp, P(u64), P(ctypes.c_uint32)], i32),
@@ -237,6 +238,10 @@ class Context:
 
     def set_semijoin(self, enabled: bool):
         _check(lib().psg_ctx_set_semijoin(self._h, 1 if enabled else 0))
+
+    def set_fused_shuffle(self, enabled: bool):
+        """nranks > 1: fused NVLink build/probe (True) or the NCCL partition/send/recv path (False)."""
+        _check(lib().psg_ctx_set_fused_shuffle(self._h, 1 if enabled else 0))
 
     def execute_plan(self, plan, data_root, mode="overlapped") -> Result:
         text = plan if isinstance(plan, str) else json.dumps(plan)

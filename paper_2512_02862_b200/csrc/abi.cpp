@@ -152,6 +152,10 @@ int psg_ctx_init_comm(psg_ctx* ctx, const void* id128) {
     std::memcpy(&id, id128, sizeof id);
     const ncclResult_t r = ncclCommInitRank(&ctx->c.nccl, ctx->c.nranks, id, ctx->c.rank);
     if (r != ncclSuccess) throw Error(PSG_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    // symmetric heap for the fused NVLink build/probe path (PSG_SYMM_MB, default 4096; 0 disables)
+    const char* e = std::getenv("PSG_SYMM_MB");
+    const size_t mb = e ? static_cast<size_t>(std::atoll(e)) : 4096;
+    ctx->c.init_symmetric_heap(mb << 20);
   });
 }
 
@@ -168,6 +172,14 @@ int psg_ctx_set_semijoin(psg_ctx* ctx, int enabled) {
   return guarded([&] {
     if (!ctx) throw InvalidInput("null ctx");
     ctx->c.semijoin = enabled != 0;
+  });
+}
+
+int psg_ctx_set_fused_shuffle(psg_ctx* ctx, int enabled) {
+  return guarded([&] {
+    if (!ctx) throw InvalidInput("null ctx");
+    ctx->c.p2p = enabled != 0 && ctx->c.symm_bytes > 0;
+    if (enabled && ctx->c.nranks > 1 && ctx->c.symm_bytes == 0) throw InvalidInput("no symmetric heap (IPC unavailable)");
   });
 }
 

@@ -82,6 +82,14 @@ struct AggTableDev {
   int32_t bloom_shift;  // 64 - log2(bloom words)
 };
 
+/// One rank's aggregation-table arrays as mapped into this process (CUDA IPC symmetric heap).
+struct AggPeer {
+  uint64_t* hot;
+  uint64_t* cold;
+  uint32_t* bloom;
+  uint64_t pad;
+};
+
 struct ScanProgram {
   int32_t n_in;        // regs [0,n_in) load from Segment::col
   int32_t n_pred;      // regs [0,n_pred) are loaded for every row (predicate columns)
@@ -117,6 +125,12 @@ struct ScanProgram {
   uint64_t semi_words;
   int32_t semi_shift;
   int32_t semi_key_reg;
+  // Fused NVLink path (SINK_BUILD / SINK_PROBE with remote = 1): every row's table operation goes
+  // to the owner rank part_of(key) directly in its (peer-mapped) table; tables are symmetric so
+  // mask/shift/hw/cw come from `agg`, only the base pointers differ per rank.
+  const AggPeer* peers;
+  int32_t remote;
+  int32_t pad_remote;
 };
 
 #if defined(__CUDACC__) || defined(__CUDACC_RTC__)

@@ -429,6 +429,8 @@ class Execution {
   BatchView upload_segments(std::vector<Segment> segs, DevBuf& holder);
 
   void build_agg_table(uint64_t build_rows, uint64_t bloom_words);
+  bool build_symmetric_agg_table(uint64_t max_rows, bool bloom);
+  void gpu_barrier();
   void finalize_grouped(ResultRows& out, bool want_rows);
   void finalize_global(ResultRows& out);
 
@@ -453,7 +455,7 @@ class Execution {
   };
   std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
   // agg table
-  DevBuf agg_hot_, agg_cold_, agg_bloom_, global_acc_;
+  DevBuf agg_hot_, agg_cold_, agg_bloom_, global_acc_, barrier_word_;
   AggTableDev aggt_{};
   uint64_t agg_cap_ = 0;
   // stats
@@ -907,6 +909,49 @@ void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words) {
   launch_agg_init(aggt_, agg_cap_, ctx_.compute);
 }
 
+/// Same layout as build_agg_table but carved from the symmetric heap with a capacity every rank
+/// derives from the same (all-reduced) maximum, so offsets match across ranks.
+bool Execution::build_symmetric_agg_table(uint64_t max_rows, bool bloom) {
+  agg_cap_ = pow2_at_least(std::max<uint64_t>(2 * max_rows, 16));
+  const int nps = static_cast<int>(probe_sum_wire.size()), nbs = static_cast<int>(build_sum_wire.size());
+  int hw = 2 + nps;
+  hw = hw <= 2 ? 2 : (hw <= 4 ? 4 : 8 * ((hw + 7) / 8));
+  const int cw = 1 + nbs;
+  const uint64_t words = bloom ? std::min<uint64_t>(pow2_at_least(std::max<uint64_t>(max_rows / 2, 1024)), 8ull << 20) : 0;
+  uint8_t* hot = ctx_.symm_alloc((agg_cap_ + 1) * hw * 8);
+  uint8_t* cold = ctx_.symm_alloc((agg_cap_ + 1) * cw * 8);
+  uint8_t* bl = words ? ctx_.symm_alloc(words * 4) : nullptr;
+  if (!hot || !cold || (words && !bl)) return false;
+  std::memset(&aggt_, 0, sizeof aggt_);
+  aggt_.hot = reinterpret_cast<uint64_t*>(hot);
+  aggt_.cold = reinterpret_cast<uint64_t*>(cold);
+  aggt_.mask = agg_cap_ - 1;
+  aggt_.shift = shift_of(agg_cap_);
+  aggt_.hw = hw;
+  aggt_.cw = cw;
+  aggt_.nps = nps;
+  aggt_.nbs = nbs;
+  for (int i = 0; i < nps; ++i) aggt_.ps_float[i] = psrc_.wire.fields[probe_sum_wire[i]].type == LType::Float64;
+  for (int i = 0; i < nbs; ++i) aggt_.bs_float[i] = bsrc_.wire.fields[build_sum_wire[i]].type == LType::Float64;
+  if (words) {
+    aggt_.bloom = reinterpret_cast<uint32_t*>(bl);
+    aggt_.bloom_mask = words - 1;
+    aggt_.bloom_shift = shift_of(words);
+  }
+  launch_agg_init(aggt_, agg_cap_, ctx_.compute);
+  return true;
+}
+
+/// Device-side barrier across ranks: a one-word all-reduce on the compute stream completes only
+/// after every rank's preceding kernels (including their peer-memory writes) have finished.
+void Execution::gpu_barrier() {
+  if (!barrier_word_.p) {
+    barrier_word_ = DevBuf(ctx_.pool, 8, ctx_.compute);
+    PSG_CUDA(cudaMemsetAsync(barrier_word_.p, 0, 8, ctx_.compute));
+  }
+  PSG_NCCL(ncclAllReduce(barrier_word_.p, barrier_word_.p, 1, ncclUint64, ncclMax, ctx_.nccl, ctx_.compute));
+}
+
 // ---------------------------------------------------------------------------- shuffle
 Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data) {
   const int n = ctx_.nranks;
@@ -1074,11 +1119,20 @@ ResultRows Execution::run(bool want_rows) {
   auto bfeed = open_feed(*bsrc_.scan, file_cols_of(bsrc_, bm));
   std::vector<Received> brecv;
   DevCols bmat;
-  if (nr == 1) {
+  // Fused NVLink path (grouped aggregates, N > 1): no shuffle of rows at all — build keys are
+  // inserted into, and probe rows aggregated in, the owner rank's table through peer memory.
+  const bool p2p = nr > 1 && agg_ && grouped_ && ctx_.p2p && ctx_.symm_bytes > 0 && jit_available();
+  ctx_.symm_top = 0;
+  DevBuf owner_hist;
+  if (nr == 1 || p2p) {
     bmat = alloc_cols(b_out.size(), std::max<uint64_t>(bfeed->total_rows, 1));
+    if (p2p) {
+      owner_hist = DevBuf(ctx_.pool, nr * 8, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(owner_hist.p, 0, nr * 8, ctx_.compute));
+    }
     BatchView v;
     while (bfeed->next(v)) {
-      materialize_into(bmat, bp, v, b_out, -1, nullptr);
+      materialize_into(bmat, bp, v, b_out, p2p ? b_out[0] : -1, p2p ? &owner_hist : nullptr);
       bfeed->done();
       st_.ingest_bytes += v.bytes;
     }
@@ -1107,9 +1161,22 @@ ResultRows Execution::run(bool want_rows) {
   }
   pt.mark("build side scan", ctx_.compute);
   uint64_t build_rows = 0;
-  if (nr == 1) build_rows = bmat.rows;
-  else
+  uint64_t p2p_max_rows = 0;
+  if (p2p) {
+    // rows each owner will hold = sum over ranks of the per-owner histograms
+    std::vector<uint64_t> local(nr), owners(nr);
+    PSG_CUDA(cudaMemcpyAsync(local.data(), owner_hist.p, nr * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    PSG_NCCL(ncclAllReduce(owner_hist.p, owner_hist.p, nr, ncclUint64, ncclSum, ctx_.nccl, ctx_.compute));
+    PSG_CUDA(cudaMemcpyAsync(owners.data(), owner_hist.p, nr * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    build_rows = owners[ctx_.rank];
+    for (uint64_t x : owners) p2p_max_rows = std::max(p2p_max_rows, x);
+    st_.bytes_received += (owners[ctx_.rank] - local[ctx_.rank]) * 8 * b_out.size();
+  } else if (nr == 1) {
+    build_rows = bmat.rows;
+  } else {
     for (auto& r : brecv) build_rows += r.rows;
+  }
 
   // Program over materialised build rows: reg k = column k of the materialised batch.
   auto batch_program = [&](int ncols) {
@@ -1124,7 +1191,7 @@ ResultRows Execution::run(bool want_rows) {
     return p;
   };
   std::vector<Segment> bsegs;
-  if (nr == 1) {
+  if (nr == 1 || p2p) {
     Segment sg;
     std::memset(&sg, 0, sizeof sg);
     for (size_t c = 0; c < b_out.size(); ++c) sg.col[c] = bmat.cols[c].as<uint64_t>();
@@ -1145,7 +1212,7 @@ ResultRows Execution::run(bool want_rows) {
   // size the filter from the largest build side so the filters line up.
   DevBuf semi_all;
   uint64_t bloom_words = 0;
-  const bool semi = agg_ && nr > 1 && ctx_.semijoin;
+  const bool semi = agg_ && nr > 1 && ctx_.semijoin && !p2p;
   if (agg_) {
     uint64_t sized_rows = build_rows;
     if (semi) {
@@ -1160,7 +1227,44 @@ ResultRows Execution::run(bool want_rows) {
     if (semi || ((cap + 1) * hw_est * 8 > (48ull << 20) && ctx_.semijoin))
       bloom_words = std::min<uint64_t>(pow2_at_least(std::max<uint64_t>(sized_rows / 2, 1024)), 8ull << 20);
   }
-  if (agg_) {
+  DevBuf peers_dev;
+  bool p2p_ok = p2p;
+  if (p2p) {
+    // symmetric tables: identical capacity on every rank (sized from the largest owner), carved
+    // from the IPC-mapped heap in the same order everywhere so peers find them at equal offsets
+    p2p_ok = build_symmetric_agg_table(p2p_max_rows, ctx_.semijoin);
+    if (!p2p_ok) throw Error(PSG_ERR_MEMORY_EXCEEDED, "symmetric heap too small for the aggregation table (raise PSG_SYMM_MB)");
+    std::vector<AggPeer> peers(nr);
+    const size_t hot_off = reinterpret_cast<uint8_t*>(aggt_.hot) - ctx_.symm;
+    const size_t cold_off = reinterpret_cast<uint8_t*>(aggt_.cold) - ctx_.symm;
+    const size_t bloom_off = aggt_.bloom ? reinterpret_cast<uint8_t*>(aggt_.bloom) - ctx_.symm : 0;
+    for (int q = 0; q < nr; ++q) {
+      peers[q].hot = reinterpret_cast<uint64_t*>(ctx_.symm_peer[q] + hot_off);
+      peers[q].cold = reinterpret_cast<uint64_t*>(ctx_.symm_peer[q] + cold_off);
+      peers[q].bloom = aggt_.bloom ? reinterpret_cast<uint32_t*>(ctx_.symm_peer[q] + bloom_off) : nullptr;
+      peers[q].pad = 0;
+    }
+    peers_dev = DevBuf(ctx_.pool, nr * sizeof(AggPeer), ctx_.compute);
+    PSG_CUDA(cudaMemcpyAsync(peers_dev.p, peers.data(), nr * sizeof(AggPeer), cudaMemcpyHostToDevice, ctx_.compute));
+    gpu_barrier();  // every owner's table is initialised before anyone inserts
+    ScanProgram p = batch_program(static_cast<int>(b_out.size()));
+    p.sink = SINK_BUILD;
+    p.agg = aggt_;
+    p.remote = 1;
+    p.peers = peers_dev.as<AggPeer>();
+    p.nparts = nr;
+    p.n_sum = static_cast<int>(build_sum_wire.size());
+    for (int b = 0; b < p.n_sum; ++b) p.sum_reg[b] = 1 + b;
+    run_scan(p, bview, false);
+    gpu_barrier();  // all inserts (and Bloom bits) landed in every owner's table
+    if (aggt_.bloom) {
+      bloom_words = aggt_.bloom_mask + 1;
+      semi_all = DevBuf(ctx_.pool, static_cast<size_t>(nr) * bloom_words * 4, ctx_.compute);
+      for (int q = 0; q < nr; ++q)
+        PSG_CUDA(cudaMemcpyAsync(semi_all.as<uint32_t>() + q * bloom_words, peers[q].bloom, bloom_words * 4,
+                                 cudaMemcpyDeviceToDevice, ctx_.compute));
+    }
+  } else if (agg_) {
     pt.mark("  pre agg alloc", ctx_.compute);
     build_agg_table(build_rows, bloom_words);
     pt.mark("  agg alloc+init", ctx_.compute);
@@ -1284,7 +1388,31 @@ ResultRows Execution::run(bool want_rows) {
     }
   };
 
-  if (nr == 1 && agg_) {
+  if (p2p) {
+    ScanProgram p = pp;
+    p.sink = SINK_PROBE;
+    p.agg = aggt_;
+    p.agg.bloom = nullptr;
+    p.remote = 1;
+    p.peers = peers_dev.as<AggPeer>();
+    p.nparts = nr;
+    if (aggt_.bloom) {
+      p.semi_bloom = semi_all.as<uint32_t>();
+      p.semi_words = bloom_words;
+      p.semi_shift = aggt_.bloom_shift;
+      p.semi_key_reg = pm.reg_of.at(psrc_.stage_refs.back()[pkey]);
+    }
+    p.key_reg = pm.reg_of.at(psrc_.stage_refs.back()[pkey]);
+    p.n_sum = static_cast<int>(probe_sum_wire.size());
+    for (int s = 0; s < p.n_sum; ++s) p.sum_reg[s] = pm.reg_of.at(psrc_.stage_refs.back()[probe_sum_wire[s]]);
+    BatchView v;
+    while (pfeed->next(v)) {
+      run_scan(p, v, staged_ != nullptr);
+      pfeed->done();
+      st_.ingest_bytes += v.bytes;
+    }
+    gpu_barrier();  // every rank's probe contributions landed before owners finalise
+  } else if (nr == 1 && agg_) {
     ScanProgram p = pp;
     p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
     p.agg = aggt_;

@@ -161,6 +161,20 @@ struct Ctx {
   uint64_t pinned_slot_bytes = 0;
   // Device event-time accounting of the dominant probe kernel.
   cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+  // Symmetric heap for the fused NVLink path (nranks > 1): one cudaMalloc'ed region per rank,
+  // mapped into every peer with CUDA IPC; per-query bump allocation in identical order on all
+  // ranks gives identical offsets, so a peer's table is symm_peer[p] + offset.
+  uint8_t* symm = nullptr;
+  size_t symm_bytes = 0, symm_top = 0;
+  std::vector<uint8_t*> symm_peer;
+  bool p2p = true;
+  void init_symmetric_heap(size_t bytes);  // collective over the NCCL communicator
+  uint8_t* symm_alloc(size_t bytes) {       // nullptr when the heap is exhausted
+    const size_t off = (symm_top + 255) & ~size_t(255);
+    if (!symm || off + bytes > symm_bytes) return nullptr;
+    symm_top = off + bytes;
+    return symm + off;
+  }
   void ensure_pinned(int nslots, uint64_t slot_bytes);
   ~Ctx();
 };

@@ -150,8 +150,68 @@ void Ctx::ensure_pinned(int nslots, uint64_t slot_bytes) {
   pinned_slot_bytes = slot_bytes;
 }
 
+void Ctx::init_symmetric_heap(size_t bytes) {
+  if (nranks < 2 || !nccl || bytes == 0) return;
+  cudaIpcMemHandle_t mine;
+  std::vector<cudaIpcMemHandle_t> all(nranks);
+  bool ok = cudaMalloc(&symm, bytes) == cudaSuccess;
+  if (ok) ok = cudaIpcGetMemHandle(&mine, symm) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    std::memset(&mine, 0, sizeof mine);
+  }
+  // all-gather the handles (and each rank's ok flag) over NCCL
+  const size_t hb = sizeof(cudaIpcMemHandle_t) + 8;
+  std::vector<uint8_t> blob(hb, 0);
+  std::memcpy(blob.data(), &mine, sizeof mine);
+  blob[sizeof mine] = ok ? 1 : 0;
+  void *d_in = nullptr, *d_out = nullptr;
+  PSG_CUDA(cudaMalloc(&d_in, hb));
+  PSG_CUDA(cudaMalloc(&d_out, hb * nranks));
+  PSG_CUDA(cudaMemcpy(d_in, blob.data(), hb, cudaMemcpyHostToDevice));
+  if (ncclAllGather(d_in, d_out, hb, ncclUint8, nccl, compute) != ncclSuccess) throw Error(PSG_ERR_NCCL, "handle all-gather");
+  std::vector<uint8_t> got(hb * nranks);
+  PSG_CUDA(cudaMemcpyAsync(got.data(), d_out, got.size(), cudaMemcpyDeviceToHost, compute));
+  PSG_CUDA(cudaStreamSynchronize(compute));
+  cudaFree(d_in);
+  cudaFree(d_out);
+  bool all_ok = true;
+  for (int p = 0; p < nranks; ++p) all_ok = all_ok && got[p * hb + sizeof(cudaIpcMemHandle_t)] == 1;
+  symm_peer.assign(nranks, nullptr);
+  for (int p = 0; p < nranks && all_ok; ++p) {
+    if (p == rank) {
+      symm_peer[p] = symm;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, got.data() + p * hb, sizeof h);
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      all_ok = false;
+      break;
+    }
+    symm_peer[p] = static_cast<uint8_t*>(ptr);
+  }
+  // every rank must agree: a single failure anywhere disables the fused path everywhere
+  int flag = all_ok ? 1 : 0;
+  int* d_flag = nullptr;
+  PSG_CUDA(cudaMalloc(&d_flag, sizeof(int)));
+  PSG_CUDA(cudaMemcpy(d_flag, &flag, sizeof(int), cudaMemcpyHostToDevice));
+  if (ncclAllReduce(d_flag, d_flag, 1, ncclInt32, ncclMin, nccl, compute) != ncclSuccess)
+    throw Error(PSG_ERR_NCCL, "p2p vote");
+  PSG_CUDA(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, compute));
+  PSG_CUDA(cudaStreamSynchronize(compute));
+  cudaFree(d_flag);
+  p2p = flag == 1;
+  symm_bytes = p2p ? bytes : 0;
+}
+
 Ctx::~Ctx() {
   cudaSetDevice(device);
+  for (int p = 0; p < static_cast<int>(symm_peer.size()); ++p)
+    if (p != rank && symm_peer[p]) cudaIpcCloseMemHandle(symm_peer[p]);
+  if (symm) cudaFree(symm);
   for (void* p : pinned) cudaFreeHost(p);
   if (nccl) ncclCommDestroy(nccl);
   if (ev_a) cudaEventDestroy(ev_a);

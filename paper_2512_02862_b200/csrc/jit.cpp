@@ -73,6 +73,78 @@ void emit_loads(std::ostringstream& s, int lo, int hi) {
   }
 }
 
+/// Semi-join screen against the all-gathered per-owner Bloom filters (local copy).
+void emit_semi(std::ostringstream& s, const ScanProgram& P) {
+  s << "    { uint32_t bw[R], bm[R];\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = bm[r] = 0; const uint64_t key = " << V(P.semi_key_reg)
+    << "[r];\n        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t h2 = key * kBloomMul;\n"
+    << "          const uint32_t d = part_of(key, static_cast<uint32_t>(P.nparts));\n"
+    << "          bm[r] = bloom_bits(h2, P.semi_shift); bw[r] = ldg_keep_u32(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift), pol_keep); } }\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n    }\n";
+}
+
+/// Fused build over NVLink: each key is inserted straight into its owner's (peer-mapped) table.
+void emit_remote_build(std::ostringstream& s, const ScanProgram& P) {
+  const int hw = P.agg.hw, cw = P.agg.cw;
+  s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R]; unsigned long long pv[R];\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0; pv[r] = kEmptyKey; if (!(pass & (1u << r))) continue;\n"
+    << "        const uint64_t key = " << V(P.key_reg) << "[r];\n"
+    << "        if (key == kEmptyKey) { sl[r] = T.mask + 1; continue; }\n"
+    << "        uint64_t* hot = P.peers[part_of(key, static_cast<uint32_t>(P.nparts))].hot;\n"
+    << "        sl[r] = slot_of(key, T.shift);\n"
+    << "        pv[r] = atomicCAS_system(reinterpret_cast<unsigned long long*>(hot + sl[r] * " << hw << "), kEmptyKey, key); }\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+    << "        const uint64_t key = " << V(P.key_reg) << "[r];\n"
+    << "        const AggPeer pe = P.peers[part_of(key, static_cast<uint32_t>(P.nparts))];\n"
+    << "        uint64_t sx = sl[r]; bool dup = pv[r] == key;\n"
+    << "        if (pv[r] != kEmptyKey && pv[r] != key) {\n"
+    << "          sx = (sx + 1) & T.mask;\n"
+    << "          while (true) { const unsigned long long prev = atomicCAS_system(reinterpret_cast<unsigned long long*>(pe.hot + sx * "
+    << hw << "), kEmptyKey, key);\n"
+    << "            if (prev == kEmptyKey || prev == key) { dup = prev == key; break; } sx = (sx + 1) & T.mask; } }\n"
+    << "        unsigned long long* cold = reinterpret_cast<unsigned long long*>(pe.cold + sx * " << cw << ");\n"
+    << "        if (sx == T.mask + 1 || dup) atomicAdd_system(cold, 1ULL);\n"
+    << "        else if (pe.bloom != nullptr) { const uint64_t h2 = key * kBloomMul;\n"
+    << "          atomicOr_system(pe.bloom + (h2 >> T.bloom_shift), bloom_bits(h2, T.bloom_shift)); }\n";
+  for (int bb = 0; bb < P.n_sum; ++bb) {
+    if (P.agg.bs_float[bb])
+      s << "        atomicAdd_system(reinterpret_cast<double*>(cold + " << 1 + bb << "), __longlong_as_double(static_cast<long long>("
+        << V(P.sum_reg[bb]) << "[r])));\n";
+    else
+      s << "        atomicAdd_system(cold + " << 1 + bb << ", static_cast<unsigned long long>(" << V(P.sum_reg[bb]) << "[r]));\n";
+  }
+  s << "      }\n    }\n";
+}
+
+/// Fused probe + aggregation over NVLink: semi-join screen locally, then probe the owner's
+/// (peer-mapped) table and accumulate in its slot with system-scope atomics.
+void emit_remote_probe(std::ostringstream& s, const ScanProgram& P) {
+  const int hw = P.agg.hw, cw = P.agg.cw;
+  if (P.semi_bloom) emit_semi(s, P);
+  s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R], k0[R]; uint64_t* hb[R];\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = ~0ULL; k0[r] = 0; hb[r] = nullptr; if (!(pass & (1u << r))) continue;\n"
+    << "        const uint64_t key = " << V(P.key_reg) << "[r];\n"
+    << "        const AggPeer pe = P.peers[part_of(key, static_cast<uint32_t>(P.nparts))];\n        hb[r] = pe.hot;\n"
+    << "        if (key == kEmptyKey) { if (pe.cold[(T.mask + 1) * " << cw << "] == 0) pass &= ~(1u << r); else sl[r] = T.mask + 1; }\n"
+    << "        else { sl[r] = slot_of(key, T.shift); k0[r] = hb[r][sl[r] * " << hw << "]; } }\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r)) || sl[r] == T.mask + 1) continue;\n"
+    << "        const uint64_t key = " << V(P.key_reg) << "[r]; uint64_t sx = sl[r], kk = k0[r];\n"
+    << "        while (kk != key && kk != kEmptyKey) { sx = (sx + 1) & T.mask; kk = hb[r][sx * " << hw << "]; }\n"
+    << "        if (kk != key) pass &= ~(1u << r); else sl[r] = sx; }\n";
+  emit_loads(s, P.n_early, P.n_in);
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+    << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(hb[r] + sl[r] * " << hw << ");\n"
+    << "        atomicAdd_system(h + 1, 1ULL);\n";
+  for (int p = 0; p < P.n_sum; ++p) {
+    if (P.agg.ps_float[p])
+      s << "        atomicAdd_system(reinterpret_cast<double*>(h + " << 2 + p << "), __longlong_as_double(static_cast<long long>("
+        << V(P.sum_reg[p]) << "[r])));\n";
+    else
+      s << "        atomicAdd_system(h + " << 2 + p << ", static_cast<unsigned long long>(" << V(P.sum_reg[p]) << "[r]));\n";
+  }
+  s << "      }\n    }\n";
+}
+
 }  // namespace
 
 std::string jit_source(const ScanProgram& P) {
@@ -167,7 +239,12 @@ std::string jit_source(const ScanProgram& P) {
     }
     s << "      }\n    }\n";
   }
-  if (probe) {
+  if (P.remote && P.sink == SINK_PROBE) {
+    emit_remote_probe(s, P);
+  } else if (P.remote && P.sink == SINK_BUILD) {
+    emit_loads(s, P.n_early, P.n_in);
+    emit_remote_build(s, P);
+  } else if (probe) {
     const bool bloom = P.agg.bloom != nullptr;
     s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R], k0[R];\n";
     if (bloom) {
@@ -399,8 +476,11 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
       return;
     }
   }
+  if (P.remote) throw Error(PSG_ERR_INTERNAL, "the fused NVLink path needs the query compiler (PSG_JIT)");
   launch_scan(P, d_segs, d_tile_seg, nsegs, ntiles, stream);
 }
+
+bool jit_available() { return jit_enabled(); }
 
 int jit_selftest(std::string& log) {
   // Representative program structures: every sink, int/float atoms, a local join with payload,
@@ -458,6 +538,22 @@ int jit_selftest(std::string& log) {
     p.n_out = 2;
     p.out_reg[0] = 2, p.out_reg[1] = 4;
     p.tile_offsets = reinterpret_cast<const uint64_t*>(16);
+    progs.push_back(p);
+  }
+  for (int sink : {SINK_BUILD, SINK_PROBE}) {
+    ScanProgram p = base();
+    p.sink = sink;
+    p.remote = 1;
+    p.nparts = 4;
+    p.n_sum = 2;
+    p.sum_reg[0] = 2;
+    p.sum_reg[1] = 3;
+    p.agg.hw = 4;
+    p.agg.cw = 2;
+    p.agg.ps_float[1] = 1;
+    p.agg.bs_float[1] = 1;
+    p.semi_bloom = reinterpret_cast<const uint32_t*>(16);
+    p.semi_key_reg = 1;
     progs.push_back(p);
   }
   int failures = 0;

@@ -22,6 +22,8 @@ struct JitStats {
   bool enabled;
 };
 JitStats jit_stats();
+/// Query compiler usable (required by the fused NVLink path, which has no interpreter variant).
+bool jit_available();
 /// Compiles representative program structures with NVRTC (no GPU needed); returns failures.
 int jit_selftest(std::string& log);
 

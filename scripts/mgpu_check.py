@@ -59,8 +59,15 @@ def main():
              ("global_agg", 0.01, 42, 1 << 20), ("empty", 0.002, 42, 1 << 20),
              ("no_aggregate", 0.002, 42, 64 << 10), ("smoke_py", 0.002, 11, 1 << 20),
              ("pipeline_test", 0.004, 42, 64 << 10)]
-    for semijoin in (True, False):
+    variants = [(True, True), (True, False), (False, True), (False, False)]  # (fused NVLink, semi-join)
+    for fused, semijoin in variants:
         ctx.set_semijoin(semijoin)
+        try:
+            ctx.set_fused_shuffle(fused)
+        except psg.PsgError:
+            if rank == 0:
+                print("fused NVLink path unavailable; skipping fused variants")
+            continue
         for pname, scale, seed, rg in cases:
             d = data(scale, seed, rg)
             plan = golden["plans"][pname]
@@ -74,7 +81,7 @@ def main():
                 dist.all_gather_object(allres, mine)
                 if rank == 0:
                     if any(x[0] == "error" for x in allres):
-                        failures.append((pname, mode, semijoin, [x for x in allres if x[0] == "error"]))
+                        failures.append((pname, mode, fused, semijoin, [x for x in allres if x[0] == "error"]))
                         continue
                     got = po.summary(allres)
                     g = [r for r in golden["results"] if r["plan"] == pname and r["nodes"] == world
@@ -86,11 +93,11 @@ def main():
                         want = po.summary(po.execute(json.dumps(plan), d, world))
                         src = "oracle"
                     ok = all(got[k] == want[k] for k in ("rows", "rowhash", "colsums", "per_node_rows"))
-                    print("%-22s %-10s semijoin=%d %-9s %s rows=%d per_node=%s" % (
-                        pname, mode, semijoin, src, "OK " if ok else "BAD", got["rows"], got["per_node_rows"]),
+                    print("%-22s %-10s fused=%d semijoin=%d %-9s %s rows=%d per_node=%s" % (
+                        pname, mode, fused, semijoin, src, "OK " if ok else "BAD", got["rows"], got["per_node_rows"]),
                         flush=True)
                     if not ok:
-                        failures.append((pname, mode, semijoin, got, want))
+                        failures.append((pname, mode, fused, semijoin, got, want))
     if rank == 0:
         print("FAILURES", len(failures))
         for f in failures:

@@ -23,6 +23,8 @@ obj = [psg.Context.unique_id() if rank == 0 else None]
 dist.broadcast_object_list(obj, src=0)
 ctx = psg.Context(local, rank, world, obj[0])
 ctx.set_ingest(io_threads=8, batch_bytes=64 << 20)
+if os.environ.get("PSG_FUSED", "1") == "0":
+    ctx.set_fused_shuffle(False)
 st = ctx.stage_plan(bench.plan_for([k for k in range(bench.SHARDS) if k % world == rank], 8), root)
 for i in range(4):
     dist.barrier()
