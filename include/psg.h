@@ -117,8 +117,9 @@ int psg_ctx_set_ingest(psg_ctx* ctx, int io_threads, uint64_t batch_bytes, int p
 int psg_ctx_set_semijoin(psg_ctx* ctx, int enabled);
 /* Fused NVLink shuffle for grouped aggregates (nranks > 1): build inserts and probe+aggregate go
  * straight into the owner rank's hash table through CUDA-IPC-mapped peer memory (system-scope
- * atomics), replacing partition -> count exchange -> ncclSend/Recv -> consume. 1 = on (default
- * when the symmetric heap could be mapped), 0 = the NCCL path. */
+ * atomics), replacing partition -> count exchange -> ncclSend/Recv -> consume. Collective on the
+ * first enable (maps every peer's symmetric heap, PSG_SYMM_MB, default 4096). 0 (default) = the
+ * NCCL path, which measured faster for Q3 (remote atomics cost NVLink bandwidth). */
 int psg_ctx_set_fused_shuffle(psg_ctx* ctx, int enabled);
 void psg_ctx_destroy(psg_ctx* ctx);
 

@@ -152,10 +152,7 @@ int psg_ctx_init_comm(psg_ctx* ctx, const void* id128) {
     std::memcpy(&id, id128, sizeof id);
     const ncclResult_t r = ncclCommInitRank(&ctx->c.nccl, ctx->c.nranks, id, ctx->c.rank);
     if (r != ncclSuccess) throw Error(PSG_ERR_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
-    // symmetric heap for the fused NVLink build/probe path (PSG_SYMM_MB, default 4096; 0 disables)
-    const char* e = std::getenv("PSG_SYMM_MB");
-    const size_t mb = e ? static_cast<size_t>(std::atoll(e)) : 4096;
-    ctx->c.init_symmetric_heap(mb << 20);
+
   });
 }
 
@@ -178,8 +175,15 @@ int psg_ctx_set_semijoin(psg_ctx* ctx, int enabled) {
 int psg_ctx_set_fused_shuffle(psg_ctx* ctx, int enabled) {
   return guarded([&] {
     if (!ctx) throw InvalidInput("null ctx");
+    if (enabled && ctx->c.nranks > 1 && ctx->c.symm == nullptr) {
+      // collective: every rank enables the fused path together (maps every peer's heap)
+      const char* e = std::getenv("PSG_SYMM_MB");
+      const size_t mb = e ? static_cast<size_t>(std::atoll(e)) : 4096;
+      PSG_CUDA(cudaSetDevice(ctx->c.device));
+      ctx->c.init_symmetric_heap(mb << 20);
+    }
+    if (enabled && ctx->c.nranks > 1 && ctx->c.symm_bytes == 0) throw InvalidInput("no symmetric heap (CUDA IPC unavailable)");
     ctx->c.p2p = enabled != 0 && ctx->c.symm_bytes > 0;
-    if (enabled && ctx->c.nranks > 1 && ctx->c.symm_bytes == 0) throw InvalidInput("no symmetric heap (IPC unavailable)");
   });
 }
 

@@ -167,7 +167,7 @@ struct Ctx {
   uint8_t* symm = nullptr;
   size_t symm_bytes = 0, symm_top = 0;
   std::vector<uint8_t*> symm_peer;
-  bool p2p = true;
+  bool p2p = false;  // opt-in (psg_ctx_set_fused_shuffle); the NCCL path measured faster for Q3
   void init_symmetric_heap(size_t bytes);  // collective over the NCCL communicator
   uint8_t* symm_alloc(size_t bytes) {       // nullptr when the heap is exhausted
     const size_t off = (symm_top + 255) & ~size_t(255);
