@@ -498,10 +498,16 @@ struct StreamSession {
   std::vector<DevBuf> slots;
   std::vector<cudaEvent_t> slot_free, copied;
   uint64_t slot_bytes = 0;
+  int regulated_slots = 0;
   size_t cursor = 0;  // next batch to consume (global order)
   int cur_slot = -1;
 
-  StreamSession(Ctx& c, const std::vector<std::pair<const ScanNode*, std::vector<int>>>& scans) : ctx(c) {
+  /// budget/ht_reserve: plan memory_budget_bytes and the bytes set aside for hash tables; the ring
+  /// depth is regulated to fit (regulate, pipeline.cpp:198-240): InfeasibleBudget when not even one
+  /// chunk batch fits, like a queue that cannot hold one chunk.
+  StreamSession(Ctx& c, const std::vector<std::pair<const ScanNode*, std::vector<int>>>& scans, uint64_t budget = 0,
+                uint64_t ht_reserve = 0)
+      : ctx(c) {
     uint64_t max_bytes = 0, max_segs = 0;
     for (auto& [scan, fcols] : scans) {
       const std::string key = scan_key(*scan, fcols);
@@ -536,7 +542,18 @@ struct StreamSession {
     const int threads = std::max(1, ctx.io_threads);
     const int pinned = ctx.pinned_slots > 0 ? ctx.pinned_slots : threads * 2 + 2;
     ingest = std::make_unique<Ingest>(ctx, files, batches, threads, slot_bytes, pinned);
-    const int nd = static_cast<int>(std::min<size_t>(batches.size(), 8));
+    int nd = static_cast<int>(std::min<size_t>(batches.size(), 8));
+    if (budget) {
+      const uint64_t fixed = ht_reserve + 2 * slot_bytes;  // tables + materialisation transients
+      if (fixed >= budget)
+        throw InfeasibleBudget("fixed residents (" + std::to_string(fixed) + " bytes) leave no room for the chunk ring in a budget of " +
+                               std::to_string(budget));
+      const uint64_t fit = (budget - fixed) / slot_bytes;
+      if (fit < 1)
+        throw InfeasibleBudget("the chunk ring cannot hold even one batch of " + std::to_string(slot_bytes) + " bytes");
+      nd = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(nd), fit));
+    }
+    regulated_slots = nd;
     for (int k = 0; k < nd; ++k) {
       slots.emplace_back(ctx.pool, slot_bytes, ctx.copy);
       cudaEvent_t x, y;
@@ -1101,7 +1118,13 @@ ResultRows Execution::run(bool want_rows) {
   for (size_t j = 0; j < bsrc_.chain.size(); ++j) bsrc_.chain[j].needed_payload = bm.payload_cols[j];
   for (size_t j = 0; j < psrc_.chain.size(); ++j) psrc_.chain[j].needed_payload = pm.payload_cols[j];
 
-  if (!staged_) session_ = std::make_unique<StreamSession>(ctx_, scan_list(bm, pm));
+  if (!staged_) {
+    // hash-table reservation for the ring regulation: the plan's estimate, else the reference
+    // planner's fallback of a quarter of the budget (pipeline.cpp:588-593)
+    uint64_t ht_reserve = plan_.ht_estimate_bytes;
+    if (ht_reserve == 0 && plan_.memory_budget_bytes) ht_reserve = plan_.memory_budget_bytes / 4;
+    session_ = std::make_unique<StreamSession>(ctx_, scan_list(bm, pm), plan_.memory_budget_bytes, ht_reserve);
+  }
   const auto t_storage = Clock::now();
   PhaseTimer pt;
   pt.mark("compile", ctx_.compute);
@@ -1636,7 +1659,18 @@ ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::strin
   // Phase-sequential modes: storage phase materialises every needed chunk in HBM, then the
   // network/compute phase runs over the staged images (run_phased, pipeline.cpp:506-556).
   const auto t0 = Clock::now();
-  std::unique_ptr<Staged> st(stage_plan(ctx, plan_json, data_root));
+  // Phase-sequential modes materialise every needed chunk: under a plan budget smaller than the
+  // staged input this raises MemoryExceeded, like the reference's blocking reader (scan.cpp:289-292).
+  const QueryPlan budget_plan = QueryPlan::from_json_text(plan_json, data_root, ctx.rank, ctx.nranks);
+  if (budget_plan.memory_budget_bytes) ctx.pool.set_budget(ctx.pool.used() + budget_plan.memory_budget_bytes);
+  std::unique_ptr<Staged> st;
+  try {
+    st.reset(stage_plan(ctx, plan_json, data_root));
+  } catch (...) {
+    ctx.pool.set_budget(0);
+    throw;
+  }
+  ctx.pool.set_budget(0);
   const double storage = secs_since(t0);
   Execution ex(ctx, plan_json, data_root, mode, st.get());
   ResultRows r = ex.run(want_rows);

@@ -1,0 +1,85 @@
+"""Randomised plans vs the oracle on the GPU: predicates (all six operators, int and float
+literals, several atoms per scan), projections, build- and probe-side sums, grouped / global /
+no aggregate, all four modes. Seeded, so failures reproduce."""
+import json
+import random
+
+import pytest
+
+import paper_2512_02862_b200 as psg
+from oracle import plan_oracle as po
+
+pytestmark = pytest.mark.gpu
+
+OPS = ["<", "<=", "==", "!=", ">=", ">"]
+RANGES = {"c_mktsegment": (0, 4), "o_custkey": (0, 1500), "o_orderdate": (19920101, 19981228),
+          "o_shippriority": (0, 4), "o_orderkey": (0, 15000), "l_orderkey": (0, 15000),
+          "l_extendedprice": (90000, 189999), "l_discount": (0, 10), "l_shipdate": (19920101, 19981228)}
+
+
+def _atoms(rng, cols):
+    out = []
+    for _ in range(rng.randint(0, 3)):
+        c = rng.choice(cols)
+        lo, hi = RANGES[c]
+        v = rng.randint(lo, hi)
+        if rng.random() < 0.2:
+            v = v + 0.5
+        out.append({"col": c, "op": rng.choice(OPS), "value": v})
+    return out
+
+
+def random_plan(rng):
+    ocols = ["o_orderkey", "o_custkey", "o_orderdate", "o_shippriority"]
+    lcols = ["l_orderkey", "l_extendedprice", "l_discount", "l_shipdate"]
+    opred = _atoms(rng, ["o_orderdate", "o_shippriority", "o_custkey"])
+    lpred = _atoms(rng, ["l_shipdate", "l_discount", "l_extendedprice"])
+    cpred = _atoms(rng, ["c_mktsegment"])
+    scans = [{"table": "customer", "paths": ["{data}/dev*/customer.psto"], "replicated": True, "predicate": cpred},
+             {"table": "orders", "paths": ["{data}/dev*/orders.node{node}.psto"], "predicate": opred},
+             {"table": "lineitem", "paths": ["{data}/dev*/lineitem.node{node}.psto"], "predicate": lpred}]
+    if rng.random() < 0.5:  # projection must keep keys and predicate columns
+        need = {"o_orderkey", "o_custkey"} | {a["col"] for a in opred}
+        scans[1]["columns"] = [c for c in ocols if c in need or rng.random() < 0.5]
+    if rng.random() < 0.5:
+        need = {"l_orderkey"} | {a["col"] for a in lpred}
+        scans[2]["columns"] = [c for c in lcols if c in need or rng.random() < 0.6]
+    plan = {"scans": scans, "joins": [
+        {"id": "co", "build": "customer", "probe": "orders", "build_key": "c_custkey", "probe_key": "o_custkey",
+         "mode": "replicated"},
+        {"id": "res", "build": "co", "probe": "lineitem", "build_key": "o_orderkey", "probe_key": "l_orderkey",
+         "mode": "shuffle"}]}
+    r = rng.random()
+    if r < 0.8:
+        ocols_p = scans[1].get("columns", ocols)
+        lcols_p = scans[2].get("columns", lcols)
+        cand = ["c_mktsegment"] + [c for c in ocols_p if c != "o_orderkey"] + list(lcols_p)
+        sums = rng.sample(cand, rng.randint(0, min(4, len(cand))))
+        plan["aggregate"] = {"group_by": "l_orderkey" if r < 0.65 else "", "sums": sums}
+    return plan
+
+
+@pytest.fixture(scope="module")
+def data(tmp_path_factory):
+    d = str(tmp_path_factory.mktemp("fz") / "d")
+    psg.gen_workload("tpch", d, devices=1, nodes=1, scale=0.01, seed=3, row_group_bytes=64 << 10)
+    return d
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = psg.Context(0)
+    c.set_ingest(io_threads=3, batch_bytes=256 << 10)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_plan_matches_oracle(ctx, data, seed):
+    rng = random.Random(seed)
+    plan = random_plan(rng)
+    mode = rng.choice(list(psg.MODES))
+    want = po.summary(po.execute(json.dumps(plan), data, 1))
+    got = ctx.execute_plan(plan, data, mode)
+    s = po.summary([(got.schema, got.rows)])
+    assert s == want, (seed, mode, json.dumps(plan))

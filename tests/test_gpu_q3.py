@@ -212,3 +212,26 @@ def test_sf10_matches_reference_golden(ctx, pdata, golden, staged):
     res = ctx.stage_plan(plan, d).run() if staged else ctx.execute_plan(plan, d)
     s = summarize(res)
     assert (s["rows"], s["colsums"][1], s["colsums"][2], s["colsums"][3], s["rowhash"]) == SF10_GOLDEN
+
+
+def test_out_of_core_budget_streams_sf10(ctx, pdata, golden):
+    """Input (2.4 GB) far above the plan budget (768 MiB): the overlapped path streams through a
+    regulated chunk ring and still returns the reference's SF10 result."""
+    plan = json.loads(json.dumps(golden["plans"]["canonical"]))
+    plan["budget_mb"] = 768
+    res = ctx.execute_plan(plan, pdata(10.0), "overlapped")
+    s = summarize(res)
+    assert (s["rows"], s["colsums"][1], s["colsums"][2], s["colsums"][3], s["rowhash"]) == SF10_GOLDEN
+    assert res.stats["peak_bytes"] <= 768 << 20
+
+
+def test_budget_errors_match_reference_classes(ctx, pdata, golden):
+    plan = json.loads(json.dumps(golden["plans"]["canonical"]))
+    plan["budget_mb"] = 8  # cannot hold one chunk batch (regulate -> InfeasibleBudget)
+    with pytest.raises(psg.PsgError) as e:
+        ctx.execute_plan(plan, pdata(1.0), "overlapped")
+    assert e.value.kind == "InfeasibleBudget"
+    plan["budget_mb"] = 64  # the blocking reader must materialise 232 MB (read_blocking -> MemoryExceeded)
+    with pytest.raises(psg.PsgError) as e:
+        ctx.execute_plan(plan, pdata(1.0), "blocking")
+    assert e.value.kind == "MemoryExceeded"
