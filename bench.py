@@ -51,7 +51,7 @@ def plan_for(shards, io_workers):
     }
 
 
-def ensure_data(root, scale, nodes, rank_is_writer=True):
+def ensure_data(root, scale, nodes, rank_is_writer=True, codec="identity"):
     marker = os.path.join(root, "DONE")
     if os.path.exists(marker):
         return root, 0.0
@@ -61,9 +61,10 @@ def ensure_data(root, scale, nodes, rank_is_writer=True):
     import paper_2512_02862_b200 as psg
     shutil.rmtree(root, ignore_errors=True)
     t = time.time()
-    psg.gen_workload("tpch", root, devices=nodes, nodes=nodes, scale=scale, seed=42)
+    psg.gen_workload("tpch", root, devices=nodes, nodes=nodes, scale=scale, seed=42, codec=codec,
+                     threads=max(3, min(32, os.cpu_count() or 3)))
     with open(marker, "w") as f:
-        f.write(json.dumps({"scale": scale, "nodes": nodes, "seed": 42}))
+        f.write(json.dumps({"scale": scale, "nodes": nodes, "seed": 42, "codec": codec}))
     return root, time.time() - t
 
 
@@ -190,6 +191,8 @@ def main():
     ap.add_argument("--no-semijoin", action="store_true")
     ap.add_argument("--io-threads", type=int, default=0)
     ap.add_argument("--batch-mb", type=int, default=64)
+    ap.add_argument("--codec", default="identity", choices=["identity", "block"],
+                    help="PSTO codec of the dataset (block = zlib chunks, inflated on the GPU)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
@@ -207,10 +210,11 @@ def main():
     cores = os.cpu_count() or 1
     io_threads = args.io_threads or max(2, min(12, cores // max(world, 1)))
 
-    data_root = os.path.join(args.data_dir, "sf%g_n%d" % (args.scale, SHARDS))
+    data_root = os.path.join(args.data_dir, "sf%g_n%d%s" % (args.scale, SHARDS, "" if args.codec == "identity"
+                                                                  else "_" + args.codec))
     gen_s = 0.0
     if rank == 0:
-        data_root, gen_s = ensure_data(data_root, args.scale, SHARDS)
+        data_root, gen_s = ensure_data(data_root, args.scale, SHARDS, codec=args.codec)
     if dist:
         dist.barrier()
 
@@ -288,7 +292,7 @@ def main():
         t = time.time()
         res = ctx.execute_plan(plan, data_root)
         e2e_t.append(time.time() - t)
-        h2d, d2h = res.stats["ingest_bytes"], res.stats["result_bytes"]
+        h2d, d2h = res.stats["h2d_bytes"], res.stats["result_bytes"]
         io_wait.append(res.stats["io_wait_s"])
         e2e_rows = res.rows.shape[0]
     sync_all()
@@ -331,7 +335,7 @@ def main():
             "data": "synthetic: reference TPC-H-analog generator, seed 42 (byte-identical re-implementation)",
             "config": {"workload": "Q3-analog SF%g canonical plan (o_orderdate<%d, l_shipdate>%d, group by l_orderkey)"
                                    % (args.scale, DATE, DATE),
-                       "scale": args.scale, "row_group_bytes": 1 << 20, "codec": "identity",
+                       "scale": args.scale, "row_group_bytes": 1 << 20, "codec": args.codec,
                        "layout": "8 node shards; rank r scans shards k%%N==r; customer replicated",
                        "l2": "inputs 24.2 GB >> 126 MB L2 (no flush needed)",
                        "value": "HBM-resident inputs, CUDA events on the engine stream, max over ranks",

@@ -98,6 +98,7 @@ typedef struct psg_stats {
   uint64_t result_rows;        /* rows of this rank's result (also when rows stay on the device) */
   double io_wait_s;            /* host time the control thread waited for storage reads */
   uint64_t jit_compiles;       /* NVRTC kernel compilations during this call (cached afterwards) */
+  uint64_t h2d_bytes;          /* host->HBM bytes copied (compressed for block-codec chunks) */
 } psg_stats;
 
 /* ---- library ---- */
@@ -160,6 +161,13 @@ int psg_partition(psg_ctx* ctx, const psg_batch* in, const char* key_column, uin
  * multisets). */
 int psg_hash_join(psg_ctx* ctx, const psg_batch* build, const char* build_key,
                   const psg_batch* probe, const char* probe_key, psg_result** out);
+
+/* codec_decompress (psto.cpp:133-143), batched and on the GPU: n chunks, host buffers.
+ * codec 0 = identity (copies src to dst; needs src_len == dst_len), 1 = block (zlib stream ->
+ * exactly dst_len bytes). Any invalid stream or size mismatch -> PSG_ERR_IO_FAILURE
+ * ("inflate failed"), like the reference. */
+int psg_codec_decompress(psg_ctx* ctx, int codec, uint64_t n, const void* const* src, const uint64_t* src_len,
+                         void* const* dst, const uint64_t* dst_len);
 
 /* ---- PSTO format (psto.hpp) ---- */
 /* TableWriter (psto.cpp:144-229): writes a batch as a PSTO file. Returns row groups written. */

@@ -31,7 +31,7 @@ STATUS = {0: "OK", 1: "UnknownColumn", 2: "MemoryExceeded", 3: "StreamClosed", 4
 EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_unique_id", "psg_ctx_init_comm",
            "psg_ctx_set_ingest", "psg_ctx_set_semijoin", "psg_ctx_set_fused_shuffle", "psg_ctx_destroy", "psg_execute_plan", "psg_stage_plan",
            "psg_execute_staged", "psg_staged_free", "psg_result_shape", "psg_result_field", "psg_result_data",
-           "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_psto_write",
+           "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_codec_decompress", "psg_psto_write",
            "psg_psto_inspect", "psg_gen_tpch", "psg_jit_selftest", "psg_tmin"]
 
 
@@ -52,7 +52,7 @@ class Stats(ctypes.Structure):
                 ("waves", ctypes.c_uint64), ("probe_kernel_ms", ctypes.c_double),
                 ("probe_kernel_launches", ctypes.c_uint64), ("probe_kernel_bytes", ctypes.c_uint64),
                 ("device_ms", ctypes.c_double), ("result_rows", ctypes.c_uint64), ("io_wait_s", ctypes.c_double),
-                ("jit_compiles", ctypes.c_uint64)]
+                ("jit_compiles", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -96,6 +96,7 @@ def lib():
             "psg_filter": ([vp, P(Batch), P(Atom), ctypes.c_uint32, P(vp)], i32),
             "psg_partition": ([vp, P(Batch), c, ctypes.c_uint32, i32, P(vp), P(u64)], i32),
             "psg_hash_join": ([vp, P(Batch), c, P(Batch), c, P(vp)], i32),
+            "psg_codec_decompress": ([vp, i32, u64, P(vp), P(u64), P(vp), P(u64)], i32),
             "psg_psto_write": ([c, P(Batch), u64, i32, P(u64)], i32),
             "psg_psto_inspect": ([c, P(u64), P(ctypes.c_uint32), P(u64), P(i32)], i32),
             "psg_gen_tpch": ([c, ctypes.c_double, i32, i32, u64, i32, u64, i32], i32),
@@ -430,14 +431,31 @@ def hash_join(build: dict, build_key, probe: dict, probe_key, ctx: Context | Non
     return Result(out)
 
 
+def codec_decompress(chunks, sizes, codec="block", ctx: Context | None = None):
+    """codec_decompress (psto.cpp:133-143) for a batch of chunks, inflated on the GPU.
+
+    ``chunks``: bytes-like compressed streams; ``sizes``: their exact uncompressed sizes. Returns
+    a list of ``bytes``. Raises PsgError(IoFailure) on any invalid stream, like the reference."""
+    n = len(chunks)
+    if len(sizes) != n:
+        raise ValueError("chunks and sizes differ in length")
+    srcs = [bytes(c) for c in chunks]
+    outs = [ctypes.create_string_buffer(max(int(z), 1)) for z in sizes]
+    src_p = (ctypes.c_void_p * max(n, 1))(*[ctypes.cast(ctypes.c_char_p(b), ctypes.c_void_p) for b in srcs])
+    dst_p = (ctypes.c_void_p * max(n, 1))(*[ctypes.cast(o, ctypes.c_void_p) for o in outs])
+    src_l = (ctypes.c_uint64 * max(n, 1))(*[len(b) for b in srcs])
+    dst_l = (ctypes.c_uint64 * max(n, 1))(*[int(z) for z in sizes])
+    kind = {"identity": 0, "block": 1}[codec] if isinstance(codec, str) else int(codec)
+    _check(lib().psg_codec_decompress((ctx or _ctx())._h, kind, n, src_p, src_l, dst_p, dst_l))
+    return [o.raw[:int(z)] for o, z in zip(outs, sizes)]
+
+
 def scan(path, predicate=None, ctx: Context | None = None):
     """Reads a PSTO table through the GPU filter (read_blocking + filter, scan.cpp:273-336)."""
     meta = inspect(path)
     import struct
     with open(path, "rb") as f:
         data = f.read()
-    if meta["codec"] != "identity":
-        raise PsgError(9, "block-codec PSTO needs the GPU inflate path (not in this build)")
     # footer walk for chunk offsets
     (flen,) = struct.unpack_from("<Q", data, len(data) - 12)
     foot = data[len(data) - 12 - flen: len(data) - 12]
@@ -450,13 +468,21 @@ def scan(path, predicate=None, ctx: Context | None = None):
     (ng,) = struct.unpack_from("<I", foot, off)
     off += 4
     cols = [[] for _ in range(nc)]
+    pending = []  # block codec: (col, stream, usize), inflated on the GPU in one batch
     for _ in range(ng):
         (rows,) = struct.unpack_from("<Q", foot, off)
         off += 8
         for c in range(nc):
-            o, cs, _us, _mn, _mx = struct.unpack_from("<5Q", foot, off)
+            o, cs, us, _mn, _mx = struct.unpack_from("<5Q", foot, off)
             off += 40
-            cols[c].append(np.frombuffer(data, dtype="<u8", count=rows, offset=o))
+            if meta["codec"] == "identity":
+                cols[c].append(np.frombuffer(data, dtype="<u8", count=rows, offset=o))
+            else:
+                pending.append((c, data[o:o + cs], us))
+    if pending:
+        raw = codec_decompress([p[1] for p in pending], [p[2] for p in pending], "block", ctx=ctx)
+        for (c, _s, _u), r in zip(pending, raw):
+            cols[c].append(np.frombuffer(r, dtype="<u8"))
     schema = meta["schema"]
     columns = {n: (np.concatenate(cols[i]) if cols[i] else np.zeros(0, np.uint64)) for i, (n, _t) in enumerate(schema)}
     types = {n: (1 if t == "float64" else 0) for n, t in schema}

@@ -274,6 +274,15 @@ int psg_partition(psg_ctx* ctx, const psg_batch* in, const char* key_column, uin
   });
 }
 
+int psg_codec_decompress(psg_ctx* ctx, int codec, uint64_t n, const void* const* src, const uint64_t* src_len,
+                         void* const* dst, const uint64_t* dst_len) {
+  return guarded([&] {
+    if (!ctx || (n && (!src || !src_len || !dst || !dst_len))) throw InvalidInput("null argument");
+    if (codec != 0 && codec != 1) throw InvalidInput("unknown codec");
+    op_codec_decompress(ctx->c, codec, n, src, src_len, dst, dst_len);
+  });
+}
+
 int psg_hash_join(psg_ctx* ctx, const psg_batch* build, const char* build_key, const psg_batch* probe,
                   const char* probe_key, psg_result** out) {
   return guarded([&] {

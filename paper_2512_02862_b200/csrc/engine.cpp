@@ -243,50 +243,83 @@ RegMap analyse(SourceDef& s, const std::vector<int>& needed, int early_wire, boo
 struct ScanBatches {
   std::vector<BatchPlan> batches;
   uint64_t total_rows = 0;
-  uint64_t total_bytes = 0;
-  uint64_t total_payload = 0;
-  uint64_t max_batch_bytes = 0;
-  uint64_t max_segs = 0;
+  uint64_t total_bytes = 0;    // H2D footprint
+  uint64_t total_dbytes = 0;   // decoded footprint (block codec)
+  uint64_t total_payload = 0;  // file bytes
+  uint64_t total_scan = 0;     // bytes the scan kernel reads
+  uint64_t max_batch_bytes = 0, max_dbytes = 0;
+  uint64_t max_segs = 0, max_jobs = 0;
+  bool inflate = false;
 };
 
 /// Groups surviving row groups of each file into batches of <= batch_bytes packed column chunks.
+/// Block-codec files keep their chunks compressed on the wire (the GPU inflates them in HBM,
+/// replacing codec_decompress in decode_group, scan.cpp:139-160); such a batch is also capped at
+/// 4 x batch_bytes of decoded columns.
 ScanBatches plan_batches(FooterCache& fc, const ScanNode& scan, const std::vector<int>& file_cols, int file_base,
                          uint64_t batch_bytes) {
   ScanBatches out;
   for (size_t f = 0; f < scan.paths.size(); ++f) {
     auto meta = fc.get(scan.paths[f]);
-    if (meta->codec != Codec::Identity)
-      throw InvalidInput("block-codec PSTO needs the GPU inflate path (not in this build): " + scan.paths[f]);
+    const bool block = meta->codec == Codec::Block;
     const auto groups = prune(*meta, scan.predicate);
     BatchPlan cur;
     cur.file = file_base + static_cast<int>(f);
+    cur.inflate = block;
     auto flush = [&] {
       if (cur.groups.empty()) return;
       cur.bytes += 16;  // tail padding: 16-byte async copies may read 8 bytes past the last chunk
+      if (block) {
+        cur.dbytes += 16;
+        // longest streams first: the decoders of one warp finish together
+        std::sort(cur.jobs.begin(), cur.jobs.end(), [](const BatchPlan::Job& a, const BatchPlan::Job& b) {
+          return a.csize != b.csize ? a.csize > b.csize : a.src_off < b.src_off;
+        });
+      }
       out.total_rows += cur.total_rows;
       out.total_bytes += cur.bytes;
+      out.total_dbytes += cur.dbytes;
       out.total_payload += cur.payload_bytes;
+      out.total_scan += cur.scan_bytes();
       out.max_batch_bytes = std::max(out.max_batch_bytes, cur.bytes);
+      out.max_dbytes = std::max(out.max_dbytes, cur.dbytes);
       out.max_segs = std::max<uint64_t>(out.max_segs, cur.groups.size());
+      out.max_jobs = std::max<uint64_t>(out.max_jobs, cur.jobs.size());
+      out.inflate = out.inflate || block;
       out.batches.push_back(std::move(cur));
       cur = BatchPlan{};
       cur.file = file_base + static_cast<int>(f);
+      cur.inflate = block;
     };
     for (size_t g : groups) {
       const GroupMeta& gm = meta->groups[g];
-      uint64_t gbytes = 0;
-      for (int c : file_cols) gbytes += gm.cols[c].csize;
-      if (!cur.groups.empty() && cur.bytes + gbytes > batch_bytes) flush();
+      uint64_t gbytes = 0, gdbytes = 0;
+      for (int c : file_cols) gbytes += gm.cols[c].csize, gdbytes += gm.cols[c].usize;
+      if (!cur.groups.empty() &&
+          (cur.bytes + gbytes > batch_bytes || (block && cur.dbytes + gdbytes > 4 * batch_bytes)))
+        flush();
       // chunks of this group in file order, packed; merge adjacent extents
       std::vector<std::pair<uint64_t, int>> order;
       for (size_t k = 0; k < file_cols.size(); ++k) order.push_back({gm.cols[file_cols[k]].offset, static_cast<int>(k)});
       std::sort(order.begin(), order.end());
       std::vector<uint64_t> pos(file_cols.size());
       for (auto& [off, k] : order) {
-        const uint64_t len = gm.cols[file_cols[k]].csize;
-        // 16-byte aligned chunk positions (cp.async in the fused kernel); padding breaks an extent
+        const ChunkMeta& ch = gm.cols[file_cols[k]];
+        const uint64_t len = ch.csize;
+        // 16-byte aligned chunk positions (vector loads in the fused kernel, aligned words in the
+        // inflate bit reader); padding breaks an extent
         cur.bytes = (cur.bytes + 15) & ~15ULL;
-        pos[k] = cur.bytes;
+        if (block) {
+          if (ch.csize > 0xFFFFFFFFull || ch.usize > 0xFFFFFFFFull)
+            throw InvalidInput("block-codec column chunk larger than 4 GiB: " + scan.paths[f]);
+          cur.dbytes = (cur.dbytes + 15) & ~15ULL;
+          cur.jobs.push_back({cur.bytes, cur.dbytes, static_cast<uint32_t>(ch.csize), static_cast<uint32_t>(ch.usize)});
+          pos[k] = cur.dbytes;
+          cur.dbytes += ch.usize;
+          cur.ubytes += ch.usize;
+        } else {
+          pos[k] = cur.bytes;
+        }
         cur.payload_bytes += len;
         if (!cur.extents.empty() && cur.extents.back().file_off + cur.extents.back().len == off &&
             cur.extents.back().buf_off + cur.extents.back().len == cur.bytes)
@@ -304,6 +337,15 @@ ScanBatches plan_batches(FooterCache& fc, const ScanNode& scan, const std::vecto
     flush();
   }
   return out;
+}
+
+/// Device inflate jobs of a block-codec batch whose compressed image is at `cbase` and whose
+/// decoded image goes to `dbase`.
+std::vector<InflateJob> inflate_jobs(const BatchPlan& b, uint8_t* cbase, uint8_t* dbase) {
+  std::vector<InflateJob> jobs(b.jobs.size());
+  for (size_t i = 0; i < b.jobs.size(); ++i)
+    jobs[i] = InflateJob{cbase + b.jobs[i].src_off, dbase + b.jobs[i].dst_off, b.jobs[i].csize, b.jobs[i].usize};
+  return jobs;
 }
 
 /// Segment descriptors of a batch placed at device address `dev_base`.
@@ -375,7 +417,8 @@ struct StagedScan {
 struct Staged {
   std::string plan_json, data_root;
   std::map<std::string, StagedScan> scans;  // key: "table|cols"
-  uint64_t bytes = 0;
+  uint64_t bytes = 0;  // decoded column-chunk bytes the scans read
+  uint64_t h2d = 0;    // bytes copied host->HBM while staging
 };
 
 namespace {
@@ -498,6 +541,13 @@ struct StreamSession {
   std::vector<DevBuf> slots;
   std::vector<cudaEvent_t> slot_free, copied;
   uint64_t slot_bytes = 0;
+  // block codec: decoded images, per-slot inflate streams, session error word
+  std::vector<DevBuf> dslots;
+  std::vector<cudaStream_t> istreams;
+  std::vector<cudaEvent_t> inflated;
+  DevBuf inflate_err;
+  uint64_t dslot_bytes = 0;
+  uint64_t h2d_bytes = 0;
   int regulated_slots = 0;
   size_t cursor = 0;  // next batch to consume (global order)
   int cur_slot = -1;
@@ -508,7 +558,7 @@ struct StreamSession {
   StreamSession(Ctx& c, const std::vector<std::pair<const ScanNode*, std::vector<int>>>& scans, uint64_t budget = 0,
                 uint64_t ht_reserve = 0)
       : ctx(c) {
-    uint64_t max_bytes = 0, max_segs = 0;
+    uint64_t max_bytes = 0, max_segs = 0, max_dbytes = 0, max_jobs = 0;
     for (auto& [scan, fcols] : scans) {
       const std::string key = scan_key(*scan, fcols);
       // union file list; plan this scan's batches against it
@@ -533,24 +583,29 @@ struct StreamSession {
       ranges[key].push_back(r);
       max_bytes = std::max(max_bytes, sb.max_batch_bytes);
       max_segs = std::max(max_segs, sb.max_segs);
+      max_dbytes = std::max(max_dbytes, sb.max_dbytes);
+      max_jobs = std::max(max_jobs, sb.max_jobs);
     }
     if (batches.empty()) return;
     const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
     const uint64_t cap = std::max(max_bytes, ctx.batch_bytes);
-    const uint64_t max_tiles = cap / 8 / T + max_segs + 1;
-    slot_bytes = (cap + max_segs * sizeof(Segment) + max_tiles * 4 + 4096 + 4095) & ~4095ULL;
+    const uint64_t max_tiles = std::max(cap, max_dbytes) / 8 / T + max_segs + 1;
+    slot_bytes = (cap + max_segs * sizeof(Segment) + max_tiles * 4 + max_jobs * sizeof(InflateJob) + 4096 + 4095) &
+                 ~4095ULL;
+    dslot_bytes = (max_dbytes + 4095) & ~4095ULL;
     const int threads = std::max(1, ctx.io_threads);
     const int pinned = ctx.pinned_slots > 0 ? ctx.pinned_slots : threads * 2 + 2;
     ingest = std::make_unique<Ingest>(ctx, files, batches, threads, slot_bytes, pinned);
     int nd = static_cast<int>(std::min<size_t>(batches.size(), 8));
+    const uint64_t per_slot = slot_bytes + dslot_bytes;
     if (budget) {
-      const uint64_t fixed = ht_reserve + 2 * slot_bytes;  // tables + materialisation transients
+      const uint64_t fixed = ht_reserve + 2 * std::max(slot_bytes, dslot_bytes);  // tables + materialisation transients
       if (fixed >= budget)
         throw InfeasibleBudget("fixed residents (" + std::to_string(fixed) + " bytes) leave no room for the chunk ring in a budget of " +
                                std::to_string(budget));
-      const uint64_t fit = (budget - fixed) / slot_bytes;
+      const uint64_t fit = (budget - fixed) / per_slot;
       if (fit < 1)
-        throw InfeasibleBudget("the chunk ring cannot hold even one batch of " + std::to_string(slot_bytes) + " bytes");
+        throw InfeasibleBudget("the chunk ring cannot hold even one batch of " + std::to_string(per_slot) + " bytes");
       nd = static_cast<int>(std::min<uint64_t>(static_cast<uint64_t>(nd), fit));
     }
     regulated_slots = nd;
@@ -561,14 +616,39 @@ struct StreamSession {
       PSG_CUDA(cudaEventCreateWithFlags(&y, cudaEventDisableTiming));
       slot_free.push_back(x);
       copied.push_back(y);
+      if (dslot_bytes) {
+        // decoded images + one inflate stream per slot: batches decode concurrently (one thread
+        // per chunk, so a single batch fills only part of the GPU)
+        dslots.emplace_back(ctx.pool, dslot_bytes, ctx.copy);
+        cudaStream_t is;
+        PSG_CUDA(cudaStreamCreateWithFlags(&is, cudaStreamNonBlocking));
+        istreams.push_back(is);
+        PSG_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+        inflated.push_back(x);
+      }
+    }
+    if (dslot_bytes) {
+      inflate_err = DevBuf(ctx.pool, sizeof(unsigned int), ctx.copy);
+      PSG_CUDA(cudaMemsetAsync(inflate_err.p, 0, sizeof(unsigned int), ctx.copy));
     }
   }
   ~StreamSession() {
     cudaStreamSynchronize(ctx.copy);
+    for (auto is : istreams) cudaStreamSynchronize(is);
     cudaStreamSynchronize(ctx.compute);
     ingest.reset();
     for (auto x : slot_free) cudaEventDestroy(x);
     for (auto x : copied) cudaEventDestroy(x);
+    for (auto x : inflated) cudaEventDestroy(x);
+    for (auto is : istreams) cudaStreamDestroy(is);
+  }
+  /// Raises IoFailure when any chunk of the session failed to inflate (codec_decompress,
+  /// psto.cpp:138-140). Call after the compute stream has drained.
+  void check_inflate() {
+    if (!inflate_err.p) return;
+    unsigned int e = 0;
+    PSG_CUDA(cudaMemcpy(&e, inflate_err.p, sizeof e, cudaMemcpyDeviceToHost));
+    if (e) throw IoFailure("inflate failed");
   }
   /// Stages batch i (must be the next in consumption order) into its HBM ring slot.
   void stage(size_t i, BatchView& v) {
@@ -576,20 +656,36 @@ struct StreamSession {
     const int k = static_cast<int>(i % slots.size());
     const BatchPlan& b = batches[i];
     auto* base = slots[k].as<uint8_t>();
+    uint8_t* dbase = b.inflate ? dslots[k].as<uint8_t>() : base;
     uint64_t nt = 0;
-    auto segs = make_segments(b, base, nt);
+    auto segs = make_segments(b, dbase, nt);
     if (i >= slots.size()) PSG_CUDA(cudaStreamWaitEvent(ctx.copy, slot_free[k], 0));
     size_t toff = 0;
     auto blob = pack_view(segs, toff);
+    size_t joff = blob.size();
+    if (b.inflate) {
+      auto jobs = inflate_jobs(b, base, dbase);
+      blob.resize(joff + jobs.size() * sizeof(InflateJob));
+      std::memcpy(blob.data() + joff, jobs.data(), jobs.size() * sizeof(InflateJob));
+    }
     ingest->copy_to_device(i, base, blob.data(), blob.size(), ctx.copy);
+    h2d_bytes += b.bytes + blob.size();
     PSG_CUDA(cudaEventRecord(copied[k], ctx.copy));
-    PSG_CUDA(cudaStreamWaitEvent(ctx.compute, copied[k], 0));
+    if (b.inflate) {
+      PSG_CUDA(cudaStreamWaitEvent(istreams[k], copied[k], 0));
+      launch_inflate(reinterpret_cast<const InflateJob*>(base + b.bytes + joff), static_cast<uint32_t>(b.jobs.size()),
+                     inflate_err.as<unsigned int>(), istreams[k]);
+      PSG_CUDA(cudaEventRecord(inflated[k], istreams[k]));
+      PSG_CUDA(cudaStreamWaitEvent(ctx.compute, inflated[k], 0));
+    } else {
+      PSG_CUDA(cudaStreamWaitEvent(ctx.compute, copied[k], 0));
+    }
     v.d_segs = reinterpret_cast<const Segment*>(base + b.bytes);
     v.d_tile_seg = reinterpret_cast<const uint32_t*>(base + b.bytes + toff);
     v.nsegs = static_cast<int>(segs.size());
     v.ntiles = nt;
     v.rows = b.total_rows;
-    v.bytes = b.payload_bytes;
+    v.bytes = b.scan_bytes();
     cur_slot = k;
     ++cursor;
   }
@@ -1544,6 +1640,10 @@ ResultRows Execution::run(bool want_rows) {
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   st_.device_ms = dms;
+  if (session_) {
+    session_->check_inflate();
+    st_.h2d_bytes = session_->h2d_bytes;
+  }
   if (session_ && session_->ingest) st_.io_wait_s = session_->ingest->wait_s();
   st_.jit_compiles = jit_stats().compiles - jit0_;
   st_.result_rows = out.nrows;
@@ -1602,23 +1702,54 @@ void Execution::stage(Staged& st) {
     if (st.scans.count(key)) continue;
     ScanBatches sb = plan_batches(ctx_.footers, *scan, fcols, 0, ctx_.batch_bytes);
     StagedScan& ss = st.scans[key];
-    ss.data = DevBuf(ctx_.pool, std::max<uint64_t>(sb.total_bytes, 8), ctx_.compute);
+    // block codec: compressed images land in a transient buffer and are inflated into `data`
+    uint64_t data_bytes = 0, wire_bytes = 0;
+    for (auto& b : sb.batches) {
+      data_bytes += b.inflate ? b.dbytes : b.bytes;
+      wire_bytes += b.inflate ? b.bytes : 0;
+    }
+    ss.data = DevBuf(ctx_.pool, std::max<uint64_t>(data_bytes, 8), ctx_.compute);
+    DevBuf wire, jobs_dev, err;
+    if (wire_bytes) wire = DevBuf(ctx_.pool, wire_bytes, ctx_.compute);
     PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
     std::vector<Segment> all;
+    std::vector<InflateJob> jobs;
     const uint64_t slot_bytes = (std::max(sb.max_batch_bytes, ctx_.batch_bytes) + 4095) & ~4095ULL;
     if (!sb.batches.empty()) {
       const int threads = std::max(1, ctx_.io_threads);
       Ingest ing(ctx_, scan->paths, sb.batches, threads, slot_bytes, threads * 2 + 2);
-      uint64_t off = 0;
+      uint64_t woff = 0, doff = 0;
       for (size_t i = 0; i < sb.batches.size(); ++i) {
-        uint8_t* base = ss.data.as<uint8_t>() + off;
+        const BatchPlan& b = sb.batches[i];
+        uint8_t* dbase = ss.data.as<uint8_t>() + doff;
+        uint8_t* base = b.inflate ? wire.as<uint8_t>() + woff : dbase;
         uint64_t nt = 0;
-        auto segs = make_segments(sb.batches[i], base, nt);
+        auto segs = make_segments(b, dbase, nt);
         all.insert(all.end(), segs.begin(), segs.end());
+        if (b.inflate) {
+          auto bj = inflate_jobs(b, base, dbase);
+          jobs.insert(jobs.end(), bj.begin(), bj.end());
+        }
         ing.copy_to_device(i, base, nullptr, 0, ctx_.copy);
-        off += sb.batches[i].bytes;
+        st.h2d += b.bytes;
+        woff += b.inflate ? b.bytes : 0;
+        doff += b.inflate ? b.dbytes : b.bytes;
       }
       PSG_CUDA(cudaStreamSynchronize(ctx_.copy));
+    }
+    if (!jobs.empty()) {
+      // one launch over every chunk of the scan: tens of thousands of concurrent decoders
+      std::sort(jobs.begin(), jobs.end(), [](const InflateJob& a, const InflateJob& b) { return a.csize > b.csize; });
+      jobs_dev = DevBuf(ctx_.pool, jobs.size() * sizeof(InflateJob), ctx_.compute);
+      err = DevBuf(ctx_.pool, sizeof(unsigned int), ctx_.compute);
+      PSG_CUDA(cudaMemcpyAsync(jobs_dev.p, jobs.data(), jobs.size() * sizeof(InflateJob), cudaMemcpyHostToDevice,
+                               ctx_.compute));
+      PSG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(unsigned int), ctx_.compute));
+      launch_inflate(jobs_dev.as<InflateJob>(), static_cast<uint32_t>(jobs.size()), err.as<unsigned int>(), ctx_.compute);
+      unsigned int e = 0;
+      PSG_CUDA(cudaMemcpyAsync(&e, err.p, sizeof e, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      if (e) throw IoFailure("inflate failed");
     }
     const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
     uint64_t tiles = 0;
@@ -1629,15 +1760,15 @@ void Execution::stage(Staged& st) {
     ss.nsegs = static_cast<int>(all.size());
     ss.ntiles = tiles;
     ss.rows = sb.total_rows;
-    ss.bytes = sb.total_bytes;
-    ss.payload = sb.total_payload;
+    ss.bytes = data_bytes;
+    ss.payload = sb.total_scan;
     if (!all.empty()) {
       auto blob = pack_view(all, ss.tile_off);
       ss.segs = DevBuf(ctx_.pool, blob.size(), ctx_.compute);
       PSG_CUDA(cudaMemcpyAsync(ss.segs.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, ctx_.compute));
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
     }
-    st.bytes += sb.total_payload;
+    st.bytes += sb.total_scan;
   }
 }
 
@@ -1678,6 +1809,7 @@ ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::strin
   r.stats.network_phase_s = r.stats.runtime_s;
   r.stats.runtime_s = secs_since(t0);
   r.stats.ingest_bytes = st->bytes;
+  r.stats.h2d_bytes = st->h2d;
   return r;
 }
 

@@ -95,6 +95,17 @@ struct BatchPlan {
   uint64_t bytes = 0;          // buffer footprint (16-byte aligned chunks + tail padding)
   uint64_t payload_bytes = 0;  // column-chunk bytes read from the file (algorithmic bytes)
   uint64_t total_rows = 0;
+  // Block codec: `extents` land compressed chunks in the H2D buffer; `pos` then addresses the
+  // decoded image (dbytes) that the inflate jobs write (src/dst offsets relative to each buffer).
+  bool inflate = false;
+  struct Job {
+    uint64_t src_off, dst_off;
+    uint32_t csize, usize;
+  };
+  std::vector<Job> jobs;
+  uint64_t dbytes = 0;  // decoded footprint (16-byte aligned chunks + tail padding)
+  uint64_t ubytes = 0;  // decoded column-chunk bytes (what the scan kernel reads)
+  uint64_t scan_bytes() const { return inflate ? ubytes : payload_bytes; }
 };
 
 struct Ctx;
@@ -226,6 +237,8 @@ struct HostBatch {
 HostBatch op_filter(Ctx& ctx, const HostBatch& in, const Predicate& pred);
 HostBatch op_partition(Ctx& ctx, const HostBatch& in, const std::string& key, uint32_t nparts, int identity,
                        std::vector<uint64_t>& part_rows);
+void op_codec_decompress(Ctx& ctx, int codec, uint64_t n, const void* const* src, const uint64_t* src_len,
+                         void* const* dst, const uint64_t* dst_len);
 HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& build_key, const HostBatch& probe,
                        const std::string& probe_key);
 

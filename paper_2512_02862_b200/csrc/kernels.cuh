@@ -68,6 +68,16 @@ size_t sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_
 void launch_iota_u32(uint32_t* out, uint64_t n, void* stream);
 void launch_rows_from_cols(const uint64_t* const* cols, int ncols, uint64_t n, uint64_t* out_rows, void* stream);
 
+// Block-codec inflate (inflate.cu): one zlib stream per job, decoded in HBM.
+struct InflateJob {
+  const uint8_t* src;  // compressed stream (4-byte aligned; may be read up to 3 bytes past csize)
+  uint8_t* dst;        // output (8-byte aligned), exactly usize bytes on success
+  uint32_t csize, usize;
+};
+/// Decodes every job; sets *d_err to nonzero if any stream is invalid (zlib's Z_DATA_ERROR,
+/// size mismatch or Adler-32 mismatch).
+void launch_inflate(const InflateJob* d_jobs, uint32_t njobs, unsigned int* d_err, void* stream);
+
 uint64_t kernel_launch_count();
 void count_external_launch();
 

@@ -39,6 +39,50 @@ void check_batch(const HostBatch& b) {
 
 }  // namespace
 
+void op_codec_decompress(Ctx& ctx, int codec, uint64_t n, const void* const* src, const uint64_t* src_len,
+                         void* const* dst, const uint64_t* dst_len) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  if (codec == 0) {  // identity (codec_decompress returns the bytes as they are)
+    for (uint64_t i = 0; i < n; ++i) {
+      if (src_len[i] != dst_len[i]) throw IoFailure("inflate failed");
+      if (src_len[i]) std::memcpy(dst[i], src[i], src_len[i]);
+    }
+    return;
+  }
+  // pack the streams 16-byte aligned into one upload, decode into one aligned output image
+  uint64_t cbytes = 0, dbytes = 0;
+  std::vector<uint64_t> coff(n), doff(n);
+  for (uint64_t i = 0; i < n; ++i) {
+    if (src_len[i] > 0xFFFFFFF0ull || dst_len[i] > 0xFFFFFFF0ull) throw InvalidInput("chunk larger than 4 GiB");
+    coff[i] = cbytes;
+    doff[i] = dbytes;
+    cbytes += (src_len[i] + 15) & ~15ULL;
+    dbytes += (dst_len[i] + 15) & ~15ULL;
+  }
+  if (n == 0) return;
+  std::vector<uint8_t> host(cbytes + 16, 0);
+  for (uint64_t i = 0; i < n; ++i)
+    if (src_len[i]) std::memcpy(host.data() + coff[i], src[i], src_len[i]);
+  DevBuf cdev(ctx.pool, host.size(), ctx.compute), ddev(ctx.pool, dbytes + 16, ctx.compute),
+      jdev(ctx.pool, n * sizeof(InflateJob), ctx.compute), err(ctx.pool, sizeof(unsigned int), ctx.compute);
+  std::vector<InflateJob> jobs(n);
+  for (uint64_t i = 0; i < n; ++i)
+    jobs[i] = InflateJob{cdev.as<uint8_t>() + coff[i], ddev.as<uint8_t>() + doff[i], static_cast<uint32_t>(src_len[i]),
+                         static_cast<uint32_t>(dst_len[i])};
+  PSG_CUDA(cudaMemcpyAsync(cdev.p, host.data(), host.size(), cudaMemcpyHostToDevice, ctx.compute));
+  PSG_CUDA(cudaMemcpyAsync(jdev.p, jobs.data(), n * sizeof(InflateJob), cudaMemcpyHostToDevice, ctx.compute));
+  PSG_CUDA(cudaMemsetAsync(err.p, 0, sizeof(unsigned int), ctx.compute));
+  launch_inflate(jdev.as<InflateJob>(), static_cast<uint32_t>(n), err.as<unsigned int>(), ctx.compute);
+  unsigned int e = 0;
+  PSG_CUDA(cudaMemcpyAsync(&e, err.p, sizeof e, cudaMemcpyDeviceToHost, ctx.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx.compute));
+  if (e) throw IoFailure("inflate failed");
+  std::vector<uint8_t> out(dbytes);
+  PSG_CUDA(cudaMemcpy(out.data(), ddev.p, dbytes, cudaMemcpyDeviceToHost));
+  for (uint64_t i = 0; i < n; ++i)
+    if (dst_len[i]) std::memcpy(dst[i], out.data() + doff[i], dst_len[i]);
+}
+
 HostBatch op_filter(Ctx& ctx, const HostBatch& in, const Predicate& pred) {
   PSG_CUDA(cudaSetDevice(ctx.device));
   check_batch(in);
