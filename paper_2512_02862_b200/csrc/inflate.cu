@@ -6,21 +6,23 @@
 // travel host->HBM as they are (3-8x fewer PCIe bytes than decoded columns) and are expanded in
 // HBM by this kernel, straight into the chunk layout the fused scan kernel reads.
 //
-// Design (B200): a deflate stream is inherently serial, so parallelism comes from chunks - one
-// thread decodes one chunk (a 256 KB column chunk is ~30-100 KB of stream) and an SM keeps 256
-// decoders in flight. Per-thread state:
-//   * bit reader: 64-bit buffer refilled with aligned 32-bit loads (chunks are 16-byte aligned);
-//   * Huffman tables in shared memory, laid out [entry][thread] so a warp's lookups are
-//     bank-conflict free whatever entries the lanes hit; decoding is branch-free canonical:
-//     the 15 left-justified per-length limits live in registers, code length = 1 + #limits <=
-//     the bit-reversed peek, symbol = sym[base[len] + (peek >> (15 - len))];
-//   * output is assembled in a 64-bit register and written as aligned 8-byte stores; matches
-//     with distance >= 8 copy 8 bytes per step (two aligned loads + funnel shift, the newest
-//     bytes taken from the register), shorter distances byte by byte;
-//   * Adler-32 of the output is folded in per 8-byte word with dp4a (zlib verifies it too).
-// Every failure zlib reports (bad header, bad block type, over-subscribed/incomplete codes,
-// invalid symbols, distance too far back, output overrun or short output, input overrun, Adler
-// mismatch) sets the job's error word; the host turns it into IoFailure("inflate failed").
+// Design (B200): one warp per chunk (persistent warps walk the job list, longest first).
+//   * Huffman decoding is inherently serial, so lane 0 runs it, with one shared-memory lookup
+//     per symbol: 10-bit (literal/length) and 8-bit (distance) first-level tables whose entries
+//     carry code length, kind, literal / base length / base distance and extra-bit count; the
+//     rare longer codes fall back to canonical decoding (left-justified per-length limits held in
+//     registers). Lane 0 also resolves matches, 8 bytes per step: output is assembled in a 64-bit
+//     register and stored as whole words into a 2 KB per-warp ring, and the last two words stay
+//     in registers, so the short distances of 8-byte column data (8, 16) never touch memory;
+//     older sources come from the ring, the oldest from the already flushed output in HBM.
+//   * The warp does the parallel parts: table construction (histogram by warp reduction,
+//     canonical symbol order by match masks, each lane fills 32 of the 1024 table slots) and the
+//     flush of every 1 KB of output as coalesced 16-byte stores, with the Adler-32 of the flushed
+//     bytes folded in by a dp4a warp reduction (zlib verifies the trailer; so do we). Lane 0 only
+//     hands control back to the warp once per KB (or block end), not per match.
+// Every failure zlib reports (bad header, reserved block type, over-subscribed or incomplete
+// codes, invalid symbols, distance too far back, output overrun or short output, reading past the
+// stream, Adler mismatch) sets the error word; the host raises IoFailure("inflate failed").
 #include <algorithm>
 #include <cstdint>
 
@@ -29,9 +31,11 @@
 namespace psg {
 namespace {
 
-constexpr int kThreads = 64;   // decoders per CTA; 48 KB of tables per CTA -> 4 CTAs per SM
-constexpr int kLitSyms = 288;  // literal/length alphabet (fixed code uses all 288)
-constexpr int kDistSyms = 32;  // distance alphabet (fixed code uses 32 five-bit codes)
+constexpr int kWarps = 4;                  // warps (= concurrent chunks) per CTA
+constexpr int kLB = 10, kDB = 8, kCB = 7;  // first-level table bits: lit/len, distance, code-length
+constexpr uint32_t kRing = 2048, kRingMask = kRing - 1;
+constexpr uint32_t kFlush = 1024;             // output flushed to HBM in 1 KB pieces
+constexpr uint32_t kFull = 0xFFFFFFFFu;
 
 __constant__ uint16_t c_lbase[29] = {3,  4,  5,  6,  7,  8,  9,  10, 11,  13,  15,  17,  19,  23, 27,
                                      31, 35, 43, 51, 59, 67, 83, 99, 115, 131, 163, 195, 227, 258};
@@ -41,124 +45,173 @@ __constant__ uint16_t c_dbase[30] = {1,   2,   3,   4,   5,   7,    9,    13,   
 __constant__ uint8_t c_dext[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 __constant__ uint8_t c_clorder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
-struct Smem {
-  uint16_t lsym[kLitSyms][kThreads];
-  uint16_t dsym[kDistSyms][kThreads];
-  int32_t lbase[16][kThreads];
-  int32_t dbase[16][kThreads];
-};
-static_assert(sizeof(Smem) <= 48 * 1024, "inflate tables exceed static shared memory");
+// First-level table entry: bits 0-3 code length (0 = longer than the table: decode canonically),
+// bits 4-5 kind, bits 8-15 literal byte or extra-bit count, bits 16-31 base length / distance or
+// code-length symbol.
+enum Kind : uint32_t { kLit = 0, kLen = 1, kEob = 2, kBad = 3 };
+constexpr uint32_t kBadEntry = (kBad << 4) | 1u;  // bits that match no code
 
-/// Canonical Huffman table: limits in registers, base/sym in shared memory (column `t`).
-/// Returns false for codes zlib rejects (inflate_table: over-subscribed, or incomplete unless it
-/// is a single one-bit code of a literal/length or distance table).
-__device__ __forceinline__ bool build_table(const uint8_t* lens, int n, bool code_lengths, uint16_t (*sym)[kThreads],
-                                            int32_t (*base)[kThreads], uint32_t (&lim)[16], int t) {
-  uint16_t cnt[16];
+struct alignas(16) WarpSmem {
+  uint8_t ring[kRing];
+  uint32_t lfast[1 << kLB];
+  uint32_t dfast[1 << kDB];  // also the code-length table (kCB bits) while reading a header
+  uint16_t lsym[288];
+  uint16_t dsym[32];
+  int32_t lbase[16];
+  int32_t dbase[16];
+  uint8_t lens[320];
+};
+static_assert(sizeof(WarpSmem) * kWarps <= 48 * 1024, "inflate shared memory exceeds the static limit");
+
+/// Canonical Huffman decode of the next code (lane 0): -1 when the bits match no code.
+__device__ __forceinline__ int canon_decode(uint64_t bits, const uint32_t (&lim)[16], const int32_t* base,
+                                            const uint16_t* sym, int& len) {
+  const uint32_t c15 = __brev(static_cast<uint32_t>(bits)) >> 17;
+  len = 1;
+#pragma unroll
+  for (int l = 1; l < 16; ++l) len += (c15 >= lim[l]) ? 1 : 0;
+  if (len > 15) return -1;
+  return sym[base[len] + static_cast<int>(c15 >> (15 - len))];
+}
+
+/// Builds a canonical code from lens[0, n) into sym/base (shared) + lim (every lane's registers)
+/// and fills the first-level table `fast` (2^fb entries) cooperatively. `what`: 0 literal/length,
+/// 1 distance, 2 code-length code. Returns false (in all lanes) for codes zlib rejects
+/// (inflate_table: over-subscribed, or incomplete unless a single one-bit lit/len or distance code).
+__device__ bool build_table(const uint8_t* lens, int n, int what, uint16_t* sym, int32_t* base, uint32_t* fast, int fb,
+                            uint32_t (&lim)[16], int lane) {
+  uint32_t cnt[16];
 #pragma unroll
   for (int l = 0; l < 16; ++l) cnt[l] = 0;
-  for (int i = 0; i < n; ++i) cnt[lens[i]]++;
-  cnt[0] = 0;
-  int maxlen = 0;
+  for (int i = lane; i < n; i += 32) {  // each lane histograms a slice ...
+    const int l = lens[i];
 #pragma unroll
-  for (int l = 1; l < 16; ++l)
-    if (cnt[l]) maxlen = l;
-  int left = 1;
-#pragma unroll
-  for (int l = 1; l < 16; ++l) {
-    left <<= 1;
-    left -= cnt[l];
-    if (left < 0) return false;  // over-subscribed
+    for (int k = 1; k < 16; ++k) cnt[k] += (l == k) ? 1u : 0u;
   }
-  if (maxlen > 0 && left > 0 && (code_lengths || maxlen != 1)) return false;  // incomplete
-  uint16_t offs[16];
-  uint32_t code = 0;
-  int off = 0;
+#pragma unroll
+  for (int k = 1; k < 16; ++k) cnt[k] = __reduce_add_sync(kFull, cnt[k]);  // ... then one reduction per length
+  int maxlen = 0, left = 1;
+  bool ok = true;
 #pragma unroll
   for (int l = 1; l < 16; ++l) {
-    offs[l] = static_cast<uint16_t>(off);
-    base[l][t] = off - static_cast<int32_t>(code);
+    if (cnt[l]) maxlen = l;
+    left = (left << 1) - static_cast<int>(cnt[l]);
+    if (left < 0) ok = false;  // over-subscribed
+  }
+  if (ok && maxlen > 0 && left > 0 && (what == 2 || maxlen != 1)) ok = false;  // incomplete
+  if (!ok) return false;
+  uint32_t offs[16];
+  uint32_t code = 0, off = 0;
+#pragma unroll
+  for (int l = 1; l < 16; ++l) {
+    offs[l] = off;
     lim[l] = (code + cnt[l]) << (15 - l);
+    if (lane == 0) base[l] = static_cast<int32_t>(off) - static_cast<int32_t>(code);
     code = (code + cnt[l]) << 1;
     off += cnt[l];
   }
-  for (int i = 0; i < n; ++i)
-    if (lens[i]) sym[offs[lens[i]]++][t] = static_cast<uint16_t>(i);
+  // symbols in canonical order, 32 at a time: rank within a length from the match mask
+  for (int g = 0; g < n; g += 32) {
+    const int i = g + lane;
+    const int l = i < n ? lens[i] : 0;
+    const uint32_t same = __match_any_sync(kFull, l);
+    const uint32_t rank = __popc(same & ((1u << lane) - 1u));
+    uint32_t my_off = 0;
+#pragma unroll
+    for (int k = 1; k < 16; ++k) {
+      if (l == k) my_off = offs[k];
+      offs[k] += __popc(__ballot_sync(kFull, l == k));
+    }
+    if (l) sym[my_off + rank] = static_cast<uint16_t>(i);
+  }
+  __syncwarp();
+  // first-level table: slot e holds the decode of bit pattern e (stream order, LSB first)
+  const int slots = 1 << fb;
+  for (int e = lane; e < slots; e += 32) {
+    const uint32_t c15 = (__brev(static_cast<uint32_t>(e)) >> (32 - fb)) << (15 - fb);
+    int len = 1;
+#pragma unroll
+    for (int l = 1; l < 16; ++l) len += (c15 >= lim[l]) ? 1 : 0;
+    uint32_t ent;
+    if (len > 15) {
+      ent = kBadEntry;
+    } else if (len > fb) {
+      ent = 0u;
+    } else {
+      const int s = sym[base[len] + static_cast<int>(c15 >> (15 - len))];
+      const uint32_t L = static_cast<uint32_t>(len);
+      if (what == 0) {
+        if (s < 256) ent = L | (kLit << 4) | (static_cast<uint32_t>(s) << 8);
+        else if (s == 256) ent = L | (kEob << 4);
+        else if (s < 286) ent = L | (kLen << 4) | (static_cast<uint32_t>(c_lext[s - 257]) << 8) |
+                                (static_cast<uint32_t>(c_lbase[s - 257]) << 16);
+        else ent = L | (kBad << 4);
+      } else if (what == 1) {
+        ent = s < 30 ? L | (static_cast<uint32_t>(c_dext[s]) << 8) | (static_cast<uint32_t>(c_dbase[s]) << 16)
+                     : L | (kBad << 4);
+      } else {
+        ent = L | (static_cast<uint32_t>(s) << 16);
+      }
+    }
+    fast[e] = ent;
+  }
+  __syncwarp();
   return true;
 }
 
-__device__ __forceinline__ uint64_t shl(uint64_t x, int s) { return s < 64 ? x << s : 0ull; }
-__device__ __forceinline__ uint64_t low_bytes(uint64_t x, int k) { return k >= 8 ? x : x & ((1ull << (8 * k)) - 1ull); }
-
-enum Mode : int { kIdle = 0, kSym = 1, kCopy = 2, kStart = 3, kHeader = 4, kStored = 5, kTrailer = 6 };
-
-/// One decoder lane: bit reader, output assembler and the block state machine. Every call of
-/// step() does a bounded amount of work - decode one symbol, or move <= 8 bytes of a match or
-/// stored block - so the 32 lanes of a warp stay on the same instruction stream.
-struct Lane {
-  // ---- job
-  const InflateJob* jobs;
-  uint32_t njobs, j, stride;
-  uint64_t usize;
-  uint32_t csize;
-  // ---- bit reader (LSB first); `nextw` is loaded one refill ahead to hide the load latency
-  const uint32_t* p;
-  const uint32_t* end;
+/// Lane 0's bit reader: LSB-first over 4-byte aligned words (chunks are 16-byte aligned).
+struct Bits {
+  const uint32_t* w0;  // stream start
+  uint32_t nwords;     // words that may be loaded (zeros are fed past them)
+  uint32_t next;       // next word index
   uint64_t b;
   int n;
-  uint32_t nextw, loaded;
-  // ---- output: bytes [0, oi) stored, `an` (< 8) pending in acc; w1/w2 = words at oi-8 / oi-16
-  uint64_t* dst;
-  uint64_t oi, acc, w1, w2;
-  int an;
-  uint32_t s1, s2;
-  // ---- block state
-  int mode;
-  bool last;
-  uint32_t rem, dist;
-  uint32_t llim[16], dlim[16];
-
   __device__ __forceinline__ void refill() {
     if (n <= 32) {
-      b |= static_cast<uint64_t>(nextw) << n;
+      const uint32_t w = next < nwords ? __ldg(w0 + next) : 0u;
+      ++next;
+      b |= static_cast<uint64_t>(w) << n;
       n += 32;
-      ++loaded;
-      nextw = p < end ? __ldg(p) : 0u;
-      ++p;
     }
   }
-  __device__ __forceinline__ uint32_t get(int k) {  // k <= 32 and n >= k
-    const uint32_t v = static_cast<uint32_t>(b) & static_cast<uint32_t>((1ull << k) - 1ull);
+  __device__ __forceinline__ uint32_t get(int k) {  // k <= 32, n >= k
+    const uint32_t v = static_cast<uint32_t>(b & ((1ull << k) - 1ull));
     b >>= k;
     n -= k;
     return v;
   }
-  __device__ __forceinline__ uint64_t consumed_bits() const { return static_cast<uint64_t>(loaded) * 32ull - n; }
-  __device__ __forceinline__ uint64_t pos() const { return oi + an; }
-
-  /// Decodes one symbol (>= 15 bits buffered); -1 for a code outside the table.
-  __device__ __forceinline__ int decode(const uint32_t (&lim)[16], const uint16_t (*sym)[kThreads],
-                                        const int32_t (*base)[kThreads], int t) {
-    const uint32_t c15 = __brev(static_cast<uint32_t>(b)) >> 17;
-    int len = 1;
-#pragma unroll
-    for (int l = 1; l < 16; ++l) len += (c15 >= lim[l]) ? 1 : 0;
-    if (len > 15) return -1;
-    const int idx = base[len][t] + static_cast<int>(c15 >> (15 - len));
-    b >>= len;
-    n -= len;
-    return sym[idx][t];
+  __device__ __forceinline__ void drop(int k) {
+    b >>= k;
+    n -= k;
   }
+  __device__ __forceinline__ uint64_t consumed() const { return static_cast<uint64_t>(next) * 32ull - n; }
+  __device__ __forceinline__ void seek(uint64_t bit) {  // restart at an absolute bit position
+    next = static_cast<uint32_t>(bit >> 5);
+    b = 0;
+    n = 0;
+    refill();
+    drop(static_cast<int>(bit & 31));
+  }
+};
 
-  __device__ __forceinline__ void flush_word(uint64_t w) {
-    dst[oi >> 3] = w;
-    const uint32_t lo = static_cast<uint32_t>(w), hi = static_cast<uint32_t>(w >> 32);
-    s2 += 8u * s1 + __dp4a(lo, 0x05060708u, 0u) + __dp4a(hi, 0x01020304u, 0u);
-    s1 += __dp4a(lo, 0x01010101u, 0u) + __dp4a(hi, 0x01010101u, 0u);
-    if ((oi & 2047) == 2040) {  // every 256 words: keep s2 below 2^32
-      s1 %= 65521u;
-      s2 %= 65521u;
-    }
+// lane-0 section outcomes
+enum Reason : int { kRFlush = 0, kREob = 1, kRErr = 2 };
+
+__device__ __forceinline__ uint64_t shl(uint64_t x, int s) { return s < 64 ? x << s : 0ull; }
+__device__ __forceinline__ uint64_t low_bytes(uint64_t x, int k) { return k >= 8 ? x : x & ((1ull << (8 * k)) - 1ull); }
+
+/// Lane 0's output assembler: bytes [0, oi) are whole words in the ring (and older ones flushed
+/// to HBM), the next `an` (< 8) bytes wait in `acc`; w1 / w2 mirror the ring words at oi-8 / oi-16
+/// so that the short distances typical of 8-byte columns never touch memory.
+struct Out0 {
+  uint64_t* ring;  // kRing / 8 words
+  const uint64_t* hbm;
+  uint64_t acc, w1, w2;
+  uint32_t oi;
+  int an;
+  __device__ __forceinline__ uint32_t pos() const { return oi + static_cast<uint32_t>(an); }
+  __device__ __forceinline__ void word(uint64_t w) {
+    ring[(oi >> 3) & (kRing / 8 - 1)] = w;
     w2 = w1;
     w1 = w;
     oi += 8;
@@ -169,227 +222,330 @@ struct Lane {
     acc |= shl(v, 8 * an);
     const int t = an + k;
     if (t >= 8) {
-      flush_word(acc);
+      word(acc);
       acc = an ? (v >> (64 - 8 * an)) : 0ull;
       an = t - 8;
     } else {
       an = t;
     }
   }
-  /// 8 bytes at position s, s + 8 <= pos() (so s < oi): from the register window when recent.
-  __device__ __forceinline__ uint64_t read8(uint64_t s) const {
+  /// 8 bytes at position s, s + 8 <= pos() (hence s < oi).
+  __device__ __forceinline__ uint64_t read8(uint32_t s) const {
     const int sh = static_cast<int>(s & 7) * 8;
-    if (static_cast<int64_t>(s) >= static_cast<int64_t>(oi) - 16) {
-      const bool q0 = s < oi - 8;  // starts in the w2 word
-      const uint64_t lo = q0 ? w2 : w1, hi = q0 ? w1 : acc;
-      return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+    uint64_t lo, hi;
+    if (s + 16 >= oi) {  // register window [oi - 16, oi + an)
+      const bool q0 = s + 8 < oi;
+      lo = q0 ? w2 : w1;
+      hi = q0 ? w1 : acc;
+    } else if (s + kRing - 8 >= oi) {  // both words still in the ring
+      lo = ring[(s >> 3) & (kRing / 8 - 1)];
+      hi = ring[((s >> 3) + 1) & (kRing / 8 - 1)];
+    } else {  // flushed long ago (flushed >= oi - 1290 > s + 16)
+      lo = __ldcg(reinterpret_cast<const unsigned long long*>(hbm) + (s >> 3));
+      hi = __ldcg(reinterpret_cast<const unsigned long long*>(hbm) + (s >> 3) + 1);
     }
-    const uint64_t* m = dst + (s >> 3);
-    const uint64_t a = m[0];
-    return sh ? (a >> sh) | (m[1] << (64 - sh)) : a;
+    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
   }
   /// The 8 bytes ending at pos() (positions before 0 are never referenced).
   __device__ __forceinline__ uint64_t last8() const { return an ? (w1 >> (8 * an)) | (acc << (64 - 8 * an)) : w1; }
-
-  __device__ __forceinline__ void fail(unsigned int* err) {
-    atomicOr(err, 1u);
-    j += stride;
-    mode = kStart;
-  }
-
-  __device__ void start(unsigned int* err) {
-    if (j >= njobs) {
-      mode = kIdle;
-      return;
-    }
-    const InflateJob job = jobs[j];
-    usize = job.usize;
-    csize = job.csize;
-    p = reinterpret_cast<const uint32_t*>(job.src);
-    end = p + (job.csize + 3) / 4;
-    nextw = p < end ? __ldg(p) : 0u;
-    ++p;
-    loaded = 0;
-    b = 0;
-    n = 0;
-    dst = reinterpret_cast<uint64_t*>(job.dst);
-    oi = acc = w1 = w2 = 0;
-    an = 0;
-    s1 = 1;
-    s2 = 0;
-    last = false;
-    refill();
-    // zlib header (RFC 1950): deflate, window <= 32K, no preset dictionary, FCHECK
-    const uint32_t cmf = get(8), flg = get(8);
-    if ((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20)) return fail(err);
-    mode = kHeader;
-  }
-
-  __device__ void header(Smem& sm, int t, unsigned int* err) {
-    if (consumed_bits() > csize * 8ull) return fail(err);  // ran past the stream
-    refill();
-    last = get(1);
-    const uint32_t type = get(2);
-    uint8_t lens[320];
-    if (type == 0) {  // stored
-      get(n & 7);
-      refill();
-      const uint32_t len = get(16), nlen = get(16);
-      if (len != (~nlen & 0xFFFFu) || pos() + len > usize) return fail(err);
-      rem = len;
-      mode = kStored;
-      return;
-    }
-    if (type == 3) return fail(err);
-    if (type == 1) {  // fixed Huffman codes
-      for (int i = 0; i < 144; ++i) lens[i] = 8;
-      for (int i = 144; i < 256; ++i) lens[i] = 9;
-      for (int i = 256; i < 280; ++i) lens[i] = 7;
-      for (int i = 280; i < 288; ++i) lens[i] = 8;
-      build_table(lens, 288, false, sm.lsym, sm.lbase, llim, t);
-      for (int i = 0; i < 32; ++i) lens[i] = 5;
-      build_table(lens, 32, false, sm.dsym, sm.dbase, dlim, t);
-      mode = kSym;
-      return;
-    }
-    // dynamic Huffman codes
-    refill();
-    const int hlit = static_cast<int>(get(5)) + 257, hdist = static_cast<int>(get(5)) + 1,
-              hclen = static_cast<int>(get(4)) + 4;
-    if (hlit > 286 || hdist > 30) return fail(err);
-    for (int i = 0; i < 19; ++i) lens[i] = 0;
-    for (int i = 0; i < hclen; ++i) {
-      refill();
-      lens[c_clorder[i]] = static_cast<uint8_t>(get(3));
-    }
-    // the code-length code goes into the distance slots; the real distance code overwrites it
-    if (!build_table(lens, 19, true, sm.dsym, sm.dbase, dlim, t)) return fail(err);
-    const int total = hlit + hdist;
-    int i = 0;
-    while (i < total) {
-      refill();
-      const int s = decode(dlim, sm.dsym, sm.dbase, t);
-      if (s < 0) return fail(err);
-      if (s < 16) {
-        lens[i++] = static_cast<uint8_t>(s);
-        continue;
-      }
-      uint8_t v = 0;
-      int rep;
-      if (s == 16) {
-        if (i == 0) return fail(err);
-        v = lens[i - 1];
-        rep = 3 + static_cast<int>(get(2));
-      } else if (s == 17) {
-        rep = 3 + static_cast<int>(get(3));
-      } else {
-        rep = 11 + static_cast<int>(get(7));
-      }
-      if (i + rep > total) return fail(err);
-      while (rep--) lens[i++] = v;
-    }
-    if (lens[256] == 0) return fail(err);  // no end-of-block code
-    if (!build_table(lens, hlit, false, sm.lsym, sm.lbase, llim, t)) return fail(err);
-    if (!build_table(lens + hlit, hdist, false, sm.dsym, sm.dbase, dlim, t)) return fail(err);
-    mode = kSym;
-  }
-
-  __device__ void trailer(unsigned int* err) {
-    get(n & 7);  // byte align
-    refill();
-    const uint32_t want = __byte_perm(get(32), 0, 0x0123);  // Adler-32 is big-endian
-    if (consumed_bits() > csize * 8ull || pos() != usize) return fail(err);
-    uint32_t a = s1 % 65521u, c = s2 % 65521u;
-    for (int k = 0; k < an; ++k) {  // sizes that are not a multiple of 8 (never for column chunks)
-      const uint32_t byte = static_cast<uint32_t>(acc >> (8 * k)) & 0xFFu;
-      reinterpret_cast<uint8_t*>(dst)[oi + k] = static_cast<uint8_t>(byte);
-      a = (a + byte) % 65521u;
-      c = (c + a) % 65521u;
-    }
-    if (want != ((c << 16) | a)) return fail(err);
-    j += stride;
-    mode = kStart;
-  }
 };
 
-__global__ void __launch_bounds__(kThreads) k_inflate(const InflateJob* __restrict__ jobs, uint32_t njobs,
-                                                     unsigned int* err) {
-  __shared__ Smem sm;
-  const int t = threadIdx.x;
-  Lane L;
-  L.jobs = jobs;
-  L.njobs = njobs;
-  L.j = blockIdx.x * kThreads + t;
-  L.stride = gridDim.x * kThreads;
-  L.mode = kStart;
+/// Flushes ring bytes [flushed, flushed + nbytes) (nbytes <= kFlush) to dst in whole 16-byte
+/// granules (chunk buffers are padded to 16 bytes) and folds them into the Adler-32 state
+/// (s1, s2 identical in every lane).
+__device__ __forceinline__ void flush(const uint8_t* ring, uint8_t* dst, uint32_t flushed, uint32_t nbytes, uint32_t& s1,
+                                      uint32_t& s2, int lane) {
+  const uint32_t mine = static_cast<uint32_t>(lane) * 32u;
+  uint32_t A = 0, B = 0;
+  if (mine < nbytes) {
+    const uint32_t rp = (flushed + mine) & kRingMask;  // 32-byte aligned, never wraps
+    const uint4 x = *reinterpret_cast<const uint4*>(ring + rp);
+    const uint4 y = *reinterpret_cast<const uint4*>(ring + rp + 16);
+    uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+    const uint32_t valid = min(32u, nbytes - mine);
+    if (valid < 32) {  // zero the bytes past the end of the stream
 #pragma unroll
-  for (int l = 0; l < 16; ++l) L.llim[l] = L.dlim[l] = 0;
-  while (__any_sync(0xFFFFFFFFu, L.mode != kIdle)) {
-    if (L.mode == kSym) {
-      L.refill();
-      int s = L.decode(L.llim, sm.lsym, sm.lbase, t);
-      if (s < 0) {
-        L.fail(err);
-      } else if (s < 256) {
-        if (L.pos() >= L.usize) {
-          L.fail(err);
-        } else {
-          L.put(static_cast<uint64_t>(s), 1);
-        }
-      } else if (s == 256) {
-        L.mode = L.last ? kTrailer : kHeader;
-      } else if (s - 257 >= 29) {
-        L.fail(err);
-      } else {
-        s -= 257;
-        const uint32_t len = c_lbase[s] + L.get(c_lext[s]);
-        L.refill();
-        const int ds = L.decode(L.dlim, sm.dsym, sm.dbase, t);
-        if (ds < 0 || ds >= 30) {
-          L.fail(err);
-        } else {
-          const uint32_t dist = c_dbase[ds] + L.get(c_dext[ds]);
-          const uint64_t q = L.pos();
-          if (dist > q || q + len > L.usize) {
-            L.fail(err);
-          } else {
-            L.rem = len;
-            L.dist = dist;
-            L.mode = kCopy;
-          }
-        }
+      for (int k = 0; k < 8; ++k) {
+        const int keep = static_cast<int>(valid) - 4 * k;
+        w[k] = keep >= 4 ? w[k] : (keep <= 0 ? 0u : (w[k] & ((1u << (8 * keep)) - 1u)));
       }
-    } else if (L.mode == kCopy) {
-      const int k = L.rem < 8 ? static_cast<int>(L.rem) : 8;
-      uint64_t v;
-      if (L.dist >= 8) {
-        v = L.read8(L.pos() - L.dist);
-      } else {  // period < 8: replicate the last `dist` bytes
-        const int d = static_cast<int>(L.dist);
-        v = low_bytes(L.last8() >> (8 * (8 - d)), d);
+    }
+    uint4* d = reinterpret_cast<uint4*>(dst + flushed + mine);
+    d[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    if (valid > 16) d[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      A = __dp4a(w[k], 0x01010101u, A);
+      // weights 32 - m for bytes m = 4k..4k+3 of this lane's slice
+      const uint32_t wt = (32u - 4u * k) | ((31u - 4u * k) << 8) | ((30u - 4u * k) << 16) | ((29u - 4u * k) << 24);
+      B = __dp4a(w[k], wt, B);
+    }
+  }
+  // a block of N bytes: s2 += N*s1 + sum_i [(N - 32i - 32) A_i + B_i], s1 += sum_i A_i
+  const int32_t tail = static_cast<int32_t>(nbytes) - static_cast<int32_t>(mine) - 32;
+  const uint32_t part = static_cast<uint32_t>(static_cast<int32_t>(B) + tail * static_cast<int32_t>(A));
+  const uint32_t SA = __reduce_add_sync(kFull, A);
+  const uint32_t SB = __reduce_add_sync(kFull, part);
+  s2 = (s2 + nbytes * s1 + SB) % 65521u;
+  s1 = (s1 + SA) % 65521u;
+}
+
+/// Lane 0's decode loop for one data phase: runs until 1 KB is ready to flush, the block ends or
+/// the stream is invalid. Stored blocks (type 0) copy `stored` more bytes; else Huffman symbols.
+__device__ __forceinline__ int decode_run(Bits& br, Out0& o, WarpSmem& sm, const uint32_t (&llim)[16],
+                                          const uint32_t (&dlim)[16], int type, uint32_t& stored, uint32_t flushed,
+                                          uint32_t usize) {
+  if (type == 0) {
+    while (stored) {
+      const int k = stored < 4 ? static_cast<int>(stored) : 4;
+      br.refill();
+      o.put(br.get(8 * k), k);
+      stored -= static_cast<uint32_t>(k);
+      if (o.oi - flushed >= kFlush) return kRFlush;
+    }
+    return kREob;
+  }
+  while (true) {
+    br.refill();
+    uint32_t e = sm.lfast[br.b & ((1u << kLB) - 1u)];
+    int cl = static_cast<int>(e & 15);
+    if (cl == 0) {  // code longer than the first-level table
+      const int s = canon_decode(br.b, llim, sm.lbase, sm.lsym, cl);
+      if (s < 0) return kRErr;
+      e = s < 256    ? (kLit << 4) | (static_cast<uint32_t>(s) << 8)
+          : s == 256 ? (kEob << 4)
+          : s < 286  ? (kLen << 4) | (static_cast<uint32_t>(c_lext[s - 257]) << 8) |
+                          (static_cast<uint32_t>(c_lbase[s - 257]) << 16)
+                     : (kBad << 4);
+    }
+    br.drop(cl);
+    const uint32_t kind = (e >> 4) & 3;
+    if (kind == kLit) {
+      if (o.pos() >= usize) return kRErr;
+      o.put(e >> 8, 1);
+      if (o.oi - flushed >= kFlush) return kRFlush;
+      continue;
+    }
+    if (kind == kEob) return kREob;
+    if (kind == kBad) return kRErr;
+    uint32_t len = (e >> 16) + br.get(static_cast<int>((e >> 8) & 15));
+    br.refill();
+    uint32_t de = sm.dfast[br.b & ((1u << kDB) - 1u)];
+    int dl = static_cast<int>(de & 15);
+    if (dl == 0) {
+      const int s = canon_decode(br.b, dlim, sm.dbase, sm.dsym, dl);
+      if (s < 0 || s >= 30) return kRErr;
+      de = (static_cast<uint32_t>(c_dext[s]) << 8) | (static_cast<uint32_t>(c_dbase[s]) << 16);
+    } else if (((de >> 4) & 3) == kBad) {
+      return kRErr;
+    }
+    br.drop(dl);
+    const uint32_t dist = (de >> 16) + br.get(static_cast<int>((de >> 8) & 15));
+    if (dist > o.pos() || o.pos() + len > usize) return kRErr;
+    if (dist >= 8) {
+      while (len) {
+        const int k = len < 8 ? static_cast<int>(len) : 8;
+        o.put(o.read8(o.pos() - dist), k);
+        len -= static_cast<uint32_t>(k);
+      }
+    } else {  // period < 8: replicate the last `dist` bytes
+      const int d = static_cast<int>(dist);
+      while (len) {
+        uint64_t v = low_bytes(o.last8() >> (8 * (8 - d)), d);
         v |= shl(v, 8 * d);
         v |= shl(v, 16 * d);
         v |= shl(v, 32 * d);
+        const int k = len < 8 ? static_cast<int>(len) : 8;
+        o.put(v, k);
+        len -= static_cast<uint32_t>(k);
       }
-      L.put(v, k);
-      L.rem -= k;
-      if (L.rem == 0) L.mode = kSym;
-    } else if (L.mode == kStored) {
-      if (L.rem == 0) {
-        L.mode = L.last ? kTrailer : kHeader;
-      } else {
-        const int k = L.rem < 4 ? static_cast<int>(L.rem) : 4;
-        L.refill();
-        L.put(L.get(8 * k), k);
-        L.rem -= k;
-      }
-    } else if (L.mode == kHeader) {
-      L.header(sm, t, err);
-    } else if (L.mode == kTrailer) {
-      L.trailer(err);
-    } else if (L.mode == kStart) {
-      L.start(err);
     }
+    if (o.oi - flushed >= kFlush) return kRFlush;
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32) k_inflate(const InflateJob* __restrict__ jobs, uint32_t njobs,
+                                                        unsigned int* err) {
+  __shared__ WarpSmem smem[kWarps];
+  const int lane = threadIdx.x & 31;
+  WarpSmem& sm = smem[threadIdx.x >> 5];
+  const uint32_t nwarps = gridDim.x * kWarps;
+  uint32_t llim[16], dlim[16];
+#pragma unroll
+  for (int l = 0; l < 16; ++l) llim[l] = dlim[l] = 0;
+
+  for (uint32_t j = blockIdx.x * kWarps + (threadIdx.x >> 5); j < njobs; j += nwarps) {
+    const InflateJob job = jobs[j];
+    const uint32_t usize = job.usize;
+    uint8_t* const dst = job.dst;
+    Bits br;
+    br.w0 = reinterpret_cast<const uint32_t*>(job.src);
+    br.nwords = (job.csize + 3) / 4;
+    br.next = 0;
+    br.b = 0;
+    br.n = 0;
+    Out0 o;
+    o.ring = reinterpret_cast<uint64_t*>(sm.ring);
+    o.hbm = reinterpret_cast<const uint64_t*>(dst);
+    o.acc = o.w1 = o.w2 = 0;
+    o.oi = 0;
+    o.an = 0;
+    uint32_t flushed = 0, s1 = 1, s2 = 0;
+    bool ok, last = false;
+    {  // zlib header (RFC 1950): deflate, window <= 32K, no preset dictionary, FCHECK
+      int bad = 0;
+      if (lane == 0) {
+        br.refill();
+        const uint32_t cmf = br.get(8), flg = br.get(8);
+        bad = (cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20);
+      }
+      ok = !__shfl_sync(kFull, bad, 0);
+    }
+    while (ok && !last) {
+      // ---------------- block header: lane 0 reads, the warp builds the tables
+      int type = 0, hlit = 0, hdist = 0, bad = 0, lastb = 0;
+      uint32_t stored = 0;
+      if (lane == 0) {
+        if (br.consumed() > job.csize * 8ull) bad = 1;  // ran past the stream
+        br.refill();
+        lastb = static_cast<int>(br.get(1));
+        type = static_cast<int>(br.get(2));
+        if (type == 0) {
+          br.drop(br.n & 7);
+          br.refill();
+          stored = br.get(16);
+          const uint32_t nlen = br.get(16);
+          if (stored != (~nlen & 0xFFFFu) || o.pos() + stored > usize) bad = 1;
+        } else if (type == 2) {
+          br.refill();
+          hlit = static_cast<int>(br.get(5)) + 257;
+          hdist = static_cast<int>(br.get(5)) + 1;
+          const int hclen = static_cast<int>(br.get(4)) + 4;
+          if (hlit > 286 || hdist > 30) bad = 1;
+          for (int i = 0; i < 19; ++i) sm.lens[i] = 0;
+          for (int i = 0; i < hclen; ++i) {
+            br.refill();
+            sm.lens[c_clorder[i]] = static_cast<uint8_t>(br.get(3));
+          }
+        } else if (type == 3) {
+          bad = 1;
+        }
+      }
+      last = __shfl_sync(kFull, lastb, 0) != 0;
+      type = __shfl_sync(kFull, type, 0);
+      hlit = __shfl_sync(kFull, hlit, 0);
+      hdist = __shfl_sync(kFull, hdist, 0);
+      if (__shfl_sync(kFull, bad, 0)) {
+        ok = false;
+        break;
+      }
+      if (type == 1) {  // fixed codes
+        for (int i = lane; i < 288; i += 32) sm.lens[i] = i < 144 ? 8 : (i < 256 ? 9 : (i < 280 ? 7 : 8));
+        __syncwarp();
+        build_table(sm.lens, 288, 0, sm.lsym, sm.lbase, sm.lfast, kLB, llim, lane);
+        sm.lens[lane] = 5;
+        __syncwarp();
+        build_table(sm.lens, 32, 1, sm.dsym, sm.dbase, sm.dfast, kDB, dlim, lane);
+      } else if (type == 2) {  // dynamic codes: the code-length code, then both code-length sequences
+        __syncwarp();
+        if (!build_table(sm.lens, 19, 2, sm.dsym, sm.dbase, sm.dfast, kCB, dlim, lane)) {
+          ok = false;
+          break;
+        }
+        if (lane == 0) {
+          const int total = hlit + hdist;
+          int i = 0;
+          while (i < total) {
+            br.refill();
+            const uint32_t e = sm.dfast[br.b & ((1u << kCB) - 1u)];
+            if (((e >> 4) & 3) == kBad) {  // bits outside the code-length code
+              bad = 1;
+              break;
+            }
+            br.drop(static_cast<int>(e & 15));
+            const int s = static_cast<int>(e >> 16);
+            if (s < 16) {
+              sm.lens[i++] = static_cast<uint8_t>(s);
+              continue;
+            }
+            uint8_t v = 0;
+            int rep;
+            if (s == 16) {
+              if (i == 0) {
+                bad = 1;
+                break;
+              }
+              v = sm.lens[i - 1];
+              rep = 3 + static_cast<int>(br.get(2));
+            } else if (s == 17) {
+              rep = 3 + static_cast<int>(br.get(3));
+            } else {
+              rep = 11 + static_cast<int>(br.get(7));
+            }
+            if (i + rep > total) {
+              bad = 1;
+              break;
+            }
+            while (rep--) sm.lens[i++] = v;
+          }
+          if (!bad && sm.lens[256] == 0) bad = 1;  // no end-of-block code
+        }
+        if (__shfl_sync(kFull, bad, 0)) {
+          ok = false;
+          break;
+        }
+        __syncwarp();
+        if (!build_table(sm.lens, hlit, 0, sm.lsym, sm.lbase, sm.lfast, kLB, llim, lane) ||
+            !build_table(sm.lens + hlit, hdist, 1, sm.dsym, sm.dbase, sm.dfast, kDB, dlim, lane)) {
+          ok = false;
+          break;
+        }
+      }
+      // ---------------- data: lane 0 decodes; the warp flushes each finished 1 KB
+      while (true) {
+        int reason = kREob;
+        uint32_t oi = 0;
+        if (lane == 0) {
+          reason = decode_run(br, o, sm, llim, dlim, type, stored, flushed, usize);
+          oi = o.oi;
+        }
+        __syncwarp();
+        reason = __shfl_sync(kFull, reason, 0);
+        oi = __shfl_sync(kFull, oi, 0);
+        if (reason == kRErr) {
+          ok = false;
+          break;
+        }
+        while (oi - flushed >= kFlush) {
+          flush(sm.ring, dst, flushed, kFlush, s1, s2, lane);
+          flushed += kFlush;
+        }
+        __syncwarp();
+        if (reason == kREob) break;
+      }
+    }
+    if (ok) {
+      // ---------------- trailer: last partial word, final flush, exact size, Adler-32
+      uint32_t P = 0;
+      if (lane == 0) {
+        if (o.an) reinterpret_cast<uint64_t*>(sm.ring)[(o.oi >> 3) & (kRing / 8 - 1)] = o.acc;
+        P = o.pos();
+      }
+      __syncwarp();
+      P = __shfl_sync(kFull, P, 0);
+      if (P != usize) ok = false;
+      if (ok && P > flushed) flush(sm.ring, dst, flushed, P - flushed, s1, s2, lane);
+      int bad = 0;
+      if (ok && lane == 0) {
+        br.drop(br.n & 7);
+        br.refill();
+        const uint32_t want = __byte_perm(br.get(32), 0, 0x0123);  // big-endian
+        bad = br.consumed() > job.csize * 8ull || want != ((s2 << 16) | s1);
+      }
+      if (__shfl_sync(kFull, bad, 0)) ok = false;
+    }
+    if (!ok && lane == 0) atomicOr(err, 1u);
+    __syncwarp();
   }
 }
 
@@ -397,9 +553,10 @@ __global__ void __launch_bounds__(kThreads) k_inflate(const InflateJob* __restri
 
 void launch_inflate(const InflateJob* d_jobs, uint32_t njobs, unsigned int* d_err, void* stream) {
   if (njobs == 0) return;
-  // persistent lanes: each takes jobs j, j + stride, ... (longest first, see plan_batches)
-  const uint32_t blocks = std::min<uint32_t>((njobs + kThreads - 1) / kThreads, 148u * 4u);
-  k_inflate<<<blocks, kThreads, 0, static_cast<cudaStream_t>(stream)>>>(d_jobs, njobs, d_err);
+  // persistent warps: warp w takes jobs w, w + nwarps, ... (longest first, see plan_batches);
+  // 6 CTAs x 4 warps fit an SM (33 KB of tables + ring per CTA)
+  const uint32_t blocks = std::min<uint32_t>((njobs + kWarps - 1) / kWarps, 148u * 6u);
+  k_inflate<<<blocks, kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(d_jobs, njobs, d_err);
   count_external_launch();
 }
 
