@@ -132,6 +132,14 @@ void psg_ctx_destroy(psg_ctx* ctx);
 int psg_execute_plan(psg_ctx* ctx, const char* plan_json, const char* data_root, int mode,
                      psg_result** out);
 
+/* Extension (the Q6 analog): plans WITHOUT a shuffled join - one root stream
+ * (a scan, or a chain of local joins against replicated scans) ending in a global aggregate -
+ * which the reference's execute_plan rejects (pipeline.cpp:334-335; psg_execute_plan keeps that
+ * InvalidInput). No exchange: each rank returns its node's unmerged partial row [rows, sums...]
+ * (the global-aggregate semantics of pipeline.cpp:277-281). */
+int psg_execute_local(psg_ctx* ctx, const char* plan_json, const char* data_root, int mode,
+                      psg_result** out);
+
 /* HBM-resident variant: psg_stage_plan reads every file the plan touches into HBM once;
  * psg_execute_staged runs the query over the staged bytes (no host I/O). When out is NULL the
  * result stays on the device (its row count is still available through stats). */

@@ -137,7 +137,8 @@ class Plan:
     raw: dict = field(default_factory=dict)
 
 
-def parse_plan(text: str, data_root: str, node: int, nodes: int) -> Plan:
+def parse_plan(text: str, data_root: str, node: int, nodes: int, local: bool = False) -> Plan:
+    """local=True: the no-shuffle plans of psg_execute_local (exactly zero shuffled joins)."""
     j = json.loads(text)
     scans = []
     for s in j["scans"]:
@@ -156,6 +157,10 @@ def parse_plan(text: str, data_root: str, node: int, nodes: int) -> Plan:
         agg = {"group_by": j["aggregate"].get("group_by", ""), "sums": list(j["aggregate"].get("sums", []))}
     plan = Plan(scans, joins, agg, j)
     shuffles = [x for x in joins if x.shuffle]
+    if local:
+        if shuffles or not agg or agg["group_by"]:
+            raise ValueError("invalid input: local plans have no shuffled join and end in a global aggregate")
+        return plan
     if len(shuffles) != 1:
         raise ValueError("invalid input: plans currently require one shuffled join")
     if agg and agg["group_by"] and agg["group_by"] != shuffles[0].probe_key:
@@ -348,6 +353,25 @@ def execute(plan_text: str, data_root: str, nodes: int):
         else:
             rows = np.stack(joined.cols, axis=1) if joined.cols else np.zeros((0, 0), np.uint64)
             results.append((joined.fields, rows))
+    return results
+
+
+def execute_local(plan_text: str, data_root: str, nodes: int):
+    """Local plans (no shuffled join; the psg_execute_local extension): per node, the root stream
+    (scan or replicated-join chain, _stream above) reduced to one global-aggregate partial row,
+    the semantics of execute_plan's global aggregate (pipeline.cpp:277-281, 892-897).
+    Returns [(schema, rows)] per node."""
+    results = []
+    for k in range(nodes):
+        plan = parse_plan(plan_text, data_root, k, nodes, local=True)
+        consumed = {j.build for j in plan.joins} | {j.probe for j in plan.joins}
+        roots = [j.id for j in plan.joins if j.id not in consumed] + \
+                [s.table for s in plan.scans if not s.replicated and s.table not in consumed]
+        assert len(roots) == 1, roots
+        tables = _local_tables(plan)
+        stream = _stream(plan, roots[0], tables)
+        results.append(aggregate(stream, "", plan.aggregate["sums"]) if stream is not None
+                       else ([], np.zeros((0, 0), np.uint64)))
     return results
 
 

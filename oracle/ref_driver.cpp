@@ -6,6 +6,11 @@
 //   gen  -> pystachio::gen_workload            (/root/reference/proj/src/bench.cpp:85-114)
 //   run  -> pystachio::run_socket_pipeline      (/root/reference/proj/src/pipeline_harness.cpp:81-109)
 //           pystachio::run_sim_pipeline         (/root/reference/proj/src/pipeline_harness.cpp:23-79)
+//   scanagg -> pystachio::read_blocking with a predicate (/root/reference/proj/src/scan.cpp:273-336,
+//           set up like the reference's pybind `scan`, python/bindings.cpp:139-155), then the
+//           global-aggregate sums of the surviving rows (HashAggregator::add semantics,
+//           pipeline.cpp:275-294: int64 sums wrap mod 2^64, float64 sums add as doubles) - the
+//           Q6-analog the reference's execute_plan cannot express
 // and prints one JSON line with result checksums (rowhash = sum over rows of FNV-1a64 of the
 // row's little-endian words) plus wall time, optionally dumping the raw rows.
 #include <chrono>
@@ -21,6 +26,7 @@
 #include "pystachio/hashing.hpp"
 #include "pystachio/pipeline_harness.hpp"
 #include "pystachio/psto.hpp"
+#include "pystachio/scan.hpp"
 
 using namespace pystachio;
 
@@ -30,6 +36,21 @@ std::string arg(int argc, char** argv, const std::string& key, const std::string
   for (int i = 1; i + 1 < argc; ++i)
     if (key == argv[i]) return argv[i + 1];
   return dflt;
+}
+
+std::vector<std::string> split(const std::string& s, char sep) {
+  std::vector<std::string> out;
+  std::string cur;
+  for (char c : s) {
+    if (c == sep) {
+      if (!cur.empty()) out.push_back(cur);
+      cur.clear();
+    } else {
+      cur += c;
+    }
+  }
+  if (!cur.empty()) out.push_back(cur);
+  return out;
 }
 
 std::string read_file(const std::string& p) {
@@ -129,6 +150,69 @@ int main(int argc, char** argv) {
         const double s =
             std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         summarize(rows, ncols, s, per_node, it == 0 ? dump : std::string());
+        std::fflush(stdout);
+      }
+      return 0;
+    }
+    if (cmd == "scanagg") {
+      // --paths a,b  --pred "col:op:value;..." (value with '.' = float literal)  --sums c1,c2
+      const auto paths = split(arg(argc, argv, "--paths", ""), ',');
+      const auto sums = split(arg(argc, argv, "--sums", ""), ',');
+      const int repeat = std::stoi(arg(argc, argv, "--repeat", "1"));
+      Predicate pred;
+      for (const auto& a : split(arg(argc, argv, "--pred", ""), ';')) {
+        const auto f = split(a, ':');
+        if (f.size() != 3) throw std::runtime_error("bad --pred atom " + a);
+        if (f[2].find('.') != std::string::npos)
+          pred.and_atom(f[0], compare_op_from_string(f[1]), std::stod(f[2]));
+        else
+          pred.and_atom(f[0], compare_op_from_string(f[1]), static_cast<std::int64_t>(std::stoll(f[2])));
+      }
+      for (int it = 0; it < repeat; ++it) {
+        const auto t0 = std::chrono::steady_clock::now();
+        RealRuntime rt;
+        Trace trace;
+        MemoryPool pool;
+        NodeExecState state;
+        SimCostConfig cost;
+        ExecEnv env{rt, trace, 0, pool, cost, StallFaultConfig{}, state};
+        DeviceConfig cfg{"dev0", 0, 0, DeviceBacking::RealFile};
+        DeviceModel dev(cfg);
+        ScanOptions opts;
+        opts.predicate = pred;
+        std::uint64_t rows = 0;
+        std::vector<std::uint64_t> isum(sums.size(), 0);
+        std::vector<double> fsum(sums.size(), 0.0);
+        std::vector<bool> is_float(sums.size(), false);
+        for (const auto& path : paths) {
+          ChunkBatch b = read_blocking(env, path, dev, opts);
+          rows += b.row_count();
+          for (std::size_t k = 0; k < sums.size(); ++k) {
+            const Column& c = b.column(sums[k]);
+            is_float[k] = c.type() == LogicalType::Float64;
+            for (std::uint64_t w : c.raw()) {
+              if (is_float[k]) {
+                double d;
+                std::memcpy(&d, &w, 8);
+                fsum[k] += d;
+              } else {
+                isum[k] += w;
+              }
+            }
+          }
+        }
+        const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        std::vector<std::vector<std::uint64_t>> out;
+        if (rows) {
+          std::vector<std::uint64_t> r{rows};
+          for (std::size_t k = 0; k < sums.size(); ++k) {
+            std::uint64_t w = isum[k];
+            if (is_float[k]) std::memcpy(&w, &fsum[k], 8);
+            r.push_back(w);
+          }
+          out.push_back(r);
+        }
+        summarize(out, 1 + sums.size(), s, {out.size()}, std::string());
         std::fflush(stdout);
       }
       return 0;

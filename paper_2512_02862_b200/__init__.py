@@ -29,7 +29,8 @@ STATUS = {0: "OK", 1: "UnknownColumn", 2: "MemoryExceeded", 3: "StreamClosed", 4
           10: "InfeasibleBudget", 11: "MalformedTrace", 12: "EmptyTrace", 100: "CudaError", 101: "NcclError",
           102: "InternalError"}
 EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_unique_id", "psg_ctx_init_comm",
-           "psg_ctx_set_ingest", "psg_ctx_set_semijoin", "psg_ctx_set_fused_shuffle", "psg_ctx_destroy", "psg_execute_plan", "psg_stage_plan",
+           "psg_ctx_set_ingest", "psg_ctx_set_semijoin", "psg_ctx_set_fused_shuffle", "psg_ctx_destroy", "psg_execute_plan",
+           "psg_execute_local", "psg_stage_plan",
            "psg_execute_staged", "psg_staged_free", "psg_result_shape", "psg_result_field", "psg_result_data",
            "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_codec_decompress", "psg_psto_write",
            "psg_psto_inspect", "psg_gen_tpch", "psg_jit_selftest", "psg_tmin"]
@@ -88,6 +89,7 @@ def lib():
             "psg_ctx_set_semijoin": ([vp, i32], i32), "psg_ctx_set_fused_shuffle": ([vp, i32], i32),
             "psg_ctx_destroy": ([vp], None),
             "psg_execute_plan": ([vp, c, c, i32, P(vp)], i32), "psg_stage_plan": ([vp, c, c, P(vp)], i32),
+            "psg_execute_local": ([vp, c, c, i32, P(vp)], i32),
             "psg_execute_staged": ([vp, vp, i32, P(vp), P(Stats)], i32), "psg_staged_free": ([vp], None),
             "psg_result_shape": ([vp, P(u64), P(ctypes.c_uint32)], i32),
             "psg_result_field": ([vp, ctypes.c_uint32, P(c), P(i32)], i32),
@@ -248,6 +250,15 @@ class Context:
         text = plan if isinstance(plan, str) else json.dumps(plan)
         out = ctypes.c_void_p()
         _check(lib().psg_execute_plan(self._h, text.encode(), data_root.encode(), MODES[mode], ctypes.byref(out)))
+        return Result(out)
+
+    def execute_local(self, plan, data_root, mode="overlapped") -> Result:
+        """Plans without a shuffled join (scan -> replicated joins -> global aggregate, the Q6
+        analog); one partial row [rows, sums...] for this rank's node. Extension: the reference's
+        execute_plan rejects such plans (pipeline.cpp:334-335)."""
+        text = plan if isinstance(plan, str) else json.dumps(plan)
+        out = ctypes.c_void_p()
+        _check(lib().psg_execute_local(self._h, text.encode(), data_root.encode(), MODES[mode], ctypes.byref(out)))
         return Result(out)
 
     def stage_plan(self, plan, data_root):

@@ -202,6 +202,16 @@ int psg_execute_plan(psg_ctx* ctx, const char* plan_json, const char* data_root,
   });
 }
 
+int psg_execute_local(psg_ctx* ctx, const char* plan_json, const char* data_root, int mode, psg_result** out) {
+  return guarded([&] {
+    if (!ctx || !plan_json || !data_root || !out) throw InvalidInput("null argument");
+    if (ctx->c.io_threads == 0) ctx->c.io_threads = 8;
+    auto r = std::make_unique<psg_result>();
+    r->r = execute_local(ctx->c, plan_json, data_root, mode);
+    *out = r.release();
+  });
+}
+
 int psg_stage_plan(psg_ctx* ctx, const char* plan_json, const char* data_root, psg_staged** out) {
   return guarded([&] {
     if (!ctx || !plan_json || !data_root || !out) throw InvalidInput("null argument");

@@ -29,7 +29,15 @@ constexpr uint64_t kSlotMul = 0xD6E8FEB86659FD93ULL;   // table slot = (k * kSlo
 constexpr uint64_t kBloomMul = 0xA24BAED4963EE407ULL;  // bloom word/bits from (k * kBloomMul)
 constexpr uint64_t kPartMul = 0x9E3779B97F4A7C15ULL;   // partition_of, hashing.hpp:26-28
 
-enum SinkKind : int { SINK_MATERIALIZE = 0, SINK_BUILD = 1, SINK_PROBE = 2, SINK_PROBE_GLOBAL = 3, SINK_COUNT = 4 };
+// SINK_AGG_SCAN: global aggregate straight off the scan (no probe) - the Q6-analog local plans.
+enum SinkKind : int {
+  SINK_MATERIALIZE = 0,
+  SINK_BUILD = 1,
+  SINK_PROBE = 2,
+  SINK_PROBE_GLOBAL = 3,
+  SINK_COUNT = 4,
+  SINK_AGG_SCAN = 5
+};
 
 /// One row group (or one received/materialised run): rows + a device pointer per input column.
 struct Segment {
@@ -116,7 +124,7 @@ struct ScanProgram {
   int32_t n_sum;
   int32_t sum_reg[kMaxSums];            // probe: probe-side sums; build: build-side sums
   AggTableDev agg;
-  unsigned long long* global_acc;       // SINK_PROBE_GLOBAL: [rows, probe sums..., build sums...]
+  unsigned long long* global_acc;       // SINK_PROBE_GLOBAL: [rows, probe sums..., build sums...]; AGG_SCAN: [rows, sums...]
   int32_t global_float[2 * kMaxSums + 1];
   // Semi-join pre-filter of a partitioned probe side (MATERIALIZE with nparts > 1): nparts
   // concatenated Bloom filters, filter d over the build keys owned by rank d. A row whose key is

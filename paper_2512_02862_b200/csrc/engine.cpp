@@ -438,6 +438,8 @@ class Execution {
       : ctx_(ctx), mode_(mode), staged_(staged), plan_(QueryPlan::from_json_text(plan_json, data_root, ctx.rank, ctx.nranks)) {}
 
   ResultRows run(bool want_rows);
+  // local plans (no shuffle): scan -> replicated joins -> global aggregate (the Q6 analog)
+  ResultRows run_local();
   // staging entry: read every scan's needed chunks into HBM
   void stage(Staged& st);
 
@@ -1655,6 +1657,113 @@ ResultRows Execution::run(bool want_rows) {
   return out;
 }
 
+// ------------------------------------------------------------------------- local plans
+/// Scan -> filter -> replicated local joins -> global aggregate, with no exchange: the Q6-analog
+/// plan family. The reference's execute_plan rejects plans without a shuffled
+/// join (pipeline.cpp:334-335), so this is an extension entry (psg_execute_local); per node it
+/// returns one unmerged partial row [rows, sums...] exactly like a global aggregate of
+/// execute_plan (pipeline.cpp:277-281, 892-897).
+ResultRows Execution::run_local() {
+  const auto t0 = Clock::now();
+  launches0_ = kernel_launch_count();
+  jit0_ = jit_stats().compiles;
+  ctx_.pool.reset_peak();
+  if (plan_.memory_budget_bytes) ctx_.pool.set_budget(ctx_.pool.used() + plan_.memory_budget_bytes);
+  cudaEvent_t ev0, ev1;
+  PSG_CUDA(cudaEventCreate(&ev0));
+  PSG_CUDA(cudaEventCreate(&ev1));
+  PSG_CUDA(cudaEventRecord(ev0, ctx_.compute));
+  plan_.validate();
+  if (plan_.shuffle_join()) throw InvalidInput("local plans have no shuffled join (use execute_plan)");
+  if (!plan_.aggregate || !plan_.aggregate->group_by.empty())
+    throw InvalidInput("local plans end in a global aggregate (no group_by)");
+  // the root: the one stream no join consumes (a scan, or the last replicated join)
+  std::set<std::string> consumed;
+  for (const auto& j : plan_.joins) consumed.insert(j.build), consumed.insert(j.probe);
+  std::vector<std::string> roots;
+  for (const auto& j : plan_.joins)
+    if (!consumed.count(j.id)) roots.push_back(j.id);
+  for (const auto& sc : plan_.scans)
+    if (!sc.replicated && !consumed.count(sc.table)) roots.push_back(sc.table);
+  if (roots.size() != 1) throw InvalidInput("a local plan needs exactly one root stream");
+  psrc_ = make_source(plan_, ctx_.footers, roots[0]);
+  agg_ = true;
+  grouped_ = false;
+  result_schema_.fields.push_back(Field{"rows", LType::Int64});
+  for (const auto& c : plan_.aggregate->sums) {
+    const size_t w = psrc_.wire.require(c);
+    result_schema_.fields.push_back(Field{"sum_" + psrc_.wire.fields[w].name, psrc_.wire.fields[w].type});
+    sum_order.push_back({1, static_cast<int>(probe_sum_wire.size())});
+    probe_sum_wire.push_back(static_cast<int>(w));
+  }
+  if (probe_sum_wire.size() > static_cast<size_t>(kMaxSums)) throw InvalidInput("too many aggregate sums");
+  ResultRows out;
+  out.schema = result_schema_;
+  std::vector<int> need = probe_sum_wire;
+  if (need.empty() && psrc_.scan->predicate.empty()) need.push_back(0);  // a column to count rows over
+  RegMap pm = analyse(psrc_, need, -1, true);
+  for (size_t j = 0; j < psrc_.chain.size(); ++j) psrc_.chain[j].needed_payload = pm.payload_cols[j];
+  {  // one ingest session: the replicated scans of the chain, then the root scan
+    std::vector<std::pair<const ScanNode*, std::vector<int>>> scans;
+    for (size_t j = 0; j < psrc_.chain.size(); ++j) {
+      LocalJoinDef& lj = psrc_.chain[j];
+      SourceDef rs;
+      rs.scan = lj.scan;
+      rs.proj = lj.proj;
+      rs.wire = lj.proj.schema;
+      std::vector<ColRef> refs;
+      for (size_t i = 0; i < rs.wire.size(); ++i) refs.push_back({-1, static_cast<int>(i)});
+      rs.stage_refs.push_back(refs);
+      std::vector<int> needed{lj.key_idx};
+      for (int p : pm.payload_cols[j]) needed.push_back(lj.payload_idx[p]);
+      RegMap rm = analyse(rs, needed, -1, false);
+      scans.push_back({lj.scan, file_cols_of(rs, rm)});
+    }
+    scans.push_back({psrc_.scan, file_cols_of(psrc_, pm)});
+    const uint64_t ht_reserve = plan_.ht_estimate_bytes ? plan_.ht_estimate_bytes : plan_.memory_budget_bytes / 4;
+    session_ = std::make_unique<StreamSession>(ctx_, scans, plan_.memory_budget_bytes, ht_reserve);
+  }
+  build_local_tables();
+  for (auto& t : pl_tables_)
+    if (!t->unique) throw InvalidInput("local join build side with duplicate keys is not supported by the fused path yet");
+  global_acc_ = DevBuf(ctx_.pool, (2 * kMaxSums + 1) * 8, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(global_acc_.p, 0, (2 * kMaxSums + 1) * 8, ctx_.compute));
+  ScanProgram p = base_program(psrc_, pm, true);
+  p.sink = SINK_AGG_SCAN;
+  p.n_sum = static_cast<int>(probe_sum_wire.size());
+  for (int k = 0; k < p.n_sum; ++k) {
+    p.sum_reg[k] = pm.reg_of.at(psrc_.stage_refs.back()[probe_sum_wire[k]]);
+    p.global_float[1 + k] = psrc_.wire.fields[probe_sum_wire[k]].type == LType::Float64;
+  }
+  p.global_acc = global_acc_.as<unsigned long long>();
+  auto feed = open_feed(*psrc_.scan, file_cols_of(psrc_, pm));
+  BatchView v;
+  while (feed->next(v)) {
+    run_scan(p, v, false);
+    feed->done();
+    st_.ingest_bytes += v.bytes;
+  }
+  finalize_global(out);
+  PSG_CUDA(cudaEventRecord(ev1, ctx_.compute));
+  PSG_CUDA(cudaEventSynchronize(ev1));
+  float dms = 0;
+  PSG_CUDA(cudaEventElapsedTime(&dms, ev0, ev1));
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  st_.device_ms = dms;
+  session_->check_inflate();
+  st_.h2d_bytes = session_->h2d_bytes;
+  if (session_->ingest) st_.io_wait_s = session_->ingest->wait_s();
+  st_.jit_compiles = jit_stats().compiles - jit0_;
+  st_.result_rows = out.nrows;
+  st_.runtime_s = secs_since(t0);
+  st_.peak_bytes = ctx_.pool.peak();
+  st_.kernel_launches = kernel_launch_count() - launches0_;
+  out.stats = st_;
+  if (plan_.memory_budget_bytes) ctx_.pool.set_budget(0);
+  return out;
+}
+
 std::vector<std::pair<const ScanNode*, std::vector<int>>> Execution::scan_list(const RegMap& bm, const RegMap& pm) {
   std::vector<std::pair<const ScanNode*, std::vector<int>>> scans;
   for (int side = 0; side < 2; ++side) {
@@ -1811,6 +1920,13 @@ ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::strin
   r.stats.ingest_bytes = st->bytes;
   r.stats.h2d_bytes = st->h2d;
   return r;
+}
+
+ResultRows execute_local(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  if (mode < 0 || mode > 3) throw InvalidInput("unknown execution mode");
+  Execution ex(ctx, plan_json, data_root, mode, nullptr);
+  return ex.run_local();
 }
 
 Staged* stage_plan(Ctx& ctx, const std::string& plan_json, const std::string& data_root) {

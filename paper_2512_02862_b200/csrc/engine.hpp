@@ -226,6 +226,8 @@ struct Staged;  // HBM-resident file images (psg_stage_plan)
 ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode,
                         Staged* staged, bool want_rows);
 Staged* stage_plan(Ctx& ctx, const std::string& plan_json, const std::string& data_root);
+/// Local plans (scan -> replicated joins -> global aggregate, no shuffle; the Q6 analog).
+ResultRows execute_local(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode);
 void free_staged(Staged* s);
 
 // op adapters (ops.cpp)

@@ -153,8 +153,8 @@ std::string jit_source(const ScanProgram& P) {
   const bool mat = P.sink == SINK_MATERIALIZE || P.sink == SINK_COUNT;
   const bool probe = P.sink == SINK_PROBE || P.sink == SINK_PROBE_GLOBAL;
   const bool part = P.sink == SINK_MATERIALIZE && P.nparts > 1;
-  const bool glob = P.sink == SINK_PROBE_GLOBAL;
-  const int nglob = glob ? 1 + P.n_sum + P.agg.nbs : 0;
+  const bool glob = P.sink == SINK_PROBE_GLOBAL || P.sink == SINK_AGG_SCAN;
+  const int nglob = glob ? 1 + P.n_sum + (P.sink == SINK_PROBE_GLOBAL ? P.agg.nbs : 0) : 0;
   // Unordered compaction (pipeline-internal materialisation): each warp stages its surviving rows
   // in shared memory and flushes 128 rows at a time with one global atomic — no block barrier.
   // The order-preserving variant (tile_offsets, SINK_COUNT: the filter op) keeps the block scan.
@@ -298,7 +298,16 @@ std::string jit_source(const ScanProgram& P) {
     s << "    }\n";
   } else {
     emit_loads(s, P.n_early, P.n_in);
-    if (P.sink == SINK_BUILD) {
+    if (P.sink == SINK_AGG_SCAN) {  // Q6-analog: rows and sums of the surviving rows
+      s << "#pragma unroll\n    for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n      g0 += 1;\n";
+      for (int p = 0; p < P.n_sum; ++p) {
+        if (P.global_float[1 + p])
+          s << "      g" << 1 + p << " += __longlong_as_double(static_cast<long long>(" << V(P.sum_reg[p]) << "[r]));\n";
+        else
+          s << "      g" << 1 + p << " += " << V(P.sum_reg[p]) << "[r];\n";
+      }
+      s << "    }\n";
+    } else if (P.sink == SINK_BUILD) {
       s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R]; unsigned long long pv[R];\n"
         << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0; pv[r] = kEmptyKey; if (!(pass & (1u << r))) continue;\n"
         << "        const uint64_t key = " << V(P.key_reg) << "[r];\n"
@@ -500,7 +509,7 @@ int jit_selftest(std::string& log) {
     p.part_key_reg = -1;
     return p;
   };
-  for (int sink : {SINK_MATERIALIZE, SINK_BUILD, SINK_PROBE, SINK_PROBE_GLOBAL, SINK_COUNT}) {
+  for (int sink : {SINK_MATERIALIZE, SINK_BUILD, SINK_PROBE, SINK_PROBE_GLOBAL, SINK_COUNT, SINK_AGG_SCAN}) {
     ScanProgram p = base();
     p.sink = sink;
     p.n_sum = 2;

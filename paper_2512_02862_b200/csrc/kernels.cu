@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
 
   if (SINK == SINK_MATERIALIZE && P.nparts > 1)
     for (int i = tid; i < P.nparts; i += kBlock) s_part[i] = 0;
-  if (SINK == SINK_PROBE_GLOBAL)
+  if (SINK == SINK_PROBE_GLOBAL || SINK == SINK_AGG_SCAN)
     for (int i = tid; i < 2 * kMaxSums + 1; i += kBlock) s_gacc[i] = 0;
   auto fetch = [&](uint64_t t, const uint64_t*& col, uint64_t& r0, uint64_t& rows) {
     const uint32_t si = __ldg(tile_seg + t);
@@ -238,7 +238,20 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
         for (int r = 0; r < R; ++r)
           if (pass & (1u << r)) V(c, r) = __ldcs(reinterpret_cast<const unsigned long long*>(col + r * kBlock + tid));
       }
-      if (SINK == SINK_BUILD) {
+      if (SINK == SINK_AGG_SCAN) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          if (!(pass & (1u << r))) continue;
+          atomicAdd(&s_gacc[0], 1ULL);
+          for (int p = 0; p < P.n_sum; ++p) {
+            const uint64_t v = V(P.sum_reg[p], r);
+            if (P.global_float[1 + p])
+              atomicAdd(reinterpret_cast<double*>(&s_gacc[1 + p]), __longlong_as_double(static_cast<long long>(v)));
+            else
+              atomicAdd(&s_gacc[1 + p], static_cast<unsigned long long>(v));
+          }
+        }
+      } else if (SINK == SINK_BUILD) {
         const AggTableDev& t = P.agg;
         // Claim the home slots of all R rows first (R CASes in flight), then resolve collisions.
         uint64_t slot[R];
@@ -330,9 +343,9 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
     for (int i = tid; i < P.nparts; i += kBlock)
       if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);
   }
-  if (SINK == SINK_PROBE_GLOBAL) {
+  if (SINK == SINK_PROBE_GLOBAL || SINK == SINK_AGG_SCAN) {
     __syncthreads();
-    const int n = 1 + P.n_sum + P.agg.nbs;
+    const int n = 1 + P.n_sum + (SINK == SINK_PROBE_GLOBAL ? P.agg.nbs : 0);
     for (int i = tid; i < n; i += kBlock) {
       if (P.global_float[i])
         atomicAdd(reinterpret_cast<double*>(&P.global_acc[i]), __longlong_as_double(static_cast<long long>(s_gacc[i])));
@@ -375,6 +388,7 @@ void launch_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_
     case SINK_PROBE: launch_scan_t<4, SINK_PROBE>(P, d_segs, d_tile_seg, ntiles, st); break;
     case SINK_PROBE_GLOBAL: launch_scan_t<4, SINK_PROBE_GLOBAL>(P, d_segs, d_tile_seg, ntiles, st); break;
     case SINK_COUNT: launch_scan_t<4, SINK_COUNT>(P, d_segs, d_tile_seg, ntiles, st); break;
+    case SINK_AGG_SCAN: launch_scan_t<4, SINK_AGG_SCAN>(P, d_segs, d_tile_seg, ntiles, st); break;
   }
 }
 

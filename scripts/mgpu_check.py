@@ -98,6 +98,28 @@ def main():
                         flush=True)
                     if not ok:
                         failures.append((pname, mode, fused, semijoin, got, want))
+    # local plans (no shuffle, psg_execute_local): one partial row per rank = per node
+    local = json.load(open(os.path.join(ROOT, "tests", "golden", "local.json")))
+    for pname in ("q6", "q6_count"):
+        d = data(0.1, 42, 1 << 20)
+        res = ctx.execute_local(local["plans"][pname], d)
+        allres = [None] * world
+        dist.all_gather_object(allres, (res.schema, res.rows.copy()))
+        if rank == 0:
+            g = [r for r in local["results"] if r["plan"] == pname and r["nodes"] == world and r["scale"] == 0.1
+                 and r["seed"] == 42 and r["codec"] == "identity"]
+            if g:
+                want = [(x["rows"], x["colsums"] if x["rows"] else []) for x in g[0]["per_node"]]
+                src = "reference"
+            else:
+                want = [(s["rows"], s["colsums"]) for s in
+                        (po.summary([x]) for x in po.execute_local(json.dumps(local["plans"][pname]), d, world))]
+                src = "oracle"
+            got = [(s["rows"], s["colsums"]) for s in (po.summary([x]) for x in allres)]
+            ok = got == want
+            print("%-22s local      %-9s %s per_node=%s" % (pname, src, "OK " if ok else "BAD", got), flush=True)
+            if not ok:
+                failures.append((pname, "local", got, want))
     if rank == 0:
         print("FAILURES", len(failures))
         for f in failures:

@@ -80,3 +80,24 @@ def test_partition_of_matches_reference_hash():
             got = po.partition_of(keys.view(np.uint64), n)
             want = [(((int(k) % 2**64) * 0x9E3779B97F4A7C15 % 2**64) >> 13) % n for k in keys]
             assert list(got) == want
+
+
+def test_oracle_local_plans_match_reference_scan(tmp_path):
+    """plan_oracle.execute_local (the Q6-analog restatement) against the reference's own
+    read_blocking + predicate + sums (tests/golden/local.json), per node."""
+    import json as _json
+    local = _json.load(open(os.path.join(os.path.dirname(__file__), "golden", "local.json")))
+    n = 0
+    for r in local["results"]:
+        if r["scale"] > 0.1:
+            continue
+        d = str(tmp_path / r["case"])
+        oracle.gen_tpch(d, r["scale"], r["nodes"], r["nodes"], r["seed"], r["codec"])
+        got = po.execute_local(_json.dumps(local["plans"][r["plan"]]), d, r["nodes"])
+        for k, want in enumerate(r["per_node"]):
+            s = po.summary([got[k]])
+            assert s["rows"] == want["rows"], (r["case"], k)
+            if want["rows"]:
+                assert s["colsums"] == want["colsums"] and s["rowhash"] == want["rowhash"], (r["case"], k)
+        n += 1
+    assert n >= 6
