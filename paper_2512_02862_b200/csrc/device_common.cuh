@@ -88,6 +88,7 @@ struct AggTableDev {
   int32_t bs_float[kMaxSums];
   int32_t shift;        // 64 - log2(cap)
   int32_t bloom_shift;  // 64 - log2(bloom words)
+  unsigned int* dups;   // set to 1 when a build key repeats (nullptr: unknown, assume repeats)
 };
 
 /// One rank's aggregation-table arrays as mapped into this process (CUDA IPC symmetric heap).
@@ -133,6 +134,11 @@ struct ScanProgram {
   uint64_t semi_words;
   int32_t semi_shift;
   int32_t semi_key_reg;
+  // MATERIALIZE with nparts > 1: rows this rank owns (part_of(key) == self_rank) are probed and
+  // aggregated into `agg` in place (grouped aggregate, key_reg / n_sum / sum_reg) and never
+  // materialised or shuffled - only rows owned by other ranks leave the kernel.
+  int32_t self_probe;
+  int32_t self_rank;
   // Fused NVLink path (SINK_BUILD / SINK_PROBE with remote = 1): every row's table operation goes
   // to the owner rank part_of(key) directly in its (peer-mapped) table; tables are symmetric so
   // mask/shift/hw/cw come from `agg`, only the base pointers differ per rank.
@@ -260,6 +266,7 @@ __device__ __forceinline__ uint64_t agg_mult(const AggTableDev& t, uint64_t slot
 __device__ __forceinline__ void agg_count_build(const AggTableDev& t, uint64_t key, uint64_t slot, bool dup) {
   if (slot == t.mask + 1 || dup) {
     atomicAdd(reinterpret_cast<unsigned long long*>(t.cold + slot * t.cw), 1ULL);
+    if (dup && t.dups != nullptr) *t.dups = 1u;
   } else if (t.bloom != nullptr) {
     const uint64_t h2 = key * kBloomMul;
     atomicOr(t.bloom + (h2 >> t.bloom_shift), bloom_bits(h2, t.bloom_shift));

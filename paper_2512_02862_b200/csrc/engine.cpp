@@ -500,7 +500,7 @@ class Execution {
   };
   std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
   // agg table
-  DevBuf agg_hot_, agg_cold_, agg_bloom_, global_acc_, barrier_word_;
+  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, global_acc_, barrier_word_;
   AggTableDev aggt_{};
   uint64_t agg_cap_ = 0;
   // stats
@@ -1015,6 +1015,9 @@ void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words) {
   aggt_.nbs = nbs;
   for (int i = 0; i < nps; ++i) aggt_.ps_float[i] = psrc_.wire.fields[probe_sum_wire[i]].type == LType::Float64;
   for (int i = 0; i < nbs; ++i) aggt_.bs_float[i] = bsrc_.wire.fields[build_sum_wire[i]].type == LType::Float64;
+  agg_dups_ = DevBuf(ctx_.pool, 4, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(agg_dups_.p, 0, 4, ctx_.compute));
+  aggt_.dups = agg_dups_.as<unsigned int>();
   if (bloom_words) {
     agg_bloom_ = DevBuf(ctx_.pool, bloom_words * 4, ctx_.compute);
     aggt_.bloom = agg_bloom_.as<uint32_t>();
@@ -1124,27 +1127,20 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
 }
 
 // ---------------------------------------------------------------------------- finalize
+/// Result rows in signed key order (HashAggregator's std::map order, pipeline.cpp:296-305).
+/// Dense keys (range <= 256 x groups, e.g. order keys): the output position of a group is its
+/// key's rank in a bitmap of present keys, so one sequential table pass writes every row in
+/// place (no sort, no gather). Sparse keys: compact -> radix sort of the varying key bits -> emit.
 void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
   const uint64_t nslots = agg_cap_ + 1;
-  DevBuf keys(ctx_.pool, nslots * 8, ctx_.compute), slots(ctx_.pool, nslots * 8, ctx_.compute);
   DevBuf counter(ctx_.pool, 24, ctx_.compute);
   const uint64_t init[3] = {0, ~0ULL, 0};
   PSG_CUDA(cudaMemcpyAsync(counter.p, init, 24, cudaMemcpyHostToDevice, ctx_.compute));
-  launch_agg_compact(aggt_, agg_cap_, keys.as<uint64_t>(), slots.as<unsigned long long>(),
-                     counter.as<unsigned long long>(), ctx_.compute);
+  launch_agg_range(aggt_, agg_cap_, counter.as<unsigned long long>(), ctx_.compute);
   uint64_t cnt[3] = {0, 0, 0};
   PSG_CUDA(cudaMemcpyAsync(cnt, counter.p, 24, cudaMemcpyDeviceToHost, ctx_.compute));
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   const uint64_t ng = cnt[0];
-  // radix-sort only the key bits that vary: every key lies in [min, max] and shares their prefix
-  int end_bit = 1;
-  if (ng > 1 && cnt[1] != cnt[2]) end_bit = 64 - __builtin_clzll(cnt[1] ^ cnt[2]);
-  DevBuf k2(ctx_.pool, std::max<uint64_t>(ng, 1) * 8, ctx_.compute), s2(ctx_.pool, std::max<uint64_t>(ng, 1) * 8, ctx_.compute);
-  size_t tb = sort_pairs_i64(nullptr, nullptr, nullptr, nullptr, ng, end_bit, nullptr, 0, ctx_.compute);
-  DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
-  if (ng)
-    sort_pairs_i64(keys.as<uint64_t>(), k2.as<uint64_t>(), slots.as<unsigned long long>(), s2.as<unsigned long long>(), ng,
-                   end_bit, tmp.p, tb, ctx_.compute);
   const int nc = static_cast<int>(result_schema_.size());
   std::vector<int32_t> kind, idx;
   kind.push_back(0), idx.push_back(0);
@@ -1154,8 +1150,39 @@ void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
     idx.push_back(k);
   }
   DevBuf rows(ctx_.pool, std::max<uint64_t>(ng, 1) * nc * 8, ctx_.compute);
-  launch_agg_emit(aggt_, k2.as<uint64_t>(), s2.as<unsigned long long>(), ng, nc, kind.data(), idx.data(), rows.as<uint64_t>(),
-                  ctx_.compute);
+  const uint64_t span = ng ? cnt[2] - cnt[1] : 0;  // flipped-key range - 1
+  static const bool dense_env = [] {
+    const char* e = std::getenv("PSG_DENSE_EMIT");
+    return !(e && std::string(e) == "0");
+  }();
+  if (ng && dense_env && span < (1ULL << 36) && span / 64 + 1 <= 4 * ng) {
+    const uint64_t words = span / 64 + 1;
+    DevBuf bitmap(ctx_.pool, words * 8, ctx_.compute), pc(ctx_.pool, words * 4, ctx_.compute),
+        prefix(ctx_.pool, words * 4, ctx_.compute);
+    PSG_CUDA(cudaMemsetAsync(bitmap.p, 0, words * 8, ctx_.compute));
+    launch_agg_mark(aggt_, agg_cap_, cnt[1], bitmap.as<unsigned long long>(), ctx_.compute);
+    launch_popc64(bitmap.as<unsigned long long>(), words, pc.as<uint32_t>(), ctx_.compute);
+    const size_t tb = exclusive_scan_u32(nullptr, nullptr, words, nullptr, 0, ctx_.compute);
+    DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
+    exclusive_scan_u32(pc.as<uint32_t>(), prefix.as<uint32_t>(), words, tmp.p, tb, ctx_.compute);
+    launch_agg_emit_dense(aggt_, agg_cap_, cnt[1], bitmap.as<unsigned long long>(), prefix.as<uint32_t>(), nc,
+                          kind.data(), idx.data(), rows.as<uint64_t>(), ctx_.compute);
+  } else if (ng) {
+    DevBuf keys(ctx_.pool, nslots * 8, ctx_.compute), slots(ctx_.pool, nslots * 8, ctx_.compute);
+    PSG_CUDA(cudaMemcpyAsync(counter.p, init, 24, cudaMemcpyHostToDevice, ctx_.compute));
+    launch_agg_compact(aggt_, agg_cap_, keys.as<uint64_t>(), slots.as<unsigned long long>(),
+                       counter.as<unsigned long long>(), ctx_.compute);
+    // radix-sort only the key bits that vary: every key lies in [min, max] and shares their prefix
+    int end_bit = 1;
+    if (ng > 1 && cnt[1] != cnt[2]) end_bit = 64 - __builtin_clzll(cnt[1] ^ cnt[2]);
+    DevBuf k2(ctx_.pool, ng * 8, ctx_.compute), s2(ctx_.pool, ng * 8, ctx_.compute);
+    size_t tb = sort_pairs_i64(nullptr, nullptr, nullptr, nullptr, ng, end_bit, nullptr, 0, ctx_.compute);
+    DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
+    sort_pairs_i64(keys.as<uint64_t>(), k2.as<uint64_t>(), slots.as<unsigned long long>(), s2.as<unsigned long long>(), ng,
+                   end_bit, tmp.p, tb, ctx_.compute);
+    launch_agg_emit(aggt_, k2.as<uint64_t>(), s2.as<unsigned long long>(), ng, nc, kind.data(), idx.data(),
+                    rows.as<uint64_t>(), ctx_.compute);
+  }
   out.nrows = ng;
   if (want_rows) {
     uint64_t* dst = out.mutable_rows(ng * nc);
@@ -1559,6 +1586,22 @@ ResultRows Execution::run(bool want_rows) {
       PSG_NCCL(ncclAllReduce(wv.p, wv.p, 1, ncclUint64, ncclMax, ctx_.nccl, ctx_.compute));
       PSG_CUDA(cudaMemcpyAsync(&waves, wv.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    }
+    // Rows this rank owns are probed and aggregated in place by the partitioning scan itself:
+    // only rows owned by other ranks are materialised and shuffled (1/N of the traffic and of
+    // the consume work disappears). PSG_SELF_PROBE=0 turns it off (A/B measurements).
+    static const bool self_probe_env = [] {
+      const char* e = std::getenv("PSG_SELF_PROBE");
+      return !(e && std::string(e) == "0");
+    }();
+    if (nr > 1 && agg_ && grouped_ && jit_available() && self_probe_env) {
+      pp.self_probe = 1;
+      pp.self_rank = ctx_.rank;
+      pp.agg = aggt_;
+      pp.agg.bloom = nullptr;  // the semi-join screen already tested the owner's (= our) filter
+      pp.key_reg = p_out[0];
+      pp.n_sum = static_cast<int>(probe_sum_wire.size());
+      for (int k = 0; k < pp.n_sum; ++k) pp.sum_reg[k] = p_out[1 + k];
     }
     for (uint64_t w = 0; w < waves; ++w) {
       BatchView v;

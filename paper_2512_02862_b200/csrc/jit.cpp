@@ -336,6 +336,32 @@ std::string jit_source(const ScanProgram& P) {
           << "          bm[r] = bloom_bits(h2, P.semi_shift); bw[r] = ldg_keep_u32(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift), pol_keep); } }\n"
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n    }\n";
       }
+      if (P.sink == SINK_MATERIALIZE && P.self_probe && P.nparts > 1) {
+        // rows owned by this rank: probe + aggregate in place (two-stage lookup), drop from the shuffle
+        s << "    { const AggTableDev& T = P.agg; uint32_t own = 0; uint64_t sl[R], k0[R];\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && part_of(" << V(P.part_key_reg)
+          << "[r], static_cast<uint32_t>(P.nparts)) == static_cast<uint32_t>(P.self_rank)) own |= 1u << r;\n"
+          << "      pass &= ~own;\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = ~0ULL; k0[r] = 0; if (own & (1u << r)) {\n"
+          << "        const uint64_t key = " << V(P.key_reg) << "[r];\n"
+          << "        if (key == kEmptyKey) { if (T.cold[(T.mask + 1) * T.cw] == 0) own &= ~(1u << r); else sl[r] = T.mask + 1; }\n"
+          << "        else { sl[r] = slot_of(key, T.shift); k0[r] = T.hot[sl[r] * " << P.agg.hw << "]; } } }\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(own & (1u << r)) || sl[r] == T.mask + 1) continue;\n"
+          << "        const uint64_t key = " << V(P.key_reg) << "[r]; uint64_t sx = sl[r], kk = k0[r];\n"
+          << "        while (kk != key && kk != kEmptyKey) { sx = (sx + 1) & T.mask; kk = T.hot[sx * " << P.agg.hw << "]; }\n"
+          << "        if (kk != key) own &= ~(1u << r); else sl[r] = sx; }\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(own & (1u << r))) continue;\n"
+          << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n"
+          << "        atomicAdd(h + 1, 1ULL);\n";
+        for (int p = 0; p < P.n_sum; ++p) {
+          if (P.agg.ps_float[p])
+            s << "        atomicAdd(reinterpret_cast<double*>(h + " << 2 + p << "), __longlong_as_double(static_cast<long long>("
+              << V(P.sum_reg[p]) << "[r])));\n";
+          else
+            s << "        atomicAdd(h + " << 2 + p << ", static_cast<unsigned long long>(" << V(P.sum_reg[p]) << "[r]));\n";
+        }
+        s << "      }\n    }\n";
+      }
       if (wstage) {
         s << "    { const uint32_t lt = (1u << lane) - 1u;\n"
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
@@ -486,6 +512,7 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
     }
   }
   if (P.remote) throw Error(PSG_ERR_INTERNAL, "the fused NVLink path needs the query compiler (PSG_JIT)");
+  if (P.self_probe) throw Error(PSG_ERR_INTERNAL, "the in-place owner probe needs the query compiler (PSG_JIT)");
   launch_scan(P, d_segs, d_tile_seg, nsegs, ntiles, stream);
 }
 
@@ -532,6 +559,12 @@ int jit_selftest(std::string& log) {
       p.semi_key_reg = 1;
     }
     progs.push_back(p);
+    if (sink == SINK_MATERIALIZE) {  // + in-place probe of the rows this rank owns
+      p.self_probe = 1;
+      p.self_rank = 2;
+      p.key_reg = 1;
+      progs.push_back(p);
+    }
   }
   {
     ScanProgram p = base();  // orders-like: filter, local join with payload, materialise

@@ -740,6 +740,50 @@ void launch_agg_compact(const AggTableDev& t, uint64_t cap, uint64_t* out_keys, 
   k_agg_compact<<<static_cast<unsigned>(blocks), 256, 0, S(stream)>>>(t, cap + 1, out_keys, out_slots, counter);
 }
 
+// ---- dense finalisation: when the group keys span a range R not much larger than the group
+// count, the output position of a group is its key's rank in a bitmap of present keys
+// (prefix popcount), so rows are written straight from a sequential table pass - no sort, no
+// gather through a sorted slot list.
+__global__ void __launch_bounds__(256) k_agg_range(AggTableDev t, uint64_t nslots, unsigned long long* counter) {
+  unsigned long long lo = ~0ULL, hi = 0, n = 0;
+  for (uint64_t s = blockIdx.x * 256ULL + threadIdx.x; s < nslots; s += gridDim.x * 256ULL) {
+    const ulonglong2 kh = *reinterpret_cast<const ulonglong2*>(t.hot + s * t.hw);
+    const bool occupied = (s == nslots - 1) ? (t.cold[s * t.cw] > 0) : (kh.x != kEmptyKey);
+    if (occupied && kh.y > 0) {
+      const unsigned long long fk = kh.x ^ 0x8000000000000000ULL;
+      lo = min(lo, fk);
+      hi = max(hi, fk);
+      ++n;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    n += __shfl_xor_sync(0xffffffffu, n, o);
+  }
+  if ((threadIdx.x & 31) == 0 && n) {
+    atomicAdd(counter, n);
+    atomicMin(counter + 1, lo);
+    atomicMax(counter + 2, hi);
+  }
+}
+__global__ void __launch_bounds__(256) k_agg_mark(AggTableDev t, uint64_t nslots, unsigned long long fmin,
+                                                  unsigned long long* bitmap) {
+  for (uint64_t s = blockIdx.x * 256ULL + threadIdx.x; s < nslots; s += gridDim.x * 256ULL) {
+    const ulonglong2 kh = *reinterpret_cast<const ulonglong2*>(t.hot + s * t.hw);
+    const bool occupied = (s == nslots - 1) ? (t.cold[s * t.cw] > 0) : (kh.x != kEmptyKey);
+    if (occupied && kh.y > 0) {
+      const uint64_t b = (kh.x ^ 0x8000000000000000ULL) - fmin;
+      atomicOr(bitmap + (b >> 6), 1ULL << (b & 63));
+    }
+  }
+}
+__global__ void k_popc64(const unsigned long long* bitmap, uint64_t nwords, uint32_t* out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nwords;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    out[i] = __popcll(bitmap[i]);
+}
+
 struct EmitCols {
   int32_t kind[2 * kMaxSums + 2];
   int32_t idx[2 * kMaxSums + 2];
@@ -751,7 +795,7 @@ __global__ void k_agg_emit(AggTableDev t, const uint64_t* keys, const unsigned l
     const uint64_t s = slots[i];
     const uint64_t* h = t.hot + s * t.hw;
     const uint64_t* c = t.cold + s * t.cw;
-    const uint64_t hits = h[1], m = agg_mult(t, s);
+    const uint64_t hits = h[1], m = (t.dups == nullptr || *t.dups != 0 || s == t.mask + 1) ? agg_mult(t, s) : 1;
     uint64_t* row = out + i * nc;
     for (int k = 0; k < nc; ++k) {
       const int kind = ec.kind[k], j = ec.idx[k];
@@ -773,6 +817,69 @@ __global__ void k_agg_emit(AggTableDev t, const uint64_t* keys, const unsigned l
     }
   }
 }
+/// Dense emit: one pass over the table; row of the group with flipped key fk goes to
+/// prefix[w] + popc(bitmap[w] & below) with w, b = (fk - fmin) / 64, % 64.
+__global__ void __launch_bounds__(256) k_agg_emit_dense(AggTableDev t, uint64_t nslots, unsigned long long fmin,
+                                                        const unsigned long long* bitmap, const uint32_t* prefix, int nc,
+                                                        EmitCols ec, uint64_t* out) {
+  const bool dups = t.dups == nullptr || *t.dups != 0;
+  for (uint64_t s = blockIdx.x * 256ULL + threadIdx.x; s < nslots; s += gridDim.x * 256ULL) {
+    const uint64_t* h = t.hot + s * t.hw;
+    const ulonglong2 kh = *reinterpret_cast<const ulonglong2*>(h);
+    const bool spill = s == nslots - 1;
+    const bool occupied = spill ? (t.cold[s * t.cw] > 0) : (kh.x != kEmptyKey);
+    if (!occupied || kh.y == 0) continue;
+    const uint64_t b = (kh.x ^ 0x8000000000000000ULL) - fmin;
+    const uint64_t w = b >> 6;
+    const uint64_t pos = prefix[w] + __popcll(bitmap[w] & ((1ULL << (b & 63)) - 1ULL));
+    const uint64_t* c = t.cold + s * t.cw;
+    const uint64_t hits = kh.y, m = (spill || dups) ? agg_mult(t, s) : 1;
+    uint64_t* row = out + pos * nc;
+    for (int k = 0; k < nc; ++k) {
+      const int kind = ec.kind[k], j = ec.idx[k];
+      uint64_t v;
+      if (kind == 0) {
+        v = kh.x;
+      } else if (kind == 1) {
+        v = hits * m;
+      } else if (kind == 2) {
+        v = t.ps_float[j] ? static_cast<uint64_t>(__double_as_longlong(
+                                static_cast<double>(m) * __longlong_as_double(static_cast<long long>(h[2 + j]))))
+                          : m * h[2 + j];
+      } else {
+        v = t.bs_float[j] ? static_cast<uint64_t>(__double_as_longlong(
+                                static_cast<double>(hits) * __longlong_as_double(static_cast<long long>(c[1 + j]))))
+                          : hits * c[1 + j];
+      }
+      row[k] = v;
+    }
+  }
+}
+
+void launch_agg_range(const AggTableDev& t, uint64_t cap, unsigned long long* counter, void* stream) {
+  count_launch();
+  k_agg_range<<<sm_count() * 8, 256, 0, S(stream)>>>(t, cap + 1, counter);
+}
+void launch_agg_mark(const AggTableDev& t, uint64_t cap, uint64_t fmin, unsigned long long* bitmap, void* stream) {
+  count_launch();
+  k_agg_mark<<<sm_count() * 8, 256, 0, S(stream)>>>(t, cap + 1, fmin, bitmap);
+}
+void launch_popc64(const unsigned long long* bitmap, uint64_t nwords, uint32_t* out, void* stream) {
+  count_launch();
+  k_popc64<<<grid_for(nwords, 256), 256, 0, S(stream)>>>(bitmap, nwords, out);
+}
+void launch_agg_emit_dense(const AggTableDev& t, uint64_t cap, uint64_t fmin, const unsigned long long* bitmap,
+                           const uint32_t* prefix, int nc, const int32_t* col_kind, const int32_t* col_idx,
+                           uint64_t* out_rows, void* stream) {
+  EmitCols ec{};
+  for (int k = 0; k < nc; ++k) {
+    ec.kind[k] = col_kind[k];
+    ec.idx[k] = col_idx[k];
+  }
+  count_launch();
+  k_agg_emit_dense<<<sm_count() * 8, 256, 0, S(stream)>>>(t, cap + 1, fmin, bitmap, prefix, nc, ec, out_rows);
+}
+
 void launch_agg_emit(const AggTableDev& t, const uint64_t* sorted_keys, const unsigned long long* sorted_slots,
                      uint64_t n, int nc, const int32_t* col_kind, const int32_t* col_idx, uint64_t* out_rows,
                      void* stream) {

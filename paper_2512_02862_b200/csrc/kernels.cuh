@@ -61,6 +61,13 @@ void launch_agg_compact(const AggTableDev& t, uint64_t cap, uint64_t* out_keys, 
 void launch_agg_emit(const AggTableDev& t, const uint64_t* sorted_keys, const unsigned long long* sorted_slots,
                      uint64_t n, int ncols_out, const int32_t* col_kind, const int32_t* col_idx, uint64_t* out_rows,
                      void* stream);
+// Dense finalisation (no sort): range + group count, key bitmap, popcounts, direct emit.
+void launch_agg_range(const AggTableDev& t, uint64_t cap, unsigned long long* counter, void* stream);
+void launch_agg_mark(const AggTableDev& t, uint64_t cap, uint64_t fmin, unsigned long long* bitmap, void* stream);
+void launch_popc64(const unsigned long long* bitmap, uint64_t nwords, uint32_t* out, void* stream);
+void launch_agg_emit_dense(const AggTableDev& t, uint64_t cap, uint64_t fmin, const unsigned long long* bitmap,
+                           const uint32_t* prefix, int nc, const int32_t* col_kind, const int32_t* col_idx,
+                           uint64_t* out_rows, void* stream);
 size_t sort_pairs_i64(const uint64_t* keys_in, uint64_t* keys_out, const unsigned long long* v_in,
                       unsigned long long* v_out, uint64_t n, int end_bit, void* tmp, size_t tmp_bytes, void* stream);
 size_t sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* v_in, uint32_t* v_out, uint64_t n,
