@@ -835,7 +835,10 @@ __global__ void __launch_bounds__(256) k_agg_emit_dense(AggTableDev t, uint64_t 
     const uint64_t* c = t.cold + s * t.cw;
     const uint64_t hits = kh.y, m = (spill || dups) ? agg_mult(t, s) : 1;
     uint64_t* row = out + pos * nc;
-    for (int k = 0; k < nc; ++k) {
+    uint64_t vals[2 * kMaxSums + 2];
+#pragma unroll
+    for (int k = 0; k < 2 * kMaxSums + 2; ++k) {
+      if (k >= nc) break;
       const int kind = ec.kind[k], j = ec.idx[k];
       uint64_t v;
       if (kind == 0) {
@@ -851,7 +854,22 @@ __global__ void __launch_bounds__(256) k_agg_emit_dense(AggTableDev t, uint64_t 
                                 static_cast<double>(hits) * __longlong_as_double(static_cast<long long>(c[1 + j]))))
                           : hits * c[1 + j];
       }
-      row[k] = v;
+      vals[k] = v;
+    }
+    // rows land at random positions: whole 16-byte stores (a 4-word row = one 32-byte sector
+    // in two transactions instead of four partial-sector ones)
+    if ((nc & 1) == 0) {
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxSums + 2; k += 2) {
+        if (k >= nc) break;
+        *reinterpret_cast<ulonglong2*>(row + k) = make_ulonglong2(vals[k], vals[k + 1]);
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxSums + 2; ++k) {
+        if (k >= nc) break;
+        row[k] = vals[k];
+      }
     }
   }
 }
