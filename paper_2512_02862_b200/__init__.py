@@ -375,12 +375,12 @@ def inspect(path):
             "schema": _footer_schema(path)}
 
 
-def gen_workload(kind, out_dir, devices=2, nodes=2, scale=0.01, seed=42, codec="identity", row_group_bytes=1 << 20,
+def gen_workload(kind, out_dir, devices=2, nodes=2, scale=0.01, seed=42, codec="block", row_group_bytes=1 << 20,
                  threads=3):
     """gen_workload(kind='tpch') (bench.cpp:85-114), byte-identical to the reference generator.
 
-    The reference's default codec is the zlib block codec; the GPU scan path reads the identity
-    codec, which is what this defaults to (pass codec='block' for reference-default files)."""
+    Defaults mirror the reference's (bindings.cpp:180-193 + GenWorkloadSpec, bench.hpp:51): the zlib
+    block codec, whose chunks the GPU inflates in HBM; codec='identity' writes raw column chunks."""
     if kind not in ("tpch", "tpch-analog"):
         raise PsgError(9, "only the tpch-analog workload is generated by this build")
     _check(lib().psg_gen_tpch(out_dir.encode(), float(scale), int(nodes), int(devices), int(seed),

@@ -13,6 +13,10 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <tuple>
+
+#include <fstream>
+#include <json.hpp>
 
 #include "psto.hpp"
 
@@ -188,11 +192,15 @@ void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, 
   if (nodes < 1 || devices < 1) throw InvalidInput("devices and nodes must be >= 1");
   namespace fs = std::filesystem;
   fs::create_directories(out_dir);
-  auto dev_dir = [&](int i) {
-    std::string d = out_dir + "/dev" + std::to_string(i % devices);
+  auto dev_dir = [&](int i) {  // device_dir, bench.cpp:44-46
+    std::string d = (fs::path(out_dir) / ("dev" + std::to_string(i % devices))).string();
     fs::create_directories(d);
     return d;
   };
+  const std::string cust_path = dev_dir(0) + "/customer.psto";
+  std::vector<std::string> opaths, lpaths;
+  for (int n = 0; n < nodes; ++n) opaths.push_back(dev_dir(0 + n) + "/orders.node" + std::to_string(n) + ".psto");
+  for (int n = 0; n < nodes; ++n) lpaths.push_back(dev_dir(1 + n) + "/lineitem.node" + std::to_string(n) + ".psto");
   const uint64_t customers = static_cast<uint64_t>(150'000 * scale);
   const uint64_t orders = static_cast<uint64_t>(1'500'000 * scale);
   const uint64_t lineitems = static_cast<uint64_t>(6'000'000 * scale);
@@ -205,11 +213,10 @@ void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, 
                    v[0] = i;
                    v[1] = r() % 5;
                  },
-                 {dev_dir(0) + "/customer.psto"}, rg_bytes, codec);
+                 {cust_path}, rg_bytes, codec);
   });
   jobs.push_back([&] {
-    std::vector<std::string> paths;
-    for (int n = 0; n < nodes; ++n) paths.push_back(dev_dir(0 + n) + "/orders.node" + std::to_string(n) + ".psto");
+    const std::vector<std::string>& paths = opaths;
     stream_table(int_schema({"o_orderkey", "o_custkey", "o_orderdate", "o_shippriority"}), orders, seed * mult + 12,
                  [customers](Mt64& r, uint64_t i, uint64_t* v) {
                    v[0] = i;
@@ -220,8 +227,7 @@ void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, 
                  paths, rg_bytes, codec);
   });
   jobs.push_back([&] {
-    std::vector<std::string> paths;
-    for (int n = 0; n < nodes; ++n) paths.push_back(dev_dir(1 + n) + "/lineitem.node" + std::to_string(n) + ".psto");
+    const std::vector<std::string>& paths = lpaths;
     stream_table(int_schema({"l_orderkey", "l_extendedprice", "l_discount", "l_shipdate"}), lineitems,
                  seed * mult + 13,
                  [orders](Mt64& r, uint64_t, uint64_t* v) {
@@ -234,21 +240,40 @@ void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, 
   });
   if (threads <= 1) {
     for (auto& j : jobs) j();
-    return;
+  } else {
+    std::vector<std::thread> ts;
+    std::vector<std::exception_ptr> errs(jobs.size());
+    for (size_t i = 0; i < jobs.size(); ++i)
+      ts.emplace_back([&, i] {
+        try {
+          jobs[i]();
+        } catch (...) {
+          errs[i] = std::current_exception();
+        }
+      });
+    for (auto& t : ts) t.join();
+    for (auto& e : errs)
+      if (e) std::rethrow_exception(e);
   }
-  std::vector<std::thread> ts;
-  std::vector<std::exception_ptr> errs(jobs.size());
-  for (size_t i = 0; i < jobs.size(); ++i)
-    ts.emplace_back([&, i] {
-      try {
-        jobs[i]();
-      } catch (...) {
-        errs[i] = std::current_exception();
-      }
-    });
-  for (auto& t : ts) t.join();
-  for (auto& e : errs)
-    if (e) std::rethrow_exception(e);
+  // manifest.json with the reference's keys and layout (gen_workload, bench.cpp:85-114)
+  nlohmann::json m;
+  m["nodes"] = nodes;
+  m["devices"] = devices;
+  m["seed"] = seed;
+  m["kind"] = "tpch-analog";
+  m["scale"] = scale;
+  m["tables"]["customer"]["replicated"] = true;
+  m["tables"]["customer"]["rows"] = customers;
+  m["tables"]["customer"]["path"] = cust_path;
+  for (auto [name, rows, paths] : {std::make_tuple("orders", orders, &opaths), std::make_tuple("lineitem", lineitems, &lpaths)}) {
+    m["tables"][name]["replicated"] = false;
+    m["tables"][name]["rows"] = rows;
+    m["tables"][name]["paths_per_node"] = *paths;
+  }
+  const std::string mpath = (fs::path(out_dir) / "manifest.json").string();
+  std::ofstream out(mpath);
+  if (!out) throw IoFailure("cannot write manifest: " + mpath);
+  out << m.dump(2) << '\n';
 }
 
 }  // namespace psg

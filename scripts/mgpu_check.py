@@ -49,7 +49,7 @@ def main():
             d = os.path.join(base, "d%d" % len(datasets))
             if rank == 0:
                 psg.gen_workload("tpch", d, devices=devices or world, nodes=world, scale=scale, seed=seed,
-                                 row_group_bytes=rg)
+                                 row_group_bytes=rg, codec="identity")
             dist.barrier()
             datasets[key] = d
         return datasets[key]

@@ -40,7 +40,7 @@ def main():
     # ---- SF1
     d1 = os.path.join(a.data_dir, "sf1_n1")
     if not os.path.exists(os.path.join(d1, "DONE")):
-        psg.gen_workload("tpch", d1, devices=1, nodes=1, scale=1.0, seed=42)
+        psg.gen_workload("tpch", d1, devices=1, nodes=1, scale=1.0, seed=42, codec="identity")
         open(os.path.join(d1, "DONE"), "w").write("ok")
     p1 = plan(["{data}/dev0/lineitem.node0.psto"])
     ctx.execute_local(p1, d1)

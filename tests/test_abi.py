@@ -40,6 +40,8 @@ def test_product_generator_matches_reference_bytes(idx, gen_hashes, tmp_path):
     got = {}
     for root, _dirs, files in os.walk(d):
         for f in files:
+            if not f.endswith(".psto"):  # the manifest names absolute paths (checked separately)
+                continue
             p = os.path.join(root, f)
             got[os.path.relpath(p, d)] = hashlib.sha256(open(p, "rb").read()).hexdigest()
     assert got == spec["files"]
@@ -87,3 +89,23 @@ def test_query_compiler_builds_every_sink_for_sm100a():
     """NVRTC specialisation of the fused scan (jit.cpp) compiles for sm_100a without a GPU."""
     failures, log = psg.jit_selftest()
     assert failures == 0, log
+
+
+def test_gen_workload_defaults_and_manifest_match_reference(tmp_path):
+    """gen_workload mirrors the reference's defaults (block codec, 1 MiB row groups,
+    bench.hpp:42-52) and writes the same manifest.json (bench.cpp:85-114)."""
+    import json as _json
+    import subprocess
+    d = str(tmp_path / "ours")
+    mpath = psg.gen_workload("tpch", d, devices=2, nodes=3, scale=0.002, seed=7)
+    m = _json.load(open(mpath))
+    assert m["kind"] == "tpch-analog" and m["nodes"] == 3 and m["devices"] == 2 and m["seed"] == 7
+    assert m["tables"]["customer"]["replicated"] and len(m["tables"]["lineitem"]["paths_per_node"]) == 3
+    assert psg.inspect(m["tables"]["lineitem"]["paths_per_node"][0])["codec"] == "block"
+    drv = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
+    if os.path.exists(drv):
+        r = str(tmp_path / "ref")
+        subprocess.run([drv, "gen", "--out", r, "--scale", "0.002", "--nodes", "3", "--devices", "2", "--seed", "7",
+                        "--codec", "block"], check=True, capture_output=True)
+        ref = open(os.path.join(r, "manifest.json")).read().replace(r, "ROOT")
+        assert open(mpath).read().replace(d, "ROOT") == ref

@@ -81,7 +81,7 @@ def test_inflate_matches_zlib_all_block_types(ctx):
 def test_inflate_psto_chunks_one_batch(ctx, tmp_path):
     """Every chunk of a block-coded PSTO file, inflated in one launch, equals the identity file."""
     psg.gen_workload("tpch", str(tmp_path / "b"), devices=1, nodes=1, scale=0.02, seed=3, codec="block")
-    psg.gen_workload("tpch", str(tmp_path / "i"), devices=1, nodes=1, scale=0.02, seed=3)
+    psg.gen_workload("tpch", str(tmp_path / "i"), devices=1, nodes=1, scale=0.02, seed=3, codec="identity")
     for t in ("lineitem.node0", "orders.node0", "customer"):
         b = psg.scan(str(tmp_path / "b" / "dev0" / (t + ".psto")), ctx=ctx)
         i = psg.scan(str(tmp_path / "i" / "dev0" / (t + ".psto")), ctx=ctx)

@@ -62,7 +62,7 @@ def random_plan(rng):
 @pytest.fixture(scope="module")
 def data(tmp_path_factory):
     d = str(tmp_path_factory.mktemp("fz") / "d")
-    psg.gen_workload("tpch", d, devices=1, nodes=1, scale=0.01, seed=3, row_group_bytes=64 << 10)
+    psg.gen_workload("tpch", d, devices=1, nodes=1, scale=0.01, seed=3, row_group_bytes=64 << 10, codec="identity")
     return d
 
 

@@ -34,7 +34,8 @@ def pdata(tmp_path_factory):
         key = (scale, seed, rg, nodes)
         if key not in cache:
             d = str(base / ("d%d" % len(cache)))
-            psg.gen_workload("tpch", d, devices=nodes, nodes=nodes, scale=scale, seed=seed, row_group_bytes=rg)
+            psg.gen_workload("tpch", d, devices=nodes, nodes=nodes, scale=scale, seed=seed, row_group_bytes=rg,
+                             codec="identity")
             cache[key] = d
         return cache[key]
 
