@@ -200,54 +200,56 @@ enum Reason : int { kRFlush = 0, kREob = 1, kRErr = 2 };
 __device__ __forceinline__ uint64_t shl(uint64_t x, int s) { return s < 64 ? x << s : 0ull; }
 __device__ __forceinline__ uint64_t low_bytes(uint64_t x, int k) { return k >= 8 ? x : x & ((1ull << (8 * k)) - 1ull); }
 
-/// Lane 0's output assembler: bytes [0, oi) are whole words in the ring (and older ones flushed
-/// to HBM), the next `an` (< 8) bytes wait in `acc`; w1 / w2 mirror the ring words at oi-8 / oi-16
-/// so that the short distances typical of 8-byte columns never touch memory.
+/// Lane 0's output assembler. Bytes [0, oi) are whole words and the next `an` (< 8) bytes are
+/// in `acc`; the ring always holds every produced byte of the last 2 KB - the partial word is
+/// stored on every append - so a match source is two shared-memory words (older ones come from
+/// the already flushed output in HBM), with no register window to branch over.
 struct Out0 {
   uint64_t* ring;  // kRing / 8 words
   const uint64_t* hbm;
-  uint64_t acc, w1, w2;
+  uint64_t acc;
   uint32_t oi;
   int an;
   __device__ __forceinline__ uint32_t pos() const { return oi + static_cast<uint32_t>(an); }
-  __device__ __forceinline__ void word(uint64_t w) {
-    ring[(oi >> 3) & (kRing / 8 - 1)] = w;
-    w2 = w1;
-    w1 = w;
-    oi += 8;
+  __device__ __forceinline__ uint64_t& slot(uint32_t byte_pos) const { return ring[(byte_pos >> 3) & (kRing / 8 - 1)]; }
+  /// Appends one literal byte.
+  __device__ __forceinline__ void put1(uint32_t byte) {
+    acc |= static_cast<uint64_t>(byte) << (8 * an);
+    slot(oi) = acc;
+    if (++an == 8) {
+      oi += 8;
+      acc = 0;
+      an = 0;
+    }
   }
   /// Appends the low k (1..8) bytes of v.
   __device__ __forceinline__ void put(uint64_t v, int k) {
     v = low_bytes(v, k);
-    acc |= shl(v, 8 * an);
+    acc |= v << (8 * an);
+    slot(oi) = acc;
     const int t = an + k;
     if (t >= 8) {
-      word(acc);
+      oi += 8;
       acc = an ? (v >> (64 - 8 * an)) : 0ull;
+      slot(oi) = acc;
       an = t - 8;
     } else {
       an = t;
     }
   }
-  /// 8 bytes at position s, s + 8 <= pos() (hence s < oi).
+  /// 8 bytes from position s (s < pos()); bytes at or past pos() are unspecified.
   __device__ __forceinline__ uint64_t read8(uint32_t s) const {
     const int sh = static_cast<int>(s & 7) * 8;
     uint64_t lo, hi;
-    if (s + 16 >= oi) {  // register window [oi - 16, oi + an)
-      const bool q0 = s + 8 < oi;
-      lo = q0 ? w2 : w1;
-      hi = q0 ? w1 : acc;
-    } else if (s + kRing - 8 >= oi) {  // both words still in the ring
-      lo = ring[(s >> 3) & (kRing / 8 - 1)];
-      hi = ring[((s >> 3) + 1) & (kRing / 8 - 1)];
+    if (s + kRing - 8 >= oi) {  // both words still in the ring
+      lo = slot(s);
+      hi = slot(s + 8);
     } else {  // flushed long ago (flushed >= oi - 1290 > s + 16)
       lo = __ldcg(reinterpret_cast<const unsigned long long*>(hbm) + (s >> 3));
       hi = __ldcg(reinterpret_cast<const unsigned long long*>(hbm) + (s >> 3) + 1);
     }
     return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
   }
-  /// The 8 bytes ending at pos() (positions before 0 are never referenced).
-  __device__ __forceinline__ uint64_t last8() const { return an ? (w1 >> (8 * an)) | (acc << (64 - 8 * an)) : w1; }
 };
 
 /// Flushes ring bytes [flushed, flushed + nbytes) (nbytes <= kFlush) to dst in whole 16-byte
@@ -322,7 +324,7 @@ __device__ __forceinline__ int decode_run(Bits& br, Out0& o, WarpSmem& sm, const
     const uint32_t kind = (e >> 4) & 3;
     if (kind == kLit) {
       if (o.pos() >= usize) return kRErr;
-      o.put(e >> 8, 1);
+      o.put1((e >> 8) & 0xFFu);
       if (o.oi - flushed >= kFlush) return kRFlush;
       continue;
     }
@@ -342,29 +344,25 @@ __device__ __forceinline__ int decode_run(Bits& br, Out0& o, WarpSmem& sm, const
     br.drop(dl);
     const uint32_t dist = (de >> 16) + br.get(static_cast<int>((de >> 8) & 15));
     if (dist > o.pos() || o.pos() + len > usize) return kRErr;
-    if (dist >= 8) {
-      while (len) {
-        const int k = len < 8 ? static_cast<int>(len) : 8;
-        o.put(o.read8(o.pos() - dist), k);
-        len -= static_cast<uint32_t>(k);
-      }
-    } else {  // period < 8: replicate the last `dist` bytes
-      const int d = static_cast<int>(dist);
-      while (len) {
-        uint64_t v = low_bytes(o.last8() >> (8 * (8 - d)), d);
-        v |= shl(v, 8 * d);
+    // 8 bytes per step; a period d < 8 replicates the d bytes before the write position
+    const int d = static_cast<int>(dist);
+    while (len) {
+      const int k = len < 8 ? static_cast<int>(len) : 8;
+      uint64_t v = o.read8(o.pos() - dist);
+      if (d < 8) {
+        v = low_bytes(v, d);
+        v |= v << (8 * d);
         v |= shl(v, 16 * d);
         v |= shl(v, 32 * d);
-        const int k = len < 8 ? static_cast<int>(len) : 8;
-        o.put(v, k);
-        len -= static_cast<uint32_t>(k);
       }
+      o.put(v, k);
+      len -= static_cast<uint32_t>(k);
     }
     if (o.oi - flushed >= kFlush) return kRFlush;
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32) k_inflate(const InflateJob* __restrict__ jobs, uint32_t njobs,
+__global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __restrict__ jobs, uint32_t njobs,
                                                         unsigned int* err) {
   __shared__ WarpSmem smem[kWarps];
   const int lane = threadIdx.x & 31;
@@ -387,7 +385,7 @@ __global__ void __launch_bounds__(kWarps * 32) k_inflate(const InflateJob* __res
     Out0 o;
     o.ring = reinterpret_cast<uint64_t*>(sm.ring);
     o.hbm = reinterpret_cast<const uint64_t*>(dst);
-    o.acc = o.w1 = o.w2 = 0;
+    o.acc = 0;
     o.oi = 0;
     o.an = 0;
     uint32_t flushed = 0, s1 = 1, s2 = 0;
@@ -555,6 +553,11 @@ void launch_inflate(const InflateJob* d_jobs, uint32_t njobs, unsigned int* d_er
   if (njobs == 0) return;
   // persistent warps: warp w takes jobs w, w + nwarps, ... (longest first, see plan_batches);
   // 6 CTAs x 4 warps fit an SM (33 KB of tables + ring per CTA)
+  static bool attr = [] {
+    return cudaFuncSetAttribute(k_inflate, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                cudaSharedmemCarveoutMaxShared) == cudaSuccess;
+  }();
+  (void)attr;
   const uint32_t blocks = std::min<uint32_t>((njobs + kWarps - 1) / kWarps, 148u * 6u);
   k_inflate<<<blocks, kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(d_jobs, njobs, d_err);
   count_external_launch();

@@ -37,10 +37,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--jobs", type=int, default=592)
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--scale", type=float, default=1.0)
     a = ap.parse_args()
-    d = "/tmp/psg_inflate/sf1_block"
+    d = "/tmp/psg_inflate/sf%g_block" % a.scale
     if not os.path.exists(d + "/DONE"):
-        psg.gen_workload("tpch", d, devices=1, nodes=1, scale=1.0, seed=42, codec="block")
+        psg.gen_workload("tpch", d, devices=1, nodes=1, scale=a.scale, seed=42, codec="block")
         open(d + "/DONE", "w").write("ok")
     ch = chunks_of(d + "/dev0/lineitem.node0.psto")[:a.jobs]
     ctx = psg.Context(0)
