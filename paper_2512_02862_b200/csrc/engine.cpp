@@ -551,7 +551,10 @@ struct StreamSession {
   uint64_t dslot_bytes = 0;
   uint64_t h2d_bytes = 0;
   int regulated_slots = 0;
-  size_t cursor = 0;  // next batch to consume (global order)
+  size_t cursor = 0;    // next batch to consume (global order)
+  size_t enqueued = 0;  // batches whose copy (+ inflate) has been enqueued
+  size_t released = 0;  // batches the consumer has released (slot_free recorded)
+  std::vector<BatchView> views;  // per ring slot
   int cur_slot = -1;
 
   /// budget/ht_reserve: plan memory_budget_bytes and the bytes set aside for hash tables; the ring
@@ -629,6 +632,7 @@ struct StreamSession {
         inflated.push_back(x);
       }
     }
+    views.resize(slots.size());
     if (dslot_bytes) {
       inflate_err = DevBuf(ctx.pool, sizeof(unsigned int), ctx.copy);
       PSG_CUDA(cudaMemsetAsync(inflate_err.p, 0, sizeof(unsigned int), ctx.copy));
@@ -652,16 +656,16 @@ struct StreamSession {
     PSG_CUDA(cudaMemcpy(&e, inflate_err.p, sizeof e, cudaMemcpyDeviceToHost));
     if (e) throw IoFailure("inflate failed");
   }
-  /// Stages batch i (must be the next in consumption order) into its HBM ring slot.
-  void stage(size_t i, BatchView& v) {
-    if (i != cursor) throw Error(PSG_ERR_INTERNAL, "ingest batches consumed out of order");
-    const int k = static_cast<int>(i % slots.size());
-    const BatchPlan& b = batches[i];
+  /// Enqueues batch j's host->HBM copy (and inflate) into its ring slot. The slot's previous
+  /// occupant (batch j - nslots) must have been released (its slot_free event recorded).
+  void enqueue(size_t j) {
+    const int k = static_cast<int>(j % slots.size());
+    const BatchPlan& b = batches[j];
     auto* base = slots[k].as<uint8_t>();
     uint8_t* dbase = b.inflate ? dslots[k].as<uint8_t>() : base;
     uint64_t nt = 0;
     auto segs = make_segments(b, dbase, nt);
-    if (i >= slots.size()) PSG_CUDA(cudaStreamWaitEvent(ctx.copy, slot_free[k], 0));
+    if (j >= slots.size()) PSG_CUDA(cudaStreamWaitEvent(ctx.copy, slot_free[k], 0));
     size_t toff = 0;
     auto blob = pack_view(segs, toff);
     size_t joff = blob.size();
@@ -670,7 +674,7 @@ struct StreamSession {
       blob.resize(joff + jobs.size() * sizeof(InflateJob));
       std::memcpy(blob.data() + joff, jobs.data(), jobs.size() * sizeof(InflateJob));
     }
-    ingest->copy_to_device(i, base, blob.data(), blob.size(), ctx.copy);
+    ingest->copy_to_device(j, base, blob.data(), blob.size(), ctx.copy);
     h2d_bytes += b.bytes + blob.size();
     PSG_CUDA(cudaEventRecord(copied[k], ctx.copy));
     if (b.inflate) {
@@ -678,21 +682,40 @@ struct StreamSession {
       launch_inflate(reinterpret_cast<const InflateJob*>(base + b.bytes + joff), static_cast<uint32_t>(b.jobs.size()),
                      inflate_err.as<unsigned int>(), istreams[k]);
       PSG_CUDA(cudaEventRecord(inflated[k], istreams[k]));
-      PSG_CUDA(cudaStreamWaitEvent(ctx.compute, inflated[k], 0));
-    } else {
-      PSG_CUDA(cudaStreamWaitEvent(ctx.compute, copied[k], 0));
     }
+    BatchView& v = views[k];
     v.d_segs = reinterpret_cast<const Segment*>(base + b.bytes);
     v.d_tile_seg = reinterpret_cast<const uint32_t*>(base + b.bytes + toff);
     v.nsegs = static_cast<int>(segs.size());
     v.ntiles = nt;
     v.rows = b.total_rows;
     v.bytes = b.scan_bytes();
+    ++enqueued;
+  }
+  /// Read-ahead: enqueue the copies (and inflates) of upcoming batches whose bytes are already
+  /// in pinned memory and whose ring slot is free, so transfers and decoding run ahead of the
+  /// consumer even when it blocks on the host (the per-wave exchange sync at N > 1).
+  void read_ahead() {
+    while (enqueued < batches.size() && enqueued < released + slots.size() && ingest->ready(enqueued)) enqueue(enqueued);
+  }
+  /// Stages batch i (must be the next in consumption order) into its HBM ring slot.
+  void stage(size_t i, BatchView& v) {
+    if (i != cursor) throw Error(PSG_ERR_INTERNAL, "ingest batches consumed out of order");
+    while (enqueued <= i) enqueue(enqueued);  // blocks on the read of batch i if needed
+    const int k = static_cast<int>(i % slots.size());
+    PSG_CUDA(cudaStreamWaitEvent(ctx.compute, batches[i].inflate ? inflated[k] : copied[k], 0));
+    v = views[k];
     cur_slot = k;
     ++cursor;
+    read_ahead();
   }
   void release() {
-    if (cur_slot >= 0) PSG_CUDA(cudaEventRecord(slot_free[cur_slot], ctx.compute));
+    if (cur_slot >= 0) {
+      PSG_CUDA(cudaEventRecord(slot_free[cur_slot], ctx.compute));
+      ++released;
+      cur_slot = -1;
+      read_ahead();
+    }
   }
 };
 

@@ -122,6 +122,8 @@ class Ingest {
   /// Blocks until batch i is in pinned memory, writes `extra` bytes (segment descriptors) after
   /// the payload, then enqueues the H2D copy of payload+extra to dst. Returns after enqueueing.
   void copy_to_device(size_t i, void* dst, const void* extra, size_t extra_bytes, cudaStream_t copy_stream);
+  /// Whether batch i is already in pinned memory (copy_to_device would not block).
+  bool ready(size_t i);
   uint64_t bytes_read() const { return bytes_read_; }
   double wait_s() const { return wait_s_; }
 

@@ -302,6 +302,11 @@ void CUDART_CB Ingest::on_copied(void* arg) {
   d->self->cv_.notify_all();
 }
 
+bool Ingest::ready(size_t i) {
+  std::lock_guard<std::mutex> lk(mu_);
+  return !error_.empty() || (slot_of_batch_[i] >= 0 && slots_[slot_of_batch_[i]].ready);
+}
+
 void Ingest::copy_to_device(size_t i, void* dst, const void* extra, size_t extra_bytes, cudaStream_t copy_stream) {
   int slot;
   {
