@@ -177,6 +177,30 @@ int psg_hash_join(psg_ctx* ctx, const psg_batch* build, const char* build_key,
 int psg_codec_decompress(psg_ctx* ctx, int codec, uint64_t n, const void* const* src, const uint64_t* src_len,
                          void* const* dst, const uint64_t* dst_len);
 
+/* HashTable (ops.hpp:49-82) as a GPU handle: build over nbatches batches of one schema
+ * (duplicates keep every row; hash_kind as in psg_partition, accepted for API parity), then
+ * any number of lookups / probes. The materialised build side is the concatenation of the
+ * batches (row r = r-th row overall). Free every table before its context. */
+typedef struct psg_hashtable psg_hashtable;
+int psg_hashtable_build(psg_ctx* ctx, const psg_batch* batches, uint32_t nbatches, const char* key_column,
+                        int hash_kind, psg_hashtable** out);
+/* row_count() and the number of payload columns (build columns minus the key). */
+int psg_hashtable_shape(const psg_hashtable* t, uint64_t* rows, uint32_t* payload_cols);
+/* key_at(row) / payload_at(col, row) for every payload column (build order, key skipped). */
+int psg_hashtable_row(const psg_hashtable* t, const char* key_column, uint64_t row, int64_t* key,
+                      uint64_t* payload);
+/* lookup(key) for n keys at once: offsets[0..n] (CSR) into rows_out, the build-row indices that
+ * carry each key (a multiset per key, like the reference's chained buckets); *total = matches.
+ * InvalidInput when total > cap (offsets and *total are still filled). */
+int psg_hashtable_lookup(psg_ctx* ctx, const psg_hashtable* t, const int64_t* keys, uint64_t n,
+                         uint64_t* offsets, uint64_t* rows_out, uint64_t cap, uint64_t* total);
+/* probe (ops.cpp:173-222): build payload ++ probe columns ("_p" on a name clash). */
+int psg_hashtable_probe(psg_ctx* ctx, const psg_hashtable* t, const psg_batch* probe, const char* probe_key,
+                        psg_result** out);
+void psg_hashtable_free(psg_hashtable* t);
+/* concat (ops.cpp:80-98): batches of one schema into one (InvalidInput on a schema mismatch). */
+int psg_concat(psg_ctx* ctx, const psg_batch* batches, uint32_t nbatches, psg_result** out);
+
 /* ---- PSTO format (psto.hpp) ---- */
 /* TableWriter (psto.cpp:144-229): writes a batch as a PSTO file. Returns row groups written. */
 int psg_psto_write(const char* path, const psg_batch* batch, uint64_t row_group_rows, int codec,

@@ -32,7 +32,9 @@ EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_uniq
            "psg_ctx_set_ingest", "psg_ctx_set_semijoin", "psg_ctx_set_fused_shuffle", "psg_ctx_destroy", "psg_execute_plan",
            "psg_execute_local", "psg_stage_plan",
            "psg_execute_staged", "psg_staged_free", "psg_result_shape", "psg_result_field", "psg_result_data",
-           "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_codec_decompress", "psg_psto_write",
+           "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_hashtable_build",
+           "psg_hashtable_shape", "psg_hashtable_row", "psg_hashtable_lookup", "psg_hashtable_probe", "psg_hashtable_free",
+           "psg_concat", "psg_codec_decompress", "psg_psto_write",
            "psg_psto_inspect", "psg_gen_tpch", "psg_jit_selftest", "psg_tmin"]
 
 
@@ -98,6 +100,13 @@ def lib():
             "psg_filter": ([vp, P(Batch), P(Atom), ctypes.c_uint32, P(vp)], i32),
             "psg_partition": ([vp, P(Batch), c, ctypes.c_uint32, i32, P(vp), P(u64)], i32),
             "psg_hash_join": ([vp, P(Batch), c, P(Batch), c, P(vp)], i32),
+            "psg_hashtable_build": ([vp, P(Batch), ctypes.c_uint32, c, i32, P(vp)], i32),
+            "psg_hashtable_shape": ([vp, P(u64), P(ctypes.c_uint32)], i32),
+            "psg_hashtable_row": ([vp, c, u64, P(ctypes.c_int64), P(u64)], i32),
+            "psg_hashtable_lookup": ([vp, vp, P(ctypes.c_int64), u64, P(u64), P(u64), u64, P(u64)], i32),
+            "psg_hashtable_probe": ([vp, vp, P(Batch), c, P(vp)], i32),
+            "psg_hashtable_free": ([vp], None),
+            "psg_concat": ([vp, P(Batch), ctypes.c_uint32, P(vp)], i32),
             "psg_codec_decompress": ([vp, i32, u64, P(vp), P(u64), P(vp), P(u64)], i32),
             "psg_psto_write": ([c, P(Batch), u64, i32, P(u64)], i32),
             "psg_psto_inspect": ([c, P(u64), P(ctypes.c_uint32), P(u64), P(i32)], i32),
@@ -429,6 +438,96 @@ def partition(columns: dict, key, nparts, hash_kind="multiply_shift", ctx: Conte
         parts.append(r.rows[at: at + counts[p]])
         at += counts[p]
     return r.schema, parts
+
+
+class HashTable:
+    """HashTable (ops.hpp:49-82) on the GPU: build over several batches of one schema (duplicates
+    keep every row), then lookup / probe any number of times. Mirrors the reference's
+    HashTable::build(batches, key, hash) / lookup(key) / probe(batch, key) / row_count /
+    key_at / payload_at."""
+
+    def __init__(self, handle, ctx, key):
+        self._h, self._ctx, self._key = handle, ctx, key
+        rows, nc = ctypes.c_uint64(), ctypes.c_uint32()
+        _check(lib().psg_hashtable_shape(self._h, ctypes.byref(rows), ctypes.byref(nc)))
+        self._rows, self._npay = rows.value, nc.value
+
+    @classmethod
+    def build(cls, batches, key_column, hash="multiply_shift", ctx: Context | None = None, types=None):
+        ctx = ctx or _ctx()
+        bs = [_make_batch(b, types) for b in batches]
+        arr = (Batch * max(len(bs), 1))(*bs)
+        out = ctypes.c_void_p()
+        _check(lib().psg_hashtable_build(ctx._h, arr, len(bs), key_column.encode(),
+                                         1 if hash == "identity" else 0, ctypes.byref(out)))
+        t = cls(out, ctx, key_column)
+        t._keep = bs
+        return t
+
+    def row_count(self):
+        return self._rows
+
+    def key_at(self, row):
+        k = ctypes.c_int64()
+        pay = (ctypes.c_uint64 * max(self._npay, 1))()
+        _check(lib().psg_hashtable_row(self._h, self._key.encode(), int(row), ctypes.byref(k), pay))
+        return k.value
+
+    def payload_at(self, col, row):
+        k = ctypes.c_int64()
+        pay = (ctypes.c_uint64 * max(self._npay, 1))()
+        _check(lib().psg_hashtable_row(self._h, self._key.encode(), int(row), ctypes.byref(k), pay))
+        return pay[col]
+
+    def lookup_many(self, keys):
+        """[indices of the build rows carrying key] for every key (one GPU pass)."""
+        ks = np.ascontiguousarray(np.asarray(keys, dtype=np.int64))
+        n = len(ks)
+        offs = np.zeros(n + 1, dtype=np.uint64)
+        total = ctypes.c_uint64()
+        cap = max(n, 1) * 4
+        while True:
+            rows = np.zeros(cap, dtype=np.uint64)
+            rc = lib().psg_hashtable_lookup(self._ctx._h, self._h, ks.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n,
+                                            offs.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                                            rows.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), cap,
+                                            ctypes.byref(total))
+            if rc == 0:
+                break
+            if total.value > cap:
+                cap = int(total.value)
+                continue
+            _check(rc)
+        return [rows[int(offs[i]):int(offs[i + 1])].tolist() for i in range(n)]
+
+    def lookup(self, key):
+        return self.lookup_many([key])[0]
+
+    def probe(self, batch: dict, probe_key, types=None) -> "Result":
+        pb = _make_batch(batch, types)
+        out = ctypes.c_void_p()
+        _check(lib().psg_hashtable_probe(self._ctx._h, self._h, ctypes.byref(pb), probe_key.encode(), ctypes.byref(out)))
+        return Result(out)
+
+    def free(self):
+        if getattr(self, "_h", None):
+            lib().psg_hashtable_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def concat(batches, ctx: Context | None = None, types=None) -> "Result":
+    """concat (ops.cpp:80-98): batches of one schema into one batch."""
+    bs = [_make_batch(b, types) for b in batches]
+    arr = (Batch * max(len(bs), 1))(*bs)
+    out = ctypes.c_void_p()
+    _check(lib().psg_concat((ctx or _ctx())._h, arr, len(bs), ctypes.byref(out)))
+    return Result(out)
 
 
 def hash_join(build: dict, build_key, probe: dict, probe_key, ctx: Context | None = None, build_types=None,

@@ -293,6 +293,78 @@ int psg_codec_decompress(psg_ctx* ctx, int codec, uint64_t n, const void* const*
   });
 }
 
+struct psg_hashtable {
+  psg::GpuHashTable* t = nullptr;
+  ~psg_hashtable() { psg::op_hashtable_free(t); }
+};
+
+int psg_hashtable_build(psg_ctx* ctx, const psg_batch* batches, uint32_t nbatches, const char* key_column, int hash_kind,
+                        psg_hashtable** out) {
+  return guarded([&] {
+    if (!ctx || !out || !key_column || (nbatches && !batches)) throw InvalidInput("null argument");
+    if (hash_kind != 0 && hash_kind != 1) throw InvalidInput("unknown hash kind");
+    std::vector<HostBatch> hs;
+    for (uint32_t i = 0; i < nbatches; ++i) hs.push_back(to_host(&batches[i]));
+    auto h = std::make_unique<psg_hashtable>();
+    h->t = op_hashtable_build(ctx->c, hs, key_column);
+    *out = h.release();
+  });
+}
+
+int psg_hashtable_shape(const psg_hashtable* t, uint64_t* rows, uint32_t* payload_cols) {
+  return guarded([&] {
+    if (!t) throw InvalidInput("null argument");
+    const HostBatch& h = op_hashtable_host(*t->t);
+    if (rows) *rows = h.rows();
+    if (payload_cols) *payload_cols = static_cast<uint32_t>(h.schema.size() - 1);
+  });
+}
+
+int psg_hashtable_row(const psg_hashtable* t, const char* key_column, uint64_t row, int64_t* key, uint64_t* payload) {
+  return guarded([&] {
+    if (!t || !key_column) throw InvalidInput("null argument");
+    const HostBatch& h = op_hashtable_host(*t->t);
+    if (row >= h.rows()) throw InvalidInput("row out of range");
+    const size_t k = h.schema.require(key_column);
+    if (key) *key = static_cast<int64_t>(h.cols[k][row]);
+    size_t o = 0;
+    for (size_t c = 0; c < h.cols.size(); ++c)
+      if (c != k && payload) payload[o++] = h.cols[c][row];
+  });
+}
+
+int psg_hashtable_lookup(psg_ctx* ctx, const psg_hashtable* t, const int64_t* keys, uint64_t n, uint64_t* offsets,
+                         uint64_t* rows_out, uint64_t cap, uint64_t* total) {
+  return guarded([&] {
+    if (!ctx || !t || (n && !keys) || !offsets || !total) throw InvalidInput("null argument");
+    std::vector<uint64_t> off;
+    auto rows = op_hashtable_lookup(ctx->c, *t->t, std::vector<int64_t>(keys, keys + n), off);
+    std::memcpy(offsets, off.data(), (n + 1) * 8);
+    *total = rows.size();
+    if (rows.size() > cap) throw InvalidInput("lookup result exceeds the output capacity");
+    if (!rows.empty()) std::memcpy(rows_out, rows.data(), rows.size() * 8);
+  });
+}
+
+int psg_hashtable_probe(psg_ctx* ctx, const psg_hashtable* t, const psg_batch* probe, const char* probe_key,
+                        psg_result** out) {
+  return guarded([&] {
+    if (!ctx || !t || !probe_key || !out) throw InvalidInput("null argument");
+    *out = to_result(op_hashtable_probe(ctx->c, *t->t, to_host(probe), probe_key));
+  });
+}
+
+void psg_hashtable_free(psg_hashtable* t) { delete t; }
+
+int psg_concat(psg_ctx* ctx, const psg_batch* batches, uint32_t nbatches, psg_result** out) {
+  return guarded([&] {
+    if (!ctx || !out || (nbatches && !batches)) throw InvalidInput("null argument");
+    std::vector<HostBatch> hs;
+    for (uint32_t i = 0; i < nbatches; ++i) hs.push_back(to_host(&batches[i]));
+    *out = to_result(op_concat(ctx->c, hs));
+  });
+}
+
 int psg_hash_join(psg_ctx* ctx, const psg_batch* build, const char* build_key, const psg_batch* probe,
                   const char* probe_key, psg_result** out) {
   return guarded([&] {

@@ -243,6 +243,14 @@ HostBatch op_partition(Ctx& ctx, const HostBatch& in, const std::string& key, ui
                        std::vector<uint64_t>& part_rows);
 void op_codec_decompress(Ctx& ctx, int codec, uint64_t n, const void* const* src, const uint64_t* src_len,
                          void* const* dst, const uint64_t* dst_len);
+struct GpuHashTable;
+GpuHashTable* op_hashtable_build(Ctx& ctx, const std::vector<HostBatch>& batches, const std::string& key_column);
+void op_hashtable_free(GpuHashTable* t);
+std::vector<uint64_t> op_hashtable_lookup(Ctx& ctx, const GpuHashTable& t, const std::vector<int64_t>& keys,
+                                          std::vector<uint64_t>& offsets);
+HostBatch op_hashtable_probe(Ctx& ctx, const GpuHashTable& t, const HostBatch& probe, const std::string& probe_key);
+const HostBatch& op_hashtable_host(const GpuHashTable& t);  // materialised build side (key_at / payload_at)
+HostBatch op_concat(Ctx& ctx, const std::vector<HostBatch>& batches);
 HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& build_key, const HostBatch& probe,
                        const std::string& probe_key);
 

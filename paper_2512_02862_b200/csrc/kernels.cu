@@ -654,6 +654,27 @@ void launch_gather(const uint64_t* const* in_cols, int ncols, const uint32_t* id
   k_gather<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, ncols, idx, n, oc);
 }
 
+/// out[c][i] = in[c][idx[i]] with 64-bit indices (row indices produced by an expanding join).
+__global__ void k_gather64(ColPtrs in, int ncols, const uint64_t* idx, uint64_t n, OutPtrs out) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t j = idx[i];
+    for (int c = 0; c < ncols; ++c) out.p[c][i] = in.p[c][j];
+  }
+}
+void launch_gather64(const uint64_t* const* in_cols, int ncols, const uint64_t* idx, uint64_t n, uint64_t* const* out,
+                     void* stream) {
+  if (n == 0 || ncols == 0) return;
+  ColPtrs pc{};
+  OutPtrs oc{};
+  for (int c = 0; c < ncols; ++c) {
+    pc.p[c] = in_cols[c];
+    oc.p[c] = out[c];
+  }
+  count_launch();
+  k_gather64<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, ncols, idx, n, oc);
+}
+
 // --------------------------------------------------------------------------- result emission
 /// counter[0] = groups, counter[1] = min, counter[2] = max of the sign-flipped keys (the sort
 /// then only needs the bits where min and max differ: all keys share the bits above). Each block

@@ -72,6 +72,8 @@ size_t sort_pairs_i64(const uint64_t* keys_in, uint64_t* keys_out, const unsigne
                       unsigned long long* v_out, uint64_t n, int end_bit, void* tmp, size_t tmp_bytes, void* stream);
 size_t sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_t* v_in, uint32_t* v_out, uint64_t n,
                       int end_bit, void* tmp, size_t tmp_bytes, void* stream);
+void launch_gather64(const uint64_t* const* in_cols, int ncols, const uint64_t* idx, uint64_t n, uint64_t* const* out,
+                     void* stream);
 void launch_iota_u32(uint32_t* out, uint64_t n, void* stream);
 void launch_rows_from_cols(const uint64_t* const* cols, int ncols, uint64_t n, uint64_t* out_rows, void* stream);
 

@@ -218,83 +218,226 @@ HostBatch op_partition(Ctx& ctx, const HostBatch& in, const std::string& key, ui
   return out;
 }
 
-HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& build_key, const HostBatch& probe,
-                       const std::string& probe_key) {
-  PSG_CUDA(cudaSetDevice(ctx.device));
-  check_batch(build);
-  check_batch(probe);
-  const size_t bk = build.schema.require(build_key);
-  const size_t pk = probe.schema.require(probe_key);
-  if (build.schema.fields[bk].type != LType::Int64) throw InvalidInput("join key must be int64: " + build_key);
-  if (probe.schema.fields[pk].type != LType::Int64) throw InvalidInput("probe key must be int64: " + probe_key);
+// ------------------------------------------------------------------ HashTable (ops.hpp:49-82)
+/// GPU analog of the reference's chained HashTable (ops.cpp:105-222): the build batches are
+/// concatenated in HBM (the "materialised build side", row r = r-th row of the concatenation),
+/// and an open-addressing CSR index maps each key to the build-row indices that carry it
+/// (duplicates keep every row). lookup returns those indices; probe expands every probe row by
+/// its matches and gathers the build payload.
+struct GpuHashTable {
+  Ctx* ctx = nullptr;
+  Schema schema;          // build schema
+  size_t key = 0;         // key column index
+  Schema payload_schema;  // build schema minus the key
+  uint64_t rows = 0, cap = 0;
+  int shift = 64;
+  std::vector<DevBuf> cols;  // materialised build side (all columns), HBM
+  DevBuf keys, cnt, start, rowidx;
+  LocalTableDev dev{};
+  HostBatch host;  // the same rows on the host (key_at / payload_at)
+};
+
+namespace {
+
+HostBatch concat_host(const std::vector<HostBatch>& batches) {
+  if (batches.empty()) throw InvalidInput("concat needs at least one batch");
   HostBatch out;
-  for (size_t c = 0; c < build.schema.size(); ++c)
-    if (c != bk) out.schema.fields.push_back(build.schema.fields[c]);
+  out.schema = batches[0].schema;
+  out.cols.resize(out.schema.size());
+  for (const auto& b : batches) {
+    check_batch(b);
+    if (b.schema.size() != out.schema.size()) throw InvalidInput("concat: batches have different schemas");
+    for (size_t c = 0; c < b.schema.size(); ++c)
+      if (b.schema.fields[c].name != out.schema.fields[c].name || b.schema.fields[c].type != out.schema.fields[c].type)
+        throw InvalidInput("concat: batches have different schemas");
+    for (size_t c = 0; c < b.cols.size(); ++c) out.cols[c].insert(out.cols[c].end(), b.cols[c].begin(), b.cols[c].end());
+  }
+  return out;
+}
+
+/// Expanding join of `probe_keys` (device, n rows) against t: per key the matching build-row
+/// indices, CSR (offsets on the device, n + 1 entries; returns the total match count).
+uint64_t expand_rows(Ctx& ctx, const GpuHashTable& t, const uint64_t* probe_keys, uint64_t n, DevBuf& offs,
+                     DevBuf& rows_out) {
+  DevBuf counts(ctx.pool, (n + 1) * 4, ctx.compute);
+  offs = DevBuf(ctx.pool, (n + 1) * 4, ctx.compute);
+  PSG_CUDA(cudaMemsetAsync(counts.p, 0, (n + 1) * 4, ctx.compute));
+  if (n) launch_expand_count(t.dev, probe_keys, n, counts.as<uint32_t>(), ctx.compute);
+  const size_t tb = exclusive_scan_u32(nullptr, nullptr, n + 1, nullptr, 0, ctx.compute);
+  DevBuf tmp(ctx.pool, std::max<size_t>(tb, 8), ctx.compute);
+  exclusive_scan_u32(counts.as<uint32_t>(), offs.as<uint32_t>(), n + 1, tmp.p, tb, ctx.compute);
+  uint32_t total = 0;
+  PSG_CUDA(cudaMemcpyAsync(&total, offs.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, ctx.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx.compute));
+  rows_out = DevBuf(ctx.pool, std::max<uint64_t>(total, 1) * 8, ctx.compute);
+  uint64_t* outp = rows_out.as<uint64_t>();
+  if (total) launch_expand_write(t.dev, probe_keys, n, offs.as<uint32_t>(), nullptr, 0, &outp, ctx.compute);
+  return total;
+}
+
+}  // namespace
+
+GpuHashTable* op_hashtable_build(Ctx& ctx, const std::vector<HostBatch>& batches, const std::string& key_column) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  auto t = std::make_unique<GpuHashTable>();
+  t->ctx = &ctx;
+  t->host = concat_host(batches);
+  t->schema = t->host.schema;
+  t->key = t->schema.require(key_column);
+  if (t->schema.fields[t->key].type != LType::Int64) throw InvalidInput("join key must be int64: " + key_column);
+  for (size_t c = 0; c < t->schema.size(); ++c)
+    if (c != t->key) t->payload_schema.fields.push_back(t->schema.fields[c]);
+  const uint64_t nb = t->rows = t->host.rows();
+  if (nb >= (1ULL << 32)) throw InvalidInput("hash table build side exceeds 2^32 rows");
+  Uploaded u = upload(ctx, t->host);
+  t->cols = std::move(u.cols);
+  t->cap = 16;
+  while (t->cap < 2 * nb) t->cap <<= 1;
+  t->shift = 64;
+  for (uint64_t c = t->cap; c > 1; c >>= 1) --t->shift;
+  t->keys = DevBuf(ctx.pool, t->cap * 8, ctx.compute);
+  t->cnt = DevBuf(ctx.pool, (t->cap + 1) * 4, ctx.compute);
+  t->start = DevBuf(ctx.pool, (t->cap + 1) * 4, ctx.compute);
+  t->rowidx = DevBuf(ctx.pool, std::max<uint64_t>(nb, 1) * 8, ctx.compute);
+  DevBuf cursor(ctx.pool, (t->cap + 1) * 4, ctx.compute), maxc(ctx.pool, 4, ctx.compute),
+      iota(ctx.pool, std::max<uint64_t>(nb, 1) * 8, ctx.compute);
+  std::vector<uint64_t> seq(nb);
+  std::iota(seq.begin(), seq.end(), 0ULL);
+  if (nb) PSG_CUDA(cudaMemcpyAsync(iota.p, seq.data(), nb * 8, cudaMemcpyHostToDevice, ctx.compute));
+  PSG_CUDA(cudaMemsetAsync(cursor.p, 0, (t->cap + 1) * 4, ctx.compute));
+  PSG_CUDA(cudaMemsetAsync(maxc.p, 0, 4, ctx.compute));
+  launch_local_init(t->keys.as<uint64_t>(), t->cnt.as<uint32_t>(), t->cap, ctx.compute);
+  const uint64_t* bk = t->cols[t->key].as<uint64_t>();
+  launch_local_count(t->keys.as<uint64_t>(), t->cnt.as<uint32_t>(), t->cap - 1, t->shift, bk, nb, maxc.as<unsigned>(),
+                     ctx.compute);
+  const size_t tb = exclusive_scan_u32(nullptr, nullptr, t->cap + 1, nullptr, 0, ctx.compute);
+  DevBuf tmp(ctx.pool, tb, ctx.compute);
+  exclusive_scan_u32(t->cnt.as<uint32_t>(), t->start.as<uint32_t>(), t->cap + 1, tmp.p, tb, ctx.compute);
+  const uint64_t* src = iota.as<uint64_t>();
+  uint64_t* dst = t->rowidx.as<uint64_t>();
+  launch_local_fill(t->keys.as<uint64_t>(), t->start.as<uint32_t>(), cursor.as<uint32_t>(), t->cap - 1, t->shift, bk, &src,
+                    &dst, 1, nb, ctx.compute);
+  t->dev.keys = t->keys.as<uint64_t>();
+  t->dev.cnt = t->cnt.as<uint32_t>();
+  t->dev.start = t->start.as<uint32_t>();
+  t->dev.mask = t->cap - 1;
+  t->dev.shift = t->shift;
+  t->dev.npayload = 1;  // CSR payload = build-row index
+  t->dev.payload[0] = t->rowidx.as<uint64_t>();
+  PSG_CUDA(cudaStreamSynchronize(ctx.compute));
+  return t.release();
+}
+
+void op_hashtable_free(GpuHashTable* t) { delete t; }
+const HostBatch& op_hashtable_host(const GpuHashTable& t) { return t.host; }
+
+std::vector<uint64_t> op_hashtable_lookup(Ctx& ctx, const GpuHashTable& t, const std::vector<int64_t>& keys,
+                                          std::vector<uint64_t>& offsets) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  const uint64_t n = keys.size();
+  DevBuf dk(ctx.pool, std::max<uint64_t>(n, 1) * 8, ctx.compute);
+  if (n) PSG_CUDA(cudaMemcpyAsync(dk.p, keys.data(), n * 8, cudaMemcpyHostToDevice, ctx.compute));
+  DevBuf offs, rows;
+  const uint64_t total = t.rows ? expand_rows(ctx, t, dk.as<uint64_t>(), n, offs, rows) : 0;
+  offsets.assign(n + 1, 0);
+  if (t.rows) {
+    std::vector<uint32_t> o32(n + 1);
+    PSG_CUDA(cudaMemcpyAsync(o32.data(), offs.p, (n + 1) * 4, cudaMemcpyDeviceToHost, ctx.compute));
+    PSG_CUDA(cudaStreamSynchronize(ctx.compute));
+    for (uint64_t i = 0; i <= n; ++i) offsets[i] = o32[i];
+  }
+  std::vector<uint64_t> out = total ? download(ctx, rows, total) : std::vector<uint64_t>{};
+  PSG_CUDA(cudaStreamSynchronize(ctx.compute));
+  return out;
+}
+
+HostBatch op_hashtable_probe(Ctx& ctx, const GpuHashTable& t, const HostBatch& probe, const std::string& probe_key) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  check_batch(probe);
+  const size_t pk = probe.schema.require(probe_key);
+  if (probe.schema.fields[pk].type != LType::Int64) throw InvalidInput("probe key must be int64: " + probe_key);
+  // output schema: build payload ++ probe columns, "_p" on a name clash (ops.cpp:193-200)
+  HostBatch out;
+  out.schema = t.payload_schema;
   for (auto f : probe.schema.fields) {
     if (out.schema.index_of(f.name)) f.name += "_p";
     out.schema.fields.push_back(f);
   }
-  const int np = static_cast<int>(build.schema.size()) - 1, nq = static_cast<int>(probe.schema.size());
+  const int np = static_cast<int>(t.payload_schema.size()), nq = static_cast<int>(probe.schema.size());
   out.cols.resize(np + nq);
-  const uint64_t nb = build.rows(), npr = probe.rows();
-  if (nb == 0 || npr == 0) return out;
-  Uploaded ub = upload(ctx, build), up = upload(ctx, probe);
-  const uint64_t cap = [&] {
-    uint64_t c = 16;
-    while (c < 2 * nb) c <<= 1;
-    return c;
-  }();
-  DevBuf keys(ctx.pool, cap * 8, ctx.compute), cnt(ctx.pool, (cap + 1) * 4, ctx.compute),
-      start(ctx.pool, (cap + 1) * 4, ctx.compute), cursor(ctx.pool, (cap + 1) * 4, ctx.compute),
-      maxc(ctx.pool, 4, ctx.compute);
-  PSG_CUDA(cudaMemsetAsync(cursor.p, 0, (cap + 1) * 4, ctx.compute));
-  PSG_CUDA(cudaMemsetAsync(maxc.p, 0, 4, ctx.compute));
-  launch_local_init(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap, ctx.compute);
-  int shift = 64;
-  for (uint64_t c = cap; c > 1; c >>= 1) --shift;
-  launch_local_count(keys.as<uint64_t>(), cnt.as<uint32_t>(), cap - 1, shift, ub.cols[bk].as<uint64_t>(), nb, maxc.as<unsigned>(),
-                     ctx.compute);
-  size_t tb = exclusive_scan_u32(nullptr, nullptr, cap + 1, nullptr, 0, ctx.compute);
-  DevBuf tmp(ctx.pool, tb, ctx.compute);
-  exclusive_scan_u32(cnt.as<uint32_t>(), start.as<uint32_t>(), cap + 1, tmp.p, tb, ctx.compute);
-  std::vector<DevBuf> payload;
-  std::vector<const uint64_t*> src;
-  std::vector<uint64_t*> dst;
-  for (size_t c = 0; c < build.schema.size(); ++c) {
-    if (c == bk) continue;
-    payload.emplace_back(ctx.pool, nb * 8, ctx.compute);
-    src.push_back(ub.cols[c].as<uint64_t>());
-    dst.push_back(payload.back().as<uint64_t>());
-  }
-  launch_local_fill(keys.as<uint64_t>(), start.as<uint32_t>(), cursor.as<uint32_t>(), cap - 1, shift, ub.cols[bk].as<uint64_t>(),
-                    src.data(), dst.data(), np, nb, ctx.compute);
-  LocalTableDev t{};
-  t.keys = keys.as<uint64_t>();
-  t.cnt = cnt.as<uint32_t>();
-  t.start = start.as<uint32_t>();
-  t.mask = cap - 1;
-  t.shift = shift;
-  t.npayload = np;
-  for (int k = 0; k < np; ++k) t.payload[k] = payload[k].as<uint64_t>();
-  DevBuf counts(ctx.pool, (npr + 1) * 4, ctx.compute), offs(ctx.pool, (npr + 1) * 4, ctx.compute);
-  PSG_CUDA(cudaMemsetAsync(counts.p, 0, (npr + 1) * 4, ctx.compute));
-  launch_expand_count(t, up.cols[pk].as<uint64_t>(), npr, counts.as<uint32_t>(), ctx.compute);
-  size_t tb2 = exclusive_scan_u32(nullptr, nullptr, npr + 1, nullptr, 0, ctx.compute);
-  DevBuf tmp2(ctx.pool, tb2, ctx.compute);
-  exclusive_scan_u32(counts.as<uint32_t>(), offs.as<uint32_t>(), npr + 1, tmp2.p, tb2, ctx.compute);
-  uint32_t total = 0;
-  PSG_CUDA(cudaMemcpyAsync(&total, offs.as<uint32_t>() + npr, 4, cudaMemcpyDeviceToHost, ctx.compute));
-  PSG_CUDA(cudaStreamSynchronize(ctx.compute));
+  const uint64_t npr = probe.rows();
+  if (t.rows == 0 || npr == 0) return out;
+  Uploaded up = upload(ctx, probe);
+  DevBuf offs, rows;
+  const uint64_t total = expand_rows(ctx, t, up.cols[pk].as<uint64_t>(), npr, offs, rows);
+  if (total == 0) return out;
+  // probe side: each probe row repeated per match (expand_write with the probe columns)
   std::vector<DevBuf> oc;
-  std::vector<const uint64_t*> pcols;
   std::vector<uint64_t*> ocols;
+  std::vector<const uint64_t*> pcols;
   for (int q = 0; q < nq; ++q) pcols.push_back(up.cols[q].as<uint64_t>());
-  for (int c = 0; c < np + nq; ++c) {
-    oc.emplace_back(ctx.pool, std::max<uint64_t>(total, 1) * 8, ctx.compute);
+  DevBuf scratch(ctx.pool, total * 8, ctx.compute);
+  ocols.push_back(scratch.as<uint64_t>());  // build-row indices again (payload 0)
+  for (int q = 0; q < nq; ++q) {
+    oc.emplace_back(ctx.pool, total * 8, ctx.compute);
     ocols.push_back(oc.back().as<uint64_t>());
   }
-  launch_expand_write(t, up.cols[pk].as<uint64_t>(), npr, offs.as<uint32_t>(), pcols.data(), nq, ocols.data(), ctx.compute);
-  for (int c = 0; c < np + nq; ++c) out.cols[c] = download(ctx, oc[c], total);
+  launch_expand_write(t.dev, up.cols[pk].as<uint64_t>(), npr, offs.as<uint32_t>(), pcols.data(), nq, ocols.data(),
+                      ctx.compute);
+  // build payload gathered by row index
+  std::vector<DevBuf> bc;
+  std::vector<const uint64_t*> bsrc;
+  std::vector<uint64_t*> bdst;
+  for (size_t c = 0; c < t.schema.size(); ++c) {
+    if (c == t.key) continue;
+    bc.emplace_back(ctx.pool, total * 8, ctx.compute);
+    bsrc.push_back(t.cols[c].as<uint64_t>());
+    bdst.push_back(bc.back().as<uint64_t>());
+  }
+  for (size_t c0 = 0; c0 < bsrc.size(); c0 += kMaxIn)
+    launch_gather64(bsrc.data() + c0, static_cast<int>(std::min<size_t>(kMaxIn, bsrc.size() - c0)),
+                    scratch.as<uint64_t>(), total, bdst.data() + c0, ctx.compute);
+  for (int c = 0; c < np; ++c) out.cols[c] = download(ctx, bc[c], total);
+  for (int q = 0; q < nq; ++q) out.cols[np + q] = download(ctx, oc[q], total);
+  PSG_CUDA(cudaStreamSynchronize(ctx.compute));
+  return out;
+}
+
+HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& build_key, const HostBatch& probe,
+                       const std::string& probe_key) {
+  std::unique_ptr<GpuHashTable> t(op_hashtable_build(ctx, {build}, build_key));
+  return op_hashtable_probe(ctx, *t, probe, probe_key);
+}
+
+/// concat (ops.cpp:80-98): batches of one schema into one batch, assembled in HBM by the copy
+/// engine (one D2D copy per input column) and returned.
+HostBatch op_concat(Ctx& ctx, const std::vector<HostBatch>& batches) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  if (batches.empty()) throw InvalidInput("concat needs at least one batch");
+  const Schema& sc = batches[0].schema;
+  uint64_t total = 0;
+  for (const auto& b : batches) {
+    check_batch(b);
+    bool same = b.schema.size() == sc.size();
+    for (size_t c = 0; same && c < sc.size(); ++c)
+      same = b.schema.fields[c].name == sc.fields[c].name && b.schema.fields[c].type == sc.fields[c].type;
+    if (!same) throw InvalidInput("concat: batches have different schemas");
+    total += b.rows();
+  }
+  HostBatch out;
+  out.schema = sc;
+  out.cols.resize(sc.size());
+  std::vector<DevBuf> dcols;
+  for (size_t c = 0; c < sc.size(); ++c) dcols.emplace_back(ctx.pool, std::max<uint64_t>(total, 1) * 8, ctx.compute);
+  uint64_t at = 0;
+  for (const auto& b : batches) {
+    const uint64_t n = b.rows();
+    for (size_t c = 0; c < sc.size() && n; ++c)
+      PSG_CUDA(cudaMemcpyAsync(dcols[c].as<uint8_t>() + at * 8, b.cols[c].data(), n * 8, cudaMemcpyHostToDevice,
+                               ctx.compute));
+    at += n;
+  }
+  for (size_t c = 0; c < sc.size(); ++c) out.cols[c] = download(ctx, dcols[c], total);
   PSG_CUDA(cudaStreamSynchronize(ctx.compute));
   return out;
 }

@@ -92,3 +92,68 @@ def test_hash_join_sentinel_key(ctx):
     mn = np.iinfo(np.int64).min
     r = psg.hash_join({"k": [mn, mn, 3], "v": [1, 2, 3]}, "k", {"pk": [mn, 3, 4]}, "pk", ctx=ctx)
     assert sorted(map(tuple, r.rows.view(np.int64).tolist())) == [(1, mn), (2, mn), (3, 3)]
+
+
+# ---- HashTable handle + concat (ops.hpp:35-82; core_ops_test.cpp:123-202) ----
+def test_hashtable_lookup_payload_and_duplicates():
+    t = psg.HashTable.build([{"k": [1, 2, 3], "v": [10, 20, 30]}], "k")
+    rows = t.lookup(2)
+    assert len(rows) == 1 and t.payload_at(0, rows[0]) == 20 and t.key_at(rows[0]) == 2
+    dup = psg.HashTable.build([{"k": [5, 5, 6], "v": [1, 2, 3]}], "k")
+    assert sorted(dup.payload_at(0, r) for r in dup.lookup(5)) == [1, 2]
+    assert dup.lookup(7) == [] and dup.row_count() == 3
+
+
+def test_hashtable_matches_dict_oracle_on_20k_random_rows():
+    rng = np.random.default_rng(17)
+    k = rng.integers(0, 5000, 20000)
+    v = rng.integers(-1 << 40, 1 << 40, 20000)
+    # two build batches: row r of the materialised build side = r-th row of the concatenation
+    t = psg.HashTable.build([{"k": k[:7000], "v": v[:7000]}, {"k": k[7000:], "v": v[7000:]}], "k")
+    assert t.row_count() == 20000
+    oracle = {}
+    for r, key in enumerate(k.tolist()):
+        oracle.setdefault(key, []).append(r)
+    probes = rng.integers(-10, 5100, 3000).tolist()
+    got = t.lookup_many(probes)
+    for key, rows in zip(probes, got):
+        assert sorted(rows) == oracle.get(key, []), key
+    assert all(t.key_at(r) == k[r] for r in range(0, 20000, 997))
+
+
+def test_hashtable_probe_payload_then_probe_columns():
+    t = psg.HashTable.build([{"k": [1, 2, 2], "v": [100, 200, 300]}], "k")
+    res = t.probe({"pk": [2, 9], "x": [7, 8]}, "pk")
+    assert [n for n, _ in res.schema] == ["v", "pk", "x"]
+    assert sorted(map(tuple, res.rows.tolist())) == [(200, 2, 7), (300, 2, 7)]
+    assert t.probe({"pk": np.zeros(0, np.int64)}, "pk").rows.shape[0] == 0
+    assert t.probe({"pk": [42]}, "pk").rows.shape[0] == 0
+    clash = t.probe({"v": [5], "k2": [1]}, "k2")
+    assert [n for n, _ in clash.schema] == ["v", "v_p", "k2"]
+
+
+def test_hashtable_probe_agrees_with_nested_loop_oracle():
+    rng = np.random.default_rng(3)
+    bk, bv, bw = rng.integers(0, 300, 2000), rng.integers(0, 1 << 30, 2000), rng.normal(size=2000)
+    pk, px = rng.integers(0, 400, 3000), rng.integers(0, 99, 3000)
+    t = psg.HashTable.build([{"k": bk, "v": bv, "w": bw}], "k")
+    res = t.probe({"pk": pk, "x": px}, "pk")
+    want = []
+    by = {}
+    for i in range(len(bk)):
+        by.setdefault(int(bk[i]), []).append(i)
+    for j in range(len(pk)):
+        for i in by.get(int(pk[j]), []):
+            want.append((int(bv[i]), int(np.float64(bw[i]).view(np.uint64)), int(pk[j]), int(px[j])))
+    assert sorted(map(tuple, res.rows.tolist())) == sorted(want)
+
+
+def test_concat_and_schema_mismatch():
+    res = psg.concat([{"a": [1, 2], "b": [3.5, 4.5]}, {"a": [9], "b": [0.25]}])
+    assert res.rows[:, 0].tolist() == [1, 2, 9]
+    assert res.rows[:, 1].view(np.float64).tolist() == [3.5, 4.5, 0.25]
+    with pytest.raises(psg.PsgError) as e:
+        psg.concat([{"a": [1]}, {"b": [1]}])
+    assert e.value.kind == "InvalidInput"
+    with pytest.raises(psg.PsgError):
+        psg.HashTable.build([{"k": [1]}, {"k": [2.5]}], "k")
