@@ -214,6 +214,14 @@ int psg_psto_inspect(const char* path, uint64_t* rows, uint32_t* ncols, uint64_t
 int psg_gen_tpch(const char* out_dir, double scale, int nodes, int devices, uint64_t seed,
                  int codec, uint64_t row_group_bytes, int threads);
 
+/* gen_workload(kind = synthetic join) (bench.cpp:93-99, workload.cpp:27-71): build table
+ * {bk, bp0..} with keys 0..build_rows-1 shuffled, probe table {pk, pp0..} with hit_ratio of its
+ * keys in the build range; round-robin node shards dev{(k + i) % devices}/{build,probe}.node{k}.psto
+ * and manifest.json. Reference defaults: 120000, 320000, 3, 0.5. Byte-identical to the reference. */
+int psg_gen_synthetic(const char* out_dir, int nodes, int devices, uint64_t seed, int codec,
+                      uint64_t row_group_bytes, uint64_t build_rows, uint64_t probe_rows, int payload_cols,
+                      double hit_ratio);
+
 /* ---- query compiler self-test: NVRTC-compiles representative fused-scan programs for sm_100a
  * (no GPU needed). Returns the number of failing programs (0 = ok), -1 on error; log gets NVRTC
  * output for failures. */

@@ -35,7 +35,7 @@ EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_uniq
            "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_hashtable_build",
            "psg_hashtable_shape", "psg_hashtable_row", "psg_hashtable_lookup", "psg_hashtable_probe", "psg_hashtable_free",
            "psg_concat", "psg_codec_decompress", "psg_psto_write",
-           "psg_psto_inspect", "psg_gen_tpch", "psg_jit_selftest", "psg_tmin"]
+           "psg_psto_inspect", "psg_gen_tpch", "psg_gen_synthetic", "psg_jit_selftest", "psg_tmin"]
 
 
 class PsgError(RuntimeError):
@@ -111,6 +111,7 @@ def lib():
             "psg_psto_write": ([c, P(Batch), u64, i32, P(u64)], i32),
             "psg_psto_inspect": ([c, P(u64), P(ctypes.c_uint32), P(u64), P(i32)], i32),
             "psg_gen_tpch": ([c, ctypes.c_double, i32, i32, u64, i32, u64, i32], i32),
+            "psg_gen_synthetic": ([c, i32, i32, u64, i32, u64, u64, u64, i32, ctypes.c_double], i32),
             "psg_tmin": ([u64, ctypes.c_double, u64, ctypes.c_double], ctypes.c_double),
             "psg_jit_selftest": ([ctypes.c_char_p, ctypes.c_size_t], i32),
         }
@@ -385,13 +386,18 @@ def inspect(path):
 
 
 def gen_workload(kind, out_dir, devices=2, nodes=2, scale=0.01, seed=42, codec="block", row_group_bytes=1 << 20,
-                 threads=3):
+                 threads=3, build_rows=120_000, probe_rows=320_000, payload_cols=3, hit_ratio=0.5):
     """gen_workload(kind='tpch') (bench.cpp:85-114), byte-identical to the reference generator.
 
     Defaults mirror the reference's (bindings.cpp:180-193 + GenWorkloadSpec, bench.hpp:51): the zlib
-    block codec, whose chunks the GPU inflates in HBM; codec='identity' writes raw column chunks."""
-    if kind not in ("tpch", "tpch-analog"):
-        raise PsgError(9, "only the tpch-analog workload is generated by this build")
+    block codec, whose chunks the GPU inflates in HBM; codec='identity' writes raw column chunks.
+    kind='synthetic' writes the synthetic join tables (SyntheticJoinSpec defaults, workload.hpp:27-33);
+    any other kind is the TPC-H analog, as in the reference's binding."""
+    if kind == "synthetic":  # the reference's pybind maps any other kind to tpch (bindings.cpp:184)
+        _check(lib().psg_gen_synthetic(out_dir.encode(), int(nodes), int(devices), int(seed),
+                                       1 if codec == "block" else 0, int(row_group_bytes), int(build_rows),
+                                       int(probe_rows), int(payload_cols), float(hit_ratio)))
+        return os.path.join(out_dir, "manifest.json")
     _check(lib().psg_gen_tpch(out_dir.encode(), float(scale), int(nodes), int(devices), int(seed),
                               1 if codec == "block" else 0, int(row_group_bytes), int(threads)))
     return os.path.join(out_dir, "manifest.json")

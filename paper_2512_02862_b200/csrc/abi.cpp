@@ -405,6 +405,16 @@ int psg_gen_tpch(const char* out_dir, double scale, int nodes, int devices, uint
   });
 }
 
+int psg_gen_synthetic(const char* out_dir, int nodes, int devices, uint64_t seed, int codec, uint64_t row_group_bytes,
+                      uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio) {
+  return guarded([&] {
+    if (!out_dir) throw InvalidInput("null argument");
+    if (codec != 0 && codec != 1) throw InvalidInput("unknown codec");
+    gen_synthetic(out_dir, nodes, devices, seed, static_cast<Codec>(codec), row_group_bytes, build_rows, probe_rows,
+                  payload_cols, hit_ratio);
+  });
+}
+
 int psg_jit_selftest(char* log, size_t cap) {
   std::string l;
   int f = 0;

@@ -254,6 +254,8 @@ HostBatch op_concat(Ctx& ctx, const std::vector<HostBatch>& batches);
 HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& build_key, const HostBatch& probe,
                        const std::string& probe_key);
 
+void gen_synthetic(const std::string& out_dir, int nodes, int devices, uint64_t seed, Codec codec, uint64_t rg_bytes,
+                   uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio);
 void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, uint64_t seed, Codec codec,
               uint64_t rg_bytes, int threads);
 

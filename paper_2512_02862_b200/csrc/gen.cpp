@@ -12,6 +12,9 @@
 #include <functional>
 #include <memory>
 #include <mutex>
+#include <algorithm>
+#include <numeric>
+#include <random>
 #include <thread>
 #include <tuple>
 
@@ -270,6 +273,95 @@ void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, 
     m["tables"][name]["rows"] = rows;
     m["tables"][name]["paths_per_node"] = *paths;
   }
+  const std::string mpath = (fs::path(out_dir) / "manifest.json").string();
+  std::ofstream out(mpath);
+  if (!out) throw IoFailure("cannot write manifest: " + mpath);
+  out << m.dump(2) << '\n';
+}
+
+/// gen_workload(kind = synthetic join) (bench.cpp:93-99; gen_build_table / gen_probe_table,
+/// workload.cpp:41-71). The reference draws from std::mt19937_64 through std::shuffle and
+/// std::uniform_real_distribution; this file is built with the same C++ standard library, so the
+/// same calls in the same order give byte-identical tables (pinned against the reference's own
+/// generator, tests/test_abi.py). Tables are sliced round-robin per node (slice_for_node,
+/// workload.cpp:73-87) and written like write_sharded (bench.cpp:48-65).
+void gen_synthetic(const std::string& out_dir, int nodes, int devices, uint64_t seed, Codec codec, uint64_t rg_bytes,
+                   uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio) {
+  if (nodes < 1 || devices < 1) throw InvalidInput("devices and nodes must be >= 1");
+  if (payload_cols < 0 || payload_cols > 14) throw InvalidInput("payload_cols out of range");
+  namespace fs = std::filesystem;
+  fs::create_directories(out_dir);
+  const uint64_t mul = 2654435761u;
+  auto side = [&](const char* key, const char* pre) {
+    Schema sc;
+    sc.fields.push_back(Field{key, LType::Int64});
+    for (int i = 0; i < payload_cols; ++i) sc.fields.push_back(Field{pre + std::to_string(i), LType::Int64});
+    return sc;
+  };
+  auto payload = [&](std::mt19937_64& rng, uint64_t rows, std::vector<std::vector<uint64_t>>& cols) {
+    for (int c = 0; c < payload_cols; ++c) {
+      std::vector<uint64_t> v(rows);
+      for (auto& x : v) x = static_cast<uint64_t>(static_cast<int64_t>(rng() % 1'000'000'000));
+      cols.push_back(std::move(v));
+    }
+  };
+  // build side: keys 0..n-1 shuffled, then payload
+  std::vector<std::vector<uint64_t>> bcols;
+  {
+    std::mt19937_64 rng(seed * mul + 1);
+    std::vector<int64_t> keys(build_rows);
+    std::iota(keys.begin(), keys.end(), int64_t{0});
+    std::shuffle(keys.begin(), keys.end(), rng);
+    bcols.emplace_back(keys.begin(), keys.end());
+    payload(rng, build_rows, bcols);
+  }
+  // probe side: a hit_ratio share of keys drawn from the build range, the rest from a miss range
+  std::vector<std::vector<uint64_t>> pcols;
+  {
+    std::mt19937_64 rng(seed * mul + 2);
+    std::uniform_real_distribution<double> coin(0.0, 1.0);
+    std::vector<uint64_t> keys(probe_rows);
+    for (auto& k : keys) {
+      if (build_rows > 0 && coin(rng) < hit_ratio)
+        k = static_cast<uint64_t>(static_cast<int64_t>(rng() % build_rows));
+      else
+        k = static_cast<uint64_t>(static_cast<int64_t>(build_rows + rng() % 1'000'000'000ull));
+    }
+    pcols.push_back(std::move(keys));
+    payload(rng, probe_rows, pcols);
+  }
+  nlohmann::json m;
+  m["nodes"] = nodes;
+  m["devices"] = devices;
+  m["seed"] = seed;
+  m["kind"] = "synthetic-join";
+  m["hit_ratio"] = hit_ratio;
+  auto write_sharded = [&](const Schema& sc, const std::vector<std::vector<uint64_t>>& cols, uint64_t rows,
+                           const std::string& name, int file_index) {
+    nlohmann::json entry;
+    entry["replicated"] = false;
+    entry["rows"] = rows;
+    auto paths = nlohmann::json::array();
+    const uint64_t rg_rows = PstoWriter::rows_for_group_bytes(sc, rg_bytes);
+    for (int node = 0; node < nodes; ++node) {
+      const std::string dir = (fs::path(out_dir) / ("dev" + std::to_string((file_index + node) % devices))).string();
+      fs::create_directories(dir);
+      const std::string path = dir + "/" + name + ".node" + std::to_string(node) + ".psto";
+      std::vector<std::vector<uint64_t>> slice(cols.size());
+      for (size_t c = 0; c < cols.size(); ++c)
+        for (uint64_t r = static_cast<uint64_t>(node); r < rows; r += static_cast<uint64_t>(nodes)) slice[c].push_back(cols[c][r]);
+      PstoWriter w(path, sc, rg_rows, codec);
+      std::vector<const uint64_t*> ptrs;
+      for (auto& c : slice) ptrs.push_back(c.data());
+      if (!slice.empty() && !slice[0].empty()) w.append(ptrs.data(), slice[0].size());
+      w.finish();
+      paths.push_back(path);
+    }
+    entry["paths_per_node"] = paths;
+    return entry;
+  };
+  m["tables"]["build"] = write_sharded(side("bk", "bp"), bcols, build_rows, "build", 0);
+  m["tables"]["probe"] = write_sharded(side("pk", "pp"), pcols, probe_rows, "probe", 1);
   const std::string mpath = (fs::path(out_dir) / "manifest.json").string();
   std::ofstream out(mpath);
   if (!out) throw IoFailure("cannot write manifest: " + mpath);

@@ -98,6 +98,31 @@ def main():
                         flush=True)
                     if not ok:
                         failures.append((pname, mode, fused, semijoin, got, want))
+    # synthetic-join workload (gen_workload kind=synthetic): per-node rows vs the reference
+    syn = json.load(open(os.path.join(ROOT, "tests", "golden", "synthetic.json")))
+    sdir = os.path.join(base, "syn")
+    if rank == 0:
+        psg.gen_workload("synthetic", sdir, devices=world, nodes=world, seed=42, codec="identity")
+    dist.barrier()
+    for pname in ("syn_agg", "syn_global", "syn_filtered", "syn_noagg"):
+        res = ctx.execute_plan(syn["plans"][pname], sdir)
+        allres = [None] * world
+        dist.all_gather_object(allres, (res.schema, res.rows.copy()))
+        if rank == 0:
+            got = po.summary(allres)
+            g = [r for r in syn["results"] if r["plan"] == pname and r["nodes"] == world and r["seed"] == 42
+                 and r["codec"] == "identity"]
+            if g:
+                want = {k: g[0][k] for k in ("rows", "rowhash", "colsums", "per_node_rows")}
+                src = "reference"
+            else:
+                want = po.summary(po.execute(json.dumps(syn["plans"][pname]), sdir, world))
+                src = "oracle"
+            ok = all(got[k] == want[k] for k in ("rows", "rowhash", "colsums", "per_node_rows"))
+            print("%-22s synthetic  %-9s %s rows=%d per_node=%s" % (pname, src, "OK " if ok else "BAD", got["rows"],
+                                                                   got["per_node_rows"]), flush=True)
+            if not ok:
+                failures.append((pname, "synthetic", got, want))
     # local plans (no shuffle, psg_execute_local): one partial row per rank = per node
     local = json.load(open(os.path.join(ROOT, "tests", "golden", "local.json")))
     for pname in ("q6", "q6_count"):

@@ -109,3 +109,23 @@ def test_gen_workload_defaults_and_manifest_match_reference(tmp_path):
                         "--codec", "block"], check=True, capture_output=True)
         ref = open(os.path.join(r, "manifest.json")).read().replace(r, "ROOT")
         assert open(mpath).read().replace(d, "ROOT") == ref
+
+
+def test_synthetic_generator_matches_reference_bytes(tmp_path):
+    """gen_workload(kind='synthetic') is byte-identical to the reference's synthetic-join tables
+    (tests/golden/synthetic.json, made by the reference generator)."""
+    import json as _json
+    syn = _json.load(open(os.path.join(ROOT, "tests", "golden", "synthetic.json")))
+    for spec in syn["gen"]:
+        d = str(tmp_path / ("s%d" % spec["seed"]))
+        m = psg.gen_workload("synthetic", d, devices=spec["devices"], nodes=spec["nodes"], seed=spec["seed"],
+                             codec=spec["codec"])
+        got = {}
+        for root, _dirs, files in os.walk(d):
+            for f in files:
+                if f.endswith(".psto"):
+                    p = os.path.join(root, f)
+                    got[os.path.relpath(p, d)] = hashlib.sha256(open(p, "rb").read()).hexdigest()
+        assert got == spec["files"]
+        man = _json.load(open(m))
+        assert man["kind"] == "synthetic-join" and man["tables"]["build"]["rows"] == 120000

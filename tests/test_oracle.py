@@ -101,3 +101,22 @@ def test_oracle_local_plans_match_reference_scan(tmp_path):
                 assert s["colsums"] == want["colsums"] and s["rowhash"] == want["rowhash"], (r["case"], k)
         n += 1
     assert n >= 6
+
+
+def test_oracle_synthetic_join_plans_match_reference(tmp_path):
+    """The oracle's executor restatement on the synthetic-join tables (all plan shapes: grouped
+    with build-side sums, global, no aggregate, build+probe predicates) against the reference's
+    own results (tests/golden/synthetic.json)."""
+    import json as _json
+    import paper_2512_02862_b200 as psg  # the generator only (byte-identical, test_abi.py)
+    syn = _json.load(open(os.path.join(os.path.dirname(__file__), "golden", "synthetic.json")))
+    seen = set()
+    for r in syn["results"]:
+        if r["case"] in seen:
+            continue
+        seen.add(r["case"])
+        d = str(tmp_path / r["case"])
+        psg.gen_workload("synthetic", d, devices=r["devices"], nodes=r["nodes"], seed=r["seed"], codec=r["codec"])
+        got = po.summary(po.execute(_json.dumps(syn["plans"][r["plan"]]), d, r["nodes"]))
+        assert (got["rows"], got["rowhash"], got["colsums"], got["per_node_rows"]) == \
+            (r["rows"], r["rowhash"], r["colsums"], r["per_node_rows"]), r["case"]
