@@ -64,6 +64,11 @@ struct LocalTableDev {
   const uint64_t* payload[kMaxPayload];  // CSR-ordered payload columns (needed ones only)
   int32_t npayload;
   int32_t shift;  // 64 - log2(cap)
+  // Dense unique keys with no payload needed (a semi-join, e.g. customer(seg) in Q3): membership
+  // bitmap over [bmin, bmin + brange) instead of the hash table (bitmap != nullptr).
+  const uint32_t* bitmap;
+  int64_t bmin;
+  uint64_t brange;
 };
 
 struct JoinDesc {
@@ -287,7 +292,12 @@ __device__ __forceinline__ uint64_t agg_lookup(const AggTableDev& t, uint64_t ke
   return agg_lookup_from(t, key, s, t.hot[s * t.hw]);
 }
 
+__device__ __forceinline__ bool local_bitmap_has(const LocalTableDev& t, uint64_t key) {
+  const uint64_t d = key - static_cast<uint64_t>(t.bmin);
+  return d < t.brange && ((__ldg(t.bitmap + (d >> 5)) >> (d & 31)) & 1u);
+}
 __device__ __forceinline__ uint64_t local_lookup(const LocalTableDev& t, uint64_t key) {
+  if (t.bitmap) return local_bitmap_has(t, key) ? 0 : ~0ULL;  // no payload in bitmap mode
   if (key == kEmptyKey) return t.cnt[t.mask + 1] > 0 ? t.mask + 1 : ~0ULL;
   uint64_t s = slot_of(key, t.shift);
   while (true) {

@@ -21,6 +21,7 @@
 #include <functional>
 #include <numeric>
 #include <cstdio>
+#include <climits>
 #include <cstdlib>
 #include <deque>
 #include <set>
@@ -492,7 +493,7 @@ class Execution {
   Schema result_schema_;
   // local tables
   struct LocalTable {
-    DevBuf keys, cnt, start;
+    DevBuf keys, cnt, start, bitmap;
     std::vector<DevBuf> payload;
     uint64_t cap = 0;
     bool unique = true;
@@ -940,6 +941,15 @@ BatchView Execution::upload_segments(std::vector<Segment> segs, DevBuf& holder) 
 }
 
 // ---------------------------------------------------------------------- local join tables
+/// PSG_LOCAL_BITMAP=0 disables the dense semi-join bitmap for local joins (A/B measurements).
+static bool bitmap_env() {
+  static const bool on = [] {
+    const char* e = std::getenv("PSG_LOCAL_BITMAP");
+    return !(e && std::string(e) == "0");
+  }();
+  return on;
+}
+
 void Execution::build_local_tables() {
   for (int side = 0; side < 2; ++side) {
     SourceDef& s = side == 0 ? bsrc_ : psrc_;
@@ -975,6 +985,42 @@ void Execution::build_local_tables() {
         st_.ingest_bytes += v.bytes;
       }
       const uint64_t n = read_count(mat);
+      const int np = static_cast<int>(lj.needed_payload.size());
+      // Semi-join fast path: no payload needed and the keys are unique and dense -> a membership
+      // bitmap over [min, max] (Q3's 3 M customer keys in 15 M: 1.9 MB, L2-resident) replaces the
+      // hash table; probes become one cached bit test.
+      if (np == 0 && n > 0 && bitmap_env()) {
+        DevBuf mm(ctx_.pool, 16, ctx_.compute);
+        const long long init[2] = {LLONG_MAX, LLONG_MIN};
+        PSG_CUDA(cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, ctx_.compute));
+        launch_minmax_i64(mat.cols[0].as<uint64_t>(), n, mm.as<long long>(), ctx_.compute);
+        long long lohi[2];
+        PSG_CUDA(cudaMemcpyAsync(lohi, mm.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+        PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+        const uint64_t range = static_cast<uint64_t>(lohi[1]) - static_cast<uint64_t>(lohi[0]) + 1;
+        if (range != 0 && range <= (1ULL << 34) && range / 64 <= n) {
+          const uint64_t words = (range + 31) / 32;
+          t->bitmap = DevBuf(ctx_.pool, words * 4, ctx_.compute);
+          DevBuf dup(ctx_.pool, 4, ctx_.compute);
+          PSG_CUDA(cudaMemsetAsync(t->bitmap.p, 0, words * 4, ctx_.compute));
+          PSG_CUDA(cudaMemsetAsync(dup.p, 0, 4, ctx_.compute));
+          launch_bitmap_set(mat.cols[0].as<uint64_t>(), n, lohi[0], t->bitmap.as<uint32_t>(), dup.as<unsigned int>(),
+                            ctx_.compute);
+          unsigned int d = 0;
+          PSG_CUDA(cudaMemcpyAsync(&d, dup.p, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+          PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+          if (!d) {  // unique: bitmap mode
+            t->unique = true;
+            std::memset(&t->dev, 0, sizeof t->dev);
+            t->dev.bitmap = t->bitmap.as<uint32_t>();
+            t->dev.bmin = lohi[0];
+            t->dev.brange = range;
+            tables.push_back(std::move(t));
+            continue;
+          }
+          t->bitmap.reset();
+        }
+      }
       // CSR hash table
       t->cap = pow2_at_least(std::max<uint64_t>(2 * n, 16));
       t->keys = DevBuf(ctx_.pool, t->cap * 8, ctx_.compute);
@@ -991,7 +1037,6 @@ void Execution::build_local_tables() {
       size_t tb = exclusive_scan_u32(nullptr, nullptr, t->cap + 1, nullptr, 0, ctx_.compute);
       DevBuf tmp(ctx_.pool, tb, ctx_.compute);
       exclusive_scan_u32(t->cnt.as<uint32_t>(), t->start.as<uint32_t>(), t->cap + 1, tmp.p, tb, ctx_.compute);
-      const int np = static_cast<int>(lj.needed_payload.size());
       std::vector<const uint64_t*> src;
       std::vector<uint64_t*> dst;
       for (int k = 0; k < np; ++k) {

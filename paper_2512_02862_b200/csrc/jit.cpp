@@ -223,6 +223,12 @@ std::string jit_source(const ScanProgram& P) {
   // Phase C: unique-key local joins (two-stage probe: home-slot loads for all rows first)
   for (int j = 0; j < P.n_joins; ++j) {
     const JoinDesc& jd = P.joins[j];
+    if (jd.t.bitmap != nullptr) {  // dense unique keys, no payload: membership bitmap (L2-resident)
+      s << "    { const LocalTableDev& T = P.joins[" << j << "].t;\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && !local_bitmap_has(T, " << V(jd.key_reg)
+        << "[r])) pass &= ~(1u << r);\n    }\n";
+      continue;
+    }
     s << "    { const LocalTableDev& T = P.joins[" << j << "].t;\n      uint64_t sl[R], k0[R];\n"
       << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = ~0ULL; k0[r] = 0; if (pass & (1u << r)) {\n"
       << "        const uint64_t key = " << V(jd.key_reg) << "[r];\n"
@@ -580,6 +586,10 @@ int jit_selftest(std::string& log) {
     p.n_out = 2;
     p.out_reg[0] = 2, p.out_reg[1] = 4;
     p.tile_offsets = reinterpret_cast<const uint64_t*>(16);
+    progs.push_back(p);
+    p.joins[0].t.npayload = 0;  // semi-join through a membership bitmap
+    p.joins[0].t.bitmap = reinterpret_cast<const uint32_t*>(16);
+    p.out_reg[1] = 2;
     progs.push_back(p);
   }
   for (int sink : {SINK_BUILD, SINK_PROBE}) {

@@ -18,6 +18,7 @@
 #include <cub/cub.cuh>
 
 #include <atomic>
+#include <climits>
 #include <cstdio>
 
 #include "kernels.cuh"
@@ -673,6 +674,44 @@ void launch_gather64(const uint64_t* const* in_cols, int ncols, const uint64_t* 
   }
   count_launch();
   k_gather64<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, ncols, idx, n, oc);
+}
+
+/// out[0] = min, out[1] = max of n signed keys (out preset to {INT64_MAX, INT64_MIN}).
+__global__ void k_minmax_i64(const uint64_t* keys, uint64_t n, long long* out) {
+  long long lo = LLONG_MAX, hi = LLONG_MIN;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const long long k = static_cast<long long>(keys[i]);
+    lo = min(lo, k);
+    hi = max(hi, k);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(out, lo);
+    atomicMax(out + 1, hi);
+  }
+}
+void launch_minmax_i64(const uint64_t* keys, uint64_t n, long long* out, void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_minmax_i64<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, n, out);
+}
+/// Membership bitmap of keys - bmin; *dup = 1 when a key repeats.
+__global__ void k_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uint32_t* bitmap, unsigned int* dup) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t d = keys[i] - static_cast<uint64_t>(bmin);
+    const uint32_t bit = 1u << (d & 31);
+    if (atomicOr(bitmap + (d >> 5), bit) & bit) *dup = 1u;
+  }
+}
+void launch_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uint32_t* bitmap, unsigned int* dup, void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_bitmap_set<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, n, bmin, bitmap, dup);
 }
 
 // --------------------------------------------------------------------------- result emission
