@@ -144,6 +144,14 @@ struct ScanProgram {
   // materialised or shuffled - only rows owned by other ranks leave the kernel.
   int32_t self_probe;
   int32_t self_rank;
+  // Bit-packed shuffle rows: MATERIALIZE with pack_n > 0 writes ONE word per row (out column 0),
+  // sum_k (reg[pack_reg[k]] - pack_min[k]) << pack_shift[k]; a program with unpack_n > 0 first
+  // expands register 0 into registers 1..unpack_n (value = pack_min + (w >> shift & mask)).
+  int32_t pack_n, unpack_n;
+  int32_t pack_reg[kMaxOut];
+  int32_t pack_shift[kMaxOut];
+  int64_t pack_min[kMaxOut];
+  uint64_t pack_mask[kMaxOut];
   // Fused NVLink path (SINK_BUILD / SINK_PROBE with remote = 1): every row's table operation goes
   // to the owner rank part_of(key) directly in its (peer-mapped) table; tables are symmetric so
   // mask/shift/hw/cw come from `agg`, only the base pointers differ per rank.

@@ -471,7 +471,8 @@ class Execution {
     std::vector<Segment> segs;  // host descriptors
     uint64_t rows = 0;
   };
-  Received exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data);
+  Received exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data,
+                    KeyField kf = KeyField{0, 0, 0});
   BatchView upload_segments(std::vector<Segment> segs, DevBuf& holder);
 
   void build_agg_table(uint64_t build_rows, uint64_t bloom_words);
@@ -1139,7 +1140,8 @@ void Execution::gpu_barrier() {
 }
 
 // ---------------------------------------------------------------------------- shuffle
-Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data) {
+Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data,
+                                        KeyField kf) {
   const int n = ctx_.nranks;
   Received rcv;
   // dest bases (exclusive scan of the per-destination histogram) and scatter into send regions
@@ -1164,7 +1166,7 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
     for (int c = 0; c < ncols; ++c) in.push_back(mat.cols[c].as<uint64_t>());
     launch_part_scatter(in.data(), ncols, nrows, key_col, n, base.as<unsigned long long>(),
                         part_counts.as<unsigned long long>(), cursor.as<unsigned long long>(), send.as<uint64_t>(),
-                        ctx_.compute);
+                        ctx_.compute, kf);
   }
   uint64_t rtotal = 0;
   for (int s = 0; s < n; ++s) rtotal += m[static_cast<size_t>(s) * n + me];
@@ -1557,8 +1559,9 @@ ResultRows Execution::run(bool want_rows) {
   }
   auto pfeed = open_feed(*psrc_.scan, file_cols_of(psrc_, pm));
   std::vector<DevCols> joined_parts;  // no-aggregate results
+  ScanProgram pack{};  // bit-packed shuffle rows (pack_n > 0), set up below
   auto consume_materialised = [&](const BatchView& v, int ncols) {
-    // v: segments whose columns are p_out order (key first)
+    // v: segments whose columns are p_out order (key first), or one bit-packed word per row
     if (agg_) {
       ScanProgram p = batch_program(ncols);
       p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
@@ -1567,6 +1570,17 @@ ResultRows Execution::run(bool want_rows) {
       p.key_reg = 0;
       p.n_sum = static_cast<int>(probe_sum_wire.size());
       for (int s = 0; s < p.n_sum; ++s) p.sum_reg[s] = 1 + s;
+      if (pack.pack_n) {  // unpack register 0 into 1..n: key, sums
+        p.unpack_n = pack.pack_n;
+        for (int k = 0; k < pack.pack_n; ++k) {
+          p.pack_min[k] = pack.pack_min[k];
+          p.pack_shift[k] = pack.pack_shift[k];
+          p.pack_mask[k] = pack.pack_mask[k];
+        }
+        p.n_regs = 1 + pack.pack_n;
+        p.key_reg = 1;
+        for (int s = 0; s < p.n_sum; ++s) p.sum_reg[s] = 2 + s;
+      }
       if (!grouped_) {
         p.global_acc = global_acc_.as<unsigned long long>();
         for (int s = 0; s < p.n_sum; ++s) p.global_float[1 + s] = aggt_.ps_float[s];
@@ -1655,14 +1669,78 @@ ResultRows Execution::run(bool want_rows) {
       PSG_CUDA(cudaMemcpyAsync(&waves, wv.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
     }
-    // Rows this rank owns are probed and aggregated in place by the partitioning scan itself:
-    // only rows owned by other ranks are materialised and shuffled (1/N of the traffic and of
-    // the consume work disappears). PSG_SELF_PROBE=0 turns it off (A/B measurements).
+    // Bit-packed shuffle rows: the footer zone maps bound every shipped column; with the ranges
+    // all-reduced (every rank packs and unpacks alike) a row whose fields fit in 64 bits travels
+    // as ONE word (Q3: key 28 + price 17 + discount 4 bits instead of 3 x 64). PSG_PACK=0: off.
+    static const bool pack_env = [] {
+      const char* e = std::getenv("PSG_PACK");
+      return !(e && std::string(e) == "0");
+    }();
+    if (nr > 1 && agg_ && jit_available() && pack_env && pneed.size() <= static_cast<size_t>(kMaxOut)) {
+      const size_t np = pneed.size();
+      std::vector<long long> lohi(2 * np);
+      for (size_t k = 0; k < np; ++k) {
+        long long lo = LLONG_MAX, hi = LLONG_MIN;
+        const ColRef ref = psrc_.stage_refs.back()[pneed[k]];
+        if (ref.join >= 0 || psrc_.wire.fields[pneed[k]].type != LType::Int64) {
+          lo = LLONG_MIN, hi = LLONG_MAX;  // not bounded by this scan's zone maps: never fits
+        } else {
+          const int fcol = psrc_.proj.file_idx[ref.idx];
+          for (const auto& path : psrc_.scan->paths) {
+            auto meta = ctx_.footers.get(path);
+            for (const auto& g : meta->groups) {
+              if (!g.rows) continue;
+              lo = std::min(lo, static_cast<long long>(g.cols[fcol].min_raw));
+              hi = std::max(hi, static_cast<long long>(g.cols[fcol].max_raw));
+            }
+          }
+        }
+        lohi[k] = ~lo;  // one MAX all-reduce for both: max(~lo) = ~min(lo)
+        lohi[np + k] = hi;
+      }
+      DevBuf red(ctx_.pool, 2 * np * 8, ctx_.compute);
+      PSG_CUDA(cudaMemcpyAsync(red.p, lohi.data(), 2 * np * 8, cudaMemcpyHostToDevice, ctx_.compute));
+      PSG_NCCL(ncclAllReduce(red.p, red.p, 2 * np, ncclInt64, ncclMax, ctx_.nccl, ctx_.compute));
+      PSG_CUDA(cudaMemcpyAsync(lohi.data(), red.p, 2 * np * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      int bits = 0;
+      bool fits = true;
+      for (size_t k = 0; k < np && fits; ++k) {
+        const long long lo = ~lohi[k], hi = lohi[np + k];
+        if (hi < lo) {  // no rows anywhere
+          pack.pack_min[k] = 0, pack.pack_mask[k] = 0, pack.pack_shift[k] = bits;
+          if (k == 0) fits = false;
+          continue;
+        }
+        const uint64_t span = static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo);
+        const int b = span ? 64 - __builtin_clzll(span) : 0;
+        if (bits + b > 64 || (k == 0 && b == 0)) fits = false;  // the key must be a real field
+        pack.pack_min[k] = lo;
+        pack.pack_shift[k] = bits;
+        pack.pack_mask[k] = b == 64 ? ~0ULL : ((1ULL << b) - 1);
+        bits += b;
+      }
+      if (fits && np > 1) {
+        pack.pack_n = static_cast<int>(np);
+        pp.pack_n = pack.pack_n;
+        for (size_t k = 0; k < np; ++k) {
+          pp.pack_reg[k] = p_out[k];
+          pp.pack_min[k] = pack.pack_min[k];
+          pp.pack_shift[k] = pack.pack_shift[k];
+          pp.pack_mask[k] = pack.pack_mask[k];
+        }
+      }
+    }
+    // When rows cannot be packed, the rows this rank owns are probed and aggregated in place by
+    // the partitioning scan itself: only rows owned by other ranks are materialised and shuffled.
+    // (Measured at N=2: packing alone 6.39 ms, owner probe alone 6.62, both 6.98, neither 6.86 -
+    // the in-kernel probe slows the scan more than it saves once rows are one word.)
+    // PSG_SELF_PROBE=0 turns it off (A/B measurements).
     static const bool self_probe_env = [] {
       const char* e = std::getenv("PSG_SELF_PROBE");
       return !(e && std::string(e) == "0");
     }();
-    if (nr > 1 && agg_ && grouped_ && jit_available() && self_probe_env) {
+    if (nr > 1 && agg_ && grouped_ && jit_available() && self_probe_env && pack.pack_n == 0) {
       pp.self_probe = 1;
       pp.self_rank = ctx_.rank;
       pp.agg = aggt_;
@@ -1671,24 +1749,26 @@ ResultRows Execution::run(bool want_rows) {
       pp.n_sum = static_cast<int>(probe_sum_wire.size());
       for (int k = 0; k < pp.n_sum; ++k) pp.sum_reg[k] = p_out[1 + k];
     }
+    const std::vector<int> mat_out = pack.pack_n ? std::vector<int>{p_out[0]} : p_out;
+    const KeyField kf = pack.pack_n ? KeyField{pack.pack_min[0], pack.pack_mask[0], 0} : KeyField{0, 0, 0};
     for (uint64_t w = 0; w < waves; ++w) {
       BatchView v;
       const bool have = pfeed->next(v);
-      DevCols mat = alloc_cols(p_out.size(), std::max<uint64_t>(have ? v.rows : 1, 1));
+      DevCols mat = alloc_cols(mat_out.size(), std::max<uint64_t>(have ? v.rows : 1, 1));
       DevBuf pc(ctx_.pool, nr * 8, ctx_.compute);
       PSG_CUDA(cudaMemsetAsync(pc.p, 0, nr * 8, ctx_.compute));
       if (have) {
-        materialize_into(mat, pp, v, p_out, p_out[0], &pc, staged_ != nullptr);
+        materialize_into(mat, pp, v, mat_out, p_out[0], &pc, staged_ != nullptr);
         pfeed->done();
         st_.ingest_bytes += v.bytes;
       }
       pt.mark("  probe materialize", ctx_.compute);
       if (nr > 1) {
-        Received r = exchange(mat, static_cast<int>(p_out.size()), 0, pc, have);
+        Received r = exchange(mat, static_cast<int>(mat_out.size()), 0, pc, have, kf);
         DevBuf holder;
         BatchView rv = upload_segments(r.segs, holder);
         pt.mark("  probe exchange", ctx_.compute);
-        consume_materialised(rv, static_cast<int>(p_out.size()));
+        consume_materialised(rv, static_cast<int>(mat_out.size()));
         PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
         pt.mark("  probe consume", ctx_.compute);
       } else {

@@ -147,6 +147,19 @@ void emit_remote_probe(std::ostringstream& s, const ScanProgram& P) {
 
 }  // namespace
 
+/// Value written to materialised output column o of row r: the register, or with pack_n > 0
+/// (one output column) the bit-packed word of the pack registers.
+std::string out_value(const ScanProgram& P, int o) {
+  if (P.pack_n == 0) return V(P.out_reg[o]) + "[r]";
+  std::string e;
+  for (int k = 0; k < P.pack_n; ++k) {
+    if (k) e += " | ";
+    e += "((" + V(P.pack_reg[k]) + "[r] - static_cast<uint64_t>(P.pack_min[" + std::to_string(k) + "])) << P.pack_shift[" +
+         std::to_string(k) + "])";
+  }
+  return "(" + e + ")";
+}
+
 std::string jit_source(const ScanProgram& P) {
   std::ostringstream s;
   const int nin = P.n_in, nregs = std::max(1, P.n_regs);
@@ -220,6 +233,9 @@ std::string jit_source(const ScanProgram& P) {
   }
   // Phase B: early columns
   emit_loads(s, P.n_pred, P.n_early);
+  for (int k = 0; k < P.unpack_n; ++k)  // bit-packed shuffle rows: register 0 -> 1..unpack_n
+    s << "#pragma unroll\n    for (int r = 0; r < R; ++r) " << V(1 + k) << "[r] = static_cast<uint64_t>(P.pack_min[" << k
+      << "]) + ((" << V(0) << "[r] >> P.pack_shift[" << k << "]) & P.pack_mask[" << k << "]);\n";
   // Phase C: unique-key local joins (two-stage probe: home-slot loads for all rows first)
   for (int j = 0; j < P.n_joins; ++j) {
     const JoinDesc& jd = P.joins[j];
@@ -375,7 +391,7 @@ std::string jit_source(const ScanProgram& P) {
           << "        const int cnt = __popc(b);\n        if (fill + cnt > 128) flush();\n"
           << "        if ((pass >> r) & 1u) { const int pos = fill + __popc(b & lt);\n";
         for (int o = 0; o < P.n_out; ++o)
-          s << "          s_stg[warp][" << o << "][pos] = " << V(P.out_reg[o]) << "[r];\n";
+          s << "          s_stg[warp][" << o << "][pos] = " << out_value(P, o) << ";\n";
         s << "        }\n        fill += cnt;\n      }\n    }\n";
       } else {
       s << "    uint32_t ballots[R];\n#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
@@ -394,7 +410,7 @@ std::string jit_source(const ScanProgram& P) {
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!((pass >> r) & 1u)) continue;\n"
           << "        const uint64_t pos = base + s_woff[warp][r] + __popc(ballots[r] & lt);\n"
           << "        if (pos >= P.out_cap) continue;\n";
-        for (int o = 0; o < P.n_out; ++o) s << "        P.out_col[" << o << "][pos] = " << V(P.out_reg[o]) << "[r];\n";
+        for (int o = 0; o < P.n_out; ++o) s << "        P.out_col[" << o << "][pos] = " << out_value(P, o) << ";\n";
         s << "      }\n    }\n";
       }
       }
@@ -481,6 +497,12 @@ Compiled compile(const std::string& body, int device) {
   }
   c.per_sm = per_sm;
   c.ok = true;
+  if (std::getenv("PSG_TRACE")) {
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(c.kern));
+    std::fprintf(stderr, "[psg] jit kernel: %d regs, %zu B local, %d CTAs/SM (%zu B source)\n", fa.numRegs,
+                 static_cast<size_t>(fa.localSizeBytes), per_sm, body.size());
+  }
   g_compile_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   ++g_compiles;
   (void)device;
@@ -518,7 +540,8 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
     }
   }
   if (P.remote) throw Error(PSG_ERR_INTERNAL, "the fused NVLink path needs the query compiler (PSG_JIT)");
-  if (P.self_probe) throw Error(PSG_ERR_INTERNAL, "the in-place owner probe needs the query compiler (PSG_JIT)");
+  if (P.self_probe || P.pack_n || P.unpack_n)
+    throw Error(PSG_ERR_INTERNAL, "the in-place owner probe / packed shuffle rows need the query compiler (PSG_JIT)");
   launch_scan(P, d_segs, d_tile_seg, nsegs, ntiles, stream);
 }
 
@@ -570,6 +593,17 @@ int jit_selftest(std::string& log) {
       p.self_rank = 2;
       p.key_reg = 1;
       progs.push_back(p);
+      p.pack_n = 3;  // + bit-packed output rows
+      p.pack_reg[0] = 1, p.pack_reg[1] = 2, p.pack_reg[2] = 3;
+      p.n_out = 1;
+      progs.push_back(p);
+    }
+    if (sink == SINK_PROBE) {  // consuming packed rows
+      ScanProgram q = p;
+      q.unpack_n = 3;
+      q.n_in = 1, q.n_pred = 0, q.n_early = 1, q.n_regs = 4, q.n_atoms = 0;
+      q.key_reg = 1;
+      progs.push_back(q);
     }
   }
   {

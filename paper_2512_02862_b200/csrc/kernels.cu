@@ -568,7 +568,7 @@ constexpr int kScatterPer = 16;  // rows per thread per chunk
 __global__ void __launch_bounds__(256) k_part_scatter(ColPtrs in, int ncols, uint64_t n, int key_col, int nparts,
                                                       const unsigned long long* dest_base,
                                                       const unsigned long long* dest_cnt, unsigned long long* cursor,
-                                                      uint64_t* send) {
+                                                      uint64_t* send, KeyField kf) {
   __shared__ unsigned int s_cnt[kMaxParts];
   __shared__ unsigned long long s_base[kMaxParts];
   const int tid = threadIdx.x, lane = tid & 31;
@@ -581,7 +581,9 @@ __global__ void __launch_bounds__(256) k_part_scatter(ColPtrs in, int ncols, uin
     for (int k = 0; k < kScatterPer; ++k) {
       const uint64_t i = c0 + k * 256 + tid;
       const bool valid = i < n;
-      const uint32_t d = valid ? part_of(in.p[key_col][i], static_cast<uint32_t>(nparts)) : 0xffffffffu;
+      uint64_t key = valid ? in.p[key_col][i] : 0;
+      if (kf.mask) key = static_cast<uint64_t>(kf.min) + ((key >> kf.shift) & kf.mask);  // bit-packed rows
+      const uint32_t d = valid ? part_of(key, static_cast<uint32_t>(nparts)) : 0xffffffffu;
       const unsigned peers = __match_any_sync(0xffffffffu, d);
       const int leader = __ffs(peers) - 1;
       unsigned int old = 0;
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(256) k_part_scatter(ColPtrs in, int ncols, uin
 }
 void launch_part_scatter(const uint64_t* const* in_cols, int ncols, uint64_t n, int key_col, int nparts,
                          const unsigned long long* dest_base, const unsigned long long* dest_cnt,
-                         unsigned long long* cursor, uint64_t* send, void* stream) {
+                         unsigned long long* cursor, uint64_t* send, void* stream, KeyField kf) {
   if (n == 0) return;
   ColPtrs pc{};
   for (int c = 0; c < ncols; ++c) pc.p[c] = in_cols[c];
@@ -619,7 +621,7 @@ void launch_part_scatter(const uint64_t* const* in_cols, int ncols, uint64_t n, 
   const uint64_t maxb = static_cast<uint64_t>(sm_count()) * 8;
   if (blocks > maxb) blocks = maxb;
   k_part_scatter<<<static_cast<unsigned>(blocks), 256, 0, S(stream)>>>(pc, ncols, n, key_col, nparts, dest_base, dest_cnt,
-                                                                      cursor, send);
+                                                                      cursor, send, kf);
 }
 
 __global__ void k_part_ids(const uint64_t* keys, uint64_t n, int nparts, int identity, uint32_t* ids) {

@@ -47,9 +47,15 @@ void launch_expand_write(LocalTableDev t, const uint64_t* probe_keys, uint64_t n
                          const uint64_t* const* probe_cols, int nprobe, uint64_t* const* out_cols, void* stream);
 
 // Partition scatter (pipeline shuffle): rows of a materialised batch into dest-major send regions.
+/// Key of a bit-packed row: min + (word >> shift & mask); mask == 0: the key column is the raw key.
+struct KeyField {
+  int64_t min;
+  uint64_t mask;
+  int32_t shift;
+};
 void launch_part_scatter(const uint64_t* const* in_cols, int ncols, uint64_t n, int key_col, int nparts,
                          const unsigned long long* dest_base, const unsigned long long* dest_cnt,
-                         unsigned long long* cursor, uint64_t* send, void* stream);
+                         unsigned long long* cursor, uint64_t* send, void* stream, KeyField kf = KeyField{0, 0, 0});
 // Stable partition for the op-level API: dest id per row.
 void launch_part_ids(const uint64_t* keys, uint64_t n, int nparts, int identity, uint32_t* ids, void* stream);
 void launch_gather(const uint64_t* const* in_cols, int ncols, const uint32_t* idx, uint64_t n, uint64_t* const* out,
