@@ -120,6 +120,24 @@ def measured_peak():
         return 6650.0, "fallback"
 
 
+def pinned_h2d_gbs(local, nbytes=1 << 30, reps=3):
+    """Pinned host -> HBM copy bandwidth of this GPU's link, measured live (the PCIe term of the
+    ingest roofline)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device="cuda:%d" % local)
+    d.copy_(h, non_blocking=True)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(reps):
+        t = time.time()
+        d.copy_(h, non_blocking=True)
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (time.time() - t) / 1e9)
+    del h, d
+    return best
+
+
 def ncu_traffic(scale):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -316,6 +334,19 @@ def main():
                 "kernel_ms_per_launch": round(per_launch_s * 1000, 4),
                 "share_of_step": round(probe_ms / max(sum(dev_ms), 1e-9), 4)}
 
+    # binding roofline of the end-to-end query: ingest (per-GPU bytes over the pinned->HBM link),
+    # the slowest rank decides; the host's page-cache read bandwidth is shared by all ranks and is
+    # the tighter bound on this box (profiles/r1_box_ingest_probe.txt)
+    e2e_roof = None
+    try:
+        bw = pinned_h2d_gbs(local)
+        t_min = max_over_ranks(h2d / 1e9 / bw) if bw > 0 else None
+        if t_min and e2e_s:
+            e2e_roof = {"bound": "ingest (pinned H2D per GPU)", "h2d_gbs_measured": round(bw, 1),
+                        "t_min_s": round(t_min, 4), "frac": round(t_min / e2e_s, 4)}
+    except Exception as e:  # never hide the main numbers
+        e2e_roof = {"error": str(e)[:200]}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -349,6 +380,7 @@ def main():
                     "io_wait_s": round(statistics.mean(io_wait), 4) if io_wait else None,
                     "ingest_gbs": round(h2d_all / 1e9 / e2e_s, 2) if e2e_s else None,
                     "path": "psg_execute_plan: PSTO files (warm page cache) -> pinned -> HBM -> rows to host"},
+            "e2e_roofline": e2e_roof,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
         }
