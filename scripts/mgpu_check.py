@@ -27,6 +27,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=float, default=0.1)
     ap.add_argument("--modes", default="overlapped,blocking")
+    ap.add_argument("--fuzz", type=int, default=30, help="random plans (tests/test_gpu_fuzz.py) checked per node")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -98,6 +99,37 @@ def main():
                         flush=True)
                     if not ok:
                         failures.append((pname, mode, fused, semijoin, got, want))
+    # randomised plans (all shapes of tests/test_gpu_fuzz.py) per node vs the oracle
+    if a.fuzz:
+        import importlib.util
+        import random
+        spec = importlib.util.spec_from_file_location("fz", os.path.join(ROOT, "tests", "test_gpu_fuzz.py"))
+        fz = importlib.util.module_from_spec(spec)
+        spec.loader.exec_module(fz)
+        d = data(0.01, 3, 64 << 10)
+        nbad = 0
+        for seed in range(a.fuzz):
+            plan = fz.random_plan(random.Random(seed))
+            try:
+                res = ctx.execute_plan(plan, d)
+                mine = (res.schema, res.rows.copy())
+            except psg.PsgError as e:
+                mine = ("error", str(e))
+            allres = [None] * world
+            dist.all_gather_object(allres, mine)
+            if rank == 0:
+                if any(x[0] == "error" for x in allres):
+                    failures.append(("fuzz", seed, [x for x in allres if x[0] == "error"]))
+                    nbad += 1
+                    continue
+                got = po.summary(allres)
+                want = po.summary(po.execute(json.dumps(plan), d, world))
+                if got != want:
+                    failures.append(("fuzz", seed, json.dumps(plan), got, want))
+                    nbad += 1
+        if rank == 0:
+            print("fuzz                   %d plans   oracle    %s (%d bad)" % (a.fuzz, "OK " if not nbad else "BAD", nbad),
+                  flush=True)
     # synthetic-join workload (gen_workload kind=synthetic): per-node rows vs the reference
     syn = json.load(open(os.path.join(ROOT, "tests", "golden", "synthetic.json")))
     sdir = os.path.join(base, "syn")

@@ -44,16 +44,32 @@ def random_plan(rng):
     if rng.random() < 0.5:
         need = {"l_orderkey"} | {a["col"] for a in lpred}
         scans[2]["columns"] = [c for c in lcols if c in need or rng.random() < 0.6]
-    plan = {"scans": scans, "joins": [
-        {"id": "co", "build": "customer", "probe": "orders", "build_key": "c_custkey", "probe_key": "o_custkey",
-         "mode": "replicated"},
-        {"id": "res", "build": "co", "probe": "lineitem", "build_key": "o_orderkey", "probe_key": "l_orderkey",
-         "mode": "shuffle"}]}
+    joins = [{"id": "co", "build": "customer", "probe": "orders", "build_key": "c_custkey", "probe_key": "o_custkey",
+              "mode": "replicated"},
+             {"id": "res", "build": "co", "probe": "lineitem", "build_key": "o_orderkey", "probe_key": "l_orderkey",
+              "mode": "shuffle"}]
+    cand_extra = ["c_mktsegment"]
+    shape = rng.random()
+    if shape < 0.15:  # no local join: orders shuffled directly
+        joins = [dict(joins[1], build="orders")]
+        cand_extra = []
+    elif shape < 0.3:  # a chain of two local joins on the build side (customer read twice)
+        scans.append({"table": "cust2", "paths": ["{data}/dev*/customer.psto"], "replicated": True,
+                      "predicate": _atoms(rng, ["c_mktsegment"])})
+        joins = [joins[0], {"id": "co2", "build": "cust2", "probe": "co", "build_key": "c_custkey",
+                            "probe_key": "o_custkey", "mode": "replicated"}, dict(joins[1], build="co2")]
+        cand_extra = ["c_mktsegment"]
+    elif shape < 0.45:  # a local join on the probe side (lineitem rows whose order key is a customer key)
+        scans.append({"table": "cust3", "paths": ["{data}/dev*/customer.psto"], "replicated": True,
+                      "predicate": _atoms(rng, ["c_mktsegment"])})
+        joins = [joins[0], {"id": "lc", "build": "cust3", "probe": "lineitem", "build_key": "c_custkey",
+                            "probe_key": "l_orderkey", "mode": "replicated"}, dict(joins[1], probe="lc")]
+    plan = {"scans": scans, "joins": joins}
     r = rng.random()
     if r < 0.8:
         ocols_p = scans[1].get("columns", ocols)
         lcols_p = scans[2].get("columns", lcols)
-        cand = ["c_mktsegment"] + [c for c in ocols_p if c != "o_orderkey"] + list(lcols_p)
+        cand = cand_extra + [c for c in ocols_p if c != "o_orderkey"] + list(lcols_p)
         sums = rng.sample(cand, rng.randint(0, min(4, len(cand))))
         plan["aggregate"] = {"group_by": "l_orderkey" if r < 0.65 else "", "sums": sums}
     return plan
@@ -74,7 +90,7 @@ def ctx():
     c.close()
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(60))
 def test_random_plan_matches_oracle(ctx, data, seed):
     rng = random.Random(seed)
     plan = random_plan(rng)
