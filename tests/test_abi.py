@@ -129,3 +129,30 @@ def test_synthetic_generator_matches_reference_bytes(tmp_path):
         assert got == spec["files"]
         man = _json.load(open(m))
         assert man["kind"] == "synthetic-join" and man["tables"]["build"]["rows"] == 120000
+
+
+def _build_cabi_example(tmp_path):
+    import subprocess
+    exe = str(tmp_path / "run_plan")
+    libdir = os.path.join(ROOT, "paper_2512_02862_b200")
+    subprocess.run(["g++", "-std=c++17", "-O1", os.path.join(ROOT, "tests", "cabi", "run_plan.cpp"),
+                    "-I" + os.path.join(ROOT, "include"), "-L" + libdir, "-lpsg", "-Wl,-rpath," + libdir, "-o", exe],
+                   check=True, capture_output=True)
+    return exe
+
+
+def test_cabi_example_compiles_links_and_fails_loudly_without_gpu(tmp_path):
+    """A C++ program against include/psg.h links to libpsg.so (the reference-side binding of
+    INTEGRATION.md); without a GPU, psg_ctx_create reports CudaError instead of computing."""
+    import subprocess
+    exe = _build_cabi_example(tmp_path)
+    plan = tmp_path / "p.json"
+    plan.write_text("{}")
+    r = subprocess.run([exe, str(plan), str(tmp_path)], capture_output=True, text=True)
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if not has_gpu:
+        assert r.returncode == 2 and "psg error" in r.stderr
