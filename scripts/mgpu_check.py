@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--scale", type=float, default=0.1)
     ap.add_argument("--modes", default="overlapped,blocking")
     ap.add_argument("--fuzz", type=int, default=30, help="random plans (tests/test_gpu_fuzz.py) checked per node")
+    ap.add_argument("--sf10", action="store_true", help="BASELINE config 2: canonical Q3 at SF10 vs the reference")
     a = ap.parse_args()
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -99,6 +100,22 @@ def main():
                         flush=True)
                     if not ok:
                         failures.append((pname, mode, fused, semijoin, got, want))
+    # BASELINE config 2: Q3 at SF10 on N GPUs; the result multiset is independent of the node
+    # count, so the union over ranks must equal the reference's SF10 golden
+    if a.sf10:
+        d = data(10.0, 42, 1 << 20)
+        for mode in ("overlapped", "blocking"):
+            res = ctx.execute_plan(golden["plans"]["canonical"], d, mode)
+            allres = [None] * world
+            dist.all_gather_object(allres, (res.schema, res.rows.copy()))
+            if rank == 0:
+                got = po.summary(allres)
+                ok = (got["rows"], got["rowhash"]) == (1218662, "661bdb187378204d") and \
+                    [int(x) for x in got["colsums"][1:]] == [2979547, 417235545352, 14897482]
+                print("%-22s %-10s SF10      %s rows=%d per_node=%s" % ("canonical", mode, "OK " if ok else "BAD",
+                                                                          got["rows"], got["per_node_rows"]), flush=True)
+                if not ok:
+                    failures.append(("sf10", mode, got))
     # randomised plans (all shapes of tests/test_gpu_fuzz.py) per node vs the oracle
     if a.fuzz:
         import importlib.util
