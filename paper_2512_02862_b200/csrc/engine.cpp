@@ -558,6 +558,7 @@ struct StreamSession {
   size_t released = 0;  // batches the consumer has released (slot_free recorded)
   std::vector<BatchView> views;  // per ring slot
   int cur_slot = -1;
+  int tl_consume = -1;  // timeline interval of the batch being consumed
 
   /// budget/ht_reserve: plan memory_budget_bytes and the bytes set aside for hash tables; the ring
   /// depth is regulated to fit (regulate, pipeline.cpp:198-240): InfeasibleBudget when not even one
@@ -676,13 +677,15 @@ struct StreamSession {
       blob.resize(joff + jobs.size() * sizeof(InflateJob));
       std::memcpy(blob.data() + joff, jobs.data(), jobs.size() * sizeof(InflateJob));
     }
-    ingest->copy_to_device(j, base, blob.data(), blob.size(), ctx.copy);
+    ingest->copy_to_device(j, base, blob.data(), blob.size(), ctx.copy);  // timeline lane 1 inside
     h2d_bytes += b.bytes + blob.size();
     PSG_CUDA(cudaEventRecord(copied[k], ctx.copy));
     if (b.inflate) {
       PSG_CUDA(cudaStreamWaitEvent(istreams[k], copied[k], 0));
+      const int ti = ctx.timeline ? ctx.timeline->gpu_begin("inflate b" + std::to_string(j), 2, istreams[k]) : -1;
       launch_inflate(reinterpret_cast<const InflateJob*>(base + b.bytes + joff), static_cast<uint32_t>(b.jobs.size()),
                      inflate_err.as<unsigned int>(), istreams[k]);
+      if (ti >= 0) ctx.timeline->gpu_end(ti, istreams[k]);
       PSG_CUDA(cudaEventRecord(inflated[k], istreams[k]));
     }
     BatchView& v = views[k];
@@ -706,6 +709,7 @@ struct StreamSession {
     while (enqueued <= i) enqueue(enqueued);  // blocks on the read of batch i if needed
     const int k = static_cast<int>(i % slots.size());
     PSG_CUDA(cudaStreamWaitEvent(ctx.compute, batches[i].inflate ? inflated[k] : copied[k], 0));
+    if (ctx.timeline) tl_consume = ctx.timeline->gpu_begin("compute b" + std::to_string(i), 3, ctx.compute);
     v = views[k];
     cur_slot = k;
     ++cursor;
@@ -713,6 +717,7 @@ struct StreamSession {
   }
   void release() {
     if (cur_slot >= 0) {
+      if (tl_consume >= 0) ctx.timeline->gpu_end(tl_consume, ctx.compute), tl_consume = -1;
       PSG_CUDA(cudaEventRecord(slot_free[cur_slot], ctx.compute));
       ++released;
       cur_slot = -1;
@@ -1144,6 +1149,7 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
                                         KeyField kf) {
   const int n = ctx_.nranks;
   Received rcv;
+  const int tl = ctx_.timeline ? ctx_.timeline->gpu_begin("exchange w" + std::to_string(st_.waves), 4, ctx_.compute) : -1;
   // dest bases (exclusive scan of the per-destination histogram) and scatter into send regions
   DevBuf base(ctx_.pool, n * 8, ctx_.compute), cursor(ctx_.pool, n * 8, ctx_.compute);
   size_t tb = exclusive_scan_u64(nullptr, nullptr, n, nullptr, 0, ctx_.compute);
@@ -1191,6 +1197,7 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
     roff += rc;
   }
   PSG_NCCL(ncclGroupEnd());
+  if (tl >= 0) ctx_.timeline->gpu_end(tl, ctx_.compute);
   xt.mark("  exchange payload", ctx_.compute);
   st_.waves += 1;
   return rcv;
@@ -1289,6 +1296,15 @@ ResultRows Execution::run(bool want_rows) {
   PSG_CUDA(cudaEventCreate(&ev0));
   PSG_CUDA(cudaEventCreate(&ev1));
   PSG_CUDA(cudaEventRecord(ev0, ctx_.compute));
+  std::unique_ptr<Timeline> timeline;
+  if (Timeline::enabled()) {
+    timeline = std::make_unique<Timeline>(ctx_.compute);
+    ctx_.timeline = timeline.get();
+  }
+  struct TimelineScope {
+    Ctx& c;
+    ~TimelineScope() { c.timeline = nullptr; }
+  } tl_scope{ctx_};
   compile();
   PSG_TRACE_MSG("run: compiled, build wire %zu cols, probe wire %zu cols", bsrc_.wire.size(), psrc_.wire.size());
   ResultRows out;
@@ -1838,6 +1854,10 @@ ResultRows Execution::run(bool want_rows) {
     st_.h2d_bytes = session_->h2d_bytes;
   }
   if (session_ && session_->ingest) st_.io_wait_s = session_->ingest->wait_s();
+  if (timeline) {
+    session_.reset();  // drains the streams and the I/O threads first
+    timeline->dump(std::getenv("PSG_TIMELINE"), ctx_.rank);
+  }
   st_.jit_compiles = jit_stats().compiles - jit0_;
   st_.result_rows = out.nrows;
   st_.runtime_s = secs_since(t0);

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <condition_variable>
 #include <deque>
 #include <map>
@@ -108,6 +109,39 @@ struct BatchPlan {
   uint64_t scan_bytes() const { return inflate ? ubytes : payload_bytes; }
 };
 
+/// Opt-in execution timeline (PSG_TIMELINE=<path>): intervals on the GPU streams (CUDA events
+/// against one origin event) and on the host I/O threads (steady_clock against the origin's host
+/// time), written as Chrome-trace JSON (<path>.rank<r>.json) - the overlap evidence nsys would give
+/// (nsys is not in the image). Lanes: 0 host reads, 1 H2D copy, 2 inflate, 3 compute, 4 exchange.
+class Timeline {
+ public:
+  static bool enabled();
+  explicit Timeline(cudaStream_t origin_stream);
+  ~Timeline();
+  int gpu_begin(const std::string& name, int lane, cudaStream_t s);
+  void gpu_end(int id, cudaStream_t s);
+  void host(const std::string& name, int lane, std::chrono::steady_clock::time_point a,
+            std::chrono::steady_clock::time_point b);
+  void dump(const std::string& path, int rank);
+
+ private:
+  struct Gpu {
+    std::string name;
+    int lane;
+    cudaEvent_t a, b;
+  };
+  struct Host {
+    std::string name;
+    int lane;
+    double a_us, b_us;
+  };
+  cudaEvent_t origin_ = nullptr;
+  std::chrono::steady_clock::time_point host_origin_;
+  std::mutex mu_;
+  std::vector<Gpu> gpu_;
+  std::vector<Host> host_;
+};
+
 struct Ctx;
 
 /// Host I/O pool -> pinned staging slots -> H2D on the copy stream (the GPU analog of IoPool +
@@ -189,6 +223,7 @@ struct Ctx {
     return symm + off;
   }
   void ensure_pinned(int nslots, uint64_t slot_bytes);
+  Timeline* timeline = nullptr;  // set for the duration of a query when PSG_TIMELINE is on
   ~Ctx();
 };
 

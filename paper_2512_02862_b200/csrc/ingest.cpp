@@ -4,6 +4,8 @@
 #include <unistd.h>
 
 #include <chrono>
+#include <cstdlib>
+#include <fstream>
 #include <map>
 #include <cstring>
 
@@ -273,6 +275,7 @@ void Ingest::worker() {
     const BatchPlan& b = batches_[job];
     auto* dst = static_cast<uint8_t*>(slots_[slot].host);
     std::string err;
+    const auto t_read = std::chrono::steady_clock::now();
     for (const Extent& e : b.extents) {
       uint64_t got = 0;
       while (got < e.len) {
@@ -285,6 +288,7 @@ void Ingest::worker() {
       }
       if (!err.empty()) break;
     }
+    if (ctx_.timeline) ctx_.timeline->host("read b" + std::to_string(job), 0, t_read, std::chrono::steady_clock::now());
     std::lock_guard<std::mutex> lk(mu_);
     if (!err.empty() && error_.empty()) error_ = err;
     bytes_read_ += b.bytes;
@@ -321,9 +325,87 @@ void Ingest::copy_to_device(size_t i, void* dst, const void* extra, size_t extra
   if (b.bytes + extra_bytes > slot_bytes_) throw InvalidInput("batch exceeds pinned slot size");
   auto* host = static_cast<uint8_t*>(slots_[slot].host);
   if (extra_bytes) std::memcpy(host + b.bytes, extra, extra_bytes);
+  const int tl = ctx_.timeline ? ctx_.timeline->gpu_begin("h2d b" + std::to_string(i), 1, copy_stream) : -1;
   PSG_CUDA(cudaMemcpyAsync(dst, host, b.bytes + extra_bytes, cudaMemcpyHostToDevice, copy_stream));
+  if (tl >= 0) ctx_.timeline->gpu_end(tl, copy_stream);
   done_args_.push_back(std::make_unique<CopyDone>(CopyDone{this, slot}));
   PSG_CUDA(cudaLaunchHostFunc(copy_stream, &Ingest::on_copied, done_args_.back().get()));
+}
+
+// ----------------------------------------------------------------------------- Timeline
+bool Timeline::enabled() {
+  static const bool on = std::getenv("PSG_TIMELINE") != nullptr;
+  return on;
+}
+
+Timeline::Timeline(cudaStream_t s) {
+  PSG_CUDA(cudaEventCreate(&origin_));
+  PSG_CUDA(cudaEventRecord(origin_, s));
+  PSG_CUDA(cudaEventSynchronize(origin_));
+  host_origin_ = std::chrono::steady_clock::now();
+}
+
+Timeline::~Timeline() {
+  for (auto& g : gpu_) {
+    cudaEventDestroy(g.a);
+    cudaEventDestroy(g.b);
+  }
+  if (origin_) cudaEventDestroy(origin_);
+}
+
+int Timeline::gpu_begin(const std::string& name, int lane, cudaStream_t s) {
+  Gpu g{name, lane, nullptr, nullptr};
+  PSG_CUDA(cudaEventCreate(&g.a));
+  PSG_CUDA(cudaEventCreate(&g.b));
+  PSG_CUDA(cudaEventRecord(g.a, s));
+  std::lock_guard<std::mutex> lk(mu_);
+  gpu_.push_back(g);
+  return static_cast<int>(gpu_.size() - 1);
+}
+
+void Timeline::gpu_end(int id, cudaStream_t s) {
+  cudaEvent_t b;
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    b = gpu_[id].b;
+  }
+  PSG_CUDA(cudaEventRecord(b, s));
+}
+
+void Timeline::host(const std::string& name, int lane, std::chrono::steady_clock::time_point a,
+                    std::chrono::steady_clock::time_point b) {
+  std::lock_guard<std::mutex> lk(mu_);
+  host_.push_back({name, lane, std::chrono::duration<double, std::micro>(a - host_origin_).count(),
+                   std::chrono::duration<double, std::micro>(b - host_origin_).count()});
+}
+
+void Timeline::dump(const std::string& path, int rank) {
+  PSG_CUDA(cudaDeviceSynchronize());
+  static const char* lanes[] = {"host reads", "H2D copy", "inflate", "compute", "exchange"};
+  std::ofstream out(path + ".rank" + std::to_string(rank) + ".json");
+  out << "{\"traceEvents\": [\n";
+  bool first = true;
+  auto emit = [&](const std::string& name, int lane, double a, double b) {
+    if (b < a) return;
+    out << (first ? "" : ",\n") << "{\"name\": \"" << name << "\", \"ph\": \"X\", \"pid\": " << rank
+        << ", \"tid\": " << lane << ", \"ts\": " << a << ", \"dur\": " << (b - a) << "}";
+    first = false;
+  };
+  for (int l = 0; l < 5; ++l) {
+    out << (first ? "" : ",\n") << "{\"name\": \"thread_name\", \"ph\": \"M\", \"pid\": " << rank
+        << ", \"tid\": " << l << ", \"args\": {\"name\": \"" << lanes[l] << "\"}}";
+    first = false;
+  }
+  for (auto& g : gpu_) {
+    float a = 0, b = 0;
+    if (cudaEventElapsedTime(&a, origin_, g.a) != cudaSuccess || cudaEventElapsedTime(&b, origin_, g.b) != cudaSuccess) {
+      cudaGetLastError();
+      continue;
+    }
+    emit(g.name, g.lane, a * 1000.0, b * 1000.0);
+  }
+  for (auto& h : host_) emit(h.name, h.lane, h.a_us, h.b_us);
+  out << "\n]}\n";
 }
 
 }  // namespace psg
