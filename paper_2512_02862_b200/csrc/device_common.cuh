@@ -94,6 +94,11 @@ struct AggTableDev {
   int32_t shift;        // 64 - log2(cap)
   int32_t bloom_shift;  // 64 - log2(bloom words)
   unsigned int* dups;   // set to 1 when a build key repeats (nullptr: unknown, assume repeats)
+  // Dense build keys: exact membership bitmap over [kmin, kmin + krange) instead of the Bloom
+  // filter (kbits != nullptr; set by the build, tested by the probe).
+  uint32_t* kbits;
+  int64_t kmin;
+  uint64_t krange;
 };
 
 /// One rank's aggregation-table arrays as mapped into this process (CUDA IPC symmetric heap).
@@ -194,7 +199,12 @@ __device__ __forceinline__ uint32_t bloom_bits(uint64_t h2, int bshift) {
   return (1u << ((h2 >> (bshift - 5)) & 31)) | (1u << ((h2 >> (bshift - 10)) & 31)) |
          (1u << ((h2 >> (bshift - 15)) & 31));
 }
+__device__ __forceinline__ bool agg_kbit(const AggTableDev& t, uint64_t key) {
+  const uint64_t d = key - static_cast<uint64_t>(t.kmin);
+  return d < t.krange && ((__ldg(t.kbits + (d >> 5)) >> (d & 31)) & 1u);
+}
 __device__ __forceinline__ bool bloom_maybe(const AggTableDev& t, uint64_t key) {
+  if (t.kbits != nullptr) return agg_kbit(t, key);
   if (t.bloom == nullptr) return true;
   const uint64_t h2 = key * kBloomMul;
   const uint32_t m = bloom_bits(h2, t.bloom_shift);
@@ -280,6 +290,9 @@ __device__ __forceinline__ void agg_count_build(const AggTableDev& t, uint64_t k
   if (slot == t.mask + 1 || dup) {
     atomicAdd(reinterpret_cast<unsigned long long*>(t.cold + slot * t.cw), 1ULL);
     if (dup && t.dups != nullptr) *t.dups = 1u;
+  } else if (t.kbits != nullptr) {
+    const uint64_t d = key - static_cast<uint64_t>(t.kmin);
+    atomicOr(t.kbits + (d >> 5), 1u << (d & 31));
   } else if (t.bloom != nullptr) {
     const uint64_t h2 = key * kBloomMul;
     atomicOr(t.bloom + (h2 >> t.bloom_shift), bloom_bits(h2, t.bloom_shift));

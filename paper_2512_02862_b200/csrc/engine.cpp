@@ -502,7 +502,7 @@ class Execution {
   };
   std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
   // agg table
-  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, global_acc_, barrier_word_;
+  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, global_acc_, barrier_word_;
   AggTableDev aggt_{};
   uint64_t agg_cap_ = 0;
   // stats
@@ -1500,7 +1500,38 @@ ResultRows Execution::run(bool want_rows) {
     }
   } else if (agg_) {
     pt.mark("  pre agg alloc", ctx_.compute);
+    // Dense build keys at one GPU: an exact membership bitmap replaces the Bloom filter (no false
+    // positives, 1 bit per key of the range; o_orderkey at SF100: 19 MB vs 32 MB). PSG_KBITS=0: off.
+    static const bool kbits_env = [] {
+      const char* e = std::getenv("PSG_KBITS");
+      return !(e && std::string(e) == "0");
+    }();
+    long long krange_lo = 0;
+    uint64_t krange = 0;
+    if (nr == 1 && bloom_words && kbits_env && bmat.rows) {
+      DevBuf mm(ctx_.pool, 16, ctx_.compute);
+      const long long init[2] = {LLONG_MAX, LLONG_MIN};
+      PSG_CUDA(cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, ctx_.compute));
+      launch_minmax_i64(bmat.cols[0].as<uint64_t>(), bmat.rows, mm.as<long long>(), ctx_.compute);
+      long long lohi[2];
+      PSG_CUDA(cudaMemcpyAsync(lohi, mm.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      const uint64_t range = static_cast<uint64_t>(lohi[1]) - static_cast<uint64_t>(lohi[0]) + 1;
+      if (range != 0 && range <= (1ULL << 36) && range / 32 <= bloom_words) {  // no larger than the Bloom
+        krange_lo = lohi[0];
+        krange = range;
+        bloom_words = 0;
+      }
+    }
     build_agg_table(build_rows, bloom_words);
+    if (krange) {
+      const uint64_t words = (krange + 31) / 32;
+      agg_kbits_ = DevBuf(ctx_.pool, words * 4, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, words * 4, ctx_.compute));
+      aggt_.kbits = agg_kbits_.as<uint32_t>();
+      aggt_.kmin = krange_lo;
+      aggt_.krange = krange;
+    }
     pt.mark("  agg alloc+init", ctx_.compute);
     ScanProgram p = batch_program(static_cast<int>(b_out.size()));
     p.sink = SINK_BUILD;

@@ -267,7 +267,10 @@ std::string jit_source(const ScanProgram& P) {
     emit_loads(s, P.n_early, P.n_in);
     emit_remote_build(s, P);
   } else if (probe) {
-    const bool bloom = P.agg.bloom != nullptr;
+    const bool bloom = P.agg.bloom != nullptr && P.agg.kbits == nullptr;
+    if (P.agg.kbits != nullptr)  // exact membership of dense build keys
+      s << "    { const AggTableDev& T = P.agg;\n#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && "
+        << V(P.key_reg) << "[r] != kEmptyKey && !agg_kbit(T, " << V(P.key_reg) << "[r])) pass &= ~(1u << r);\n    }\n";
     s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R], k0[R];\n";
     if (bloom) {
       s << "      uint32_t bw[R], bm[R];\n"
@@ -597,6 +600,11 @@ int jit_selftest(std::string& log) {
       p.pack_reg[0] = 1, p.pack_reg[1] = 2, p.pack_reg[2] = 3;
       p.n_out = 1;
       progs.push_back(p);
+    }
+    if (sink == SINK_PROBE) {  // exact membership bitmap instead of the Bloom filter
+      ScanProgram q = p;
+      q.agg.kbits = reinterpret_cast<uint32_t*>(16);
+      progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // consuming packed rows
       ScanProgram q = p;
