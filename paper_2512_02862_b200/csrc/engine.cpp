@@ -1212,12 +1212,25 @@ void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
   const uint64_t nslots = agg_cap_ + 1;
   DevBuf counter(ctx_.pool, 24, ctx_.compute);
   const uint64_t init[3] = {0, ~0ULL, 0};
-  PSG_CUDA(cudaMemcpyAsync(counter.p, init, 24, cudaMemcpyHostToDevice, ctx_.compute));
-  launch_agg_range(aggt_, agg_cap_, counter.as<unsigned long long>(), ctx_.compute);
   uint64_t cnt[3] = {0, 0, 0};
-  PSG_CUDA(cudaMemcpyAsync(cnt, counter.p, 24, cudaMemcpyDeviceToHost, ctx_.compute));
-  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
-  const uint64_t ng = cnt[0];
+  static const bool dense_env = [] {
+    const char* e = std::getenv("PSG_DENSE_EMIT");
+    return !(e && std::string(e) == "0");
+  }();
+  const uint64_t flip = 0x8000000000000000ULL;
+  if (aggt_.kbits != nullptr && dense_env) {
+    // the exact build-key range bounds every group: no range pass; the group count comes out of
+    // the bitmap prefix below
+    cnt[0] = ~0ULL;
+    cnt[1] = static_cast<uint64_t>(aggt_.kmin) ^ flip;
+    cnt[2] = (static_cast<uint64_t>(aggt_.kmin) + aggt_.krange - 1) ^ flip;
+  } else {
+    PSG_CUDA(cudaMemcpyAsync(counter.p, init, 24, cudaMemcpyHostToDevice, ctx_.compute));
+    launch_agg_range(aggt_, agg_cap_, counter.as<unsigned long long>(), ctx_.compute);
+    PSG_CUDA(cudaMemcpyAsync(cnt, counter.p, 24, cudaMemcpyDeviceToHost, ctx_.compute));
+    PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  }
+  uint64_t ng = cnt[0];
   const int nc = static_cast<int>(result_schema_.size());
   std::vector<int32_t> kind, idx;
   kind.push_back(0), idx.push_back(0);
@@ -1226,13 +1239,10 @@ void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
     kind.push_back(side == 1 ? 2 : 3);
     idx.push_back(k);
   }
-  DevBuf rows(ctx_.pool, std::max<uint64_t>(ng, 1) * nc * 8, ctx_.compute);
+  DevBuf rows;
   const uint64_t span = ng ? cnt[2] - cnt[1] : 0;  // flipped-key range - 1
-  static const bool dense_env = [] {
-    const char* e = std::getenv("PSG_DENSE_EMIT");
-    return !(e && std::string(e) == "0");
-  }();
-  if (ng && dense_env && span < (1ULL << 36) && span / 64 + 1 <= 4 * ng) {
+  const bool known = ng != ~0ULL;
+  if (ng && dense_env && span < (1ULL << 36) && (!known || span / 64 + 1 <= 4 * ng)) {
     const uint64_t words = span / 64 + 1;
     DevBuf bitmap(ctx_.pool, words * 8, ctx_.compute), pc(ctx_.pool, words * 4, ctx_.compute),
         prefix(ctx_.pool, words * 4, ctx_.compute);
@@ -1242,9 +1252,26 @@ void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
     const size_t tb = exclusive_scan_u32(nullptr, nullptr, words, nullptr, 0, ctx_.compute);
     DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
     exclusive_scan_u32(pc.as<uint32_t>(), prefix.as<uint32_t>(), words, tmp.p, tb, ctx_.compute);
-    launch_agg_emit_dense(aggt_, agg_cap_, cnt[1], bitmap.as<unsigned long long>(), prefix.as<uint32_t>(), nc,
-                          kind.data(), idx.data(), rows.as<uint64_t>(), ctx_.compute);
+    if (!known) {  // groups = last prefix + last count
+      uint32_t tail[2] = {0, 0};
+      PSG_CUDA(cudaMemcpyAsync(&tail[0], prefix.as<uint32_t>() + words - 1, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaMemcpyAsync(&tail[1], pc.as<uint32_t>() + words - 1, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      ng = static_cast<uint64_t>(tail[0]) + tail[1];
+    }
+    rows = DevBuf(ctx_.pool, std::max<uint64_t>(ng, 1) * nc * 8, ctx_.compute);
+    if (ng)
+      launch_agg_emit_dense(aggt_, agg_cap_, cnt[1], bitmap.as<unsigned long long>(), prefix.as<uint32_t>(), nc,
+                            kind.data(), idx.data(), rows.as<uint64_t>(), ctx_.compute);
   } else if (ng) {
+    if (!known) {  // sparse fallback needs the exact count and range
+      PSG_CUDA(cudaMemcpyAsync(counter.p, init, 24, cudaMemcpyHostToDevice, ctx_.compute));
+      launch_agg_range(aggt_, agg_cap_, counter.as<unsigned long long>(), ctx_.compute);
+      PSG_CUDA(cudaMemcpyAsync(cnt, counter.p, 24, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      ng = cnt[0];
+    }
+    rows = DevBuf(ctx_.pool, std::max<uint64_t>(ng, 1) * nc * 8, ctx_.compute);
     DevBuf keys(ctx_.pool, nslots * 8, ctx_.compute), slots(ctx_.pool, nslots * 8, ctx_.compute);
     PSG_CUDA(cudaMemcpyAsync(counter.p, init, 24, cudaMemcpyHostToDevice, ctx_.compute));
     launch_agg_compact(aggt_, agg_cap_, keys.as<uint64_t>(), slots.as<unsigned long long>(),
