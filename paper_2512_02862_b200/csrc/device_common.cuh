@@ -149,6 +149,11 @@ struct ScanProgram {
   // materialised or shuffled - only rows owned by other ranks leave the kernel.
   int32_t self_probe;
   int32_t self_rank;
+  // Exact semi-join: one global membership bitmap of every rank's build keys over
+  // [semi_kmin, semi_kmin + semi_krange) (replaces semi_bloom when set).
+  const uint32_t* semi_kbits;
+  int64_t semi_kmin;
+  uint64_t semi_krange;
   // Bit-packed shuffle rows: MATERIALIZE with pack_n > 0 writes ONE word per row (out column 0),
   // sum_k (reg[pack_reg[k]] - pack_min[k]) << pack_shift[k]; a program with unpack_n > 0 first
   // expands register 0 into registers 1..unpack_n (value = pack_min + (w >> shift & mask)).
@@ -261,6 +266,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 /// Semi-join test: false only when key is certainly not a build key of its owner rank.
 __device__ __forceinline__ bool semi_maybe(const ScanProgram& P, uint64_t key) {
   if (key == kEmptyKey) return true;  // the spill key is never in the filters
+  if (P.semi_kbits != nullptr) {
+    const uint64_t d = key - static_cast<uint64_t>(P.semi_kmin);
+    return d < P.semi_krange && ((__ldg(P.semi_kbits + (d >> 5)) >> (d & 31)) & 1u);
+  }
   const uint64_t h2 = key * kBloomMul;
   const uint32_t d = part_of(key, static_cast<uint32_t>(P.nparts));
   const uint32_t w = __ldg(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift));

@@ -1529,13 +1529,39 @@ ResultRows Execution::run(bool want_rows) {
     pt.mark("  pre agg alloc", ctx_.compute);
     // Dense build keys at one GPU: an exact membership bitmap replaces the Bloom filter (no false
     // positives, 1 bit per key of the range; o_orderkey at SF100: 19 MB vs 32 MB). PSG_KBITS=0: off.
-    static const bool kbits_env = [] {
+    // PSG_KBITS: unset/1 = one GPU only, 2 = also the global bitmap at N > 1 (parity-green, but
+    // measured slower at N=2: 7.37 vs 6.37 ms - the partitioning scan slows more than the exact
+    // filter saves), 0 = off.
+    static const int kbits_mode = [] {
       const char* e = std::getenv("PSG_KBITS");
-      return !(e && std::string(e) == "0");
+      return e ? std::atoi(e) : 1;
     }();
+    const bool kbits_env = kbits_mode >= 1;
     long long krange_lo = 0;
     uint64_t krange = 0;
-    if (nr == 1 && bloom_words && kbits_env && bmat.rows) {
+    if (nr > 1 && semi && kbits_mode >= 2) {
+      // N > 1: one GLOBAL bitmap of all build keys over the all-reduced key range; every key's
+      // bit is set by its owner only, so a SUM all-reduce of the rank bitmaps is their OR
+      DevBuf mm(ctx_.pool, 16, ctx_.compute);
+      const long long init[2] = {LLONG_MAX, LLONG_MIN};
+      PSG_CUDA(cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, ctx_.compute));
+      for (const auto& sg : bsegs) launch_minmax_i64(sg.col[0], sg.rows, mm.as<long long>(), ctx_.compute);
+      long long lohi[2];
+      PSG_CUDA(cudaMemcpyAsync(lohi, mm.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      long long enc[2] = {~lohi[0], lohi[1]};  // max(~lo) = ~min(lo)
+      PSG_CUDA(cudaMemcpyAsync(mm.p, enc, 16, cudaMemcpyHostToDevice, ctx_.compute));
+      PSG_NCCL(ncclAllReduce(mm.p, mm.p, 2, ncclInt64, ncclMax, ctx_.nccl, ctx_.compute));
+      PSG_CUDA(cudaMemcpyAsync(enc, mm.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      const long long lo = ~enc[0], hi = enc[1];
+      const uint64_t range = hi >= lo ? static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo) + 1 : 0;
+      if (range != 0 && range <= (1ULL << 36) && range / 32 <= static_cast<uint64_t>(nr) * bloom_words) {
+        krange_lo = lo;
+        krange = range;
+        bloom_words = 0;
+      }
+    } else if (nr == 1 && bloom_words && kbits_env && bmat.rows) {
       DevBuf mm(ctx_.pool, 16, ctx_.compute);
       const long long init[2] = {LLONG_MAX, LLONG_MIN};
       PSG_CUDA(cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, ctx_.compute));
@@ -1565,8 +1591,11 @@ ResultRows Execution::run(bool want_rows) {
     p.agg = aggt_;
     p.n_sum = static_cast<int>(build_sum_wire.size());
     for (int b = 0; b < p.n_sum; ++b) p.sum_reg[b] = 1 + b;
-    run_scan(p, bview, false);  // also sets the Bloom bits of every inserted key
-    if (semi) {
+    run_scan(p, bview, false);  // also sets the Bloom (or key-bitmap) bits of every inserted key
+    if (semi && krange) {  // disjoint bits: SUM == OR
+      PSG_NCCL(ncclAllReduce(agg_kbits_.p, agg_kbits_.p, (krange + 31) / 32, ncclUint32, ncclSum, ctx_.nccl,
+                             ctx_.compute));
+    } else if (semi) {
       semi_all = DevBuf(ctx_.pool, static_cast<size_t>(nr) * bloom_words * 4, ctx_.compute);
       PSG_NCCL(ncclAllGather(agg_bloom_.p, semi_all.p, bloom_words * 4, ncclUint8, ctx_.nccl, ctx_.compute));
     }
@@ -1625,7 +1654,12 @@ ResultRows Execution::run(bool want_rows) {
   ScanProgram pp = base_program(psrc_, pm, true);
   std::vector<int> p_out;
   for (int w : pneed) p_out.push_back(pm.reg_of.at(psrc_.stage_refs.back()[w]));
-  if (semi) {
+  if (semi && aggt_.kbits) {
+    pp.semi_kbits = aggt_.kbits;
+    pp.semi_kmin = aggt_.kmin;
+    pp.semi_krange = aggt_.krange;
+    pp.semi_key_reg = p_out[0];
+  } else if (semi) {
     pp.semi_bloom = semi_all.as<uint32_t>();
     pp.semi_words = bloom_words;
     pp.semi_shift = aggt_.bloom_shift;
@@ -1640,7 +1674,7 @@ ResultRows Execution::run(bool want_rows) {
       ScanProgram p = batch_program(ncols);
       p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
       p.agg = aggt_;
-      if (semi) p.agg.bloom = nullptr;  // received rows already passed the owner's filter
+      if (semi) p.agg.bloom = nullptr, p.agg.kbits = nullptr;  // received rows already passed the filter
       p.key_reg = 0;
       p.n_sum = static_cast<int>(probe_sum_wire.size());
       for (int s = 0; s < p.n_sum; ++s) p.sum_reg[s] = 1 + s;

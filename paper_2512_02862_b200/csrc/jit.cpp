@@ -268,9 +268,13 @@ std::string jit_source(const ScanProgram& P) {
     emit_remote_build(s, P);
   } else if (probe) {
     const bool bloom = P.agg.bloom != nullptr && P.agg.kbits == nullptr;
-    if (P.agg.kbits != nullptr)  // exact membership of dense build keys
-      s << "    { const AggTableDev& T = P.agg;\n#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && "
-        << V(P.key_reg) << "[r] != kEmptyKey && !agg_kbit(T, " << V(P.key_reg) << "[r])) pass &= ~(1u << r);\n    }\n";
+    if (P.agg.kbits != nullptr)  // exact membership of dense build keys; all R words in flight first
+      s << "    { const AggTableDev& T = P.agg; uint32_t bw[R], bb[R];\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 1u; bb[r] = 0u; const uint64_t key = " << V(P.key_reg)
+        << "[r];\n        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+        << "          bw[r] = 0u; if (d < T.krange) { bb[r] = static_cast<uint32_t>(d & 31); "
+           "bw[r] = ldg_keep_u32(T.kbits + (d >> 5), pol_keep); } } }\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!((bw[r] >> bb[r]) & 1u)) pass &= ~(1u << r);\n    }\n";
     s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R], k0[R];\n";
     if (bloom) {
       s << "      uint32_t bw[R], bm[R];\n"
@@ -353,7 +357,16 @@ std::string jit_source(const ScanProgram& P) {
       }
       s << "      }\n    }\n";
     } else {  // MATERIALIZE / COUNT
-      if (P.sink == SINK_MATERIALIZE && P.semi_bloom != nullptr) {
+      if (P.sink == SINK_MATERIALIZE && P.semi_kbits != nullptr) {  // exact global key bitmap
+        // two stages, like the Bloom screen: all R bitmap words in flight before any test
+        s << "    { uint32_t bw[R], bb[R];\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 1u; bb[r] = 0u; const uint64_t key = "
+          << V(P.semi_key_reg) << "[r];\n"
+          << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(P.semi_kmin);\n"
+          << "          bw[r] = 0u; if (d < P.semi_krange) { bb[r] = static_cast<uint32_t>(d & 31); "
+             "bw[r] = ldg_keep_u32(P.semi_kbits + (d >> 5), pol_keep); } } }\n"
+          << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!((bw[r] >> bb[r]) & 1u)) pass &= ~(1u << r);\n    }\n";
+      } else if (P.sink == SINK_MATERIALIZE && P.semi_bloom != nullptr) {
         s << "    { uint32_t bw[R], bm[R];\n"
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = bm[r] = 0; const uint64_t key = " << V(P.semi_key_reg)
           << "[r];\n        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t h2 = key * kBloomMul;\n"
@@ -600,6 +613,12 @@ int jit_selftest(std::string& log) {
       p.pack_reg[0] = 1, p.pack_reg[1] = 2, p.pack_reg[2] = 3;
       p.n_out = 1;
       progs.push_back(p);
+    }
+    if (sink == SINK_MATERIALIZE) {  // exact global semi-join bitmap instead of the Blooms
+      ScanProgram q = p;
+      q.semi_bloom = nullptr;
+      q.semi_kbits = reinterpret_cast<const uint32_t*>(16);
+      progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // exact membership bitmap instead of the Bloom filter
       ScanProgram q = p;

@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kBlock) k_scan(const __grid_constant__ ScanPro
           }
         }
       } else {  // SINK_MATERIALIZE / SINK_COUNT
-        if (SINK == SINK_MATERIALIZE && P.semi_bloom != nullptr) {
+        if (SINK == SINK_MATERIALIZE && (P.semi_bloom != nullptr || P.semi_kbits != nullptr)) {
 #pragma unroll
           for (int r = 0; r < R; ++r)
             if ((pass & (1u << r)) && !semi_maybe(P, V(P.semi_key_reg, r))) pass &= ~(1u << r);
