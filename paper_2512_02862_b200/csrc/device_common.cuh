@@ -99,7 +99,26 @@ struct AggTableDev {
   uint32_t* kbits;
   int64_t kmin;
   uint64_t krange;
+  // Bit-packed accumulators (int probe-side sums bounded by the footer zone maps): word 1 of a hot
+  // slot holds the hit count in its low bits (hits_mask) and every packed sum p, accumulated as
+  // value - packed_min[p], in the field at packed_shift[p] (packed_shift < 0: own word 2 + p).
+  // One atomicAdd per hit covers them all; word 1 != 0 still means "hit".
+  int32_t npacked;
+  int32_t packed_shift[kMaxSums];
+  uint64_t packed_mask[kMaxSums];
+  int64_t packed_min[kMaxSums];
+  uint64_t hits_mask;
 };
+
+/// Hit count and probe-side sum p of a hot slot (decodes the packed accumulator).
+__device__ __forceinline__ uint64_t agg_hits(const AggTableDev& t, const uint64_t* h) {
+  return t.npacked ? (h[1] & t.hits_mask) : h[1];
+}
+__device__ __forceinline__ uint64_t agg_psum(const AggTableDev& t, const uint64_t* h, int p, uint64_t hits) {
+  if (t.npacked && t.packed_shift[p] >= 0)
+    return ((h[1] >> t.packed_shift[p]) & t.packed_mask[p]) + hits * static_cast<uint64_t>(t.packed_min[p]);
+  return h[2 + p];
+}
 
 /// One rank's aggregation-table arrays as mapped into this process (CUDA IPC symmetric heap).
 struct AggPeer {

@@ -476,6 +476,7 @@ class Execution {
   BatchView upload_segments(std::vector<Segment> segs, DevBuf& holder);
 
   void build_agg_table(uint64_t build_rows, uint64_t bloom_words);
+  void pack_accumulators();
   bool build_symmetric_agg_table(uint64_t max_rows, bool bloom);
   void gpu_barrier();
   void finalize_grouped(ResultRows& out, bool want_rows);
@@ -1101,6 +1102,79 @@ void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words) {
   launch_agg_init(aggt_, agg_cap_, ctx_.compute);
 }
 
+/// Bit-packed accumulators: the footer zone maps bound every int probe-side sum column and the
+/// total probe row count bounds any group's hits, so the hit count and each sum whose field
+/// (offset by its minimum) provably fits share word 1 of the hot slot - one atomicAdd per matched
+/// row instead of one per accumulator (Q3: hits + discount in one word, price alone: 2 instead
+/// of 3). Bounds are all-reduced at N > 1 (a rank's table also receives other ranks' rows).
+/// PSG_ACCPACK=0: off.
+void Execution::pack_accumulators() {
+  static const bool env = [] {
+    const char* e = std::getenv("PSG_ACCPACK");
+    return !(e && std::string(e) == "0");
+  }();
+  if (!env || !grouped_ || !jit_available() || ctx_.p2p) return;
+  const int np = static_cast<int>(probe_sum_wire.size());
+  if (np == 0) return;
+  // [~min_0..np), max_0..np), rows] all-reduced with MAX (rows as MAX of the SUM-encoded... SUM below)
+  std::vector<long long> mm(2 * np, 0);
+  long long rows = 0;
+  std::vector<bool> ok(np, true);
+  for (const auto& path : psrc_.scan->paths) rows += static_cast<long long>(ctx_.footers.get(path)->total_rows());
+  for (int k = 0; k < np; ++k) {
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    const ColRef ref = psrc_.stage_refs.back()[probe_sum_wire[k]];
+    if (ref.join >= 0 || psrc_.wire.fields[probe_sum_wire[k]].type != LType::Int64) {
+      lo = LLONG_MIN, hi = LLONG_MAX;
+    } else {
+      const int fcol = psrc_.proj.file_idx[ref.idx];
+      for (const auto& path : psrc_.scan->paths)
+        for (const auto& g : ctx_.footers.get(path)->groups)
+          if (g.rows) {
+            lo = std::min(lo, static_cast<long long>(g.cols[fcol].min_raw));
+            hi = std::max(hi, static_cast<long long>(g.cols[fcol].max_raw));
+          }
+    }
+    mm[k] = ~lo;
+    mm[np + k] = hi;
+  }
+  if (ctx_.nranks > 1) {
+    DevBuf d(ctx_.pool, (2 * np + 1) * 8, ctx_.compute);
+    PSG_CUDA(cudaMemcpyAsync(d.p, mm.data(), 2 * np * 8, cudaMemcpyHostToDevice, ctx_.compute));
+    PSG_CUDA(cudaMemcpyAsync(d.as<long long>() + 2 * np, &rows, 8, cudaMemcpyHostToDevice, ctx_.compute));
+    PSG_NCCL(ncclAllReduce(d.p, d.p, 2 * np, ncclInt64, ncclMax, ctx_.nccl, ctx_.compute));
+    PSG_NCCL(ncclAllReduce(d.as<long long>() + 2 * np, d.as<long long>() + 2 * np, 1, ncclInt64, ncclSum, ctx_.nccl,
+                           ctx_.compute));
+    PSG_CUDA(cudaMemcpyAsync(mm.data(), d.p, 2 * np * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    PSG_CUDA(cudaMemcpyAsync(&rows, d.as<long long>() + 2 * np, 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  }
+  auto bits = [](unsigned __int128 x) {
+    int b = 0;
+    while (x) ++b, x >>= 1;
+    return b;
+  };
+  const int bh = bits(static_cast<unsigned __int128>(std::max<long long>(rows, 1)));
+  int shift = bh, packed = 0;
+  for (int k = 0; k < np; ++k) {
+    aggt_.packed_shift[k] = -1;
+    const long long lo = ~mm[k], hi = mm[np + k];
+    if (aggt_.ps_float[k] || hi < lo || lo == LLONG_MIN || hi == LLONG_MAX) continue;
+    const unsigned __int128 span = static_cast<unsigned __int128>(static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo));
+    const int b = bits(span * static_cast<unsigned __int128>(rows));
+    if (b > 63 || shift + b > 64) continue;
+    aggt_.packed_shift[k] = shift;
+    aggt_.packed_mask[k] = b == 0 ? 0 : (b == 64 ? ~0ULL : ((1ULL << b) - 1));
+    aggt_.packed_min[k] = lo;
+    shift += b;
+    ++packed;
+  }
+  if (packed) {
+    aggt_.npacked = packed;
+    aggt_.hits_mask = bh >= 64 ? ~0ULL : ((1ULL << bh) - 1);
+  }
+}
+
 /// Same layout as build_agg_table but carved from the symmetric heap with a capacity every rank
 /// derives from the same (all-reduced) maximum, so offsets match across ranks.
 bool Execution::build_symmetric_agg_table(uint64_t max_rows, bool bloom) {
@@ -1585,6 +1659,7 @@ ResultRows Execution::run(bool want_rows) {
       aggt_.kmin = krange_lo;
       aggt_.krange = krange;
     }
+    pack_accumulators();
     pt.mark("  agg alloc+init", ctx_.compute);
     ScanProgram p = batch_program(static_cast<int>(b_out.size()));
     p.sink = SINK_BUILD;

@@ -160,6 +160,26 @@ std::string out_value(const ScanProgram& P, int o) {
   return "(" + e + ")";
 }
 
+/// Accumulation of one matched probe row r into hot slot h (SINK_PROBE and the owner probe):
+/// hits (+ packed sums) with one atomicAdd on word 1, unpacked sums on their own words.
+void emit_accumulate(std::ostringstream& s, const ScanProgram& P, const char* indent) {
+  const bool packed = P.agg.npacked > 0;
+  s << indent << "{ unsigned long long inc = 1ULL;\n";
+  for (int p = 0; p < P.n_sum; ++p)
+    if (packed && !P.agg.ps_float[p] && P.agg.packed_shift[p] >= 0)
+      s << indent << "  inc += (static_cast<unsigned long long>(" << V(P.sum_reg[p]) << "[r]) - static_cast<unsigned long long>(T.packed_min["
+        << p << "])) << T.packed_shift[" << p << "];\n";
+  s << indent << "  atomicAdd(h + 1, inc); }\n";
+  for (int p = 0; p < P.n_sum; ++p) {
+    if (packed && !P.agg.ps_float[p] && P.agg.packed_shift[p] >= 0) continue;
+    if (P.agg.ps_float[p])
+      s << indent << "atomicAdd(reinterpret_cast<double*>(h + " << 2 + p << "), __longlong_as_double(static_cast<long long>("
+        << V(P.sum_reg[p]) << "[r])));\n";
+    else
+      s << indent << "atomicAdd(h + " << 2 + p << ", static_cast<unsigned long long>(" << V(P.sum_reg[p]) << "[r]));\n";
+  }
+}
+
 std::string jit_source(const ScanProgram& P) {
   std::ostringstream s;
   const int nin = P.n_in, nregs = std::max(1, P.n_regs);
@@ -295,15 +315,8 @@ std::string jit_source(const ScanProgram& P) {
     emit_loads(s, P.n_early, P.n_in);
     if (P.sink == SINK_PROBE) {
       s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
-        << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n"
-        << "        atomicAdd(h + 1, 1ULL);\n";
-      for (int p = 0; p < P.n_sum; ++p) {
-        if (P.agg.ps_float[p])
-          s << "        atomicAdd(reinterpret_cast<double*>(h + " << 2 + p << "), __longlong_as_double(static_cast<long long>("
-            << V(P.sum_reg[p]) << "[r])));\n";
-        else
-          s << "        atomicAdd(h + " << 2 + p << ", static_cast<unsigned long long>(" << V(P.sum_reg[p]) << "[r]));\n";
-      }
+        << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
+      emit_accumulate(s, P, "        ");
       s << "      }\n";
     } else {
       s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
@@ -389,15 +402,8 @@ std::string jit_source(const ScanProgram& P) {
           << "        while (kk != key && kk != kEmptyKey) { sx = (sx + 1) & T.mask; kk = T.hot[sx * " << P.agg.hw << "]; }\n"
           << "        if (kk != key) own &= ~(1u << r); else sl[r] = sx; }\n"
           << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(own & (1u << r))) continue;\n"
-          << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n"
-          << "        atomicAdd(h + 1, 1ULL);\n";
-        for (int p = 0; p < P.n_sum; ++p) {
-          if (P.agg.ps_float[p])
-            s << "        atomicAdd(reinterpret_cast<double*>(h + " << 2 + p << "), __longlong_as_double(static_cast<long long>("
-              << V(P.sum_reg[p]) << "[r])));\n";
-          else
-            s << "        atomicAdd(h + " << 2 + p << ", static_cast<unsigned long long>(" << V(P.sum_reg[p]) << "[r]));\n";
-        }
+          << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
+        emit_accumulate(s, P, "        ");
         s << "      }\n    }\n";
       }
       if (wstage) {
@@ -556,8 +562,8 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
     }
   }
   if (P.remote) throw Error(PSG_ERR_INTERNAL, "the fused NVLink path needs the query compiler (PSG_JIT)");
-  if (P.self_probe || P.pack_n || P.unpack_n)
-    throw Error(PSG_ERR_INTERNAL, "the in-place owner probe / packed shuffle rows need the query compiler (PSG_JIT)");
+  if (P.self_probe || P.pack_n || P.unpack_n || P.agg.npacked)
+    throw Error(PSG_ERR_INTERNAL, "owner probe / packed rows / packed accumulators need the query compiler (PSG_JIT)");
   launch_scan(P, d_segs, d_tile_seg, nsegs, ntiles, stream);
 }
 
@@ -618,6 +624,13 @@ int jit_selftest(std::string& log) {
       ScanProgram q = p;
       q.semi_bloom = nullptr;
       q.semi_kbits = reinterpret_cast<const uint32_t*>(16);
+      progs.push_back(q);
+    }
+    if (sink == SINK_PROBE) {  // packed accumulators: hits + sum 0 in word 1, sum 1 (float) alone
+      ScanProgram q = p;
+      q.agg.npacked = 1;
+      q.agg.packed_shift[0] = 30;
+      q.agg.packed_shift[1] = -1;
       progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // exact membership bitmap instead of the Bloom filter

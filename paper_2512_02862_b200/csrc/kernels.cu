@@ -857,7 +857,7 @@ __global__ void k_agg_emit(AggTableDev t, const uint64_t* keys, const unsigned l
     const uint64_t s = slots[i];
     const uint64_t* h = t.hot + s * t.hw;
     const uint64_t* c = t.cold + s * t.cw;
-    const uint64_t hits = h[1], m = (t.dups == nullptr || *t.dups != 0 || s == t.mask + 1) ? agg_mult(t, s) : 1;
+    const uint64_t hits = agg_hits(t, h), m = (t.dups == nullptr || *t.dups != 0 || s == t.mask + 1) ? agg_mult(t, s) : 1;
     uint64_t* row = out + i * nc;
     for (int k = 0; k < nc; ++k) {
       const int kind = ec.kind[k], j = ec.idx[k];
@@ -869,7 +869,7 @@ __global__ void k_agg_emit(AggTableDev t, const uint64_t* keys, const unsigned l
       } else if (kind == 2) {  // probe-side sum: each probe row pairs with m build rows
         v = t.ps_float[j] ? static_cast<uint64_t>(__double_as_longlong(
                                 static_cast<double>(m) * __longlong_as_double(static_cast<long long>(h[2 + j]))))
-                          : m * h[2 + j];
+                          : m * agg_psum(t, h, j, hits);
       } else {  // build-side sum: each matched probe row adds the key's build-side total
         v = t.bs_float[j] ? static_cast<uint64_t>(__double_as_longlong(
                                 static_cast<double>(hits) * __longlong_as_double(static_cast<long long>(c[1 + j]))))
@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(256) k_agg_emit_dense(AggTableDev t, uint64_t 
     const uint64_t w = b >> 6;
     const uint64_t pos = prefix[w] + __popcll(bitmap[w] & ((1ULL << (b & 63)) - 1ULL));
     const uint64_t* c = t.cold + s * t.cw;
-    const uint64_t hits = kh.y, m = (spill || dups) ? agg_mult(t, s) : 1;
+    const uint64_t hits = t.npacked ? (kh.y & t.hits_mask) : kh.y, m = (spill || dups) ? agg_mult(t, s) : 1;
     uint64_t* row = out + pos * nc;
     uint64_t vals[2 * kMaxSums + 2];
 #pragma unroll
@@ -910,7 +910,7 @@ __global__ void __launch_bounds__(256) k_agg_emit_dense(AggTableDev t, uint64_t 
       } else if (kind == 2) {
         v = t.ps_float[j] ? static_cast<uint64_t>(__double_as_longlong(
                                 static_cast<double>(m) * __longlong_as_double(static_cast<long long>(h[2 + j]))))
-                          : m * h[2 + j];
+                          : m * agg_psum(t, h, j, hits);
       } else {
         v = t.bs_float[j] ? static_cast<uint64_t>(__double_as_longlong(
                                 static_cast<double>(hits) * __longlong_as_double(static_cast<long long>(c[1 + j]))))
