@@ -7,19 +7,20 @@
 // HBM by this kernel, straight into the chunk layout the fused scan kernel reads.
 //
 // Design (B200): one warp per chunk (persistent warps walk the job list, longest first).
-//   * Huffman decoding is inherently serial, so lane 0 runs it, with one shared-memory lookup
-//     per symbol: 10-bit (literal/length) and 8-bit (distance) first-level tables whose entries
-//     carry code length, kind, literal / base length / base distance and extra-bit count; the
-//     rare longer codes fall back to canonical decoding (left-justified per-length limits held in
-//     registers). Lane 0 also resolves matches, 8 bytes per step: output is assembled in a 64-bit
-//     register and stored as whole words into a 2 KB per-warp ring, and the last two words stay
-//     in registers, so the short distances of 8-byte column data (8, 16) never touch memory;
-//     older sources come from the ring, the oldest from the already flushed output in HBM.
-//   * The warp does the parallel parts: table construction (histogram by warp reduction,
-//     canonical symbol order by match masks, each lane fills 32 of the 1024 table slots) and the
-//     flush of every 1 KB of output as coalesced 16-byte stores, with the Adler-32 of the flushed
-//     bytes folded in by a dp4a warp reduction (zlib verifies the trailer; so do we). Lane 0 only
-//     hands control back to the warp once per KB (or block end), not per match.
+//   * Huffman decoding is inherently serial, so the whole warp runs it in lockstep on identical
+//     state (a warp instruction costs one issue slot however many lanes are active), with one
+//     shared-memory lookup per symbol: 10-bit (literal/length) and 8-bit (distance) first-level
+//     tables whose entries carry code length, kind, literal / base length / base distance and
+//     extra-bit count; the rare longer codes fall back to canonical decoding (left-justified
+//     per-length limits held in registers).
+//   * Output goes to a 2 KB per-warp ring that always holds the last 2 KB. A literal is one byte
+//     store; a match is copied by the 32 lanes at once (lane i writes byte pos + i from byte
+//     pos - dist + i mod dist, one round per 32 bytes), so its cost does not grow with its length
+//     up to 32 bytes. Sources older than the ring come from the already flushed output in HBM.
+//   * Parallel parts: table construction (histogram by warp reduction, canonical symbol order by
+//     match masks, each lane fills 32 of the 1024 table slots), stored-block copies (32 bytes per
+//     round) and the flush of every 1 KB of output as coalesced 16-byte stores, with the Adler-32
+//     of the flushed bytes folded in by a dp4a warp reduction (zlib verifies the trailer; so do we).
 // Every failure zlib reports (bad header, reserved block type, over-subscribed or incomplete
 // codes, invalid symbols, distance too far back, output overrun or short output, reading past the
 // stream, Adler mismatch) sets the error word; the host raises IoFailure("inflate failed").
@@ -136,7 +137,7 @@ __device__ bool build_table(const uint8_t* lens, int n, int what, uint16_t* sym,
     if (len > 15) {
       ent = kBadEntry;
     } else if (len > fb) {
-      ent = 0u;
+      ent = kBad << 4;  // code length 0: decode canonically (kind bits keep it off the literal path)
     } else {
       const int s = sym[base[len] + static_cast<int>(c15 >> (15 - len))];
       const uint32_t L = static_cast<uint32_t>(len);
@@ -159,19 +160,31 @@ __device__ bool build_table(const uint8_t* lens, int n, int what, uint16_t* sym,
   return true;
 }
 
-/// Lane 0's bit reader: LSB-first over 4-byte aligned words (chunks are 16-byte aligned).
+/// Bit reader: LSB-first over 4-byte aligned words (chunks are 16-byte aligned). Every lane of
+/// the warp holds the same state (the loads are broadcasts).
 struct Bits {
   const uint32_t* w0;  // stream start
-  uint32_t nwords;     // words that may be loaded (zeros are fed past them)
-  uint32_t next;       // next word index
+  uint32_t nlast;      // last word that may be loaded (chunks are padded to 16 bytes)
+  uint32_t next;       // index of the word in `nw`
+  uint32_t nw;         // prefetched next word: its load is off the decode chain
   uint64_t b;
   int n;
+  __device__ __forceinline__ void start(const void* src, uint32_t csize) {
+    w0 = reinterpret_cast<const uint32_t*>(src);
+    nlast = csize > 4 ? (csize - 1) / 4 : 0;
+    next = 0;
+    nw = __ldg(w0);
+    b = 0;
+    n = 0;
+  }
+  // Past the stream the reader feeds repeats of the last word; any stream that consumes them is
+  // rejected by the consumed-bits checks (block headers, trailer), as zlib rejects it.
   __device__ __forceinline__ void refill() {
     if (n <= 32) {
-      const uint32_t w = next < nwords ? __ldg(w0 + next) : 0u;
-      ++next;
-      b |= static_cast<uint64_t>(w) << n;
+      b |= static_cast<uint64_t>(nw) << n;
       n += 32;
+      ++next;
+      nw = __ldg(w0 + min(next, nlast));
     }
   }
   __device__ __forceinline__ uint32_t get(int k) {  // k <= 32, n >= k
@@ -187,6 +200,7 @@ struct Bits {
   __device__ __forceinline__ uint64_t consumed() const { return static_cast<uint64_t>(next) * 32ull - n; }
   __device__ __forceinline__ void seek(uint64_t bit) {  // restart at an absolute bit position
     next = static_cast<uint32_t>(bit >> 5);
+    nw = __ldg(w0 + min(next, nlast));
     b = 0;
     n = 0;
     refill();
@@ -194,61 +208,48 @@ struct Bits {
   }
 };
 
-// lane-0 section outcomes
+// decode-section outcomes
 enum Reason : int { kRFlush = 0, kREob = 1, kRErr = 2 };
 
-__device__ __forceinline__ uint64_t shl(uint64_t x, int s) { return s < 64 ? x << s : 0ull; }
-__device__ __forceinline__ uint64_t low_bytes(uint64_t x, int k) { return k >= 8 ? x : x & ((1ull << (8 * k)) - 1ull); }
-
-/// Lane 0's output assembler. Bytes [0, oi) are whole words and the next `an` (< 8) bytes are
-/// in `acc`; the ring always holds every produced byte of the last 2 KB - the partial word is
-/// stored on every append - so a match source is two shared-memory words (older ones come from
-/// the already flushed output in HBM), with no register window to branch over.
-struct Out0 {
-  uint64_t* ring;  // kRing / 8 words
-  const uint64_t* hbm;
-  uint64_t acc;
-  uint32_t oi;
-  int an;
-  __device__ __forceinline__ uint32_t pos() const { return oi + static_cast<uint32_t>(an); }
-  __device__ __forceinline__ uint64_t& slot(uint32_t byte_pos) const { return ring[(byte_pos >> 3) & (kRing / 8 - 1)]; }
-  /// Appends one literal byte.
-  __device__ __forceinline__ void put1(uint32_t byte) {
-    acc |= static_cast<uint64_t>(byte) << (8 * an);
-    slot(oi) = acc;
-    if (++an == 8) {
-      oi += 8;
-      acc = 0;
-      an = 0;
-    }
+/// Output state (identical in every lane): `pos` bytes produced; the ring holds the last 2 KB.
+struct Out {
+  uint8_t* ring;
+  const uint8_t* hbm;  // the chunk's output, flushed up to the warp's `flushed`
+  uint32_t pos;
+  /// One literal byte.
+  __device__ __forceinline__ void lit(uint32_t byte) {
+    ring[pos & kRingMask] = static_cast<uint8_t>(byte);
+    ++pos;
   }
-  /// Appends the low k (1..8) bytes of v.
-  __device__ __forceinline__ void put(uint64_t v, int k) {
-    v = low_bytes(v, k);
-    acc |= v << (8 * an);
-    slot(oi) = acc;
-    const int t = an + k;
-    if (t >= 8) {
-      oi += 8;
-      acc = an ? (v >> (64 - 8 * an)) : 0ull;
-      slot(oi) = acc;
-      an = t - 8;
-    } else {
-      an = t;
+  /// A match, copied by the whole warp 32 bytes per round. Output byte pos + i repeats byte
+  /// pos - dist + (i mod dist), which always precedes pos, so the rounds are independent: every
+  /// source is read before the round's stores, and a store only recycles the ring slot of a byte
+  /// 2 KB back. Sources within 2 KB come from the ring, older ones from the flushed output (at
+  /// least 1790 bytes back, while the flush trails pos by less than 1282).
+  __device__ __forceinline__ void match(uint32_t len, uint32_t dist, int lane) {
+    const uint32_t s0 = pos - dist;
+    const bool wrap = dist < len;  // the period repeats inside the match
+    const float rd = wrap ? __frcp_rn(static_cast<float>(dist)) : 0.f;
+    const bool near = dist <= kRing;
+    auto copy = [&](uint32_t i) {
+      if (i < len) {
+        uint32_t off = i;
+        if (wrap) {  // i mod dist: (i + 1/2) / dist is >= 1/(2 dist) away from an integer
+          const uint32_t q = static_cast<uint32_t>((static_cast<float>(i) + 0.5f) * rd);
+          off = i - q * dist;
+        }
+        const uint32_t src = s0 + off;
+        const uint8_t v = near ? ring[src & kRingMask] : __ldcg(hbm + src);
+        ring[(pos + i) & kRingMask] = v;
+      }
+    };
+    copy(static_cast<uint32_t>(lane));
+    if (len > 32) {
+#pragma unroll 1
+      for (uint32_t base = 32; base < len; base += 32) copy(base + static_cast<uint32_t>(lane));
     }
-  }
-  /// 8 bytes from position s (s < pos()); bytes at or past pos() are unspecified.
-  __device__ __forceinline__ uint64_t read8(uint32_t s) const {
-    const int sh = static_cast<int>(s & 7) * 8;
-    uint64_t lo, hi;
-    if (s + kRing - 8 >= oi) {  // both words still in the ring
-      lo = slot(s);
-      hi = slot(s + 8);
-    } else {  // flushed long ago (flushed >= oi - 1290 > s + 16)
-      lo = __ldcg(reinterpret_cast<const unsigned long long*>(hbm) + (s >> 3));
-      hi = __ldcg(reinterpret_cast<const unsigned long long*>(hbm) + (s >> 3) + 1);
-    }
-    return sh ? (lo >> sh) | (hi << (64 - sh)) : lo;
+    __syncwarp();  // the copied bytes are sources / flush input for other lanes
+    pos += len;
   }
 };
 
@@ -292,24 +293,47 @@ __device__ __forceinline__ void flush(const uint8_t* ring, uint8_t* dst, uint32_
   s1 = (s1 + SA) % 65521u;
 }
 
-/// Lane 0's decode loop for one data phase: runs until 1 KB is ready to flush, the block ends or
-/// the stream is invalid. Stored blocks (type 0) copy `stored` more bytes; else Huffman symbols.
-__device__ __forceinline__ int decode_run(Bits& br, Out0& o, WarpSmem& sm, const uint32_t (&llim)[16],
+/// The warp's decode loop for one data phase (every lane runs it in lockstep): runs until 1 KB
+/// is ready to flush, the block ends or the stream is invalid. Stored blocks (type 0) copy
+/// `stored` more bytes; else Huffman symbols.
+__device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, const uint32_t (&llim)[16],
                                           const uint32_t (&dlim)[16], int type, uint32_t& stored, uint32_t flushed,
-                                          uint32_t usize) {
-  if (type == 0) {
-    while (stored) {
-      const int k = stored < 4 ? static_cast<int>(stored) : 4;
-      br.refill();
-      o.put(br.get(8 * k), k);
-      stored -= static_cast<uint32_t>(k);
-      if (o.oi - flushed >= kFlush) return kRFlush;
+                                          uint32_t usize, uint32_t csize, int lane) {
+  // Output past usize is caught here, before its flush could write outside the chunk (the ring
+  // absorbs up to one match past the flush point), or by the trailer's exact-size check.
+  const uint32_t limit = flushed + kFlush;
+  if (type == 0) {  // byte aligned: the warp copies 32 stream bytes per round
+    const uint64_t bit = br.consumed();
+    const uint8_t* src = reinterpret_cast<const uint8_t*>(br.w0) + (bit >> 3);
+    const uint32_t avail = csize > (bit >> 3) ? csize - static_cast<uint32_t>(bit >> 3) : 0u;
+    uint32_t done = 0;
+    int r = kREob;
+    while (done < stored) {
+      const uint32_t k = min(32u, stored - done);
+      if (static_cast<uint32_t>(lane) < k) {
+        const uint32_t j = done + static_cast<uint32_t>(lane);
+        o.ring[(o.pos + static_cast<uint32_t>(lane)) & kRingMask] = j < avail ? __ldg(src + j) : 0;
+      }
+      o.pos += k;
+      done += k;
+      if (o.pos >= limit) {
+        r = o.pos > usize ? kRErr : kRFlush;
+        break;
+      }
     }
-    return kREob;
+    stored -= done;
+    br.seek(bit + 8ull * done);
+    return r;
   }
   while (true) {
     br.refill();
     uint32_t e = sm.lfast[br.b & ((1u << kLB) - 1u)];
+    if ((e & 0x30u) == 0) {  // literal with a short code: the hot path
+      br.drop(static_cast<int>(e & 15));
+      o.lit(e >> 8);
+      if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
+      continue;
+    }
     int cl = static_cast<int>(e & 15);
     if (cl == 0) {  // code longer than the first-level table
       const int s = canon_decode(br.b, llim, sm.lbase, sm.lsym, cl);
@@ -323,14 +347,13 @@ __device__ __forceinline__ int decode_run(Bits& br, Out0& o, WarpSmem& sm, const
     br.drop(cl);
     const uint32_t kind = (e >> 4) & 3;
     if (kind == kLit) {
-      if (o.pos() >= usize) return kRErr;
-      o.put1((e >> 8) & 0xFFu);
-      if (o.oi - flushed >= kFlush) return kRFlush;
+      o.lit(e >> 8);
+      if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
       continue;
     }
     if (kind == kEob) return kREob;
     if (kind == kBad) return kRErr;
-    uint32_t len = (e >> 16) + br.get(static_cast<int>((e >> 8) & 15));
+    const uint32_t len = (e >> 16) + br.get(static_cast<int>((e >> 8) & 15));
     br.refill();
     uint32_t de = sm.dfast[br.b & ((1u << kDB) - 1u)];
     int dl = static_cast<int>(de & 15);
@@ -343,22 +366,9 @@ __device__ __forceinline__ int decode_run(Bits& br, Out0& o, WarpSmem& sm, const
     }
     br.drop(dl);
     const uint32_t dist = (de >> 16) + br.get(static_cast<int>((de >> 8) & 15));
-    if (dist > o.pos() || o.pos() + len > usize) return kRErr;
-    // 8 bytes per step; a period d < 8 replicates the d bytes before the write position
-    const int d = static_cast<int>(dist);
-    while (len) {
-      const int k = len < 8 ? static_cast<int>(len) : 8;
-      uint64_t v = o.read8(o.pos() - dist);
-      if (d < 8) {
-        v = low_bytes(v, d);
-        v |= v << (8 * d);
-        v |= shl(v, 16 * d);
-        v |= shl(v, 32 * d);
-      }
-      o.put(v, k);
-      len -= static_cast<uint32_t>(k);
-    }
-    if (o.oi - flushed >= kFlush) return kRFlush;
+    if (dist > o.pos) return kRErr;
+    o.match(len, dist, lane);
+    if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
   }
 }
 
@@ -377,144 +387,133 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __
     const uint32_t usize = job.usize;
     uint8_t* const dst = job.dst;
     Bits br;
-    br.w0 = reinterpret_cast<const uint32_t*>(job.src);
-    br.nwords = (job.csize + 3) / 4;
-    br.next = 0;
-    br.b = 0;
-    br.n = 0;
-    Out0 o;
-    o.ring = reinterpret_cast<uint64_t*>(sm.ring);
-    o.hbm = reinterpret_cast<const uint64_t*>(dst);
-    o.acc = 0;
-    o.oi = 0;
-    o.an = 0;
+    br.start(job.src, job.csize);
+    Out o;
+    o.ring = sm.ring;
+    o.hbm = dst;
+    o.pos = 0;
     uint32_t flushed = 0, s1 = 1, s2 = 0;
     bool ok, last = false;
     {  // zlib header (RFC 1950): deflate, window <= 32K, no preset dictionary, FCHECK
-      int bad = 0;
-      if (lane == 0) {
-        br.refill();
-        const uint32_t cmf = br.get(8), flg = br.get(8);
-        bad = (cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20);
-      }
-      ok = !__shfl_sync(kFull, bad, 0);
+      br.refill();
+      const uint32_t cmf = br.get(8), flg = br.get(8);
+      ok = !((cmf & 15) != 8 || (cmf >> 4) > 7 || ((cmf << 8) | flg) % 31 != 0 || (flg & 0x20));
     }
+    // Every lane runs the serial parts in lockstep on identical state (one issue slot either
+    // way); shared-memory stores of those parts write one value to one address from all lanes.
     while (ok && !last) {
-      // ---------------- block header: lane 0 reads, the warp builds the tables
-      int type = 0, hlit = 0, hdist = 0, bad = 0, lastb = 0;
-      uint32_t stored = 0;
-      if (lane == 0) {
-        if (br.consumed() > job.csize * 8ull) bad = 1;  // ran past the stream
-        br.refill();
-        lastb = static_cast<int>(br.get(1));
-        type = static_cast<int>(br.get(2));
-        if (type == 0) {
-          br.drop(br.n & 7);
-          br.refill();
-          stored = br.get(16);
-          const uint32_t nlen = br.get(16);
-          if (stored != (~nlen & 0xFFFFu) || o.pos() + stored > usize) bad = 1;
-        } else if (type == 2) {
-          br.refill();
-          hlit = static_cast<int>(br.get(5)) + 257;
-          hdist = static_cast<int>(br.get(5)) + 1;
-          const int hclen = static_cast<int>(br.get(4)) + 4;
-          if (hlit > 286 || hdist > 30) bad = 1;
-          for (int i = 0; i < 19; ++i) sm.lens[i] = 0;
-          for (int i = 0; i < hclen; ++i) {
-            br.refill();
-            sm.lens[c_clorder[i]] = static_cast<uint8_t>(br.get(3));
-          }
-        } else if (type == 3) {
-          bad = 1;
-        }
-      }
-      last = __shfl_sync(kFull, lastb, 0) != 0;
-      type = __shfl_sync(kFull, type, 0);
-      hlit = __shfl_sync(kFull, hlit, 0);
-      hdist = __shfl_sync(kFull, hdist, 0);
-      if (__shfl_sync(kFull, bad, 0)) {
+      // ---------------- block header, then the warp builds the tables
+      if (br.consumed() > job.csize * 8ull) {  // ran past the stream
         ok = false;
         break;
       }
-      if (type == 1) {  // fixed codes
+      br.refill();
+      last = br.get(1) != 0;
+      const int type = static_cast<int>(br.get(2));
+      uint32_t stored = 0;
+      if (type == 3) {
+        ok = false;
+        break;
+      }
+      if (type == 0) {
+        br.drop(br.n & 7);
+        br.refill();
+        stored = br.get(16);
+        const uint32_t nlen = br.get(16);
+        if (stored != (~nlen & 0xFFFFu) || o.pos + stored > usize) {
+          ok = false;
+          break;
+        }
+      } else if (type == 1) {  // fixed codes
         for (int i = lane; i < 288; i += 32) sm.lens[i] = i < 144 ? 8 : (i < 256 ? 9 : (i < 280 ? 7 : 8));
         __syncwarp();
         build_table(sm.lens, 288, 0, sm.lsym, sm.lbase, sm.lfast, kLB, llim, lane);
         sm.lens[lane] = 5;
         __syncwarp();
         build_table(sm.lens, 32, 1, sm.dsym, sm.dbase, sm.dfast, kDB, dlim, lane);
-      } else if (type == 2) {  // dynamic codes: the code-length code, then both code-length sequences
+      } else {  // dynamic codes: the code-length code, then both code-length sequences
+        br.refill();
+        const int hlit = static_cast<int>(br.get(5)) + 257;
+        const int hdist = static_cast<int>(br.get(5)) + 1;
+        const int hclen = static_cast<int>(br.get(4)) + 4;
+        if (hlit > 286 || hdist > 30) {
+          ok = false;
+          break;
+        }
+        if (lane < 19) sm.lens[lane] = 0;
+        __syncwarp();
+        for (int i = 0; i < hclen; ++i) {
+          br.refill();
+          sm.lens[c_clorder[i]] = static_cast<uint8_t>(br.get(3));
+        }
         __syncwarp();
         if (!build_table(sm.lens, 19, 2, sm.dsym, sm.dbase, sm.dfast, kCB, dlim, lane)) {
           ok = false;
           break;
         }
-        if (lane == 0) {
-          const int total = hlit + hdist;
-          int i = 0;
-          while (i < total) {
-            br.refill();
-            const uint32_t e = sm.dfast[br.b & ((1u << kCB) - 1u)];
-            if (((e >> 4) & 3) == kBad) {  // bits outside the code-length code
-              bad = 1;
-              break;
-            }
-            br.drop(static_cast<int>(e & 15));
-            const int s = static_cast<int>(e >> 16);
-            if (s < 16) {
-              sm.lens[i++] = static_cast<uint8_t>(s);
-              continue;
-            }
-            uint8_t v = 0;
-            int rep;
-            if (s == 16) {
-              if (i == 0) {
-                bad = 1;
-                break;
-              }
-              v = sm.lens[i - 1];
-              rep = 3 + static_cast<int>(br.get(2));
-            } else if (s == 17) {
-              rep = 3 + static_cast<int>(br.get(3));
-            } else {
-              rep = 11 + static_cast<int>(br.get(7));
-            }
-            if (i + rep > total) {
-              bad = 1;
-              break;
-            }
-            while (rep--) sm.lens[i++] = v;
+        const int total = hlit + hdist;
+        int i = 0;
+        bool bad = false;
+        uint8_t prev = 0;
+        while (i < total) {
+          br.refill();
+          const uint32_t e = sm.dfast[br.b & ((1u << kCB) - 1u)];
+          if (((e >> 4) & 3) == kBad) {  // bits outside the code-length code
+            bad = true;
+            break;
           }
-          if (!bad && sm.lens[256] == 0) bad = 1;  // no end-of-block code
+          br.drop(static_cast<int>(e & 15));
+          const int sy = static_cast<int>(e >> 16);
+          if (sy < 16) {
+            sm.lens[i++] = prev = static_cast<uint8_t>(sy);
+            continue;
+          }
+          uint8_t v = 0;
+          int rep;
+          if (sy == 16) {
+            if (i == 0) {
+              bad = true;
+              break;
+            }
+            v = prev;
+            rep = 3 + static_cast<int>(br.get(2));
+          } else if (sy == 17) {
+            rep = 3 + static_cast<int>(br.get(3));
+          } else {
+            rep = 11 + static_cast<int>(br.get(7));
+          }
+          if (i + rep > total) {
+            bad = true;
+            break;
+          }
+          if (lane < rep) sm.lens[i + lane] = v;  // rep <= 138: at most 5 rounds
+          if (lane + 32 < rep) sm.lens[i + lane + 32] = v;
+          if (lane + 64 < rep) sm.lens[i + lane + 64] = v;
+          if (lane + 96 < rep) sm.lens[i + lane + 96] = v;
+          if (lane + 128 < rep) sm.lens[i + lane + 128] = v;
+          i += rep;
+          prev = v;
         }
-        if (__shfl_sync(kFull, bad, 0)) {
+        __syncwarp();
+        if (bad || sm.lens[256] == 0) {  // (no end-of-block code)
           ok = false;
           break;
         }
-        __syncwarp();
         if (!build_table(sm.lens, hlit, 0, sm.lsym, sm.lbase, sm.lfast, kLB, llim, lane) ||
             !build_table(sm.lens + hlit, hdist, 1, sm.dsym, sm.dbase, sm.dfast, kDB, dlim, lane)) {
           ok = false;
           break;
         }
       }
-      // ---------------- data: lane 0 decodes; the warp flushes each finished 1 KB
+      // ---------------- data: the warp decodes; each finished 1 KB is flushed
       while (true) {
-        int reason = kREob;
-        uint32_t oi = 0;
-        if (lane == 0) {
-          reason = decode_run(br, o, sm, llim, dlim, type, stored, flushed, usize);
-          oi = o.oi;
-        }
-        __syncwarp();
-        reason = __shfl_sync(kFull, reason, 0);
-        oi = __shfl_sync(kFull, oi, 0);
+        const int reason = decode_run(br, o, sm, llim, dlim, type, stored, flushed, usize, job.csize, lane);
         if (reason == kRErr) {
           ok = false;
           break;
         }
-        while (oi - flushed >= kFlush) {
+        __syncwarp();
+        while (o.pos - flushed >= kFlush) {
           flush(sm.ring, dst, flushed, kFlush, s1, s2, lane);
           flushed += kFlush;
         }
@@ -523,24 +522,17 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __
       }
     }
     if (ok) {
-      // ---------------- trailer: last partial word, final flush, exact size, Adler-32
-      uint32_t P = 0;
-      if (lane == 0) {
-        if (o.an) reinterpret_cast<uint64_t*>(sm.ring)[(o.oi >> 3) & (kRing / 8 - 1)] = o.acc;
-        P = o.pos();
-      }
-      __syncwarp();
-      P = __shfl_sync(kFull, P, 0);
+      // ---------------- trailer: final flush, exact size, Adler-32
+      const uint32_t P = o.pos;
       if (P != usize) ok = false;
+      __syncwarp();
       if (ok && P > flushed) flush(sm.ring, dst, flushed, P - flushed, s1, s2, lane);
-      int bad = 0;
-      if (ok && lane == 0) {
+      if (ok) {
         br.drop(br.n & 7);
         br.refill();
         const uint32_t want = __byte_perm(br.get(32), 0, 0x0123);  // big-endian
-        bad = br.consumed() > job.csize * 8ull || want != ((s2 << 16) | s1);
+        if (br.consumed() > job.csize * 8ull || want != ((s2 << 16) | s1)) ok = false;
       }
-      if (__shfl_sync(kFull, bad, 0)) ok = false;
     }
     if (!ok && lane == 0) atomicOr(err, 1u);
     __syncwarp();

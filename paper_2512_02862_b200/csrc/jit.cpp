@@ -10,6 +10,7 @@
 // Fallback when NVRTC is unavailable: the interpreter k_scan (still GPU; there is no CPU path).
 #include <cuda_runtime.h>
 #include <nvrtc.h>
+#include <unistd.h>
 
 #include <chrono>
 #include <cstdio>
@@ -498,6 +499,15 @@ Compiled compile(const std::string& body, int device) {
   Compiled c;
   const auto t0 = std::chrono::steady_clock::now();
   std::string cubin, log;
+  if (const char* dir = std::getenv("PSG_JIT_DUMP")) {
+    // diagnostics: the generated kernel source, for offline SASS inspection (nvcc -cubin)
+    static int seq = 0;
+    const std::string path = std::string(dir) + "/psg_jit_" + std::to_string(getpid()) + "_" + std::to_string(seq++) + ".cu";
+    if (FILE* f = std::fopen(path.c_str(), "w")) {
+      std::fwrite(body.data(), 1, body.size(), f);
+      std::fclose(f);
+    }
+  }
   if (!nvrtc_cubin(body, cubin, log)) {
     std::fprintf(stderr, "[psg] NVRTC compile failed (falling back to the interpreter kernel):\n%s\n", log.c_str());
     return c;
