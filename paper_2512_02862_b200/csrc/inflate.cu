@@ -46,26 +46,32 @@ __constant__ uint16_t c_dbase[30] = {1,   2,   3,   4,   5,   7,    9,    13,   
 __constant__ uint8_t c_dext[30] = {0, 0, 0, 0, 1, 1, 2, 2, 3, 3, 4, 4, 5, 5, 6, 6, 7, 7, 8, 8, 9, 9, 10, 10, 11, 11, 12, 12, 13, 13};
 __constant__ uint8_t c_clorder[19] = {16, 17, 18, 0, 8, 7, 9, 6, 10, 5, 11, 4, 12, 3, 13, 2, 14, 1, 15};
 
-// First-level table entry: bits 0-3 code length (0 = longer than the table: decode canonically),
-// bits 4-5 kind, bits 8-15 literal byte or extra-bit count, bits 16-31 base length / distance or
-// code-length symbol.
-enum Kind : uint32_t { kLit = 0, kLen = 1, kEob = 2, kBad = 3 };
-constexpr uint32_t kBadEntry = (kBad << 4) | 1u;  // bits that match no code
+// First-level table entries. Literal/length (16 bits): bits 0-3 code length (0 = longer than the
+// table: decode canonically), bit 4 literal flag; a literal keeps its byte in bits 8-15, any other
+// symbol keeps in bits 5-7 its extra-bit count (0-5 for a length; 6 end of block; 7 invalid or long
+// code) and in bits 8-15 its base length - 3. Distance / code-length (32 bits): bits 0-3 code
+// length, bit 4 slow flag (invalid, or longer than the table), bits 8-11 extra-bit count, bits
+// 16-31 base distance or code-length symbol.
+constexpr uint32_t kLitFlag = 0x10u, kSlow = 0x10u;
+constexpr uint32_t kXEob = 6u, kXSlow = 7u;
+constexpr uint32_t kBadEntry = kSlow | 1u;  // bits that match no code
 
 struct alignas(16) WarpSmem {
   uint8_t ring[kRing];
-  uint32_t lfast[1 << kLB];
+  uint16_t lfast[1 << kLB];
   uint32_t dfast[1 << kDB];  // also the code-length table (kCB bits) while reading a header
   uint16_t lsym[288];
   uint16_t dsym[32];
   int32_t lbase[16];
   int32_t dbase[16];
+  uint32_t llim[16];  // left-justified per-length limits of the canonical codes
+  uint32_t dlim[16];
   uint8_t lens[320];
 };
-static_assert(sizeof(WarpSmem) * kWarps <= 48 * 1024, "inflate shared memory exceeds the static limit");
+static_assert(sizeof(WarpSmem) * kWarps <= 26 * 1024, "inflate shared memory: 8 CTAs per SM");
 
 /// Canonical Huffman decode of the next code (lane 0): -1 when the bits match no code.
-__device__ __forceinline__ int canon_decode(uint64_t bits, const uint32_t (&lim)[16], const int32_t* base,
+__device__ __forceinline__ int canon_decode(uint64_t bits, const uint32_t* lim, const int32_t* base,
                                             const uint16_t* sym, int& len) {
   const uint32_t c15 = __brev(static_cast<uint32_t>(bits)) >> 17;
   len = 1;
@@ -75,12 +81,13 @@ __device__ __forceinline__ int canon_decode(uint64_t bits, const uint32_t (&lim)
   return sym[base[len] + static_cast<int>(c15 >> (15 - len))];
 }
 
-/// Builds a canonical code from lens[0, n) into sym/base (shared) + lim (every lane's registers)
-/// and fills the first-level table `fast` (2^fb entries) cooperatively. `what`: 0 literal/length,
+/// Builds a canonical code from lens[0, n) into sym/base/lim (shared) and fills the first-level
+/// table `fast` (2^fb entries; 16-bit entries for literal/length) cooperatively. `what`: 0 literal/length,
 /// 1 distance, 2 code-length code. Returns false (in all lanes) for codes zlib rejects
 /// (inflate_table: over-subscribed, or incomplete unless a single one-bit lit/len or distance code).
-__device__ bool build_table(const uint8_t* lens, int n, int what, uint16_t* sym, int32_t* base, uint32_t* fast, int fb,
-                            uint32_t (&lim)[16], int lane) {
+__device__ bool build_table(const uint8_t* lens, int n, int what, uint16_t* sym, int32_t* base, void* fast_, int fb,
+                            uint32_t* slim, int lane) {
+  uint32_t lim[16];
   uint32_t cnt[16];
 #pragma unroll
   for (int l = 0; l < 16; ++l) cnt[l] = 0;
@@ -108,6 +115,7 @@ __device__ bool build_table(const uint8_t* lens, int n, int what, uint16_t* sym,
     offs[l] = off;
     lim[l] = (code + cnt[l]) << (15 - l);
     if (lane == 0) base[l] = static_cast<int32_t>(off) - static_cast<int32_t>(code);
+    if (lane == 0) slim[l] = lim[l];
     code = (code + cnt[l]) << 1;
     off += cnt[l];
   }
@@ -135,26 +143,27 @@ __device__ bool build_table(const uint8_t* lens, int n, int what, uint16_t* sym,
     for (int l = 1; l < 16; ++l) len += (c15 >= lim[l]) ? 1 : 0;
     uint32_t ent;
     if (len > 15) {
-      ent = kBadEntry;
+      ent = what == 0 ? ((kXSlow << 5) | 1u) : kBadEntry;
     } else if (len > fb) {
-      ent = kBad << 4;  // code length 0: decode canonically (kind bits keep it off the literal path)
+      ent = what == 0 ? (kXSlow << 5) : kSlow;  // code length 0: decode canonically
     } else {
       const int s = sym[base[len] + static_cast<int>(c15 >> (15 - len))];
       const uint32_t L = static_cast<uint32_t>(len);
       if (what == 0) {
-        if (s < 256) ent = L | (kLit << 4) | (static_cast<uint32_t>(s) << 8);
-        else if (s == 256) ent = L | (kEob << 4);
-        else if (s < 286) ent = L | (kLen << 4) | (static_cast<uint32_t>(c_lext[s - 257]) << 8) |
-                                (static_cast<uint32_t>(c_lbase[s - 257]) << 16);
-        else ent = L | (kBad << 4);
+        if (s < 256) ent = L | kLitFlag | (static_cast<uint32_t>(s) << 8);
+        else if (s == 256) ent = L | (kXEob << 5);
+        else if (s < 286) ent = L | (static_cast<uint32_t>(c_lext[s - 257]) << 5) |
+                                (static_cast<uint32_t>(c_lbase[s - 257] - 3) << 8);
+        else ent = L | (kXSlow << 5);  // symbols 286, 287: invalid
       } else if (what == 1) {
         ent = s < 30 ? L | (static_cast<uint32_t>(c_dext[s]) << 8) | (static_cast<uint32_t>(c_dbase[s]) << 16)
-                     : L | (kBad << 4);
+                     : L | kSlow;
       } else {
         ent = L | (static_cast<uint32_t>(s) << 16);
       }
     }
-    fast[e] = ent;
+    if (what == 0) static_cast<uint16_t*>(fast_)[e] = static_cast<uint16_t>(ent);
+    else static_cast<uint32_t*>(fast_)[e] = ent;
   }
   __syncwarp();
   return true;
@@ -296,8 +305,7 @@ __device__ __forceinline__ void flush(const uint8_t* ring, uint8_t* dst, uint32_
 /// The warp's decode loop for one data phase (every lane runs it in lockstep): runs until 1 KB
 /// is ready to flush, the block ends or the stream is invalid. Stored blocks (type 0) copy
 /// `stored` more bytes; else Huffman symbols.
-__device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, const uint32_t (&llim)[16],
-                                          const uint32_t (&dlim)[16], int type, uint32_t& stored, uint32_t flushed,
+__device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, int type, uint32_t& stored, uint32_t flushed,
                                           uint32_t usize, uint32_t csize, int lane) {
   // Output past usize is caught here, before its flush could write outside the chunk (the ring
   // absorbs up to one match past the flush point), or by the trailer's exact-size check.
@@ -328,41 +336,42 @@ __device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, const 
   while (true) {
     br.refill();
     uint32_t e = sm.lfast[br.b & ((1u << kLB) - 1u)];
-    if ((e & 0x30u) == 0) {  // literal with a short code: the hot path
+    if (e & kLitFlag) {  // literal with a short code: the hot path
       br.drop(static_cast<int>(e & 15));
       o.lit(e >> 8);
       if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
       continue;
     }
-    int cl = static_cast<int>(e & 15);
-    if (cl == 0) {  // code longer than the first-level table
-      const int s = canon_decode(br.b, llim, sm.lbase, sm.lsym, cl);
-      if (s < 0) return kRErr;
-      e = s < 256    ? (kLit << 4) | (static_cast<uint32_t>(s) << 8)
-          : s == 256 ? (kEob << 4)
-          : s < 286  ? (kLen << 4) | (static_cast<uint32_t>(c_lext[s - 257]) << 8) |
-                          (static_cast<uint32_t>(c_lbase[s - 257]) << 16)
-                     : (kBad << 4);
+    uint32_t x = (e >> 5) & 7, len;
+    if (x < kXEob) {  // length with a short code
+      br.drop(static_cast<int>(e & 15));
+      len = (e >> 8) + 3 + br.get(static_cast<int>(x));
+    } else {  // cold: end of block, invalid bits, or a code longer than the table
+      int cl = static_cast<int>(e & 15);
+      if (x == kXEob) {
+        br.drop(cl);
+        return kREob;
+      }
+      if (cl != 0) return kRErr;
+      const int s = canon_decode(br.b, sm.llim, sm.lbase, sm.lsym, cl);
+      if (s < 0 || s >= 286) return kRErr;
+      br.drop(cl);
+      if (s == 256) return kREob;
+      if (s < 256) {
+        o.lit(static_cast<uint32_t>(s));
+        if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
+        continue;
+      }
+      len = c_lbase[s - 257] + br.get(c_lext[s - 257]);
     }
-    br.drop(cl);
-    const uint32_t kind = (e >> 4) & 3;
-    if (kind == kLit) {
-      o.lit(e >> 8);
-      if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
-      continue;
-    }
-    if (kind == kEob) return kREob;
-    if (kind == kBad) return kRErr;
-    const uint32_t len = (e >> 16) + br.get(static_cast<int>((e >> 8) & 15));
     br.refill();
     uint32_t de = sm.dfast[br.b & ((1u << kDB) - 1u)];
     int dl = static_cast<int>(de & 15);
-    if (dl == 0) {
-      const int s = canon_decode(br.b, dlim, sm.dbase, sm.dsym, dl);
+    if (de & kSlow) {
+      if (dl != 0) return kRErr;
+      const int s = canon_decode(br.b, sm.dlim, sm.dbase, sm.dsym, dl);
       if (s < 0 || s >= 30) return kRErr;
       de = (static_cast<uint32_t>(c_dext[s]) << 8) | (static_cast<uint32_t>(c_dbase[s]) << 16);
-    } else if (((de >> 4) & 3) == kBad) {
-      return kRErr;
     }
     br.drop(dl);
     const uint32_t dist = (de >> 16) + br.get(static_cast<int>((de >> 8) & 15));
@@ -372,15 +381,12 @@ __device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, const 
   }
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __restrict__ jobs, uint32_t njobs,
+__global__ void __launch_bounds__(kWarps * 32, 8) k_inflate(const InflateJob* __restrict__ jobs, uint32_t njobs,
                                                         unsigned int* err) {
   __shared__ WarpSmem smem[kWarps];
   const int lane = threadIdx.x & 31;
   WarpSmem& sm = smem[threadIdx.x >> 5];
   const uint32_t nwarps = gridDim.x * kWarps;
-  uint32_t llim[16], dlim[16];
-#pragma unroll
-  for (int l = 0; l < 16; ++l) llim[l] = dlim[l] = 0;
 
   for (uint32_t j = blockIdx.x * kWarps + (threadIdx.x >> 5); j < njobs; j += nwarps) {
     const InflateJob job = jobs[j];
@@ -427,10 +433,10 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __
       } else if (type == 1) {  // fixed codes
         for (int i = lane; i < 288; i += 32) sm.lens[i] = i < 144 ? 8 : (i < 256 ? 9 : (i < 280 ? 7 : 8));
         __syncwarp();
-        build_table(sm.lens, 288, 0, sm.lsym, sm.lbase, sm.lfast, kLB, llim, lane);
+        build_table(sm.lens, 288, 0, sm.lsym, sm.lbase, sm.lfast, kLB, sm.llim, lane);
         sm.lens[lane] = 5;
         __syncwarp();
-        build_table(sm.lens, 32, 1, sm.dsym, sm.dbase, sm.dfast, kDB, dlim, lane);
+        build_table(sm.lens, 32, 1, sm.dsym, sm.dbase, sm.dfast, kDB, sm.dlim, lane);
       } else {  // dynamic codes: the code-length code, then both code-length sequences
         br.refill();
         const int hlit = static_cast<int>(br.get(5)) + 257;
@@ -447,7 +453,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __
           sm.lens[c_clorder[i]] = static_cast<uint8_t>(br.get(3));
         }
         __syncwarp();
-        if (!build_table(sm.lens, 19, 2, sm.dsym, sm.dbase, sm.dfast, kCB, dlim, lane)) {
+        if (!build_table(sm.lens, 19, 2, sm.dsym, sm.dbase, sm.dfast, kCB, sm.dlim, lane)) {
           ok = false;
           break;
         }
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __
         while (i < total) {
           br.refill();
           const uint32_t e = sm.dfast[br.b & ((1u << kCB) - 1u)];
-          if (((e >> 4) & 3) == kBad) {  // bits outside the code-length code
+          if (e & kSlow) {  // bits outside the code-length code
             bad = true;
             break;
           }
@@ -499,15 +505,15 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __
           ok = false;
           break;
         }
-        if (!build_table(sm.lens, hlit, 0, sm.lsym, sm.lbase, sm.lfast, kLB, llim, lane) ||
-            !build_table(sm.lens + hlit, hdist, 1, sm.dsym, sm.dbase, sm.dfast, kDB, dlim, lane)) {
+        if (!build_table(sm.lens, hlit, 0, sm.lsym, sm.lbase, sm.lfast, kLB, sm.llim, lane) ||
+            !build_table(sm.lens + hlit, hdist, 1, sm.dsym, sm.dbase, sm.dfast, kDB, sm.dlim, lane)) {
           ok = false;
           break;
         }
       }
       // ---------------- data: the warp decodes; each finished 1 KB is flushed
       while (true) {
-        const int reason = decode_run(br, o, sm, llim, dlim, type, stored, flushed, usize, job.csize, lane);
+        const int reason = decode_run(br, o, sm, type, stored, flushed, usize, job.csize, lane);
         if (reason == kRErr) {
           ok = false;
           break;
@@ -544,13 +550,13 @@ __global__ void __launch_bounds__(kWarps * 32, 6) k_inflate(const InflateJob* __
 void launch_inflate(const InflateJob* d_jobs, uint32_t njobs, unsigned int* d_err, void* stream) {
   if (njobs == 0) return;
   // persistent warps: warp w takes jobs w, w + nwarps, ... (longest first, see plan_batches);
-  // 6 CTAs x 4 warps fit an SM (33 KB of tables + ring per CTA)
+  // 8 CTAs x 4 warps fit an SM (25 KB of tables + ring per CTA, <= 64 registers)
   static bool attr = [] {
     return cudaFuncSetAttribute(k_inflate, cudaFuncAttributePreferredSharedMemoryCarveout,
                                 cudaSharedmemCarveoutMaxShared) == cudaSuccess;
   }();
   (void)attr;
-  const uint32_t blocks = std::min<uint32_t>((njobs + kWarps - 1) / kWarps, 148u * 6u);
+  const uint32_t blocks = std::min<uint32_t>((njobs + kWarps - 1) / kWarps, 148u * 8u);
   k_inflate<<<blocks, kWarps * 32, 0, static_cast<cudaStream_t>(stream)>>>(d_jobs, njobs, d_err);
   count_external_launch();
 }
