@@ -206,6 +206,13 @@ struct Bits {
     b >>= k;
     n -= k;
   }
+  /// Drops a k-bit code and returns the x extra bits after it (k + x <= 32, n >= k + x).
+  __device__ __forceinline__ uint32_t code_extra(int k, int x) {
+    const uint32_t v = (static_cast<uint32_t>(b) >> k) & ((1u << x) - 1u);
+    b >>= k + x;
+    n -= k + x;
+    return v;
+  }
   __device__ __forceinline__ uint64_t consumed() const { return static_cast<uint64_t>(next) * 32ull - n; }
   __device__ __forceinline__ void seek(uint64_t bit) {  // restart at an absolute bit position
     next = static_cast<uint32_t>(bit >> 5);
@@ -344,8 +351,7 @@ __device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, int ty
     }
     uint32_t x = (e >> 5) & 7, len;
     if (x < kXEob) {  // length with a short code
-      br.drop(static_cast<int>(e & 15));
-      len = (e >> 8) + 3 + br.get(static_cast<int>(x));
+      len = (e >> 8) + 3 + br.code_extra(static_cast<int>(e & 15), static_cast<int>(x));
     } else {  // cold: end of block, invalid bits, or a code longer than the table
       int cl = static_cast<int>(e & 15);
       if (x == kXEob) {
@@ -373,10 +379,17 @@ __device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, int ty
       if (s < 0 || s >= 30) return kRErr;
       de = (static_cast<uint32_t>(c_dext[s]) << 8) | (static_cast<uint32_t>(c_dbase[s]) << 16);
     }
-    br.drop(dl);
-    const uint32_t dist = (de >> 16) + br.get(static_cast<int>((de >> 8) & 15));
-    if (dist > o.pos) return kRErr;
-    o.match(len, dist, lane);
+    const uint32_t dist = (de >> 16) + br.code_extra(dl, static_cast<int>((de >> 8) & 15));
+    if (dist >= len && dist <= kRing && len <= 32 && dist <= o.pos) {
+      // the common match: sources in the ring, no overlap with the output, one round
+      if (static_cast<uint32_t>(lane) < len)
+        o.ring[(o.pos + static_cast<uint32_t>(lane)) & kRingMask] = o.ring[(o.pos - dist + static_cast<uint32_t>(lane)) & kRingMask];
+      __syncwarp();
+      o.pos += len;
+    } else {
+      if (dist > o.pos) return kRErr;
+      o.match(len, dist, lane);
+    }
     if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
   }
 }
