@@ -343,11 +343,25 @@ __device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, int ty
   while (true) {
     br.refill();
     uint32_t e = sm.lfast[br.b & ((1u << kLB) - 1u)];
-    if (e & kLitFlag) {  // literal with a short code: the hot path
+    if (e & kLitFlag) {
+      // Literals with short codes, the hot path: a refill leaves >= 33 bits, enough for three
+      // 10-bit lookups; the flush check runs once per group (the ring has room past the limit).
       br.drop(static_cast<int>(e & 15));
       o.lit(e >> 8);
+      e = sm.lfast[br.b & ((1u << kLB) - 1u)];
+      if (e & kLitFlag) {
+        br.drop(static_cast<int>(e & 15));
+        o.lit(e >> 8);
+        e = sm.lfast[br.b & ((1u << kLB) - 1u)];
+        if (e & kLitFlag) {
+          br.drop(static_cast<int>(e & 15));
+          o.lit(e >> 8);
+          if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
+          continue;
+        }
+      }
       if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
-      continue;
+      br.refill();  // the entry in e stays valid: a refill only appends bits
     }
     uint32_t x = (e >> 5) & 7, len;
     if (x < kXEob) {  // length with a short code
