@@ -196,6 +196,14 @@ struct Bits {
       nw = __ldg(w0 + min(next, nlast));
     }
   }
+  /// Appends the prefetched word (n <= 32).
+  __device__ __forceinline__ void refill_now() {
+    __syncwarp();  // (also keeps the rare call sites branches rather than predicated code)
+    b |= static_cast<uint64_t>(nw) << n;
+    n += 32;
+    ++next;
+    nw = __ldg(w0 + min(next, nlast));
+  }
   __device__ __forceinline__ uint32_t get(int k) {  // k <= 32, n >= k
     const uint32_t v = static_cast<uint32_t>(b & ((1ull << k) - 1ull));
     b >>= k;
@@ -361,7 +369,7 @@ __device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, int ty
         }
       }
       if (o.pos >= limit) return o.pos > usize ? kRErr : kRFlush;
-      br.refill();  // the entry in e stays valid: a refill only appends bits
+      if (__builtin_expect(br.n < 15, 0)) br.refill_now();  // (>= 13 bits left) a length code + its extra bits; e stays valid
     }
     uint32_t x = (e >> 5) & 7, len;
     if (x < kXEob) {  // length with a short code
@@ -373,6 +381,7 @@ __device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, int ty
         return kREob;
       }
       if (cl != 0) return kRErr;
+      br.refill();  // a long code + extra bits: <= 20
       const int s = canon_decode(br.b, sm.llim, sm.lbase, sm.lsym, cl);
       if (s < 0 || s >= 286) return kRErr;
       br.drop(cl);
@@ -384,11 +393,13 @@ __device__ __forceinline__ int decode_run(Bits& br, Out& o, WarpSmem& sm, int ty
       }
       len = c_lbase[s - 257] + br.get(c_lext[s - 257]);
     }
-    br.refill();
+    // the 8-bit lookup and a short distance code + its extra bits need <= 21 bits
+    if (__builtin_expect(br.n < 21, 0)) br.refill_now();
     uint32_t de = sm.dfast[br.b & ((1u << kDB) - 1u)];
     int dl = static_cast<int>(de & 15);
     if (de & kSlow) {
       if (dl != 0) return kRErr;
+      br.refill();  // a long code + extra bits: <= 28
       const int s = canon_decode(br.b, sm.dlim, sm.dbase, sm.dsym, dl);
       if (s < 0 || s >= 30) return kRErr;
       de = (static_cast<uint32_t>(c_dext[s]) << 8) | (static_cast<uint32_t>(c_dbase[s]) << 16);
