@@ -181,6 +181,22 @@ void emit_accumulate(std::ostringstream& s, const ScanProgram& P, const char* in
   }
 }
 
+/// CTAs per SM the kernel is compiled for (register cap 65536 / (256 x this)). PSG_JIT_MINB
+/// overrides it (measurement knob).
+int min_blocks(const ScanProgram& P) {
+  static const int env = [] {
+    const char* e = std::getenv("PSG_JIT_MINB");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env > 0) return env;
+  // 6 x 256 threads: 40 registers. At 8 (32 registers) the probe/build programs spill 16-64 B
+  // per thread, and the local-memory stores go through to L2 (8 GB per SF100 probe launch in the
+  // ncu capture); A/B at N=1 SF100: probe kernel 4.47/4.52 -> 4.42/4.35 ms, query 7.90/7.95 ->
+  // 7.74/7.67 ms; 4 CTAs/SM (52 registers, no spills) is slower (5.30 ms).
+  (void)P;
+  return 6;
+}
+
 std::string jit_source(const ScanProgram& P) {
   std::ostringstream s;
   const int nin = P.n_in, nregs = std::max(1, P.n_regs);
@@ -200,7 +216,7 @@ std::string jit_source(const ScanProgram& P) {
   // the next tile's descriptor is prefetched while the current one computes: no block barrier
   // except the compaction prefix of the materialising sinks.
   s << "using namespace psg;\n#define R 4\n"
-    << "extern \"C\" __global__ void __launch_bounds__(256, " << (P.sink == SINK_MATERIALIZE || P.sink == SINK_COUNT ? 6 : 8)
+    << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks(P)
     << ") psg_jit_scan(const __grid_constant__ ScanProgram P, "
        "const Segment* __restrict__ segs, const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {\n";
   if (bscan) s << "  __shared__ uint32_t s_wcnt[8][R], s_woff[8][R];\n  __shared__ unsigned long long s_base;\n";
