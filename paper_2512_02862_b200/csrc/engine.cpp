@@ -437,6 +437,9 @@ class Execution {
   struct Feed;
   Execution(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode, Staged* staged)
       : ctx_(ctx), mode_(mode), staged_(staged), plan_(QueryPlan::from_json_text(plan_json, data_root, ctx.rank, ctx.nranks)) {}
+  ~Execution() {
+    if (build_pending_) cudaStreamSynchronize(ctx_.comm);  // (error paths) before the tables go
+  }
 
   ResultRows run(bool want_rows);
   // local plans (no shuffle): scan -> replicated joins -> global aggregate (the Q6 analog)
@@ -505,6 +508,19 @@ class Execution {
   // agg table
   DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, global_acc_, barrier_word_;
   AggTableDev aggt_{};
+  // the build insert running on ctx_.comm concurrently with the probe side (N > 1 Bloom path)
+  struct Event {
+    cudaEvent_t e = nullptr;
+    Event() { cudaEventCreateWithFlags(&e, cudaEventDisableTiming); }
+    ~Event() {
+      if (e) cudaEventDestroy(e);
+    }
+    Event(const Event&) = delete;
+    Event& operator=(const Event&) = delete;
+    cudaEvent_t get() const { return e; }
+  };
+  Event build_fork_, build_done_;
+  bool build_pending_ = false;
   uint64_t agg_cap_ = 0;
   // stats
   psg_stats st_{};
@@ -1666,8 +1682,30 @@ ResultRows Execution::run(bool want_rows) {
     p.agg = aggt_;
     p.n_sum = static_cast<int>(build_sum_wire.size());
     for (int b = 0; b < p.n_sum; ++b) p.sum_reg[b] = 1 + b;
-    run_scan(p, bview, false);  // also sets the Bloom (or key-bitmap) bits of every inserted key
-    if (semi && krange) {  // disjoint bits: SUM == OR
+    // N > 1 with the Bloom screen: the filter is set from the received keys in a separate pass and
+    // all-gathered first, then the table insert runs on the aux stream while the probe side scans,
+    // semi-join-screens, partitions and shuffles on the compute stream; the compute stream joins
+    // the insert only where the table is first used (consume, or the in-place owner probe).
+    // PSG_BUILD_OVERLAP=0: off.
+    static const bool overlap_env = [] {
+      const char* e = std::getenv("PSG_BUILD_OVERLAP");
+      return !(e && std::string(e) == "0");
+    }();
+    if (semi && !krange && aggt_.bloom && overlap_env) {
+      for (const auto& sg : bsegs) launch_bloom_keys(sg.col[0], sg.rows, aggt_.bloom, aggt_.bloom_shift, ctx_.compute);
+      PSG_CUDA(cudaEventRecord(build_fork_.get(), ctx_.compute));
+      PSG_CUDA(cudaStreamWaitEvent(ctx_.comm, build_fork_.get(), 0));
+      p.agg.bloom = nullptr;
+      if (bview.nsegs) fused_scan(p, bview.d_segs, bview.d_tile_seg, bview.nsegs, bview.ntiles, ctx_.comm);
+      PSG_CUDA(cudaEventRecord(build_done_.get(), ctx_.comm));
+      build_pending_ = true;
+      semi_all = DevBuf(ctx_.pool, static_cast<size_t>(nr) * bloom_words * 4, ctx_.compute);
+      PSG_NCCL(ncclAllGather(agg_bloom_.p, semi_all.p, bloom_words * 4, ncclUint8, ctx_.nccl, ctx_.compute));
+    } else {
+      run_scan(p, bview, false);  // also sets the Bloom (or key-bitmap) bits of every inserted key
+    }
+    if (build_pending_) {
+    } else if (semi && krange) {  // disjoint bits: SUM == OR
       PSG_NCCL(ncclAllReduce(agg_kbits_.p, agg_kbits_.p, (krange + 31) / 32, ncclUint32, ncclSum, ctx_.nccl,
                              ctx_.compute));
     } else if (semi) {
@@ -1721,8 +1759,22 @@ ResultRows Execution::run(bool want_rows) {
     for (int c = 0; c < nc - 1; ++c) t.dev.payload[c] = t.payload[c].as<uint64_t>();
     PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   }
+  // the received build rows stay allocated until the (possibly concurrent) insert has finished
+  std::vector<Received> brecv_hold;
+  DevCols bmat_hold;
+  if (build_pending_) {
+    brecv_hold = std::move(brecv);
+    bmat_hold = std::move(bmat);
+  }
   brecv.clear();
   bmat = DevCols{};
+  auto join_build = [&] {
+    if (!build_pending_) return;
+    PSG_CUDA(cudaStreamWaitEvent(ctx_.compute, build_done_.get(), 0));
+    build_pending_ = false;
+    brecv_hold.clear();
+    bmat_hold = DevCols{};
+  };
 
   pt.mark("build table", ctx_.compute);
   // ---------------- probe side ----------------
@@ -1745,6 +1797,7 @@ ResultRows Execution::run(bool want_rows) {
   ScanProgram pack{};  // bit-packed shuffle rows (pack_n > 0), set up below
   auto consume_materialised = [&](const BatchView& v, int ncols) {
     // v: segments whose columns are p_out order (key first), or one bit-packed word per row
+    join_build();
     if (agg_) {
       ScanProgram p = batch_program(ncols);
       p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
@@ -1924,6 +1977,7 @@ ResultRows Execution::run(bool want_rows) {
       return !(e && std::string(e) == "0");
     }();
     if (nr > 1 && agg_ && grouped_ && jit_available() && self_probe_env && pack.pack_n == 0) {
+      join_build();  // the scan itself probes this rank's table
       pp.self_probe = 1;
       pp.self_rank = ctx_.rank;
       pp.agg = aggt_;
@@ -1969,6 +2023,7 @@ ResultRows Execution::run(bool want_rows) {
       }
     }
   }
+  join_build();
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   st_.storage_phase_s = secs_since(t_storage);
 

@@ -710,6 +710,24 @@ __global__ void k_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uin
     if (atomicOr(bitmap + (d >> 5), bit) & bit) *dup = 1u;
   }
 }
+/// Bloom bits of a key column (the semi-join filter of the received build rows, set ahead of the
+/// table insert so the probe side can start screening while the insert runs).
+__global__ void k_bloom_keys(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* bloom, int shift) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = keys[i];
+    if (key == kEmptyKey) continue;  // null keys are never screened
+    const uint64_t h2 = key * kBloomMul;
+    atomicOr(bloom + (h2 >> shift), bloom_bits(h2, shift));
+  }
+}
+
+void launch_bloom_keys(const uint64_t* keys, uint64_t n, uint32_t* bloom, int shift, void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_bloom_keys<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, n, bloom, shift);
+}
+
 void launch_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uint32_t* bitmap, unsigned int* dup, void* stream) {
   if (n == 0) return;
   count_launch();
