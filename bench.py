@@ -328,7 +328,7 @@ def main():
         achieved = per_launch_bytes / per_launch_s / 1e9
         ach = max_over_ranks(-achieved) * -1 if dist else achieved  # slowest rank
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": ncu_traffic(args.scale), "kernel": "k_scan<4,SINK_PROBE> (lineitem scan+filter+probe+agg)"
+                "traffic": ncu_traffic(args.scale), "kernel": "psg_jit_scan SINK_PROBE (lineitem scan+filter+probe+agg)"
                 if world == 1 else "k_scan<4,SINK_MATERIALIZE> (lineitem scan+filter+partition)",
                 "algorithmic_bytes_per_launch": int(per_launch_bytes), "peak_kind": peak_kind,
                 "kernel_ms_per_launch": round(per_launch_s * 1000, 4),
