@@ -208,7 +208,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-semijoin", action="store_true")
     ap.add_argument("--io-threads", type=int, default=0)
-    ap.add_argument("--batch-mb", type=int, default=64)
+    ap.add_argument("--batch-mb", type=int, default=128)
     ap.add_argument("--codec", default="identity", choices=["identity", "block"],
                     help="PSTO codec of the dataset (block = zlib chunks, inflated on the GPU)")
     args = ap.parse_args()

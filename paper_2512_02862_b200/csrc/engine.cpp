@@ -621,7 +621,13 @@ struct StreamSession {
     const int threads = std::max(1, ctx.io_threads);
     const int pinned = ctx.pinned_slots > 0 ? ctx.pinned_slots : threads * 2 + 2;
     ingest = std::make_unique<Ingest>(ctx, files, batches, threads, slot_bytes, pinned);
-    int nd = static_cast<int>(std::min<size_t>(batches.size(), 8));
+    // HBM ring depth: batches in flight between the readers and the scan. PSG_RING_SLOTS
+    // overrides it (measurement knob).
+    static const int ring_env = [] {
+      const char* e = std::getenv("PSG_RING_SLOTS");
+      return e ? std::atoi(e) : 0;
+    }();
+    int nd = static_cast<int>(std::min<size_t>(batches.size(), ring_env > 0 ? ring_env : 8));
     const uint64_t per_slot = slot_bytes + dslot_bytes;
     if (budget) {
       const uint64_t fixed = ht_reserve + 2 * std::max(slot_bytes, dslot_bytes);  // tables + materialisation transients
