@@ -36,7 +36,7 @@ def main():
         nid = obj[0]
     io = max(2, min(12, (os.cpu_count() or 4) // world))
     ctx = psg.Context(local, rank, world, nid)
-    ctx.set_ingest(io_threads=io, batch_bytes=64 << 20)
+    ctx.set_ingest(io_threads=io, batch_bytes=128 << 20)  # bench.py default
     plan = bench.plan_for([k for k in range(bench.SHARDS) if k % world == rank], io)
     for _ in range(3):  # the last run's timeline stays on disk
         if dist:
