@@ -414,6 +414,7 @@ struct StagedScan {
   size_t tile_off = 0;
   int nsegs = 0;
   uint64_t ntiles = 0, rows = 0, bytes = 0;
+  std::vector<Segment> host_segs;  // the same segments on the host (chunked probe pipeline)
 };
 struct Staged {
   std::string plan_json, data_root;
@@ -466,7 +467,7 @@ class Execution {
                         int part_key_reg, DevBuf* part_counts, bool timed = false);
   DevCols alloc_cols(size_t ncols, uint64_t cap);
   uint64_t read_count(DevCols& c);
-  void run_scan(const ScanProgram& p, const BatchView& v, bool timed);
+  void run_scan(const ScanProgram& p, const BatchView& v, bool timed, cudaStream_t stream = nullptr);
 
   // shuffle (nranks > 1)
   struct Received {
@@ -475,8 +476,8 @@ class Execution {
     uint64_t rows = 0;
   };
   Received exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data,
-                    KeyField kf = KeyField{0, 0, 0});
-  BatchView upload_segments(std::vector<Segment> segs, DevBuf& holder);
+                    KeyField kf = KeyField{0, 0, 0}, cudaStream_t stream = nullptr);
+  BatchView upload_segments(std::vector<Segment> segs, DevBuf& holder, cudaStream_t stream = nullptr);
 
   void build_agg_table(uint64_t build_rows, uint64_t bloom_words);
   void pack_accumulators();
@@ -540,6 +541,8 @@ struct Execution::Feed {
   virtual ~Feed() = default;
   virtual bool next(BatchView& v) = 0;
   virtual void done() = 0;
+  /// Staged scans: the segments on the host (nullptr when streaming).
+  virtual const std::vector<Segment>* host_segments() const { return nullptr; }
   uint64_t total_rows = 0;
   size_t nbatches = 0;
 };
@@ -784,6 +787,7 @@ struct StagedFeed : Execution::Feed {
     return true;
   }
   void done() override {}
+  const std::vector<Segment>* host_segments() const override { return &s->host_segs; }
 };
 
 std::unique_ptr<Execution::Feed> Execution::open_feed(const ScanNode& scan, const std::vector<int>& file_cols) {
@@ -913,12 +917,13 @@ uint64_t Execution::read_count(DevCols& c) {
   return n;
 }
 
-void Execution::run_scan(const ScanProgram& p, const BatchView& v, bool timed) {
+void Execution::run_scan(const ScanProgram& p, const BatchView& v, bool timed, cudaStream_t stream) {
   if (v.nsegs == 0) return;
-  if (timed) PSG_CUDA(cudaEventRecord(ctx_.ev_a, ctx_.compute));
-  fused_scan(p, v.d_segs, v.d_tile_seg, v.nsegs, v.ntiles, ctx_.compute);
+  cudaStream_t st = stream ? stream : ctx_.compute;
+  if (timed) PSG_CUDA(cudaEventRecord(ctx_.ev_a, st));
+  fused_scan(p, v.d_segs, v.d_tile_seg, v.nsegs, v.ntiles, st);
   if (timed) {
-    PSG_CUDA(cudaEventRecord(ctx_.ev_b, ctx_.compute));
+    PSG_CUDA(cudaEventRecord(ctx_.ev_b, st));
     PSG_CUDA(cudaEventSynchronize(ctx_.ev_b));
     float ms = 0;
     PSG_CUDA(cudaEventElapsedTime(&ms, ctx_.ev_a, ctx_.ev_b));
@@ -947,7 +952,8 @@ void Execution::materialize_into(DevCols& out, const ScanProgram& p0, const Batc
   run_scan(p, v, timed);
 }
 
-BatchView Execution::upload_segments(std::vector<Segment> segs, DevBuf& holder) {
+BatchView Execution::upload_segments(std::vector<Segment> segs, DevBuf& holder, cudaStream_t stream) {
+  cudaStream_t st = stream ? stream : ctx_.compute;
   BatchView v;
   const uint64_t T = static_cast<uint64_t>(scan_tile_rows());
   uint64_t tiles = 0;
@@ -959,8 +965,8 @@ BatchView Execution::upload_segments(std::vector<Segment> segs, DevBuf& holder) 
   if (segs.empty()) return v;
   size_t toff = 0;
   auto blob = pack_view(segs, toff);
-  holder = DevBuf(ctx_.pool, blob.size(), ctx_.compute);
-  PSG_CUDA(cudaMemcpyAsync(holder.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, ctx_.compute));
+  holder = DevBuf(ctx_.pool, blob.size(), st);
+  PSG_CUDA(cudaMemcpyAsync(holder.p, blob.data(), blob.size(), cudaMemcpyHostToDevice, st));
   host_keep_.push_back(std::move(blob));  // pageable source must outlive the async copy
   v.d_segs = holder.as<Segment>();
   v.d_tile_seg = reinterpret_cast<const uint32_t*>(holder.as<uint8_t>() + toff);
@@ -1242,45 +1248,46 @@ void Execution::gpu_barrier() {
 
 // ---------------------------------------------------------------------------- shuffle
 Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, DevBuf& part_counts, bool have_data,
-                                        KeyField kf) {
+                                        KeyField kf, cudaStream_t stream) {
+  cudaStream_t st = stream ? stream : ctx_.compute;
   const int n = ctx_.nranks;
   Received rcv;
-  const int tl = ctx_.timeline ? ctx_.timeline->gpu_begin("exchange w" + std::to_string(st_.waves), 4, ctx_.compute) : -1;
+  const int tl = ctx_.timeline ? ctx_.timeline->gpu_begin("exchange w" + std::to_string(st_.waves), 4, st) : -1;
   // dest bases (exclusive scan of the per-destination histogram) and scatter into send regions
-  DevBuf base(ctx_.pool, n * 8, ctx_.compute), cursor(ctx_.pool, n * 8, ctx_.compute);
-  size_t tb = exclusive_scan_u64(nullptr, nullptr, n, nullptr, 0, ctx_.compute);
-  DevBuf tmp(ctx_.pool, tb, ctx_.compute);
-  exclusive_scan_u64(part_counts.as<unsigned long long>(), base.as<unsigned long long>(), n, tmp.p, tb, ctx_.compute);
-  PSG_CUDA(cudaMemsetAsync(cursor.p, 0, n * 8, ctx_.compute));
+  DevBuf base(ctx_.pool, n * 8, st), cursor(ctx_.pool, n * 8, st);
+  size_t tb = exclusive_scan_u64(nullptr, nullptr, n, nullptr, 0, st);
+  DevBuf tmp(ctx_.pool, tb, st);
+  exclusive_scan_u64(part_counts.as<unsigned long long>(), base.as<unsigned long long>(), n, tmp.p, tb, st);
+  PSG_CUDA(cudaMemsetAsync(cursor.p, 0, n * 8, st));
   // counts matrix: allgather of every rank's histogram
-  DevBuf matrix(ctx_.pool, static_cast<size_t>(n) * n * 8, ctx_.compute);
-  PSG_NCCL(ncclAllGather(part_counts.p, matrix.p, n, ncclUint64, ctx_.nccl, ctx_.compute));
+  DevBuf matrix(ctx_.pool, static_cast<size_t>(n) * n * 8, st);
+  PSG_NCCL(ncclAllGather(part_counts.p, matrix.p, n, ncclUint64, ctx_.nccl, st));
   std::vector<uint64_t> m(static_cast<size_t>(n) * n);
-  PSG_CUDA(cudaMemcpyAsync(m.data(), matrix.p, m.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
-  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));  // the one data-dependent host sync per wave
+  PSG_CUDA(cudaMemcpyAsync(m.data(), matrix.p, m.size() * 8, cudaMemcpyDeviceToHost, st));
+  PSG_CUDA(cudaStreamSynchronize(st));  // the one data-dependent host sync per wave
   PhaseTimer xt;
   const int me = ctx_.rank;
   uint64_t nrows = 0;
   for (int d = 0; d < n; ++d) nrows += m[static_cast<size_t>(me) * n + d];
-  DevBuf send(ctx_.pool, std::max<uint64_t>(nrows, 1) * ncols * 8, ctx_.compute);
+  DevBuf send(ctx_.pool, std::max<uint64_t>(nrows, 1) * ncols * 8, st);
   if (have_data && nrows) {
     std::vector<const uint64_t*> in;
     for (int c = 0; c < ncols; ++c) in.push_back(mat.cols[c].as<uint64_t>());
     launch_part_scatter(in.data(), ncols, nrows, key_col, n, base.as<unsigned long long>(),
                         part_counts.as<unsigned long long>(), cursor.as<unsigned long long>(), send.as<uint64_t>(),
-                        ctx_.compute, kf);
+                        st, kf);
   }
   uint64_t rtotal = 0;
   for (int s = 0; s < n; ++s) rtotal += m[static_cast<size_t>(s) * n + me];
-  rcv.buf = DevBuf(ctx_.pool, std::max<uint64_t>(rtotal, 1) * ncols * 8 + 16, ctx_.compute);
+  rcv.buf = DevBuf(ctx_.pool, std::max<uint64_t>(rtotal, 1) * ncols * 8 + 16, st);
   rcv.rows = rtotal;
   PSG_NCCL(ncclGroupStart());
   uint64_t soff = 0, roff = 0;
   for (int p = 0; p < n; ++p) {
     const uint64_t sc = m[static_cast<size_t>(me) * n + p];
     const uint64_t rc = m[static_cast<size_t>(p) * n + me];
-    if (sc) PSG_NCCL(ncclSend(send.as<uint64_t>() + soff * ncols, sc * ncols, ncclUint64, p, ctx_.nccl, ctx_.compute));
-    if (rc) PSG_NCCL(ncclRecv(rcv.buf.as<uint64_t>() + roff * ncols, rc * ncols, ncclUint64, p, ctx_.nccl, ctx_.compute));
+    if (sc) PSG_NCCL(ncclSend(send.as<uint64_t>() + soff * ncols, sc * ncols, ncclUint64, p, ctx_.nccl, st));
+    if (rc) PSG_NCCL(ncclRecv(rcv.buf.as<uint64_t>() + roff * ncols, rc * ncols, ncclUint64, p, ctx_.nccl, st));
     if (rc) {
       Segment sg;
       std::memset(&sg, 0, sizeof sg);
@@ -1293,8 +1300,8 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
     roff += rc;
   }
   PSG_NCCL(ncclGroupEnd());
-  if (tl >= 0) ctx_.timeline->gpu_end(tl, ctx_.compute);
-  xt.mark("  exchange payload", ctx_.compute);
+  if (tl >= 0) ctx_.timeline->gpu_end(tl, st);
+  xt.mark("  exchange payload", st);
   st_.waves += 1;
   return rcv;
 }
@@ -1801,9 +1808,10 @@ ResultRows Execution::run(bool want_rows) {
   auto pfeed = open_feed(*psrc_.scan, file_cols_of(psrc_, pm));
   std::vector<DevCols> joined_parts;  // no-aggregate results
   ScanProgram pack{};  // bit-packed shuffle rows (pack_n > 0), set up below
-  auto consume_materialised = [&](const BatchView& v, int ncols) {
-    // v: segments whose columns are p_out order (key first), or one bit-packed word per row
-    join_build();
+  auto consume_materialised = [&](const BatchView& v, int ncols, cudaStream_t cs = nullptr) {
+    // v: segments whose columns are p_out order (key first), or one bit-packed word per row.
+    // cs: the aux stream of the chunked pipeline (ordered after the table insert already)
+    if (!cs) join_build();
     if (agg_) {
       ScanProgram p = batch_program(ncols);
       p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
@@ -1828,7 +1836,7 @@ ResultRows Execution::run(bool want_rows) {
         for (int s = 0; s < p.n_sum; ++s) p.global_float[1 + s] = aggt_.ps_float[s];
         for (int b = 0; b < aggt_.nbs; ++b) p.global_float[1 + p.n_sum + b] = aggt_.bs_float[b];
       }
-      run_scan(p, v, false);
+      run_scan(p, v, false, cs);
     } else {
       // compact, then expanding join against the final CSR table
       DevCols c = alloc_cols(ncols, std::max<uint64_t>(v.rows, 1));
@@ -1994,6 +2002,85 @@ ResultRows Execution::run(bool want_rows) {
     }
     const std::vector<int> mat_out = pack.pack_n ? std::vector<int>{p_out[0]} : p_out;
     const KeyField kf = pack.pack_n ? KeyField{pack.pack_min[0], pack.pack_mask[0], 0} : KeyField{0, 0, 0};
+    // Staged probe side at N > 1: the scan is cut into K chunks of whole segments; chunk k+1's
+    // scan/screen/partition kernel runs on the compute stream while chunk k is exchanged (counts,
+    // scatter, NCCL send/recv) and consumed into the table on the aux stream, so the shuffle and
+    // the table probes could overlap the scan. K is the same on every rank (collective order).
+    // Parity-green (scripts/mgpu_check.py staged runs) but measured slower, so off by default:
+    // N=2 SF100 5.98 ms unchunked vs 7.0-7.3 (K=2, 4) and 6.85 (K=8) - the persistent scan grid
+    // holds every SM until it ends, so the NCCL and consume kernels on the aux stream wait for it
+    // anyway, and each chunk adds a count all-gather, a host sync and a send/recv round.
+    // PSG_PROBE_CHUNKS: K (default 1 = off).
+    static const int probe_chunks = [] {
+      const char* e = std::getenv("PSG_PROBE_CHUNKS");
+      return e ? std::max(1, std::atoi(e)) : 1;
+    }();
+    const std::vector<Segment>* hsegs = pfeed->host_segments();
+    if (nr > 1 && agg_ && hsegs != nullptr && waves == 1 && probe_chunks > 1) {
+      const int K = probe_chunks;
+      BatchView whole;
+      if (pfeed->next(whole)) st_.ingest_bytes += whole.bytes;
+      std::vector<std::vector<Segment>> parts(K);
+      uint64_t tot = 0, acc = 0;
+      for (const auto& sg : *hsegs) tot += sg.rows;
+      int k = 0;
+      for (const auto& sg : *hsegs) {
+        while (k < K - 1 && acc >= tot * static_cast<uint64_t>(k + 1) / K) ++k;
+        parts[k].push_back(sg);
+        acc += sg.rows;
+      }
+      struct Evs {
+        std::vector<cudaEvent_t> e;
+        Evs(size_t n, unsigned flags) : e(n) {
+          for (auto& x : e) cudaEventCreateWithFlags(&x, flags);
+        }
+        ~Evs() {
+          for (auto x : e) cudaEventDestroy(x);
+        }
+      };
+      Evs done(K + 1, cudaEventDisableTiming), t0(K, cudaEventDefault), t1(K, cudaEventDefault);
+      std::vector<DevBuf> seg_hold(K), rholds(K);
+      std::vector<BatchView> views(K);
+      for (int c = 0; c < K; ++c) views[c] = upload_segments(parts[c], seg_hold[c]);
+      std::vector<DevCols> mats;
+      std::vector<DevBuf> pcs;
+      std::vector<Received> recvs;
+      mats.reserve(K), pcs.reserve(K), recvs.reserve(K);
+      // the aux stream starts after everything queued so far (tables, filters, segment tables)
+      PSG_CUDA(cudaEventRecord(done.e[K], ctx_.compute));
+      PSG_CUDA(cudaStreamWaitEvent(ctx_.comm, done.e[K], 0));
+      auto launch_chunk = [&](int c) {
+        mats.push_back(alloc_cols(mat_out.size(), std::max<uint64_t>(views[c].rows, 1)));
+        pcs.emplace_back(ctx_.pool, nr * 8, ctx_.compute);
+        PSG_CUDA(cudaMemsetAsync(pcs[c].p, 0, nr * 8, ctx_.compute));
+        PSG_CUDA(cudaEventRecord(t0.e[c], ctx_.compute));
+        materialize_into(mats[c], pp, views[c], mat_out, p_out[0], &pcs[c], false);
+        PSG_CUDA(cudaEventRecord(t1.e[c], ctx_.compute));
+        PSG_CUDA(cudaEventRecord(done.e[c], ctx_.compute));
+      };
+      launch_chunk(0);
+      for (int c = 0; c < K; ++c) {
+        if (c + 1 < K) launch_chunk(c + 1);
+        PSG_CUDA(cudaStreamWaitEvent(ctx_.comm, done.e[c], 0));
+        recvs.push_back(exchange(mats[c], static_cast<int>(mat_out.size()), 0, pcs[c], views[c].nsegs > 0, kf, ctx_.comm));
+        BatchView rv = upload_segments(recvs[c].segs, rholds[c], ctx_.comm);
+        consume_materialised(rv, static_cast<int>(mat_out.size()), ctx_.comm);
+      }
+      PSG_CUDA(cudaEventRecord(done.e[K], ctx_.comm));
+      PSG_CUDA(cudaStreamWaitEvent(ctx_.compute, done.e[K], 0));
+      join_build();
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      for (int c = 0; c < K; ++c) {
+        if (!views[c].nsegs) continue;
+        float ms = 0;
+        PSG_CUDA(cudaEventElapsedTime(&ms, t0.e[c], t1.e[c]));
+        st_.probe_kernel_ms += ms;
+        st_.probe_kernel_launches += 1;
+      }
+      st_.probe_kernel_bytes += whole.bytes;
+      pt.mark("  probe chunks (scan | exchange + consume)", ctx_.compute);
+      waves = 0;
+    }
     for (uint64_t w = 0; w < waves; ++w) {
       BatchView v;
       const bool have = pfeed->next(v);
@@ -2306,6 +2393,7 @@ void Execution::stage(Staged& st) {
       tiles += (s.rows + T - 1) / T;
     }
     ss.nsegs = static_cast<int>(all.size());
+    ss.host_segs = all;
     ss.ntiles = tiles;
     ss.rows = sb.total_rows;
     ss.bytes = data_bytes;

@@ -26,7 +26,7 @@ from oracle import plan_oracle as po  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--scale", type=float, default=0.1)
-    ap.add_argument("--modes", default="overlapped,blocking")
+    ap.add_argument("--modes", default="overlapped,blocking,staged")
     ap.add_argument("--fuzz", type=int, default=30, help="random plans (tests/test_gpu_fuzz.py) checked per node")
     ap.add_argument("--sf10", action="store_true", help="BASELINE config 2: canonical Q3 at SF10 vs the reference")
     a = ap.parse_args()
@@ -44,6 +44,17 @@ def main():
     ctx.set_ingest(io_threads=4, batch_bytes=2 << 20)
     failures = []
     datasets = {}
+
+    def run(plan, d, mode="overlapped"):
+        """execute_plan in a streaming mode, or stage_plan + run ("staged": HBM-resident inputs,
+        the chunked probe pipeline at N > 1)."""
+        if mode == "staged":
+            st = ctx.stage_plan(plan, d)
+            try:
+                return st.run()
+            finally:
+                st.free()
+        return ctx.execute_plan(plan, d, mode)
 
     def data(scale, seed=42, rg=1 << 20, devices=None):
         key = (scale, seed, rg, devices)
@@ -75,7 +86,7 @@ def main():
             plan = golden["plans"][pname]
             for mode in a.modes.split(","):
                 try:
-                    res = ctx.execute_plan(plan, d, mode)
+                    res = run(plan, d, mode)
                     mine = (res.schema, res.rows.copy())
                 except psg.PsgError as e:
                     mine = ("error", str(e))
@@ -104,8 +115,8 @@ def main():
     # count, so the union over ranks must equal the reference's SF10 golden
     if a.sf10:
         d = data(10.0, 42, 1 << 20)
-        for mode in ("overlapped", "blocking"):
-            res = ctx.execute_plan(golden["plans"]["canonical"], d, mode)
+        for mode in ("overlapped", "blocking", "staged"):
+            res = run(golden["plans"]["canonical"], d, mode)
             allres = [None] * world
             dist.all_gather_object(allres, (res.schema, res.rows.copy()))
             if rank == 0:
@@ -128,7 +139,7 @@ def main():
         for seed in range(a.fuzz):
             plan = fz.random_plan(random.Random(seed))
             try:
-                res = ctx.execute_plan(plan, d)
+                res = run(plan, d, "staged" if seed % 2 else "overlapped")
                 mine = (res.schema, res.rows.copy())
             except psg.PsgError as e:
                 mine = ("error", str(e))
