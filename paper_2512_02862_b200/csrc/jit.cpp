@@ -34,6 +34,7 @@ namespace {
 struct Compiled {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
+  int block = kBlock;  // threads per CTA (jit_block)
   int per_sm = 1;
   bool ok = false;
 };
@@ -181,6 +182,27 @@ void emit_accumulate(std::ostringstream& s, const ScanProgram& P, const char* in
   }
 }
 
+/// Rows per thread per tile (R) of the kernel: R x 32 rows per warp, 1024 / (32 R) warps per
+/// block (a tile is always 1024 rows).
+int jit_rows(const ScanProgram& P) {
+  // PSG_JIT_R: 4 | 8 (every program) | p (probe sinks at 8: default) | pm (probe + materialise).
+  // The probe programs are latency-bound on their chain of dependent loads (predicate, key
+  // bitmap, home slot, sums): 8 rows per thread at 64 registers (4 warps x 8 CTAs per SM) keep
+  // 8192 rows in flight per SM vs 6144 at R = 4, 40 registers, 6 x 8 warps. Measured SF100:
+  // N=1 query 7.69/7.64 -> 7.49/7.44 ms (probe kernel 4.37/4.41 -> 4.23/4.20), N=2 6.00 -> 5.95;
+  // the partitioning materialise programs are slower at R = 8 (N=2 probe-side scan 2.15 -> 2.68).
+  static const std::string env = [] {
+    const char* e = std::getenv("PSG_JIT_R");
+    return std::string(e ? e : "p");
+  }();
+  if (env == "8") return 8;
+  const bool probe = P.sink == SINK_PROBE || P.sink == SINK_PROBE_GLOBAL;
+  if (env == "p") return probe ? 8 : 4;
+  if (env == "pm") return probe || P.sink == SINK_MATERIALIZE ? 8 : 4;
+  return 4;
+}
+int jit_block(const ScanProgram& P) { return 1024 / jit_rows(P); }
+
 /// CTAs per SM the kernel is compiled for (register cap 65536 / (256 x this)). PSG_JIT_MINB
 /// overrides it (measurement knob).
 int min_blocks(const ScanProgram& P) {
@@ -193,8 +215,7 @@ int min_blocks(const ScanProgram& P) {
   // per thread, and the local-memory stores go through to L2 (8 GB per SF100 probe launch in the
   // ncu capture); A/B at N=1 SF100: probe kernel 4.47/4.52 -> 4.42/4.35 ms, query 7.90/7.95 ->
   // 7.74/7.67 ms; 4 CTAs/SM (52 registers, no spills) is slower (5.30 ms).
-  (void)P;
-  return 6;
+  return jit_rows(P) == 8 ? 8 : 6;
 }
 
 std::string jit_source(const ScanProgram& P) {
@@ -215,19 +236,20 @@ std::string jit_source(const ScanProgram& P) {
   // Tile descriptors are fetched per warp into registers (lane c holds column c's pointer) and
   // the next tile's descriptor is prefetched while the current one computes: no block barrier
   // except the compaction prefix of the materialising sinks.
-  s << "using namespace psg;\n#define R 4\n"
-    << "extern \"C\" __global__ void __launch_bounds__(256, " << min_blocks(P)
+  const int RR = jit_rows(P), NT = jit_block(P), NW = NT / 32;
+  s << "using namespace psg;\n#define R " << RR << "\n"
+    << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << min_blocks(P)
     << ") psg_jit_scan(const __grid_constant__ ScanProgram P, "
        "const Segment* __restrict__ segs, const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {\n";
-  if (bscan) s << "  __shared__ uint32_t s_wcnt[8][R], s_woff[8][R];\n  __shared__ unsigned long long s_base;\n";
-  if (wstage) s << "  __shared__ uint64_t s_stg[8][" << P.n_out << "][128];\n";
+  if (bscan) s << "  __shared__ uint32_t s_wcnt[" << NW << "][R], s_woff[" << NW << "][R];\n  __shared__ unsigned long long s_base;\n";
+  if (wstage) s << "  __shared__ uint64_t s_stg[" << NW << "][" << P.n_out << "][128];\n";
   if (part) s << "  __shared__ unsigned long long s_part[" << kMaxParts << "];\n";
   if (glob) s << "  __shared__ unsigned long long s_gacc[" << nglob << "];\n";
-  s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  const int wrow = warp * 128 + lane;\n"
+  s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  const int wrow = warp * (R * 32) + lane;\n"
     << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep; (void)wrow;\n";
-  if (part) s << "  for (int i = tid; i < " << kMaxParts << "; i += 256) s_part[i] = 0;\n";
+  if (part) s << "  for (int i = tid; i < " << kMaxParts << "; i += " << NT << ") s_part[i] = 0;\n";
   if (glob) {
-    s << "  for (int i = tid; i < " << nglob << "; i += 256) s_gacc[i] = 0;\n";
+    s << "  for (int i = tid; i < " << nglob << "; i += " << NT << ") s_gacc[i] = 0;\n";
     for (int i = 0; i < nglob; ++i)
       s << "  " << (P.global_float[i] ? "double" : "unsigned long long") << " g" << i << " = 0;\n";
   }
@@ -251,9 +273,9 @@ std::string jit_source(const ScanProgram& P) {
     << "    const uint64_t next = tile + gridDim.x;\n"
     << "    const uint64_t* pf_col = nullptr; uint64_t pf_r0 = 0; int pf_rows = 0;\n"
     << "    if (next < ntiles) fetch(next, pf_col, pf_r0, pf_rows);\n"
-    << "    const uint64_t row0 = cur_r0;\n    const int nrows = cur_rows - warp * 128;\n"
+    << "    const uint64_t row0 = cur_r0;\n    const int nrows = cur_rows - warp * (R * 32);\n"
     << "    uint32_t pass = 0;\n#pragma unroll\n    for (int r = 0; r < R; ++r) if (r * 32 + lane < nrows) pass |= 1u << r;\n";
-  for (int r = 0; r < nregs; ++r) s << "    uint64_t " << V(r) << "[R] = {0, 0, 0, 0};\n";
+  for (int r = 0; r < nregs; ++r) s << "    uint64_t " << V(r) << "[R] = {};\n";
   // Phase A: predicate columns + atoms. The early (key) columns are loaded in the same phase, for
   // every valid row: a selective-enough predicate still touches nearly every 32-byte sector of
   // them, and their loads then overlap the predicate loads instead of waiting on the filter
@@ -446,7 +468,7 @@ std::string jit_source(const ScanProgram& P) {
       s << "    uint32_t ballots[R];\n#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
         << "      ballots[r] = __ballot_sync(0xffffffffu, (pass >> r) & 1u);\n"
         << "      if (lane == 0) s_wcnt[warp][r] = __popc(ballots[r]); }\n    __syncthreads();\n"
-        << "    if (tid == 0) { uint32_t acc = 0;\n      for (int w = 0; w < 8; ++w) for (int r = 0; r < R; ++r) { s_woff[w][r] = acc; acc += s_wcnt[w][r]; }\n";
+        << "    if (tid == 0) { uint32_t acc = 0;\n      for (int w = 0; w < " << NW << "; ++w) for (int r = 0; r < R; ++r) { s_woff[w][r] = acc; acc += s_wcnt[w][r]; }\n";
       if (P.sink == SINK_COUNT)
         s << "      P.tile_counts[tile] = acc;\n";
       else if (P.tile_offsets)
@@ -477,7 +499,7 @@ std::string jit_source(const ScanProgram& P) {
   s << "    cur_col = pf_col; cur_r0 = pf_r0; cur_rows = pf_rows;\n  }\n";
   if (wstage) s << "  flush();\n";
   if (part)
-    s << "  __syncthreads();\n  for (int i = tid; i < P.nparts; i += 256) if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
+    s << "  __syncthreads();\n  for (int i = tid; i < P.nparts; i += " << NT << ") if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
   if (glob) {
     for (int i = 0; i < nglob; ++i) {
       if (P.global_float[i])
@@ -485,7 +507,7 @@ std::string jit_source(const ScanProgram& P) {
       else
         s << "  atomicAdd(&s_gacc[" << i << "], g" << i << ");\n";
     }
-    s << "  __syncthreads();\n  for (int i = tid; i < " << nglob << "; i += 256) {\n"
+    s << "  __syncthreads();\n  for (int i = tid; i < " << nglob << "; i += " << NT << ") {\n"
       << "    if (P.global_float[i]) atomicAdd(reinterpret_cast<double*>(&P.global_acc[i]), "
          "__longlong_as_double(static_cast<long long>(s_gacc[i])));\n"
       << "    else atomicAdd(&P.global_acc[i], s_gacc[i]); }\n";
@@ -521,8 +543,9 @@ bool nvrtc_cubin(const std::string& body, std::string& cubin, std::string& log) 
   return true;
 }
 
-Compiled compile(const std::string& body, int device) {
+Compiled compile(const std::string& body, int device, int block) {
   Compiled c;
+  c.block = block;
   const auto t0 = std::chrono::steady_clock::now();
   std::string cubin, log;
   if (const char* dir = std::getenv("PSG_JIT_DUMP")) {
@@ -547,7 +570,7 @@ Compiled compile(const std::string& body, int device) {
     return c;
   }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(c.kern), kBlock, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(c.kern), c.block, 0) !=
           cudaSuccess ||
       per_sm < 1) {
     cudaGetLastError();
@@ -581,7 +604,7 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
       std::lock_guard<std::mutex> lk(g_mu);
       auto key = std::make_pair(dev, body);
       auto it = g_cache.find(key);
-      if (it == g_cache.end()) it = g_cache.emplace(key, compile(body, dev)).first;
+      if (it == g_cache.end()) it = g_cache.emplace(key, compile(body, dev, jit_block(P))).first;
       c = it->second;
     }
     if (c.ok) {
@@ -592,7 +615,7 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
       void* args[] = {const_cast<ScanProgram*>(&P), const_cast<Segment**>(&d_segs), const_cast<uint32_t**>(&d_tile_seg),
                       &ntiles};
       count_external_launch();
-      PSG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(c.kern), dim3(static_cast<unsigned>(grid)), dim3(kBlock),
+      PSG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(c.kern), dim3(static_cast<unsigned>(grid)), dim3(c.block),
                                 args, 0, stream));
       return;
     }
