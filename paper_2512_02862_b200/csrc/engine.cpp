@@ -1718,6 +1718,7 @@ ResultRows Execution::run(bool want_rows) {
       run_scan(p, bview, false);  // also sets the Bloom (or key-bitmap) bits of every inserted key
     }
     if (build_pending_) {
+      // (the Bloom filters were all-gathered above)
     } else if (semi && krange) {  // disjoint bits: SUM == OR
       PSG_NCCL(ncclAllReduce(agg_kbits_.p, agg_kbits_.p, (krange + 31) / 32, ncclUint32, ncclSum, ctx_.nccl,
                              ctx_.compute));
