@@ -108,6 +108,10 @@ struct AggTableDev {
   uint64_t packed_mask[kMaxSums];
   int64_t packed_min[kMaxSums];
   uint64_t hits_mask;
+  // Rank-indexed table (one GPU, unique dense build keys; krank != nullptr): the slot of a key is
+  // its rank among the build keys, krank[w] + popc(kbits64[w] below the key's bit) for 64-bit
+  // bitmap word w, so slots [0, mask] are all occupied in key order and nothing is hashed.
+  const uint32_t* krank;
 };
 
 /// Hit count and probe-side sum p of a hot slot (decodes the packed accumulator).
@@ -223,6 +227,13 @@ __device__ __forceinline__ uint32_t bloom_bits(uint64_t h2, int bshift) {
   return (1u << ((h2 >> (bshift - 5)) & 31)) | (1u << ((h2 >> (bshift - 10)) & 31)) |
          (1u << ((h2 >> (bshift - 15)) & 31));
 }
+/// Rank-indexed table: the slot of key (a build key) from the 64-bit view of the key bitmap.
+__device__ __forceinline__ uint64_t agg_rank_slot(const AggTableDev& t, uint64_t key) {
+  const uint64_t d = key - static_cast<uint64_t>(t.kmin);
+  const uint64_t w = __ldg(reinterpret_cast<const unsigned long long*>(t.kbits) + (d >> 6));
+  return __ldg(t.krank + (d >> 6)) + __popcll(w & ((1ULL << (d & 63)) - 1ULL));
+}
+
 __device__ __forceinline__ bool agg_kbit(const AggTableDev& t, uint64_t key) {
   const uint64_t d = key - static_cast<uint64_t>(t.kmin);
   return d < t.krange && ((__ldg(t.kbits + (d >> 5)) >> (d & 31)) & 1u);
@@ -269,6 +280,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ uint32_t ldg_keep_u32(const uint32_t* p, uint64_t policy) {
   uint32_t v;
   asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(policy));
+  return v;
+}
+__device__ __forceinline__ uint64_t ldg_keep_u64(const void* p, uint64_t policy) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(policy));
   return v;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -479,7 +479,7 @@ class Execution {
                     KeyField kf = KeyField{0, 0, 0}, cudaStream_t stream = nullptr);
   BatchView upload_segments(std::vector<Segment> segs, DevBuf& holder, cudaStream_t stream = nullptr);
 
-  void build_agg_table(uint64_t build_rows, uint64_t bloom_words);
+  void build_agg_table(uint64_t build_rows, uint64_t bloom_words, uint64_t rank_slots = 0);
   void pack_accumulators();
   bool build_symmetric_agg_table(uint64_t max_rows, bool bloom);
   void gpu_barrier();
@@ -507,7 +507,7 @@ class Execution {
   };
   std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
   // agg table
-  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, global_acc_, barrier_word_;
+  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, agg_krank_, global_acc_, barrier_word_;
   AggTableDev aggt_{};
   // the build insert running on ctx_.comm concurrently with the probe side (N > 1 Bloom path)
   struct Event {
@@ -1099,19 +1099,21 @@ void Execution::build_local_tables() {
 }
 
 // --------------------------------------------------------------------------- agg table
-void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words) {
-  agg_cap_ = pow2_at_least(std::max<uint64_t>(2 * build_rows, 16));
+void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words, uint64_t rank_slots) {
+  // rank_slots > 0: rank-indexed table of exactly that many slots (+ the spill slot), written
+  // whole by the rank build (no init pass, no hashing)
+  agg_cap_ = rank_slots ? rank_slots : pow2_at_least(std::max<uint64_t>(2 * build_rows, 16));
   const int nps = static_cast<int>(probe_sum_wire.size()), nbs = static_cast<int>(build_sum_wire.size());
   int hw = 2 + nps;
   hw = hw <= 2 ? 2 : (hw <= 4 ? 4 : 8 * ((hw + 7) / 8));
-  const int cw = 1 + nbs;
+  const int cw = rank_slots ? (2 + nbs) & ~1 : 1 + nbs;  // rank table: even (16-byte stores)
   agg_hot_ = DevBuf(ctx_.pool, (agg_cap_ + 1) * hw * 8, ctx_.compute);
   agg_cold_ = DevBuf(ctx_.pool, (agg_cap_ + 1) * cw * 8, ctx_.compute);
   std::memset(&aggt_, 0, sizeof aggt_);
   aggt_.hot = agg_hot_.as<uint64_t>();
   aggt_.cold = agg_cold_.as<uint64_t>();
   aggt_.mask = agg_cap_ - 1;
-  aggt_.shift = shift_of(agg_cap_);
+  aggt_.shift = rank_slots ? 0 : shift_of(agg_cap_);
   aggt_.hw = hw;
   aggt_.cw = cw;
   aggt_.nps = nps;
@@ -1127,7 +1129,7 @@ void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words) {
     aggt_.bloom_mask = bloom_words - 1;
     aggt_.bloom_shift = shift_of(bloom_words);
   }
-  launch_agg_init(aggt_, agg_cap_, ctx_.compute);
+  if (!rank_slots) launch_agg_init(aggt_, agg_cap_, ctx_.compute);
 }
 
 /// Bit-packed accumulators: the footer zone maps bound every int probe-side sum column and the
@@ -1679,14 +1681,48 @@ ResultRows Execution::run(bool want_rows) {
         bloom_words = 0;
       }
     }
-    build_agg_table(build_rows, bloom_words);
+    // Rank-indexed table (one GPU, grouped, unique dense build keys): the key bitmap is set from
+    // the build keys first (with a duplicate check) and its 64-bit words' popcount prefix turns a
+    // key into its rank = its slot; the table is then exactly one slot per build key in key
+    // order, written by plain stores. PSG_RANK_TABLE=0: the hashed table.
+    static const bool rank_env = [] {
+      const char* e = std::getenv("PSG_RANK_TABLE");
+      return !(e && e[0] == '0');
+    }();
+    bool rank_mode = false;
+    const uint64_t kwords64 = (krange + 63) / 64;
+    if (nr == 1 && krange && grouped_ && rank_env && krange_lo != LLONG_MIN && !p2p &&
+        kwords64 < (1ULL << 32) && bmat.rows < (1ULL << 32)) {
+      agg_kbits_ = DevBuf(ctx_.pool, kwords64 * 8, ctx_.compute);
+      DevBuf dup(ctx_.pool, 4, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, kwords64 * 8, ctx_.compute));
+      PSG_CUDA(cudaMemsetAsync(dup.p, 0, 4, ctx_.compute));
+      launch_bitmap_set(bmat.cols[0].as<uint64_t>(), bmat.rows, krange_lo, agg_kbits_.as<uint32_t>(),
+                        dup.as<unsigned int>(), ctx_.compute);
+      unsigned int d = 1;
+      PSG_CUDA(cudaMemcpyAsync(&d, dup.p, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      if (!d) {
+        DevBuf cnt(ctx_.pool, kwords64 * 4, ctx_.compute);
+        agg_krank_ = DevBuf(ctx_.pool, kwords64 * 4, ctx_.compute);
+        launch_popc64(agg_kbits_.as<unsigned long long>(), kwords64, cnt.as<uint32_t>(), ctx_.compute);
+        const size_t tb = exclusive_scan_u32(nullptr, nullptr, kwords64, nullptr, 0, ctx_.compute);
+        DevBuf tmp(ctx_.pool, tb, ctx_.compute);
+        exclusive_scan_u32(cnt.as<uint32_t>(), agg_krank_.as<uint32_t>(), kwords64, tmp.p, tb, ctx_.compute);
+        rank_mode = true;
+      }
+    }
+    build_agg_table(build_rows, bloom_words, rank_mode ? bmat.rows : 0);
     if (krange) {
-      const uint64_t words = (krange + 31) / 32;
-      agg_kbits_ = DevBuf(ctx_.pool, words * 4, ctx_.compute);
-      PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, words * 4, ctx_.compute));
+      if (!rank_mode) {
+        const uint64_t words = (krange + 31) / 32;
+        agg_kbits_ = DevBuf(ctx_.pool, words * 4, ctx_.compute);
+        PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, words * 4, ctx_.compute));
+      }
       aggt_.kbits = agg_kbits_.as<uint32_t>();
       aggt_.kmin = krange_lo;
       aggt_.krange = krange;
+      if (rank_mode) aggt_.krank = agg_krank_.as<uint32_t>();
     }
     pack_accumulators();
     pt.mark("  agg alloc+init", ctx_.compute);
@@ -1704,7 +1740,11 @@ ResultRows Execution::run(bool want_rows) {
       const char* e = std::getenv("PSG_BUILD_OVERLAP");
       return !(e && std::string(e) == "0");
     }();
-    if (semi && !krange && aggt_.bloom && overlap_env) {
+    if (rank_mode) {
+      RankSums rs{};
+      for (int b = 0; b < p.n_sum; ++b) rs.col[b] = bmat.cols[1 + b].as<uint64_t>();
+      launch_rank_build(aggt_, bmat.cols[0].as<uint64_t>(), rs, bmat.rows, ctx_.compute);
+    } else if (semi && !krange && aggt_.bloom && overlap_env) {
       for (const auto& sg : bsegs) launch_bloom_keys(sg.col[0], sg.rows, aggt_.bloom, aggt_.bloom_shift, ctx_.compute);
       PSG_CUDA(cudaEventRecord(build_fork_.get(), ctx_.compute));
       PSG_CUDA(cudaStreamWaitEvent(ctx_.comm, build_fork_.get(), 0));

@@ -335,6 +335,23 @@ std::string jit_source(const ScanProgram& P) {
   } else if (P.remote && P.sink == SINK_BUILD) {
     emit_loads(s, P.n_early, P.n_in);
     emit_remote_build(s, P);
+  } else if (probe && P.agg.krank != nullptr && P.sink == SINK_PROBE) {
+    // Rank-indexed table: the key's 64-bit bitmap word and its block prefix (both L2-resident)
+    // give membership and the slot at once - no hashing, no collision chain.
+    s << "    { const AggTableDev& T = P.agg; uint64_t sl[R]; unsigned long long bw[R]; uint32_t bp[R], bb[R];\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bp[r] = 0; bb[r] = 0; const uint64_t key = " << V(P.key_reg) << "[r];\n"
+      << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+      << "          if (d < T.krange) { bb[r] = static_cast<uint32_t>(d & 63);\n"
+      << "            bw[r] = ldg_keep_u64(reinterpret_cast<const unsigned long long*>(T.kbits) + (d >> 6), pol_keep);\n"
+      << "            bp[r] = ldg_keep_u32(T.krank + (d >> 6), pol_keep); } } }\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0;\n"
+      << "        if (!((bw[r] >> bb[r]) & 1ULL)) pass &= ~(1u << r);\n"
+      << "        else sl[r] = bp[r] + static_cast<uint64_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n";
+    emit_loads(s, P.n_early, P.n_in);
+    s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+      << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
+    emit_accumulate(s, P, "        ");
+    s << "      }\n    }\n";
   } else if (probe) {
     const bool bloom = P.agg.bloom != nullptr && P.agg.kbits == nullptr;
     if (P.agg.kbits != nullptr)  // exact membership of dense build keys; all R words in flight first
@@ -695,6 +712,8 @@ int jit_selftest(std::string& log) {
     if (sink == SINK_PROBE) {  // exact membership bitmap instead of the Bloom filter
       ScanProgram q = p;
       q.agg.kbits = reinterpret_cast<uint32_t*>(16);
+      progs.push_back(q);
+      q.agg.krank = reinterpret_cast<const uint32_t*>(16);  // rank-indexed table
       progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // consuming packed rows

@@ -710,6 +710,46 @@ __global__ void k_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uin
     if (atomicOr(bitmap + (d >> 5), bit) & bit) *dup = 1u;
   }
 }
+/// Rank-indexed aggregation table build (unique dense build keys, one GPU): row i of the build
+/// side lands in the slot of its key's rank - plain stores, no CAS, every slot written once.
+/// Build-side double sums are stored as 0.0 + v (the value a hash-table insert accumulates).
+__global__ void k_rank_build(AggTableDev t, const uint64_t* __restrict__ keys, RankSums bs, uint64_t n) {
+  const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (tid == 0) {  // the spill slot (slot n) is never occupied
+    for (int k = 0; k < t.hw; ++k) t.hot[n * t.hw + k] = 0;
+    for (int k = 0; k < t.cw; ++k) t.cold[n * t.cw + k] = 0;
+  }
+  // hw and cw are even here (the rank table pads cw): whole 16-byte stores, full sectors
+  for (uint64_t i = tid; i < n; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t key = keys[i];
+    uint64_t cv[2 * kMaxSums + 2];
+    cv[0] = 0;
+#pragma unroll
+    for (int b = 0; b < kMaxSums; ++b) {
+      if (b >= t.nbs) break;
+      const uint64_t v = bs.col[b][i];
+      cv[1 + b] = t.bs_float[b]
+                      ? static_cast<uint64_t>(__double_as_longlong(0.0 + __longlong_as_double(static_cast<long long>(v))))
+                      : v;
+    }
+    const uint64_t r = agg_rank_slot(t, key);
+    ulonglong2* h = reinterpret_cast<ulonglong2*>(t.hot + r * t.hw);
+    h[0] = make_ulonglong2(key, 0ULL);
+    for (int k = 1; k < t.hw / 2; ++k) h[k] = make_ulonglong2(0ULL, 0ULL);
+    ulonglong2* c = reinterpret_cast<ulonglong2*>(t.cold + r * t.cw);
+#pragma unroll
+    for (int k = 0; k < kMaxSums + 1; ++k) {
+      if (2 * k >= t.cw) break;
+      c[k] = make_ulonglong2(cv[2 * k], 1 + 2 * k <= t.nbs ? cv[2 * k + 1] : 0ULL);
+    }
+  }
+}
+
+void launch_rank_build(const AggTableDev& t, const uint64_t* keys, const RankSums& bs, uint64_t n, void* stream) {
+  count_launch();
+  k_rank_build<<<grid_for(std::max<uint64_t>(n, 1), 256), 256, 0, S(stream)>>>(t, keys, bs, n);
+}
+
 /// Bloom bits of a key column (the semi-join filter of the received build rows, set ahead of the
 /// table insert so the probe side can start screening while the insert runs).
 __global__ void k_bloom_keys(const uint64_t* __restrict__ keys, uint64_t n, uint32_t* bloom, int shift) {
