@@ -1106,7 +1106,7 @@ void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words, uint6
   const int nps = static_cast<int>(probe_sum_wire.size()), nbs = static_cast<int>(build_sum_wire.size());
   int hw = 2 + nps;
   hw = hw <= 2 ? 2 : (hw <= 4 ? 4 : 8 * ((hw + 7) / 8));
-  const int cw = rank_slots ? (2 + nbs) & ~1 : 1 + nbs;  // rank table: even (16-byte stores)
+  const int cw = rank_slots ? (4 + nbs) & ~3 : 1 + nbs;  // rank table: whole 32-byte rows
   agg_hot_ = DevBuf(ctx_.pool, (agg_cap_ + 1) * hw * 8, ctx_.compute);
   agg_cold_ = DevBuf(ctx_.pool, (agg_cap_ + 1) * cw * 8, ctx_.compute);
   std::memset(&aggt_, 0, sizeof aggt_);

@@ -710,6 +710,11 @@ __global__ void k_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uin
     if (atomicOr(bitmap + (d >> 5), bit) & bit) *dup = 1u;
   }
 }
+/// One 256-bit global store (sm_100: STG.256 - a whole 32-byte sector in one request).
+__device__ __forceinline__ void st256(uint64_t* p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
+
 /// Rank-indexed aggregation table build (unique dense build keys, one GPU): row i of the build
 /// side lands in the slot of its key's rank - plain stores, no CAS, every slot written once.
 /// Build-side double sums are stored as 0.0 + v (the value a hash-table insert accumulates).
@@ -719,7 +724,6 @@ __global__ void k_rank_build(AggTableDev t, const uint64_t* __restrict__ keys, R
     for (int k = 0; k < t.hw; ++k) t.hot[n * t.hw + k] = 0;
     for (int k = 0; k < t.cw; ++k) t.cold[n * t.cw + k] = 0;
   }
-  // hw and cw are even here (the rank table pads cw): whole 16-byte stores, full sectors
   for (uint64_t i = tid; i < n; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t key = keys[i];
     uint64_t cv[2 * kMaxSums + 2];
@@ -733,14 +737,19 @@ __global__ void k_rank_build(AggTableDev t, const uint64_t* __restrict__ keys, R
                       : v;
     }
     const uint64_t r = agg_rank_slot(t, key);
-    ulonglong2* h = reinterpret_cast<ulonglong2*>(t.hot + r * t.hw);
-    h[0] = make_ulonglong2(key, 0ULL);
-    for (int k = 1; k < t.hw / 2; ++k) h[k] = make_ulonglong2(0ULL, 0ULL);
-    ulonglong2* c = reinterpret_cast<ulonglong2*>(t.cold + r * t.cw);
+    uint64_t* h = t.hot + r * t.hw;
+    if (t.hw % 4 == 0) {  // whole 32-byte sectors per store: no partial-sector fills from DRAM
+      st256(h, key, 0, 0, 0);
+      for (int k = 4; k < t.hw; k += 4) st256(h + k, 0, 0, 0, 0);
+    } else {
+      *reinterpret_cast<ulonglong2*>(h) = make_ulonglong2(key, 0ULL);
+    }
+    uint64_t* c = t.cold + r * t.cw;  // cw is a multiple of 4 here
 #pragma unroll
-    for (int k = 0; k < kMaxSums + 1; ++k) {
-      if (2 * k >= t.cw) break;
-      c[k] = make_ulonglong2(cv[2 * k], 1 + 2 * k <= t.nbs ? cv[2 * k + 1] : 0ULL);
+    for (int k = 0; k < 2 * kMaxSums + 2; k += 4) {
+      if (k >= t.cw) break;
+      auto w = [&](int j) { return j <= t.nbs ? cv[j] : 0ULL; };
+      st256(c + k, w(k), w(k + 1), w(k + 2), w(k + 3));
     }
   }
 }
