@@ -952,6 +952,7 @@ __global__ void __launch_bounds__(256) k_agg_emit_dense(AggTableDev t, uint64_t 
                                                         const unsigned long long* bitmap, const uint32_t* prefix, int nc,
                                                         EmitCols ec, uint64_t* out) {
   const bool dups = t.dups == nullptr || *t.dups != 0;
+  const bool st32 = (nc & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
   for (uint64_t s = blockIdx.x * 256ULL + threadIdx.x; s < nslots; s += gridDim.x * 256ULL) {
     const uint64_t* h = t.hot + s * t.hw;
     const ulonglong2 kh = *reinterpret_cast<const ulonglong2*>(h);
@@ -985,9 +986,15 @@ __global__ void __launch_bounds__(256) k_agg_emit_dense(AggTableDev t, uint64_t 
       }
       vals[k] = v;
     }
-    // rows land at random positions: whole 16-byte stores (a 4-word row = one 32-byte sector
-    // in two transactions instead of four partial-sector ones)
-    if ((nc & 1) == 0) {
+    // rows land at random positions (hashed table): whole 32-byte stores where rows are whole
+    // sectors (no partial-sector fills from DRAM), else 16-byte stores
+    if (st32) {
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxSums + 2; k += 4) {
+        if (k >= nc) break;
+        st256(row + k, vals[k], vals[k + 1], vals[k + 2], vals[k + 3]);
+      }
+    } else if ((nc & 1) == 0) {
 #pragma unroll
       for (int k = 0; k < 2 * kMaxSums + 2; k += 2) {
         if (k >= nc) break;
