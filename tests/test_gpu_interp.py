@@ -1,6 +1,7 @@
-"""The nvcc-built interpreter kernel (k_scan; used when the NVRTC query compiler is unavailable,
-PSG_JIT=0) against the reference's golden results. The JIT-only specialisations (owner probe,
-packed shuffle rows, fused NVLink path) are switched off by the engine in that mode."""
+"""Engine fallbacks against the reference's golden results: the nvcc-built interpreter kernel
+(k_scan; used when the NVRTC query compiler is unavailable, PSG_JIT=0 - the JIT-only
+specialisations such as the owner probe, packed shuffle rows and fused NVLink path are switched
+off by the engine in that mode) and the hashed aggregation table at one GPU (PSG_RANK_TABLE=0)."""
 import os
 import subprocess
 import sys
@@ -13,6 +14,16 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def test_interpreter_kernels_match_golden():
     env = dict(os.environ, PSG_JIT="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "BAD 0" in r.stdout
+
+
+def test_hashed_aggregation_table_matches_golden():
+    """PSG_RANK_TABLE=0: the one-GPU grouped join uses the hashed open-addressing aggregation table
+    (CAS insert) instead of the rank-indexed one; both must give the reference's results."""
+    env = dict(os.environ, PSG_RANK_TABLE="0")
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
