@@ -8,12 +8,16 @@ Metric (BASELINE.json): Q3 SF100 query seconds + roofline fraction at 1/2/4/8 B2
 
 One "step" = one full query over the SF100 dataset. Two timings per step:
   value : inputs already resident in HBM (psg_stage_plan once, then psg_execute_staged per step);
-          device time from CUDA events on the engine's compute stream, max over ranks.
+          device time from CUDA events on the engine's compute stream, max over ranks; the result
+          stays in HBM (the same steps with the result rows copied to the host are reported as
+          value_rows_to_host).
   e2e   : the public call a user makes (psg_execute_plan): PSTO files (page cache) -> pinned ->
           HBM on copy streams -> kernels -> NCCL shuffle -> result rows back to the host.
+Parity: the e2e result's checksum (rowhash summed over ranks, tests/golden/sf100.json - made by the
+reference engine itself over the same files) is checked every run; a mismatch exits non-zero.
 Data: the reference's generator (byte-identical re-implementation, tests/golden/gen_hashes.json),
-seed 42, identity codec, 1 MiB row groups, written once as 8 node shards (dev0..dev7); rank r of N
-scans node shards k = r (mod N); customer is replicated. Inputs (24.2 GB) are >> L2 (126 MB).
+seed 42, 1 MiB row groups, written once as 8 node shards (dev0..dev7) by a separate process; rank r
+of N scans node shards k = r (mod N); customer is replicated. Inputs (24.2 GB) are >> L2 (126 MB).
 """
 import argparse
 import json
@@ -30,6 +34,8 @@ sys.path.insert(0, ROOT)
 METRIC = "TPC-H Q3 SF100 query sec + roofline fraction at 1/2/4/8 B200 vs CPU reference"
 SHARDS = 8
 DATE = 19950315
+NVLINK_GBS = 900.0  # per direction, NVLink 5 through NVSwitch
+REF_DRIVER = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
 
 
 def plan_for(shards, io_workers):
@@ -51,21 +57,34 @@ def plan_for(shards, io_workers):
     }
 
 
-def ensure_data(root, scale, nodes, rank_is_writer=True, codec="identity"):
+def data_root_for(data_dir, scale, codec):
+    return os.path.join(data_dir, "sf%g_n%d%s" % (scale, SHARDS, "" if codec == "identity" else "_" + codec))
+
+
+def gen_data_subprocess(root, scale, nodes, codec="identity"):
+    """Writes the dataset once (DONE marker) in a SEPARATE process, so a process that only times the
+    reference engine never maps the product library. Returns the generation seconds (0 if cached)."""
     marker = os.path.join(root, "DONE")
     if os.path.exists(marker):
-        return root, 0.0
-    if not rank_is_writer:
-        return root, 0.0
-    import shutil
-    import paper_2512_02862_b200 as psg
-    shutil.rmtree(root, ignore_errors=True)
+        return 0.0
     t = time.time()
-    psg.gen_workload("tpch", root, devices=nodes, nodes=nodes, scale=scale, seed=42, codec=codec,
-                     threads=max(3, min(32, os.cpu_count() or 3)))
+    code = ("import shutil, sys; sys.path.insert(0, %r); import paper_2512_02862_b200 as psg; "
+            "shutil.rmtree(%r, ignore_errors=True); "
+            "psg.gen_workload('tpch', %r, devices=%d, nodes=%d, scale=%r, seed=42, codec=%r, threads=%d)"
+            % (ROOT, root, root, nodes, nodes, scale, codec, max(3, min(32, os.cpu_count() or 3))))
+    subprocess.run([sys.executable, "-c", code], check=True)
     with open(marker, "w") as f:
         f.write(json.dumps({"scale": scale, "nodes": nodes, "seed": 42, "codec": codec}))
-    return root, time.time() - t
+    return time.time() - t
+
+
+def golden(scale):
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "sf100.json")) as f:
+            g = json.load(f)
+        return g if float(g["scale"]) == float(scale) else None
+    except OSError:
+        return None
 
 
 class Clocks:
@@ -138,39 +157,38 @@ def pinned_h2d_gbs(local, nbytes=1 << 30, reps=3):
     return best
 
 
-def ncu_traffic(scale):
+def ncu_traffic(scale, n, kernel):
+    """dram read+write bytes per launch of `kernel` from one `ncu --set full` capture at (scale, N)
+    (profiles/ncu_traffic.json; the capture each entry came from is named there)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             t = json.load(f)
-        return t.get("dram_bytes_per_launch") if float(t.get("scale", -1)) == float(scale) else None
+        for e in t.get("entries", []):
+            if float(e["scale"]) == float(scale) and int(e["n"]) == int(n) and e["kernel"] == kernel:
+                return e["dram_bytes_per_launch"], e.get("capture")
     except Exception:
-        return None
+        pass
+    return None, None
 
 
-# ------------------------------------------------------------------------------ CPU baselines
-def cpu_reference_run(sample_scale, steps, warmup, cores, data_dir):
-    """Runs the UNMODIFIED reference engine (oracle/_ref/ref_driver, run_socket_pipeline node 0 of 1,
-    Overlapped mode) on a bounded sample; returns (per-step seconds list, kind, note)."""
-    driver = os.path.join(ROOT, "oracle", "_ref", "ref_driver")
-    d, _ = ensure_data(os.path.join(data_dir, "sf%g_n1" % sample_scale), sample_scale, 1)
-    plan = plan_for([0], cores)
-    plan["scans"][1]["paths"] = ["{data}/dev0/orders.node0.psto"]
-    plan["scans"][2]["paths"] = ["{data}/dev0/lineitem.node0.psto"]
-    if os.path.exists(driver):
-        out = subprocess.run([driver, "run", "--plan-json", json.dumps(plan), "--data", d, "--mode", "overlapped",
-                              "--backend", "socket", "--repeat", str(steps + warmup)],
-                             capture_output=True, text=True, check=True).stdout.strip().splitlines()
-        res = [json.loads(x) for x in out if x.startswith("{")]
-        return [r["seconds"] for r in res[warmup:]], "reference", res[0]
-    # oracle port (numpy restatement), single thread
-    from oracle import plan_oracle as po
-    times = []
-    for i in range(steps + warmup):
-        t = time.time()
-        r = po.summary(po.execute(json.dumps(plan), d, 1))
-        if i >= warmup:
-            times.append(time.time() - t)
-    return times, "port", r
+# ------------------------------------------------------------------------------ CPU reference
+def reference_runs(data, cores, steps, warmup, budget_s):
+    """The UNMODIFIED reference engine (oracle/_ref/ref_driver: execute_plan through
+    run_socket_pipeline, node 0 of 1, Overlapped, io_workers = cores) over the SAME 8-shard files
+    the GPU arm scans - the whole SF100 query per step, no extrapolation. Each run is its own
+    process; runs stop when the next would exceed budget_s. Returns (timed runs, warmup runs)."""
+    plan = plan_for(range(SHARDS), cores)
+    timed, warm = [], []
+    t0 = time.time()
+    while len(timed) < steps:
+        last = (timed or warm or [{"seconds": 0}])[-1]["seconds"]
+        if (timed or warm) and time.time() - t0 + 1.1 * last > budget_s:
+            break
+        r = subprocess.run([REF_DRIVER, "run", "--plan-json", json.dumps(plan), "--data", data, "--mode", "overlapped",
+                            "--backend", "socket", "--repeat", "1"], capture_output=True, text=True, check=True)
+        res = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][0])
+        (warm if len(warm) < warmup else timed).append(res)
+    return timed, warm
 
 
 def run_reference_arm(args):
@@ -178,18 +196,32 @@ def run_reference_arm(args):
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    times, kind, r = cpu_reference_run(args.sample_scale, args.steps, args.warmup, cores, args.data_dir)
-    scale_up = args.scale / args.sample_scale
-    v = statistics.mean(times) * scale_up
-    sample = "Q3-analog SF%g (1 node, warm page cache), time x %g extrapolated linearly to SF%g" % (
-        args.sample_scale, scale_up, args.scale)
+    data = data_root_for(args.data_dir, args.scale, "identity")
+    gen_s = gen_data_subprocess(data, args.scale, SHARDS)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    budget = args.ref_budget_s if args.ref_budget_s else (1200.0 if world == 1 else 480.0)
+    timed, warm = reference_runs(data, cores, args.steps, min(args.warmup, 1), budget - gen_s)
+    runs = timed or warm
+    v = statistics.mean(r["seconds"] for r in runs)
+    g = golden(args.scale)
+    parity = {"rowhash": runs[0]["rowhash"], "groups": runs[0]["rows"],
+              "golden_rowhash": g["rowhash"] if g else None,
+              "match": None if g is None else all(r["rowhash"] == g["rowhash"] and r["rows"] == g["groups"] for r in runs)}
+    sample = ("whole SF%g query per step over the bench's 8 shard files (node 0 of 1, Overlapped, warm page cache, "
+              "io_workers=%d); %d timed + %d warm-up runs within a %.0f s budget (requested %d + %d)"
+              % (args.scale, cores, len(timed), len(warm), budget, args.steps, args.warmup))
     line = {"metric": METRIC, "impl": "reference", "value": round(v, 4), "unit": "s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(v * 1000, 3), "higher_is_better": False,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generator)",
-            "config": {"workload": "Q3-analog SF%g sample of the SF%g query" % (args.sample_scale, args.scale),
+            "steps": len(runs), "warmup": len(warm), "ms_per_step": round(v * 1000, 3), "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic: reference TPC-H-analog generator, seed 42 (same files as the GPU arm)",
+            "config": {"workload": "Q3-analog SF%g canonical plan (o_orderdate<%d, l_shipdate>%d, group by l_orderkey)"
+                                   % (args.scale, DATE, DATE),
+                       "scale": args.scale, "codec": "identity", "row_group_bytes": 1 << 20,
                        "engine": "reference execute_plan via run_socket_pipeline (node 0 of 1), Overlapped",
-                       "io_workers": cores, "sample_rows": r.get("rows")},
-            "cpu_baseline": {"value": round(v, 4), "unit": "s", "cores": cores, "kind": kind, "sample": sample},
+                       "io_workers": cores, "steps_requested": args.steps, "warmup_requested": args.warmup,
+                       "step_seconds": [round(r["seconds"], 3) for r in runs], "gen_s": round(gen_s, 1)},
+            "parity": parity,
+            "cpu_baseline": {"value": round(v, 4), "unit": "s", "cores": cores, "kind": "reference", "sample": sample},
             "e2e": {"value": round(v, 4), "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -202,10 +234,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--scale", type=float, default=100.0)
-    ap.add_argument("--sample-scale", type=float, default=10.0)
     ap.add_argument("--data-dir", default=os.environ.get("PSG_BENCH_DATA", "/tmp/psg_bench"))
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--ref-budget-s", type=float, default=0.0,
+                    help="reference arm: wall budget for its runs (default 1200 s at N=1, 480 s at N>1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-block", action="store_true", help="skip the block-codec e2e config")
     ap.add_argument("--no-semijoin", action="store_true")
     ap.add_argument("--io-threads", type=int, default=0)
     ap.add_argument("--batch-mb", type=int, default=0,
@@ -213,32 +247,35 @@ def main():
                          "bigger batches fill the GPU with inflate work at N=1, smaller ones pipeline better "
                          "when each rank streams 1/N of the data)")
     ap.add_argument("--codec", default="identity", choices=["identity", "block"],
-                    help="PSTO codec of the dataset (block = zlib chunks, inflated on the GPU)")
+                    help="PSTO codec of the headline dataset (block = zlib chunks, inflated on the GPU)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
 
-    import paper_2512_02862_b200 as psg
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
     dist = None
     if world > 1:
-        import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cores = os.cpu_count() or 1
     io_threads = args.io_threads or max(2, min(12, cores // max(world, 1)))
 
-    data_root = os.path.join(args.data_dir, "sf%g_n%d%s" % (args.scale, SHARDS, "" if args.codec == "identity"
-                                                                  else "_" + args.codec))
+    data_root = data_root_for(args.data_dir, args.scale, args.codec)
+    block_root = data_root_for(args.data_dir, args.scale, "block")
+    with_block = not args.no_block and args.codec == "identity"
     gen_s = 0.0
     if rank == 0:
-        data_root, gen_s = ensure_data(data_root, args.scale, SHARDS, codec=args.codec)
+        gen_s = gen_data_subprocess(data_root, args.scale, SHARDS, args.codec)
+        if with_block:
+            gen_s += gen_data_subprocess(block_root, args.scale, SHARDS, "block")
     if dist:
         dist.barrier()
 
+    import paper_2512_02862_b200 as psg
     nccl_id = None
     if world > 1:
         obj = [psg.Context.unique_id() if rank == 0 else None]
@@ -257,21 +294,21 @@ def main():
         if dist:
             dist.barrier()
 
-    def max_over_ranks(x):
+    def reduce(x, op="max", dtype=torch.float64):
         if not dist:
             return x
-        import torch
-        t = torch.tensor([float(x)], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        t = torch.tensor([x], device="cuda", dtype=dtype)
+        dist.all_reduce(t, op={"max": dist.ReduceOp.MAX, "sum": dist.ReduceOp.SUM}[op])
+        return t.item()
 
-    def sum_over_ranks(x):
-        if not dist:
-            return x
-        import torch
-        t = torch.tensor([float(x)], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t)
-        return float(t.item())
+    def wrap_sum_u64(vals):
+        """sum of u64 words over ranks, mod 2^64 (NCCL int64 sums wrap like the reference's u64)."""
+        s = [(v - (1 << 64)) if v >= (1 << 63) else v for v in vals]
+        if dist:
+            t = torch.tensor(s, device="cuda", dtype=torch.int64)
+            dist.all_reduce(t)
+            s = t.tolist()
+        return [v % (1 << 64) for v in s]
 
     # ---------------- value: HBM-resident inputs ----------------
     t = time.time()
@@ -280,86 +317,134 @@ def main():
     for _ in range(args.warmup):
         staged.run(want_rows=False)
     sync_all()
-    dev_ms = []
-    launches = 0
-    probe_ms = probe_bytes = probe_launches = 0
-    rows = 0
+    dev_ms, sts = [], []
     clk = Clocks(local).__enter__()
-    if True:
-        wall0 = time.time()
-        for _ in range(args.steps):
-            sync_all()  # every step starts aligned across ranks (the barrier is outside the engine's events)
-            st = staged.run(want_rows=False)
-            dev_ms.append(st["device_ms"])
-            launches += st["kernel_launches"]
-            probe_ms += st["probe_kernel_ms"]
-            probe_bytes += st["probe_kernel_bytes"]
-            probe_launches += st["probe_kernel_launches"]
-            rows = st["result_rows"]
+    wall0 = time.time()
+    for _ in range(args.steps):
+        sync_all()  # every step starts aligned across ranks (the barrier is outside the engine's events)
+        st = staged.run(want_rows=False)
+        dev_ms.append(st["device_ms"])
+        sts.append(st)
     sync_all()
     wall_value = (time.time() - wall0) / max(args.steps, 1)
-    value_s = max_over_ranks(sum(dev_ms) / 1000.0 / max(args.steps, 1))
-    total_groups = sum_over_ranks(rows)
+    value_s = reduce(sum(dev_ms) / 1000.0 / max(args.steps, 1))
+    total = lambda k: sum(s[k] for s in sts)
+    launches = total("kernel_launches")
+    groups = int(reduce(float(sts[-1]["result_rows"]), "sum"))
+    # the same query with its result rows copied to the host (pinned), device-timed like value
+    rows_ms = []
+    for _ in range(min(args.steps, 5)):
+        sync_all()
+        res = staged.run(want_rows=True)
+        rows_ms.append(res.stats["device_ms"])
+        del res
+    value_rows_s = reduce(statistics.mean(rows_ms) / 1000.0) if rows_ms else None
     staged.free()
 
     # ---------------- e2e: storage-resident, through psg_execute_plan ----------------
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
-    warm = [ctx.execute_plan(plan, data_root) for _ in range(min(args.warmup, 2))]  # pinned result blocks
-    del warm
-    sync_all()
-    e2e_t, h2d, d2h = [], 0, 0
-    e2e_rows = 0
-    io_wait = []
-    for _ in range(e2e_steps):
+    def e2e_run(root, steps, tag):
+        warm = [ctx.execute_plan(plan, root) for _ in range(min(args.warmup, 2))]  # pinned result blocks
+        del warm
         sync_all()
-        t = time.time()
-        res = ctx.execute_plan(plan, data_root)
-        e2e_t.append(time.time() - t)
-        h2d, d2h = res.stats["h2d_bytes"], res.stats["result_bytes"]
-        io_wait.append(res.stats["io_wait_s"])
-        e2e_rows = res.rows.shape[0]
-    sync_all()
-    clk.__exit__(None, None, None)
-    e2e_s = max_over_ranks(statistics.mean(e2e_t)) if e2e_t else None
-    h2d_all, d2h_all = sum_over_ranks(h2d), sum_over_ranks(d2h)
-    e2e_groups = sum_over_ranks(e2e_rows)
+        times, last = [], None
+        for _ in range(steps):
+            sync_all()
+            t = time.time()
+            last = ctx.execute_plan(plan, root)
+            times.append(time.time() - t)
+        sync_all()
+        e2e_s = reduce(statistics.mean(times)) if times else None
+        h2d, d2h = last.stats["h2d_bytes"], last.stats["result_bytes"]
+        cs = last.checksum()
+        hs = wrap_sum_u64([int(cs["rowhash"], 16)] + [int(x) for x in cs["colsums"]])
+        g = golden(args.scale)
+        nrows = int(reduce(float(cs["rows"]), "sum"))
+        parity = {"rowhash": "%016x" % hs[0], "groups": nrows, "colsums": [str(x) for x in hs[1:]],
+                  "golden_rowhash": g["rowhash"] if g else None,
+                  "match": None if g is None else ("%016x" % hs[0] == g["rowhash"] and nrows == g["groups"]
+                                                   and [str(x) for x in hs[1:]] == g["colsums"])}
+        out = {"value": round(e2e_s, 4) if e2e_s else None, "unit": "s",
+               "h2d_bytes_per_step": int(reduce(float(h2d), "sum")), "d2h_bytes_per_step": int(reduce(float(d2h), "sum")),
+               "steps": steps, "io_wait_s": round(reduce(last.stats["io_wait_s"]), 4),
+               "path": "psg_execute_plan: PSTO files (%s, warm page cache) -> pinned -> HBM -> rows to host" % tag}
+        out["ingest_gbs"] = round(out["h2d_bytes_per_step"] / 1e9 / e2e_s, 2) if e2e_s else None
+        return out, parity, h2d, e2e_s
 
-    # ---------------- roofline of the dominant kernel (lineitem fused scan) ----------------
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
+    e2e, parity, h2d_rank, e2e_s = e2e_run(data_root, e2e_steps, args.codec)
+    e2e_block = None
+    if with_block:
+        e2e_block, parity_block, _, _ = e2e_run(block_root, min(e2e_steps, 10), "block codec")
+        e2e_block["parity_match"] = parity_block["match"]
+        parity["block_match"] = parity_block["match"]
+    clk.__exit__(None, None, None)
+
+    # ---------------- roofline of the dominant kernel ----------------
     peak, peak_kind = measured_peak()
     roof = None
-    if probe_launches:
-        per_launch_bytes = probe_bytes / probe_launches
-        per_launch_s = probe_ms / 1000.0 / probe_launches
-        achieved = per_launch_bytes / per_launch_s / 1e9
-        ach = max_over_ranks(-achieved) * -1 if dist else achieved  # slowest rank
+    pl = total("probe_kernel_launches")
+    if pl:
+        per_launch_bytes = total("probe_kernel_bytes") / pl
+        per_launch_s = total("probe_kernel_ms") / 1000.0 / pl
+        ach = -reduce(-(per_launch_bytes / per_launch_s / 1e9))  # slowest rank
+        kernel = "psg_jit_scan SINK_PROBE (lineitem scan+filter+probe+agg)" if world == 1 else \
+            "psg_jit_scan SINK_MATERIALIZE (lineitem scan+filter+semi-join+partition)"
+        traffic, capture = ncu_traffic(args.scale, world, kernel)
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
-                "traffic": ncu_traffic(args.scale), "kernel": "psg_jit_scan SINK_PROBE (lineitem scan+filter+probe+agg)"
-                if world == 1 else "k_scan<4,SINK_MATERIALIZE> (lineitem scan+filter+partition)",
+                "traffic": traffic, "traffic_capture": capture, "kernel": kernel,
                 "algorithmic_bytes_per_launch": int(per_launch_bytes), "peak_kind": peak_kind,
                 "kernel_ms_per_launch": round(per_launch_s * 1000, 4),
-                "share_of_step": round(probe_ms / max(sum(dev_ms), 1e-9), 4)}
+                "share_of_step": round(total("probe_kernel_ms") / max(sum(dev_ms), 1e-9), 4)}
 
-    # binding roofline of the end-to-end query: ingest (per-GPU bytes over the pinned->HBM link),
-    # the slowest rank decides; the host's page-cache read bandwidth is shared by all ranks and is
-    # the tighter bound on this box (profiles/r1_box_ingest_probe.txt)
+    # ---------------- shuffle (N > 1): bytes over NVLink per GPU and their rate ----------------
+    shuffle = None
+    if world > 1:
+        recv = reduce(total("bytes_received") / len(sts))
+        xms = reduce(total("exchange_ms") / len(sts))
+        ref_recv = (0.55 + 10.39) * args.scale / 100 * 1e9 * (world - 1) / world ** 2
+        shuffle = {"bytes_received_per_gpu": int(recv), "exchange_ms": round(xms, 4),
+                   "gbs": round(recv / 1e9 / (xms / 1000.0), 1) if xms > 0 else None, "nvlink_gbs": NVLINK_GBS,
+                   "frac_of_nvlink": round(recv / 1e9 / (xms / 1000.0) / NVLINK_GBS, 4) if xms > 0 else None,
+                   "reference_wire_bytes_per_gpu": int(ref_recv),
+                   "note": "semi-join-reduced, bit-packed rows (DESIGN.md §2); reference wire schema figure alongside"}
+
+    # ---------------- binding roofline of the end-to-end query (bench.cpp:35-40) ----------
     e2e_roof = None
     try:
+        probes = []
+        for _ in range(3):
+            sync_all()
+            probes.append(ctx.ingest_probe(plan, data_root)["runtime_s"])
+        ingest_s = reduce(statistics.median(probes))
         bw = pinned_h2d_gbs(local)
-        t_min = max_over_ranks(h2d / 1e9 / bw) if bw > 0 else None
-        if t_min and e2e_s:
-            e2e_roof = {"bound": "ingest (pinned H2D per GPU)", "h2d_gbs_measured": round(bw, 1),
-                        "t_min_s": round(t_min, 4), "frac": round(t_min / e2e_s, 4)}
+        pcie_s = reduce(h2d_rank / 1e9 / bw)
+        recv_b = shuffle["bytes_received_per_gpu"] if shuffle else 0
+        terms = {
+            "ingest_pipelined_s": round(ingest_s, 4),  # page cache -> pinned -> HBM, all ranks at once, engine threads
+            "pcie_h2d_s": round(pcie_s, 4),            # this GPU's bytes over its pinned H2D link
+            "nvlink_s": round(recv_b / 1e9 / NVLINK_GBS, 6),
+            "hbm_s": round(reduce(total("ingest_bytes") / len(sts)) / 1e9 / peak, 6),  # column chunks read once
+        }
+        bind = max(terms, key=terms.get)
+        t_min = terms[bind]
+        e2e_roof = {"terms": terms, "bound": bind, "t_min_s": t_min, "frac": round(t_min / e2e_s, 4) if e2e_s else None,
+                    "h2d_gbs_measured": round(bw, 1),
+                    "ingest_gbs_pipelined": round(reduce(float(h2d_rank), "sum") / 1e9 / ingest_s, 1),
+                    "note": "frac = binding term / e2e seconds; ingest term measured live through psg_ingest_probe"}
     except Exception as e:  # never hide the main numbers
         e2e_roof = {"error": str(e)[:200]}
 
+    # ---------------- CPU reference (N=1, rank 0): the whole SF100 query, one run ----------------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.codec == "identity":
         try:
-            times, kind, r = cpu_reference_run(args.sample_scale, 1, 0, cores, args.data_dir)
-            f = args.scale / args.sample_scale
-            cpu = {"value": round(statistics.mean(times) * f, 3), "unit": "s", "cores": cores, "kind": kind,
-                   "sample": "Q3-analog SF%g (node 0 of 1, Overlapped, warm page cache, io_workers=%d) x %g "
-                             "extrapolated linearly to SF%g" % (args.sample_scale, cores, f, args.scale)}
+            if not os.path.exists(REF_DRIVER):
+                raise RuntimeError("oracle/_ref/ref_driver not built")
+            timed, _ = reference_runs(data_root, cores, 1, 0, 1e9)
+            r = timed[0]
+            cpu = {"value": round(r["seconds"], 3), "unit": "s", "cores": cores, "kind": "reference",
+                   "sample": "one whole SF%g query (the same files; node 0 of 1, Overlapped, warm page cache, "
+                             "io_workers=%d), not extrapolated; rowhash %s" % (args.scale, cores, r["rowhash"])}
         except Exception as e:  # baseline failure must not hide the GPU number
             cpu = {"value": None, "unit": "s", "cores": cores, "kind": "reference", "sample": "failed: %s" % e}
 
@@ -374,17 +459,19 @@ def main():
                        "scale": args.scale, "row_group_bytes": 1 << 20, "codec": args.codec,
                        "layout": "8 node shards; rank r scans shards k%%N==r; customer replicated",
                        "l2": "inputs 24.2 GB >> 126 MB L2 (no flush needed)",
-                       "value": "HBM-resident inputs, CUDA events on the engine stream, max over ranks",
+                       "value": "HBM-resident inputs, CUDA events on the engine stream, max over ranks; result rows "
+                                "stay in HBM (value_rows_to_host_s adds their D2H)",
                        "io_threads": io_threads, "batch_mb": args.batch_mb,
                        "semijoin_bloom": not args.no_semijoin, "stage_s": round(stage_s, 3),
-                       "gen_s": round(gen_s, 2), "groups": int(total_groups), "wall_s_per_value_step": round(wall_value, 6)},
+                       "gen_s": round(gen_s, 2), "groups": groups, "wall_s_per_value_step": round(wall_value, 6),
+                       "agg_table": int(sts[-1]["agg_table"])},
+            "value_rows_to_host_s": round(value_rows_s, 6) if value_rows_s else None,
+            "parity": parity,
             "roofline": roof,
+            "shuffle": shuffle,
             "cpu_baseline": cpu,
-            "e2e": {"value": round(e2e_s, 4) if e2e_s else None, "unit": "s", "h2d_bytes_per_step": int(h2d_all),
-                    "d2h_bytes_per_step": int(d2h_all), "steps": e2e_steps, "groups": int(e2e_groups),
-                    "io_wait_s": round(statistics.mean(io_wait), 4) if io_wait else None,
-                    "ingest_gbs": round(h2d_all / 1e9 / e2e_s, 2) if e2e_s else None,
-                    "path": "psg_execute_plan: PSTO files (warm page cache) -> pinned -> HBM -> rows to host"},
+            "e2e": e2e,
+            "e2e_block": e2e_block,
             "e2e_roofline": e2e_roof,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),
@@ -393,6 +480,9 @@ def main():
     ctx.close()
     if dist:
         dist.destroy_process_group()
+    if parity["match"] is False or parity.get("block_match") is False:
+        sys.stderr.write("PARITY FAILURE: result checksum differs from tests/golden/sf100.json\n")
+        sys.exit(1)
 
 
 if __name__ == "__main__":

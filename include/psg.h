@@ -22,7 +22,7 @@
 extern "C" {
 #endif
 
-#define PSG_ABI_VERSION 1
+#define PSG_ABI_VERSION 2
 
 /* Status codes — 1:1 with pystachio::Error subclasses (errors.hpp:21-87) + CUDA/NCCL. */
 typedef enum psg_status {
@@ -99,11 +99,24 @@ typedef struct psg_stats {
   double io_wait_s;            /* host time the control thread waited for storage reads */
   uint64_t jit_compiles;       /* NVRTC kernel compilations during this call (cached afterwards) */
   uint64_t h2d_bytes;          /* host->HBM bytes copied (compressed for block-codec chunks) */
+  uint64_t agg_table;          /* shuffle-join table kind: 0 none (no aggregate), 1 hashed, 2 hashed +
+                                  Bloom screen, 3 hashed + exact key bitmap, 4 rank-indexed (dense
+                                  unique build keys), 5 symmetric peer-mapped (fused NVLink) */
+  uint64_t bytes_sent;         /* shuffle payload bytes sent to peers */
+  double exchange_ms;          /* summed CUDA-event time of the shuffle send/recv groups */
 } psg_stats;
 
 /* ---- library ---- */
 int psg_abi_version(void);
 const char* psg_last_error(void);
+
+/* Host-only: parses + validates a plan like QueryPlan::from_json_text (pipeline.cpp:108-156,
+ * validate :178-196) for node `node` of `nodes` and writes the resolved scans as JSON
+ * {"scans":[{"table","replicated","paths":[...]}],"shuffle":id|null} into out (NUL-terminated,
+ * truncated to cap; *needed = full size + 1). Errors: InvalidInput (bad JSON / plan shape),
+ * IoFailure (a path matches no file). */
+int psg_plan_resolve(const char* plan_json, const char* data_root, int node, int nodes, char* out, size_t cap,
+                     size_t* needed);
 
 /* ---- per-GPU context (ExecEnv + Fabric + DeviceManager + MetadataCache, exec.hpp:84-92) ---- */
 /* device: CUDA ordinal; rank/nranks: this GPU's node id and the node count (Fabric::node_count). */
@@ -137,6 +150,12 @@ int psg_execute_plan(psg_ctx* ctx, const char* plan_json, const char* data_root,
  * which the reference's execute_plan rejects (pipeline.cpp:334-335; psg_execute_plan keeps that
  * InvalidInput). No exchange: each rank returns its node's unmerged partial row [rows, sums...]
  * (the global-aggregate semantics of pipeline.cpp:277-281). */
+/* Measurement: moves every column chunk the plan reads storage -> pinned -> HBM through the same
+ * ingest session psg_execute_plan uses (same I/O threads, ring and copy stream; block-codec
+ * chunks are also inflated) and runs no query kernels. stats: runtime_s, h2d_bytes,
+ * ingest_bytes, io_wait_s - the ingest term of the end-to-end roofline (bench.cpp:35-40 t_min). */
+int psg_ingest_probe(psg_ctx* ctx, const char* plan_json, const char* data_root, psg_stats* out);
+
 int psg_execute_local(psg_ctx* ctx, const char* plan_json, const char* data_root, int mode,
                       psg_result** out);
 
@@ -153,6 +172,10 @@ int psg_result_shape(const psg_result* r, uint64_t* nrows, uint32_t* ncols);
 int psg_result_field(const psg_result* r, uint32_t col, const char** name, int* type);
 const uint64_t* psg_result_data(const psg_result* r); /* row-major nrows*ncols words */
 int psg_result_stats(const psg_result* r, psg_stats* out);
+/* Result checksum (host-side, over the rows already on the host): rowhash = sum over rows of
+ * FNV-1a64 of the row's little-endian words mod 2^64 (additive over ranks, independent of row
+ * order) and per-column wrap-around sums into colsums[0..min(ncols, ncols_cap)). */
+int psg_result_checksum(const psg_result* r, uint64_t* rowhash, uint64_t* colsums, uint32_t ncols_cap);
 void psg_result_free(psg_result* r);
 
 /* ---- operator adapters (ops.hpp:35-83): host batch -> HBM -> kernel -> host ---- */

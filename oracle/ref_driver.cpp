@@ -25,6 +25,7 @@
 #include "pystachio/bench.hpp"
 #include "pystachio/hashing.hpp"
 #include "pystachio/pipeline_harness.hpp"
+#include "pystachio/pipeline.hpp"
 #include "pystachio/psto.hpp"
 #include "pystachio/scan.hpp"
 
@@ -214,6 +215,47 @@ int main(int argc, char** argv) {
         }
         summarize(out, 1 + sums.size(), s, {out.size()}, std::string());
         std::fflush(stdout);
+      }
+      return 0;
+    }
+    if (cmd == "plan") {
+      // QueryPlan::from_json_text (pipeline.cpp:108-156) for node --node of --nodes: the resolved
+      // scans as JSON, or {"error": "<reference exception class>"}
+      const std::string plan = arg(argc, argv, "--plan-json", "");
+      const std::string data = arg(argc, argv, "--data", "data");
+      const int node = std::stoi(arg(argc, argv, "--node", "0"));
+      const int nodes = std::stoi(arg(argc, argv, "--nodes", "1"));
+      auto q = [](const std::string& x) {
+        std::string o = "\"";
+        for (char ch : x) {
+          if (ch == '"' || ch == '\\') o += '\\';
+          o += ch;
+        }
+        return o + "\"";
+      };
+      try {
+        const QueryPlan p = QueryPlan::from_json_text(plan, data, node, nodes);
+        std::string j = "{\"scans\": [";
+        for (std::size_t i = 0; i < p.scans.size(); ++i) {
+          const ScanNode& sc = p.scans[i];
+          j += (i ? ", " : "") + std::string("{\"table\": ") + q(sc.table) + ", \"replicated\": " +
+               (sc.replicated ? "true" : "false") + ", \"paths\": [";
+          for (std::size_t k = 0; k < sc.paths.size(); ++k) j += (k ? ", " : "") + q(sc.paths[k]);
+          j += "]}";
+        }
+        const JoinNode* sj = p.shuffle_join();
+        j += "], \"shuffle\": " + (sj ? q(sj->id) : std::string("null")) + "}";
+        std::printf("%s\n", j.c_str());
+      } catch (const InvalidInput&) {
+        std::printf("{\"error\": \"InvalidInput\"}\n");
+      } catch (const IoFailure&) {
+        std::printf("{\"error\": \"IoFailure\"}\n");
+      } catch (const UnknownColumn&) {
+        std::printf("{\"error\": \"UnknownColumn\"}\n");
+      } catch (const Error&) {
+        std::printf("{\"error\": \"Error\"}\n");
+      } catch (const std::exception&) {  // nlohmann::json exceptions (malformed / mistyped JSON)
+        std::printf("{\"error\": \"json\"}\n");
       }
       return 0;
     }

@@ -35,7 +35,8 @@ EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_uniq
            "psg_result_stats", "psg_result_free", "psg_filter", "psg_partition", "psg_hash_join", "psg_hashtable_build",
            "psg_hashtable_shape", "psg_hashtable_row", "psg_hashtable_lookup", "psg_hashtable_probe", "psg_hashtable_free",
            "psg_concat", "psg_codec_decompress", "psg_psto_write",
-           "psg_psto_inspect", "psg_gen_tpch", "psg_gen_synthetic", "psg_jit_selftest", "psg_tmin"]
+           "psg_psto_inspect", "psg_gen_tpch", "psg_gen_synthetic", "psg_jit_selftest", "psg_tmin",
+           "psg_plan_resolve", "psg_result_checksum", "psg_ingest_probe"]
 
 
 class PsgError(RuntimeError):
@@ -55,7 +56,8 @@ class Stats(ctypes.Structure):
                 ("waves", ctypes.c_uint64), ("probe_kernel_ms", ctypes.c_double),
                 ("probe_kernel_launches", ctypes.c_uint64), ("probe_kernel_bytes", ctypes.c_uint64),
                 ("device_ms", ctypes.c_double), ("result_rows", ctypes.c_uint64), ("io_wait_s", ctypes.c_double),
-                ("jit_compiles", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64)]
+                ("jit_compiles", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
+                ("agg_table", ctypes.c_uint64), ("bytes_sent", ctypes.c_uint64), ("exchange_ms", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -114,6 +116,9 @@ def lib():
             "psg_gen_synthetic": ([c, i32, i32, u64, i32, u64, u64, u64, i32, ctypes.c_double], i32),
             "psg_tmin": ([u64, ctypes.c_double, u64, ctypes.c_double], ctypes.c_double),
             "psg_jit_selftest": ([ctypes.c_char_p, ctypes.c_size_t], i32),
+            "psg_ingest_probe": ([vp, c, c, P(Stats)], i32),
+            "psg_result_checksum": ([vp, P(u64), P(u64), ctypes.c_uint32], i32),
+            "psg_plan_resolve": ([c, c, i32, i32, ctypes.c_char_p, ctypes.c_size_t, P(ctypes.c_size_t)], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -126,6 +131,17 @@ def lib():
 def _check(rc):
     if rc != 0:
         raise PsgError(rc, lib().psg_last_error().decode(errors="replace"))
+
+
+def resolve_plan(plan, data_root, node=0, nodes=1):
+    """Host-only plan parse + validation (QueryPlan::from_json_text, pipeline.cpp:108-156): the
+    resolved scans {"scans": [{"table", "replicated", "paths"}], "shuffle": id | None}."""
+    text = (plan if isinstance(plan, str) else json.dumps(plan)).encode()
+    need = ctypes.c_size_t(0)
+    _check(lib().psg_plan_resolve(text, data_root.encode(), node, nodes, None, 0, ctypes.byref(need)))
+    buf = ctypes.create_string_buffer(need.value)
+    _check(lib().psg_plan_resolve(text, data_root.encode(), node, nodes, buf, need.value, None))
+    return json.loads(buf.value.decode())
 
 
 # ------------------------------------------------------------------------------ batches
@@ -216,6 +232,17 @@ class Result:
             self.rows = np.zeros((n.value, k.value), np.uint64)
             L.psg_result_free(handle)
 
+    def checksum(self):
+        """{"rows", "rowhash", "colsums"}: rowhash = sum over rows of FNV-1a64 of the row's words
+        (mod 2^64, additive over ranks), the reference harness's result checksum."""
+        k = len(self.schema)
+        if self.rows.shape[0] == 0:
+            return {"rows": 0, "rowhash": "%016x" % 0, "colsums": ["0"] * k}
+        h = ctypes.c_uint64()
+        cs = (ctypes.c_uint64 * max(k, 1))()
+        _check(lib().psg_result_checksum(self._owner.h, ctypes.byref(h), cs, k))
+        return {"rows": int(self.rows.shape[0]), "rowhash": "%016x" % h.value, "colsums": [str(cs[i]) for i in range(k)]}
+
     def column(self, name):
         i = [n for n, _t in self.schema].index(name)
         col = self.rows[:, i]
@@ -270,6 +297,14 @@ class Context:
         out = ctypes.c_void_p()
         _check(lib().psg_execute_local(self._h, text.encode(), data_root.encode(), MODES[mode], ctypes.byref(out)))
         return Result(out)
+
+    def ingest_probe(self, plan, data_root) -> dict:
+        """The plan's storage -> pinned -> HBM ingest alone (same session as execute_plan, no query
+        kernels): stats dict with runtime_s / h2d_bytes - the e2e roofline's ingest term."""
+        text = plan if isinstance(plan, str) else json.dumps(plan)
+        st = Stats()
+        _check(lib().psg_ingest_probe(self._h, text.encode(), data_root.encode(), ctypes.byref(st)))
+        return st.as_dict()
 
     def stage_plan(self, plan, data_root):
         text = plan if isinstance(plan, str) else json.dumps(plan)

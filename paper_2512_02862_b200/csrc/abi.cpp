@@ -105,6 +105,39 @@ Predicate to_pred(const psg_atom* atoms, uint32_t n) {
 extern "C" {
 
 int psg_abi_version(void) { return PSG_ABI_VERSION; }
+
+int psg_plan_resolve(const char* plan_json, const char* data_root, int node, int nodes, char* out, size_t cap,
+                     size_t* needed) {
+  return guarded([&] {
+    if (!plan_json || !data_root) throw InvalidInput("null plan or data root");
+    const QueryPlan p = QueryPlan::from_json_text(plan_json, data_root, node, nodes);
+    // {"scans":[{"table":..,"replicated":b,"paths":[..]}..],"shuffle":"id"|null}
+    auto q = [](const std::string& x) {
+      std::string o = "\"";
+      for (char ch : x) {
+        if (ch == '"' || ch == '\\') o += '\\';
+        o += ch;
+      }
+      return o + "\"";
+    };
+    std::string j = "{\"scans\": [";
+    for (size_t i = 0; i < p.scans.size(); ++i) {
+      const ScanNode& sc = p.scans[i];
+      j += (i ? ", " : "") + std::string("{\"table\": ") + q(sc.table) + ", \"replicated\": " +
+           (sc.replicated ? "true" : "false") + ", \"paths\": [";
+      for (size_t k = 0; k < sc.paths.size(); ++k) j += (k ? ", " : "") + q(sc.paths[k]);
+      j += "]}";
+    }
+    const JoinNode* sj = p.shuffle_join();
+    j += "], \"shuffle\": " + (sj ? q(sj->id) : std::string("null")) + "}";
+    if (needed) *needed = j.size() + 1;
+    if (out && cap) {
+      const size_t n = std::min(cap - 1, j.size());
+      std::memcpy(out, j.data(), n);
+      out[n] = '\0';
+    }
+  });
+}
 const char* psg_last_error(void) { return g_err.c_str(); }
 
 int psg_ctx_create(int device, int rank, int nranks, psg_ctx** out) {
@@ -212,6 +245,14 @@ int psg_execute_local(psg_ctx* ctx, const char* plan_json, const char* data_root
   });
 }
 
+int psg_ingest_probe(psg_ctx* ctx, const char* plan_json, const char* data_root, psg_stats* out) {
+  return guarded([&] {
+    if (!ctx || !plan_json || !data_root || !out) throw InvalidInput("null argument");
+    if (ctx->c.io_threads == 0) ctx->c.io_threads = 8;
+    *out = ingest_only(ctx->c, plan_json, data_root).stats;
+  });
+}
+
 int psg_stage_plan(psg_ctx* ctx, const char* plan_json, const char* data_root, psg_staged** out) {
   return guarded([&] {
     if (!ctx || !plan_json || !data_root || !out) throw InvalidInput("null argument");
@@ -260,6 +301,31 @@ int psg_result_stats(const psg_result* r, psg_stats* out) {
   return guarded([&] {
     if (!r || !out) throw InvalidInput("null argument");
     *out = r->r.stats;
+  });
+}
+
+int psg_result_checksum(const psg_result* r, uint64_t* rowhash, uint64_t* colsums, uint32_t ncols_cap) {
+  return guarded([&] {
+    if (!r || !rowhash) throw InvalidInput("null argument");
+    const uint64_t n = r->r.nrows;
+    const size_t nc = r->r.schema.size();
+    const uint64_t* w = r->r.data();
+    // sum over rows of FNV-1a64 of the row's little-endian bytes (mod 2^64): order-independent and
+    // additive over ranks, the reference harness's result checksum (hashing.hpp fnv1a64)
+    uint64_t h = 0;
+    std::vector<uint64_t> cs(nc, 0);
+    for (uint64_t i = 0; i < n; ++i) {
+      uint64_t f = 0xcbf29ce484222325ULL;
+      for (size_t c = 0; c < nc; ++c) {
+        const uint64_t x = w[i * nc + c];
+        cs[c] += x;
+        for (int b = 0; b < 8; ++b) f = (f ^ ((x >> (8 * b)) & 0xFF)) * 0x100000001b3ULL;
+      }
+      h += f;
+    }
+    *rowhash = h;
+    if (colsums)
+      for (size_t c = 0; c < nc && c < ncols_cap; ++c) colsums[c] = cs[c];
   });
 }
 

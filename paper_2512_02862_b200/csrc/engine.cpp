@@ -447,6 +447,9 @@ class Execution {
   ResultRows run_local();
   // staging entry: read every scan's needed chunks into HBM
   void stage(Staged& st);
+  // storage -> pinned -> HBM of every chunk the plan reads, through the same ingest session as
+  // run(), with no kernels (block codec: + inflate): the ingest term of the e2e roofline
+  ResultRows run_ingest_only();
 
  private:
   // ---- compilation ----
@@ -522,6 +525,30 @@ class Execution {
   };
   Event build_fork_, build_done_;
   bool build_pending_ = false;
+  // timed shuffle send/recv groups (psg_stats.exchange_ms, summed once the query has drained)
+  struct TimedPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    TimedPair() {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+    }
+    ~TimedPair() {
+      cudaEventDestroy(a);
+      cudaEventDestroy(b);
+    }
+    TimedPair(const TimedPair&) = delete;
+    TimedPair& operator=(const TimedPair&) = delete;
+  };
+  std::vector<std::unique_ptr<TimedPair>> xfer_ev_;
+  void sum_exchange_time() {
+    double ms = 0;
+    for (auto& t : xfer_ev_) {
+      float x = 0;
+      if (cudaEventElapsedTime(&x, t->a, t->b) == cudaSuccess) ms += x;
+    }
+    cudaGetLastError();
+    st_.exchange_ms = ms;
+  }
   uint64_t agg_cap_ = 0;
   // stats
   psg_stats st_{};
@@ -1283,6 +1310,8 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
   for (int s = 0; s < n; ++s) rtotal += m[static_cast<size_t>(s) * n + me];
   rcv.buf = DevBuf(ctx_.pool, std::max<uint64_t>(rtotal, 1) * ncols * 8 + 16, st);
   rcv.rows = rtotal;
+  xfer_ev_.push_back(std::make_unique<TimedPair>());
+  PSG_CUDA(cudaEventRecord(xfer_ev_.back()->a, st));
   PSG_NCCL(ncclGroupStart());
   uint64_t soff = 0, roff = 0;
   for (int p = 0; p < n; ++p) {
@@ -1298,10 +1327,12 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
       rcv.segs.push_back(sg);
       if (p != me) st_.bytes_received += rc * ncols * 8;
     }
+    if (p != me) st_.bytes_sent += sc * ncols * 8;
     soff += sc;
     roff += rc;
   }
   PSG_NCCL(ncclGroupEnd());
+  PSG_CUDA(cudaEventRecord(xfer_ev_.back()->b, st));
   if (tl >= 0) ctx_.timeline->gpu_end(tl, st);
   xt.mark("  exchange payload", st);
   st_.waves += 1;
@@ -1590,7 +1621,14 @@ ResultRows Execution::run(bool want_rows) {
     }
     const uint64_t cap = pow2_at_least(std::max<uint64_t>(2 * build_rows, 16));
     const int hw_est = 2 + static_cast<int>(probe_sum_wire.size()) <= 4 ? 4 : 8;
-    if (semi || ((cap + 1) * hw_est * 8 > (48ull << 20) && ctx_.semijoin))
+    // A one-GPU table larger than ~L2/2.5 gets a membership screen (Bloom filter, or the exact key
+    // bitmap / rank-indexed table below). PSG_SCREEN_MIN_MB overrides the 48 MB threshold (0: always
+    // - lets small parity cases exercise the bitmap and rank-table paths).
+    static const uint64_t screen_min = [] {
+      const char* e = std::getenv("PSG_SCREEN_MIN_MB");
+      return (e ? std::strtoull(e, nullptr, 10) : 48ull) << 20;
+    }();
+    if (semi || ((cap + 1) * hw_est * 8 > screen_min && ctx_.semijoin))
       bloom_words = std::min<uint64_t>(pow2_at_least(std::max<uint64_t>(sized_rows / 2, 1024)), 8ull << 20);
   }
   DevBuf peers_dev;
@@ -1599,6 +1637,7 @@ ResultRows Execution::run(bool want_rows) {
     // symmetric tables: identical capacity on every rank (sized from the largest owner), carved
     // from the IPC-mapped heap in the same order everywhere so peers find them at equal offsets
     p2p_ok = build_symmetric_agg_table(p2p_max_rows, ctx_.semijoin);
+    st_.agg_table = 5;
     if (!p2p_ok) throw Error(PSG_ERR_MEMORY_EXCEEDED, "symmetric heap too small for the aggregation table (raise PSG_SYMM_MB)");
     std::vector<AggPeer> peers(nr);
     const size_t hot_off = reinterpret_cast<uint8_t*>(aggt_.hot) - ctx_.symm;
@@ -1691,7 +1730,7 @@ ResultRows Execution::run(bool want_rows) {
     }();
     bool rank_mode = false;
     const uint64_t kwords64 = (krange + 63) / 64;
-    if (nr == 1 && krange && grouped_ && rank_env && krange_lo != LLONG_MIN && !p2p &&
+    if (nr == 1 && krange && grouped_ && rank_env && jit_available() && krange_lo != LLONG_MIN && !p2p &&
         kwords64 < (1ULL << 32) && bmat.rows < (1ULL << 32)) {
       agg_kbits_ = DevBuf(ctx_.pool, kwords64 * 8, ctx_.compute);
       DevBuf dup(ctx_.pool, 4, ctx_.compute);
@@ -1713,6 +1752,7 @@ ResultRows Execution::run(bool want_rows) {
       }
     }
     build_agg_table(build_rows, bloom_words, rank_mode ? bmat.rows : 0);
+    st_.agg_table = rank_mode ? 4 : (krange ? 3 : (bloom_words ? 2 : 1));
     if (krange) {
       if (!rank_mode) {
         const uint64_t words = (krange + 31) / 32;
@@ -2205,6 +2245,7 @@ ResultRows Execution::run(bool want_rows) {
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   st_.device_ms = dms;
+  sum_exchange_time();
   if (session_) {
     session_->check_inflate();
     st_.h2d_bytes = session_->h2d_bytes;
@@ -2354,6 +2395,42 @@ std::vector<std::pair<const ScanNode*, std::vector<int>>> Execution::scan_list(c
   scans.push_back({bsrc_.scan, file_cols_of(bsrc_, bm)});
   scans.push_back({psrc_.scan, file_cols_of(psrc_, pm)});
   return scans;
+}
+
+ResultRows Execution::run_ingest_only() {
+  const auto t0 = Clock::now();
+  compile();
+  const int bkey = static_cast<int>(bsrc_.wire.require(shuffle_->build_key));
+  const int pkey = static_cast<int>(psrc_.wire.require(shuffle_->probe_key));
+  std::vector<int> bneed{bkey}, pneed{pkey};
+  if (agg_) {
+    for (int w : build_sum_wire) bneed.push_back(w);
+    for (int w : probe_sum_wire) pneed.push_back(w);
+  } else {
+    for (size_t i = 0; i < bsrc_.wire.size(); ++i)
+      if (static_cast<int>(i) != bkey) bneed.push_back(static_cast<int>(i));
+    for (size_t i = 0; i < psrc_.wire.size(); ++i)
+      if (static_cast<int>(i) != pkey) pneed.push_back(static_cast<int>(i));
+  }
+  RegMap bm = analyse(bsrc_, bneed, bkey, true);
+  RegMap pm = analyse(psrc_, pneed, pkey, true);
+  for (size_t j = 0; j < bsrc_.chain.size(); ++j) bsrc_.chain[j].needed_payload = bm.payload_cols[j];
+  for (size_t j = 0; j < psrc_.chain.size(); ++j) psrc_.chain[j].needed_payload = pm.payload_cols[j];
+  session_ = std::make_unique<StreamSession>(ctx_, scan_list(bm, pm), 0, 0);
+  for (size_t i = 0; i < session_->batches.size(); ++i) {
+    BatchView v;
+    session_->stage(i, v);
+    st_.ingest_bytes += v.bytes;
+    session_->release();
+  }
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  session_->check_inflate();
+  ResultRows out;
+  st_.h2d_bytes = session_->h2d_bytes;
+  if (session_->ingest) st_.io_wait_s = session_->ingest->wait_s();
+  st_.runtime_s = secs_since(t0);
+  out.stats = st_;
+  return out;
 }
 
 void Execution::stage(Staged& st) {
@@ -2508,5 +2585,11 @@ Staged* stage_plan(Ctx& ctx, const std::string& plan_json, const std::string& da
 }
 
 void free_staged(Staged* s) { delete s; }
+
+ResultRows ingest_only(Ctx& ctx, const std::string& plan_json, const std::string& data_root) {
+  PSG_CUDA(cudaSetDevice(ctx.device));
+  Execution ex(ctx, plan_json, data_root, PSG_MODE_OVERLAPPED, nullptr);
+  return ex.run_ingest_only();
+}
 
 }  // namespace psg

@@ -266,6 +266,8 @@ Staged* stage_plan(Ctx& ctx, const std::string& plan_json, const std::string& da
 /// Local plans (scan -> replicated joins -> global aggregate, no shuffle; the Q6 analog).
 ResultRows execute_local(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode);
 void free_staged(Staged* s);
+/// The plan's storage -> pinned -> HBM pipeline alone (no kernels except block-codec inflate).
+ResultRows ingest_only(Ctx& ctx, const std::string& plan_json, const std::string& data_root);
 
 // op adapters (ops.cpp)
 struct HostBatch {

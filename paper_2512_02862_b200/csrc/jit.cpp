@@ -658,8 +658,9 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
     }
   }
   if (P.remote) throw Error(PSG_ERR_INTERNAL, "the fused NVLink path needs the query compiler (PSG_JIT)");
-  if (P.self_probe || P.pack_n || P.unpack_n || P.agg.npacked)
-    throw Error(PSG_ERR_INTERNAL, "owner probe / packed rows / packed accumulators need the query compiler (PSG_JIT)");
+  if (P.self_probe || P.pack_n || P.unpack_n || P.agg.npacked || P.agg.krank)
+    throw Error(PSG_ERR_INTERNAL,
+                "owner probe / packed rows / packed accumulators / rank-indexed table need the query compiler (PSG_JIT)");
   launch_scan(P, d_segs, d_tile_seg, nsegs, ntiles, stream);
 }
 

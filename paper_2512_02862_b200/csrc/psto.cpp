@@ -78,6 +78,9 @@ TableMeta parse_footer_bytes(const uint8_t* tail, size_t tail_len, uint64_t file
   }
   const uint32_t ng = r.get<uint32_t>();
   const uint64_t data_end = tail_offset + tail_len - 12 - flen;
+  // every group record is 8 + 40 bytes per column: bound the count by what the footer holds
+  // before allocating (a corrupt count must not allocate gigabytes)
+  if (static_cast<uint64_t>(ng) * (8 + 40ull * ncols) > r.n - r.off) throw CorruptFooter("row-group count exceeds footer");
   m.groups.resize(ng);
   for (uint32_t g = 0; g < ng; ++g) {
     GroupMeta& gm = m.groups[g];
@@ -90,8 +93,14 @@ TableMeta parse_footer_bytes(const uint8_t* tail, size_t tail_len, uint64_t file
       ch.usize = r.get<uint64_t>();
       ch.min_raw = r.get<uint64_t>();
       ch.max_raw = r.get<uint64_t>();
-      if (ch.offset < 4 || ch.offset + ch.csize > data_end) throw CorruptFooter("column chunk outside file bounds");
-      if (ch.usize != gm.rows * kValueBytes) throw CorruptFooter("uncompressed size disagrees with row count");
+      // (written without offset + csize, which can wrap)
+      if (ch.offset < 4 || ch.offset > data_end || ch.csize > data_end - ch.offset)
+        throw CorruptFooter("column chunk outside file bounds");
+      if (gm.rows > (~0ULL) / kValueBytes || ch.usize != gm.rows * kValueBytes)
+        throw CorruptFooter("uncompressed size disagrees with row count");
+      // identity chunks are read in place by the fused kernels (rows * 8 bytes from the offset)
+      if (m.codec == Codec::Identity && ch.csize != ch.usize)
+        throw CorruptFooter("identity chunk size disagrees with its row count");
       const bool ok = m.schema.fields[c].type == LType::Int64 ? zone_ok<int64_t>(ch) : zone_ok<double>(ch);
       if (gm.rows > 0 && !ok) throw CorruptFooter("zone stats inverted");
     }

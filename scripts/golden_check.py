@@ -20,6 +20,7 @@ def main():
     ctx = psg.Context(0)
     ctx.set_ingest(io_threads=4, batch_bytes=2 << 20)
     bad = 0
+    kinds = {}  # psg_stats.agg_table kind -> cases (4 = rank-indexed table)
     with tempfile.TemporaryDirectory() as tmp:
         cache = {}
 
@@ -39,6 +40,7 @@ def main():
             res = ctx.execute_plan(g["plans"][r["plan"]], data(r["scale"], r["seed"], r["rg_bytes"], r["codec"]),
                                    r["mode"])
             s = po.summary([(res.schema, res.rows)])
+            kinds[res.stats["agg_table"]] = kinds.get(res.stats["agg_table"], 0) + 1
             if r["plan"] == "global_agg" and r["nodes"] > 1:
                 ok = s["colsums"] == r["colsums"]
             else:
@@ -70,6 +72,7 @@ def main():
             bad += not ok
             print("%-26s %s" % (r["case"], "OK" if ok else "BAD"), flush=True)
     ctx.close()
+    print("AGG_TABLES", json.dumps({str(k): v for k, v in sorted(kinds.items())}))
     print("BAD", bad)
     sys.exit(1 if bad else 0)
 

@@ -19,7 +19,7 @@ def test_library_exports_every_header_symbol():
     L = psg.lib()
     for name in declared:
         assert hasattr(L, name), name
-    assert L.psg_abi_version() == 1
+    assert L.psg_abi_version() == 2
 
 
 def test_no_gpu_fails_loudly():

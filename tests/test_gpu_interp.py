@@ -3,6 +3,7 @@
 specialisations such as the owner probe, packed shuffle rows and fused NVLink path are switched
 off by the engine in that mode), the hashed aggregation table at one GPU (PSG_RANK_TABLE=0) and
 the row-ordered rank-table build (PSG_RANK_HOT_SEQ=0) and strided tile order (PSG_CONTIG_TILES=0)."""
+import json
 import os
 import subprocess
 import sys
@@ -19,6 +20,46 @@ def test_interpreter_kernels_match_golden():
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "BAD 0" in r.stdout
+
+
+def _tables(out):
+    line = [x for x in out.splitlines() if x.startswith("AGG_TABLES")][0]
+    return {int(k): v for k, v in json.loads(line.split(" ", 1)[1]).items()}
+
+
+def test_rank_table_on_small_cases_matches_golden():
+    """PSG_SCREEN_MIN_MB=0: every one-GPU grouped join gets the membership screen, so the small
+    golden cases (dense unique o_orderkey) run through the exact key bitmap and the rank-indexed
+    table (k_bitmap_set, k_rank_hot, k_rank_build, the rank probe) - asserted from psg_stats."""
+    env = dict(os.environ, PSG_SCREEN_MIN_MB="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "BAD 0" in r.stdout
+    assert _tables(r.stdout).get(4, 0) > 0, r.stdout[-500:]
+
+
+def test_rank_table_row_ordered_build_matches_golden():
+    """PSG_SCREEN_MIN_MB=0 + PSG_RANK_HOT_SEQ=0: the rank table's hot slots written by the
+    row-ordered build pass (incl. its 16-byte-store branch) on the small golden cases."""
+    env = dict(os.environ, PSG_SCREEN_MIN_MB="0", PSG_RANK_HOT_SEQ="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "BAD 0" in r.stdout
+    assert _tables(r.stdout).get(4, 0) > 0, r.stdout[-500:]
+
+
+def test_interpreter_with_screen_falls_back_to_hashed_table():
+    """PSG_JIT=0 + PSG_SCREEN_MIN_MB=0: the interpreter kernel cannot run the rank-indexed table, so
+    the engine must pick the hashed table (+ exact key bitmap) instead (no rank mode without JIT)."""
+    env = dict(os.environ, PSG_JIT="0", PSG_SCREEN_MIN_MB="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "BAD 0" in r.stdout
+    t = _tables(r.stdout)
+    assert t.get(4, 0) == 0 and t.get(3, 0) > 0, t
 
 
 def test_hashed_aggregation_table_matches_golden():
