@@ -469,6 +469,13 @@ class Execution {
   void materialize_into(DevCols& out, const ScanProgram& p0, const BatchView& v, const std::vector<int>& out_regs,
                         int part_key_reg, DevBuf* part_counts, bool timed = false);
   DevCols alloc_cols(size_t ncols, uint64_t cap);
+  // Local joins whose build side repeats keys (HashTable::build keeps duplicates and probe emits
+  // every match, ops.cpp:105-222, apply_chain pipeline.cpp:431-448): the chain cannot stay in
+  // registers, so the batch is compacted first (predicate only) and each join then expands it
+  // (count -> exclusive scan -> write; payload ++ probe columns like ops.cpp:193-200).
+  bool dup_chain(const SourceDef& s) const;
+  DevCols materialize_chain(const SourceDef& s, const RegMap& m, const BatchView& v, const std::vector<int>& out_regs);
+  DevCols concat_cols(std::vector<DevCols>& parts, size_t ncols);
   uint64_t read_count(DevCols& c);
   void run_scan(const ScanProgram& p, const BatchView& v, bool timed, cudaStream_t stream = nullptr);
 
@@ -933,6 +940,107 @@ DevCols Execution::alloc_cols(size_t ncols, uint64_t cap) {
   c.count = DevBuf(ctx_.pool, 8, ctx_.compute);
   PSG_CUDA(cudaMemsetAsync(c.count.p, 0, 8, ctx_.compute));
   return c;
+}
+
+bool Execution::dup_chain(const SourceDef& s) const {
+  const auto& tables = (&s == &bsrc_) ? bl_tables_ : pl_tables_;
+  for (const auto& t : tables)
+    if (!t->unique) return true;
+  return false;
+}
+
+DevCols Execution::materialize_chain(const SourceDef& s, const RegMap& m, const BatchView& v,
+                                     const std::vector<int>& out_regs) {
+  auto& tables = (&s == &bsrc_) ? bl_tables_ : pl_tables_;
+  // 1. predicate + compaction of the base columns the chain and the sink read (no joins in-kernel)
+  ScanProgram p = base_program(s, m, false);
+  std::vector<int> base_regs(m.n_in);
+  std::iota(base_regs.begin(), base_regs.end(), 0);
+  DevCols base = alloc_cols(base_regs.size(), std::max<uint64_t>(v.rows, 1));
+  materialize_into(base, p, v, base_regs, -1, nullptr);
+  uint64_t n = read_count(base);
+  std::vector<ColRef> refs;
+  for (int c = 0; c < m.n_in; ++c) refs.push_back({-1, m.base_proj[c]});
+  std::vector<DevBuf> cols = std::move(base.cols);
+  // 2. one expansion per local join, in chain order
+  for (size_t j = 0; j < s.chain.size(); ++j) {
+    const ColRef kref = s.stage_refs[j][s.chain[j].probe_key_stage];
+    const size_t ki = std::find(refs.begin(), refs.end(), kref) - refs.begin();
+    if (ki == refs.size()) throw Error(PSG_ERR_INTERNAL, "join key column not materialised");
+    const LocalTableDev& t = tables[j]->dev;
+    const uint64_t* keys = cols[ki].as<uint64_t>();
+    DevBuf counts(ctx_.pool, (n + 1) * 4, ctx_.compute), offs(ctx_.pool, (n + 1) * 4, ctx_.compute);
+    PSG_CUDA(cudaMemsetAsync(counts.p, 0, (n + 1) * 4, ctx_.compute));
+    launch_expand_count(t, keys, n, counts.as<uint32_t>(), ctx_.compute);
+    const size_t tb = exclusive_scan_u32(nullptr, nullptr, n + 1, nullptr, 0, ctx_.compute);
+    DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
+    exclusive_scan_u32(counts.as<uint32_t>(), offs.as<uint32_t>(), n + 1, tmp.p, tb, ctx_.compute);
+    uint32_t total = 0;
+    PSG_CUDA(cudaMemcpyAsync(&total, offs.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+    PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    const int np = t.npayload;
+    std::vector<DevBuf> next;
+    std::vector<ColRef> nrefs;
+    for (int k = 0; k < np; ++k) {
+      next.emplace_back(ctx_.pool, std::max<uint64_t>(total, 1) * 8 + 16, ctx_.compute);
+      nrefs.push_back({static_cast<int>(j), m.payload_cols[j][k]});
+    }
+    for (size_t c = 0; c < cols.size(); ++c) {
+      next.emplace_back(ctx_.pool, std::max<uint64_t>(total, 1) * 8 + 16, ctx_.compute);
+      nrefs.push_back(refs[c]);
+    }
+    std::vector<const uint64_t*> in;
+    std::vector<uint64_t*> out;
+    for (auto& c : cols) in.push_back(c.as<uint64_t>());
+    for (auto& c : next) out.push_back(c.as<uint64_t>());
+    if (np + in.size() > static_cast<size_t>(kMaxOut)) throw InvalidInput("local join chain carries too many columns");
+    launch_expand_write(t, keys, n, offs.as<uint32_t>(), in.data(), static_cast<int>(in.size()), out.data(), ctx_.compute);
+    cols = std::move(next);
+    refs = std::move(nrefs);
+    n = total;
+  }
+  // 3. the requested registers, in order
+  std::map<int, ColRef> ref_of_reg;
+  for (const auto& [ref, reg] : m.reg_of) ref_of_reg[reg] = ref;
+  DevCols out;
+  out.cap = std::max<uint64_t>(n, 1);
+  out.rows = n;
+  std::vector<bool> taken(cols.size(), false);
+  for (int r : out_regs) {
+    const size_t i = std::find(refs.begin(), refs.end(), ref_of_reg.at(r)) - refs.begin();
+    if (i == refs.size()) throw Error(PSG_ERR_INTERNAL, "chain output column not materialised");
+    if (!taken[i]) {
+      taken[i] = true;
+      out.cols.push_back(std::move(cols[i]));
+    } else {  // the same column twice (e.g. key and a sum of it)
+      DevBuf cp(ctx_.pool, out.cap * 8 + 16, ctx_.compute);
+      PSG_CUDA(cudaMemcpyAsync(cp.p, out.cols[std::find(out_regs.begin(), out_regs.end(), r) - out_regs.begin()].p, n * 8,
+                               cudaMemcpyDeviceToDevice, ctx_.compute));
+      out.cols.push_back(std::move(cp));
+    }
+  }
+  out.count = DevBuf(ctx_.pool, 8, ctx_.compute);
+  PSG_CUDA(cudaMemcpyAsync(out.count.p, &out.rows, 8, cudaMemcpyHostToDevice, ctx_.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));  // the host source above is a stack value
+  return out;
+}
+
+DevCols Execution::concat_cols(std::vector<DevCols>& parts, size_t ncols) {
+  uint64_t total = 0;
+  for (auto& p : parts) total += p.rows;
+  DevCols out = alloc_cols(ncols, std::max<uint64_t>(total, 1));
+  uint64_t at = 0;
+  for (auto& p : parts) {
+    for (size_t c = 0; c < ncols && p.rows; ++c)
+      PSG_CUDA(cudaMemcpyAsync(out.cols[c].as<uint64_t>() + at, p.cols[c].p, p.rows * 8, cudaMemcpyDeviceToDevice,
+                               ctx_.compute));
+    at += p.rows;
+  }
+  out.rows = total;
+  PSG_CUDA(cudaMemcpyAsync(out.count.p, &out.rows, 8, cudaMemcpyHostToDevice, ctx_.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  parts.clear();
+  return out;
 }
 
 uint64_t Execution::read_count(DevCols& c) {
@@ -1504,10 +1612,7 @@ ResultRows Execution::run(bool want_rows) {
   pt.mark("compile", ctx_.compute);
   build_local_tables();
   pt.mark("local tables", ctx_.compute);
-  for (auto& t : bl_tables_)
-    if (!t->unique) throw InvalidInput("local join build side with duplicate keys is not supported by the fused path yet");
-  for (auto& t : pl_tables_)
-    if (!t->unique) throw InvalidInput("local join build side with duplicate keys is not supported by the fused path yet");
+  const bool bdup = dup_chain(bsrc_), pdup = dup_chain(psrc_);  // expanding local joins
 
   // ---------------- build side ----------------
   ScanProgram bp = base_program(bsrc_, bm, true);
@@ -1518,7 +1623,7 @@ ResultRows Execution::run(bool want_rows) {
   DevCols bmat;
   // Fused NVLink path (grouped aggregates, N > 1): no shuffle of rows at all — build keys are
   // inserted into, and probe rows aggregated in, the owner rank's table through peer memory.
-  const bool p2p = nr > 1 && agg_ && grouped_ && ctx_.p2p && ctx_.symm_bytes > 0 && jit_available();
+  const bool p2p = nr > 1 && agg_ && grouped_ && ctx_.p2p && ctx_.symm_bytes > 0 && jit_available() && !bdup && !pdup;
   ctx_.symm_top = 0;
   DevBuf owner_hist;
   if (nr == 1 || p2p) {
@@ -1528,12 +1633,19 @@ ResultRows Execution::run(bool want_rows) {
       PSG_CUDA(cudaMemsetAsync(owner_hist.p, 0, nr * 8, ctx_.compute));
     }
     BatchView v;
+    std::vector<DevCols> parts;
     while (bfeed->next(v)) {
-      materialize_into(bmat, bp, v, b_out, p2p ? b_out[0] : -1, p2p ? &owner_hist : nullptr);
+      if (bdup)
+        parts.push_back(materialize_chain(bsrc_, bm, v, b_out));
+      else
+        materialize_into(bmat, bp, v, b_out, p2p ? b_out[0] : -1, p2p ? &owner_hist : nullptr);
       bfeed->done();
       st_.ingest_bytes += v.bytes;
     }
-    read_count(bmat);
+    if (bdup)
+      bmat = concat_cols(parts, b_out.size());
+    else
+      read_count(bmat);
   } else {
     // agree on the wave count (the reference's kDoneFlag vote, pipeline.cpp:696-722)
     uint64_t waves = bfeed->nbatches;
@@ -1548,7 +1660,12 @@ ResultRows Execution::run(bool want_rows) {
       DevCols mat = alloc_cols(b_out.size(), std::max<uint64_t>(have ? v.rows : 1, 1));
       DevBuf pc(ctx_.pool, nr * 8, ctx_.compute);
       PSG_CUDA(cudaMemsetAsync(pc.p, 0, nr * 8, ctx_.compute));
-      if (have) {
+      if (have && bdup) {
+        mat = materialize_chain(bsrc_, bm, v, b_out);
+        launch_part_hist(mat.cols[0].as<uint64_t>(), mat.rows, nr, pc.as<unsigned long long>(), ctx_.compute);
+        bfeed->done();
+        st_.ingest_bytes += v.bytes;
+      } else if (have) {
         materialize_into(mat, bp, v, b_out, b_out[0], &pc);
         bfeed->done();
         st_.ingest_bytes += v.bytes;
@@ -1973,7 +2090,7 @@ ResultRows Execution::run(bool want_rows) {
       st_.ingest_bytes += v.bytes;
     }
     gpu_barrier();  // every rank's probe contributions landed before owners finalise
-  } else if (nr == 1 && agg_) {
+  } else if (nr == 1 && agg_ && !pdup) {
     ScanProgram p = pp;
     p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
     p.agg = aggt_;
@@ -2007,7 +2124,7 @@ ResultRows Execution::run(bool want_rows) {
       const char* e = std::getenv("PSG_PACK");
       return !(e && std::string(e) == "0");
     }();
-    if (nr > 1 && agg_ && jit_available() && pack_env && pneed.size() <= static_cast<size_t>(kMaxOut)) {
+    if (nr > 1 && agg_ && jit_available() && pack_env && !pdup && pneed.size() <= static_cast<size_t>(kMaxOut)) {
       const size_t np = pneed.size();
       std::vector<long long> lohi(2 * np);
       for (size_t k = 0; k < np; ++k) {
@@ -2071,7 +2188,7 @@ ResultRows Execution::run(bool want_rows) {
       const char* e = std::getenv("PSG_SELF_PROBE");
       return !(e && std::string(e) == "0");
     }();
-    if (nr > 1 && agg_ && grouped_ && jit_available() && self_probe_env && pack.pack_n == 0) {
+    if (nr > 1 && agg_ && grouped_ && jit_available() && self_probe_env && pack.pack_n == 0 && !pdup) {
       join_build();  // the scan itself probes this rank's table
       pp.self_probe = 1;
       pp.self_rank = ctx_.rank;
@@ -2097,7 +2214,7 @@ ResultRows Execution::run(bool want_rows) {
       return e ? std::max(1, std::atoi(e)) : 1;
     }();
     const std::vector<Segment>* hsegs = pfeed->host_segments();
-    if (nr > 1 && agg_ && hsegs != nullptr && waves == 1 && probe_chunks > 1) {
+    if (nr > 1 && agg_ && hsegs != nullptr && waves == 1 && probe_chunks > 1 && !pdup) {
       const int K = probe_chunks;
       BatchView whole;
       if (pfeed->next(whole)) st_.ingest_bytes += whole.bytes;
@@ -2168,7 +2285,12 @@ ResultRows Execution::run(bool want_rows) {
       DevCols mat = alloc_cols(mat_out.size(), std::max<uint64_t>(have ? v.rows : 1, 1));
       DevBuf pc(ctx_.pool, nr * 8, ctx_.compute);
       PSG_CUDA(cudaMemsetAsync(pc.p, 0, nr * 8, ctx_.compute));
-      if (have) {
+      if (have && pdup) {
+        mat = materialize_chain(psrc_, pm, v, mat_out);
+        if (nr > 1) launch_part_hist(mat.cols[0].as<uint64_t>(), mat.rows, nr, pc.as<unsigned long long>(), ctx_.compute);
+        pfeed->done();
+        st_.ingest_bytes += v.bytes;
+      } else if (have) {
         materialize_into(mat, pp, v, mat_out, p_out[0], &pc, staged_ != nullptr);
         pfeed->done();
         st_.ingest_bytes += v.bytes;
@@ -2332,8 +2454,7 @@ ResultRows Execution::run_local() {
     session_ = std::make_unique<StreamSession>(ctx_, scans, plan_.memory_budget_bytes, ht_reserve);
   }
   build_local_tables();
-  for (auto& t : pl_tables_)
-    if (!t->unique) throw InvalidInput("local join build side with duplicate keys is not supported by the fused path yet");
+  const bool pdup = dup_chain(psrc_);
   global_acc_ = DevBuf(ctx_.pool, (2 * kMaxSums + 1) * 8, ctx_.compute);
   PSG_CUDA(cudaMemsetAsync(global_acc_.p, 0, (2 * kMaxSums + 1) * 8, ctx_.compute));
   ScanProgram p = base_program(psrc_, pm, true);
@@ -2347,7 +2468,37 @@ ResultRows Execution::run_local() {
   auto feed = open_feed(*psrc_.scan, file_cols_of(psrc_, pm));
   BatchView v;
   while (feed->next(v)) {
-    run_scan(p, v, false);
+    if (pdup) {  // expanding local joins: compact + expand, then sum the materialised rows
+      std::vector<int> regs;
+      for (int w : need) regs.push_back(pm.reg_of.at(psrc_.stage_refs.back()[w]));
+      DevCols mat = materialize_chain(psrc_, pm, v, regs);
+      ScanProgram q;
+      std::memset(&q, 0, sizeof q);
+      q.n_in = static_cast<int>(regs.size());
+      q.n_early = q.n_in;
+      q.n_regs = std::max(1, q.n_in);
+      q.part_key_reg = -1;
+      q.key_reg = -1;
+      q.sink = SINK_AGG_SCAN;
+      q.n_sum = p.n_sum;
+      for (int k = 0; k < q.n_sum; ++k) {
+        q.sum_reg[k] = k;  // need[k] == probe_sum_wire[k]
+        q.global_float[1 + k] = p.global_float[1 + k];
+      }
+      q.global_acc = p.global_acc;
+      Segment sg;
+      std::memset(&sg, 0, sizeof sg);
+      for (size_t c = 0; c < regs.size(); ++c) sg.col[c] = mat.cols[c].as<uint64_t>();
+      sg.rows = mat.rows;
+      std::vector<Segment> one;
+      if (sg.rows) one.push_back(sg);
+      DevBuf holder;
+      BatchView mv = upload_segments(one, holder);
+      run_scan(q, mv, false);
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    } else {
+      run_scan(p, v, false);
+    }
     feed->done();
     st_.ingest_bytes += v.bytes;
   }

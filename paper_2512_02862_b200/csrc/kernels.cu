@@ -527,7 +527,7 @@ __global__ void k_expand_count(LocalTableDev t, const uint64_t* pk, uint64_t n, 
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t s = local_lookup(t, pk[i]);
-    counts[i] = s == ~0ULL ? 0u : t.cnt[s];
+    counts[i] = s == ~0ULL ? 0u : (t.bitmap ? 1u : t.cnt[s]);  // bitmap tables: unique keys, no payload
   }
 }
 void launch_expand_count(LocalTableDev t, const uint64_t* pk, uint64_t n, uint32_t* counts, void* stream) {
@@ -542,7 +542,7 @@ __global__ void k_expand_write(LocalTableDev t, const uint64_t* pk, uint64_t n, 
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t s = local_lookup(t, pk[i]);
     if (s == ~0ULL) continue;
-    const uint32_t c = t.cnt[s], st = t.start[s];
+    const uint32_t c = t.bitmap ? 1u : t.cnt[s], st = t.bitmap ? 0u : t.start[s];
     const uint64_t o = off[i];
     for (uint32_t k = 0; k < c; ++k) {
       for (int p = 0; p < t.npayload; ++p) out.p[p][o + k] = t.payload[p][st + k];
@@ -677,6 +677,30 @@ void launch_gather64(const uint64_t* const* in_cols, int ncols, const uint64_t* 
   }
   count_launch();
   k_gather64<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, ncols, idx, n, oc);
+}
+
+/// Destination histogram of n keys (partition_of, hashing.hpp:35-37): one shared atomic per
+/// (warp, destination) from __match_any_sync groups, one global atomic per (block, destination).
+__global__ void k_part_hist(const uint64_t* __restrict__ keys, uint64_t n, int nparts, unsigned long long* counts) {
+  __shared__ unsigned long long s_cnt[kMaxParts];
+  for (int d = threadIdx.x; d < nparts; d += blockDim.x) s_cnt[d] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = blockIdx.x * static_cast<uint64_t>(blockDim.x); base < n;
+       base += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t i = base + threadIdx.x;
+    const uint32_t d = i < n ? part_of(keys[i], static_cast<uint32_t>(nparts)) : 0xffffffffu;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (d != 0xffffffffu && lane == __ffs(peers) - 1) atomicAdd(&s_cnt[d], static_cast<unsigned long long>(__popc(peers)));
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < nparts; d += blockDim.x)
+    if (s_cnt[d]) atomicAdd(&counts[d], s_cnt[d]);
+}
+void launch_part_hist(const uint64_t* keys, uint64_t n, int nparts, unsigned long long* counts, void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_part_hist<<<grid_for(n, 256), 256, 0, S(stream)>>>(keys, n, nparts, counts);
 }
 
 /// out[0] = min, out[1] = max of n signed keys (out preset to {INT64_MAX, INT64_MIN}).

@@ -99,3 +99,54 @@ def test_random_plan_matches_oracle(ctx, data, seed):
     got = ctx.execute_plan(plan, data, mode)
     s = po.summary([(got.schema, got.rows)])
     assert s == want, (seed, mode, json.dumps(plan))
+
+
+def random_dup_plan(rng):
+    """Replicated build sides with repeated keys (HashTable::build keeps duplicates and the probe
+    emits every match, ops.cpp:105-222): orders replicated and built on o_custkey."""
+    def atoms(cols):  # at most one range atom per scan, so most plans return rows
+        if rng.random() < 0.4:
+            return []
+        c = rng.choice(cols)
+        lo, hi = RANGES[c]
+        return [{"col": c, "op": rng.choice(["<", "<=", ">=", ">", "!="]), "value": rng.randint(lo, hi)}]
+
+    opred = atoms(["o_orderdate", "o_shippriority"])
+    lpred = atoms(["l_shipdate", "l_discount", "l_extendedprice"])
+    cpred = atoms(["c_mktsegment"])
+    scans = [{"table": "orders", "paths": ["{data}/dev*/orders.node{node}.psto"], "replicated": True, "predicate": opred},
+             {"table": "customer", "paths": ["{data}/dev*/customer.psto"], "predicate": cpred},
+             {"table": "lineitem", "paths": ["{data}/dev*/lineitem.node{node}.psto"], "predicate": lpred}]
+    oc = {"id": "oc", "build": "orders", "probe": "customer", "build_key": "o_custkey", "probe_key": "c_custkey",
+          "mode": "replicated"}
+    if rng.random() < 0.5:  # expanding chain on the shuffle build side
+        joins = [oc, {"id": "res", "build": "oc", "probe": "lineitem", "build_key": "o_orderkey",
+                      "probe_key": "l_orderkey", "mode": "shuffle"}]
+        group = "l_orderkey"
+    else:  # ... on the shuffle probe side (lineitem shuffled as the build side, keys repeat)
+        joins = [oc, {"id": "res", "build": "lineitem", "probe": "oc", "build_key": "l_orderkey",
+                      "probe_key": "o_orderkey", "mode": "shuffle"}]
+        group = "o_orderkey"
+    if rng.random() < 0.3:  # a second, unique-key local join after the expanding one
+        scans.append({"table": "cust2", "paths": ["{data}/dev*/customer.psto"], "replicated": True,
+                      "predicate": atoms(["c_mktsegment"])})
+        j2 = {"id": "oc2", "build": "cust2", "probe": "oc", "build_key": "c_custkey", "probe_key": "c_custkey",
+              "mode": "replicated"}
+        joins = [joins[0], j2] + [dict(joins[1], **({"build": "oc2"} if joins[1]["build"] == "oc" else {"probe": "oc2"}))]
+    plan = {"scans": scans, "joins": joins}
+    r = rng.random()
+    if r < 0.85:
+        cand = ["l_extendedprice", "l_discount", "l_shipdate", "o_orderdate", "o_shippriority", "c_mktsegment"]
+        plan["aggregate"] = {"group_by": group if r < 0.7 else "", "sums": rng.sample(cand, rng.randint(0, 4))}
+    return plan
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_duplicate_key_plan_matches_oracle(ctx, data, seed):
+    rng = random.Random(1000 + seed)
+    plan = random_dup_plan(rng)
+    mode = rng.choice(list(psg.MODES))
+    want = po.summary(po.execute(json.dumps(plan), data, 1))
+    got = ctx.execute_plan(plan, data, mode)
+    s = po.summary([(got.schema, got.rows)])
+    assert s == want, (seed, mode, json.dumps(plan))
