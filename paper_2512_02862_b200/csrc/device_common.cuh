@@ -112,6 +112,9 @@ struct AggTableDev {
   // its rank among the build keys, krank[w] + popc(kbits64[w] below the key's bit) for 64-bit
   // bitmap word w, so slots [0, mask] are all occupied in key order and nothing is hashed.
   const uint32_t* krank;
+  // {kbits64[w], krank[w]} interleaved per 64-key word (16 B): membership and rank of a key in ONE
+  // L2 sector (nullptr: use kbits/krank)
+  const unsigned long long* krec;
 };
 
 /// Hit count and probe-side sum p of a hot slot (decodes the packed accumulator).
@@ -190,7 +193,10 @@ struct ScanProgram {
   // mask/shift/hw/cw come from `agg`, only the base pointers differ per rank.
   const AggPeer* peers;
   int32_t remote;
-  int32_t pad_remote;
+  // the engine guarantees 16-byte aligned column chunks and readable padding past each chunk's
+  // end (PSTO batches, staged images): the query compiler may then stream the early columns into
+  // shared memory with bulk copies (the warp-specialised probe, jit.cpp)
+  int32_t staged_ok;
 };
 
 #if defined(__CUDACC__) || defined(__CUDACC_RTC__)
@@ -286,6 +292,17 @@ __device__ __forceinline__ uint64_t ldg_keep_u64(const void* p, uint64_t policy)
   uint64_t v;
   asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(policy));
   return v;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+/// Makes mbarrier.init visible to the async (bulk-copy) proxy before the first copy.
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n\tfence.proxy.async.shared::cta;" ::: "memory");
+}
+/// 16-byte L2-resident record (evict_last policy), e.g. the rank table's {bits, rank} word.
+__device__ __forceinline__ void ldg_keep_v2u64(const unsigned long long* p, uint64_t policy, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u64 {%0, %1}, [%2], %3;" : "=l"(a), "=l"(b) : "l"(p), "l"(policy));
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;

@@ -517,7 +517,7 @@ class Execution {
   };
   std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
   // agg table
-  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, agg_krank_, global_acc_, barrier_word_;
+  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, agg_krank_, agg_krec_, global_acc_, barrier_word_;
   AggTableDev aggt_{};
   // the build insert running on ctx_.comm concurrently with the probe side (N > 1 Bloom path)
   struct Event {
@@ -1865,6 +1865,9 @@ ResultRows Execution::run(bool want_rows) {
         const size_t tb = exclusive_scan_u32(nullptr, nullptr, kwords64, nullptr, 0, ctx_.compute);
         DevBuf tmp(ctx_.pool, tb, ctx_.compute);
         exclusive_scan_u32(cnt.as<uint32_t>(), agg_krank_.as<uint32_t>(), kwords64, tmp.p, tb, ctx_.compute);
+        agg_krec_ = DevBuf(ctx_.pool, kwords64 * 16, ctx_.compute);
+        launch_krec_build(agg_kbits_.as<unsigned long long>(), agg_krank_.as<uint32_t>(), kwords64,
+                          agg_krec_.as<unsigned long long>(), ctx_.compute);
         rank_mode = true;
       }
     }
@@ -1879,7 +1882,10 @@ ResultRows Execution::run(bool want_rows) {
       aggt_.kbits = agg_kbits_.as<uint32_t>();
       aggt_.kmin = krange_lo;
       aggt_.krange = krange;
-      if (rank_mode) aggt_.krank = agg_krank_.as<uint32_t>();
+      if (rank_mode) {
+        aggt_.krank = agg_krank_.as<uint32_t>();
+        aggt_.krec = agg_krec_.as<unsigned long long>();
+      }
     }
     pack_accumulators();
     pt.mark("  agg alloc+init", ctx_.compute);
@@ -2093,6 +2099,7 @@ ResultRows Execution::run(bool want_rows) {
   } else if (nr == 1 && agg_ && !pdup) {
     ScanProgram p = pp;
     p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
+    p.staged_ok = 1;  // PSTO batches / staged images: 16-byte aligned chunks with tail padding
     p.agg = aggt_;
     p.key_reg = pm.reg_of.at(psrc_.stage_refs.back()[pkey]);
     p.n_sum = static_cast<int>(probe_sum_wire.size());

@@ -35,6 +35,7 @@ struct Compiled {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kern = nullptr;
   int block = kBlock;  // threads per CTA (jit_block)
+  int smem = 0;        // dynamic shared memory per CTA (the staged probe's ring)
   int per_sm = 1;
   bool ok = false;
 };
@@ -182,6 +183,101 @@ void emit_accumulate(std::ostringstream& s, const ScanProgram& P, const char* in
   }
 }
 
+
+/// Rank-indexed table probe (SINK_PROBE): the key's 64-bit bitmap word and its block prefix (both
+/// L2-resident; one 16-byte {bits, rank} record when krec is set) give membership and the slot at
+/// once - no hashing, no collision chain. `late` emits the loads of the non-key columns (for the
+/// surviving rows only), then every survivor accumulates into its hot slot.
+template <class Late>
+void emit_rank_probe(std::ostringstream& s, const ScanProgram& P, Late late) {
+  s << "    { const AggTableDev& T = P.agg; uint64_t sl[R]; unsigned long long bw[R]; uint64_t bp[R]; uint32_t bb[R];\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bp[r] = 0; bb[r] = 0; const uint64_t key = " << V(P.key_reg) << "[r];\n"
+    << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+    << "          if (d < T.krange) { bb[r] = static_cast<uint32_t>(d & 63);\n";
+  if (P.agg.krec != nullptr)
+    s << "            uint64_t a, b; ldg_keep_v2u64(T.krec + 2 * (d >> 6), pol_keep, a, b); bw[r] = a; bp[r] = b; } } }\n";
+  else
+    s << "            bw[r] = ldg_keep_u64(reinterpret_cast<const unsigned long long*>(T.kbits) + (d >> 6), pol_keep);\n"
+      << "            bp[r] = ldg_keep_u32(T.krank + (d >> 6), pol_keep); } } }\n";
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0;\n"
+    << "        if (!((bw[r] >> bb[r]) & 1ULL)) pass &= ~(1u << r);\n"
+    << "        else sl[r] = bp[r] + static_cast<uint64_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n";
+  late();
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+    << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
+  emit_accumulate(s, P, "        ");
+  s << "      }\n    }\n";
+}
+
+/// Predicate atoms: clear a row's pass bit when an atom fails.
+void emit_atoms(std::ostringstream& s, const ScanProgram& P) {
+  for (int a = 0; a < P.n_atoms; ++a) {
+    const AtomDesc& at = P.atoms[a];
+    if (at.is_float) {
+      s << "    { const double lit = __longlong_as_double(static_cast<long long>(P.atoms[" << a << "].lit));\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!(__longlong_as_double(static_cast<long long>(" << V(at.reg)
+        << "[r])) " << op_str(at.op) << " lit)) pass &= ~(1u << r);\n    }\n";
+    } else {
+      s << "    { const long long lit = static_cast<long long>(P.atoms[" << a << "].lit);\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!(static_cast<long long>(" << V(at.reg) << "[r]) "
+        << op_str(at.op) << " lit)) pass &= ~(1u << r);\n    }\n";
+    }
+  }
+}
+
+/// Unique-key local joins of the chain (two-stage probe: home-slot loads for all rows first).
+void emit_joins(std::ostringstream& s, const ScanProgram& P) {
+  for (int j = 0; j < P.n_joins; ++j) {
+    const JoinDesc& jd = P.joins[j];
+    if (jd.t.bitmap != nullptr) {  // dense unique keys, no payload: membership bitmap (L2-resident)
+      s << "    { const LocalTableDev& T = P.joins[" << j << "].t;\n"
+        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && !local_bitmap_has(T, " << V(jd.key_reg)
+        << "[r])) pass &= ~(1u << r);\n    }\n";
+      continue;
+    }
+    s << "    { const LocalTableDev& T = P.joins[" << j << "].t;\n      uint64_t sl[R], k0[R];\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = ~0ULL; k0[r] = 0; if (pass & (1u << r)) {\n"
+      << "        const uint64_t key = " << V(jd.key_reg) << "[r];\n"
+      << "        if (key == kEmptyKey) { if (T.cnt[T.mask + 1] == 0) pass &= ~(1u << r); else { sl[r] = T.mask + 1; k0[r] = key; } }\n"
+      << "        else { sl[r] = slot_of(key, T.shift); k0[r] = T.keys[sl[r]]; } } }\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+      << "        const uint64_t key = " << V(jd.key_reg) << "[r]; uint64_t sx = sl[r], kk = k0[r];\n"
+      << "        if (sx != T.mask + 1) { while (kk != key && kk != kEmptyKey) { sx = (sx + 1) & T.mask; kk = T.keys[sx]; }\n"
+      << "          if (kk != key) { pass &= ~(1u << r); continue; } }\n";
+    if (jd.t.npayload > 0) {
+      s << "        const uint32_t st = T.start[sx];\n";
+      for (int p = 0; p < jd.t.npayload; ++p)
+        s << "        " << V(jd.payload_reg[p]) << "[r] = T.payload[" << p << "][st];\n";
+    }
+    s << "      }\n    }\n";
+  }
+}
+
+/// Warp-specialised probe for the one-GPU rank-indexed table (PSG_TMA=0: off). Shape knobs:
+/// PSG_TMA_NG consumer groups of 8 warps (default 2), PSG_TMA_NS ring stages (6), PSG_TMA_CTAS
+/// CTAs per SM (2).
+struct StagedShape {
+  int groups, stages, ctas;
+};
+StagedShape staged_shape() {
+  static const StagedShape sh = [] {
+    auto env = [](const char* n, int d) {
+      const char* e = std::getenv(n);
+      return e ? std::max(1, std::atoi(e)) : d;
+    };
+    return StagedShape{env("PSG_TMA_NG", 2), env("PSG_TMA_NS", 6), env("PSG_TMA_CTAS", 2)};
+  }();
+  return sh;
+}
+bool staged_probe(const ScanProgram& P) {
+  static const bool on = [] {
+    const char* e = std::getenv("PSG_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on && P.staged_ok && P.sink == SINK_PROBE && P.agg.krec != nullptr && !P.remote && P.unpack_n == 0 &&
+         P.n_early >= 1 && P.n_early <= 4 && P.n_in <= kMaxIn;
+}
+
 /// Rows per thread per tile (R) of the kernel: R x 32 rows per warp, 1024 / (32 R) warps per
 /// block (a tile is always 1024 rows).
 int jit_rows(const ScanProgram& P) {
@@ -218,7 +314,11 @@ int min_blocks(const ScanProgram& P) {
   return jit_rows(P) == 8 ? 8 : 6;
 }
 
+std::string jit_source_staged(const ScanProgram& P);
+bool staged_probe(const ScanProgram& P);
+
 std::string jit_source(const ScanProgram& P) {
+  if (staged_probe(P)) return jit_source_staged(P);
   std::ostringstream s;
   const int nin = P.n_in, nregs = std::max(1, P.n_regs);
   const bool mat = P.sink == SINK_MATERIALIZE || P.sink == SINK_COUNT;
@@ -308,70 +408,21 @@ std::string jit_source(const ScanProgram& P) {
   }();
   const bool keys_first = early_keys && P.n_pred > 0 && P.n_early > P.n_pred;
   emit_loads(s, 0, keys_first ? P.n_early : P.n_pred);
-  for (int a = 0; a < P.n_atoms; ++a) {
-    const AtomDesc& at = P.atoms[a];
-    if (at.is_float) {
-      s << "    { const double lit = __longlong_as_double(static_cast<long long>(P.atoms[" << a << "].lit));\n"
-        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!(__longlong_as_double(static_cast<long long>(" << V(at.reg)
-        << "[r])) " << op_str(at.op) << " lit)) pass &= ~(1u << r);\n    }\n";
-    } else {
-      s << "    { const long long lit = static_cast<long long>(P.atoms[" << a << "].lit);\n"
-        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!(static_cast<long long>(" << V(at.reg) << "[r]) "
-        << op_str(at.op) << " lit)) pass &= ~(1u << r);\n    }\n";
-    }
-  }
+  emit_atoms(s, P);
   // Phase B: early columns
   if (!keys_first) emit_loads(s, P.n_pred, P.n_early);
   for (int k = 0; k < P.unpack_n; ++k)  // bit-packed shuffle rows: register 0 -> 1..unpack_n
     s << "#pragma unroll\n    for (int r = 0; r < R; ++r) " << V(1 + k) << "[r] = static_cast<uint64_t>(P.pack_min[" << k
       << "]) + ((" << V(0) << "[r] >> P.pack_shift[" << k << "]) & P.pack_mask[" << k << "]);\n";
-  // Phase C: unique-key local joins (two-stage probe: home-slot loads for all rows first)
-  for (int j = 0; j < P.n_joins; ++j) {
-    const JoinDesc& jd = P.joins[j];
-    if (jd.t.bitmap != nullptr) {  // dense unique keys, no payload: membership bitmap (L2-resident)
-      s << "    { const LocalTableDev& T = P.joins[" << j << "].t;\n"
-        << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && !local_bitmap_has(T, " << V(jd.key_reg)
-        << "[r])) pass &= ~(1u << r);\n    }\n";
-      continue;
-    }
-    s << "    { const LocalTableDev& T = P.joins[" << j << "].t;\n      uint64_t sl[R], k0[R];\n"
-      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = ~0ULL; k0[r] = 0; if (pass & (1u << r)) {\n"
-      << "        const uint64_t key = " << V(jd.key_reg) << "[r];\n"
-      << "        if (key == kEmptyKey) { if (T.cnt[T.mask + 1] == 0) pass &= ~(1u << r); else { sl[r] = T.mask + 1; k0[r] = key; } }\n"
-      << "        else { sl[r] = slot_of(key, T.shift); k0[r] = T.keys[sl[r]]; } } }\n"
-      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
-      << "        const uint64_t key = " << V(jd.key_reg) << "[r]; uint64_t sx = sl[r], kk = k0[r];\n"
-      << "        if (sx != T.mask + 1) { while (kk != key && kk != kEmptyKey) { sx = (sx + 1) & T.mask; kk = T.keys[sx]; }\n"
-      << "          if (kk != key) { pass &= ~(1u << r); continue; } }\n";
-    if (jd.t.npayload > 0) {
-      s << "        const uint32_t st = T.start[sx];\n";
-      for (int p = 0; p < jd.t.npayload; ++p)
-        s << "        " << V(jd.payload_reg[p]) << "[r] = T.payload[" << p << "][st];\n";
-    }
-    s << "      }\n    }\n";
-  }
+  // Phase C: unique-key local joins
+  emit_joins(s, P);
   if (P.remote && P.sink == SINK_PROBE) {
     emit_remote_probe(s, P);
   } else if (P.remote && P.sink == SINK_BUILD) {
     emit_loads(s, P.n_early, P.n_in);
     emit_remote_build(s, P);
   } else if (probe && P.agg.krank != nullptr && P.sink == SINK_PROBE) {
-    // Rank-indexed table: the key's 64-bit bitmap word and its block prefix (both L2-resident)
-    // give membership and the slot at once - no hashing, no collision chain.
-    s << "    { const AggTableDev& T = P.agg; uint64_t sl[R]; unsigned long long bw[R]; uint32_t bp[R], bb[R];\n"
-      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bp[r] = 0; bb[r] = 0; const uint64_t key = " << V(P.key_reg) << "[r];\n"
-      << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
-      << "          if (d < T.krange) { bb[r] = static_cast<uint32_t>(d & 63);\n"
-      << "            bw[r] = ldg_keep_u64(reinterpret_cast<const unsigned long long*>(T.kbits) + (d >> 6), pol_keep);\n"
-      << "            bp[r] = ldg_keep_u32(T.krank + (d >> 6), pol_keep); } } }\n"
-      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0;\n"
-      << "        if (!((bw[r] >> bb[r]) & 1ULL)) pass &= ~(1u << r);\n"
-      << "        else sl[r] = bp[r] + static_cast<uint64_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n";
-    emit_loads(s, P.n_early, P.n_in);
-    s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
-      << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
-    emit_accumulate(s, P, "        ");
-    s << "      }\n    }\n";
+    emit_rank_probe(s, P, [&] { emit_loads(s, P.n_early, P.n_in); });
   } else if (probe) {
     const bool bloom = P.agg.bloom != nullptr && P.agg.kbits == nullptr;
     if (P.agg.kbits != nullptr)  // exact membership of dense build keys; all R words in flight first
@@ -553,6 +604,75 @@ std::string jit_source(const ScanProgram& P) {
   return s.str();
 }
 
+
+/// The warp-specialised probe kernel (sm_100a bulk copies + mbarriers). Warp 0 is the producer:
+/// one lane streams each 1024-row tile's EARLY columns (predicate + key, the columns every row
+/// needs) global -> shared memory with cp.async.bulk into an NS-stage ring, completing on the
+/// stage's `full` mbarrier. NG groups of 8 consumer warps take tiles round-robin (group g: tiles
+/// g, g + NG, ...), each warp 128 rows of the tile (R = 4 per lane): it copies its rows out of
+/// shared memory into registers, releases the stage (`empty` mbarrier, so the producer refills it
+/// while this warp works), then evaluates the predicate, probes the rank table (one L2-resident
+/// 16-byte record per key), gathers the LATE columns (the sums) from HBM for the surviving rows
+/// only and accumulates with atomics. The dense stream is decoupled from the dependent
+/// lookup/gather chain, so the HBM stream stays full while consumers wait on L2/HBM latency.
+std::string jit_source_staged(const ScanProgram& P) {
+  std::ostringstream s;
+  const StagedShape sh = staged_shape();
+  const int NG = sh.groups, NS = std::max(sh.stages, NG), NE = P.n_early, NIN = P.n_in, nregs = std::max(1, P.n_regs);
+  const int NT = 32 * (1 + 8 * NG);
+  s << "using namespace psg;\n#define R 4\n"
+    << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << sh.ctas
+    << ") psg_jit_scan(const __grid_constant__ ScanProgram P, "
+       "const Segment* __restrict__ segs, const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {\n"
+    << "  extern __shared__ __align__(128) unsigned char smem_raw[];\n"
+    << "  uint64_t* stg = reinterpret_cast<uint64_t*>(smem_raw);  // [" << NS << "][" << NE << "][1024]\n"
+    << "  __shared__ __align__(8) uint64_t full_bar[" << NS << "], empty_bar[" << NS << "];\n"
+    << "  __shared__ const uint64_t* s_col[" << NS << "][" << std::max(1, NIN) << "];\n"
+    << "  __shared__ int s_rows[" << NS << "];\n"
+    << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
+    << "  if (tid == 0) {\n    for (int i = 0; i < " << NS << "; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], 8); }\n"
+    << "    mbar_fence_init();\n  }\n  __syncthreads();\n"
+    << "  const uint64_t per_cta = (ntiles + gridDim.x - 1) / gridDim.x;\n"
+    << "  const uint64_t t_beg = blockIdx.x * per_cta;\n"
+    << "  const uint64_t t_end = t_beg + per_cta < ntiles ? t_beg + per_cta : ntiles;\n"
+    << "  if (warp == 0) {  // producer\n"
+    << "    if (lane == 0) {\n      const uint64_t pol_stream = l2_evict_first();\n"
+    << "      for (uint64_t k = 0; t_beg + k < t_end; ++k) {\n"
+    << "        const int st = static_cast<int>(k % " << NS << "); const uint32_t ph = static_cast<uint32_t>((k / " << NS << ") & 1);\n"
+    << "        if (k >= " << NS << ") mbar_wait(&empty_bar[st], ph ^ 1u);\n"
+    << "        const uint64_t t = t_beg + k;\n        const Segment* sg = segs + __ldg(tile_seg + t);\n"
+    << "        const uint64_t r0 = (t - sg->tile_begin) * 1024ULL;\n"
+    << "        const int rows = static_cast<int>(min(1024ULL, sg->rows - r0));\n";
+  for (int c = NE; c < NIN; ++c) s << "        s_col[st][" << c << "] = sg->col[" << c << "] + r0;\n";
+  s << "        s_rows[st] = rows;\n        const uint32_t bytes = (static_cast<uint32_t>(rows) * 8u + 15u) & ~15u;\n"
+    << "        mbar_arrive_expect_tx(&full_bar[st], " << NE << "u * bytes);\n";
+  for (int c = 0; c < NE; ++c)
+    s << "        bulk_g2s(stg + (st * " << NE << " + " << c << ") * 1024, sg->col[" << c << "] + r0, bytes, &full_bar[st], pol_stream);\n";
+  s << "      }\n    }\n    return;\n  }\n"
+    << "  const uint64_t pol_keep = l2_evict_last();\n"
+    << "  const int cw = (warp - 1) & 7, grp = (warp - 1) >> 3;\n  const int wrow = cw * (R * 32) + lane;\n"
+    << "  for (uint64_t k = grp; t_beg + k < t_end; k += " << NG << ") {\n"
+    << "    const int st = static_cast<int>(k % " << NS << "); const uint32_t ph = static_cast<uint32_t>((k / " << NS << ") & 1);\n"
+    << "    mbar_wait(&full_bar[st], ph);\n"
+    << "    const int nrows = s_rows[st] - cw * (R * 32);\n"
+    << "    uint32_t pass = 0;\n#pragma unroll\n    for (int r = 0; r < R; ++r) if (r * 32 + lane < nrows) pass |= 1u << r;\n";
+  for (int r = 0; r < nregs; ++r) s << "    uint64_t " << V(r) << "[R] = {};\n";
+  for (int c = 0; c < NE; ++c)
+    s << "#pragma unroll\n    for (int r = 0; r < R; ++r) if (pass & (1u << r)) " << V(c) << "[r] = stg[(st * " << NE << " + " << c
+      << ") * 1024 + wrow + r * 32];\n";
+  for (int c = NE; c < NIN; ++c) s << "    const uint64_t* lc" << c << " = s_col[st][" << c << "];\n";
+  s << "    __syncwarp();\n    if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage consumed: the producer may refill it\n";
+  emit_atoms(s, P);
+  emit_joins(s, P);
+  emit_rank_probe(s, P, [&] {
+    for (int c = NE; c < NIN; ++c)
+      s << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (pass & (1u << r)) " << V(c)
+        << "[r] = __ldcs(reinterpret_cast<const unsigned long long*>(lc" << c << " + wrow + r * 32));\n";
+  });
+  s << "  }\n}\n";
+  return s.str();
+}
+
 namespace {
 
 /// NVRTC: CUDA C++ -> sm_100a cubin. Returns false (with the log) on failure.
@@ -580,9 +700,10 @@ bool nvrtc_cubin(const std::string& body, std::string& cubin, std::string& log) 
   return true;
 }
 
-Compiled compile(const std::string& body, int device, int block) {
+Compiled compile(const std::string& body, int device, int block, int smem) {
   Compiled c;
   c.block = block;
+  c.smem = smem;
   const auto t0 = std::chrono::steady_clock::now();
   std::string cubin, log;
   if (const char* dir = std::getenv("PSG_JIT_DUMP")) {
@@ -606,8 +727,14 @@ Compiled compile(const std::string& body, int device, int block) {
     cudaGetLastError();
     return c;
   }
+  if (c.smem > 48 * 1024 &&
+      cudaFuncSetAttribute(reinterpret_cast<const void*>(c.kern), cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem) !=
+          cudaSuccess) {
+    cudaGetLastError();
+    return c;
+  }
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(c.kern), c.block, 0) !=
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, reinterpret_cast<const void*>(c.kern), c.block, c.smem) !=
           cudaSuccess ||
       per_sm < 1) {
     cudaGetLastError();
@@ -618,8 +745,8 @@ Compiled compile(const std::string& body, int device, int block) {
   if (std::getenv("PSG_TRACE")) {
     cudaFuncAttributes fa{};
     cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(c.kern));
-    std::fprintf(stderr, "[psg] jit kernel: %d regs, %zu B local, %d CTAs/SM (%zu B source)\n", fa.numRegs,
-                 static_cast<size_t>(fa.localSizeBytes), per_sm, body.size());
+    std::fprintf(stderr, "[psg] jit kernel: %d regs, %zu B local, %d CTAs/SM, %d threads, %d B dynamic smem (%zu B source)\n",
+                 fa.numRegs, static_cast<size_t>(fa.localSizeBytes), per_sm, c.block, c.smem, body.size());
   }
   g_compile_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   ++g_compiles;
@@ -641,7 +768,15 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
       std::lock_guard<std::mutex> lk(g_mu);
       auto key = std::make_pair(dev, body);
       auto it = g_cache.find(key);
-      if (it == g_cache.end()) it = g_cache.emplace(key, compile(body, dev, jit_block(P))).first;
+      if (it == g_cache.end()) {
+        int block = jit_block(P), smem = 0;
+        if (staged_probe(P)) {
+          const StagedShape sh = staged_shape();
+          block = 32 * (1 + 8 * sh.groups);
+          smem = std::max(sh.stages, sh.groups) * P.n_early * 1024 * 8;
+        }
+        it = g_cache.emplace(key, compile(body, dev, block, smem)).first;
+      }
       c = it->second;
     }
     if (c.ok) {
@@ -653,7 +788,7 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
                       &ntiles};
       count_external_launch();
       PSG_CUDA(cudaLaunchKernel(reinterpret_cast<const void*>(c.kern), dim3(static_cast<unsigned>(grid)), dim3(c.block),
-                                args, 0, stream));
+                                args, static_cast<size_t>(c.smem), stream));
       return;
     }
   }
@@ -736,6 +871,13 @@ int jit_selftest(std::string& log) {
       progs.push_back(q);
       q.agg.krank = reinterpret_cast<const uint32_t*>(16);  // rank-indexed table
       progs.push_back(q);
+      q.agg.krec = reinterpret_cast<const unsigned long long*>(16);  // + interleaved rank records
+      progs.push_back(q);
+      q.staged_ok = 1;  // the warp-specialised bulk-copy probe
+      q.agg.npacked = 1;
+      q.agg.packed_shift[0] = 30;
+      q.agg.packed_shift[1] = -1;
+      progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // consuming packed rows
       ScanProgram q = p;
@@ -782,12 +924,25 @@ int jit_selftest(std::string& log) {
     progs.push_back(p);
   }
   int failures = 0;
+  int seq = 0;
   for (auto& p : progs) {
     std::string cubin, l;
-    if (!nvrtc_cubin(jit_source(p), cubin, l) || cubin.empty()) {
+    const std::string src = jit_source(p);
+    if (!nvrtc_cubin(src, cubin, l) || cubin.empty()) {
       ++failures;
       log += "sink " + std::to_string(p.sink) + ": " + l + "\n";
+    } else if (const char* dir = std::getenv("PSG_JIT_DUMP")) {  // cubins + sources for cuobjdump -sass
+      const std::string base = std::string(dir) + "/selftest_" + std::to_string(seq) + (staged_probe(p) ? "_staged" : "");
+      if (FILE* f = std::fopen((base + ".cubin").c_str(), "wb")) {
+        std::fwrite(cubin.data(), 1, cubin.size(), f);
+        std::fclose(f);
+      }
+      if (FILE* f = std::fopen((base + ".cu").c_str(), "w")) {
+        std::fwrite(src.data(), 1, src.size(), f);
+        std::fclose(f);
+      }
     }
+    ++seq;
   }
   return failures;
 }

@@ -679,6 +679,25 @@ void launch_gather64(const uint64_t* const* in_cols, int ncols, const uint64_t* 
   k_gather64<<<grid_for(n, 256), 256, 0, S(stream)>>>(pc, ncols, idx, n, oc);
 }
 
+/// Interleaved rank records: krec[2w] = 64-bit bitmap word w, krec[2w+1] = krank[w] (one 16-byte
+/// load per probe instead of two 4/8-byte loads from two arrays).
+__global__ void k_krec_build(const unsigned long long* __restrict__ bits, const uint32_t* __restrict__ krank, uint64_t n,
+                             unsigned long long* __restrict__ krec) {
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < n;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    ulonglong2 v;
+    v.x = bits[w];
+    v.y = krank[w];
+    reinterpret_cast<ulonglong2*>(krec)[w] = v;
+  }
+}
+void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, uint64_t n, unsigned long long* krec,
+                       void* stream) {
+  if (n == 0) return;
+  count_launch();
+  k_krec_build<<<grid_for(n, 256), 256, 0, S(stream)>>>(bits, krank, n, krec);
+}
+
 /// Destination histogram of n keys (partition_of, hashing.hpp:35-37): one shared atomic per
 /// (warp, destination) from __match_any_sync groups, one global atomic per (block, destination).
 __global__ void k_part_hist(const uint64_t* __restrict__ keys, uint64_t n, int nparts, unsigned long long* counts) {

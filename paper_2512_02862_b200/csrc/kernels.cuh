@@ -80,6 +80,8 @@ size_t sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_
                       int end_bit, void* tmp, size_t tmp_bytes, void* stream);
 void launch_gather64(const uint64_t* const* in_cols, int ncols, const uint64_t* idx, uint64_t n, uint64_t* const* out,
                      void* stream);
+void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, uint64_t n, unsigned long long* krec,
+                       void* stream);
 void launch_part_hist(const uint64_t* keys, uint64_t n, int nparts, unsigned long long* counts, void* stream);
 void launch_minmax_i64(const uint64_t* keys, uint64_t n, long long* out, void* stream);
 void launch_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uint32_t* bitmap, unsigned int* dup, void* stream);
