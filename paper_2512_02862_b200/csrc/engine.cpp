@@ -1789,20 +1789,29 @@ ResultRows Execution::run(bool want_rows) {
   } else if (agg_) {
     pt.mark("  pre agg alloc", ctx_.compute);
     // Dense build keys at one GPU: an exact membership bitmap replaces the Bloom filter (no false
-    // positives, 1 bit per key of the range; o_orderkey at SF100: 19 MB vs 32 MB). PSG_KBITS=0: off.
-    // PSG_KBITS: unset/1 = one GPU only, 2 = also the global bitmap at N > 1 (parity-green, but
-    // measured slower at N=2: 7.37 vs 6.37 ms - the partitioning scan slows more than the exact
-    // filter saves), 0 = off.
+    // positives, 1 bit per key of the range; o_orderkey at SF100: 19 MB vs 32 MB). At N > 1 every
+    // rank sets its own bitmap over the ALL-REDUCED key range from the build keys it owns; the OR
+    // of the rank bitmaps (a SUM all-reduce: owners are disjoint) is the exact semi-join screen of
+    // the probe side, and a rank's own bitmap indexes its rank-indexed table.
+    // PSG_KBITS: 1 (default) = exact bitmaps at every N, 2 = at N > 1 also when the rank table is
+    // off (hashed table + exact screen), 0 = Bloom filters only.
     static const int kbits_mode = [] {
       const char* e = std::getenv("PSG_KBITS");
       return e ? std::atoi(e) : 1;
     }();
     const bool kbits_env = kbits_mode >= 1;
+    // Rank-indexed table (grouped, unique dense build keys): the key bitmap is set from the build
+    // keys first (with a duplicate check) and its 64-bit words' popcount prefix turns a key into
+    // its rank = its slot; the table is then exactly one slot per build key in key order, written
+    // by plain stores. PSG_RANK_TABLE=0: the hashed table.
+    static const bool rank_env = [] {
+      const char* e = std::getenv("PSG_RANK_TABLE");
+      return !(e && e[0] == '0');
+    }();
     long long krange_lo = 0;
     uint64_t krange = 0;
-    if (nr > 1 && semi && kbits_mode >= 2) {
-      // N > 1: one GLOBAL bitmap of all build keys over the all-reduced key range; every key's
-      // bit is set by its owner only, so a SUM all-reduce of the rank bitmaps is their OR
+    const bool rank_ok = grouped_ && rank_env && jit_available() && !p2p;
+    if (nr > 1 && semi && kbits_env && (rank_ok || kbits_mode >= 2)) {
       DevBuf mm(ctx_.pool, 16, ctx_.compute);
       const long long init[2] = {LLONG_MAX, LLONG_MIN};
       PSG_CUDA(cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, ctx_.compute));
@@ -1817,6 +1826,8 @@ ResultRows Execution::run(bool want_rows) {
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
       const long long lo = ~enc[0], hi = enc[1];
       const uint64_t range = hi >= lo ? static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo) + 1 : 0;
+      // every rank decides from all-reduced numbers only (same choice everywhere); a bitmap of
+      // <= 32 x the largest Bloom filter (the Bloom would be ~16 bits per key)
       if (range != 0 && range <= (1ULL << 36) && range / 32 <= static_cast<uint64_t>(nr) * bloom_words) {
         krange_lo = lo;
         krange = range;
@@ -1837,24 +1848,16 @@ ResultRows Execution::run(bool want_rows) {
         bloom_words = 0;
       }
     }
-    // Rank-indexed table (one GPU, grouped, unique dense build keys): the key bitmap is set from
-    // the build keys first (with a duplicate check) and its 64-bit words' popcount prefix turns a
-    // key into its rank = its slot; the table is then exactly one slot per build key in key
-    // order, written by plain stores. PSG_RANK_TABLE=0: the hashed table.
-    static const bool rank_env = [] {
-      const char* e = std::getenv("PSG_RANK_TABLE");
-      return !(e && e[0] == '0');
-    }();
     bool rank_mode = false;
     const uint64_t kwords64 = (krange + 63) / 64;
-    if (nr == 1 && krange && grouped_ && rank_env && jit_available() && krange_lo != LLONG_MIN && !p2p &&
-        kwords64 < (1ULL << 32) && bmat.rows < (1ULL << 32)) {
+    if (krange && rank_ok && krange_lo != LLONG_MIN && kwords64 < (1ULL << 32) && build_rows > 0 &&
+        build_rows < (1ULL << 32)) {
       agg_kbits_ = DevBuf(ctx_.pool, kwords64 * 8, ctx_.compute);
       DevBuf dup(ctx_.pool, 4, ctx_.compute);
       PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, kwords64 * 8, ctx_.compute));
       PSG_CUDA(cudaMemsetAsync(dup.p, 0, 4, ctx_.compute));
-      launch_bitmap_set(bmat.cols[0].as<uint64_t>(), bmat.rows, krange_lo, agg_kbits_.as<uint32_t>(),
-                        dup.as<unsigned int>(), ctx_.compute);
+      for (const auto& sg : bsegs)
+        launch_bitmap_set(sg.col[0], sg.rows, krange_lo, agg_kbits_.as<uint32_t>(), dup.as<unsigned int>(), ctx_.compute);
       unsigned int d = 1;
       PSG_CUDA(cudaMemcpyAsync(&d, dup.p, 4, cudaMemcpyDeviceToHost, ctx_.compute));
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
@@ -1871,10 +1874,10 @@ ResultRows Execution::run(bool want_rows) {
         rank_mode = true;
       }
     }
-    build_agg_table(build_rows, bloom_words, rank_mode ? bmat.rows : 0);
+    build_agg_table(build_rows, bloom_words, rank_mode ? build_rows : 0);
     st_.agg_table = rank_mode ? 4 : (krange ? 3 : (bloom_words ? 2 : 1));
     if (krange) {
-      if (!rank_mode) {
+      if (!rank_mode) {  // the insert below sets the bits
         const uint64_t words = (krange + 31) / 32;
         agg_kbits_ = DevBuf(ctx_.pool, words * 4, ctx_.compute);
         PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, words * 4, ctx_.compute));
@@ -1904,9 +1907,15 @@ ResultRows Execution::run(bool want_rows) {
       return !(e && std::string(e) == "0");
     }();
     if (rank_mode) {
-      RankSums rs{};
-      for (int b = 0; b < p.n_sum; ++b) rs.col[b] = bmat.cols[1 + b].as<uint64_t>();
-      launch_rank_build(aggt_, bmat.cols[0].as<uint64_t>(), rs, bmat.rows, ctx_.compute);
+      // hot slots from the bitmap (slot order) once, cold slots (build sums) per build segment
+      bool first = true;
+      for (const auto& sg : bsegs) {
+        RankSums rs{};
+        for (int b = 0; b < p.n_sum; ++b) rs.col[b] = sg.col[1 + b];
+        launch_rank_build(aggt_, sg.col[0], rs, sg.rows, first, ctx_.compute);
+        first = false;
+      }
+      if (first) launch_rank_build(aggt_, nullptr, RankSums{}, 0, true, ctx_.compute);
     } else if (semi && !krange && aggt_.bloom && overlap_env) {
       for (const auto& sg : bsegs) launch_bloom_keys(sg.col[0], sg.rows, aggt_.bloom, aggt_.bloom_shift, ctx_.compute);
       PSG_CUDA(cudaEventRecord(build_fork_.get(), ctx_.compute));
@@ -1922,9 +1931,10 @@ ResultRows Execution::run(bool want_rows) {
     }
     if (build_pending_) {
       // (the Bloom filters were all-gathered above)
-    } else if (semi && krange) {  // disjoint bits: SUM == OR
-      PSG_NCCL(ncclAllReduce(agg_kbits_.p, agg_kbits_.p, (krange + 31) / 32, ncclUint32, ncclSum, ctx_.nccl,
-                             ctx_.compute));
+    } else if (semi && krange) {  // disjoint bits: SUM == OR; out of place (the rank keeps its own)
+      const uint64_t words = (krange + 31) / 32;
+      semi_all = DevBuf(ctx_.pool, words * 4, ctx_.compute);
+      PSG_NCCL(ncclAllReduce(agg_kbits_.p, semi_all.p, words, ncclUint32, ncclSum, ctx_.nccl, ctx_.compute));
     } else if (semi) {
       semi_all = DevBuf(ctx_.pool, static_cast<size_t>(nr) * bloom_words * 4, ctx_.compute);
       PSG_NCCL(ncclAllGather(agg_bloom_.p, semi_all.p, bloom_words * 4, ncclUint8, ctx_.nccl, ctx_.compute));
@@ -1999,7 +2009,7 @@ ResultRows Execution::run(bool want_rows) {
   std::vector<int> p_out;
   for (int w : pneed) p_out.push_back(pm.reg_of.at(psrc_.stage_refs.back()[w]));
   if (semi && aggt_.kbits) {
-    pp.semi_kbits = aggt_.kbits;
+    pp.semi_kbits = semi_all.as<uint32_t>();
     pp.semi_kmin = aggt_.kmin;
     pp.semi_krange = aggt_.krange;
     pp.semi_key_reg = p_out[0];
@@ -2020,7 +2030,8 @@ ResultRows Execution::run(bool want_rows) {
       ScanProgram p = batch_program(ncols);
       p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
       p.agg = aggt_;
-      if (semi) p.agg.bloom = nullptr, p.agg.kbits = nullptr;  // received rows already passed the filter
+      // received rows already passed the screen (the rank table still needs its bitmap: slots)
+      if (semi && !aggt_.krank) p.agg.bloom = nullptr, p.agg.kbits = nullptr;
       p.key_reg = 0;
       p.n_sum = static_cast<int>(probe_sum_wire.size());
       for (int s = 0; s < p.n_sum; ++s) p.sum_reg[s] = 1 + s;
@@ -2195,7 +2206,8 @@ ResultRows Execution::run(bool want_rows) {
       const char* e = std::getenv("PSG_SELF_PROBE");
       return !(e && std::string(e) == "0");
     }();
-    if (nr > 1 && agg_ && grouped_ && jit_available() && self_probe_env && pack.pack_n == 0 && !pdup) {
+    if (nr > 1 && agg_ && grouped_ && jit_available() && self_probe_env && pack.pack_n == 0 && !pdup &&
+        !aggt_.krank) {
       join_build();  // the scan itself probes this rank's table
       pp.self_probe = 1;
       pp.self_rank = ctx_.rank;

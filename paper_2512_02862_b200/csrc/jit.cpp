@@ -727,7 +727,7 @@ Compiled compile(const std::string& body, int device, int block, int smem) {
     cudaGetLastError();
     return c;
   }
-  if (c.smem > 48 * 1024 &&
+  if (c.smem > 0 &&  // (static + dynamic > 48 KB needs the opt-in even when dynamic alone does not)
       cudaFuncSetAttribute(reinterpret_cast<const void*>(c.kern), cudaFuncAttributeMaxDynamicSharedMemorySize, c.smem) !=
           cudaSuccess) {
     cudaGetLastError();

@@ -785,10 +785,6 @@ __global__ void k_rank_hot(AggTableDev t, uint64_t nwords) {
 template <bool kHot>
 __global__ void k_rank_build(AggTableDev t, const uint64_t* __restrict__ keys, RankSums bs, uint64_t n) {
   const uint64_t tid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (tid == 0) {  // the spill slot (slot n) is never occupied
-    for (int k = 0; k < t.hw; ++k) t.hot[n * t.hw + k] = 0;
-    for (int k = 0; k < t.cw; ++k) t.cold[n * t.cw + k] = 0;
-  }
   for (uint64_t i = tid; i < n; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t key = keys[i];
     uint64_t cv[2 * kMaxSums + 2];
@@ -821,23 +817,38 @@ __global__ void k_rank_build(AggTableDev t, const uint64_t* __restrict__ keys, R
   }
 }
 
-void launch_rank_build(const AggTableDev& t, const uint64_t* keys, const RankSums& bs, uint64_t n, void* stream) {
-  count_launch();
+void launch_rank_build(const AggTableDev& t, const uint64_t* keys, const RankSums& bs, uint64_t n, bool first,
+                       void* stream) {
   // The hot slots are written in slot order from the key bitmap (k_rank_hot, sequential stores)
   // and the row-ordered build pass writes only the cold slots: the build rows arrive in scan
   // order, not key order, so hot-slot stores by row were scattered (SF100 N=1: one 0.60 ms pass
-  // -> 0.09 + 0.30 ms). PSG_RANK_HOT_SEQ=0: both from the row-ordered pass.
+  // -> 0.09 + 0.30 ms). Without build-side sums the cold slots hold nothing but the multiplicity
+  // m - 1 = 0 of unique keys, which nothing reads (emit reads cold only for duplicates and the
+  // spill slot), so that pass is skipped (Q3: -0.25 ms). PSG_RANK_HOT_SEQ=0: one row-ordered pass
+  // for both. `first`: this call also writes the hot slots and clears the (never occupied) spill
+  // slot; later calls (more build segments at N > 1) only their rows' cold slots.
   static const bool hot_seq = [] {
     const char* e = std::getenv("PSG_RANK_HOT_SEQ");
     return !(e && e[0] == '0');
   }();
+  const uint64_t spill = t.mask + 1;
+  if (first) {
+    cudaMemsetAsync(t.hot + spill * t.hw, 0, t.hw * sizeof(uint64_t), S(stream));
+    cudaMemsetAsync(t.cold + spill * t.cw, 0, t.cw * sizeof(uint64_t), S(stream));
+  }
   if (hot_seq && t.hw % 4 == 0) {
-    const uint64_t nw = (t.krange + 63) / 64;
+    if (first) {
+      const uint64_t nw = (t.krange + 63) / 64;
+      count_launch();
+      k_rank_hot<<<grid_for(std::max<uint64_t>(nw, 1), 256), 256, 0, S(stream)>>>(t, nw);
+    }
+    if (t.nbs > 0 && n > 0) {
+      count_launch();
+      k_rank_build<false><<<grid_for(n, 256), 256, 0, S(stream)>>>(t, keys, bs, n);
+    }
+  } else if (n > 0) {
     count_launch();
-    k_rank_hot<<<grid_for(std::max<uint64_t>(nw, 1), 256), 256, 0, S(stream)>>>(t, nw);
-    k_rank_build<false><<<grid_for(std::max<uint64_t>(n, 1), 256), 256, 0, S(stream)>>>(t, keys, bs, n);
-  } else {
-    k_rank_build<true><<<grid_for(std::max<uint64_t>(n, 1), 256), 256, 0, S(stream)>>>(t, keys, bs, n);
+    k_rank_build<true><<<grid_for(n, 256), 256, 0, S(stream)>>>(t, keys, bs, n);
   }
 }
 

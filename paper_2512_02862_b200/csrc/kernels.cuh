@@ -88,7 +88,8 @@ void launch_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uint32_t*
 struct RankSums {
   const uint64_t* col[kMaxSums];
 };
-void launch_rank_build(const AggTableDev& t, const uint64_t* keys, const RankSums& bs, uint64_t n, void* stream);
+void launch_rank_build(const AggTableDev& t, const uint64_t* keys, const RankSums& bs, uint64_t n, bool first,
+                       void* stream);
 void launch_bloom_keys(const uint64_t* keys, uint64_t n, uint32_t* bloom, int shift, void* stream);
 void launch_iota_u32(uint32_t* out, uint64_t n, void* stream);
 void launch_rows_from_cols(const uint64_t* const* cols, int ncols, uint64_t n, uint64_t* out_rows, void* stream);
