@@ -110,6 +110,20 @@ typedef struct psg_stats {
 int psg_abi_version(void);
 const char* psg_last_error(void);
 
+/* Host-only shuffle protocol (the functions every rank evaluates on all-gathered / all-reduced
+ * inputs; run_waves size exchange, pipeline.cpp:690-722):
+ *  psg_shuffle_plan: from the n x n count matrix [src][dst] (row-major), rank me's send offsets
+ *    into its destination-major slab and receive offsets per source (rows).
+ *  psg_pack_plan: one-word row layout from all-reduced per-column bounds (column 0 = key); fits=0
+ *    when the fields do not fit in 64 bits.
+ *  psg_partition_of: partition_of(key) = ((key * 0x9E3779B97F4A7C15) >> 13) % nparts
+ *    (hashing.hpp:35-37), the destination of a shuffled row. */
+int psg_shuffle_plan(const uint64_t* matrix, int n, int me, uint64_t* send_off, uint64_t* recv_off,
+                     uint64_t* send_rows, uint64_t* recv_rows);
+int psg_pack_plan(const int64_t* lo, const int64_t* hi, int ncols, int64_t* min, int* shift, uint64_t* mask,
+                  int* fits);
+int psg_partition_of(const int64_t* keys, uint64_t n, uint32_t nparts, uint32_t* out);
+
 /* Host-only: parses + validates a plan like QueryPlan::from_json_text (pipeline.cpp:108-156,
  * validate :178-196) for node `node` of `nodes` and writes the resolved scans as JSON
  * {"scans":[{"table","replicated","paths":[...]}],"shuffle":id|null} into out (NUL-terminated,

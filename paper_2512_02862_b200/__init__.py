@@ -36,7 +36,8 @@ EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_uniq
            "psg_hashtable_shape", "psg_hashtable_row", "psg_hashtable_lookup", "psg_hashtable_probe", "psg_hashtable_free",
            "psg_concat", "psg_codec_decompress", "psg_psto_write",
            "psg_psto_inspect", "psg_gen_tpch", "psg_gen_synthetic", "psg_jit_selftest", "psg_tmin",
-           "psg_plan_resolve", "psg_result_checksum", "psg_ingest_probe"]
+           "psg_plan_resolve", "psg_result_checksum", "psg_ingest_probe",
+           "psg_shuffle_plan", "psg_pack_plan", "psg_partition_of"]
 
 
 class PsgError(RuntimeError):
@@ -117,6 +118,9 @@ def lib():
             "psg_tmin": ([u64, ctypes.c_double, u64, ctypes.c_double], ctypes.c_double),
             "psg_jit_selftest": ([ctypes.c_char_p, ctypes.c_size_t], i32),
             "psg_ingest_probe": ([vp, c, c, P(Stats)], i32),
+            "psg_shuffle_plan": ([P(u64), i32, i32, P(u64), P(u64), P(u64), P(u64)], i32),
+            "psg_pack_plan": ([P(ctypes.c_int64), P(ctypes.c_int64), i32, P(ctypes.c_int64), P(i32), P(u64), P(i32)], i32),
+            "psg_partition_of": ([P(ctypes.c_int64), u64, ctypes.c_uint32, P(ctypes.c_uint32)], i32),
             "psg_result_checksum": ([vp, P(u64), P(u64), ctypes.c_uint32], i32),
             "psg_plan_resolve": ([c, c, i32, i32, ctypes.c_char_p, ctypes.c_size_t, P(ctypes.c_size_t)], i32),
         }
@@ -131,6 +135,42 @@ def lib():
 def _check(rc):
     if rc != 0:
         raise PsgError(rc, lib().psg_last_error().decode(errors="replace"))
+
+
+def shuffle_plan(matrix, me):
+    """(send_off, recv_off, send_rows, recv_rows) of rank `me` from the all-gathered n x n count
+    matrix [src][dst] - the engine's own host function (csrc/shuffle_plan.cpp)."""
+    m = np.ascontiguousarray(matrix, dtype=np.uint64)
+    n = m.shape[0]
+    so, ro = np.zeros(n, np.uint64), np.zeros(n, np.uint64)
+    sr, rr = ctypes.c_uint64(), ctypes.c_uint64()
+    P = ctypes.POINTER(ctypes.c_uint64)
+    _check(lib().psg_shuffle_plan(m.ctypes.data_as(P), n, me, so.ctypes.data_as(P), ro.ctypes.data_as(P),
+                                  ctypes.byref(sr), ctypes.byref(rr)))
+    return so, ro, sr.value, rr.value
+
+
+def pack_plan(lo, hi):
+    """One-word shuffle-row layout {fits, min, shift, mask} from all-reduced bounds."""
+    lo = np.ascontiguousarray(lo, dtype=np.int64)
+    hi = np.ascontiguousarray(hi, dtype=np.int64)
+    k = len(lo)
+    mn, sh, mk = np.zeros(k, np.int64), np.zeros(k, np.int32), np.zeros(k, np.uint64)
+    fits = ctypes.c_int()
+    I64 = ctypes.POINTER(ctypes.c_int64)
+    _check(lib().psg_pack_plan(lo.ctypes.data_as(I64), hi.ctypes.data_as(I64), k, mn.ctypes.data_as(I64),
+                               sh.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                               mk.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ctypes.byref(fits)))
+    return {"fits": bool(fits.value), "min": mn, "shift": sh, "mask": mk}
+
+
+def partition_of(keys, nparts):
+    """Destination rank of each key (hashing.hpp:35-37), host evaluation."""
+    k = np.ascontiguousarray(keys, dtype=np.int64)
+    out = np.zeros(len(k), np.uint32)
+    _check(lib().psg_partition_of(k.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), len(k), nparts,
+                                  out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))))
+    return out
 
 
 def resolve_plan(plan, data_root, node=0, nodes=1):

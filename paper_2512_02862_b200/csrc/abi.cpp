@@ -10,6 +10,7 @@
 
 #include "engine.hpp"
 #include "jit.hpp"
+#include "shuffle_plan.hpp"
 
 using namespace psg;
 
@@ -105,6 +106,41 @@ Predicate to_pred(const psg_atom* atoms, uint32_t n) {
 extern "C" {
 
 int psg_abi_version(void) { return PSG_ABI_VERSION; }
+
+int psg_shuffle_plan(const uint64_t* matrix, int n, int me, uint64_t* send_off, uint64_t* recv_off,
+                     uint64_t* send_rows, uint64_t* recv_rows) {
+  return guarded([&] {
+    if (!matrix) throw InvalidInput("null count matrix");
+    const ExchangePlan x = plan_exchange(matrix, n, me);
+    for (int p = 0; p < n; ++p) {
+      if (send_off) send_off[p] = x.send_off[p];
+      if (recv_off) recv_off[p] = x.recv_off[p];
+    }
+    if (send_rows) *send_rows = x.send_rows;
+    if (recv_rows) *recv_rows = x.recv_rows;
+  });
+}
+
+int psg_pack_plan(const int64_t* lo, const int64_t* hi, int ncols, int64_t* min, int* shift, uint64_t* mask, int* fits) {
+  return guarded([&] {
+    if (!lo || !hi || ncols < 1 || ncols > kMaxOut) throw InvalidInput("pack plan: bad columns");
+    const PackLayout L = plan_pack(lo, hi, ncols);
+    for (int k = 0; k < ncols; ++k) {
+      if (min) min[k] = L.min[k];
+      if (shift) shift[k] = L.shift[k];
+      if (mask) mask[k] = L.mask[k];
+    }
+    if (fits) *fits = L.fits ? 1 : 0;
+  });
+}
+
+int psg_partition_of(const int64_t* keys, uint64_t n, uint32_t nparts, uint32_t* out) {
+  return guarded([&] {
+    if ((!keys || !out) && n) throw InvalidInput("null argument");
+    if (nparts == 0) throw InvalidInput("nparts must be > 0");
+    for (uint64_t i = 0; i < n; ++i) out[i] = partition_of_host(static_cast<uint64_t>(keys[i]), nparts);
+  });
+}
 
 int psg_plan_resolve(const char* plan_json, const char* data_root, int node, int nodes, char* out, size_t cap,
                      size_t* needed) {

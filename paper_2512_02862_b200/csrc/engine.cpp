@@ -28,6 +28,7 @@
 
 #include "engine.hpp"
 #include "jit.hpp"
+#include "shuffle_plan.hpp"
 
 #define PSG_NCCL(call)                                                                              \
   do {                                                                                              \
@@ -1404,8 +1405,8 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
   PSG_CUDA(cudaStreamSynchronize(st));  // the one data-dependent host sync per wave
   PhaseTimer xt;
   const int me = ctx_.rank;
-  uint64_t nrows = 0;
-  for (int d = 0; d < n; ++d) nrows += m[static_cast<size_t>(me) * n + d];
+  const ExchangePlan xp = plan_exchange(m.data(), n, me);
+  const uint64_t nrows = xp.send_rows;
   DevBuf send(ctx_.pool, std::max<uint64_t>(nrows, 1) * ncols * 8, st);
   if (have_data && nrows) {
     std::vector<const uint64_t*> in;
@@ -1414,17 +1415,15 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
                         part_counts.as<unsigned long long>(), cursor.as<unsigned long long>(), send.as<uint64_t>(),
                         st, kf);
   }
-  uint64_t rtotal = 0;
-  for (int s = 0; s < n; ++s) rtotal += m[static_cast<size_t>(s) * n + me];
+  const uint64_t rtotal = xp.recv_rows;
   rcv.buf = DevBuf(ctx_.pool, std::max<uint64_t>(rtotal, 1) * ncols * 8 + 16, st);
   rcv.rows = rtotal;
   xfer_ev_.push_back(std::make_unique<TimedPair>());
   PSG_CUDA(cudaEventRecord(xfer_ev_.back()->a, st));
   PSG_NCCL(ncclGroupStart());
-  uint64_t soff = 0, roff = 0;
   for (int p = 0; p < n; ++p) {
-    const uint64_t sc = m[static_cast<size_t>(me) * n + p];
-    const uint64_t rc = m[static_cast<size_t>(p) * n + me];
+    const uint64_t sc = xp.send_cnt[p], rc = xp.recv_cnt[p];
+    const uint64_t soff = xp.send_off[p], roff = xp.recv_off[p];
     if (sc) PSG_NCCL(ncclSend(send.as<uint64_t>() + soff * ncols, sc * ncols, ncclUint64, p, ctx_.nccl, st));
     if (rc) PSG_NCCL(ncclRecv(rcv.buf.as<uint64_t>() + roff * ncols, rc * ncols, ncclUint64, p, ctx_.nccl, st));
     if (rc) {
@@ -1436,8 +1435,6 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
       if (p != me) st_.bytes_received += rc * ncols * 8;
     }
     if (p != me) st_.bytes_sent += sc * ncols * 8;
-    soff += sc;
-    roff += rc;
   }
   PSG_NCCL(ncclGroupEnd());
   PSG_CUDA(cudaEventRecord(xfer_ev_.back()->b, st));
@@ -2169,22 +2166,14 @@ ResultRows Execution::run(bool want_rows) {
       PSG_NCCL(ncclAllReduce(red.p, red.p, 2 * np, ncclInt64, ncclMax, ctx_.nccl, ctx_.compute));
       PSG_CUDA(cudaMemcpyAsync(lohi.data(), red.p, 2 * np * 8, cudaMemcpyDeviceToHost, ctx_.compute));
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
-      int bits = 0;
-      bool fits = true;
-      for (size_t k = 0; k < np && fits; ++k) {
-        const long long lo = ~lohi[k], hi = lohi[np + k];
-        if (hi < lo) {  // no rows anywhere
-          pack.pack_min[k] = 0, pack.pack_mask[k] = 0, pack.pack_shift[k] = bits;
-          if (k == 0) fits = false;
-          continue;
-        }
-        const uint64_t span = static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo);
-        const int b = span ? 64 - __builtin_clzll(span) : 0;
-        if (bits + b > 64 || (k == 0 && b == 0)) fits = false;  // the key must be a real field
-        pack.pack_min[k] = lo;
-        pack.pack_shift[k] = bits;
-        pack.pack_mask[k] = b == 64 ? ~0ULL : ((1ULL << b) - 1);
-        bits += b;
+      std::vector<int64_t> plo(np), phi(np);
+      for (size_t k = 0; k < np; ++k) plo[k] = ~lohi[k], phi[k] = lohi[np + k];
+      const PackLayout L = plan_pack(plo.data(), phi.data(), static_cast<int>(np));
+      const bool fits = L.fits;
+      for (size_t k = 0; k < np; ++k) {
+        pack.pack_min[k] = L.min[k];
+        pack.pack_shift[k] = L.shift[k];
+        pack.pack_mask[k] = L.mask[k];
       }
       if (fits && np > 1) {
         pack.pack_n = static_cast<int>(np);
