@@ -24,6 +24,8 @@ constexpr int kMaxOut = 16;
 constexpr int kMaxSums = 8;
 constexpr int kMaxParts = 64;
 constexpr int kBlock = 256;
+constexpr int kBucketSlots = 4096;  // rank-table slots per aggregation bucket (shared-memory slice)
+constexpr int kBucketBits = 12;
 constexpr int kRowsPerThread = 4;
 constexpr uint64_t kSlotMul = 0xD6E8FEB86659FD93ULL;   // table slot = (k * kSlotMul) >> shift
 constexpr uint64_t kBloomMul = 0xA24BAED4963EE407ULL;  // bloom word/bits from (k * kBloomMul)
@@ -193,6 +195,17 @@ struct ScanProgram {
   // mask/shift/hw/cw come from `agg`, only the base pointers differ per rank.
   const AggPeer* peers;
   int32_t remote;
+  // Bucketed aggregation (rank-indexed table, SINK_PROBE): a surviving row is appended as ONE word
+  // to the bucket of its slot (slot >> kBucketBits): slot & (kBucketSlots - 1) in the low bits,
+  // then every probe sum k as (v - bkt_min[k]) & bkt_mask[k] at bkt_shift[k]. k_bucket_agg then
+  // folds each bucket in shared memory and adds it to the hot slots once, so the table's random
+  // read-modify-writes never go to HBM. A full bucket falls back to the direct atomic update.
+  uint64_t* bkt;             // [nbuckets][bkt_cap]
+  unsigned int* bkt_fill;    // [nbuckets] appended entries (may exceed bkt_cap: overflowed)
+  uint32_t bkt_cap;
+  int32_t bkt_shift[kMaxSums];
+  uint64_t bkt_mask[kMaxSums];
+  int64_t bkt_min[kMaxSums];
   // the engine guarantees 16-byte aligned column chunks and readable padding past each chunk's
   // end (PSTO batches, staged images): the query compiler may then stream the early columns into
   // shared memory with bulk copies (the warp-specialised probe, jit.cpp)

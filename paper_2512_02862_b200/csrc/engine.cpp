@@ -519,6 +519,8 @@ class Execution {
   std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
   // agg table
   DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, agg_krank_, agg_krec_, global_acc_, barrier_word_;
+  DevBuf bkt_, bkt_fill_;  // bucketed aggregation (rank table, one GPU)
+  bool setup_buckets(ScanProgram& p, BucketDev& bd, uint64_t& nbuckets);
   AggTableDev aggt_{};
   // the build insert running on ctx_.comm concurrently with the probe side (N > 1 Bloom path)
   struct Event {
@@ -1266,6 +1268,59 @@ void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words, uint6
     aggt_.bloom_shift = shift_of(bloom_words);
   }
   if (!rank_slots) launch_agg_init(aggt_, agg_cap_, ctx_.compute);
+}
+
+/// Bucketed aggregation for the one-GPU rank-indexed table (ScanProgram::bkt, k_bucket_agg):
+/// possible when every probe-side sum is an int column of the probe scan whose zone-map span fits,
+/// with the slot's low bits, in one 64-bit word. Bucket capacity: the expected survivors (probe
+/// rows x the build keys' share of the key range) / buckets x 1.5; overflow is applied directly.
+/// PSG_BUCKETS=0: off.
+bool Execution::setup_buckets(ScanProgram& p, BucketDev& bd, uint64_t& nbuckets) {
+  static const bool env = [] {
+    const char* e = std::getenv("PSG_BUCKETS");
+    return !(e && e[0] == '0');
+  }();
+  const int np = static_cast<int>(probe_sum_wire.size());
+  if (!env || !jit_available() || np > 3 || aggt_.krange == 0 || agg_cap_ == 0) return false;
+  int shift = kBucketBits;
+  uint64_t probe_rows = 0;
+  for (const auto& path : psrc_.scan->paths) probe_rows += ctx_.footers.get(path)->total_rows();
+  for (int k = 0; k < np; ++k) {
+    const ColRef ref = psrc_.stage_refs.back()[probe_sum_wire[k]];
+    if (ref.join >= 0 || psrc_.wire.fields[probe_sum_wire[k]].type != LType::Int64) return false;
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    const int fcol = psrc_.proj.file_idx[ref.idx];
+    for (const auto& path : psrc_.scan->paths)
+      for (const auto& g : ctx_.footers.get(path)->groups)
+        if (g.rows) {
+          lo = std::min(lo, static_cast<long long>(g.cols[fcol].min_raw));
+          hi = std::max(hi, static_cast<long long>(g.cols[fcol].max_raw));
+        }
+    if (hi < lo) lo = hi = 0;
+    const uint64_t span = static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo);
+    const int w = span ? 64 - __builtin_clzll(span) : 0;
+    if (shift + w > 64) return false;
+    p.bkt_shift[k] = bd.shift[k] = shift;
+    p.bkt_mask[k] = bd.mask[k] = w == 64 ? ~0ULL : ((1ULL << w) - 1);
+    p.bkt_min[k] = bd.min[k] = lo;
+    bd.word[k] = 1 + k;  // hot word 2 + k
+    shift += w;
+  }
+  nbuckets = (agg_cap_ + kBucketSlots - 1) / kBucketSlots;
+  const double share = std::min(1.0, static_cast<double>(agg_cap_) / static_cast<double>(aggt_.krange));
+  const uint64_t cap = static_cast<uint64_t>(1.5 * static_cast<double>(probe_rows) * share / static_cast<double>(nbuckets)) + 1024;
+  if (cap >= (1ULL << 31)) return false;
+  bkt_ = DevBuf(ctx_.pool, nbuckets * cap * 8, ctx_.compute);
+  bkt_fill_ = DevBuf(ctx_.pool, nbuckets * 4, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(bkt_fill_.p, 0, nbuckets * 4, ctx_.compute));
+  p.bkt = bkt_.as<uint64_t>();
+  p.bkt_fill = bkt_fill_.as<unsigned int>();
+  p.bkt_cap = static_cast<uint32_t>(cap);
+  bd.bkt = p.bkt;
+  bd.fill = p.bkt_fill;
+  bd.cap = p.bkt_cap;
+  bd.nacc = 1 + np;
+  return true;
 }
 
 /// Bit-packed accumulators: the footer zone maps bound every int probe-side sum column and the
@@ -2117,12 +2172,16 @@ ResultRows Execution::run(bool want_rows) {
       for (int s = 0; s < p.n_sum; ++s) p.global_float[1 + s] = aggt_.ps_float[s];
       for (int b = 0; b < aggt_.nbs; ++b) p.global_float[1 + p.n_sum + b] = aggt_.bs_float[b];
     }
+    BucketDev bd{};
+    uint64_t nbuckets = 0;
+    const bool buckets = grouped_ && aggt_.krec != nullptr && setup_buckets(p, bd, nbuckets);
     BatchView v;
     while (pfeed->next(v)) {
       run_scan(p, v, staged_ != nullptr);
       pfeed->done();
       st_.ingest_bytes += v.bytes;
     }
+    if (buckets) launch_bucket_agg(aggt_, bd, nbuckets, agg_cap_, ctx_.compute);
   } else {
     uint64_t waves = pfeed->nbatches;
     if (nr > 1) {

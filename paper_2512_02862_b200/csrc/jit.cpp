@@ -203,8 +203,17 @@ void emit_rank_probe(std::ostringstream& s, const ScanProgram& P, Late late) {
     << "        if (!((bw[r] >> bb[r]) & 1ULL)) pass &= ~(1u << r);\n"
     << "        else sl[r] = bp[r] + static_cast<uint64_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n";
   late();
-  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
-    << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n";
+  if (P.bkt != nullptr) {  // append one word to the slot's bucket (k_bucket_agg folds it)
+    s << "        const uint64_t b = sl[r] >> " << kBucketBits << ";\n"
+      << "        const unsigned pos = atomicAdd(P.bkt_fill + b, 1u);\n"
+      << "        if (pos < P.bkt_cap) {\n          uint64_t e = sl[r] & " << (kBucketSlots - 1) << "ULL;\n";
+    for (int k = 0; k < P.n_sum; ++k)
+      s << "          e |= ((" << V(P.sum_reg[k]) << "[r] - static_cast<uint64_t>(P.bkt_min[" << k << "])) & P.bkt_mask[" << k
+        << "]) << P.bkt_shift[" << k << "];\n";
+    s << "          P.bkt[b * P.bkt_cap + pos] = e;\n          continue;\n        }\n";
+  }
+  s << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
   emit_accumulate(s, P, "        ");
   s << "      }\n    }\n";
 }
@@ -877,6 +886,9 @@ int jit_selftest(std::string& log) {
       q.agg.npacked = 1;
       q.agg.packed_shift[0] = 30;
       q.agg.packed_shift[1] = -1;
+      progs.push_back(q);
+      q.bkt = reinterpret_cast<uint64_t*>(16);  // + bucketed aggregation
+      q.agg.ps_float[1] = 0;
       progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // consuming packed rows

@@ -698,6 +698,56 @@ void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, ui
   k_krec_build<<<grid_for(n, 256), 256, 0, S(stream)>>>(bits, krank, n, krec);
 }
 
+/// Bucketed aggregation, phase 2: one CTA per bucket folds its appended words (slot low bits +
+/// offset-encoded probe sums, see ScanProgram::bkt) into shared-memory accumulators laid out like
+/// hot-slot words 1..nacc (word 1 = hits (+ packed sums), then the unpacked sums), then adds them
+/// to the bucket's kBucketSlots hot slots - sequential 32-byte rows instead of random HBM atomics.
+/// Entries past bkt_cap were applied directly by the probe. Integer sums only (wrap-around adds).
+__global__ void __launch_bounds__(512) k_bucket_agg(AggTableDev t, BucketDev b, uint64_t nslots) {
+  extern __shared__ unsigned long long acc[];  // [nacc][kBucketSlots]
+  const int nacc = b.nacc;
+  for (int i = threadIdx.x; i < nacc * kBucketSlots; i += blockDim.x) acc[i] = 0;
+  __syncthreads();
+  const uint64_t bucket = blockIdx.x;
+  const uint32_t n = min(b.fill[bucket], b.cap);
+  const uint64_t* e = b.bkt + bucket * b.cap;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const uint64_t w = __ldcs(reinterpret_cast<const unsigned long long*>(e + i));
+    const uint32_t sl = static_cast<uint32_t>(w & (kBucketSlots - 1));
+    unsigned long long inc = 1ULL;
+    for (int k = 0; k < t.nps; ++k) {
+      const uint64_t v = static_cast<uint64_t>(b.min[k]) + ((w >> b.shift[k]) & b.mask[k]);
+      if (t.npacked && t.packed_shift[k] >= 0)
+        inc += (v - static_cast<uint64_t>(t.packed_min[k])) << t.packed_shift[k];
+      else
+        atomicAdd(&acc[b.word[k] * kBucketSlots + sl], static_cast<unsigned long long>(v));
+    }
+    atomicAdd(&acc[sl], inc);
+  }
+  __syncthreads();
+  const uint64_t s0 = bucket << kBucketBits;
+  for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) {
+    const uint64_t s = s0 + i;
+    if (s >= nslots) break;
+    uint64_t* h = t.hot + s * t.hw;
+    for (int j = 0; j < nacc; ++j) {
+      const unsigned long long a = acc[j * kBucketSlots + i];
+      if (a) h[1 + j] += a;
+    }
+  }
+}
+void launch_bucket_agg(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots, void* stream) {
+  if (nbuckets == 0) return;
+  const int smem = b.nacc * kBucketSlots * 8;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bucket_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBucketSlots * 8);
+    attr = true;
+  }
+  count_launch();
+  k_bucket_agg<<<static_cast<unsigned>(nbuckets), 512, smem, S(stream)>>>(t, b, nslots);
+}
+
 /// Destination histogram of n keys (partition_of, hashing.hpp:35-37): one shared atomic per
 /// (warp, destination) from __match_any_sync groups, one global atomic per (block, destination).
 __global__ void k_part_hist(const uint64_t* __restrict__ keys, uint64_t n, int nparts, unsigned long long* counts) {

@@ -80,6 +80,19 @@ size_t sort_pairs_u32(const uint32_t* keys_in, uint32_t* keys_out, const uint32_
                       int end_bit, void* tmp, size_t tmp_bytes, void* stream);
 void launch_gather64(const uint64_t* const* in_cols, int ncols, const uint64_t* idx, uint64_t n, uint64_t* const* out,
                      void* stream);
+/// Phase-2 view of the bucketed aggregation (ScanProgram::bkt): nacc accumulator words per slot
+/// (hot words 1..nacc); word[k] = the accumulator an unpacked probe sum k adds to.
+struct BucketDev {
+  const uint64_t* bkt;
+  const unsigned int* fill;
+  uint32_t cap;
+  int32_t nacc;
+  int32_t shift[kMaxSums];
+  uint64_t mask[kMaxSums];
+  int64_t min[kMaxSums];
+  int32_t word[kMaxSums];
+};
+void launch_bucket_agg(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots, void* stream);
 void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, uint64_t n, unsigned long long* krec,
                        void* stream);
 void launch_part_hist(const uint64_t* keys, uint64_t n, int nparts, unsigned long long* counts, void* stream);
