@@ -520,7 +520,12 @@ class Execution {
   // agg table
   DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, agg_krank_, agg_krec_, global_acc_, barrier_word_;
   DevBuf bkt_, bkt_fill_;  // bucketed aggregation (rank table, one GPU)
-  bool setup_buckets(ScanProgram& p, BucketDev& bd, uint64_t& nbuckets);
+  bool bucket_mode_ = false;
+  BucketDev bd_{};
+  uint64_t nbuckets_ = 0;
+  bool setup_buckets();
+  void apply_buckets(ScanProgram& p) const;
+  void finalize_buckets(ResultRows& out, bool want_rows);
   AggTableDev aggt_{};
   // the build insert running on ctx_.comm concurrently with the probe side (N > 1 Bloom path)
   struct Event {
@@ -1275,13 +1280,14 @@ void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words, uint6
 /// with the slot's low bits, in one 64-bit word. Bucket capacity: the expected survivors (probe
 /// rows x the build keys' share of the key range) / buckets x 1.5; overflow is applied directly.
 /// PSG_BUCKETS=0: off.
-bool Execution::setup_buckets(ScanProgram& p, BucketDev& bd, uint64_t& nbuckets) {
+bool Execution::setup_buckets() {
   static const bool env = [] {
     const char* e = std::getenv("PSG_BUCKETS");
     return !(e && e[0] == '0');
   }();
   const int np = static_cast<int>(probe_sum_wire.size());
   if (!env || !jit_available() || np > 3 || aggt_.krange == 0 || agg_cap_ == 0) return false;
+  BucketDev bd{};
   int shift = kBucketBits;
   uint64_t probe_rows = 0;
   for (const auto& path : psrc_.scan->paths) probe_rows += ctx_.footers.get(path)->total_rows();
@@ -1300,27 +1306,70 @@ bool Execution::setup_buckets(ScanProgram& p, BucketDev& bd, uint64_t& nbuckets)
     const uint64_t span = static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo);
     const int w = span ? 64 - __builtin_clzll(span) : 0;
     if (shift + w > 64) return false;
-    p.bkt_shift[k] = bd.shift[k] = shift;
-    p.bkt_mask[k] = bd.mask[k] = w == 64 ? ~0ULL : ((1ULL << w) - 1);
-    p.bkt_min[k] = bd.min[k] = lo;
+    bd.shift[k] = shift;
+    bd.mask[k] = w == 64 ? ~0ULL : ((1ULL << w) - 1);
+    bd.min[k] = lo;
     bd.word[k] = 1 + k;  // hot word 2 + k
     shift += w;
   }
-  nbuckets = (agg_cap_ + kBucketSlots - 1) / kBucketSlots;
+  const uint64_t nb = (agg_cap_ + kBucketSlots - 1) / kBucketSlots;
   const double share = std::min(1.0, static_cast<double>(agg_cap_) / static_cast<double>(aggt_.krange));
-  const uint64_t cap = static_cast<uint64_t>(1.5 * static_cast<double>(probe_rows) * share / static_cast<double>(nbuckets)) + 1024;
+  const uint64_t cap = static_cast<uint64_t>(1.5 * static_cast<double>(probe_rows) * share / static_cast<double>(nb)) + 1024;
   if (cap >= (1ULL << 31)) return false;
-  bkt_ = DevBuf(ctx_.pool, nbuckets * cap * 8, ctx_.compute);
-  bkt_fill_ = DevBuf(ctx_.pool, nbuckets * 4, ctx_.compute);
-  PSG_CUDA(cudaMemsetAsync(bkt_fill_.p, 0, nbuckets * 4, ctx_.compute));
-  p.bkt = bkt_.as<uint64_t>();
-  p.bkt_fill = bkt_fill_.as<unsigned int>();
-  p.bkt_cap = static_cast<uint32_t>(cap);
-  bd.bkt = p.bkt;
-  bd.fill = p.bkt_fill;
-  bd.cap = p.bkt_cap;
+  bkt_ = DevBuf(ctx_.pool, nb * cap * 8, ctx_.compute);
+  bkt_fill_ = DevBuf(ctx_.pool, nb * 4, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(bkt_fill_.p, 0, nb * 4, ctx_.compute));
+  bd.bkt = bkt_.as<uint64_t>();
+  bd.fill = bkt_fill_.as<unsigned int>();
+  bd.cap = static_cast<uint32_t>(cap);
   bd.nacc = 1 + np;
+  bd_ = bd;
+  nbuckets_ = nb;
   return true;
+}
+
+void Execution::apply_buckets(ScanProgram& p) const {
+  p.bkt = const_cast<uint64_t*>(bd_.bkt);
+  p.bkt_fill = const_cast<unsigned int*>(bd_.fill);
+  p.bkt_cap = bd_.cap;
+  for (int k = 0; k < kMaxSums; ++k) {
+    p.bkt_shift[k] = bd_.shift[k];
+    p.bkt_mask[k] = bd_.mask[k];
+    p.bkt_min[k] = bd_.min[k];
+  }
+}
+
+/// Bucketed finalisation: groups per bucket -> exclusive scan -> rows written per bucket in key
+/// order (k_bucket_count, k_bucket_emit); the only host sync is the group total for the output.
+void Execution::finalize_buckets(ResultRows& out, bool want_rows) {
+  const int nc = static_cast<int>(result_schema_.size());
+  std::vector<int32_t> kind, idx;
+  kind.push_back(0), idx.push_back(0);
+  kind.push_back(1), idx.push_back(0);
+  for (auto [side, k] : sum_order) {
+    kind.push_back(side == 1 ? 2 : 3);
+    idx.push_back(k);
+  }
+  DevBuf counts(ctx_.pool, (nbuckets_ + 1) * 4, ctx_.compute), offs(ctx_.pool, (nbuckets_ + 1) * 4, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(counts.p, 0, (nbuckets_ + 1) * 4, ctx_.compute));
+  launch_bucket_count(aggt_, bd_, nbuckets_, agg_cap_, counts.as<uint32_t>(), ctx_.compute);
+  const size_t tb = exclusive_scan_u32(nullptr, nullptr, nbuckets_ + 1, nullptr, 0, ctx_.compute);
+  DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
+  exclusive_scan_u32(counts.as<uint32_t>(), offs.as<uint32_t>(), nbuckets_ + 1, tmp.p, tb, ctx_.compute);
+  uint32_t ng = 0;
+  PSG_CUDA(cudaMemcpyAsync(&ng, offs.as<uint32_t>() + nbuckets_, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  DevBuf rows(ctx_.pool, std::max<uint64_t>(ng, 1) * nc * 8, ctx_.compute);
+  if (ng)
+    launch_bucket_emit(aggt_, bd_, nbuckets_, agg_cap_, offs.as<uint32_t>(), nc, kind.data(), idx.data(), rows.as<uint64_t>(),
+                       ctx_.compute);
+  out.nrows = ng;
+  if (want_rows) {
+    uint64_t* dst = out.mutable_rows(static_cast<uint64_t>(ng) * nc);
+    if (ng) PSG_CUDA(cudaMemcpyAsync(dst, rows.p, static_cast<uint64_t>(ng) * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    st_.result_bytes += static_cast<uint64_t>(ng) * nc * 8;
+  }
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
 }
 
 /// Bit-packed accumulators: the footer zone maps bound every int probe-side sum column and the
@@ -1505,6 +1554,7 @@ Execution::Received Execution::exchange(DevCols& mat, int ncols, int key_col, De
 /// key's rank in a bitmap of present keys, so one sequential table pass writes every row in
 /// place (no sort, no gather). Sparse keys: compact -> radix sort of the varying key bits -> emit.
 void Execution::finalize_grouped(ResultRows& out, bool want_rows) {
+  if (bucket_mode_) return finalize_buckets(out, want_rows);
   const uint64_t nslots = agg_cap_ + 1;
   DevBuf counter(ctx_.pool, 24, ctx_.compute);
   const uint64_t init[3] = {0, ~0ULL, 0};
@@ -1943,6 +1993,9 @@ ResultRows Execution::run(bool want_rows) {
       }
     }
     pack_accumulators();
+    // one GPU, rank table, fused probe: bucketed aggregation (the hot table is then only the target
+    // of bucket overflow - zeroed instead of initialised with keys)
+    if (rank_mode && nr == 1 && grouped_ && !pdup) bucket_mode_ = setup_buckets();
     pt.mark("  agg alloc+init", ctx_.compute);
     ScanProgram p = batch_program(static_cast<int>(b_out.size()));
     p.sink = SINK_BUILD;
@@ -1961,13 +2014,14 @@ ResultRows Execution::run(bool want_rows) {
     if (rank_mode) {
       // hot slots from the bitmap (slot order) once, cold slots (build sums) per build segment
       bool first = true;
+      if (bucket_mode_) PSG_CUDA(cudaMemsetAsync(agg_hot_.p, 0, agg_hot_.bytes, ctx_.compute));
       for (const auto& sg : bsegs) {
         RankSums rs{};
         for (int b = 0; b < p.n_sum; ++b) rs.col[b] = sg.col[1 + b];
-        launch_rank_build(aggt_, sg.col[0], rs, sg.rows, first, ctx_.compute);
+        launch_rank_build(aggt_, sg.col[0], rs, sg.rows, first, !bucket_mode_, ctx_.compute);
         first = false;
       }
-      if (first) launch_rank_build(aggt_, nullptr, RankSums{}, 0, true, ctx_.compute);
+      if (first) launch_rank_build(aggt_, nullptr, RankSums{}, 0, true, !bucket_mode_, ctx_.compute);
     } else if (semi && !krange && aggt_.bloom && overlap_env) {
       for (const auto& sg : bsegs) launch_bloom_keys(sg.col[0], sg.rows, aggt_.bloom, aggt_.bloom_shift, ctx_.compute);
       PSG_CUDA(cudaEventRecord(build_fork_.get(), ctx_.compute));
@@ -2172,16 +2226,13 @@ ResultRows Execution::run(bool want_rows) {
       for (int s = 0; s < p.n_sum; ++s) p.global_float[1 + s] = aggt_.ps_float[s];
       for (int b = 0; b < aggt_.nbs; ++b) p.global_float[1 + p.n_sum + b] = aggt_.bs_float[b];
     }
-    BucketDev bd{};
-    uint64_t nbuckets = 0;
-    const bool buckets = grouped_ && aggt_.krec != nullptr && setup_buckets(p, bd, nbuckets);
+    if (bucket_mode_) apply_buckets(p);
     BatchView v;
     while (pfeed->next(v)) {
       run_scan(p, v, staged_ != nullptr);
       pfeed->done();
       st_.ingest_bytes += v.bytes;
     }
-    if (buckets) launch_bucket_agg(aggt_, bd, nbuckets, agg_cap_, ctx_.compute);
   } else {
     uint64_t waves = pfeed->nbatches;
     if (nr > 1) {

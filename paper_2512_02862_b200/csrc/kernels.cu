@@ -46,6 +46,11 @@ inline unsigned grid_for(uint64_t n, int per_block) {
   if (b > cap) b = cap;
   return static_cast<unsigned>(b < 1 ? 1 : b);
 }
+
+/// One 256-bit global store (sm_100: STG.256 - a whole 32-byte sector in one request).
+__device__ __forceinline__ void st256(uint64_t* p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
+  asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
+}
 }  // namespace
 
 uint64_t kernel_launch_count() { return g_launches.load(); }
@@ -698,25 +703,78 @@ void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, ui
   k_krec_build<<<grid_for(n, 256), 256, 0, S(stream)>>>(bits, krank, n, krec);
 }
 
-/// Bucketed aggregation, phase 2: one CTA per bucket folds its appended words (slot low bits +
-/// offset-encoded probe sums, see ScanProgram::bkt) into shared-memory accumulators laid out like
-/// hot-slot words 1..nacc (word 1 = hits (+ packed sums), then the unpacked sums), then adds them
-/// to the bucket's kBucketSlots hot slots - sequential 32-byte rows instead of random HBM atomics.
-/// Entries past bkt_cap were applied directly by the probe. Integer sums only (wrap-around adds).
-__global__ void __launch_bounds__(512) k_bucket_agg(AggTableDev t, BucketDev b, uint64_t nslots) {
-  extern __shared__ unsigned long long acc[];  // [nacc][kBucketSlots]
+/// Output column recipe of the emit kernels: kind 0 key, 1 rows, 2 probe sum idx, 3 build sum idx.
+struct EmitCols {
+  int32_t kind[2 * kMaxSums + 2];
+  int32_t idx[2 * kMaxSums + 2];
+};
+
+/// Bucketed aggregation, finalisation (one CTA per bucket of kBucketSlots consecutive rank-table
+/// slots; ScanProgram::bkt). The probe appended one word per surviving row to its slot's bucket
+/// (slot low bits + offset-encoded probe sums); entries past the bucket capacity were added
+/// straight into the (zeroed) hot table instead. Pass 1 counts the groups (slots with hits) per
+/// bucket, an exclusive scan turns the counts into output offsets, and pass 2 folds the bucket in
+/// shared memory and writes its result rows in key order: keys come from the key bitmap (slot =
+/// krank[w] + set bits below), so the table in HBM is never read or written on the common path.
+namespace {
+__device__ __forceinline__ uint64_t bucket_value(const BucketDev& b, uint64_t w, int k) {
+  return static_cast<uint64_t>(b.min[k]) + ((w >> b.shift[k]) & b.mask[k]);
+}
+/// largest word index w with krank[w] <= s (krank is non-decreasing, krank[0] = 0)
+__device__ __forceinline__ uint64_t rank_word_of(const AggTableDev& t, uint64_t nwords, uint64_t s) {
+  uint64_t lo = 0, hi = nwords;  // answer in [lo, hi)
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (t.krank[mid] <= s) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+}  // namespace
+
+__global__ void __launch_bounds__(512) k_bucket_count(AggTableDev t, BucketDev b, uint64_t nslots, uint32_t* counts) {
+  __shared__ uint32_t hits[kBucketSlots];
+  __shared__ uint32_t s_total;
+  for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) hits[i] = 0;
+  if (threadIdx.x == 0) s_total = 0;
+  __syncthreads();
+  const uint64_t bucket = blockIdx.x, s0 = bucket << kBucketBits;
+  const uint32_t fill = b.fill[bucket], n = min(fill, b.cap);
+  const uint64_t* e = b.bkt + bucket * b.cap;
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
+    atomicAdd(&hits[__ldcs(reinterpret_cast<const unsigned long long*>(e + i)) & (kBucketSlots - 1)], 1u);
+  __syncthreads();
+  uint32_t mine = 0;
+  for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) {
+    const uint64_t s = s0 + i;
+    if (s >= nslots) break;
+    uint64_t h = hits[i];
+    if (fill > b.cap) h += agg_hits(t, t.hot + s * t.hw);  // overflowed bucket: + the direct updates
+    mine += h != 0;
+  }
+  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_total, mine);
+  __syncthreads();
+  if (threadIdx.x == 0) counts[bucket] = s_total;
+}
+
+__global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b, uint64_t nslots, uint64_t nwords,
+                                                     const uint32_t* offsets, int nc, EmitCols ec, uint64_t* out) {
+  extern __shared__ unsigned long long acc[];  // [nacc][kBucketSlots], then uint16 pos[kBucketSlots]
   const int nacc = b.nacc;
+  uint16_t* pos = reinterpret_cast<uint16_t*>(acc + nacc * kBucketSlots);
+  __shared__ uint32_t s_warp[16];
   for (int i = threadIdx.x; i < nacc * kBucketSlots; i += blockDim.x) acc[i] = 0;
   __syncthreads();
-  const uint64_t bucket = blockIdx.x;
-  const uint32_t n = min(b.fill[bucket], b.cap);
+  const uint64_t bucket = blockIdx.x, s0 = bucket << kBucketBits;
+  const uint64_t s_end = min(s0 + kBucketSlots, nslots);
+  const uint32_t fill = b.fill[bucket], n = min(fill, b.cap);
   const uint64_t* e = b.bkt + bucket * b.cap;
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     const uint64_t w = __ldcs(reinterpret_cast<const unsigned long long*>(e + i));
     const uint32_t sl = static_cast<uint32_t>(w & (kBucketSlots - 1));
     unsigned long long inc = 1ULL;
     for (int k = 0; k < t.nps; ++k) {
-      const uint64_t v = static_cast<uint64_t>(b.min[k]) + ((w >> b.shift[k]) & b.mask[k]);
+      const uint64_t v = bucket_value(b, w, k);
       if (t.npacked && t.packed_shift[k] >= 0)
         inc += (v - static_cast<uint64_t>(t.packed_min[k])) << t.packed_shift[k];
       else
@@ -725,27 +783,116 @@ __global__ void __launch_bounds__(512) k_bucket_agg(AggTableDev t, BucketDev b, 
     atomicAdd(&acc[sl], inc);
   }
   __syncthreads();
-  const uint64_t s0 = bucket << kBucketBits;
-  for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) {
-    const uint64_t s = s0 + i;
-    if (s >= nslots) break;
-    uint64_t* h = t.hot + s * t.hw;
-    for (int j = 0; j < nacc; ++j) {
-      const unsigned long long a = acc[j * kBucketSlots + i];
-      if (a) h[1 + j] += a;
+  if (fill > b.cap)  // overflowed bucket: fold in the direct updates of its slots
+    for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) {
+      const uint64_t s = s0 + i;
+      if (s >= s_end) break;
+      const uint64_t* h = t.hot + s * t.hw;
+      for (int j = 0; j < nacc; ++j) acc[j * kBucketSlots + i] += h[1 + j];
+    }
+  __syncthreads();
+  // exclusive prefix of "slot has hits" over the bucket (8 consecutive slots per thread)
+  const int per = kBucketSlots / 512, base = threadIdx.x * per;
+  uint32_t local[kBucketSlots / 512];
+  uint32_t run = 0;
+  for (int k = 0; k < per; ++k) {
+    const uint64_t a = acc[base + k];
+    const uint64_t hts = t.npacked ? (a & t.hits_mask) : a;
+    local[k] = run;
+    run += (hts != 0 && s0 + base + k < s_end) ? 1u : 0u;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t incl = run;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[wid] = incl;
+  __syncthreads();
+  uint32_t wbase = 0;
+  for (int w = 0; w < wid; ++w) wbase += s_warp[w];
+  const uint32_t excl = wbase + incl - run;
+  for (int k = 0; k < per; ++k) pos[base + k] = static_cast<uint16_t>(excl + local[k]);
+  __syncthreads();
+  // rows in key order: walk the key-bitmap words covering the bucket's slots
+  const uint64_t w0 = rank_word_of(t, nwords, s0);
+  const unsigned long long* bits = reinterpret_cast<const unsigned long long*>(t.kbits);
+  const uint64_t obase = offsets[bucket];
+  const bool st32 = (nc & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
+  for (uint64_t w = w0 + threadIdx.x; w < nwords; w += blockDim.x) {
+    uint64_t s = t.krank[w];
+    if (s >= s_end) break;
+    unsigned long long m = bits[w];
+    while (m) {
+      const int bit = __ffsll(static_cast<long long>(m)) - 1;
+      m &= m - 1;
+      const uint64_t slot = s++;
+      if (slot < s0) continue;
+      if (slot >= s_end) break;
+      const int i = static_cast<int>(slot - s0);
+      uint64_t h[2 + kMaxSums];
+      h[0] = static_cast<uint64_t>(t.kmin) + (w << 6) + bit;
+      for (int j = 0; j < nacc; ++j) h[1 + j] = acc[j * kBucketSlots + i];
+      const uint64_t hits = t.npacked ? (h[1] & t.hits_mask) : h[1];
+      if (!hits) continue;
+      const uint64_t* c = t.cold + slot * t.cw;
+      uint64_t vals[2 * kMaxSums + 2];
+#pragma unroll
+      for (int k = 0; k < 2 * kMaxSums + 2; ++k) {
+        if (k >= nc) break;
+        const int kind = ec.kind[k], j = ec.idx[k];
+        uint64_t v;
+        if (kind == 0) v = h[0];
+        else if (kind == 1) v = hits;  // unique build keys: multiplicity 1
+        else if (kind == 2) v = agg_psum(t, h, j, hits);
+        else
+          v = t.bs_float[j] ? static_cast<uint64_t>(__double_as_longlong(
+                                  static_cast<double>(hits) * __longlong_as_double(static_cast<long long>(c[1 + j]))))
+                            : hits * c[1 + j];
+        vals[k] = v;
+      }
+      uint64_t* row = out + (obase + pos[i]) * nc;
+      if (st32) {
+#pragma unroll
+        for (int k = 0; k < 2 * kMaxSums + 2; k += 4) {
+          if (k >= nc) break;
+          st256(row + k, vals[k], vals[k + 1], vals[k + 2], vals[k + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 2 * kMaxSums + 2; ++k) {
+          if (k >= nc) break;
+          row[k] = vals[k];
+        }
+      }
     }
   }
 }
-void launch_bucket_agg(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots, void* stream) {
+
+void launch_bucket_count(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots, uint32_t* counts,
+                         void* stream) {
   if (nbuckets == 0) return;
-  const int smem = b.nacc * kBucketSlots * 8;
+  count_launch();
+  k_bucket_count<<<static_cast<unsigned>(nbuckets), 512, 0, S(stream)>>>(t, b, nslots, counts);
+}
+void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots,
+                        const uint32_t* offsets, int nc, const int32_t* col_kind, const int32_t* col_idx,
+                        uint64_t* out_rows, void* stream) {
+  if (nbuckets == 0) return;
+  EmitCols ec{};
+  for (int k = 0; k < nc; ++k) {
+    ec.kind[k] = col_kind[k];
+    ec.idx[k] = col_idx[k];
+  }
+  const int smem = b.nacc * kBucketSlots * 8 + kBucketSlots * 2;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_bucket_agg, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBucketSlots * 8);
+    cudaFuncSetAttribute(k_bucket_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBucketSlots * 8 + kBucketSlots * 2);
     attr = true;
   }
   count_launch();
-  k_bucket_agg<<<static_cast<unsigned>(nbuckets), 512, smem, S(stream)>>>(t, b, nslots);
+  k_bucket_emit<<<static_cast<unsigned>(nbuckets), 512, smem, S(stream)>>>(t, b, nslots, (t.krange + 63) / 64, offsets,
+                                                                           nc, ec, out_rows);
 }
 
 /// Destination histogram of n keys (partition_of, hashing.hpp:35-37): one shared atomic per
@@ -803,10 +950,6 @@ __global__ void k_bitmap_set(const uint64_t* keys, uint64_t n, int64_t bmin, uin
     const uint32_t bit = 1u << (d & 31);
     if (atomicOr(bitmap + (d >> 5), bit) & bit) *dup = 1u;
   }
-}
-/// One 256-bit global store (sm_100: STG.256 - a whole 32-byte sector in one request).
-__device__ __forceinline__ void st256(uint64_t* p, uint64_t a, uint64_t b, uint64_t c, uint64_t d) {
-  asm volatile("st.global.v4.u64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c), "l"(d) : "memory");
 }
 
 /// Hot slots of the rank-indexed table in slot (= key) order: one thread per 64-bit word of the
@@ -868,7 +1011,7 @@ __global__ void k_rank_build(AggTableDev t, const uint64_t* __restrict__ keys, R
 }
 
 void launch_rank_build(const AggTableDev& t, const uint64_t* keys, const RankSums& bs, uint64_t n, bool first,
-                       void* stream) {
+                       bool write_hot, void* stream) {
   // The hot slots are written in slot order from the key bitmap (k_rank_hot, sequential stores)
   // and the row-ordered build pass writes only the cold slots: the build rows arrive in scan
   // order, not key order, so hot-slot stores by row were scattered (SF100 N=1: one 0.60 ms pass
@@ -886,7 +1029,12 @@ void launch_rank_build(const AggTableDev& t, const uint64_t* keys, const RankSum
     cudaMemsetAsync(t.hot + spill * t.hw, 0, t.hw * sizeof(uint64_t), S(stream));
     cudaMemsetAsync(t.cold + spill * t.cw, 0, t.cw * sizeof(uint64_t), S(stream));
   }
-  if (hot_seq && t.hw % 4 == 0) {
+  if (!write_hot) {  // bucketed aggregation: the hot table is zeroed, keys come from the bitmap
+    if (t.nbs > 0 && n > 0) {
+      count_launch();
+      k_rank_build<false><<<grid_for(n, 256), 256, 0, S(stream)>>>(t, keys, bs, n);
+    }
+  } else if (hot_seq && t.hw % 4 == 0) {
     if (first) {
       const uint64_t nw = (t.krange + 63) / 64;
       count_launch();
@@ -1056,10 +1204,6 @@ __global__ void k_popc64(const unsigned long long* bitmap, uint64_t nwords, uint
     out[i] = __popcll(bitmap[i]);
 }
 
-struct EmitCols {
-  int32_t kind[2 * kMaxSums + 2];
-  int32_t idx[2 * kMaxSums + 2];
-};
 __global__ void k_agg_emit(AggTableDev t, const uint64_t* keys, const unsigned long long* slots, uint64_t n, int nc,
                            EmitCols ec, uint64_t* out) {
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;

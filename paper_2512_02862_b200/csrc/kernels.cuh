@@ -92,7 +92,11 @@ struct BucketDev {
   int64_t min[kMaxSums];
   int32_t word[kMaxSums];
 };
-void launch_bucket_agg(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots, void* stream);
+void launch_bucket_count(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots, uint32_t* counts,
+                         void* stream);
+void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots,
+                        const uint32_t* offsets, int nc, const int32_t* col_kind, const int32_t* col_idx,
+                        uint64_t* out_rows, void* stream);
 void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, uint64_t n, unsigned long long* krec,
                        void* stream);
 void launch_part_hist(const uint64_t* keys, uint64_t n, int nparts, unsigned long long* counts, void* stream);
@@ -102,7 +106,7 @@ struct RankSums {
   const uint64_t* col[kMaxSums];
 };
 void launch_rank_build(const AggTableDev& t, const uint64_t* keys, const RankSums& bs, uint64_t n, bool first,
-                       void* stream);
+                       bool write_hot, void* stream);
 void launch_bloom_keys(const uint64_t* keys, uint64_t n, uint32_t* bloom, int shift, void* stream);
 void launch_iota_u32(uint32_t* out, uint64_t n, void* stream);
 void launch_rows_from_cols(const uint64_t* const* cols, int ncols, uint64_t n, uint64_t* out_rows, void* stream);
