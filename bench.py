@@ -246,6 +246,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-block", action="store_true", help="skip the block-codec e2e config")
     ap.add_argument("--no-semijoin", action="store_true")
+    ap.add_argument("--budget-gb", type=float, default=2.0,
+                    help="plan memory_budget_bytes of the out-of-core e2e config (0: skip)")
     ap.add_argument("--io-threads", type=int, default=0)
     ap.add_argument("--batch-mb", type=int, default=0,
                     help="ingest batch size; default 128 MB at one GPU, 64 MB per rank at N > 1 (measured: "
@@ -378,6 +380,27 @@ def main():
 
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else args.steps
     e2e, parity, h2d_rank, e2e_s = e2e_run(data_root, e2e_steps, args.codec)
+    # out-of-core: the same query under a plan memory budget far below its 24 GB of input (the
+    # SF1000-on-8-GPUs regime of BASELINE configs[4] scaled to one GPU: regulate + bounded chunk
+    # ring, pipeline.cpp:198-240; acceptance C9: peak device bytes <= budget)
+    e2e_budget = None
+    if args.budget_gb > 0:
+        bplan = dict(plan, memory_budget_bytes=int(args.budget_gb * (1 << 30)))
+        bt, bpeak = [], 0
+        try:
+            for _ in range(min(e2e_steps, 3)):
+                sync_all()
+                t = time.time()
+                r = ctx.execute_plan(bplan, data_root)
+                bt.append(time.time() - t)
+                bpeak = max(bpeak, r.stats["peak_bytes"])
+                del r
+            e2e_budget = {"value": round(reduce(statistics.mean(bt)), 4), "unit": "s",
+                          "budget_bytes": bplan["memory_budget_bytes"], "peak_bytes": int(reduce(float(bpeak))),
+                          "input_bytes_per_gpu": int(h2d_rank), "steps": len(bt),
+                          "within_budget": bool(reduce(float(bpeak)) <= bplan["memory_budget_bytes"])}
+        except Exception as e:
+            e2e_budget = {"error": str(e)[:200], "budget_bytes": bplan["memory_budget_bytes"]}
     e2e_block = None
     if with_block:
         e2e_block, parity_block, _, _ = e2e_run(block_root, min(e2e_steps, 10), "block codec")
@@ -478,6 +501,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_block": e2e_block,
+            "e2e_budget": e2e_budget,
             "e2e_roofline": e2e_roof,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -1360,9 +1360,10 @@ void Execution::finalize_buckets(ResultRows& out, bool want_rows) {
   PSG_CUDA(cudaMemcpyAsync(&ng, offs.as<uint32_t>() + nbuckets_, 4, cudaMemcpyDeviceToHost, ctx_.compute));
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   DevBuf rows(ctx_.pool, std::max<uint64_t>(ng, 1) * nc * 8, ctx_.compute);
+  DevBuf first_word(ctx_.pool, nbuckets_ * 4, ctx_.compute);
   if (ng)
-    launch_bucket_emit(aggt_, bd_, nbuckets_, agg_cap_, offs.as<uint32_t>(), nc, kind.data(), idx.data(), rows.as<uint64_t>(),
-                       ctx_.compute);
+    launch_bucket_emit(aggt_, bd_, nbuckets_, agg_cap_, offs.as<uint32_t>(), first_word.as<uint32_t>(), nc, kind.data(),
+                       idx.data(), rows.as<uint64_t>(), ctx_.compute);
   out.nrows = ng;
   if (want_rows) {
     uint64_t* dst = out.mutable_rows(static_cast<uint64_t>(ng) * nc);

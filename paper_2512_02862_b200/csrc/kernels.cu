@@ -720,16 +720,18 @@ namespace {
 __device__ __forceinline__ uint64_t bucket_value(const BucketDev& b, uint64_t w, int k) {
   return static_cast<uint64_t>(b.min[k]) + ((w >> b.shift[k]) & b.mask[k]);
 }
-/// largest word index w with krank[w] <= s (krank is non-decreasing, krank[0] = 0)
-__device__ __forceinline__ uint64_t rank_word_of(const AggTableDev& t, uint64_t nwords, uint64_t s) {
-  uint64_t lo = 0, hi = nwords;  // answer in [lo, hi)
-  while (hi - lo > 1) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (t.krank[mid] <= s) lo = mid; else hi = mid;
-  }
-  return lo;
-}
 }  // namespace
+
+/// First key-bitmap word of every bucket: word w holds slots [krank[w], krank[w+1]), so bucket b
+/// (first slot b * kBucketSlots) starts in the w whose range contains it.
+__global__ void k_bucket_words(AggTableDev t, uint64_t nwords, uint64_t nslots, uint32_t* first_word) {
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < nwords;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t lo = t.krank[w], hi = w + 1 < nwords ? t.krank[w + 1] : nslots;
+    for (uint64_t b = (lo + kBucketSlots - 1) >> kBucketBits; (b << kBucketBits) < hi; ++b)
+      first_word[b] = static_cast<uint32_t>(w);
+  }
+}
 
 __global__ void __launch_bounds__(512) k_bucket_count(AggTableDev t, BucketDev b, uint64_t nslots, uint32_t* counts) {
   __shared__ uint32_t hits[kBucketSlots];
@@ -758,7 +760,8 @@ __global__ void __launch_bounds__(512) k_bucket_count(AggTableDev t, BucketDev b
 }
 
 __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b, uint64_t nslots, uint64_t nwords,
-                                                     const uint32_t* offsets, int nc, EmitCols ec, uint64_t* out) {
+                                                     const uint32_t* offsets, const uint32_t* first_word, int nc,
+                                                     EmitCols ec, uint64_t* out) {
   extern __shared__ unsigned long long acc[];  // [nacc][kBucketSlots], then uint16 pos[kBucketSlots]
   const int nacc = b.nacc;
   uint16_t* pos = reinterpret_cast<uint16_t*>(acc + nacc * kBucketSlots);
@@ -815,7 +818,7 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
   for (int k = 0; k < per; ++k) pos[base + k] = static_cast<uint16_t>(excl + local[k]);
   __syncthreads();
   // rows in key order: walk the key-bitmap words covering the bucket's slots
-  const uint64_t w0 = rank_word_of(t, nwords, s0);
+  const uint64_t w0 = first_word[bucket];
   const unsigned long long* bits = reinterpret_cast<const unsigned long long*>(t.kbits);
   const uint64_t obase = offsets[bucket];
   const bool st32 = (nc & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
@@ -876,9 +879,12 @@ void launch_bucket_count(const AggTableDev& t, const BucketDev& b, uint64_t nbuc
   k_bucket_count<<<static_cast<unsigned>(nbuckets), 512, 0, S(stream)>>>(t, b, nslots, counts);
 }
 void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots,
-                        const uint32_t* offsets, int nc, const int32_t* col_kind, const int32_t* col_idx,
-                        uint64_t* out_rows, void* stream) {
+                        const uint32_t* offsets, uint32_t* first_word, int nc, const int32_t* col_kind,
+                        const int32_t* col_idx, uint64_t* out_rows, void* stream) {
   if (nbuckets == 0) return;
+  const uint64_t nwords = (t.krange + 63) / 64;
+  count_launch();
+  k_bucket_words<<<grid_for(nwords, 256), 256, 0, S(stream)>>>(t, nwords, nslots, first_word);
   EmitCols ec{};
   for (int k = 0; k < nc; ++k) {
     ec.kind[k] = col_kind[k];
@@ -891,7 +897,7 @@ void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuck
     attr = true;
   }
   count_launch();
-  k_bucket_emit<<<static_cast<unsigned>(nbuckets), 512, smem, S(stream)>>>(t, b, nslots, (t.krange + 63) / 64, offsets,
+  k_bucket_emit<<<static_cast<unsigned>(nbuckets), 512, smem, S(stream)>>>(t, b, nslots, nwords, offsets, first_word,
                                                                            nc, ec, out_rows);
 }
 
