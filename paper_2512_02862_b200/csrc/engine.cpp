@@ -467,8 +467,9 @@ class Execution {
   // ---- stages ----
   void build_local_tables();
   ScanProgram base_program(const SourceDef& s, const RegMap& m, bool with_joins);
+  // aligned: v is a feed batch (16-byte aligned PSTO chunks with tail padding; bulk copies allowed)
   void materialize_into(DevCols& out, const ScanProgram& p0, const BatchView& v, const std::vector<int>& out_regs,
-                        int part_key_reg, DevBuf* part_counts, bool timed = false);
+                        int part_key_reg, DevBuf* part_counts, bool timed = false, bool aligned = false);
   DevCols alloc_cols(size_t ncols, uint64_t cap);
   // Local joins whose build side repeats keys (HashTable::build keeps duplicates and probe emits
   // every match, ops.cpp:105-222, apply_chain pipeline.cpp:431-448): the chain cannot stay in
@@ -965,7 +966,7 @@ DevCols Execution::materialize_chain(const SourceDef& s, const RegMap& m, const 
   std::vector<int> base_regs(m.n_in);
   std::iota(base_regs.begin(), base_regs.end(), 0);
   DevCols base = alloc_cols(base_regs.size(), std::max<uint64_t>(v.rows, 1));
-  materialize_into(base, p, v, base_regs, -1, nullptr);
+  materialize_into(base, p, v, base_regs, -1, nullptr, false, true);
   uint64_t n = read_count(base);
   std::vector<ColRef> refs;
   for (int c = 0; c < m.n_in; ++c) refs.push_back({-1, m.base_proj[c]});
@@ -1077,9 +1078,10 @@ void Execution::run_scan(const ScanProgram& p, const BatchView& v, bool timed, c
 }
 
 void Execution::materialize_into(DevCols& out, const ScanProgram& p0, const BatchView& v, const std::vector<int>& out_regs,
-                                 int part_key_reg, DevBuf* part_counts, bool timed) {
+                                 int part_key_reg, DevBuf* part_counts, bool timed, bool aligned) {
   ScanProgram p = p0;
   p.sink = SINK_MATERIALIZE;
+  p.staged_ok = aligned ? 1 : 0;
   p.n_out = static_cast<int>(out_regs.size());
   for (int o = 0; o < p.n_out; ++o) {
     p.out_reg[o] = out_regs[o];
@@ -1158,7 +1160,7 @@ void Execution::build_local_tables() {
       DevCols mat = alloc_cols(out_regs.size(), std::max<uint64_t>(feed->total_rows, 1));
       BatchView v;
       while (feed->next(v)) {
-        materialize_into(mat, p, v, out_regs, -1, nullptr);
+        materialize_into(mat, p, v, out_regs, -1, nullptr, false, true);
         feed->done();
         st_.ingest_bytes += v.bytes;
       }
@@ -1741,7 +1743,7 @@ ResultRows Execution::run(bool want_rows) {
       if (bdup)
         parts.push_back(materialize_chain(bsrc_, bm, v, b_out));
       else
-        materialize_into(bmat, bp, v, b_out, p2p ? b_out[0] : -1, p2p ? &owner_hist : nullptr);
+        materialize_into(bmat, bp, v, b_out, p2p ? b_out[0] : -1, p2p ? &owner_hist : nullptr, false, true);
       bfeed->done();
       st_.ingest_bytes += v.bytes;
     }
@@ -1769,7 +1771,7 @@ ResultRows Execution::run(bool want_rows) {
         bfeed->done();
         st_.ingest_bytes += v.bytes;
       } else if (have) {
-        materialize_into(mat, bp, v, b_out, b_out[0], &pc);
+        materialize_into(mat, bp, v, b_out, b_out[0], &pc, false, true);
         bfeed->done();
         st_.ingest_bytes += v.bytes;
       }
@@ -2371,7 +2373,7 @@ ResultRows Execution::run(bool want_rows) {
         pcs.emplace_back(ctx_.pool, nr * 8, ctx_.compute);
         PSG_CUDA(cudaMemsetAsync(pcs[c].p, 0, nr * 8, ctx_.compute));
         PSG_CUDA(cudaEventRecord(t0.e[c], ctx_.compute));
-        materialize_into(mats[c], pp, views[c], mat_out, p_out[0], &pcs[c], false);
+        materialize_into(mats[c], pp, views[c], mat_out, p_out[0], &pcs[c], false, true);
         PSG_CUDA(cudaEventRecord(t1.e[c], ctx_.compute));
         PSG_CUDA(cudaEventRecord(done.e[c], ctx_.compute));
       };
@@ -2410,7 +2412,7 @@ ResultRows Execution::run(bool want_rows) {
         pfeed->done();
         st_.ingest_bytes += v.bytes;
       } else if (have) {
-        materialize_into(mat, pp, v, mat_out, p_out[0], &pc, staged_ != nullptr);
+        materialize_into(mat, pp, v, mat_out, p_out[0], &pc, staged_ != nullptr, true);
         pfeed->done();
         st_.ingest_bytes += v.bytes;
       }

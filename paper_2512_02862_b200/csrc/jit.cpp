@@ -262,6 +262,29 @@ void emit_joins(std::ostringstream& s, const ScanProgram& P) {
   }
 }
 
+/// Semi-join screen of a partitioning scan (MATERIALIZE with nparts > 1): drop rows whose key is
+/// certainly absent on its owner rank - exact global key bitmap, or the owner's Bloom filter.
+/// Two stages: all R filter words in flight before any test.
+void emit_semi_screen(std::ostringstream& s, const ScanProgram& P) {
+  if (P.semi_kbits != nullptr) {  // exact global key bitmap
+    // two stages, like the Bloom screen: all R bitmap words in flight before any test
+    s << "    { uint32_t bw[R], bb[R];\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 1u; bb[r] = 0u; const uint64_t key = "
+      << V(P.semi_key_reg) << "[r];\n"
+      << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(P.semi_kmin);\n"
+      << "          bw[r] = 0u; if (d < P.semi_krange) { bb[r] = static_cast<uint32_t>(d & 31); "
+         "bw[r] = ldg_keep_u32(P.semi_kbits + (d >> 5), pol_keep); } } }\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!((bw[r] >> bb[r]) & 1u)) pass &= ~(1u << r);\n    }\n";
+  } else if (P.semi_bloom != nullptr) {
+    s << "    { uint32_t bw[R], bm[R];\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = bm[r] = 0; const uint64_t key = " << V(P.semi_key_reg)
+      << "[r];\n        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t h2 = key * kBloomMul;\n"
+      << "          const uint32_t d = part_of(key, static_cast<uint32_t>(P.nparts));\n"
+      << "          bm[r] = bloom_bits(h2, P.semi_shift); bw[r] = ldg_keep_u32(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift), pol_keep); } }\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n    }\n";
+  }
+}
+
 /// Warp-specialised probe for the one-GPU rank-indexed table (PSG_TMA=0: off). Shape knobs:
 /// PSG_TMA_NG consumer groups of 8 warps (default 2), PSG_TMA_NS ring stages (6), PSG_TMA_CTAS
 /// CTAs per SM (2).
@@ -283,8 +306,10 @@ bool staged_probe(const ScanProgram& P) {
     const char* e = std::getenv("PSG_TMA");
     return !(e && e[0] == '0');
   }();
-  return on && P.staged_ok && P.sink == SINK_PROBE && P.agg.krec != nullptr && !P.remote && P.unpack_n == 0 &&
-         P.n_early >= 1 && P.n_early <= 4 && P.n_in <= kMaxIn;
+  if (!on || !P.staged_ok || P.remote || P.unpack_n != 0 || P.n_early < 1 || P.n_early > 4 || P.n_in > kMaxIn) return false;
+  if (P.sink == SINK_PROBE) return P.agg.krec != nullptr;
+  // unordered warp-staged compaction (+ partition histogram, semi-join screen, packed rows)
+  return P.sink == SINK_MATERIALIZE && P.tile_offsets == nullptr && P.n_out >= 1 && P.n_out <= 4 && !P.self_probe;
 }
 
 /// Rows per thread per tile (R) of the kernel: R x 32 rows per warp, 1024 / (32 R) warps per
@@ -485,6 +510,11 @@ std::string jit_source(const ScanProgram& P) {
     }
     s << "    }\n";
   } else {
+    // the semi-join screen runs before the late columns are loaded when its key is an early
+    // column (at N > 1 it drops ~90% of the probe side: their late sectors are never read)
+    const bool screen_early = P.sink == SINK_MATERIALIZE && (P.semi_kbits != nullptr || P.semi_bloom != nullptr) &&
+                              P.semi_key_reg < P.n_early;
+    if (screen_early) emit_semi_screen(s, P);
     emit_loads(s, P.n_early, P.n_in);
     if (P.sink == SINK_AGG_SCAN) {  // Q6-analog: rows and sums of the surviving rows
       s << "#pragma unroll\n    for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n      g0 += 1;\n";
@@ -516,23 +546,7 @@ std::string jit_source(const ScanProgram& P) {
       }
       s << "      }\n    }\n";
     } else {  // MATERIALIZE / COUNT
-      if (P.sink == SINK_MATERIALIZE && P.semi_kbits != nullptr) {  // exact global key bitmap
-        // two stages, like the Bloom screen: all R bitmap words in flight before any test
-        s << "    { uint32_t bw[R], bb[R];\n"
-          << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 1u; bb[r] = 0u; const uint64_t key = "
-          << V(P.semi_key_reg) << "[r];\n"
-          << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(P.semi_kmin);\n"
-          << "          bw[r] = 0u; if (d < P.semi_krange) { bb[r] = static_cast<uint32_t>(d & 31); "
-             "bw[r] = ldg_keep_u32(P.semi_kbits + (d >> 5), pol_keep); } } }\n"
-          << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (!((bw[r] >> bb[r]) & 1u)) pass &= ~(1u << r);\n    }\n";
-      } else if (P.sink == SINK_MATERIALIZE && P.semi_bloom != nullptr) {
-        s << "    { uint32_t bw[R], bm[R];\n"
-          << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = bm[r] = 0; const uint64_t key = " << V(P.semi_key_reg)
-          << "[r];\n        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t h2 = key * kBloomMul;\n"
-          << "          const uint32_t d = part_of(key, static_cast<uint32_t>(P.nparts));\n"
-          << "          bm[r] = bloom_bits(h2, P.semi_shift); bw[r] = ldg_keep_u32(P.semi_bloom + d * P.semi_words + (h2 >> P.semi_shift), pol_keep); } }\n"
-          << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((pass & (1u << r)) && (bw[r] & bm[r]) != bm[r]) pass &= ~(1u << r);\n    }\n";
-      }
+      if (P.sink == SINK_MATERIALIZE && !screen_early) emit_semi_screen(s, P);
       if (P.sink == SINK_MATERIALIZE && P.self_probe && P.nparts > 1) {
         // rows owned by this rank: probe + aggregate in place (two-stage lookup), drop from the shuffle
         s << "    { const AggTableDev& T = P.agg; uint32_t own = 0; uint64_t sl[R], k0[R];\n"
@@ -638,8 +652,16 @@ std::string jit_source_staged(const ScanProgram& P) {
     << "  __shared__ __align__(8) uint64_t full_bar[" << NS << "], empty_bar[" << NS << "];\n"
     << "  __shared__ const uint64_t* s_col[" << NS << "][" << std::max(1, NIN) << "];\n"
     << "  __shared__ int s_rows[" << NS << "];\n"
-    << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n"
-    << "  if (tid == 0) {\n    for (int i = 0; i < " << NS << "; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], 8); }\n"
+    << "  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;\n";
+  const bool mat = P.sink == SINK_MATERIALIZE;
+  if (mat) {
+    // per consumer warp staging rows (dynamic shared memory after the ring)
+    s << "  uint64_t* s_stg = stg + " << NS * NE * 1024 << ";\n";
+    if (P.nparts > 1)
+      s << "  __shared__ unsigned long long s_part[" << kMaxParts << "];\n"
+        << "  for (int i = tid; i < " << kMaxParts << "; i += " << NT << ") s_part[i] = 0;\n";
+  }
+  s << "  if (tid == 0) {\n    for (int i = 0; i < " << NS << "; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], 8); }\n"
     << "    mbar_fence_init();\n  }\n  __syncthreads();\n"
     << "  const uint64_t per_cta = (ntiles + gridDim.x - 1) / gridDim.x;\n"
     << "  const uint64_t t_beg = blockIdx.x * per_cta;\n"
@@ -658,8 +680,18 @@ std::string jit_source_staged(const ScanProgram& P) {
   for (int c = 0; c < NE; ++c)
     s << "        bulk_g2s(stg + (st * " << NE << " + " << c << ") * 1024, sg->col[" << c << "] + r0, bytes, &full_bar[st], pol_stream);\n";
   s << "      }\n    }\n    return;\n  }\n"
-    << "  const uint64_t pol_keep = l2_evict_last();\n"
-    << "  const int cw = (warp - 1) & 7, grp = (warp - 1) >> 3;\n  const int wrow = cw * (R * 32) + lane;\n"
+    << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep;\n"
+    << "  const int cw = (warp - 1) & 7, grp = (warp - 1) >> 3;\n  const int wrow = cw * (R * 32) + lane;\n";
+  if (mat) {
+    s << "  int fill = 0;\n  auto flush = [&]() {\n    __syncwarp();\n    if (fill == 0) return;\n"
+      << "    unsigned long long base = 0;\n    if (lane == 0) base = atomicAdd(P.out_count, static_cast<unsigned long long>(fill));\n"
+      << "    base = __shfl_sync(0xffffffffu, base, 0);\n"
+      << "    for (int i = lane; i < fill; i += 32) { if (base + i >= P.out_cap) continue;\n";
+    for (int o = 0; o < P.n_out; ++o)
+      s << "      P.out_col[" << o << "][base + i] = s_stg[((warp - 1) * " << P.n_out << " + " << o << ") * 128 + i];\n";
+    s << "    }\n    fill = 0;\n    __syncwarp();\n  };\n";
+  }
+  s
     << "  for (uint64_t k = grp; t_beg + k < t_end; k += " << NG << ") {\n"
     << "    const int st = static_cast<int>(k % " << NS << "); const uint32_t ph = static_cast<uint32_t>((k / " << NS << ") & 1);\n"
     << "    mbar_wait(&full_bar[st], ph);\n"
@@ -673,12 +705,42 @@ std::string jit_source_staged(const ScanProgram& P) {
   s << "    __syncwarp();\n    if (lane == 0) mbar_arrive(&empty_bar[st]);  // stage consumed: the producer may refill it\n";
   emit_atoms(s, P);
   emit_joins(s, P);
-  emit_rank_probe(s, P, [&] {
+  auto late = [&] {
     for (int c = NE; c < NIN; ++c)
       s << "#pragma unroll\n      for (int r = 0; r < R; ++r) if (pass & (1u << r)) " << V(c)
         << "[r] = __ldcs(reinterpret_cast<const unsigned long long*>(lc" << c << " + wrow + r * 32));\n";
-  });
-  s << "  }\n}\n";
+  };
+  if (P.sink == SINK_PROBE) {
+    emit_rank_probe(s, P, late);
+    s << "  }\n}\n";
+    return s.str();
+  }
+  // MATERIALIZE: screen -> late columns -> per-warp staging in shared memory, flushed 128 rows at
+  // a time with one global atomic; destination histogram in shared memory (part)
+  const bool part = P.nparts > 1;
+  const bool screen_early = (P.semi_kbits != nullptr || P.semi_bloom != nullptr) && P.semi_key_reg < NE;
+  if (screen_early) emit_semi_screen(s, P);
+  late();
+  if (!screen_early) emit_semi_screen(s, P);
+  s << "    { const uint32_t lt = (1u << lane) - 1u;\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+    << "        const unsigned b = __ballot_sync(0xffffffffu, (pass >> r) & 1u);\n"
+    << "        const int cnt = __popc(b);\n        if (fill + cnt > 128) flush();\n"
+    << "        if ((pass >> r) & 1u) { const int pos = fill + __popc(b & lt);\n";
+  for (int o = 0; o < P.n_out; ++o)
+    s << "          s_stg[((warp - 1) * " << P.n_out << " + " << o << ") * 128 + pos] = " << out_value(P, o) << ";\n";
+  s << "        }\n        fill += cnt;\n      }\n    }\n";
+  if (part)
+    s << "#pragma unroll\n    for (int r = 0; r < R; ++r) {\n"
+      << "      const bool on = (pass >> r) & 1u;\n"
+      << "      const uint32_t d = on ? part_of(" << V(P.part_key_reg) << "[r], static_cast<uint32_t>(P.nparts)) : 0xffffffffu;\n"
+      << "      const unsigned peers = __match_any_sync(0xffffffffu, d);\n"
+      << "      if (on && lane == __ffs(peers) - 1) atomicAdd(&s_part[d], static_cast<unsigned long long>(__popc(peers)));\n    }\n";
+  s << "  }\n  flush();\n";
+  if (part)
+    s << "  asm volatile(\"bar.sync 1, " << 32 * 8 * NG << ";\" ::: \"memory\");  // consumers only (the producer exited)\n"
+      << "  for (int i = tid - 32; i < P.nparts; i += " << 32 * 8 * NG << ") if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
+  s << "}\n";
   return s.str();
 }
 
@@ -783,6 +845,7 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
           const StagedShape sh = staged_shape();
           block = 32 * (1 + 8 * sh.groups);
           smem = std::max(sh.stages, sh.groups) * P.n_early * 1024 * 8;
+          if (P.sink == SINK_MATERIALIZE) smem += 8 * sh.groups * P.n_out * 128 * 8;
         }
         it = g_cache.emplace(key, compile(body, dev, block, smem)).first;
       }
@@ -865,6 +928,14 @@ int jit_selftest(std::string& log) {
       ScanProgram q = p;
       q.semi_bloom = nullptr;
       q.semi_kbits = reinterpret_cast<const uint32_t*>(16);
+      progs.push_back(q);
+      q.self_probe = 0;  // the warp-specialised bulk-copy partitioning scan (packed rows)
+      q.staged_ok = 1;
+      progs.push_back(q);
+      q.pack_n = 0;  // ... and with plain multi-column rows, no partition
+      q.n_out = 3;
+      q.nparts = 0;
+      q.semi_kbits = nullptr;
       progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // packed accumulators: hits + sum 0 in word 1, sum 1 (float) alone
