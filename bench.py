@@ -246,7 +246,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-block", action="store_true", help="skip the block-codec e2e config")
     ap.add_argument("--no-semijoin", action="store_true")
-    ap.add_argument("--budget-gb", type=float, default=2.0,
+    ap.add_argument("--budget-gb", type=float, default=4.0,
                     help="plan memory_budget_bytes of the out-of-core e2e config (0: skip)")
     ap.add_argument("--io-threads", type=int, default=0)
     ap.add_argument("--batch-mb", type=int, default=0,
@@ -374,6 +374,7 @@ def main():
         out = {"value": round(e2e_s, 4) if e2e_s else None, "unit": "s",
                "h2d_bytes_per_step": int(reduce(float(h2d), "sum")), "d2h_bytes_per_step": int(reduce(float(d2h), "sum")),
                "steps": steps, "io_wait_s": round(reduce(last.stats["io_wait_s"]), 4),
+               "peak_device_bytes": int(reduce(float(last.stats["peak_bytes"]))),
                "path": "psg_execute_plan: PSTO files (%s, warm page cache) -> pinned -> HBM -> rows to host" % tag}
         out["ingest_gbs"] = round(out["h2d_bytes_per_step"] / 1e9 / e2e_s, 2) if e2e_s else None
         return out, parity, h2d, e2e_s

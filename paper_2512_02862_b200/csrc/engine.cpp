@@ -1661,12 +1661,25 @@ void Execution::finalize_global(ResultRows& out) {
 }
 
 // ---------------------------------------------------------------------------------- run
+/// Scope of a plan memory budget on the device pool: cleared on every exit path (a failed
+/// budgeted query must not leave its budget on the context for the next one).
+struct BudgetScope {
+  DevicePool& pool;
+  bool on;
+  BudgetScope(DevicePool& p, uint64_t budget) : pool(p), on(budget != 0) {
+    if (on) pool.set_budget(pool.used() + budget);
+  }
+  ~BudgetScope() {
+    if (on) pool.set_budget(0);
+  }
+};
+
 ResultRows Execution::run(bool want_rows) {
   const auto t0 = Clock::now();
   launches0_ = kernel_launch_count();
   jit0_ = jit_stats().compiles;
   ctx_.pool.reset_peak();
-  if (plan_.memory_budget_bytes) ctx_.pool.set_budget(ctx_.pool.used() + plan_.memory_budget_bytes);
+  BudgetScope budget_scope(ctx_.pool, plan_.memory_budget_bytes);
   PSG_TRACE_MSG("run: compile");
   cudaEvent_t ev0, ev1;
   PSG_CUDA(cudaEventCreate(&ev0));
@@ -2504,7 +2517,6 @@ ResultRows Execution::run(bool want_rows) {
   st_.peak_bytes = ctx_.pool.peak();
   st_.kernel_launches = kernel_launch_count() - launches0_;
   out.stats = st_;
-  if (plan_.memory_budget_bytes) ctx_.pool.set_budget(0);
   return out;
 }
 
@@ -2519,7 +2531,7 @@ ResultRows Execution::run_local() {
   launches0_ = kernel_launch_count();
   jit0_ = jit_stats().compiles;
   ctx_.pool.reset_peak();
-  if (plan_.memory_budget_bytes) ctx_.pool.set_budget(ctx_.pool.used() + plan_.memory_budget_bytes);
+  BudgetScope budget_scope(ctx_.pool, plan_.memory_budget_bytes);
   cudaEvent_t ev0, ev1;
   PSG_CUDA(cudaEventCreate(&ev0));
   PSG_CUDA(cudaEventCreate(&ev1));
@@ -2640,7 +2652,6 @@ ResultRows Execution::run_local() {
   st_.peak_bytes = ctx_.pool.peak();
   st_.kernel_launches = kernel_launch_count() - launches0_;
   out.stats = st_;
-  if (plan_.memory_budget_bytes) ctx_.pool.set_budget(0);
   return out;
 }
 

@@ -759,14 +759,38 @@ __global__ void __launch_bounds__(512) k_bucket_count(AggTableDev t, BucketDev b
   if (threadIdx.x == 0) counts[bucket] = s_total;
 }
 
+/// Shared-memory fold of one bucket: hits[i] (u32) and, per probe sum k, the 64-bit sum of the
+/// offset-encoded fields as two u32 words (lo with carry into hi: native 32-bit shared atomics; a
+/// 64-bit shared atomicAdd compiles to a CAS loop). sum_k = fields + hits * bkt_min[k] (mod 2^64).
+struct BucketSmem {
+  uint32_t* hits;
+  uint32_t* lo;  // [nps][kBucketSlots]
+  uint32_t* hi;
+  uint16_t* pos;
+};
+__device__ __forceinline__ BucketSmem bucket_smem(unsigned char* base, int nps) {
+  BucketSmem m;
+  m.hits = reinterpret_cast<uint32_t*>(base);
+  m.lo = m.hits + kBucketSlots;
+  m.hi = m.lo + nps * kBucketSlots;
+  m.pos = reinterpret_cast<uint16_t*>(m.hi + nps * kBucketSlots);
+  return m;
+}
+__device__ __forceinline__ void add64_u32pair(uint32_t* lo, uint32_t* hi, uint64_t v) {
+  const uint32_t vl = static_cast<uint32_t>(v), vh = static_cast<uint32_t>(v >> 32);
+  const uint32_t old = atomicAdd(lo, vl);
+  const uint32_t carry = (old + vl) < old ? 1u : 0u;
+  if (vh + carry) atomicAdd(hi, vh + carry);
+}
+
 __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b, uint64_t nslots, uint64_t nwords,
                                                      const uint32_t* offsets, const uint32_t* first_word, int nc,
                                                      EmitCols ec, uint64_t* out) {
-  extern __shared__ unsigned long long acc[];  // [nacc][kBucketSlots], then uint16 pos[kBucketSlots]
-  const int nacc = b.nacc;
-  uint16_t* pos = reinterpret_cast<uint16_t*>(acc + nacc * kBucketSlots);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nps = t.nps;
+  const BucketSmem m = bucket_smem(smem_raw, nps);
   __shared__ uint32_t s_warp[16];
-  for (int i = threadIdx.x; i < nacc * kBucketSlots; i += blockDim.x) acc[i] = 0;
+  for (int i = threadIdx.x; i < (1 + 2 * nps) * kBucketSlots; i += blockDim.x) m.hits[i] = 0;
   __syncthreads();
   const uint64_t bucket = blockIdx.x, s0 = bucket << kBucketBits;
   const uint64_t s_end = min(s0 + kBucketSlots, nslots);
@@ -775,35 +799,32 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
   for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
     const uint64_t w = __ldcs(reinterpret_cast<const unsigned long long*>(e + i));
     const uint32_t sl = static_cast<uint32_t>(w & (kBucketSlots - 1));
-    unsigned long long inc = 1ULL;
-    for (int k = 0; k < t.nps; ++k) {
-      const uint64_t v = bucket_value(b, w, k);
-      if (t.npacked && t.packed_shift[k] >= 0)
-        inc += (v - static_cast<uint64_t>(t.packed_min[k])) << t.packed_shift[k];
-      else
-        atomicAdd(&acc[b.word[k] * kBucketSlots + sl], static_cast<unsigned long long>(v));
-    }
-    atomicAdd(&acc[sl], inc);
+    atomicAdd(&m.hits[sl], 1u);
+    for (int k = 0; k < nps; ++k) add64_u32pair(&m.lo[k * kBucketSlots + sl], &m.hi[k * kBucketSlots + sl], (w >> b.shift[k]) & b.mask[k]);
   }
   __syncthreads();
-  if (fill > b.cap)  // overflowed bucket: fold in the direct updates of its slots
+  if (fill > b.cap)  // overflowed bucket: fold in the direct (hot-table) updates of its slots
     for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) {
       const uint64_t s = s0 + i;
       if (s >= s_end) break;
       const uint64_t* h = t.hot + s * t.hw;
-      for (int j = 0; j < nacc; ++j) acc[j * kBucketSlots + i] += h[1 + j];
+      const uint64_t hits = agg_hits(t, h);
+      if (!hits) continue;
+      m.hits[i] += static_cast<uint32_t>(hits);
+      for (int k = 0; k < nps; ++k) {
+        const uint64_t f = agg_psum(t, h, k, hits) - hits * static_cast<uint64_t>(b.min[k]);  // as offset fields
+        const uint64_t cur = (static_cast<uint64_t>(m.hi[k * kBucketSlots + i]) << 32) | m.lo[k * kBucketSlots + i];
+        const uint64_t nv = cur + f;
+        m.lo[k * kBucketSlots + i] = static_cast<uint32_t>(nv);
+        m.hi[k * kBucketSlots + i] = static_cast<uint32_t>(nv >> 32);
+      }
     }
   __syncthreads();
   // exclusive prefix of "slot has hits" over the bucket (8 consecutive slots per thread)
-  const int per = kBucketSlots / 512, base = threadIdx.x * per;
-  uint32_t local[kBucketSlots / 512];
+  constexpr int per = kBucketSlots / 512;
+  const int base = threadIdx.x * per;
   uint32_t run = 0;
-  for (int k = 0; k < per; ++k) {
-    const uint64_t a = acc[base + k];
-    const uint64_t hts = t.npacked ? (a & t.hits_mask) : a;
-    local[k] = run;
-    run += (hts != 0 && s0 + base + k < s_end) ? 1u : 0u;
-  }
+  for (int k = 0; k < per; ++k) run += (m.hits[base + k] != 0 && s0 + base + k < s_end) ? 1u : 0u;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t incl = run;
   for (int o = 1; o < 32; o <<= 1) {
@@ -812,62 +833,48 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
   }
   if (lane == 31) s_warp[wid] = incl;
   __syncthreads();
-  uint32_t wbase = 0;
-  for (int w = 0; w < wid; ++w) wbase += s_warp[w];
-  const uint32_t excl = wbase + incl - run;
-  for (int k = 0; k < per; ++k) pos[base + k] = static_cast<uint16_t>(excl + local[k]);
+  uint32_t acc = incl - run;
+  for (int w = 0; w < wid; ++w) acc += s_warp[w];
+  for (int k = 0; k < per; ++k) {
+    m.pos[base + k] = static_cast<uint16_t>(acc);
+    acc += (m.hits[base + k] != 0 && s0 + base + k < s_end) ? 1u : 0u;
+  }
   __syncthreads();
   // rows in key order: walk the key-bitmap words covering the bucket's slots
-  const uint64_t w0 = first_word[bucket];
   const unsigned long long* bits = reinterpret_cast<const unsigned long long*>(t.kbits);
   const uint64_t obase = offsets[bucket];
-  const bool st32 = (nc & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
-  for (uint64_t w = w0 + threadIdx.x; w < nwords; w += blockDim.x) {
+  const bool st32 = nc == 4 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
+  for (uint64_t w = first_word[bucket] + threadIdx.x; w < nwords; w += blockDim.x) {
     uint64_t s = t.krank[w];
     if (s >= s_end) break;
-    unsigned long long m = bits[w];
-    while (m) {
-      const int bit = __ffsll(static_cast<long long>(m)) - 1;
-      m &= m - 1;
+    unsigned long long mb = bits[w];
+    while (mb) {
+      const int bit = __ffsll(static_cast<long long>(mb)) - 1;
+      mb &= mb - 1;
       const uint64_t slot = s++;
       if (slot < s0) continue;
       if (slot >= s_end) break;
       const int i = static_cast<int>(slot - s0);
-      uint64_t h[2 + kMaxSums];
-      h[0] = static_cast<uint64_t>(t.kmin) + (w << 6) + bit;
-      for (int j = 0; j < nacc; ++j) h[1 + j] = acc[j * kBucketSlots + i];
-      const uint64_t hits = t.npacked ? (h[1] & t.hits_mask) : h[1];
+      const uint64_t hits = m.hits[i];
       if (!hits) continue;
-      const uint64_t* c = t.cold + slot * t.cw;
-      uint64_t vals[2 * kMaxSums + 2];
-#pragma unroll
-      for (int k = 0; k < 2 * kMaxSums + 2; ++k) {
-        if (k >= nc) break;
+      const uint64_t key = static_cast<uint64_t>(t.kmin) + (w << 6) + bit;
+      auto col = [&](int k) -> uint64_t {
         const int kind = ec.kind[k], j = ec.idx[k];
-        uint64_t v;
-        if (kind == 0) v = h[0];
-        else if (kind == 1) v = hits;  // unique build keys: multiplicity 1
-        else if (kind == 2) v = agg_psum(t, h, j, hits);
-        else
-          v = t.bs_float[j] ? static_cast<uint64_t>(__double_as_longlong(
-                                  static_cast<double>(hits) * __longlong_as_double(static_cast<long long>(c[1 + j]))))
-                            : hits * c[1 + j];
-        vals[k] = v;
-      }
-      uint64_t* row = out + (obase + pos[i]) * nc;
-      if (st32) {
-#pragma unroll
-        for (int k = 0; k < 2 * kMaxSums + 2; k += 4) {
-          if (k >= nc) break;
-          st256(row + k, vals[k], vals[k + 1], vals[k + 2], vals[k + 3]);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 2 * kMaxSums + 2; ++k) {
-          if (k >= nc) break;
-          row[k] = vals[k];
-        }
-      }
+        if (kind == 0) return key;
+        if (kind == 1) return hits;  // unique build keys: multiplicity 1
+        if (kind == 2)
+          return ((static_cast<uint64_t>(m.hi[j * kBucketSlots + i]) << 32) | m.lo[j * kBucketSlots + i]) +
+                 hits * static_cast<uint64_t>(b.min[j]);
+        const uint64_t c = t.cold[slot * t.cw + 1 + j];
+        return t.bs_float[j] ? static_cast<uint64_t>(__double_as_longlong(
+                                   static_cast<double>(hits) * __longlong_as_double(static_cast<long long>(c))))
+                             : hits * c;
+      };
+      uint64_t* row = out + (obase + m.pos[i]) * nc;
+      if (st32)
+        st256(row, col(0), col(1), col(2), col(3));
+      else
+        for (int k = 0; k < nc; ++k) row[k] = col(k);
     }
   }
 }
@@ -890,10 +897,10 @@ void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuck
     ec.kind[k] = col_kind[k];
     ec.idx[k] = col_idx[k];
   }
-  const int smem = b.nacc * kBucketSlots * 8 + kBucketSlots * 2;
+  const int smem = (1 + 2 * t.nps) * kBucketSlots * 4 + kBucketSlots * 2;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_bucket_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * kBucketSlots * 8 + kBucketSlots * 2);
+    cudaFuncSetAttribute(k_bucket_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (1 + 2 * 3) * kBucketSlots * 4 + kBucketSlots * 2);
     attr = true;
   }
   count_launch();
