@@ -124,6 +124,38 @@ int psg_pack_plan(const int64_t* lo, const int64_t* hi, int ncols, int64_t* min,
                   int* fits);
 int psg_partition_of(const int64_t* keys, uint64_t n, uint32_t nparts, uint32_t* out);
 
+/* ---- distributed-join microbenchmark (run_join / run_sim_join, join.cpp:55-124, join_harness.cpp:43-97) ----
+ * The symmetric-repartitioning hash join in the reference's four schedules on CUDA streams:
+ * variant 0 blocking (whole tables, one stream, a cudaMalloc per buffer), 1 blocking-opt (pooled),
+ * 2 chunking, 3 deferred (the probe of wave w is issued after wave w+k's shuffle). */
+typedef struct psg_join_spec {
+  int variant;           /* JoinVariant (join.hpp:31) */
+  int stream_count;      /* compute streams of the chunked variants (join.hpp:42) */
+  uint64_t chunk_rows;   /* wave size (join.hpp:40) */
+} psg_join_spec;
+typedef struct psg_join_workload { /* SyntheticJoinSpec (workload.hpp:27-33) */
+  uint64_t build_rows, probe_rows;
+  int payload_cols;
+  double hit_ratio;
+  uint64_t seed;
+} psg_join_workload;
+typedef struct psg_join_stats {
+  double runtime_s;       /* host wall time of the join (inputs in host memory, H2D included) */
+  double device_ms;       /* CUDA-event time, first to last step */
+  uint64_t result_rows;   /* this rank's joined rows */
+  uint64_t bytes_received;/* shuffle payload bytes from peers */
+  uint64_t left_waves, right_waves;
+  uint64_t host_syncs;    /* data-dependent waits of the control thread */
+} psg_join_stats;
+/* Host-only: the schedule (PlanStep list, join.hpp:70-95) as triples {phase, stream, wave};
+ * phases in PlanStep::Phase order (concat_left=0 ... drain=10). */
+int psg_join_schedule(int variant, int stream_count, int left_waves, int right_waves, int32_t* out, size_t cap_steps,
+                      size_t* nsteps);
+/* Runs this rank's part of the join over its slice (slice_for_node) of the synthetic workload;
+ * rows (optional, collect) = build payload ++ probe columns per joined row. */
+int psg_run_synthetic_join(psg_ctx* ctx, const psg_join_spec* spec, const psg_join_workload* workload, int collect_rows,
+                           psg_join_stats* stats, psg_result** rows);
+
 /* Host-only: parses + validates a plan like QueryPlan::from_json_text (pipeline.cpp:108-156,
  * validate :178-196) for node `node` of `nodes` and writes the resolved scans as JSON
  * {"scans":[{"table","replicated","paths":[...]}],"shuffle":id|null} into out (NUL-terminated,

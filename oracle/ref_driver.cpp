@@ -25,6 +25,8 @@
 #include "pystachio/bench.hpp"
 #include "pystachio/hashing.hpp"
 #include "pystachio/pipeline_harness.hpp"
+#include "pystachio/join.hpp"
+#include "pystachio/join_harness.hpp"
 #include "pystachio/pipeline.hpp"
 #include "pystachio/psto.hpp"
 #include "pystachio/scan.hpp"
@@ -216,6 +218,43 @@ int main(int argc, char** argv) {
         summarize(out, 1 + sums.size(), s, {out.size()}, std::string());
         std::fflush(stdout);
       }
+      return 0;
+    }
+    if (cmd == "joinplan") {
+      // make_plan (join.cpp:126-134): the schedule as [[phase, stream, wave], ...]
+      JoinSpec spec;
+      spec.variant = join_variant_from_string(arg(argc, argv, "--variant", "deferred"));
+      spec.stream_count = std::stoi(arg(argc, argv, "--streams", "2"));
+      const int lw = std::stoi(arg(argc, argv, "--left", "1")), rw = std::stoi(arg(argc, argv, "--right", "1"));
+      const SchedulePlan p = make_plan(spec, lw, rw);
+      std::printf("[");
+      for (std::size_t i = 0; i < p.steps.size(); ++i)
+        std::printf("%s[%d, %d, %d]", i ? ", " : "", static_cast<int>(p.steps[i].phase), p.steps[i].stream,
+                    p.steps[i].wave);
+      std::printf("]\n");
+      return 0;
+    }
+    if (cmd == "join") {
+      // run_sim_join (join_harness.cpp:43-97): every node of the distributed join, rows collected
+      SimJoinOptions opts;
+      opts.spec.variant = join_variant_from_string(arg(argc, argv, "--variant", "deferred"));
+      opts.spec.build_key = "bk";  // the synthetic workload's key columns (workload.cpp:44,57)
+      opts.spec.probe_key = "pk";
+      opts.spec.node_count = std::stoi(arg(argc, argv, "--nodes", "2"));
+      opts.spec.stream_count = std::stoi(arg(argc, argv, "--streams", "2"));
+      opts.spec.chunk_rows = std::stoull(arg(argc, argv, "--chunk-rows", "32768"));
+      opts.workload.build_rows = std::stoull(arg(argc, argv, "--build-rows", "120000"));
+      opts.workload.probe_rows = std::stoull(arg(argc, argv, "--probe-rows", "320000"));
+      opts.workload.payload_cols = std::stoi(arg(argc, argv, "--payload", "3"));
+      opts.workload.hit_ratio = std::stod(arg(argc, argv, "--hit-ratio", "0.5"));
+      opts.workload.seed = std::stoull(arg(argc, argv, "--seed", "42"));
+      const auto t0 = std::chrono::steady_clock::now();
+      SimJoinOutcome out = run_sim_join(opts);
+      const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      std::vector<std::size_t> per_node;
+      for (const auto& st : out.per_node) per_node.push_back(st.result_rows);
+      const std::size_t ncols = out.rows.empty() ? 0 : out.rows[0].size();
+      summarize(out.rows, ncols, s, per_node, std::string());
       return 0;
     }
     if (cmd == "plan") {

@@ -37,7 +37,7 @@ EXPORTS = ["psg_abi_version", "psg_last_error", "psg_ctx_create", "psg_comm_uniq
            "psg_concat", "psg_codec_decompress", "psg_psto_write",
            "psg_psto_inspect", "psg_gen_tpch", "psg_gen_synthetic", "psg_jit_selftest", "psg_tmin",
            "psg_plan_resolve", "psg_result_checksum", "psg_ingest_probe",
-           "psg_shuffle_plan", "psg_pack_plan", "psg_partition_of"]
+           "psg_shuffle_plan", "psg_pack_plan", "psg_partition_of", "psg_join_schedule", "psg_run_synthetic_join"]
 
 
 class PsgError(RuntimeError):
@@ -59,6 +59,27 @@ class Stats(ctypes.Structure):
                 ("device_ms", ctypes.c_double), ("result_rows", ctypes.c_uint64), ("io_wait_s", ctypes.c_double),
                 ("jit_compiles", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
                 ("agg_table", ctypes.c_uint64), ("bytes_sent", ctypes.c_uint64), ("exchange_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+JOIN_VARIANTS = {"blocking": 0, "blocking-opt": 1, "chunking": 2, "deferred": 3}
+
+
+class JoinSpec(ctypes.Structure):
+    _fields_ = [("variant", ctypes.c_int), ("stream_count", ctypes.c_int), ("chunk_rows", ctypes.c_uint64)]
+
+
+class JoinWorkload(ctypes.Structure):
+    _fields_ = [("build_rows", ctypes.c_uint64), ("probe_rows", ctypes.c_uint64), ("payload_cols", ctypes.c_int),
+                ("hit_ratio", ctypes.c_double), ("seed", ctypes.c_uint64)]
+
+
+class JoinStats(ctypes.Structure):
+    _fields_ = [("runtime_s", ctypes.c_double), ("device_ms", ctypes.c_double), ("result_rows", ctypes.c_uint64),
+                ("bytes_received", ctypes.c_uint64), ("left_waves", ctypes.c_uint64), ("right_waves", ctypes.c_uint64),
+                ("host_syncs", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -118,6 +139,8 @@ def lib():
             "psg_tmin": ([u64, ctypes.c_double, u64, ctypes.c_double], ctypes.c_double),
             "psg_jit_selftest": ([ctypes.c_char_p, ctypes.c_size_t], i32),
             "psg_ingest_probe": ([vp, c, c, P(Stats)], i32),
+            "psg_join_schedule": ([i32, i32, i32, i32, P(ctypes.c_int32), ctypes.c_size_t, P(ctypes.c_size_t)], i32),
+            "psg_run_synthetic_join": ([vp, P(JoinSpec), P(JoinWorkload), i32, P(JoinStats), P(vp)], i32),
             "psg_shuffle_plan": ([P(u64), i32, i32, P(u64), P(u64), P(u64), P(u64)], i32),
             "psg_pack_plan": ([P(ctypes.c_int64), P(ctypes.c_int64), i32, P(ctypes.c_int64), P(i32), P(u64), P(i32)], i32),
             "psg_partition_of": ([P(ctypes.c_int64), u64, ctypes.c_uint32, P(ctypes.c_uint32)], i32),
@@ -135,6 +158,16 @@ def lib():
 def _check(rc):
     if rc != 0:
         raise PsgError(rc, lib().psg_last_error().decode(errors="replace"))
+
+
+def join_schedule(variant, stream_count, left_waves, right_waves):
+    """The join schedule [(phase, stream, wave)] (PlanStep list of make_plan, join.cpp:126-134)."""
+    n = ctypes.c_size_t()
+    v = JOIN_VARIANTS[variant] if isinstance(variant, str) else variant
+    _check(lib().psg_join_schedule(v, stream_count, left_waves, right_waves, None, 0, ctypes.byref(n)))
+    buf = (ctypes.c_int32 * (3 * max(n.value, 1)))()
+    _check(lib().psg_join_schedule(v, stream_count, left_waves, right_waves, buf, n.value, ctypes.byref(n)))
+    return [[buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]] for i in range(n.value)]
 
 
 def shuffle_plan(matrix, me):
@@ -337,6 +370,18 @@ class Context:
         out = ctypes.c_void_p()
         _check(lib().psg_execute_local(self._h, text.encode(), data_root.encode(), MODES[mode], ctypes.byref(out)))
         return Result(out)
+
+    def run_synthetic_join(self, variant="deferred", stream_count=2, chunk_rows=32 * 1024, build_rows=120_000,
+                           probe_rows=320_000, payload_cols=3, hit_ratio=0.5, seed=42, collect_rows=True):
+        """run_join (join.cpp) over this rank's slice of the synthetic join workload
+        (SyntheticJoinSpec, workload.hpp:27-33). Returns (stats dict, Result or None)."""
+        spec = JoinSpec(JOIN_VARIANTS[variant] if isinstance(variant, str) else variant, stream_count, chunk_rows)
+        wl = JoinWorkload(build_rows, probe_rows, payload_cols, hit_ratio, seed)
+        st = JoinStats()
+        out = ctypes.c_void_p()
+        _check(lib().psg_run_synthetic_join(self._h, ctypes.byref(spec), ctypes.byref(wl), 1 if collect_rows else 0,
+                                            ctypes.byref(st), ctypes.byref(out) if collect_rows else None))
+        return st.as_dict(), (Result(out) if collect_rows else None)
 
     def ingest_probe(self, plan, data_root) -> dict:
         """The plan's storage -> pinned -> HBM ingest alone (same session as execute_plan, no query

@@ -142,6 +142,62 @@ int psg_partition_of(const int64_t* keys, uint64_t n, uint32_t nparts, uint32_t*
   });
 }
 
+int psg_join_schedule(int variant, int stream_count, int left_waves, int right_waves, int32_t* out, size_t cap_steps,
+                      size_t* nsteps) {
+  return guarded([&] {
+    if (variant < 0 || variant > kJoinDeferred) throw InvalidInput("unknown join variant");
+    if (stream_count < 1 || left_waves < 0 || right_waves < 0) throw InvalidInput("bad schedule shape");
+    const auto steps = join_schedule(variant, stream_count, left_waves, right_waves);
+    if (nsteps) *nsteps = steps.size();
+    for (size_t i = 0; i < steps.size() && i < cap_steps && out; ++i) {
+      out[3 * i] = static_cast<int32_t>(steps[i].phase);
+      out[3 * i + 1] = steps[i].stream;
+      out[3 * i + 2] = steps[i].wave;
+    }
+  });
+}
+
+int psg_run_synthetic_join(psg_ctx* ctx, const psg_join_spec* spec, const psg_join_workload* workload, int collect_rows,
+                           psg_join_stats* stats, psg_result** rows) {
+  return guarded([&] {
+    if (!ctx || !spec || !workload) throw InvalidInput("null argument");
+    HostTable build, probe;
+    synthetic_join_tables(workload->seed, workload->build_rows, workload->probe_rows, workload->payload_cols,
+                          workload->hit_ratio, ctx->c.rank, ctx->c.nranks, build, probe);
+    JoinSpecC js;
+    js.variant = spec->variant;
+    js.stream_count = spec->stream_count;
+    js.chunk_rows = spec->chunk_rows;
+    JoinOutcome o = run_join(ctx->c, js, build, probe, collect_rows != 0 && rows != nullptr);
+    if (stats) {
+      stats->runtime_s = o.runtime_s;
+      stats->device_ms = o.device_ms;
+      stats->result_rows = o.result_rows;
+      stats->bytes_received = o.bytes_received;
+      stats->left_waves = o.left_waves;
+      stats->right_waves = o.right_waves;
+      stats->host_syncs = o.host_syncs;
+    }
+    if (rows) {
+      auto r = std::make_unique<psg_result>();
+      // build payload ++ probe columns, "_p" on a name clash (ops.cpp:193-200)
+      for (size_t c = 1; c < build.names.size(); ++c) r->r.schema.fields.push_back(Field{build.names[c], LType::Int64});
+      for (const auto& nm : probe.names) {
+        Field f{nm, LType::Int64};
+        if (r->r.schema.index_of(f.name)) f.name += "_p";
+        r->r.schema.fields.push_back(f);
+      }
+      const size_t nc = r->r.schema.size();
+      const uint64_t n = o.cols.empty() ? 0 : o.cols[0].size();
+      r->r.nrows = n;
+      uint64_t* w = r->r.mutable_rows(n * nc);
+      for (size_t c = 0; c < nc && !o.cols.empty(); ++c)
+        for (uint64_t i = 0; i < n; ++i) w[i * nc + c] = o.cols[c][i];
+      *rows = r.release();
+    }
+  });
+}
+
 int psg_plan_resolve(const char* plan_json, const char* data_root, int node, int nodes, char* out, size_t cap,
                      size_t* needed) {
   return guarded([&] {

@@ -291,6 +291,41 @@ HostBatch op_concat(Ctx& ctx, const std::vector<HostBatch>& batches);
 HostBatch op_hash_join(Ctx& ctx, const HostBatch& build, const std::string& build_key, const HostBatch& probe,
                        const std::string& probe_key);
 
+// ------------------------------------------------------------ distributed-join microbenchmark
+/// JoinVariant (join.hpp:31): blocking, blocking-opt, chunking, deferred.
+constexpr int kJoinBlocking = 0, kJoinBlockingOpt = 1, kJoinChunking = 2, kJoinDeferred = 3;
+/// One schedule step (PlanStep, join.hpp:70-87): phase, stream (== stream count: the dedicated
+/// build stream), wave (-1: none).
+struct JoinStep {
+  enum class Phase { ConcatLeft, PartitionLeft, SizesLeft, ShuffleLeft, Build, ConcatRight, PartitionRight, SizesRight,
+                     ShuffleRight, Probe, Drain };
+  Phase phase;
+  int stream;
+  int wave;
+};
+std::vector<JoinStep> join_schedule(int variant, int streams, int left_waves, int right_waves);
+struct JoinSpecC {
+  int variant = kJoinDeferred;
+  int stream_count = 2;
+  uint64_t chunk_rows = 32 * 1024;
+};
+/// Host columns of one node's input (key column first).
+struct HostTable {
+  std::vector<std::string> names;
+  std::vector<std::vector<uint64_t>> cols;
+  uint64_t rows() const { return cols.empty() ? 0 : cols[0].size(); }
+};
+struct JoinOutcome {
+  double runtime_s = 0, device_ms = 0;
+  uint64_t result_rows = 0, bytes_received = 0, left_waves = 0, right_waves = 0, host_syncs = 0;
+  std::vector<std::vector<uint64_t>> cols;  // collected result columns (build payload ++ probe)
+};
+JoinOutcome run_join(Ctx& ctx, const JoinSpecC& spec, const HostTable& build, const HostTable& probe, bool collect);
+/// gen_build_table / gen_probe_table (workload.cpp:41-71) of the synthetic join workload, this
+/// node's slice (slice_for_node, workload.cpp:73-87).
+void synthetic_join_tables(uint64_t seed, uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio,
+                           int node, int nodes, HostTable& build, HostTable& probe);
+
 void gen_synthetic(const std::string& out_dir, int nodes, int devices, uint64_t seed, Codec codec, uint64_t rg_bytes,
                    uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio);
 void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, uint64_t seed, Codec codec,

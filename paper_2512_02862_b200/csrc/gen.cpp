@@ -21,6 +21,7 @@
 #include <fstream>
 #include <json.hpp>
 
+#include "engine.hpp"
 #include "psto.hpp"
 
 namespace psg {
@@ -285,19 +286,13 @@ void gen_tpch(const std::string& out_dir, double scale, int nodes, int devices, 
 /// same calls in the same order give byte-identical tables (pinned against the reference's own
 /// generator, tests/test_abi.py). Tables are sliced round-robin per node (slice_for_node,
 /// workload.cpp:73-87) and written like write_sharded (bench.cpp:48-65).
-void gen_synthetic(const std::string& out_dir, int nodes, int devices, uint64_t seed, Codec codec, uint64_t rg_bytes,
-                   uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio) {
-  if (nodes < 1 || devices < 1) throw InvalidInput("devices and nodes must be >= 1");
-  if (payload_cols < 0 || payload_cols > 14) throw InvalidInput("payload_cols out of range");
-  namespace fs = std::filesystem;
-  fs::create_directories(out_dir);
+namespace {
+/// gen_build_table / gen_probe_table (workload.cpp:41-71): build keys 0..n-1 shuffled, probe keys a
+/// hit_ratio share drawn from the build range and the rest from a miss range; payload columns of
+/// values < 1e9 (payload_columns, workload.cpp:29-37).
+void synthetic_columns(uint64_t seed, uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio,
+                       std::vector<std::vector<uint64_t>>& bcols, std::vector<std::vector<uint64_t>>& pcols) {
   const uint64_t mul = 2654435761u;
-  auto side = [&](const char* key, const char* pre) {
-    Schema sc;
-    sc.fields.push_back(Field{key, LType::Int64});
-    for (int i = 0; i < payload_cols; ++i) sc.fields.push_back(Field{pre + std::to_string(i), LType::Int64});
-    return sc;
-  };
   auto payload = [&](std::mt19937_64& rng, uint64_t rows, std::vector<std::vector<uint64_t>>& cols) {
     for (int c = 0; c < payload_cols; ++c) {
       std::vector<uint64_t> v(rows);
@@ -305,8 +300,6 @@ void gen_synthetic(const std::string& out_dir, int nodes, int devices, uint64_t 
       cols.push_back(std::move(v));
     }
   };
-  // build side: keys 0..n-1 shuffled, then payload
-  std::vector<std::vector<uint64_t>> bcols;
   {
     std::mt19937_64 rng(seed * mul + 1);
     std::vector<int64_t> keys(build_rows);
@@ -315,8 +308,6 @@ void gen_synthetic(const std::string& out_dir, int nodes, int devices, uint64_t 
     bcols.emplace_back(keys.begin(), keys.end());
     payload(rng, build_rows, bcols);
   }
-  // probe side: a hit_ratio share of keys drawn from the build range, the rest from a miss range
-  std::vector<std::vector<uint64_t>> pcols;
   {
     std::mt19937_64 rng(seed * mul + 2);
     std::uniform_real_distribution<double> coin(0.0, 1.0);
@@ -330,6 +321,46 @@ void gen_synthetic(const std::string& out_dir, int nodes, int devices, uint64_t 
     pcols.push_back(std::move(keys));
     payload(rng, probe_rows, pcols);
   }
+}
+}  // namespace
+
+void synthetic_join_tables(uint64_t seed, uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio,
+                           int node, int nodes, HostTable& build, HostTable& probe) {
+  if (nodes < 1 || node < 0 || node >= nodes) throw InvalidInput("node out of range");
+  if (payload_cols < 0 || payload_cols > 14) throw InvalidInput("payload_cols out of range");
+  std::vector<std::vector<uint64_t>> bcols, pcols;
+  synthetic_columns(seed, build_rows, probe_rows, payload_cols, hit_ratio, bcols, pcols);
+  auto slice = [&](std::vector<std::vector<uint64_t>>& cols, HostTable& t, const char* key, const char* pre) {
+    t.names = {key};
+    for (int i = 0; i < payload_cols; ++i) t.names.push_back(pre + std::to_string(i));
+    t.cols.assign(cols.size(), {});
+    for (size_t c = 0; c < cols.size(); ++c) {
+      if (nodes == 1) {
+        t.cols[c] = std::move(cols[c]);
+        continue;
+      }
+      for (uint64_t r = static_cast<uint64_t>(node); r < cols[c].size(); r += static_cast<uint64_t>(nodes))
+        t.cols[c].push_back(cols[c][r]);
+    }
+  };
+  slice(bcols, build, "bk", "bp");
+  slice(pcols, probe, "pk", "pp");
+}
+
+void gen_synthetic(const std::string& out_dir, int nodes, int devices, uint64_t seed, Codec codec, uint64_t rg_bytes,
+                   uint64_t build_rows, uint64_t probe_rows, int payload_cols, double hit_ratio) {
+  if (nodes < 1 || devices < 1) throw InvalidInput("devices and nodes must be >= 1");
+  if (payload_cols < 0 || payload_cols > 14) throw InvalidInput("payload_cols out of range");
+  namespace fs = std::filesystem;
+  fs::create_directories(out_dir);
+  auto side = [&](const char* key, const char* pre) {
+    Schema sc;
+    sc.fields.push_back(Field{key, LType::Int64});
+    for (int i = 0; i < payload_cols; ++i) sc.fields.push_back(Field{pre + std::to_string(i), LType::Int64});
+    return sc;
+  };
+  std::vector<std::vector<uint64_t>> bcols, pcols;
+  synthetic_columns(seed, build_rows, probe_rows, payload_cols, hit_ratio, bcols, pcols);
   nlohmann::json m;
   m["nodes"] = nodes;
   m["devices"] = devices;
