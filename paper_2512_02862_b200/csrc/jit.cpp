@@ -289,7 +289,8 @@ void emit_semi_screen(std::ostringstream& s, const ScanProgram& P) {
 /// PSG_TMA_NG consumer groups of 8 warps (default 2), PSG_TMA_NS ring stages (6), PSG_TMA_CTAS
 /// CTAs per SM (2).
 struct StagedShape {
-  int groups, stages, ctas;
+  int groups, stages, ctas, rows;  // rows: per consumer lane per tile (4 or 8); 1024 / (32 rows) warps per group
+  int warps() const { return 1024 / (32 * rows); }
 };
 StagedShape staged_shape() {
   static const StagedShape sh = [] {
@@ -297,7 +298,8 @@ StagedShape staged_shape() {
       const char* e = std::getenv(n);
       return e ? std::max(1, std::atoi(e)) : d;
     };
-    return StagedShape{env("PSG_TMA_NG", 2), env("PSG_TMA_NS", 6), env("PSG_TMA_CTAS", 2)};
+    const int r = env("PSG_TMA_R", 4) >= 8 ? 8 : 4;
+    return StagedShape{env("PSG_TMA_NG", 2), env("PSG_TMA_NS", 6), env("PSG_TMA_CTAS", 2), r};
   }();
   return sh;
 }
@@ -642,8 +644,9 @@ std::string jit_source_staged(const ScanProgram& P) {
   std::ostringstream s;
   const StagedShape sh = staged_shape();
   const int NG = sh.groups, NS = std::max(sh.stages, NG), NE = P.n_early, NIN = P.n_in, nregs = std::max(1, P.n_regs);
-  const int NT = 32 * (1 + 8 * NG);
-  s << "using namespace psg;\n#define R 4\n"
+  const int CW = sh.warps();  // consumer warps per group (one tile each)
+  const int NT = 32 * (1 + CW * NG);
+  s << "using namespace psg;\n#define R " << sh.rows << "\n"
     << "extern \"C\" __global__ void __launch_bounds__(" << NT << ", " << sh.ctas
     << ") psg_jit_scan(const __grid_constant__ ScanProgram P, "
        "const Segment* __restrict__ segs, const uint32_t* __restrict__ tile_seg, uint64_t ntiles) {\n"
@@ -661,7 +664,7 @@ std::string jit_source_staged(const ScanProgram& P) {
       s << "  __shared__ unsigned long long s_part[" << kMaxParts << "];\n"
         << "  for (int i = tid; i < " << kMaxParts << "; i += " << NT << ") s_part[i] = 0;\n";
   }
-  s << "  if (tid == 0) {\n    for (int i = 0; i < " << NS << "; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], 8); }\n"
+  s << "  if (tid == 0) {\n    for (int i = 0; i < " << NS << "; ++i) { mbar_init(&full_bar[i], 1); mbar_init(&empty_bar[i], " << CW << "); }\n"
     << "    mbar_fence_init();\n  }\n  __syncthreads();\n"
     << "  const uint64_t per_cta = (ntiles + gridDim.x - 1) / gridDim.x;\n"
     << "  const uint64_t t_beg = blockIdx.x * per_cta;\n"
@@ -681,7 +684,7 @@ std::string jit_source_staged(const ScanProgram& P) {
     s << "        bulk_g2s(stg + (st * " << NE << " + " << c << ") * 1024, sg->col[" << c << "] + r0, bytes, &full_bar[st], pol_stream);\n";
   s << "      }\n    }\n    return;\n  }\n"
     << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep;\n"
-    << "  const int cw = (warp - 1) & 7, grp = (warp - 1) >> 3;\n  const int wrow = cw * (R * 32) + lane;\n";
+    << "  const int cw = (warp - 1) % " << CW << ", grp = (warp - 1) / " << CW << ";\n  const int wrow = cw * (R * 32) + lane;\n";
   if (mat) {
     s << "  int fill = 0;\n  auto flush = [&]() {\n    __syncwarp();\n    if (fill == 0) return;\n"
       << "    unsigned long long base = 0;\n    if (lane == 0) base = atomicAdd(P.out_count, static_cast<unsigned long long>(fill));\n"
@@ -738,8 +741,8 @@ std::string jit_source_staged(const ScanProgram& P) {
       << "      if (on && lane == __ffs(peers) - 1) atomicAdd(&s_part[d], static_cast<unsigned long long>(__popc(peers)));\n    }\n";
   s << "  }\n  flush();\n";
   if (part)
-    s << "  asm volatile(\"bar.sync 1, " << 32 * 8 * NG << ";\" ::: \"memory\");  // consumers only (the producer exited)\n"
-      << "  for (int i = tid - 32; i < P.nparts; i += " << 32 * 8 * NG << ") if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
+    s << "  asm volatile(\"bar.sync 1, " << 32 * CW * NG << ";\" ::: \"memory\");  // consumers only (the producer exited)\n"
+      << "  for (int i = tid - 32; i < P.nparts; i += " << 32 * CW * NG << ") if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
   s << "}\n";
   return s.str();
 }
@@ -843,9 +846,9 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
         int block = jit_block(P), smem = 0;
         if (staged_probe(P)) {
           const StagedShape sh = staged_shape();
-          block = 32 * (1 + 8 * sh.groups);
+          block = 32 * (1 + sh.warps() * sh.groups);
           smem = std::max(sh.stages, sh.groups) * P.n_early * 1024 * 8;
-          if (P.sink == SINK_MATERIALIZE) smem += 8 * sh.groups * P.n_out * 128 * 8;
+          if (P.sink == SINK_MATERIALIZE) smem += sh.warps() * sh.groups * P.n_out * 128 * 8;
         }
         it = g_cache.emplace(key, compile(body, dev, block, smem)).first;
       }

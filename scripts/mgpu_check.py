@@ -158,6 +158,39 @@ def main():
         if rank == 0:
             print("fuzz                   %d plans   oracle    %s (%d bad)" % (a.fuzz, "OK " if not nbad else "BAD", nbad),
                   flush=True)
+    # duplicate-key replicated joins (expanding chains) at N ranks vs the reference per node
+    for pname in ("dup_build_chain", "dup_probe_chain"):
+        d = data(0.01, 42, 1 << 20)
+        res = ctx.execute_plan(golden["plans"][pname], d)
+        allres = [None] * world
+        dist.all_gather_object(allres, (res.schema, res.rows.copy()))
+        if rank == 0:
+            got = po.summary(allres)
+            want = po.summary(po.execute(json.dumps(golden["plans"][pname]), d, world))
+            ok = got == want
+            print("%-22s dupkeys    oracle    %s rows=%d per_node=%s" % (pname, "OK " if ok else "BAD", got["rows"],
+                                                                         got["per_node_rows"]), flush=True)
+            if not ok:
+                failures.append((pname, "dupkeys", got, want))
+    # the distributed-join microbenchmark (run_join variants over NCCL): the union of the ranks'
+    # rows equals the reference's run_sim_join rows (tests/golden/join.json)
+    jg = json.load(open(os.path.join(ROOT, "tests", "golden", "join.json")))
+    for g in jg["joins"][:6]:
+        wl = g["workload"]
+        for variant in ("blocking", "blocking-opt", "chunking", "deferred"):
+            _st, res = ctx.run_synthetic_join(variant, 1 if variant.startswith("blocking") else 2, g["chunk_rows"],
+                                              wl["build_rows"], wl["probe_rows"], wl["payload"], wl["hit_ratio"],
+                                              wl["seed"])
+            allres = [None] * world
+            dist.all_gather_object(allres, (res.schema, res.rows.copy()))
+            if rank == 0:
+                got = po.summary(allres)
+                ok = (got["rows"], got["rowhash"], got["colsums"]) == (g["rows"], g["rowhash"], g["colsums"])
+                print("%-22s %-10s reference %s rows=%d per_node=%s" % ("join_%d" % wl["seed"], variant,
+                                                                       "OK " if ok else "BAD", got["rows"],
+                                                                       got["per_node_rows"]), flush=True)
+                if not ok:
+                    failures.append(("join", variant, wl, got))
     # synthetic-join workload (gen_workload kind=synthetic): per-node rows vs the reference
     syn = json.load(open(os.path.join(ROOT, "tests", "golden", "synthetic.json")))
     sdir = os.path.join(base, "syn")
