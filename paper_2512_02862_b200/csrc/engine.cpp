@@ -1341,8 +1341,9 @@ void Execution::apply_buckets(ScanProgram& p) const {
   }
 }
 
-/// Bucketed finalisation: groups per bucket -> exclusive scan -> rows written per bucket in key
-/// order (k_bucket_count, k_bucket_emit); the only host sync is the group total for the output.
+/// Bucketed finalisation: one kernel folds every bucket, finds its output offset by decoupled
+/// look-back and writes its rows in key order (k_bucket_emit); the group total (the last bucket's
+/// inclusive prefix) is read once at the end, when the rows go to the host.
 void Execution::finalize_buckets(ResultRows& out, bool want_rows) {
   const int nc = static_cast<int>(result_schema_.size());
   std::vector<int32_t> kind, idx;
@@ -1352,25 +1353,23 @@ void Execution::finalize_buckets(ResultRows& out, bool want_rows) {
     kind.push_back(side == 1 ? 2 : 3);
     idx.push_back(k);
   }
-  DevBuf counts(ctx_.pool, (nbuckets_ + 1) * 4, ctx_.compute), offs(ctx_.pool, (nbuckets_ + 1) * 4, ctx_.compute);
-  PSG_CUDA(cudaMemsetAsync(counts.p, 0, (nbuckets_ + 1) * 4, ctx_.compute));
-  launch_bucket_count(aggt_, bd_, nbuckets_, agg_cap_, counts.as<uint32_t>(), ctx_.compute);
-  const size_t tb = exclusive_scan_u32(nullptr, nullptr, nbuckets_ + 1, nullptr, 0, ctx_.compute);
-  DevBuf tmp(ctx_.pool, std::max<size_t>(tb, 8), ctx_.compute);
-  exclusive_scan_u32(counts.as<uint32_t>(), offs.as<uint32_t>(), nbuckets_ + 1, tmp.p, tb, ctx_.compute);
-  uint32_t ng = 0;
-  PSG_CUDA(cudaMemcpyAsync(&ng, offs.as<uint32_t>() + nbuckets_, 4, cudaMemcpyDeviceToHost, ctx_.compute));
-  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
-  DevBuf rows(ctx_.pool, std::max<uint64_t>(ng, 1) * nc * 8, ctx_.compute);
+  // rows are written at their final offsets: size the output for the upper bound (one group per
+  // build key) instead of syncing on the count
+  DevBuf state(ctx_.pool, nbuckets_ * 8, ctx_.compute), ticket(ctx_.pool, 8, ctx_.compute);
   DevBuf first_word(ctx_.pool, nbuckets_ * 4, ctx_.compute);
-  if (ng)
-    launch_bucket_emit(aggt_, bd_, nbuckets_, agg_cap_, offs.as<uint32_t>(), first_word.as<uint32_t>(), nc, kind.data(),
-                       idx.data(), rows.as<uint64_t>(), ctx_.compute);
+  DevBuf rows(ctx_.pool, std::max<uint64_t>(agg_cap_, 1) * nc * 8, ctx_.compute);
+  launch_bucket_emit(aggt_, bd_, nbuckets_, agg_cap_, state.as<unsigned long long>(), ticket.as<unsigned int>(),
+                     first_word.as<uint32_t>(), nc, kind.data(), idx.data(), rows.as<uint64_t>(), ctx_.compute);
+  unsigned long long last = 0;
+  PSG_CUDA(cudaMemcpyAsync(&last, state.as<unsigned long long>() + (nbuckets_ - 1), 8, cudaMemcpyDeviceToHost,
+                           ctx_.compute));
+  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  const uint64_t ng = last & ((1ULL << 62) - 1);
   out.nrows = ng;
   if (want_rows) {
-    uint64_t* dst = out.mutable_rows(static_cast<uint64_t>(ng) * nc);
-    if (ng) PSG_CUDA(cudaMemcpyAsync(dst, rows.p, static_cast<uint64_t>(ng) * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
-    st_.result_bytes += static_cast<uint64_t>(ng) * nc * 8;
+    uint64_t* dst = out.mutable_rows(ng * nc);
+    if (ng) PSG_CUDA(cudaMemcpyAsync(dst, rows.p, ng * nc * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+    st_.result_bytes += ng * nc * 8;
   }
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
 }

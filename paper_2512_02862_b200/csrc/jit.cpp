@@ -310,8 +310,15 @@ bool staged_probe(const ScanProgram& P) {
   }();
   if (!on || !P.staged_ok || P.remote || P.unpack_n != 0 || P.n_early < 1 || P.n_early > 4 || P.n_in > kMaxIn) return false;
   if (P.sink == SINK_PROBE) return P.agg.krec != nullptr;
-  // unordered warp-staged compaction (+ partition histogram, semi-join screen, packed rows)
-  return P.sink == SINK_MATERIALIZE && P.tile_offsets == nullptr && P.n_out >= 1 && P.n_out <= 4 && !P.self_probe;
+  // unordered warp-staged compaction (+ partition histogram, semi-join screen, packed rows):
+  // opt-in (PSG_TMA_MAT=1) - the SF100 orders scan measured slower staged (0.97 vs 0.73 ms: three
+  // early columns leave room for one CTA per SM)
+  static const bool mat_on = [] {
+    const char* e = std::getenv("PSG_TMA_MAT");
+    return e && e[0] == '1';
+  }();
+  return mat_on && P.sink == SINK_MATERIALIZE && P.tile_offsets == nullptr && P.n_out >= 1 && P.n_out <= 4 &&
+         !P.self_probe;
 }
 
 /// Rows per thread per tile (R) of the kernel: R x 32 rows per warp, 1024 / (32 R) warps per

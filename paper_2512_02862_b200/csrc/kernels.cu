@@ -733,32 +733,6 @@ __global__ void k_bucket_words(AggTableDev t, uint64_t nwords, uint64_t nslots, 
   }
 }
 
-__global__ void __launch_bounds__(512) k_bucket_count(AggTableDev t, BucketDev b, uint64_t nslots, uint32_t* counts) {
-  __shared__ uint32_t hits[kBucketSlots];
-  __shared__ uint32_t s_total;
-  for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) hits[i] = 0;
-  if (threadIdx.x == 0) s_total = 0;
-  __syncthreads();
-  const uint64_t bucket = blockIdx.x, s0 = bucket << kBucketBits;
-  const uint32_t fill = b.fill[bucket], n = min(fill, b.cap);
-  const uint64_t* e = b.bkt + bucket * b.cap;
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x)
-    atomicAdd(&hits[__ldcs(reinterpret_cast<const unsigned long long*>(e + i)) & (kBucketSlots - 1)], 1u);
-  __syncthreads();
-  uint32_t mine = 0;
-  for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) {
-    const uint64_t s = s0 + i;
-    if (s >= nslots) break;
-    uint64_t h = hits[i];
-    if (fill > b.cap) h += agg_hits(t, t.hot + s * t.hw);  // overflowed bucket: + the direct updates
-    mine += h != 0;
-  }
-  for (int o = 16; o > 0; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
-  if ((threadIdx.x & 31) == 0 && mine) atomicAdd(&s_total, mine);
-  __syncthreads();
-  if (threadIdx.x == 0) counts[bucket] = s_total;
-}
-
 /// Shared-memory fold of one bucket: hits[i] (u32) and, per probe sum k, the 64-bit sum of the
 /// offset-encoded fields as two u32 words (lo with carry into hi: native 32-bit shared atomics; a
 /// 64-bit shared atomicAdd compiles to a CAS loop). sum_k = fields + hits * bkt_min[k] (mod 2^64).
@@ -783,16 +757,22 @@ __device__ __forceinline__ void add64_u32pair(uint32_t* lo, uint32_t* hi, uint64
   if (vh + carry) atomicAdd(hi, vh + carry);
 }
 
+/// Single pass with decoupled look-back: a CTA claims the next bucket from a ticket (so every
+/// lower bucket is already owned by a running CTA), folds it, publishes its group count, adds up
+/// its predecessors' published counts/prefixes for its output offset, publishes its inclusive
+/// prefix and writes its rows. state[b] = (status << 62) | value: 1 = count, 2 = inclusive prefix.
 __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b, uint64_t nslots, uint64_t nwords,
-                                                     const uint32_t* offsets, const uint32_t* first_word, int nc,
-                                                     EmitCols ec, uint64_t* out) {
+                                                     unsigned long long* state, unsigned int* ticket,
+                                                     const uint32_t* first_word, int nc, EmitCols ec, uint64_t* out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nps = t.nps;
   const BucketSmem m = bucket_smem(smem_raw, nps);
   __shared__ uint32_t s_warp[16];
+  __shared__ uint64_t s_bucket, s_base;
+  if (threadIdx.x == 0) s_bucket = atomicAdd(ticket, 1u);
   for (int i = threadIdx.x; i < (1 + 2 * nps) * kBucketSlots; i += blockDim.x) m.hits[i] = 0;
   __syncthreads();
-  const uint64_t bucket = blockIdx.x, s0 = bucket << kBucketBits;
+  const uint64_t bucket = s_bucket, s0 = bucket << kBucketBits;
   const uint64_t s_end = min(s0 + kBucketSlots, nslots);
   const uint32_t fill = b.fill[bucket], n = min(fill, b.cap);
   const uint64_t* e = b.bkt + bucket * b.cap;
@@ -839,10 +819,30 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
     m.pos[base + k] = static_cast<uint16_t>(acc);
     acc += (m.hits[base + k] != 0 && s0 + base + k < s_end) ? 1u : 0u;
   }
+  if (threadIdx.x == 0) {  // look-back: this bucket's output offset
+    uint32_t total = 0;
+    for (int w = 0; w < 16; ++w) total += s_warp[w];
+    constexpr unsigned long long kCount = 1ULL << 62, kPrefix = 2ULL << 62, kVal = (1ULL << 62) - 1;
+    unsigned long long prefix = 0;
+    if (bucket == 0) {
+      atomicExch(&state[0], kPrefix | total);
+    } else {
+      atomicExch(&state[bucket], kCount | total);
+      for (int64_t j = static_cast<int64_t>(bucket) - 1; j >= 0;) {
+        const unsigned long long v = atomicAdd(&state[j], 0ULL);
+        if ((v >> 62) == 0) continue;  // predecessor still folding (it runs: it claimed its ticket first)
+        prefix += v & kVal;
+        if ((v >> 62) == 2) break;
+        --j;
+      }
+      atomicExch(&state[bucket], kPrefix | (prefix + total));
+    }
+    s_base = prefix;
+  }
   __syncthreads();
   // rows in key order: walk the key-bitmap words covering the bucket's slots
   const unsigned long long* bits = reinterpret_cast<const unsigned long long*>(t.kbits);
-  const uint64_t obase = offsets[bucket];
+  const uint64_t obase = s_base;
   const bool st32 = nc == 4 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
   for (uint64_t w = first_word[bucket] + threadIdx.x; w < nwords; w += blockDim.x) {
     uint64_t s = t.krank[w];
@@ -879,15 +879,9 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
   }
 }
 
-void launch_bucket_count(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots, uint32_t* counts,
-                         void* stream) {
-  if (nbuckets == 0) return;
-  count_launch();
-  k_bucket_count<<<static_cast<unsigned>(nbuckets), 512, 0, S(stream)>>>(t, b, nslots, counts);
-}
 void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots,
-                        const uint32_t* offsets, uint32_t* first_word, int nc, const int32_t* col_kind,
-                        const int32_t* col_idx, uint64_t* out_rows, void* stream) {
+                        unsigned long long* state, unsigned int* ticket, uint32_t* first_word, int nc,
+                        const int32_t* col_kind, const int32_t* col_idx, uint64_t* out_rows, void* stream) {
   if (nbuckets == 0) return;
   const uint64_t nwords = (t.krange + 63) / 64;
   count_launch();
@@ -904,7 +898,9 @@ void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuck
     attr = true;
   }
   count_launch();
-  k_bucket_emit<<<static_cast<unsigned>(nbuckets), 512, smem, S(stream)>>>(t, b, nslots, nwords, offsets, first_word,
+  cudaMemsetAsync(state, 0, nbuckets * sizeof(unsigned long long), S(stream));
+  cudaMemsetAsync(ticket, 0, sizeof(unsigned int), S(stream));
+  k_bucket_emit<<<static_cast<unsigned>(nbuckets), 512, smem, S(stream)>>>(t, b, nslots, nwords, state, ticket, first_word,
                                                                            nc, ec, out_rows);
 }
 

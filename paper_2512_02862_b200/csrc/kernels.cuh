@@ -92,11 +92,11 @@ struct BucketDev {
   int64_t min[kMaxSums];
   int32_t word[kMaxSums];
 };
-void launch_bucket_count(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots, uint32_t* counts,
-                         void* stream);
+/// One pass: fold each bucket, decoupled look-back for its output offset, rows in key order.
+/// state: nbuckets words of scratch; *ticket receives the group total's inputs (see kernels.cu).
 void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots,
-                        const uint32_t* offsets, uint32_t* first_word, int nc, const int32_t* col_kind,
-                        const int32_t* col_idx, uint64_t* out_rows, void* stream);
+                        unsigned long long* state, unsigned int* ticket, uint32_t* first_word, int nc,
+                        const int32_t* col_kind, const int32_t* col_idx, uint64_t* out_rows, void* stream);
 void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, uint64_t n, unsigned long long* krec,
                        void* stream);
 void launch_part_hist(const uint64_t* keys, uint64_t n, int nparts, unsigned long long* counts, void* stream);

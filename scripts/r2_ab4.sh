@@ -13,5 +13,13 @@ run PSG_TMA_R=8 PSG_TMA_NG=3 PSG_TMA_NS=4 PSG_TMA_CTAS=2
 run PSG_TMA_R=8 PSG_TMA_NG=6 PSG_TMA_NS=8 PSG_TMA_CTAS=1
 run PSG_TMA_R=4 PSG_TMA_NG=2 PSG_TMA_NS=4 PSG_TMA_CTAS=2
 run PSG_TMA=1
+run PSG_TMA_MAT=1 PSG_TMA_NS=4
+echo "== with nvidia-smi polling (bench's clock sampler)"
+(nvidia-smi --query-gpu=clocks.sm --format=csv,noheader -lms 100 > /dev/null 2>&1 & echo $! > /tmp/smi.pid)
+run PSG_TMA=1
+kill $(cat /tmp/smi.pid)
+python scripts/q3_value.py --steps 2 --warmup 1 > /dev/null 2>&1 && \
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r2_launches_n1e.csv \
+  python scripts/q3_value.py --steps 1 --warmup 1 > /dev/null 2>&1; echo "ncu rc=$?"
 timeout 900 python scripts/join_bench.py --build-rows 120000000 --probe-rows 320000000 > gpurun_out/r2_join_n1.json 2> gpurun_out/r2_join_n1.err; echo "join rc=$?"
 cat gpurun_out/r2_join_n1.json; tail -3 gpurun_out/r2_join_n1.err
