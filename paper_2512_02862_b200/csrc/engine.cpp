@@ -1170,13 +1170,15 @@ void Execution::build_local_tables() {
       // bitmap over [min, max] (Q3's 3 M customer keys in 15 M: 1.9 MB, L2-resident) replaces the
       // hash table; probes become one cached bit test.
       if (np == 0 && n > 0 && bitmap_env()) {
-        DevBuf mm(ctx_.pool, 16, ctx_.compute);
-        const long long init[2] = {LLONG_MAX, LLONG_MIN};
-        PSG_CUDA(cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, ctx_.compute));
-        launch_minmax_i64(mat.cols[0].as<uint64_t>(), n, mm.as<long long>(), ctx_.compute);
-        long long lohi[2];
-        PSG_CUDA(cudaMemcpyAsync(lohi, mm.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
-        PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+        // key range from the replicated scan's footer zone maps (a superset of the surviving keys)
+        long long lohi[2] = {LLONG_MAX, LLONG_MIN};
+        const int fcol = lj.proj.file_idx[lj.key_idx];
+        for (const auto& path : lj.scan->paths)
+          for (const auto& g : ctx_.footers.get(path)->groups)
+            if (g.rows) {
+              lohi[0] = std::min(lohi[0], static_cast<long long>(g.cols[fcol].min_raw));
+              lohi[1] = std::max(lohi[1], static_cast<long long>(g.cols[fcol].max_raw));
+            }
         const uint64_t range = static_cast<uint64_t>(lohi[1]) - static_cast<uint64_t>(lohi[0]) + 1;
         if (range != 0 && range <= (1ULL << 34) && range / 64 <= n) {
           const uint64_t words = (range + 31) / 32;
@@ -1951,13 +1953,25 @@ ResultRows Execution::run(bool want_rows) {
         bloom_words = 0;
       }
     } else if (nr == 1 && bloom_words && kbits_env && bmat.rows) {
-      DevBuf mm(ctx_.pool, 16, ctx_.compute);
-      const long long init[2] = {LLONG_MAX, LLONG_MIN};
-      PSG_CUDA(cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, ctx_.compute));
-      launch_minmax_i64(bmat.cols[0].as<uint64_t>(), bmat.rows, mm.as<long long>(), ctx_.compute);
-      long long lohi[2];
-      PSG_CUDA(cudaMemcpyAsync(lohi, mm.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
-      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      // the key range: from the build scan's footer zone maps when the key is one of its columns
+      // (a superset of the surviving keys' range: no kernel, no host round trip), else measured
+      long long lohi[2] = {LLONG_MAX, LLONG_MIN};
+      const ColRef kref = bsrc_.stage_refs.back()[bkey];
+      if (kref.join < 0) {
+        const int fcol = bsrc_.proj.file_idx[kref.idx];
+        for (const auto& path : bsrc_.scan->paths)
+          for (const auto& g : ctx_.footers.get(path)->groups)
+            if (g.rows) {
+              lohi[0] = std::min(lohi[0], static_cast<long long>(g.cols[fcol].min_raw));
+              lohi[1] = std::max(lohi[1], static_cast<long long>(g.cols[fcol].max_raw));
+            }
+      } else {
+        DevBuf mm(ctx_.pool, 16, ctx_.compute);
+        PSG_CUDA(cudaMemcpyAsync(mm.p, lohi, 16, cudaMemcpyHostToDevice, ctx_.compute));
+        launch_minmax_i64(bmat.cols[0].as<uint64_t>(), bmat.rows, mm.as<long long>(), ctx_.compute);
+        PSG_CUDA(cudaMemcpyAsync(lohi, mm.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+        PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      }
       const uint64_t range = static_cast<uint64_t>(lohi[1]) - static_cast<uint64_t>(lohi[0]) + 1;
       if (range != 0 && range <= (1ULL << 36) && range / 32 <= bloom_words) {  // no larger than the Bloom
         krange_lo = lohi[0];
