@@ -286,7 +286,7 @@ void emit_semi_screen(std::ostringstream& s, const ScanProgram& P) {
 }
 
 /// Warp-specialised probe for the one-GPU rank-indexed table (PSG_TMA=0: off). Shape knobs:
-/// PSG_TMA_NG consumer groups of 8 warps (default 2), PSG_TMA_NS ring stages (6), PSG_TMA_CTAS
+/// PSG_TMA_NG consumer groups of 8 warps (default 2), PSG_TMA_NS ring stages (4), PSG_TMA_CTAS
 /// CTAs per SM (2).
 struct StagedShape {
   int groups, stages, ctas, rows;  // rows: per consumer lane per tile (4 or 8); 1024 / (32 rows) warps per group
@@ -299,7 +299,7 @@ StagedShape staged_shape() {
       return e ? std::max(1, std::atoi(e)) : d;
     };
     const int r = env("PSG_TMA_R", 4) >= 8 ? 8 : 4;
-    return StagedShape{env("PSG_TMA_NG", 2), env("PSG_TMA_NS", 6), env("PSG_TMA_CTAS", 2), r};
+    return StagedShape{env("PSG_TMA_NG", 2), env("PSG_TMA_NS", 4), env("PSG_TMA_CTAS", 2), r};
   }();
   return sh;
 }

@@ -80,7 +80,9 @@ struct Cols {
 class JoinRun {
  public:
   JoinRun(Ctx& ctx, const JoinSpecC& spec, const HostTable& build, const HostTable& probe, bool collect)
-      : ctx_(ctx), spec_(spec), build_(build), probe_(probe), collect_(collect) {}
+      : ctx_(ctx), spec_(spec), build_(build), probe_(probe), collect_(collect) {
+    pool_.init(ctx.device, 0);
+  }
   ~JoinRun();
   JoinOutcome run();
 
@@ -116,6 +118,9 @@ class JoinRun {
   void probe(int w, cudaStream_t s);
 
   Ctx& ctx_;
+  // a pool of this run's own: its blocks are keyed by this run's streams, so it is emptied before
+  // the streams are destroyed (the context pool would keep stale stream keys)
+  DevicePool pool_;
   JoinSpecC spec_;
   const HostTable& build_;
   const HostTable& probe_;
@@ -139,6 +144,11 @@ JoinRun::~JoinRun() {
   for (auto s : streams_) cudaStreamSynchronize(s);
   cudaStreamSynchronize(ctx_.comm);
   for (auto& [p, s] : raw_) cudaFree(p);
+  tkeys_.reset();
+  tcnt_.reset();
+  tstart_.reset();
+  tpay_.clear();
+  pool_.release_cache();
   for (auto& side : {&left_, &right_})
     for (auto& w : side->waves)
       if (w.shuffled) cudaEventDestroy(w.shuffled);
@@ -156,7 +166,7 @@ void* JoinRun::dalloc(size_t bytes, cudaStream_t s) {
     raw_.push_back({p, s});
     return p;
   }
-  return ctx_.pool.alloc(bytes, s);
+  return pool_.alloc(bytes, s);
 }
 void JoinRun::dfree(void* p, cudaStream_t s) {
   if (!p) return;
@@ -166,7 +176,7 @@ void JoinRun::dfree(void* p, cudaStream_t s) {
     raw_.erase(std::remove_if(raw_.begin(), raw_.end(), [&](const auto& x) { return x.first == p; }), raw_.end());
     return;
   }
-  ctx_.pool.free(p, s);
+  pool_.free(p, s);
 }
 
 /// Blocking variants: the node's whole table becomes one wave (concat of its chunks).
@@ -294,7 +304,7 @@ void JoinRun::build(cudaStream_t s) {
   }
   // gather the received blocks into one columnar image
   std::vector<DevBuf> all;
-  for (int c = 0; c < nc; ++c) all.emplace_back(ctx_.pool, std::max<uint64_t>(n, 1) * 8, s);
+  for (int c = 0; c < nc; ++c) all.emplace_back(pool_, std::max<uint64_t>(n, 1) * 8, s);
   uint64_t at = 0;
   for (auto& w : left_.waves) {
     uint64_t off = 0;
@@ -315,22 +325,22 @@ void JoinRun::build(cudaStream_t s) {
   while (cap < 2 * n) cap <<= 1;
   int shift = 64;
   for (uint64_t c = cap; c > 1; c >>= 1) --shift;
-  tkeys_ = DevBuf(ctx_.pool, cap * 8, s);
-  tcnt_ = DevBuf(ctx_.pool, (cap + 1) * 4, s);
-  tstart_ = DevBuf(ctx_.pool, (cap + 1) * 4, s);
-  DevBuf cursor(ctx_.pool, (cap + 1) * 4, s), maxc(ctx_.pool, 4, s);
+  tkeys_ = DevBuf(pool_, cap * 8, s);
+  tcnt_ = DevBuf(pool_, (cap + 1) * 4, s);
+  tstart_ = DevBuf(pool_, (cap + 1) * 4, s);
+  DevBuf cursor(pool_, (cap + 1) * 4, s), maxc(pool_, 4, s);
   PSG_CUDA(cudaMemsetAsync(maxc.p, 0, 4, s));
   PSG_CUDA(cudaMemsetAsync(cursor.p, 0, (cap + 1) * 4, s));
   launch_local_init(tkeys_.as<uint64_t>(), tcnt_.as<uint32_t>(), cap, s);
   launch_local_count(tkeys_.as<uint64_t>(), tcnt_.as<uint32_t>(), cap - 1, shift, all[0].as<uint64_t>(), n,
                      maxc.as<unsigned>(), s);
   const size_t tb = exclusive_scan_u32(nullptr, nullptr, cap + 1, nullptr, 0, s);
-  DevBuf tmp(ctx_.pool, tb, s);
+  DevBuf tmp(pool_, tb, s);
   exclusive_scan_u32(tcnt_.as<uint32_t>(), tstart_.as<uint32_t>(), cap + 1, tmp.p, tb, s);
   std::vector<const uint64_t*> src;
   std::vector<uint64_t*> dst;
   for (int c = 1; c < nc; ++c) {
-    tpay_.emplace_back(ctx_.pool, std::max<uint64_t>(n, 1) * 8, s);
+    tpay_.emplace_back(pool_, std::max<uint64_t>(n, 1) * 8, s);
     src.push_back(all[c].as<uint64_t>());
     dst.push_back(tpay_.back().as<uint64_t>());
   }
