@@ -325,13 +325,17 @@ def main():
         staged.run(want_rows=False)
     sync_all()
     dev_ms, sts = [], []
-    clk = Clocks(local).__enter__()
+    clk = Clocks(local)
+    if os.environ.get("PSG_BENCH_NO_CLOCKS") != "1":  # A/B knob: the sampler's effect on the value loop
+        clk.__enter__()
     wall0 = time.time()
     for _ in range(args.steps):
         sync_all()  # every step starts aligned across ranks (the barrier is outside the engine's events)
         st = staged.run(want_rows=False)
         dev_ms.append(st["device_ms"])
         sts.append(st)
+    if os.environ.get("PSG_BENCH_VERBOSE") == "1" and rank == 0:
+        sys.stderr.write("value steps (device ms): %s\n" % [round(x, 3) for x in dev_ms])
     sync_all()
     wall_value = (time.time() - wall0) / max(args.steps, 1)
     value_s = reduce(sum(dev_ms) / 1000.0 / max(args.steps, 1))

@@ -172,10 +172,20 @@ int psg_run_synthetic_join(psg_ctx* ctx, const psg_join_spec* spec, const psg_jo
     const auto key = std::make_tuple(workload->build_rows, workload->probe_rows, workload->payload_cols,
                                      workload->hit_ratio, workload->seed, ctx->c.rank, ctx->c.nranks);
     if (key != last_key || build.cols.empty()) {
+      for (HostTable* t : {&build, &probe})
+        for (auto& c : t->cols)
+          if (!c.empty()) cudaHostUnregister(c.data());
+      cudaGetLastError();
       build = HostTable{};
       probe = HostTable{};
       synthetic_join_tables(workload->seed, workload->build_rows, workload->probe_rows, workload->payload_cols,
                             workload->hit_ratio, ctx->c.rank, ctx->c.nranks, build, probe);
+      // page-locked, like the pinned staging of the storage path: the waves' H2D copies run at
+      // PCIe speed instead of through the driver's pageable bounce buffers
+      for (HostTable* t : {&build, &probe})
+        for (auto& c : t->cols)
+          if (!c.empty() && cudaHostRegister(c.data(), c.size() * 8, cudaHostRegisterDefault) != cudaSuccess)
+            cudaGetLastError();  // (stays pageable: slower copies, same results)
       last_key = key;
     }
     JoinSpecC js;

@@ -24,8 +24,8 @@ constexpr int kMaxOut = 16;
 constexpr int kMaxSums = 8;
 constexpr int kMaxParts = 64;
 constexpr int kBlock = 256;
-constexpr int kBucketSlots = 4096;  // rank-table slots per aggregation bucket (shared-memory slice)
-constexpr int kBucketBits = 12;
+constexpr int kBucketSlots = 2048;  // rank-table slots per aggregation bucket (shared-memory slice)
+constexpr int kBucketBits = 11;
 constexpr int kRowsPerThread = 4;
 constexpr uint64_t kSlotMul = 0xD6E8FEB86659FD93ULL;   // table slot = (k * kSlotMul) >> shift
 constexpr uint64_t kBloomMul = 0xA24BAED4963EE407ULL;  // bloom word/bits from (k * kBloomMul)

@@ -800,24 +800,29 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
       }
     }
   __syncthreads();
-  // exclusive prefix of "slot has hits" over the bucket (8 consecutive slots per thread)
-  constexpr int per = kBucketSlots / 512;
-  const int base = threadIdx.x * per;
-  uint32_t run = 0;
-  for (int k = 0; k < per; ++k) run += (m.hits[base + k] != 0 && s0 + base + k < s_end) ? 1u : 0u;
+  // exclusive prefix of "slot has hits" over the bucket: warp w owns slots [w * per32 * 32, ...) as
+  // per32 rows of 32 consecutive slots, lane = slot within the row (conflict-free shared reads);
+  // ballots give the in-row prefix, row totals the in-warp prefix, warp totals the rest
+  constexpr int per32 = kBucketSlots / 512;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  uint32_t incl = run;
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
+  const int wbase = wid * per32 * 32;
+  uint32_t wsum = 0;
+  unsigned flags[per32];
+#pragma unroll
+  for (int k = 0; k < per32; ++k) {
+    const int i = wbase + k * 32 + lane;
+    flags[k] = __ballot_sync(0xffffffffu, m.hits[i] != 0 && s0 + i < s_end);
+    wsum += __popc(flags[k]);
   }
-  if (lane == 31) s_warp[wid] = incl;
+  if (lane == 0) s_warp[wid] = wsum;
   __syncthreads();
-  uint32_t acc = incl - run;
+  uint32_t acc = 0;
   for (int w = 0; w < wid; ++w) acc += s_warp[w];
-  for (int k = 0; k < per; ++k) {
-    m.pos[base + k] = static_cast<uint16_t>(acc);
-    acc += (m.hits[base + k] != 0 && s0 + base + k < s_end) ? 1u : 0u;
+  const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+  for (int k = 0; k < per32; ++k) {
+    m.pos[wbase + k * 32 + lane] = static_cast<uint16_t>(acc + __popc(flags[k] & below));
+    acc += __popc(flags[k]);
   }
   if (threadIdx.x == 0) {  // look-back: this bucket's output offset
     uint32_t total = 0;
