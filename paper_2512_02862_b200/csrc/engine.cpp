@@ -1714,7 +1714,10 @@ ResultRows Execution::run(bool want_rows) {
     for (size_t i = 0; i < psrc_.wire.size(); ++i)
       if (static_cast<int>(i) != pkey) pneed.push_back(static_cast<int>(i));
   }
-  RegMap bm = analyse(bsrc_, bneed, bkey, true);
+  // the build side's key is a late column: only rows passing the predicate and the local joins
+  // need it (Q3 orders: 9% - most of its sectors are never read); the probe side's key is early
+  // (its screen / table lookup needs it for every row that passes the predicate)
+  RegMap bm = analyse(bsrc_, bneed, -1, true);
   RegMap pm = analyse(psrc_, pneed, pkey, true);
   for (size_t j = 0; j < bsrc_.chain.size(); ++j) bsrc_.chain[j].needed_payload = bm.payload_cols[j];
   for (size_t j = 0; j < psrc_.chain.size(); ++j) psrc_.chain[j].needed_payload = pm.payload_cols[j];
@@ -2708,7 +2711,7 @@ ResultRows Execution::run_ingest_only() {
     for (size_t i = 0; i < psrc_.wire.size(); ++i)
       if (static_cast<int>(i) != pkey) pneed.push_back(static_cast<int>(i));
   }
-  RegMap bm = analyse(bsrc_, bneed, bkey, true);
+  RegMap bm = analyse(bsrc_, bneed, -1, true);
   RegMap pm = analyse(psrc_, pneed, pkey, true);
   for (size_t j = 0; j < bsrc_.chain.size(); ++j) bsrc_.chain[j].needed_payload = bm.payload_cols[j];
   for (size_t j = 0; j < psrc_.chain.size(); ++j) psrc_.chain[j].needed_payload = pm.payload_cols[j];
@@ -2743,7 +2746,7 @@ void Execution::stage(Staged& st) {
     for (size_t i = 0; i < psrc_.wire.size(); ++i)
       if (static_cast<int>(i) != pkey) pneed.push_back(static_cast<int>(i));
   }
-  RegMap bm = analyse(bsrc_, bneed, bkey, true);
+  RegMap bm = analyse(bsrc_, bneed, -1, true);
   RegMap pm = analyse(psrc_, pneed, pkey, true);
   const auto scans = scan_list(bm, pm);
   for (auto& [scan, fcols] : scans) {
