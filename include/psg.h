@@ -104,6 +104,7 @@ typedef struct psg_stats {
                                   unique build keys), 5 symmetric peer-mapped (fused NVLink) */
   uint64_t bytes_sent;         /* shuffle payload bytes sent to peers */
   double exchange_ms;          /* summed CUDA-event time of the shuffle send/recv groups */
+  uint64_t bucket_overflow;    /* rows that found their aggregation bucket full (bucketed aggregation) */
 } psg_stats;
 
 /* ---- library ---- */

@@ -199,13 +199,18 @@ struct ScanProgram {
   // to the bucket of its slot (slot >> kBucketBits): slot & (kBucketSlots - 1) in the low bits,
   // then every probe sum k as (v - bkt_min[k]) & bkt_mask[k] at bkt_shift[k]. k_bucket_agg then
   // folds each bucket in shared memory and adds it to the hot slots once, so the table's random
-  // read-modify-writes never go to HBM. A full bucket falls back to the direct atomic update.
+  // read-modify-writes never go to HBM. A full bucket spills to the overflow list below.
   uint64_t* bkt;             // [nbuckets][bkt_cap]
   unsigned int* bkt_fill;    // [nbuckets] appended entries (may exceed bkt_cap: overflowed)
   uint32_t bkt_cap;
   int32_t bkt_shift[kMaxSums];
   uint64_t bkt_mask[kMaxSums];
   int64_t bkt_min[kMaxSums];
+  // a full bucket's rows go to one overflow list: {full slot, entry word} pairs; beyond its
+  // capacity the engine re-runs the query without buckets (bkt_ovf_count > bkt_ovf_cap)
+  uint64_t* bkt_ovf;
+  unsigned int* bkt_ovf_count;
+  uint32_t bkt_ovf_cap;
   // the engine guarantees 16-byte aligned column chunks and readable padding past each chunk's
   // end (PSTO batches, staged images): the query compiler may then stream the early columns into
   // shared memory with bulk copies (the warp-specialised probe, jit.cpp)

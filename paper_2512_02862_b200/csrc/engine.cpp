@@ -38,6 +38,12 @@
 
 namespace psg {
 
+/// The bucketed aggregation's overflow list filled up (extreme key skew): the query is re-run with
+/// the table's direct atomic updates (execute_plan), so results never depend on bucket sizing.
+struct BucketOverflow : Error {
+  BucketOverflow() : Error(PSG_ERR_INTERNAL, "aggregation bucket overflow") {}
+};
+
 namespace {
 
 using Clock = std::chrono::steady_clock;
@@ -520,7 +526,7 @@ class Execution {
   std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
   // agg table
   DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, agg_krank_, agg_krec_, global_acc_, barrier_word_;
-  DevBuf bkt_, bkt_fill_;  // bucketed aggregation (rank table, one GPU)
+  DevBuf bkt_, bkt_fill_, bkt_ovf_, bkt_ovf_count_;  // bucketed aggregation (rank table, one GPU)
   bool bucket_mode_ = false;
   BucketDev bd_{};
   uint64_t nbuckets_ = 0;
@@ -1290,7 +1296,7 @@ bool Execution::setup_buckets() {
     return !(e && e[0] == '0');
   }();
   const int np = static_cast<int>(probe_sum_wire.size());
-  if (!env || !jit_available() || np > 3 || aggt_.krange == 0 || agg_cap_ == 0) return false;
+  if (!env || ctx_.no_buckets || !jit_available() || np > 3 || aggt_.krange == 0 || agg_cap_ == 0) return false;
   BucketDev bd{};
   int shift = kBucketBits;
   uint64_t probe_rows = 0;
@@ -1318,7 +1324,13 @@ bool Execution::setup_buckets() {
   }
   const uint64_t nb = (agg_cap_ + kBucketSlots - 1) / kBucketSlots;
   const double share = std::min(1.0, static_cast<double>(agg_cap_) / static_cast<double>(aggt_.krange));
-  const uint64_t cap = static_cast<uint64_t>(1.5 * static_cast<double>(probe_rows) * share / static_cast<double>(nb)) + 1024;
+  // PSG_BUCKET_CAP / PSG_BUCKET_OVF_CAP override the capacities (tests: force the overflow paths)
+  static const uint64_t cap_env = [] {
+    const char* e = std::getenv("PSG_BUCKET_CAP");
+    return e ? std::strtoull(e, nullptr, 10) : 0ULL;
+  }();
+  const uint64_t cap = cap_env ? cap_env
+                               : static_cast<uint64_t>(1.5 * static_cast<double>(probe_rows) * share / static_cast<double>(nb)) + 1024;
   if (cap >= (1ULL << 31)) return false;
   bkt_ = DevBuf(ctx_.pool, nb * cap * 8, ctx_.compute);
   bkt_fill_ = DevBuf(ctx_.pool, nb * 4, ctx_.compute);
@@ -1327,12 +1339,25 @@ bool Execution::setup_buckets() {
   bd.fill = bkt_fill_.as<unsigned int>();
   bd.cap = static_cast<uint32_t>(cap);
   bd.nacc = 1 + np;
+  static const uint32_t kOvfCap = [] {  // 1 MB: scanned by every bucket CTA when not empty
+    const char* e = std::getenv("PSG_BUCKET_OVF_CAP");
+    return e ? static_cast<uint32_t>(std::strtoul(e, nullptr, 10)) : (1u << 16);
+  }();
+  bkt_ovf_ = DevBuf(ctx_.pool, kOvfCap * 16, ctx_.compute);
+  bkt_ovf_count_ = DevBuf(ctx_.pool, 4, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(bkt_ovf_count_.p, 0, 4, ctx_.compute));
+  bd.ovf = bkt_ovf_.as<uint64_t>();
+  bd.ovf_count = bkt_ovf_count_.as<unsigned int>();
+  bd.ovf_cap = kOvfCap;
   bd_ = bd;
   nbuckets_ = nb;
   return true;
 }
 
 void Execution::apply_buckets(ScanProgram& p) const {
+  p.bkt_ovf = const_cast<uint64_t*>(bd_.ovf);
+  p.bkt_ovf_count = const_cast<unsigned int*>(bd_.ovf_count);
+  p.bkt_ovf_cap = bd_.ovf_cap;
   p.bkt = const_cast<uint64_t*>(bd_.bkt);
   p.bkt_fill = const_cast<unsigned int*>(bd_.fill);
   p.bkt_cap = bd_.cap;
@@ -1363,9 +1388,13 @@ void Execution::finalize_buckets(ResultRows& out, bool want_rows) {
   launch_bucket_emit(aggt_, bd_, nbuckets_, agg_cap_, state.as<unsigned long long>(), ticket.as<unsigned int>(),
                      first_word.as<uint32_t>(), nc, kind.data(), idx.data(), rows.as<uint64_t>(), ctx_.compute);
   unsigned long long last = 0;
+  unsigned int novf = 0;
   PSG_CUDA(cudaMemcpyAsync(&last, state.as<unsigned long long>() + (nbuckets_ - 1), 8, cudaMemcpyDeviceToHost,
                            ctx_.compute));
+  PSG_CUDA(cudaMemcpyAsync(&novf, bd_.ovf_count, 4, cudaMemcpyDeviceToHost, ctx_.compute));
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  st_.bucket_overflow = novf;
+  if (novf > bd_.ovf_cap) throw BucketOverflow();  // execute_plan re-runs the query without buckets
   const uint64_t ng = last & ((1ULL << 62) - 1);
   out.nrows = ng;
   if (want_rows) {
@@ -2046,7 +2075,6 @@ ResultRows Execution::run(bool want_rows) {
     if (rank_mode) {
       // hot slots from the bitmap (slot order) once, cold slots (build sums) per build segment
       bool first = true;
-      if (bucket_mode_) PSG_CUDA(cudaMemsetAsync(agg_hot_.p, 0, agg_hot_.bytes, ctx_.compute));
       for (const auto& sg : bsegs) {
         RankSums rs{};
         for (int b = 0; b < p.n_sum; ++b) rs.col[b] = sg.col[1 + b];
@@ -2832,13 +2860,30 @@ ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::strin
   PSG_CUDA(cudaSetDevice(ctx.device));
   if (mode < 0 || mode > 3) throw InvalidInput("unknown execution mode");
   if (ctx.nranks > 1 && ctx.nccl == nullptr) throw InvalidInput("nranks > 1 needs psg_ctx_init_comm first");
+  // a bucket-overflow-list overflow re-runs the query once without buckets
+  auto with_retry = [&](auto&& once) {
+    try {
+      return once();
+    } catch (const BucketOverflow&) {
+      struct Flag {
+        Ctx& c;
+        ~Flag() { c.no_buckets = false; }
+      } flag{ctx};
+      ctx.no_buckets = true;
+      return once();
+    }
+  };
   if (staged) {
-    Execution ex(ctx, staged->plan_json, staged->data_root, mode, staged);
-    return ex.run(want_rows);
+    return with_retry([&] {
+      Execution ex(ctx, staged->plan_json, staged->data_root, mode, staged);
+      return ex.run(want_rows);
+    });
   }
   if (mode == PSG_MODE_OVERLAPPED) {
-    Execution ex(ctx, plan_json, data_root, mode, nullptr);
-    return ex.run(want_rows);
+    return with_retry([&] {
+      Execution ex(ctx, plan_json, data_root, mode, nullptr);
+      return ex.run(want_rows);
+    });
   }
   // Phase-sequential modes: storage phase materialises every needed chunk in HBM, then the
   // network/compute phase runs over the staged images (run_phased, pipeline.cpp:506-556).
@@ -2856,8 +2901,10 @@ ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::strin
   }
   ctx.pool.set_budget(0);
   const double storage = secs_since(t0);
-  Execution ex(ctx, plan_json, data_root, mode, st.get());
-  ResultRows r = ex.run(want_rows);
+  ResultRows r = with_retry([&] {
+    Execution ex(ctx, plan_json, data_root, mode, st.get());
+    return ex.run(want_rows);
+  });
   r.stats.storage_phase_s = storage;
   r.stats.network_phase_s = r.stats.runtime_s;
   r.stats.runtime_s = secs_since(t0);

@@ -224,6 +224,7 @@ struct Ctx {
   }
   void ensure_pinned(int nslots, uint64_t slot_bytes);
   Timeline* timeline = nullptr;  // set for the duration of a query when PSG_TIMELINE is on
+  bool no_buckets = false;       // set while a query re-runs after a bucket-overflow-list overflow
   ~Ctx();
 };
 

@@ -204,14 +204,18 @@ void emit_rank_probe(std::ostringstream& s, const ScanProgram& P, Late late) {
     << "        else sl[r] = bp[r] + static_cast<uint64_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n";
   late();
   s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n";
-  if (P.bkt != nullptr) {  // append one word to the slot's bucket (k_bucket_agg folds it)
+  if (P.bkt != nullptr) {  // append one word to the slot's bucket (k_bucket_emit folds it)
     s << "        const uint64_t b = sl[r] >> " << kBucketBits << ";\n"
       << "        const unsigned pos = atomicAdd(P.bkt_fill + b, 1u);\n"
-      << "        if (pos < P.bkt_cap) {\n          uint64_t e = sl[r] & " << (kBucketSlots - 1) << "ULL;\n";
+      << "        uint64_t e = sl[r] & " << (kBucketSlots - 1) << "ULL;\n";
     for (int k = 0; k < P.n_sum; ++k)
-      s << "          e |= ((" << V(P.sum_reg[k]) << "[r] - static_cast<uint64_t>(P.bkt_min[" << k << "])) & P.bkt_mask[" << k
+      s << "        e |= ((" << V(P.sum_reg[k]) << "[r] - static_cast<uint64_t>(P.bkt_min[" << k << "])) & P.bkt_mask[" << k
         << "]) << P.bkt_shift[" << k << "];\n";
-    s << "          P.bkt[b * P.bkt_cap + pos] = e;\n          continue;\n        }\n";
+    s << "        if (pos < P.bkt_cap) {\n";
+    s << "          P.bkt[b * P.bkt_cap + pos] = e;\n        } else {  // bucket full: the overflow list\n"
+      << "          const unsigned o = atomicAdd(P.bkt_ovf_count, 1u);\n"
+      << "          if (o < P.bkt_ovf_cap) { P.bkt_ovf[2 * o] = sl[r]; P.bkt_ovf[2 * o + 1] = e; }\n        }\n"
+      << "        continue;\n";
   }
   s << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
   emit_accumulate(s, P, "        ");

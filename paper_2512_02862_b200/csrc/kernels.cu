@@ -783,22 +783,16 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
     for (int k = 0; k < nps; ++k) add64_u32pair(&m.lo[k * kBucketSlots + sl], &m.hi[k * kBucketSlots + sl], (w >> b.shift[k]) & b.mask[k]);
   }
   __syncthreads();
-  if (fill > b.cap)  // overflowed bucket: fold in the direct (hot-table) updates of its slots
-    for (int i = threadIdx.x; i < kBucketSlots; i += blockDim.x) {
-      const uint64_t s = s0 + i;
-      if (s >= s_end) break;
-      const uint64_t* h = t.hot + s * t.hw;
-      const uint64_t hits = agg_hits(t, h);
-      if (!hits) continue;
-      m.hits[i] += static_cast<uint32_t>(hits);
-      for (int k = 0; k < nps; ++k) {
-        const uint64_t f = agg_psum(t, h, k, hits) - hits * static_cast<uint64_t>(b.min[k]);  // as offset fields
-        const uint64_t cur = (static_cast<uint64_t>(m.hi[k * kBucketSlots + i]) << 32) | m.lo[k * kBucketSlots + i];
-        const uint64_t nv = cur + f;
-        m.lo[k * kBucketSlots + i] = static_cast<uint32_t>(nv);
-        m.hi[k * kBucketSlots + i] = static_cast<uint32_t>(nv >> 32);
-      }
-    }
+  // rows that found a bucket full sit in the overflow list (rare; empty on the common path)
+  const uint32_t novf = min(*b.ovf_count, b.ovf_cap);
+  for (uint32_t i = threadIdx.x; i < novf; i += blockDim.x) {
+    const uint64_t slot = b.ovf[2 * i];
+    if ((slot >> kBucketBits) != bucket) continue;
+    const uint64_t w = b.ovf[2 * i + 1];
+    const uint32_t sl = static_cast<uint32_t>(slot & (kBucketSlots - 1));
+    atomicAdd(&m.hits[sl], 1u);
+    for (int k = 0; k < nps; ++k) add64_u32pair(&m.lo[k * kBucketSlots + sl], &m.hi[k * kBucketSlots + sl], (w >> b.shift[k]) & b.mask[k]);
+  }
   __syncthreads();
   // exclusive prefix of "slot has hits" over the bucket: warp w owns slots [w * per32 * 32, ...) as
   // per32 rows of 32 consecutive slots, lane = slot within the row (conflict-free shared reads);

@@ -91,6 +91,9 @@ struct BucketDev {
   uint64_t mask[kMaxSums];
   int64_t min[kMaxSums];
   int32_t word[kMaxSums];
+  const uint64_t* ovf;            // {slot, entry} pairs of rows that found their bucket full
+  const unsigned int* ovf_count;  // entries appended (may exceed ovf_cap: the engine re-runs)
+  uint32_t ovf_cap;
 };
 /// One pass: fold each bucket, decoupled look-back for its output offset, rows in key order.
 /// state: nbuckets words of scratch; *ticket receives the group total's inputs (see kernels.cu).

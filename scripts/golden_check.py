@@ -21,6 +21,7 @@ def main():
     ctx.set_ingest(io_threads=4, batch_bytes=2 << 20)
     bad = 0
     kinds = {}  # psg_stats.agg_table kind -> cases (4 = rank-indexed table)
+    ovf = [0]  # rows that went through the bucket overflow list
     with tempfile.TemporaryDirectory() as tmp:
         cache = {}
 
@@ -41,6 +42,7 @@ def main():
                                    r["mode"])
             s = po.summary([(res.schema, res.rows)])
             kinds[res.stats["agg_table"]] = kinds.get(res.stats["agg_table"], 0) + 1
+            ovf[0] += res.stats["bucket_overflow"]
             if r["plan"] == "global_agg" and r["nodes"] > 1:
                 ok = s["colsums"] == r["colsums"]
             else:
@@ -73,6 +75,7 @@ def main():
             print("%-26s %s" % (r["case"], "OK" if ok else "BAD"), flush=True)
     ctx.close()
     print("AGG_TABLES", json.dumps({str(k): v for k, v in sorted(kinds.items())}))
+    print("BUCKET_OVERFLOW", ovf[0])
     print("BAD", bad)
     sys.exit(1 if bad else 0)
 

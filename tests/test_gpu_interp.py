@@ -39,6 +39,28 @@ def test_rank_table_on_small_cases_matches_golden():
     assert _tables(r.stdout).get(4, 0) > 0, r.stdout[-500:]
 
 
+def test_bucket_overflow_list_matches_golden():
+    """PSG_BUCKET_CAP=8: tiny aggregation buckets, so most matched rows go through the overflow
+    list that every bucket CTA folds - results unchanged."""
+    env = dict(os.environ, PSG_SCREEN_MIN_MB="0", PSG_BUCKET_CAP="8")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "BAD 0" in r.stdout
+    n = int([x for x in r.stdout.splitlines() if x.startswith("BUCKET_OVERFLOW")][0].split()[1])
+    assert n > 0
+
+
+def test_bucket_overflow_rerun_matches_golden():
+    """PSG_BUCKET_CAP=8 + PSG_BUCKET_OVF_CAP=4: the overflow list itself overflows, so the query is
+    re-run with direct table updates - results unchanged."""
+    env = dict(os.environ, PSG_SCREEN_MIN_MB="0", PSG_BUCKET_CAP="8", PSG_BUCKET_OVF_CAP="4")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "BAD 0" in r.stdout
+
+
 def test_rank_table_row_ordered_build_matches_golden():
     """PSG_SCREEN_MIN_MB=0 + PSG_RANK_HOT_SEQ=0: the rank table's hot slots written by the
     row-ordered build pass (incl. its 16-byte-store branch) on the small golden cases."""
