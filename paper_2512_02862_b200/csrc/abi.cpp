@@ -280,6 +280,15 @@ int psg_ctx_create(int device, int rank, int nranks, psg_ctx** out) {
     PSG_CUDA(cudaEventCreate(&c.ev_a));
     PSG_CUDA(cudaEventCreate(&c.ev_b));
     c.pool.init(device, 0);
+    // L2 fetch granularity: the late columns are gathered for a few percent of the rows, so a
+    // miss should bring in the 32-byte sector it needs, not a wider line. PSG_L2_FETCH=<bytes>
+    // (32..128; 0 = leave the driver default).
+    static const long fetch = [] {
+      const char* e = std::getenv("PSG_L2_FETCH");
+      return e ? std::atol(e) : 32L;
+    }();
+    if (fetch > 0 && cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(fetch)) != cudaSuccess)
+      cudaGetLastError();
     *out = ctx.release();
   });
 }
