@@ -62,16 +62,46 @@ bool trace_on() { return trace_level() > 0; }
       std::fputc('\n', stderr);             \
     }                                       \
   } while (0)
+/// PSG_TRACE=1: phase times with a stream sync at every mark; 2: host timestamps only; 3: CUDA
+/// events on the stream + host timestamps, no syncs, printed when the query ends (device time per
+/// phase including its idle gaps, next to the host time - where the GPU waits for the host).
 struct PhaseTimer {
   Clock::time_point t0 = Clock::now(), last = t0;
+  struct Mark {
+    const char* what;
+    cudaEvent_t ev;
+    double host_ms;
+  };
+  std::vector<Mark> marks;
+  cudaStream_t stream0 = nullptr;
   void mark(const char* what, cudaStream_t s) {
     if (!trace_on()) return;
+    if (trace_level() == 3) {
+      Mark m{what, nullptr, std::chrono::duration<double, std::milli>(Clock::now() - t0).count()};
+      cudaEventCreate(&m.ev);
+      cudaEventRecord(m.ev, s);
+      if (marks.empty()) stream0 = s;
+      marks.push_back(m);
+      return;
+    }
     if (trace_level() == 1) cudaStreamSynchronize(s);  // level 2: host timestamps only
     const auto now = Clock::now();
     std::fprintf(stderr, "[psg] %-28s %8.3f ms (total %8.3f)\n", what,
                  std::chrono::duration<double, std::milli>(now - last).count(),
                  std::chrono::duration<double, std::milli>(now - t0).count());
     last = now;
+  }
+  ~PhaseTimer() {
+    if (marks.empty()) return;
+    cudaEventSynchronize(marks.back().ev);
+    for (size_t i = 1; i < marks.size(); ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, marks[i - 1].ev, marks[i].ev);
+      std::fprintf(stderr, "[psg] %-34s device %8.3f ms   host %8.3f ms (at %8.3f)\n", marks[i].what, ms,
+                   marks[i].host_ms - marks[i - 1].host_ms, marks[i].host_ms);
+    }
+    for (auto& m : marks) cudaEventDestroy(m.ev);
+    cudaGetLastError();
   }
 };
 double secs_since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }

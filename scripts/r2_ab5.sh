@@ -10,6 +10,7 @@ run PSG_L2_FETCH=64
 run PSG_L2_FETCH=128
 run PSG_L2_FETCH=32 PSG_TMA=0
 run PSG_L2_FETCH=32
+PSG_TRACE=3 python scripts/q3_value.py --steps 1 --warmup 2 > gpurun_out/r2_phases_n1.txt 2>&1; tail -14 gpurun_out/r2_phases_n1.txt
 python scripts/q3_value.py --steps 2 --warmup 1 > /dev/null 2>&1 && \
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none --csv --log-file gpurun_out/r2_launches_n1f.csv \
   python scripts/q3_value.py --steps 1 --warmup 1 > /dev/null 2>&1; echo "ncu rc=$?"
