@@ -2054,6 +2054,7 @@ ResultRows Execution::run(bool want_rows) {
       unsigned int d = 1;
       PSG_CUDA(cudaMemcpyAsync(&d, dup.p, 4, cudaMemcpyDeviceToHost, ctx_.compute));
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      pt.mark("  key bitmap + dup check", ctx_.compute);
       if (!d) {
         DevBuf cnt(ctx_.pool, kwords64 * 4, ctx_.compute);
         agg_krank_ = DevBuf(ctx_.pool, kwords64 * 4, ctx_.compute);
@@ -2067,6 +2068,7 @@ ResultRows Execution::run(bool want_rows) {
         rank_mode = true;
       }
     }
+    pt.mark("  rank records", ctx_.compute);
     build_agg_table(build_rows, bloom_words, rank_mode ? build_rows : 0);
     st_.agg_table = rank_mode ? 4 : (krange ? 3 : (bloom_words ? 2 : 1));
     if (krange) {
@@ -2083,7 +2085,9 @@ ResultRows Execution::run(bool want_rows) {
         aggt_.krec = agg_krec_.as<unsigned long long>();
       }
     }
+    pt.mark("  agg table", ctx_.compute);
     pack_accumulators();
+    pt.mark("  pack accumulators", ctx_.compute);
     // one GPU, rank table, fused probe: bucketed aggregation (the hot table is then only the target
     // of bucket overflow - zeroed instead of initialised with keys)
     if (rank_mode && nr == 1 && grouped_ && !pdup) bucket_mode_ = setup_buckets();
