@@ -421,8 +421,11 @@ def main():
         per_launch_bytes = total("probe_kernel_bytes") / pl
         per_launch_s = total("probe_kernel_ms") / 1000.0 / pl
         ach = -reduce(-(per_launch_bytes / per_launch_s / 1e9))  # slowest rank
+        fused = any(x.get("shuffle_fused") for x in sts)
         kernel = "psg_jit_scan SINK_PROBE (lineitem scan+filter+probe+agg)" if world == 1 else \
-            "psg_jit_scan SINK_MATERIALIZE (lineitem scan+filter+semi-join+partition)"
+            ("psg_jit_scan SINK_PROBE + peer-slab shuffle (lineitem scan+filter+semi-join+probe+agg, remote rows "
+             "stored to their owners over NVLink)" if fused else
+             "psg_jit_scan SINK_MATERIALIZE (lineitem scan+filter+semi-join+partition)")
         traffic, capture = ncu_traffic(args.scale, world, kernel)
         roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s", "frac": round(ach / peak, 4),
                 "traffic": traffic, "traffic_capture": capture, "kernel": kernel,
@@ -434,13 +437,18 @@ def main():
     shuffle = None
     if world > 1:
         recv = reduce(total("bytes_received") / len(sts))
-        xms = reduce(total("exchange_ms") / len(sts))
+        fused = any(x.get("shuffle_fused") for x in sts)
+        # fused (peer-slab) shuffle: the bytes move inside the probe kernel, so its time is the
+        # transfer window; else the CUDA-event time of the NCCL send/recv groups
+        xms = reduce((total("probe_kernel_ms") if fused else total("exchange_ms")) / len(sts))
         ref_recv = (0.55 + 10.39) * args.scale / 100 * 1e9 * (world - 1) / world ** 2
-        shuffle = {"bytes_received_per_gpu": int(recv), "exchange_ms": round(xms, 4),
+        shuffle = {"bytes_received_per_gpu": int(recv), "exchange_ms": round(xms, 4), "fused": fused,
                    "gbs": round(recv / 1e9 / (xms / 1000.0), 1) if xms > 0 else None, "nvlink_gbs": NVLINK_GBS,
                    "frac_of_nvlink": round(recv / 1e9 / (xms / 1000.0) / NVLINK_GBS, 4) if xms > 0 else None,
                    "reference_wire_bytes_per_gpu": int(ref_recv),
-                   "note": "semi-join-reduced, bit-packed rows (DESIGN.md §2); reference wire schema figure alongside"}
+                   "note": ("peer-slab stores from inside the probe kernel (exchange_ms = that kernel's time: the "
+                            "shuffle overlaps the scan entirely); " if fused else "") +
+                           "semi-join-reduced, bit-packed rows (DESIGN.md §2); reference wire schema figure alongside"}
 
     # ---------------- binding roofline of the end-to-end query (bench.cpp:35-40) ----------
     e2e_roof = None

@@ -105,6 +105,8 @@ typedef struct psg_stats {
   uint64_t bytes_sent;         /* shuffle payload bytes sent to peers */
   double exchange_ms;          /* summed CUDA-event time of the shuffle send/recv groups */
   uint64_t bucket_overflow;    /* rows that found their aggregation bucket full (bucketed aggregation) */
+  uint64_t shuffle_fused;      /* 1: the shuffle ran inside the probe kernel (peer-slab stores over
+                                  NVLink; bytes_received counts them, exchange_ms stays 0) */
 } psg_stats;
 
 /* ---- library ---- */

@@ -59,7 +59,7 @@ class Stats(ctypes.Structure):
                 ("device_ms", ctypes.c_double), ("result_rows", ctypes.c_uint64), ("io_wait_s", ctypes.c_double),
                 ("jit_compiles", ctypes.c_uint64), ("h2d_bytes", ctypes.c_uint64),
                 ("agg_table", ctypes.c_uint64), ("bytes_sent", ctypes.c_uint64), ("exchange_ms", ctypes.c_double),
-                ("bucket_overflow", ctypes.c_uint64)]
+                ("bucket_overflow", ctypes.c_uint64), ("shuffle_fused", ctypes.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

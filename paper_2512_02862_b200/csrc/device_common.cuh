@@ -23,6 +23,7 @@ constexpr int kMaxRegs = 26;  // interpreter smem = n_regs * 4 rows * 256 thread
 constexpr int kMaxOut = 16;
 constexpr int kMaxSums = 8;
 constexpr int kMaxParts = 64;
+constexpr int kMaxSlabPeers = 16;  // peer-slab shuffle: GPUs of one box
 constexpr int kBlock = 256;
 constexpr int kBucketSlots = 2048;  // rank-table slots per aggregation bucket (shared-memory slice)
 constexpr int kBucketBits = 11;
@@ -38,7 +39,8 @@ enum SinkKind : int {
   SINK_PROBE = 2,
   SINK_PROBE_GLOBAL = 3,
   SINK_COUNT = 4,
-  SINK_AGG_SCAN = 5
+  SINK_AGG_SCAN = 5,
+  SINK_KEYBITS = 6
 };
 
 /// One row group (or one received/materialised run): rows + a device pointer per input column.
@@ -211,11 +213,30 @@ struct ScanProgram {
   uint64_t* bkt_ovf;
   unsigned int* bkt_ovf_count;
   uint32_t bkt_ovf_cap;
+  // SINK_KEYBITS: a build side that only feeds the rank-indexed table sets bit (key - kb_min) of
+  // kb_bits for every surviving row instead of materialising it; kb_flag |= 1 when the bit was
+  // already set (a duplicate key), |= 2 for a key outside [kb_min, kb_min + kb_range); kb_count
+  // counts the rows.
+  uint32_t* kb_bits;
+  int64_t kb_min;
+  uint64_t kb_range;
+  unsigned int* kb_flag;
+  unsigned long long* kb_count;
+  // Peer-slab shuffle (SINK_PROBE at N > 1, slab = 1): after the global semi-join screen, a row
+  // owned by rank d != self_rank is bit-packed (pack_*) and stored straight into this rank's
+  // region of d's receive slab through NVLink (slab_dst[d], peer-mapped), at a position reserved
+  // with one atomic per (warp, destination) on slab_cnt[d]; rows this rank owns are probed in
+  // place. No materialisation, no count exchange, no NCCL on the data path.
+  uint64_t* slab_dst[kMaxSlabPeers];
+  unsigned long long* slab_cnt;
+  uint64_t slab_cap;
+  int32_t slab;
   // the engine guarantees 16-byte aligned column chunks and readable padding past each chunk's
   // end (PSTO batches, staged images): the query compiler may then stream the early columns into
   // shared memory with bulk copies (the warp-specialised probe, jit.cpp)
   int32_t staged_ok;
 };
+static_assert(sizeof(ScanProgram) <= 4096, "ScanProgram is a kernel parameter (4 KB limit)");
 
 #if defined(__CUDACC__) || defined(__CUDACC_RTC__)
 /// partition_of (hashing.hpp:26-37): ((k * 0x9E3779B97F4A7C15) >> 13) % n

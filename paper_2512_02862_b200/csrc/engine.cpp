@@ -43,6 +43,11 @@ namespace psg {
 struct BucketOverflow : Error {
   BucketOverflow() : Error(PSG_ERR_INTERNAL, "aggregation bucket overflow") {}
 };
+/// The key-bitmap build found what a rank-indexed table cannot hold (duplicate build keys, keys
+/// outside the zone-map range, no keys at all): the query is re-run on the materialising build path.
+struct KeybitsRetry : Error {
+  KeybitsRetry() : Error(PSG_ERR_INTERNAL, "key-bitmap build not applicable") {}
+};
 
 namespace {
 
@@ -55,6 +60,50 @@ int trace_level() {
   return lvl;
 }
 bool trace_on() { return trace_level() > 0; }
+/// A one-GPU aggregation table larger than this gets a membership screen (Bloom filter, or the
+/// exact key bitmap / rank-indexed table). PSG_SCREEN_MIN_MB overrides the 48 MB default (0:
+/// always - lets small parity cases exercise the bitmap and rank-table paths).
+uint64_t screen_min_bytes() {
+  static const uint64_t v = [] {
+    const char* e = std::getenv("PSG_SCREEN_MIN_MB");
+    return (e ? std::strtoull(e, nullptr, 10) : 48ull) << 20;
+  }();
+  return v;
+}
+/// PSG_KBITS: 1 (default) = exact key bitmaps at every N, 2 = at N > 1 also when the rank table
+/// is off (hashed table + exact screen), 0 = Bloom filters only.
+int kbits_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("PSG_KBITS");
+    return e ? std::atoi(e) : 1;
+  }();
+  return v;
+}
+/// PSG_RANK_TABLE=0: the hashed aggregation table instead of the rank-indexed one.
+bool rank_table_env() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_RANK_TABLE");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+/// PSG_KEYBITS=0: the build side of a rank-indexed table is materialised and shuffled instead of
+/// being scanned straight into the key bitmap.
+bool keybits_env() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_KEYBITS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+/// PSG_SLAB=0: the NCCL shuffle of packed probe rows instead of the peer-slab stores.
+bool slab_env() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_SLAB");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 #define PSG_TRACE_MSG(...)                  \
   do {                                      \
     if (trace_on()) {                       \
@@ -477,6 +526,7 @@ class Execution {
       : ctx_(ctx), mode_(mode), staged_(staged), plan_(QueryPlan::from_json_text(plan_json, data_root, ctx.rank, ctx.nranks)) {}
   ~Execution() {
     if (build_pending_) cudaStreamSynchronize(ctx_.comm);  // (error paths) before the tables go
+    for (auto& e : timed_) cudaEventDestroy(e.first), cudaEventDestroy(e.second);
   }
 
   ResultRows run(bool want_rows);
@@ -515,6 +565,27 @@ class Execution {
   DevCols materialize_chain(const SourceDef& s, const RegMap& m, const BatchView& v, const std::vector<int>& out_regs);
   DevCols concat_cols(std::vector<DevCols>& parts, size_t ncols);
   uint64_t read_count(DevCols& c);
+  // event pairs around the timed (dominant) kernel launches, resolved after the query's last sync
+  // (no host sync per launch)
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed_;
+  void resolve_timed() {
+    for (auto& e : timed_) {
+      float ms = 0;
+      PSG_CUDA(cudaEventElapsedTime(&ms, e.first, e.second));
+      st_.probe_kernel_ms += ms;
+      cudaEventDestroy(e.first), cudaEventDestroy(e.second);
+    }
+    timed_.clear();
+  }
+  /// Widens [lo, hi] by the footer zone maps of column fcol over the files (cached per footer).
+  void zone_range(const std::vector<std::string>& paths, int fcol, long long& lo, long long& hi) {
+    for (const auto& path : paths) {
+      auto m = ctx_.footers.get(path);
+      if (fcol < 0 || static_cast<size_t>(fcol) >= m->zmin.size()) continue;
+      lo = std::min<long long>(lo, m->zmin[fcol]);
+      hi = std::max<long long>(hi, m->zmax[fcol]);
+    }
+  }
   void run_scan(const ScanProgram& p, const BatchView& v, bool timed, cudaStream_t stream = nullptr);
 
   // shuffle (nranks > 1)
@@ -560,7 +631,18 @@ class Execution {
   bool bucket_mode_ = false;
   BucketDev bd_{};
   uint64_t nbuckets_ = 0;
-  bool setup_buckets();
+  /// Bucketed aggregation; at N > 1 (peer-slab shuffle) the probe sums' value ranges are the
+  /// all-reduced ones (prange_lo/hi, probe_sum_wire order) and probe_rows the global total, so
+  /// every rank encodes alike and sizes its buckets for the rows it will own.
+  bool setup_buckets(const int64_t* prange_lo = nullptr, const int64_t* prange_hi = nullptr, uint64_t probe_rows_all = 0);
+  /// Symmetric heap of at least `bytes` (collective; every rank passes the same value).
+  bool ensure_symmetric(size_t bytes);
+  // peer-slab shuffle (N > 1): counters and receive slab in the symmetric heap
+  bool slab_mode_ = false;
+  PackLayout slab_pack_;
+  uint64_t slab_cap_ = 0;
+  size_t slab_cnt_off_ = 0, slab_off_ = 0;
+  DevBuf slab_recv_;
   void apply_buckets(ScanProgram& p) const;
   void finalize_buckets(ResultRows& out, bool want_rows);
   AggTableDev aggt_{};
@@ -1100,14 +1182,16 @@ uint64_t Execution::read_count(DevCols& c) {
 void Execution::run_scan(const ScanProgram& p, const BatchView& v, bool timed, cudaStream_t stream) {
   if (v.nsegs == 0) return;
   cudaStream_t st = stream ? stream : ctx_.compute;
-  if (timed) PSG_CUDA(cudaEventRecord(ctx_.ev_a, st));
+  std::pair<cudaEvent_t, cudaEvent_t> ev{nullptr, nullptr};
+  if (timed) {
+    PSG_CUDA(cudaEventCreate(&ev.first));
+    PSG_CUDA(cudaEventCreate(&ev.second));
+    timed_.push_back(ev);
+    PSG_CUDA(cudaEventRecord(ev.first, st));
+  }
   fused_scan(p, v.d_segs, v.d_tile_seg, v.nsegs, v.ntiles, st);
   if (timed) {
-    PSG_CUDA(cudaEventRecord(ctx_.ev_b, st));
-    PSG_CUDA(cudaEventSynchronize(ctx_.ev_b));
-    float ms = 0;
-    PSG_CUDA(cudaEventElapsedTime(&ms, ctx_.ev_a, ctx_.ev_b));
-    st_.probe_kernel_ms += ms;
+    PSG_CUDA(cudaEventRecord(ev.second, st));
     st_.probe_kernel_launches += 1;
     st_.probe_kernel_bytes += v.bytes;
   }
@@ -1208,13 +1292,7 @@ void Execution::build_local_tables() {
       if (np == 0 && n > 0 && bitmap_env()) {
         // key range from the replicated scan's footer zone maps (a superset of the surviving keys)
         long long lohi[2] = {LLONG_MAX, LLONG_MIN};
-        const int fcol = lj.proj.file_idx[lj.key_idx];
-        for (const auto& path : lj.scan->paths)
-          for (const auto& g : ctx_.footers.get(path)->groups)
-            if (g.rows) {
-              lohi[0] = std::min(lohi[0], static_cast<long long>(g.cols[fcol].min_raw));
-              lohi[1] = std::max(lohi[1], static_cast<long long>(g.cols[fcol].max_raw));
-            }
+        zone_range(lj.scan->paths, lj.proj.file_idx[lj.key_idx], lohi[0], lohi[1]);
         const uint64_t range = static_cast<uint64_t>(lohi[1]) - static_cast<uint64_t>(lohi[0]) + 1;
         if (range != 0 && range <= (1ULL << 34) && range / 64 <= n) {
           const uint64_t words = (range + 31) / 32;
@@ -1320,7 +1398,7 @@ void Execution::build_agg_table(uint64_t build_rows, uint64_t bloom_words, uint6
 /// with the slot's low bits, in one 64-bit word. Bucket capacity: the expected survivors (probe
 /// rows x the build keys' share of the key range) / buckets x 1.5; overflow is applied directly.
 /// PSG_BUCKETS=0: off.
-bool Execution::setup_buckets() {
+bool Execution::setup_buckets(const int64_t* prange_lo, const int64_t* prange_hi, uint64_t probe_rows_all) {
   static const bool env = [] {
     const char* e = std::getenv("PSG_BUCKETS");
     return !(e && e[0] == '0');
@@ -1329,19 +1407,17 @@ bool Execution::setup_buckets() {
   if (!env || ctx_.no_buckets || !jit_available() || np > 3 || aggt_.krange == 0 || agg_cap_ == 0) return false;
   BucketDev bd{};
   int shift = kBucketBits;
-  uint64_t probe_rows = 0;
-  for (const auto& path : psrc_.scan->paths) probe_rows += ctx_.footers.get(path)->total_rows();
+  uint64_t probe_rows = probe_rows_all;
+  if (!probe_rows)
+    for (const auto& path : psrc_.scan->paths) probe_rows += ctx_.footers.get(path)->total_rows();
   for (int k = 0; k < np; ++k) {
     const ColRef ref = psrc_.stage_refs.back()[probe_sum_wire[k]];
     if (ref.join >= 0 || psrc_.wire.fields[probe_sum_wire[k]].type != LType::Int64) return false;
     long long lo = LLONG_MAX, hi = LLONG_MIN;
-    const int fcol = psrc_.proj.file_idx[ref.idx];
-    for (const auto& path : psrc_.scan->paths)
-      for (const auto& g : ctx_.footers.get(path)->groups)
-        if (g.rows) {
-          lo = std::min(lo, static_cast<long long>(g.cols[fcol].min_raw));
-          hi = std::max(hi, static_cast<long long>(g.cols[fcol].max_raw));
-        }
+    if (prange_lo)
+      lo = prange_lo[k], hi = prange_hi[k];
+    else
+      zone_range(psrc_.scan->paths, psrc_.proj.file_idx[ref.idx], lo, hi);
     if (hi < lo) lo = hi = 0;
     const uint64_t span = static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo);
     const int w = span ? 64 - __builtin_clzll(span) : 0;
@@ -1417,13 +1493,24 @@ void Execution::finalize_buckets(ResultRows& out, bool want_rows) {
   DevBuf rows(ctx_.pool, std::max<uint64_t>(agg_cap_, 1) * nc * 8, ctx_.compute);
   launch_bucket_emit(aggt_, bd_, nbuckets_, agg_cap_, state.as<unsigned long long>(), ticket.as<unsigned int>(),
                      first_word.as<uint32_t>(), nc, kind.data(), idx.data(), rows.as<uint64_t>(), ctx_.compute);
-  unsigned long long last = 0;
+  unsigned long long last = 0, recv = 0;
   unsigned int novf = 0;
   PSG_CUDA(cudaMemcpyAsync(&last, state.as<unsigned long long>() + (nbuckets_ - 1), 8, cudaMemcpyDeviceToHost,
                            ctx_.compute));
-  PSG_CUDA(cudaMemcpyAsync(&novf, bd_.ovf_count, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+  if (ctx_.nranks > 1) {  // the re-run decision is collective: the largest overflow of any rank
+    DevBuf o(ctx_.pool, 4, ctx_.compute);
+    PSG_NCCL(ncclAllReduce(bd_.ovf_count, o.p, 1, ncclUint32, ncclMax, ctx_.nccl, ctx_.compute));
+    PSG_CUDA(cudaMemcpyAsync(&novf, o.p, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+  } else {
+    PSG_CUDA(cudaMemcpyAsync(&novf, bd_.ovf_count, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+  }
+  if (slab_recv_.p) PSG_CUDA(cudaMemcpyAsync(&recv, slab_recv_.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   st_.bucket_overflow = novf;
+  if (slab_recv_.p) {
+    st_.bytes_received += recv * 8;
+    st_.shuffle_fused = 1;
+  }
   if (novf > bd_.ovf_cap) throw BucketOverflow();  // execute_plan re-runs the query without buckets
   const uint64_t ng = last & ((1ULL << 62) - 1);
   out.nrows = ng;
@@ -1460,13 +1547,7 @@ void Execution::pack_accumulators() {
     if (ref.join >= 0 || psrc_.wire.fields[probe_sum_wire[k]].type != LType::Int64) {
       lo = LLONG_MIN, hi = LLONG_MAX;
     } else {
-      const int fcol = psrc_.proj.file_idx[ref.idx];
-      for (const auto& path : psrc_.scan->paths)
-        for (const auto& g : ctx_.footers.get(path)->groups)
-          if (g.rows) {
-            lo = std::min(lo, static_cast<long long>(g.cols[fcol].min_raw));
-            hi = std::max(hi, static_cast<long long>(g.cols[fcol].max_raw));
-          }
+      zone_range(psrc_.scan->paths, psrc_.proj.file_idx[ref.idx], lo, hi);
     }
     mm[k] = ~lo;
     mm[np + k] = hi;
@@ -1539,6 +1620,16 @@ bool Execution::build_symmetric_agg_table(uint64_t max_rows, bool bloom) {
   }
   launch_agg_init(aggt_, agg_cap_, ctx_.compute);
   return true;
+}
+
+bool Execution::ensure_symmetric(size_t bytes) {
+  if (ctx_.symm_bytes >= bytes) return true;
+  if (ctx_.symm_failed) return false;
+  // collective: grow every rank's heap together (1 GiB granules), re-mapping the peers' heaps
+  ctx_.free_symmetric_heap();
+  ctx_.init_symmetric_heap((bytes + (1ull << 30) - 1) & ~((1ull << 30) - 1));
+  if (ctx_.symm_bytes == 0) ctx_.symm_failed = true;  // (all ranks voted alike)
+  return ctx_.symm_bytes >= bytes;
 }
 
 /// Device-side barrier across ranks: a one-word all-reduce on the compute stream completes only
@@ -1807,7 +1898,94 @@ ResultRows Execution::run(bool want_rows) {
   const bool p2p = nr > 1 && agg_ && grouped_ && ctx_.p2p && ctx_.symm_bytes > 0 && jit_available() && !bdup && !pdup;
   ctx_.symm_top = 0;
   DevBuf owner_hist;
-  if (nr == 1 || p2p) {
+  // Key-bitmap build: a grouped aggregate over a rank-indexed table whose build side carries
+  // nothing but unique keys (Q3's orders) needs only the SET of build keys. The build scan then
+  // sets each surviving key's bit in a bitmap over the zone-map key range (SINK_KEYBITS) - no
+  // build rows are materialised, and at N > 1 none are shuffled: a SUM all-reduce of the rank
+  // bitmaps (disjoint when the keys are unique; checked) is the global key set, the semi-join
+  // screen of the probe side, and each rank keeps the bits it owns (partition_of) as its table.
+  // Every decision below comes from all-reduced values, so all ranks agree. PSG_KEYBITS=0: off.
+  bool kb_direct = false;
+  long long kb_lo = 0;
+  uint64_t kb_range = 0;
+  DevBuf kb_cnt;  // [rows that set a bit (u64), flag (u32)]
+  // peer-slab shuffle inputs, from the same all-reduce (N > 1): the probe columns' zone ranges
+  // (bit-packed rows) and the largest probe side (slab capacity)
+  std::vector<int64_t> slab_plo, slab_phi;
+  uint64_t slab_max_rows = 0, probe_rows_all = 0;
+  if (keybits_env() && agg_ && grouped_ && !p2p && !bdup && !ctx_.no_keybits && jit_available() && rank_table_env() &&
+      kbits_mode() >= 1 && b_out.size() == 1 && build_sum_wire.empty() && ctx_.semijoin) {
+    const ColRef kref = bsrc_.stage_refs.back()[bkey];
+    if (kref.join < 0) {
+      const size_t np = pneed.size();
+      // MAX-reduced: [~lo, hi, probe rows, ~plo[k], phi[k]...]; SUM-reduced: [build rows, probe rows]
+      std::vector<long long> mx(3 + 2 * np), sm(2, 0);
+      long long lo = LLONG_MAX, hi = LLONG_MIN;
+      zone_range(bsrc_.scan->paths, bsrc_.proj.file_idx[kref.idx], lo, hi);
+      for (const auto& path : bsrc_.scan->paths) sm[0] += static_cast<long long>(ctx_.footers.get(path)->total_rows());
+      for (const auto& path : psrc_.scan->paths) sm[1] += static_cast<long long>(ctx_.footers.get(path)->total_rows());
+      mx[0] = ~lo, mx[1] = hi, mx[2] = sm[1];
+      for (size_t k = 0; k < np; ++k) {
+        long long a = LLONG_MAX, b = LLONG_MIN;
+        const ColRef ref = psrc_.stage_refs.back()[pneed[k]];
+        if (ref.join >= 0 || psrc_.wire.fields[pneed[k]].type != LType::Int64)
+          a = LLONG_MIN, b = LLONG_MAX;  // not bounded by the zone maps: never packs
+        else
+          zone_range(psrc_.scan->paths, psrc_.proj.file_idx[ref.idx], a, b);
+        mx[3 + k] = ~a, mx[3 + np + k] = b;
+      }
+      if (nr > 1) {
+        DevBuf red(ctx_.pool, (mx.size() + sm.size()) * 8, ctx_.compute);
+        long long* d = red.as<long long>();
+        PSG_CUDA(cudaMemcpyAsync(d, mx.data(), mx.size() * 8, cudaMemcpyHostToDevice, ctx_.compute));
+        PSG_CUDA(cudaMemcpyAsync(d + mx.size(), sm.data(), sm.size() * 8, cudaMemcpyHostToDevice, ctx_.compute));
+        PSG_NCCL(ncclAllReduce(d, d, mx.size(), ncclInt64, ncclMax, ctx_.nccl, ctx_.compute));
+        PSG_NCCL(ncclAllReduce(d + mx.size(), d + mx.size(), sm.size(), ncclInt64, ncclSum, ctx_.nccl, ctx_.compute));
+        PSG_CUDA(cudaMemcpyAsync(mx.data(), d, mx.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+        PSG_CUDA(cudaMemcpyAsync(sm.data(), d + mx.size(), sm.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+        PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      }
+      lo = ~mx[0], hi = mx[1];
+      slab_max_rows = static_cast<uint64_t>(mx[2]);
+      probe_rows_all = static_cast<uint64_t>(sm[1]);
+      for (size_t k = 0; k < np; ++k) slab_plo.push_back(~mx[3 + k]), slab_phi.push_back(mx[3 + np + k]);
+      const uint64_t rows = static_cast<uint64_t>(sm[0]);
+      const uint64_t range = hi >= lo ? static_cast<uint64_t>(hi) - static_cast<uint64_t>(lo) + 1 : 0;
+      // the same tests as the materialising path, on the footer row count: a table big enough to
+      // want a screen (one GPU), and a bitmap no larger than the Bloom filter it replaces
+      const uint64_t cap = pow2_at_least(std::max<uint64_t>(2 * rows, 16));
+      const int hw_est = 2 + static_cast<int>(probe_sum_wire.size()) <= 4 ? 4 : 8;
+      const uint64_t bloom = std::min<uint64_t>(pow2_at_least(std::max<uint64_t>(rows / 2, 1024)), 8ull << 20);
+      const bool screen = nr > 1 || (cap + 1) * hw_est * 8 > screen_min_bytes();
+      if (screen && range != 0 && range <= (1ULL << 36) && lo != LLONG_MIN && range / 32 <= bloom * static_cast<uint64_t>(nr) &&
+          (range + 63) / 64 < (1ULL << 32)) {
+        kb_direct = true;
+        kb_lo = lo;
+        kb_range = range;
+      }
+    }
+  }
+  if (kb_direct) {
+    const uint64_t words64 = (kb_range + 63) / 64;
+    agg_kbits_ = DevBuf(ctx_.pool, words64 * 8, ctx_.compute);
+    kb_cnt = DevBuf(ctx_.pool, 16, ctx_.compute);
+    PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, words64 * 8, ctx_.compute));
+    PSG_CUDA(cudaMemsetAsync(kb_cnt.p, 0, 16, ctx_.compute));
+    ScanProgram p = bp;
+    p.sink = SINK_KEYBITS;
+    p.key_reg = b_out[0];
+    p.kb_bits = agg_kbits_.as<uint32_t>();
+    p.kb_min = kb_lo;
+    p.kb_range = kb_range;
+    p.kb_count = kb_cnt.as<unsigned long long>();
+    p.kb_flag = reinterpret_cast<unsigned int*>(kb_cnt.as<unsigned long long>() + 1);
+    BatchView v;
+    while (bfeed->next(v)) {
+      run_scan(p, v, false);
+      bfeed->done();
+      st_.ingest_bytes += v.bytes;
+    }
+  } else if (nr == 1 || p2p) {
     bmat = alloc_cols(b_out.size(), std::max<uint64_t>(bfeed->total_rows, 1));
     if (p2p) {
       owner_hist = DevBuf(ctx_.pool, nr * 8, ctx_.compute);
@@ -1886,7 +2064,9 @@ ResultRows Execution::run(bool want_rows) {
     return p;
   };
   std::vector<Segment> bsegs;
-  if (nr == 1 || p2p) {
+  if (kb_direct) {
+    // (no build rows: the key bitmap is the whole build side)
+  } else if (nr == 1 || p2p) {
     Segment sg;
     std::memset(&sg, 0, sizeof sg);
     for (size_t c = 0; c < b_out.size(); ++c) sg.col[c] = bmat.cols[c].as<uint64_t>();
@@ -1908,7 +2088,7 @@ ResultRows Execution::run(bool want_rows) {
   DevBuf semi_all;
   uint64_t bloom_words = 0;
   const bool semi = agg_ && nr > 1 && ctx_.semijoin && !p2p;
-  if (agg_) {
+  if (agg_ && !kb_direct) {
     uint64_t sized_rows = build_rows;
     if (semi) {
       DevBuf mv(ctx_.pool, 8, ctx_.compute);
@@ -1919,14 +2099,8 @@ ResultRows Execution::run(bool want_rows) {
     }
     const uint64_t cap = pow2_at_least(std::max<uint64_t>(2 * build_rows, 16));
     const int hw_est = 2 + static_cast<int>(probe_sum_wire.size()) <= 4 ? 4 : 8;
-    // A one-GPU table larger than ~L2/2.5 gets a membership screen (Bloom filter, or the exact key
-    // bitmap / rank-indexed table below). PSG_SCREEN_MIN_MB overrides the 48 MB threshold (0: always
-    // - lets small parity cases exercise the bitmap and rank-table paths).
-    static const uint64_t screen_min = [] {
-      const char* e = std::getenv("PSG_SCREEN_MIN_MB");
-      return (e ? std::strtoull(e, nullptr, 10) : 48ull) << 20;
-    }();
-    if (semi || ((cap + 1) * hw_est * 8 > screen_min && ctx_.semijoin))
+    // a one-GPU table larger than ~L2/2.5 gets a membership screen (screen_min_bytes)
+    if (semi || ((cap + 1) * hw_est * 8 > screen_min_bytes() && ctx_.semijoin))
       bloom_words = std::min<uint64_t>(pow2_at_least(std::max<uint64_t>(sized_rows / 2, 1024)), 8ull << 20);
   }
   DevBuf peers_dev;
@@ -1974,25 +2148,44 @@ ResultRows Execution::run(bool want_rows) {
     // rank sets its own bitmap over the ALL-REDUCED key range from the build keys it owns; the OR
     // of the rank bitmaps (a SUM all-reduce: owners are disjoint) is the exact semi-join screen of
     // the probe side, and a rank's own bitmap indexes its rank-indexed table.
-    // PSG_KBITS: 1 (default) = exact bitmaps at every N, 2 = at N > 1 also when the rank table is
-    // off (hashed table + exact screen), 0 = Bloom filters only.
-    static const int kbits_mode = [] {
-      const char* e = std::getenv("PSG_KBITS");
-      return e ? std::atoi(e) : 1;
-    }();
-    const bool kbits_env = kbits_mode >= 1;
+    const bool kbits_env = kbits_mode() >= 1;
     // Rank-indexed table (grouped, unique dense build keys): the key bitmap is set from the build
     // keys first (with a duplicate check) and its 64-bit words' popcount prefix turns a key into
     // its rank = its slot; the table is then exactly one slot per build key in key order, written
     // by plain stores. PSG_RANK_TABLE=0: the hashed table.
-    static const bool rank_env = [] {
-      const char* e = std::getenv("PSG_RANK_TABLE");
-      return !(e && e[0] == '0');
-    }();
+    const bool rank_env = rank_table_env();
     long long krange_lo = 0;
     uint64_t krange = 0;
     const bool rank_ok = grouped_ && rank_env && jit_available() && !p2p;
-    if (nr > 1 && semi && kbits_env && (rank_ok || kbits_mode >= 2)) {
+    if (kb_direct) {
+      // the key bitmap was set by the build scan itself: N > 1 all-reduces it into the global key
+      // set (semi_all) and keeps the bits this rank owns; one host read checks the key counts
+      const uint64_t words64 = (kb_range + 63) / 64;
+      DevBuf cnts(ctx_.pool, 16, ctx_.compute);  // [own bits, global bits]
+      PSG_CUDA(cudaMemsetAsync(cnts.p, 0, 16, ctx_.compute));
+      if (nr > 1) {
+        semi_all = DevBuf(ctx_.pool, words64 * 8, ctx_.compute);
+        PSG_NCCL(ncclAllReduce(agg_kbits_.p, semi_all.p, words64, ncclUint64, ncclSum, ctx_.nccl, ctx_.compute));
+        PSG_NCCL(ncclAllReduce(kb_cnt.p, kb_cnt.p, 1, ncclUint64, ncclSum, ctx_.nccl, ctx_.compute));
+        PSG_NCCL(ncclAllReduce(kb_cnt.as<unsigned long long>() + 1, kb_cnt.as<unsigned long long>() + 1, 1, ncclUint64,
+                               ncclMax, ctx_.nccl, ctx_.compute));
+        launch_own_mask(semi_all.as<unsigned long long>(), agg_kbits_.as<unsigned long long>(), words64, kb_lo, nr,
+                        ctx_.rank, cnts.as<unsigned long long>(), ctx_.compute);
+      }
+      uint64_t h[4] = {0, 0, 0, 0};
+      PSG_CUDA(cudaMemcpyAsync(h, kb_cnt.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      pt.mark("  key bitmap (all-reduce, own bits)", ctx_.compute);
+      const uint64_t rows_set = h[0], flag = h[1];
+      // duplicates within a rank set the flag; across ranks the SUM carried, so the global bit
+      // count falls short of the rows that set bits
+      if (flag != 0 || rows_set == 0 || rows_set >= (1ULL << 32) || (nr > 1 && h[3] != rows_set)) throw KeybitsRetry();
+      build_rows = nr > 1 ? h[2] : rows_set;
+      krange_lo = kb_lo;
+      krange = kb_range;
+      bloom_words = 0;
+    } else if (nr > 1 && semi && kbits_env && (rank_ok || kbits_mode() >= 2)) {
       DevBuf mm(ctx_.pool, 16, ctx_.compute);
       const long long init[2] = {LLONG_MAX, LLONG_MIN};
       PSG_CUDA(cudaMemcpyAsync(mm.p, init, 16, cudaMemcpyHostToDevice, ctx_.compute));
@@ -2020,13 +2213,7 @@ ResultRows Execution::run(bool want_rows) {
       long long lohi[2] = {LLONG_MAX, LLONG_MIN};
       const ColRef kref = bsrc_.stage_refs.back()[bkey];
       if (kref.join < 0) {
-        const int fcol = bsrc_.proj.file_idx[kref.idx];
-        for (const auto& path : bsrc_.scan->paths)
-          for (const auto& g : ctx_.footers.get(path)->groups)
-            if (g.rows) {
-              lohi[0] = std::min(lohi[0], static_cast<long long>(g.cols[fcol].min_raw));
-              lohi[1] = std::max(lohi[1], static_cast<long long>(g.cols[fcol].max_raw));
-            }
+        zone_range(bsrc_.scan->paths, bsrc_.proj.file_idx[kref.idx], lohi[0], lohi[1]);
       } else {
         DevBuf mm(ctx_.pool, 16, ctx_.compute);
         PSG_CUDA(cudaMemcpyAsync(mm.p, lohi, 16, cudaMemcpyHostToDevice, ctx_.compute));
@@ -2043,8 +2230,22 @@ ResultRows Execution::run(bool want_rows) {
     }
     bool rank_mode = false;
     const uint64_t kwords64 = (krange + 63) / 64;
-    if (krange && rank_ok && krange_lo != LLONG_MIN && kwords64 < (1ULL << 32) && build_rows > 0 &&
-        build_rows < (1ULL << 32)) {
+    auto rank_records = [&] {  // popcount prefix per 64-bit word + interleaved {bits, rank} records
+      DevBuf cnt(ctx_.pool, kwords64 * 4, ctx_.compute);
+      agg_krank_ = DevBuf(ctx_.pool, kwords64 * 4, ctx_.compute);
+      launch_popc64(agg_kbits_.as<unsigned long long>(), kwords64, cnt.as<uint32_t>(), ctx_.compute);
+      const size_t tb = exclusive_scan_u32(nullptr, nullptr, kwords64, nullptr, 0, ctx_.compute);
+      DevBuf tmp(ctx_.pool, tb, ctx_.compute);
+      exclusive_scan_u32(cnt.as<uint32_t>(), agg_krank_.as<uint32_t>(), kwords64, tmp.p, tb, ctx_.compute);
+      agg_krec_ = DevBuf(ctx_.pool, kwords64 * 16, ctx_.compute);
+      launch_krec_build(agg_kbits_.as<unsigned long long>(), agg_krank_.as<uint32_t>(), kwords64,
+                        agg_krec_.as<unsigned long long>(), ctx_.compute);
+    };
+    if (kb_direct) {
+      rank_records();
+      rank_mode = true;
+    } else if (krange && rank_ok && krange_lo != LLONG_MIN && kwords64 < (1ULL << 32) && build_rows > 0 &&
+               build_rows < (1ULL << 32)) {
       agg_kbits_ = DevBuf(ctx_.pool, kwords64 * 8, ctx_.compute);
       DevBuf dup(ctx_.pool, 4, ctx_.compute);
       PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, kwords64 * 8, ctx_.compute));
@@ -2056,20 +2257,13 @@ ResultRows Execution::run(bool want_rows) {
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
       pt.mark("  key bitmap + dup check", ctx_.compute);
       if (!d) {
-        DevBuf cnt(ctx_.pool, kwords64 * 4, ctx_.compute);
-        agg_krank_ = DevBuf(ctx_.pool, kwords64 * 4, ctx_.compute);
-        launch_popc64(agg_kbits_.as<unsigned long long>(), kwords64, cnt.as<uint32_t>(), ctx_.compute);
-        const size_t tb = exclusive_scan_u32(nullptr, nullptr, kwords64, nullptr, 0, ctx_.compute);
-        DevBuf tmp(ctx_.pool, tb, ctx_.compute);
-        exclusive_scan_u32(cnt.as<uint32_t>(), agg_krank_.as<uint32_t>(), kwords64, tmp.p, tb, ctx_.compute);
-        agg_krec_ = DevBuf(ctx_.pool, kwords64 * 16, ctx_.compute);
-        launch_krec_build(agg_kbits_.as<unsigned long long>(), agg_krank_.as<uint32_t>(), kwords64,
-                          agg_krec_.as<unsigned long long>(), ctx_.compute);
+        rank_records();
         rank_mode = true;
       }
     }
     pt.mark("  rank records", ctx_.compute);
-    build_agg_table(build_rows, bloom_words, rank_mode ? build_rows : 0);
+    // (a rank that owns no keys at N > 1 keeps a one-slot table nobody probes)
+    build_agg_table(build_rows, bloom_words, rank_mode ? std::max<uint64_t>(build_rows, 1) : 0);
     st_.agg_table = rank_mode ? 4 : (krange ? 3 : (bloom_words ? 2 : 1));
     if (krange) {
       if (!rank_mode) {  // the insert below sets the bits
@@ -2086,11 +2280,43 @@ ResultRows Execution::run(bool want_rows) {
       }
     }
     pt.mark("  agg table", ctx_.compute);
-    pack_accumulators();
-    pt.mark("  pack accumulators", ctx_.compute);
     // one GPU, rank table, fused probe: bucketed aggregation (the hot table is then only the target
     // of bucket overflow - zeroed instead of initialised with keys)
-    if (rank_mode && nr == 1 && grouped_ && !pdup) bucket_mode_ = setup_buckets();
+    // Peer-slab shuffle (N > 1, key-bitmap build): probe rows owned by another rank travel as one
+    // bit-packed word stored by the probe kernel straight into the owner's receive slab over
+    // NVLink (symmetric heap, one region per source rank, sized for the largest probe side), the
+    // owners fold them into their buckets after a device-side barrier. PSG_SLAB=0: NCCL shuffle.
+    // (every input of these decisions is all-reduced or plan-wide: all ranks agree)
+    bool slab_cand = false;
+    PackLayout slab_layout;
+    uint64_t slab_cap = 0;
+    if (kb_direct && nr > 1 && !pdup && slab_env() && !ctx_.no_buckets && nr <= kMaxSlabPeers && pneed.size() >= 2 &&
+        pneed.size() <= 4 && slab_plo.size() == pneed.size()) {
+      slab_layout = plan_pack(slab_plo.data(), slab_phi.data(), static_cast<int>(pneed.size()));
+      slab_cap = std::max<uint64_t>(slab_max_rows, 1);
+      const size_t need = 512 + static_cast<size_t>(nr) * slab_cap * 8;
+      const bool budget_ok = plan_.memory_budget_bytes == 0 || need <= plan_.memory_budget_bytes / 2;
+      slab_cand = slab_layout.fits && budget_ok && ensure_symmetric(need);
+    }
+    if (rank_mode && (nr == 1 || slab_cand) && grouped_ && !pdup)
+      bucket_mode_ = slab_cand ? setup_buckets(slab_plo.data() + 1, slab_phi.data() + 1, probe_rows_all) : setup_buckets();
+    if (slab_cand && bucket_mode_) {
+      ctx_.symm_top = 0;
+      uint8_t* cnt = ctx_.symm_alloc(static_cast<size_t>(nr) * 8);
+      uint8_t* slab = ctx_.symm_alloc(static_cast<size_t>(nr) * slab_cap * 8);
+      if (!cnt || !slab) throw Error(PSG_ERR_INTERNAL, "symmetric heap layout");
+      slab_mode_ = true;
+      slab_pack_ = std::move(slab_layout);
+      slab_cap_ = slab_cap;
+      slab_cnt_off_ = static_cast<size_t>(cnt - ctx_.symm);
+      slab_off_ = static_cast<size_t>(slab - ctx_.symm);
+    } else if (nr > 1) {
+      bucket_mode_ = false;  // the NCCL shuffle's consume kernel updates the table directly
+    }
+    // packed accumulators serve the hot table's atomics: not needed when buckets take every row
+    // (a collective at N > 1; bucket_mode_ is the same on every rank)
+    if (!bucket_mode_) pack_accumulators();
+    pt.mark("  pack accumulators", ctx_.compute);
     pt.mark("  agg alloc+init", ctx_.compute);
     ScanProgram p = batch_program(static_cast<int>(b_out.size()));
     p.sink = SINK_BUILD;
@@ -2131,6 +2357,8 @@ ResultRows Execution::run(bool want_rows) {
     }
     if (build_pending_) {
       // (the Bloom filters were all-gathered above)
+    } else if (kb_direct) {
+      // (semi_all is the all-reduced global key bitmap already)
     } else if (semi && krange) {  // disjoint bits: SUM == OR; out of place (the rank keeps its own)
       const uint64_t words = (krange + 31) / 32;
       semi_all = DevBuf(ctx_.pool, words * 4, ctx_.compute);
@@ -2307,6 +2535,76 @@ ResultRows Execution::run(bool want_rows) {
       st_.ingest_bytes += v.bytes;
     }
     gpu_barrier();  // every rank's probe contributions landed before owners finalise
+  } else if (slab_mode_) {
+    // peer-slab shuffle: one fused kernel per probe batch - predicate, global semi-join screen,
+    // late columns, owned rows probed in place, other rows stored into their owner's slab over
+    // NVLink; then a device-side barrier and the owners fold what they received
+    ScanProgram p = pp;
+    p.sink = SINK_PROBE;
+    p.staged_ok = 1;
+    p.agg = aggt_;
+    p.key_reg = pm.reg_of.at(psrc_.stage_refs.back()[pkey]);
+    p.n_sum = static_cast<int>(probe_sum_wire.size());
+    for (int k = 0; k < p.n_sum; ++k) p.sum_reg[k] = pm.reg_of.at(psrc_.stage_refs.back()[probe_sum_wire[k]]);
+    apply_buckets(p);
+    const int np = static_cast<int>(pneed.size());
+    p.pack_n = np;
+    for (int k = 0; k < np; ++k) {
+      p.pack_reg[k] = p_out[k];
+      p.pack_min[k] = slab_pack_.min[k];
+      p.pack_shift[k] = slab_pack_.shift[k];
+      p.pack_mask[k] = slab_pack_.mask[k];
+    }
+    p.slab = 1;
+    p.nparts = nr;
+    p.self_rank = ctx_.rank;
+    p.slab_cap = slab_cap_;
+    unsigned long long* my_cnt = reinterpret_cast<unsigned long long*>(ctx_.symm + slab_cnt_off_);
+    p.slab_cnt = my_cnt;
+    for (int d = 0; d < nr; ++d)
+      p.slab_dst[d] = d == ctx_.rank ? nullptr
+                                     : reinterpret_cast<uint64_t*>(ctx_.symm_peer[d] + slab_off_) + static_cast<uint64_t>(ctx_.rank) * slab_cap_;
+    // (the previous query's readers of these counters finished before this query's all-reduce)
+    PSG_CUDA(cudaMemsetAsync(my_cnt, 0, static_cast<size_t>(nr) * 8, ctx_.compute));
+    BatchView v;
+    while (pfeed->next(v)) {
+      run_scan(p, v, staged_ != nullptr);
+      pfeed->done();
+      st_.ingest_bytes += v.bytes;
+    }
+    pt.mark("  probe + slab stores", ctx_.compute);
+    gpu_barrier();  // every source's slab stores landed
+    pt.mark("  barrier", ctx_.compute);
+    SlabConsume c{};
+    c.slab = reinterpret_cast<const uint64_t*>(ctx_.symm + slab_off_);
+    for (int r = 0; r < nr; ++r)
+      c.src_cnt[r] = r == ctx_.rank ? nullptr
+                                    : reinterpret_cast<const unsigned long long*>(ctx_.symm_peer[r] + slab_cnt_off_) + ctx_.rank;
+    c.cap = slab_cap_;
+    c.nsrc = nr;
+    c.npack = np;
+    for (int k = 0; k < np; ++k) {
+      c.pshift[k] = slab_pack_.shift[k];
+      c.pmask[k] = slab_pack_.mask[k];
+      c.pmin[k] = slab_pack_.min[k];
+    }
+    c.bkt = p.bkt;
+    c.fill = p.bkt_fill;
+    c.bcap = p.bkt_cap;
+    for (int k = 0; k < kMaxSums; ++k) {
+      c.bshift[k] = p.bkt_shift[k];
+      c.bmask[k] = p.bkt_mask[k];
+      c.bmin[k] = p.bkt_min[k];
+    }
+    c.ovf = p.bkt_ovf;
+    c.ovf_count = p.bkt_ovf_count;
+    c.ovf_cap = p.bkt_ovf_cap;
+    slab_recv_ = DevBuf(ctx_.pool, 8, ctx_.compute);
+    PSG_CUDA(cudaMemsetAsync(slab_recv_.p, 0, 8, ctx_.compute));
+    c.received = slab_recv_.as<unsigned long long>();
+    if (const char* e = std::getenv("PSG_SLAB_DIAG")) c.diag = std::atoi(e);
+    launch_slab_consume(aggt_, c, ctx_.compute);
+    pt.mark("  slab consume", ctx_.compute);
   } else if (nr == 1 && agg_ && !pdup) {
     ScanProgram p = pp;
     p.sink = grouped_ ? SINK_PROBE : SINK_PROBE_GLOBAL;
@@ -2352,15 +2650,7 @@ ResultRows Execution::run(bool want_rows) {
         if (ref.join >= 0 || psrc_.wire.fields[pneed[k]].type != LType::Int64) {
           lo = LLONG_MIN, hi = LLONG_MAX;  // not bounded by this scan's zone maps: never fits
         } else {
-          const int fcol = psrc_.proj.file_idx[ref.idx];
-          for (const auto& path : psrc_.scan->paths) {
-            auto meta = ctx_.footers.get(path);
-            for (const auto& g : meta->groups) {
-              if (!g.rows) continue;
-              lo = std::min(lo, static_cast<long long>(g.cols[fcol].min_raw));
-              hi = std::max(hi, static_cast<long long>(g.cols[fcol].max_raw));
-            }
-          }
+          zone_range(psrc_.scan->paths, psrc_.proj.file_idx[ref.idx], lo, hi);
         }
         lohi[k] = ~lo;  // one MAX all-reduce for both: max(~lo) = ~min(lo)
         lohi[np + k] = hi;
@@ -2579,6 +2869,7 @@ ResultRows Execution::run(bool want_rows) {
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   st_.device_ms = dms;
+  resolve_timed();
   sum_exchange_time();
   if (session_) {
     session_->check_inflate();
@@ -2721,6 +3012,7 @@ ResultRows Execution::run_local() {
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   st_.device_ms = dms;
+  resolve_timed();
   session_->check_inflate();
   st_.h2d_bytes = session_->h2d_bytes;
   if (session_->ingest) st_.io_wait_s = session_->ingest->wait_s();
@@ -2894,17 +3186,24 @@ ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::strin
   PSG_CUDA(cudaSetDevice(ctx.device));
   if (mode < 0 || mode > 3) throw InvalidInput("unknown execution mode");
   if (ctx.nranks > 1 && ctx.nccl == nullptr) throw InvalidInput("nranks > 1 needs psg_ctx_init_comm first");
-  // a bucket-overflow-list overflow re-runs the query once without buckets
+  // a bucket-overflow-list overflow re-runs the query without buckets, a key-bitmap build that
+  // does not apply re-runs it on the materialising build path (every rank takes the same decision:
+  // both come from all-reduced values)
   auto with_retry = [&](auto&& once) {
-    try {
-      return once();
-    } catch (const BucketOverflow&) {
-      struct Flag {
-        Ctx& c;
-        ~Flag() { c.no_buckets = false; }
-      } flag{ctx};
-      ctx.no_buckets = true;
-      return once();
+    struct Flags {
+      Ctx& c;
+      ~Flags() { c.no_buckets = c.no_keybits = false; }
+    } flags{ctx};
+    for (int attempt = 0;; ++attempt) {
+      try {
+        return once();
+      } catch (const BucketOverflow&) {
+        if (ctx.no_buckets || attempt >= 2) throw;
+        ctx.no_buckets = true;
+      } catch (const KeybitsRetry&) {
+        if (ctx.no_keybits || attempt >= 2) throw;
+        ctx.no_keybits = true;
+      }
     }
   };
   if (staged) {

@@ -1,5 +1,6 @@
 // Device memory pool, footer cache and the chunked storage->HBM ingest pipeline.
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <sys/stat.h>
 #include <unistd.h>
 
@@ -139,6 +140,39 @@ std::shared_ptr<const TableMeta> FooterCache::get(const std::string& path) {
   return meta;
 }
 
+// ----------------------------------------------------------------------------- FileMapCache
+FileMapping::~FileMapping() {
+  if (base) ::munmap(const_cast<uint8_t*>(base), bytes);
+}
+
+bool FileMapCache::enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PSG_MMAP");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+std::shared_ptr<const FileMapping> FileMapCache::get(const std::string& path) {
+  struct stat st;
+  if (::stat(path.c_str(), &st) != 0 || st.st_size <= 0) return nullptr;
+  const std::pair<int64_t, uint64_t> stamp{static_cast<int64_t>(st.st_mtim.tv_sec) * 1000000000LL + st.st_mtim.tv_nsec,
+                                           static_cast<uint64_t>(st.st_size)};
+  std::lock_guard<std::mutex> lk(mu_);
+  auto it = map_.find(path);
+  if (it != map_.end() && it->second.first == stamp) return it->second.second;
+  const int fd = ::open(path.c_str(), O_RDONLY);
+  if (fd < 0) return nullptr;
+  void* p = ::mmap(nullptr, static_cast<size_t>(st.st_size), PROT_READ, MAP_SHARED, fd, 0);
+  ::close(fd);
+  if (p == MAP_FAILED) return nullptr;
+  auto m = std::make_shared<FileMapping>();
+  m->base = static_cast<const uint8_t*>(p);
+  m->bytes = static_cast<size_t>(st.st_size);
+  map_[path] = {stamp, m};
+  return m;
+}
+
 // ----------------------------------------------------------------------------- Ctx
 void Ctx::ensure_pinned(int nslots, uint64_t slot_bytes) {
   if (static_cast<int>(pinned.size()) >= nslots && pinned_slot_bytes >= slot_bytes) return;
@@ -205,8 +239,36 @@ void Ctx::init_symmetric_heap(size_t bytes) {
   PSG_CUDA(cudaMemcpyAsync(&flag, d_flag, sizeof(int), cudaMemcpyDeviceToHost, compute));
   PSG_CUDA(cudaStreamSynchronize(compute));
   cudaFree(d_flag);
-  p2p = flag == 1;
-  symm_bytes = p2p ? bytes : 0;
+  symm_bytes = flag == 1 ? bytes : 0;
+  if (flag != 1) free_symmetric_heap_local();
+}
+
+void Ctx::free_symmetric_heap_local() {
+  for (int p = 0; p < static_cast<int>(symm_peer.size()); ++p)
+    if (p != rank && symm_peer[p]) cudaIpcCloseMemHandle(symm_peer[p]);
+  symm_peer.clear();
+  if (symm) cudaFree(symm);
+  symm = nullptr;
+  symm_bytes = symm_top = 0;
+}
+
+void Ctx::free_symmetric_heap() {
+  if (!symm && symm_peer.empty()) return;
+  PSG_CUDA(cudaDeviceSynchronize());
+  for (int p = 0; p < static_cast<int>(symm_peer.size()); ++p)
+    if (p != rank && symm_peer[p]) cudaIpcCloseMemHandle(symm_peer[p]);
+  symm_peer.clear();
+  // every peer has unmapped this rank's heap before it is freed
+  if (nccl) {
+    int* d = nullptr;
+    PSG_CUDA(cudaMalloc(&d, sizeof(int)));
+    if (ncclAllReduce(d, d, 1, ncclInt32, ncclMax, nccl, compute) != ncclSuccess) throw Error(PSG_ERR_NCCL, "heap barrier");
+    PSG_CUDA(cudaStreamSynchronize(compute));
+    cudaFree(d);
+  }
+  if (symm) cudaFree(symm);
+  symm = nullptr;
+  symm_bytes = symm_top = 0;
 }
 
 Ctx::~Ctx() {
@@ -235,6 +297,7 @@ Ingest::Ingest(Ctx& ctx, const std::vector<std::string>& files, const std::vecto
     }
     ::posix_fadvise(fd, 0, 0, POSIX_FADV_SEQUENTIAL);
     fds_.push_back(fd);
+    maps_.push_back(FileMapCache::enabled() ? ctx.maps.get(f) : nullptr);
   }
   ctx.ensure_pinned(nslots, slot_bytes);
   slots_.resize(nslots);
@@ -276,7 +339,12 @@ void Ingest::worker() {
     auto* dst = static_cast<uint8_t*>(slots_[slot].host);
     std::string err;
     const auto t_read = std::chrono::steady_clock::now();
+    const FileMapping* m = maps_[b.file].get();
     for (const Extent& e : b.extents) {
+      if (m != nullptr && e.file_off + e.len <= m->bytes) {  // straight out of the page cache
+        std::memcpy(dst + e.buf_off, m->base + e.file_off, e.len);
+        continue;
+      }
       uint64_t got = 0;
       while (got < e.len) {
         const ssize_t k = ::pread(fds_[b.file], dst + e.buf_off + got, e.len - got, static_cast<off_t>(e.file_off + got));

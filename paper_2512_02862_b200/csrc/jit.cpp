@@ -184,6 +184,8 @@ void emit_accumulate(std::ostringstream& s, const ScanProgram& P, const char* in
 }
 
 
+void emit_rank_tail(std::ostringstream& s, const ScanProgram& P);
+
 /// Rank-indexed table probe (SINK_PROBE): the key's 64-bit bitmap word and its block prefix (both
 /// L2-resident; one 16-byte {bits, rank} record when krec is set) give membership and the slot at
 /// once - no hashing, no collision chain. `late` emits the loads of the non-key columns (for the
@@ -203,6 +205,13 @@ void emit_rank_probe(std::ostringstream& s, const ScanProgram& P, Late late) {
     << "        if (!((bw[r] >> bb[r]) & 1ULL)) pass &= ~(1u << r);\n"
     << "        else sl[r] = bp[r] + static_cast<uint64_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n";
   late();
+  emit_rank_tail(s, P);
+  s << "    }\n";
+}
+
+/// Every row still in `pass` accumulates into its rank-table slot sl[r]: one word appended to the
+/// slot's bucket (bucketed aggregation), else atomics on the hot slot.
+void emit_rank_tail(std::ostringstream& s, const ScanProgram& P) {
   s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n";
   if (P.bkt != nullptr) {  // append one word to the slot's bucket (k_bucket_emit folds it)
     s << "        const uint64_t b = sl[r] >> " << kBucketBits << ";\n"
@@ -219,7 +228,78 @@ void emit_rank_probe(std::ostringstream& s, const ScanProgram& P, Late late) {
   }
   s << "        unsigned long long* h = reinterpret_cast<unsigned long long*>(T.hot + sl[r] * " << P.agg.hw << ");\n";
   emit_accumulate(s, P, "        ");
-  s << "      }\n    }\n";
+  s << "      }\n";
+}
+
+/// Peer-slab shuffle (P.slab, SINK_PROBE at N > 1): per-warp staging of the rows owned by other
+/// ranks in shared memory (packed word + destination), flushed 128 rows at a time: per destination
+/// ONE atomic reserves the positions in its slab region and the lanes store consecutive words
+/// over NVLink (coalesced). Per-row reservations on one counter serialised at the L2 (SF100 N=2:
+/// probe 1.7 -> 6.8 ms); per flush they are ~30x fewer. `w` indexes the warp's staging row.
+/// PSG_SLAB_DIAG (measurement only - results are wrong when set): 1 no NVLink stores, 2 remote
+/// rows dropped before staging.
+int slab_diag() {
+  static const int v = [] {
+    const char* e = std::getenv("PSG_SLAB_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
+void emit_slab_prologue(std::ostringstream& s, int nwarps, const std::string& w) {
+  s << "  __shared__ uint64_t s_slab[" << nwarps << "][128];\n  __shared__ unsigned char s_sdst[" << nwarps << "][128];\n"
+    << "  int sfill = 0;\n"
+    << "  auto sflush = [&]() {\n    __syncwarp();\n    if (sfill == 0) return;\n"
+    << "    const int ln = threadIdx.x & 31; const uint32_t lt = (1u << ln) - 1u;\n"
+    << "    for (int d = 0; d < P.nparts; ++d) {\n      if (d == P.self_rank) continue;\n"
+    << "      unsigned c = 0;\n      for (int i = ln; i < sfill; i += 32) c += s_sdst[" << w << "][i] == d;\n"
+    << "      const unsigned tot = __reduce_add_sync(0xffffffffu, c);\n      if (tot == 0) continue;\n"
+    << "      unsigned long long base = 0;\n"
+    << "      if (ln == 0) base = atomicAdd(P.slab_cnt + d, static_cast<unsigned long long>(tot));\n"
+    << "      base = __shfl_sync(0xffffffffu, base, 0);\n      unsigned off = 0;\n"
+    << "      for (int i0 = 0; i0 < sfill; i0 += 32) {\n        const int i = i0 + ln;\n"
+    << "        const bool mine = i < sfill && s_sdst[" << w << "][i] == d;\n"
+    << "        const unsigned b = __ballot_sync(0xffffffffu, mine);\n"
+    << "        if (mine) { const uint64_t pos = base + off + __popc(b & lt); if (pos < P.slab_cap" << ((slab_diag() & 1) ? " && pos == ~0ULL" : "")
+    << ") P.slab_dst[d][pos] = s_slab[" << w << "][i]; }\n"
+    << "        off += __popc(b);\n      }\n    }\n    sfill = 0;\n    __syncwarp();\n  };\n";
+}
+
+/// The probe with the peer-slab shuffle: ONE dependent lookup per row, chosen by its owner -
+/// a row this rank owns reads its 16-byte rank record (membership + slot, as at one GPU), any
+/// other row the word of the global key bitmap (the exact semi-join screen). `late` then loads
+/// the non-key columns of the survivors; remote survivors are staged (bit-packed, with their
+/// destination) for the slab flush, owned survivors accumulate into their slots.
+template <class Late>
+void emit_slab_probe(std::ostringstream& s, const ScanProgram& P, Late late, const std::string& w) {
+  s << "    { const AggTableDev& T = P.agg; unsigned long long bw[R]; uint64_t bp[R], sl[R]; uint32_t bb[R], dst[R];\n"
+    << "      uint32_t own = 0, rem = 0;\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bp[r] = 0; bb[r] = 0; dst[r] = 0; const uint64_t key = "
+    << V(P.key_reg) << "[r];\n"
+    << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+    << "          if (d < T.krange) { const uint32_t o = part_of(key, static_cast<uint32_t>(P.nparts)); dst[r] = o;\n"
+    << "            if (o == static_cast<uint32_t>(P.self_rank)) { own |= 1u << r; bb[r] = static_cast<uint32_t>(d & 63);\n"
+    << "              uint64_t a, b; ldg_keep_v2u64(T.krec + 2 * (d >> 6), pol_keep, a, b); bw[r] = a; bp[r] = b; }\n"
+    << "            else { rem |= 1u << r; bb[r] = static_cast<uint32_t>(d & 31); bw[r] = ldg_keep_u32(P.semi_kbits + (d >> 5), pol_keep); } } } }\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0;\n"
+    << "        if (!((bw[r] >> bb[r]) & 1ULL)) { own &= ~(1u << r); rem &= ~(1u << r); }\n"
+    << "        else if ((own >> r) & 1u) sl[r] = bp[r] + static_cast<uint64_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n"
+    << "      pass = own | rem;\n";
+  late();
+  if (slab_diag() & 2) s << "      rem = 0;\n";
+  s << "      const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+    << "        const bool on = (rem >> r) & 1u;\n"
+    << "        const unsigned b = __ballot_sync(0xffffffffu, on);\n"
+    << "        const int cnt = __popc(b);\n        if (cnt == 0) continue;\n"
+    << "        if (sfill + cnt > 128) sflush();\n"
+    << "        if (on) { const int pos = sfill + __popc(b & lt);\n"
+    << "          s_slab[" << w << "][pos] = " << out_value(P, 0) << ";\n"
+    << "          s_sdst[" << w << "][pos] = static_cast<unsigned char>(dst[r]); }\n"
+    << "        sfill += cnt;\n      }\n"
+    << "      pass = own;\n";
+  emit_rank_tail(s, P);
+  s << "    }\n";
 }
 
 /// Predicate atoms: clear a row's pass bit when an atom fails.
@@ -394,6 +474,10 @@ std::string jit_source(const ScanProgram& P) {
   if (glob) s << "  __shared__ unsigned long long s_gacc[" << nglob << "];\n";
   s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  const int wrow = warp * (R * 32) + lane;\n"
     << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep; (void)wrow;\n";
+  if (P.slab) emit_slab_prologue(s, NW, "warp");
+  // SINK_KEYBITS row count: per lane, one atomic per warp at the end (a per-tile atomic on one
+  // counter serialises at the L2)
+  if (P.sink == SINK_KEYBITS) s << "  unsigned long long kb_rows = 0;\n";
   if (part) s << "  for (int i = tid; i < " << kMaxParts << "; i += " << NT << ") s_part[i] = 0;\n";
   if (glob) {
     s << "  for (int i = tid; i < " << nglob << "; i += " << NT << ") s_gacc[i] = 0;\n";
@@ -468,6 +552,8 @@ std::string jit_source(const ScanProgram& P) {
   } else if (P.remote && P.sink == SINK_BUILD) {
     emit_loads(s, P.n_early, P.n_in);
     emit_remote_build(s, P);
+  } else if (probe && P.agg.krec != nullptr && P.sink == SINK_PROBE && P.slab) {
+    emit_slab_probe(s, P, [&] { emit_loads(s, P.n_early, P.n_in); }, "warp");
   } else if (probe && P.agg.krank != nullptr && P.sink == SINK_PROBE) {
     emit_rank_probe(s, P, [&] { emit_loads(s, P.n_early, P.n_in); });
   } else if (probe) {
@@ -538,6 +624,13 @@ std::string jit_source(const ScanProgram& P) {
           s << "      g" << 1 + p << " += " << V(P.sum_reg[p]) << "[r];\n";
       }
       s << "    }\n";
+    } else if (P.sink == SINK_KEYBITS) {  // build side straight into the key bitmap
+      s << "    { unsigned nset = 0;\n#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+        << "        const uint64_t d = " << V(P.key_reg) << "[r] - static_cast<uint64_t>(P.kb_min);\n"
+        << "        ++nset;\n        if (d >= P.kb_range) { atomicOr(P.kb_flag, 2u); continue; }\n"
+        << "        const uint32_t bit = 1u << (d & 31);\n"
+        << "        if (atomicOr(P.kb_bits + (d >> 5), bit) & bit) atomicOr(P.kb_flag, 1u); }\n"
+        << "      kb_rows += nset;\n    }\n";
     } else if (P.sink == SINK_BUILD) {
       s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R]; unsigned long long pv[R];\n"
         << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0; pv[r] = kEmptyKey; if (!(pass & (1u << r))) continue;\n"
@@ -622,6 +715,10 @@ std::string jit_source(const ScanProgram& P) {
   if (bscan) s << "    __syncthreads();\n";  // s_base / s_woff reuse by the next tile
   s << "    cur_col = pf_col; cur_r0 = pf_r0; cur_rows = pf_rows;\n  }\n";
   if (wstage) s << "  flush();\n";
+  if (P.slab) s << "  sflush();\n";
+  if (P.sink == SINK_KEYBITS)
+    s << "  for (int o = 16; o > 0; o >>= 1) kb_rows += __shfl_xor_sync(0xffffffffu, kb_rows, o);\n"
+      << "  if (lane == 0 && kb_rows) atomicAdd(P.kb_count, kb_rows);\n";
   if (part)
     s << "  __syncthreads();\n  for (int i = tid; i < P.nparts; i += " << NT << ") if (s_part[i]) atomicAdd(&P.part_counts[i], s_part[i]);\n";
   if (glob) {
@@ -636,6 +733,7 @@ std::string jit_source(const ScanProgram& P) {
          "__longlong_as_double(static_cast<long long>(s_gacc[i])));\n"
       << "    else atomicAdd(&P.global_acc[i], s_gacc[i]); }\n";
   }
+  if (P.slab) s << "  __threadfence_system();  // slab stores visible to the owners before the kernel ends\n";
   s << "}\n";
   return s.str();
 }
@@ -696,6 +794,7 @@ std::string jit_source_staged(const ScanProgram& P) {
   s << "      }\n    }\n    return;\n  }\n"
     << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep;\n"
     << "  const int cw = (warp - 1) % " << CW << ", grp = (warp - 1) / " << CW << ";\n  const int wrow = cw * (R * 32) + lane;\n";
+  if (P.slab && P.sink == SINK_PROBE) emit_slab_prologue(s, CW * NG, "warp - 1");
   if (mat) {
     s << "  int fill = 0;\n  auto flush = [&]() {\n    __syncwarp();\n    if (fill == 0) return;\n"
       << "    unsigned long long base = 0;\n    if (lane == 0) base = atomicAdd(P.out_count, static_cast<unsigned long long>(fill));\n"
@@ -725,8 +824,13 @@ std::string jit_source_staged(const ScanProgram& P) {
         << "[r] = __ldcs(reinterpret_cast<const unsigned long long*>(lc" << c << " + wrow + r * 32));\n";
   };
   if (P.sink == SINK_PROBE) {
-    emit_rank_probe(s, P, late);
-    s << "  }\n}\n";
+    if (P.slab) {
+      emit_slab_probe(s, P, late, "warp - 1");
+      s << "  }\n  sflush();\n  __threadfence_system();  // slab stores visible to the owners before the kernel ends\n}\n";
+    } else {
+      emit_rank_probe(s, P, late);
+      s << "  }\n}\n";
+    }
     return s.str();
   }
   // MATERIALIZE: screen -> late columns -> per-warp staging in shared memory, flushed 128 rows at
@@ -879,7 +983,7 @@ void fused_scan(const ScanProgram& P, const Segment* d_segs, const uint32_t* d_t
     }
   }
   if (P.remote) throw Error(PSG_ERR_INTERNAL, "the fused NVLink path needs the query compiler (PSG_JIT)");
-  if (P.self_probe || P.pack_n || P.unpack_n || P.agg.npacked || P.agg.krank)
+  if (P.self_probe || P.pack_n || P.unpack_n || P.agg.npacked || P.agg.krank || P.slab || P.sink == SINK_KEYBITS)
     throw Error(PSG_ERR_INTERNAL,
                 "owner probe / packed rows / packed accumulators / rank-indexed table need the query compiler (PSG_JIT)");
   launch_scan(P, d_segs, d_tile_seg, nsegs, ntiles, stream);
@@ -975,6 +1079,16 @@ int jit_selftest(std::string& log) {
       q.bkt = reinterpret_cast<uint64_t*>(16);  // + bucketed aggregation
       q.agg.ps_float[1] = 0;
       progs.push_back(q);
+      q.slab = 1;  // + peer-slab shuffle: global screen, packed rows to the owners' slabs
+      q.nparts = 4;
+      q.self_rank = 1;
+      q.semi_kbits = reinterpret_cast<const uint32_t*>(16);
+      q.semi_key_reg = 1;
+      q.pack_n = 3;
+      q.pack_reg[0] = 1, q.pack_reg[1] = 2, q.pack_reg[2] = 3;
+      progs.push_back(q);
+      q.staged_ok = 0;  // ... in the register kernel
+      progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // consuming packed rows
       ScanProgram q = p;
@@ -983,6 +1097,11 @@ int jit_selftest(std::string& log) {
       q.key_reg = 1;
       progs.push_back(q);
     }
+  }
+  {
+    ScanProgram p = base();  // build side straight into the key bitmap
+    p.sink = SINK_KEYBITS;
+    progs.push_back(p);
   }
   {
     ScanProgram p = base();  // orders-like: filter, local join with payload, materialise

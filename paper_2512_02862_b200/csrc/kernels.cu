@@ -703,6 +703,97 @@ void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, ui
   k_krec_build<<<grid_for(n, 256), 256, 0, S(stream)>>>(bits, krank, n, krec);
 }
 
+/// Owner bitmap at N > 1: own[w] = the bits of the global key bitmap word w whose key this rank
+/// owns (partition_of(key) == self). cnt[0] += own bits, cnt[1] += global bits (the engine checks
+/// the global count against the rows that set it: a SUM all-reduce of overlapping bitmaps carries).
+__global__ void k_own_mask(const unsigned long long* __restrict__ global, unsigned long long* __restrict__ own,
+                           uint64_t nwords, int64_t kmin, int nparts, int self, unsigned long long* cnt) {
+  unsigned long long no = 0, ng = 0;
+  for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < nwords;
+       w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long g = global[w], m = 0, rest = g;
+    const uint64_t base = static_cast<uint64_t>(kmin) + (w << 6);
+    while (rest) {
+      const int b = __ffsll(static_cast<long long>(rest)) - 1;
+      rest &= rest - 1;
+      if (part_of(base + b, static_cast<uint32_t>(nparts)) == static_cast<uint32_t>(self)) m |= 1ULL << b;
+    }
+    own[w] = m;
+    no += __popcll(m);
+    ng += __popcll(g);
+  }
+  no = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(no));
+  ng = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(ng));
+  if ((threadIdx.x & 31) == 0 && (no | ng)) {
+    atomicAdd(cnt, no);
+    atomicAdd(cnt + 1, ng);
+  }
+}
+void launch_own_mask(const unsigned long long* global, unsigned long long* own, uint64_t nwords, int64_t kmin, int nparts,
+                     int self, unsigned long long* cnt, void* stream) {
+  if (nwords == 0) return;
+  count_launch();
+  k_own_mask<<<grid_for(nwords, 256), 256, 0, S(stream)>>>(global, own, nwords, kmin, nparts, self, cnt);
+}
+
+/// Peer-slab shuffle, owner side: every packed row the other ranks stored into this rank's
+/// receive slab (region r = source r, *c.src_cnt[r] rows, read from the source's counters through
+/// NVLink after the cross-rank barrier) is unpacked, finds its slot in the rank-indexed table
+/// (one 16-byte rank record) and is appended to the slot's aggregation bucket - the same entry
+/// the probe kernel appends for the rows it owns (ScanProgram::bkt).
+__global__ void __launch_bounds__(256) k_slab_consume(AggTableDev t, SlabConsume c) {
+  const uint64_t gtid = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  __shared__ unsigned long long s_n[kMaxSlabPeers];  // one NVLink read per (block, source)
+  if (threadIdx.x < c.nsrc)
+    s_n[threadIdx.x] = c.src_cnt[threadIdx.x] == nullptr
+                           ? 0ULL
+                           : *reinterpret_cast<const volatile unsigned long long*>(c.src_cnt[threadIdx.x]);
+  __syncthreads();
+  for (int src = 0; src < c.nsrc; ++src) {
+    const uint64_t n = min(static_cast<uint64_t>(s_n[src]), c.cap);
+    if (n == 0) continue;
+    if (gtid == 0) atomicAdd(c.received, static_cast<unsigned long long>(n));
+    const uint64_t* in = c.slab + static_cast<uint64_t>(src) * c.cap;
+    for (uint64_t i = gtid; i < n; i += stride) {
+      const uint64_t w = __ldcs(reinterpret_cast<const unsigned long long*>(in + i));
+      const uint64_t key = static_cast<uint64_t>(c.pmin[0]) + ((w >> c.pshift[0]) & c.pmask[0]);
+      const uint64_t d = key - static_cast<uint64_t>(t.kmin);
+      if (d >= t.krange) continue;  // (the senders' global screen guarantees membership)
+      const ulonglong2 rec = __ldg(reinterpret_cast<const ulonglong2*>(t.krec) + (d >> 6));
+      if (!((rec.x >> (d & 63)) & 1ULL)) continue;
+      const uint64_t slot = rec.y + static_cast<uint64_t>(__popcll(rec.x & ((1ULL << (d & 63)) - 1ULL)));
+      uint64_t e = slot & static_cast<uint64_t>(kBucketSlots - 1);
+      for (int k = 0; k + 1 < c.npack; ++k) {
+        const uint64_t v = static_cast<uint64_t>(c.pmin[1 + k]) + ((w >> c.pshift[1 + k]) & c.pmask[1 + k]);
+        e |= ((v - static_cast<uint64_t>(c.bmin[k])) & c.bmask[k]) << c.bshift[k];
+      }
+      const uint64_t b = slot >> kBucketBits;
+      if (c.diag & 4) {  // measurement only (PSG_SLAB_DIAG=4): no bucket append
+        if (e == ~0ULL) c.bkt[b] = e;
+        continue;
+      }
+      const unsigned pos = atomicAdd(c.fill + b, 1u);
+      if (pos < c.bcap) {
+        c.bkt[b * c.bcap + pos] = e;
+      } else {
+        const unsigned o = atomicAdd(c.ovf_count, 1u);
+        if (o < c.ovf_cap) {
+          c.ovf[2 * o] = slot;
+          c.ovf[2 * o + 1] = e;
+        }
+      }
+    }
+  }
+}
+void launch_slab_consume(const AggTableDev& t, const SlabConsume& c, void* stream) {
+  count_launch();
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_slab_consume<<<sms * 4, 256, 0, S(stream)>>>(t, c);
+}
+
 /// Output column recipe of the emit kernels: kind 0 key, 1 rows, 2 probe sum idx, 3 build sum idx.
 struct EmitCols {
   int32_t kind[2 * kMaxSums + 2];

@@ -100,6 +100,33 @@ struct BucketDev {
 void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots,
                         unsigned long long* state, unsigned int* ticket, uint32_t* first_word, int nc,
                         const int32_t* col_kind, const int32_t* col_idx, uint64_t* out_rows, void* stream);
+/// Own-key bitmap of a rank (N > 1) from the global one; cnt[0..1] += own / global popcounts.
+void launch_own_mask(const unsigned long long* global, unsigned long long* own, uint64_t nwords, int64_t kmin, int nparts,
+                     int self, unsigned long long* cnt, void* stream);
+/// Peer-slab shuffle, owner side (kernels.cu k_slab_consume).
+struct SlabConsume {
+  const uint64_t* slab;                                // this rank's receive slab: region r = source r
+  const unsigned long long* src_cnt[kMaxSlabPeers];    // rows source r stored here (peer-mapped; null: none)
+  uint64_t cap;                                        // rows per region
+  int32_t nsrc;
+  int32_t npack;                                       // packed fields: key, then the probe sums
+  int32_t pshift[kMaxSums + 1];
+  uint64_t pmask[kMaxSums + 1];
+  int64_t pmin[kMaxSums + 1];
+  // the bucket entry format of the probe kernel (ScanProgram::bkt_*)
+  uint64_t* bkt;
+  unsigned int* fill;
+  uint32_t bcap;
+  int32_t bshift[kMaxSums];
+  uint64_t bmask[kMaxSums];
+  int64_t bmin[kMaxSums];
+  uint64_t* ovf;
+  unsigned int* ovf_count;
+  uint32_t ovf_cap;
+  unsigned long long* received;                        // += rows consumed (stats)
+  int32_t diag;                                        // PSG_SLAB_DIAG (measurement only)
+};
+void launch_slab_consume(const AggTableDev& t, const SlabConsume& c, void* stream);
 void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, uint64_t n, unsigned long long* krec,
                        void* stream);
 void launch_part_hist(const uint64_t* keys, uint64_t n, int nparts, unsigned long long* counts, void* stream);

@@ -106,6 +106,7 @@ TableMeta parse_footer_bytes(const uint8_t* tail, size_t tail_len, uint64_t file
     }
   }
   if (r.off != r.n) throw CorruptFooter("trailing bytes in footer");
+  m.summarise();
   m.footer_bytes = flen;
   m.file_size = file_size;
   return m;
@@ -311,6 +312,7 @@ TableMeta PstoWriter::finish() {
   }
   fd_ = -1;
   meta_.footer_bytes = flen;
+  meta_.summarise();
   return meta_;
 }
 

@@ -5,6 +5,7 @@
 // (encode_footer psto.cpp:192-213, parse_footer_bytes :231-292, prune :320-343).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -28,10 +29,26 @@ struct TableMeta {
   std::vector<GroupMeta> groups;
   uint64_t footer_bytes = 0;
   uint64_t file_size = 0;
-  uint64_t total_rows() const {
-    uint64_t n = 0;
-    for (auto& g : groups) n += g.rows;
-    return n;
+  // whole-file summaries of the zone maps (filled once per parsed footer, so the planner's range
+  // questions cost one lookup per file instead of a walk over every row group): rows, and per
+  // column the min/max of the raw words read as signed integers over the non-empty groups
+  // (zmin > zmax when the file has no rows)
+  uint64_t nrows = 0;
+  std::vector<int64_t> zmin, zmax;
+  uint64_t total_rows() const { return nrows; }
+  void summarise() {
+    nrows = 0;
+    const size_t nc = schema.size();
+    zmin.assign(nc, INT64_MAX);
+    zmax.assign(nc, INT64_MIN);
+    for (const auto& g : groups) {
+      nrows += g.rows;
+      if (!g.rows) continue;
+      for (size_t c = 0; c < nc && c < g.cols.size(); ++c) {
+        zmin[c] = std::min(zmin[c], static_cast<int64_t>(g.cols[c].min_raw));
+        zmax[c] = std::max(zmax[c], static_cast<int64_t>(g.cols[c].max_raw));
+      }
+    }
   }
 };
 
