@@ -202,9 +202,13 @@ struct ScanProgram {
   // then every probe sum k as (v - bkt_min[k]) & bkt_mask[k] at bkt_shift[k]. k_bucket_agg then
   // folds each bucket in shared memory and adds it to the hot slots once, so the table's random
   // read-modify-writes never go to HBM. A full bucket spills to the overflow list below.
-  uint64_t* bkt;             // [nbuckets][bkt_cap]
-  unsigned int* bkt_fill;    // [nbuckets] appended entries (may exceed bkt_cap: overflowed)
+  // Each bucket is split into 2^bkt_sub_bits sub-lists (a row goes to sub-list threadIdx & (S-1)):
+  // S x more append counters - the L2 serves atomics on few distinct words far slower (measured:
+  // 42 G/s on 3.6 K counters vs 142 G/s on 64 K, profiles/r2_atomic_probe.txt).
+  uint64_t* bkt;             // [nbuckets << bkt_sub_bits][bkt_cap]
+  unsigned int* bkt_fill;    // [nbuckets << bkt_sub_bits] appended entries (may exceed bkt_cap: overflowed)
   uint32_t bkt_cap;
+  int32_t bkt_sub_bits;
   int32_t bkt_shift[kMaxSums];
   uint64_t bkt_mask[kMaxSums];
   int64_t bkt_min[kMaxSums];
@@ -231,6 +235,10 @@ struct ScanProgram {
   unsigned long long* slab_cnt;
   uint64_t slab_cap;
   int32_t slab;
+  // {global key-bitmap word, rank of this rank's first own key in the word} per 64 keys: ONE
+  // 16-byte lookup screens every row and gives an own row its slot (own keys below it in the word
+  // are the global bits whose key this rank owns - counted by hashing only those few keys)
+  const unsigned long long* slab_grec;
   // the engine guarantees 16-byte aligned column chunks and readable padding past each chunk's
   // end (PSTO batches, staged images): the query compiler may then stream the early columns into
   // shared memory with bulk copies (the warp-specialised probe, jit.cpp)

@@ -643,6 +643,7 @@ class Execution {
   uint64_t slab_cap_ = 0;
   size_t slab_cnt_off_ = 0, slab_off_ = 0;
   DevBuf slab_recv_;
+  DevBuf slab_grec_;  // {global bitmap word, own rank} records (ScanProgram::slab_grec)
   void apply_buckets(ScanProgram& p) const;
   void finalize_buckets(ResultRows& out, bool want_rows);
   AggTableDev aggt_{};
@@ -1435,15 +1436,29 @@ bool Execution::setup_buckets(const int64_t* prange_lo, const int64_t* prange_hi
     const char* e = std::getenv("PSG_BUCKET_CAP");
     return e ? std::strtoull(e, nullptr, 10) : 0ULL;
   }();
+  // 2^sub_bits sub-lists per bucket (PSG_BUCKET_SUB): more distinct append counters. SF100 A/B:
+  // one GPU 4.60 ms with 1 sub-list vs 4.79 with 16 (the emit walks 16 lists, the probe keeps 16x
+  // more open bucket tails); N=2 4.15 vs 4.07 (the owner-side fold of the received rows, a burst
+  // of appends, 0.43 -> 0.20 ms). Default: 1 at one GPU, 16 at N > 1.
+  static const int sub_env = [] {
+    const char* e = std::getenv("PSG_BUCKET_SUB");
+    return e ? std::max(1, std::atoi(e)) : 0;
+  }();
+  const int sub_req = sub_env ? sub_env : (ctx_.nranks > 1 ? 16 : 1);
+  int sub_bits = 0;
+  while ((2 << sub_bits) <= sub_req && sub_bits < 5) ++sub_bits;
+  const uint64_t nsub = nb << sub_bits;
   const uint64_t cap = cap_env ? cap_env
-                               : static_cast<uint64_t>(1.5 * static_cast<double>(probe_rows) * share / static_cast<double>(nb)) + 1024;
+                               : static_cast<uint64_t>(1.5 * static_cast<double>(probe_rows) * share / static_cast<double>(nsub)) +
+                                     (1024 >> sub_bits) + 64;
   if (cap >= (1ULL << 31)) return false;
-  bkt_ = DevBuf(ctx_.pool, nb * cap * 8, ctx_.compute);
-  bkt_fill_ = DevBuf(ctx_.pool, nb * 4, ctx_.compute);
-  PSG_CUDA(cudaMemsetAsync(bkt_fill_.p, 0, nb * 4, ctx_.compute));
+  bkt_ = DevBuf(ctx_.pool, nsub * cap * 8, ctx_.compute);
+  bkt_fill_ = DevBuf(ctx_.pool, nsub * 4, ctx_.compute);
+  PSG_CUDA(cudaMemsetAsync(bkt_fill_.p, 0, nsub * 4, ctx_.compute));
   bd.bkt = bkt_.as<uint64_t>();
   bd.fill = bkt_fill_.as<unsigned int>();
   bd.cap = static_cast<uint32_t>(cap);
+  bd.sub_bits = sub_bits;
   bd.nacc = 1 + np;
   static const uint32_t kOvfCap = [] {  // 1 MB: scanned by every bucket CTA when not empty
     const char* e = std::getenv("PSG_BUCKET_OVF_CAP");
@@ -1467,6 +1482,7 @@ void Execution::apply_buckets(ScanProgram& p) const {
   p.bkt = const_cast<uint64_t*>(bd_.bkt);
   p.bkt_fill = const_cast<unsigned int*>(bd_.fill);
   p.bkt_cap = bd_.cap;
+  p.bkt_sub_bits = bd_.sub_bits;
   for (int k = 0; k < kMaxSums; ++k) {
     p.bkt_shift[k] = bd_.shift[k];
     p.bkt_mask[k] = bd_.mask[k];
@@ -2310,6 +2326,9 @@ ResultRows Execution::run(bool want_rows) {
       slab_cap_ = slab_cap;
       slab_cnt_off_ = static_cast<size_t>(cnt - ctx_.symm);
       slab_off_ = static_cast<size_t>(slab - ctx_.symm);
+      slab_grec_ = DevBuf(ctx_.pool, kwords64 * 16, ctx_.compute);
+      launch_krec_build(semi_all.as<unsigned long long>(), agg_krank_.as<uint32_t>(), kwords64,
+                        slab_grec_.as<unsigned long long>(), ctx_.compute);
     } else if (nr > 1) {
       bucket_mode_ = false;  // the NCCL shuffle's consume kernel updates the table directly
     }
@@ -2556,6 +2575,7 @@ ResultRows Execution::run(bool want_rows) {
       p.pack_mask[k] = slab_pack_.mask[k];
     }
     p.slab = 1;
+    p.slab_grec = slab_grec_.as<unsigned long long>();
     p.nparts = nr;
     p.self_rank = ctx_.rank;
     p.slab_cap = slab_cap_;
@@ -2591,6 +2611,7 @@ ResultRows Execution::run(bool want_rows) {
     c.bkt = p.bkt;
     c.fill = p.bkt_fill;
     c.bcap = p.bkt_cap;
+    c.bsub_bits = p.bkt_sub_bits;
     for (int k = 0; k < kMaxSums; ++k) {
       c.bshift[k] = p.bkt_shift[k];
       c.bmask[k] = p.bkt_mask[k];

@@ -214,7 +214,7 @@ void emit_rank_probe(std::ostringstream& s, const ScanProgram& P, Late late) {
 void emit_rank_tail(std::ostringstream& s, const ScanProgram& P) {
   s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n";
   if (P.bkt != nullptr) {  // append one word to the slot's bucket (k_bucket_emit folds it)
-    s << "        const uint64_t b = sl[r] >> " << kBucketBits << ";\n"
+    s << "        const uint64_t b = ((sl[r] >> " << kBucketBits << ") << P.bkt_sub_bits) | (threadIdx.x & ((1u << P.bkt_sub_bits) - 1u));\n"
       << "        const unsigned pos = atomicAdd(P.bkt_fill + b, 1u);\n"
       << "        uint64_t e = sl[r] & " << (kBucketSlots - 1) << "ULL;\n";
     for (int k = 0; k < P.n_sum; ++k)
@@ -265,13 +265,55 @@ void emit_slab_prologue(std::ostringstream& s, int nwarps, const std::string& w)
     << "        off += __popc(b);\n      }\n    }\n    sfill = 0;\n    __syncwarp();\n  };\n";
 }
 
+/// The probe with the peer-slab shuffle: ONE dependent 16-byte lookup per row into the global
+/// records {global key-bitmap word, own rank at the word} (the same footprint as the one-GPU rank
+/// records). A key absent from the global bitmap drops the row; a key this rank owns gets its slot
+/// = own rank + the own keys below it in the word (the set global bits below it whose key hashes
+/// to this rank - a handful of multiply-shifts); any other key's row is staged (bit-packed, with
+/// its destination) for the slab flush. `late` loads the non-key columns of the survivors.
+template <class Late>
+void emit_slab_probe1(std::ostringstream& s, const ScanProgram& P, Late late, const std::string& w) {
+  s << "    { const AggTableDev& T = P.agg; unsigned long long gw[R]; uint32_t orr[R], sl[R], bb[R], dst[R];\n"
+    << "      uint32_t own = 0, rem = 0;\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { gw[r] = 0; orr[r] = 0; bb[r] = 0; dst[r] = 0; const uint64_t key = "
+    << V(P.key_reg) << "[r];\n"
+    << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+    << "          if (d < T.krange) { bb[r] = static_cast<uint32_t>(d & 63); dst[r] = part_of(key, static_cast<uint32_t>(P.nparts));\n"
+    << "            uint64_t a, b; ldg_keep_v2u64(P.slab_grec + 2 * (d >> 6), pol_keep, a, b); gw[r] = a; orr[r] = static_cast<uint32_t>(b); } } }\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0;\n"
+    << "        if (!((gw[r] >> bb[r]) & 1ULL)) continue;\n"
+    << "        if (dst[r] != static_cast<uint32_t>(P.self_rank)) { rem |= 1u << r; continue; }\n"
+    << "        own |= 1u << r;\n"
+    << "        const uint64_t base = " << V(P.key_reg) << "[r] - bb[r];\n"
+    << "        unsigned long long m = gw[r] & ((1ULL << bb[r]) - 1ULL); uint32_t c = orr[r];\n"
+    << "        while (m) { const int i = __ffsll(static_cast<long long>(m)) - 1; m &= m - 1;\n"
+    << "          if (part_of(base + i, static_cast<uint32_t>(P.nparts)) == static_cast<uint32_t>(P.self_rank)) ++c; }\n"
+    << "        sl[r] = c; }\n"
+    << "      pass = own | rem;\n";
+  late();
+  if (slab_diag() & 2) s << "      rem = 0;\n";
+  s << "      const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+    << "        const bool on = (rem >> r) & 1u;\n"
+    << "        const unsigned b = __ballot_sync(0xffffffffu, on);\n"
+    << "        const int cnt = __popc(b);\n        if (cnt == 0) continue;\n"
+    << "        if (sfill + cnt > 128) sflush();\n"
+    << "        if (on) { const int pos = sfill + __popc(b & lt);\n"
+    << "          s_slab[" << w << "][pos] = " << out_value(P, 0) << ";\n"
+    << "          s_sdst[" << w << "][pos] = static_cast<unsigned char>(dst[r]); }\n"
+    << "        sfill += cnt;\n      }\n"
+    << "      pass = own;\n";
+  emit_rank_tail(s, P);
+  s << "    }\n";
+}
+
 /// The probe with the peer-slab shuffle: ONE dependent lookup per row, chosen by its owner -
 /// a row this rank owns reads its 16-byte rank record (membership + slot, as at one GPU), any
 /// other row the word of the global key bitmap (the exact semi-join screen). `late` then loads
 /// the non-key columns of the survivors; remote survivors are staged (bit-packed, with their
 /// destination) for the slab flush, owned survivors accumulate into their slots.
 template <class Late>
-void emit_slab_probe(std::ostringstream& s, const ScanProgram& P, Late late, const std::string& w) {
+void emit_slab_probe2(std::ostringstream& s, const ScanProgram& P, Late late, const std::string& w) {
   s << "    { const AggTableDev& T = P.agg; unsigned long long bw[R]; uint64_t bp[R], sl[R]; uint32_t bb[R], dst[R];\n"
     << "      uint32_t own = 0, rem = 0;\n"
     << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bp[r] = 0; bb[r] = 0; dst[r] = 0; const uint64_t key = "
@@ -300,6 +342,23 @@ void emit_slab_probe(std::ostringstream& s, const ScanProgram& P, Late late, con
     << "      pass = own;\n";
   emit_rank_tail(s, P);
   s << "    }\n";
+}
+
+/// PSG_SLAB_GREC=1: the one-lookup variant over the global records (emit_slab_probe1); default the
+/// two-lookup variant (emit_slab_probe2: own rank records / global bitmap by owner).
+bool slab_grec_env() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_SLAB_GREC");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
+template <class Late>
+void emit_slab_probe(std::ostringstream& s, const ScanProgram& P, Late late, const std::string& w) {
+  if (P.slab_grec != nullptr && slab_grec_env())
+    emit_slab_probe1(s, P, late, w);
+  else
+    emit_slab_probe2(s, P, late, w);
 }
 
 /// Predicate atoms: clear a row's pass bit when an atom fails.
@@ -1086,6 +1145,7 @@ int jit_selftest(std::string& log) {
       q.semi_key_reg = 1;
       q.pack_n = 3;
       q.pack_reg[0] = 1, q.pack_reg[1] = 2, q.pack_reg[2] = 3;
+      q.slab_grec = reinterpret_cast<const unsigned long long*>(16);
       progs.push_back(q);
       q.staged_ok = 0;  // ... in the register kernel
       progs.push_back(q);

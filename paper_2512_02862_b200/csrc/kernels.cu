@@ -768,7 +768,7 @@ __global__ void __launch_bounds__(256) k_slab_consume(AggTableDev t, SlabConsume
         const uint64_t v = static_cast<uint64_t>(c.pmin[1 + k]) + ((w >> c.pshift[1 + k]) & c.pmask[1 + k]);
         e |= ((v - static_cast<uint64_t>(c.bmin[k])) & c.bmask[k]) << c.bshift[k];
       }
-      const uint64_t b = slot >> kBucketBits;
+      const uint64_t b = ((slot >> kBucketBits) << c.bsub_bits) | (threadIdx.x & ((1u << c.bsub_bits) - 1u));
       if (c.diag & 4) {  // measurement only (PSG_SLAB_DIAG=4): no bucket append
         if (e == ~0ULL) c.bkt[b] = e;
         continue;
@@ -865,13 +865,16 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
   __syncthreads();
   const uint64_t bucket = s_bucket, s0 = bucket << kBucketBits;
   const uint64_t s_end = min(s0 + kBucketSlots, nslots);
-  const uint32_t fill = b.fill[bucket], n = min(fill, b.cap);
-  const uint64_t* e = b.bkt + bucket * b.cap;
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-    const uint64_t w = __ldcs(reinterpret_cast<const unsigned long long*>(e + i));
-    const uint32_t sl = static_cast<uint32_t>(w & (kBucketSlots - 1));
-    atomicAdd(&m.hits[sl], 1u);
-    for (int k = 0; k < nps; ++k) add64_u32pair(&m.lo[k * kBucketSlots + sl], &m.hi[k * kBucketSlots + sl], (w >> b.shift[k]) & b.mask[k]);
+  for (uint64_t sub = bucket << b.sub_bits; sub < (bucket + 1) << b.sub_bits; ++sub) {
+    const uint32_t n = min(b.fill[sub], b.cap);
+    const uint64_t* e = b.bkt + sub * b.cap;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+      const uint64_t w = __ldcs(reinterpret_cast<const unsigned long long*>(e + i));
+      const uint32_t sl = static_cast<uint32_t>(w & (kBucketSlots - 1));
+      atomicAdd(&m.hits[sl], 1u);
+      for (int k = 0; k < nps; ++k)
+        add64_u32pair(&m.lo[k * kBucketSlots + sl], &m.hi[k * kBucketSlots + sl], (w >> b.shift[k]) & b.mask[k]);
+    }
   }
   __syncthreads();
   // rows that found a bucket full sit in the overflow list (rare; empty on the common path)

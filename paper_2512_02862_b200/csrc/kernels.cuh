@@ -83,9 +83,10 @@ void launch_gather64(const uint64_t* const* in_cols, int ncols, const uint64_t* 
 /// Phase-2 view of the bucketed aggregation (ScanProgram::bkt): nacc accumulator words per slot
 /// (hot words 1..nacc); word[k] = the accumulator an unpacked probe sum k adds to.
 struct BucketDev {
-  const uint64_t* bkt;
+  const uint64_t* bkt;         // [nbuckets << sub_bits][cap]: sub-lists of a bucket (ScanProgram::bkt)
   const unsigned int* fill;
   uint32_t cap;
+  int32_t sub_bits;
   int32_t nacc;
   int32_t shift[kMaxSums];
   uint64_t mask[kMaxSums];
@@ -117,6 +118,7 @@ struct SlabConsume {
   uint64_t* bkt;
   unsigned int* fill;
   uint32_t bcap;
+  int32_t bsub_bits;
   int32_t bshift[kMaxSums];
   uint64_t bmask[kMaxSums];
   int64_t bmin[kMaxSums];
