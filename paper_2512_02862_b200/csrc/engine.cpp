@@ -45,6 +45,9 @@ struct BucketOverflow : Error {
 };
 /// The key-bitmap build found what a rank-indexed table cannot hold (duplicate build keys, keys
 /// outside the zone-map range, no keys at all): the query is re-run on the materialising build path.
+/// Outbox slack of the peer-slab shuffle: one partly filled 256-word chunk per (warp, destination)
+/// of the probe kernel (148 SMs x 64 warps).
+constexpr uint64_t kSlabChunkSlack = 148ull * 64 * 256;
 struct KeybitsRetry : Error {
   KeybitsRetry() : Error(PSG_ERR_INTERNAL, "key-bitmap build not applicable") {}
 };
@@ -1278,6 +1281,50 @@ void Execution::build_local_tables() {
       PSG_TRACE_MSG("local table %s: regs %d in %d", lj.node->id.c_str(), m.n_regs, m.n_in);
       auto feed = open_feed(*rs.scan, file_cols_of(rs, m));
       PSG_TRACE_MSG("local table: feed %zu batches %llu rows", feed->nbatches, static_cast<unsigned long long>(feed->total_rows));
+      // Semi-join build straight into the membership bitmap (no payload, unique keys): the scan
+      // sets each surviving key's bit (SINK_KEYBITS) - no materialised keys, no bitmap pass. A
+      // duplicate key (or one outside the zone-map range) re-runs the query on the CSR table path.
+      if (lj.needed_payload.empty() && bitmap_env() && keybits_env() && jit_available() && !ctx_.no_keybits) {
+        long long lohi[2] = {LLONG_MAX, LLONG_MIN};
+        zone_range(lj.scan->paths, lj.proj.file_idx[lj.key_idx], lohi[0], lohi[1]);
+        const uint64_t range = lohi[1] >= lohi[0] ? static_cast<uint64_t>(lohi[1]) - static_cast<uint64_t>(lohi[0]) + 1 : 0;
+        if (range != 0 && range <= (1ULL << 34) && range / 64 <= feed->total_rows) {
+          const uint64_t words = (range + 31) / 32;
+          t->bitmap = DevBuf(ctx_.pool, words * 4, ctx_.compute);
+          DevBuf kc(ctx_.pool, 16, ctx_.compute);
+          PSG_CUDA(cudaMemsetAsync(t->bitmap.p, 0, words * 4, ctx_.compute));
+          PSG_CUDA(cudaMemsetAsync(kc.p, 0, 16, ctx_.compute));
+          ScanProgram kp = p;
+          kp.sink = SINK_KEYBITS;
+          kp.key_reg = out_regs[0];
+          kp.kb_bits = t->bitmap.as<uint32_t>();
+          kp.kb_min = lohi[0];
+          kp.kb_range = range;
+          kp.kb_count = kc.as<unsigned long long>();
+          kp.kb_flag = reinterpret_cast<unsigned int*>(kc.as<unsigned long long>() + 1);
+          BatchView v;
+          while (feed->next(v)) {
+            run_scan(kp, v, false);
+            feed->done();
+            st_.ingest_bytes += v.bytes;
+          }
+          uint64_t h[2] = {0, 0};
+          PSG_CUDA(cudaMemcpyAsync(h, kc.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+          PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+          if (h[1] == 0) {
+            t->unique = true;
+            std::memset(&t->dev, 0, sizeof t->dev);
+            t->dev.bitmap = t->bitmap.as<uint32_t>();
+            t->dev.bmin = lohi[0];
+            t->dev.brange = range;
+            tables.push_back(std::move(t));
+            continue;
+          }
+          // duplicates: the query re-runs with the materialising build (the replicated scan is the
+          // same on every rank, so every rank decides alike)
+          throw KeybitsRetry();
+        }
+      }
       DevCols mat = alloc_cols(out_regs.size(), std::max<uint64_t>(feed->total_rows, 1));
       BatchView v;
       while (feed->next(v)) {
@@ -2309,10 +2356,12 @@ ResultRows Execution::run(bool want_rows) {
     if (kb_direct && nr > 1 && !pdup && slab_env() && !ctx_.no_buckets && nr <= kMaxSlabPeers && pneed.size() >= 2 &&
         pneed.size() <= 4 && slab_plo.size() == pneed.size()) {
       slab_layout = plan_pack(slab_plo.data(), slab_phi.data(), static_cast<int>(pneed.size()));
-      slab_cap = std::max<uint64_t>(slab_max_rows, 1);
+      // every row, plus one partly filled chunk per (warp, destination) of the probe kernel
+      slab_cap = std::max<uint64_t>(slab_max_rows, 1) + kSlabChunkSlack;
       const size_t need = 512 + static_cast<size_t>(nr) * slab_cap * 8;
       const bool budget_ok = plan_.memory_budget_bytes == 0 || need <= plan_.memory_budget_bytes / 2;
-      slab_cand = slab_layout.fits && budget_ok && ensure_symmetric(need);
+      // (packed rows of at most 63 bits: bit 63 marks the padding of partly filled chunks)
+      slab_cand = slab_layout.fits && slab_layout.bits < 64 && budget_ok && ensure_symmetric(need);
     }
     if (rank_mode && (nr == 1 || slab_cand) && grouped_ && !pdup)
       bucket_mode_ = slab_cand ? setup_buckets(slab_plo.data() + 1, slab_phi.data() + 1, probe_rows_all) : setup_buckets();
@@ -2581,9 +2630,18 @@ ResultRows Execution::run(bool want_rows) {
     p.slab_cap = slab_cap_;
     unsigned long long* my_cnt = reinterpret_cast<unsigned long long*>(ctx_.symm + slab_cnt_off_);
     p.slab_cnt = my_cnt;
+    // pull (default): remote rows go to this rank's OWN outbox region for their destination (local
+    // HBM stores) and the owner reads them over NVLink after the barrier - the probe kernel's peer
+    // stores measured 0.3 ms of the 2.6 ms N=2 kernel. PSG_SLAB_PUSH=1: stores into the owner's
+    // inbox through NVLink from inside the probe kernel.
+    static const bool push = [] {
+      const char* e = std::getenv("PSG_SLAB_PUSH");
+      return e && e[0] == '1';
+    }();
     for (int d = 0; d < nr; ++d)
       p.slab_dst[d] = d == ctx_.rank ? nullptr
-                                     : reinterpret_cast<uint64_t*>(ctx_.symm_peer[d] + slab_off_) + static_cast<uint64_t>(ctx_.rank) * slab_cap_;
+                      : push ? reinterpret_cast<uint64_t*>(ctx_.symm_peer[d] + slab_off_) + static_cast<uint64_t>(ctx_.rank) * slab_cap_
+                             : reinterpret_cast<uint64_t*>(ctx_.symm + slab_off_) + static_cast<uint64_t>(d) * slab_cap_;
     // (the previous query's readers of these counters finished before this query's all-reduce)
     PSG_CUDA(cudaMemsetAsync(my_cnt, 0, static_cast<size_t>(nr) * 8, ctx_.compute));
     BatchView v;
@@ -2596,7 +2654,10 @@ ResultRows Execution::run(bool want_rows) {
     gpu_barrier();  // every source's slab stores landed
     pt.mark("  barrier", ctx_.compute);
     SlabConsume c{};
-    c.slab = reinterpret_cast<const uint64_t*>(ctx_.symm + slab_off_);
+    for (int r = 0; r < nr; ++r)
+      c.src_rows[r] = r == ctx_.rank ? nullptr
+                      : push ? reinterpret_cast<const uint64_t*>(ctx_.symm + slab_off_) + static_cast<uint64_t>(r) * slab_cap_
+                             : reinterpret_cast<const uint64_t*>(ctx_.symm_peer[r] + slab_off_) + static_cast<uint64_t>(ctx_.rank) * slab_cap_;
     for (int r = 0; r < nr; ++r)
       c.src_cnt[r] = r == ctx_.rank ? nullptr
                                     : reinterpret_cast<const unsigned long long*>(ctx_.symm_peer[r] + slab_cnt_off_) + ctx_.rank;
@@ -2640,6 +2701,47 @@ ResultRows Execution::run(bool want_rows) {
       for (int b = 0; b < aggt_.nbs; ++b) p.global_float[1 + p.n_sum + b] = aggt_.bs_float[b];
     }
     if (bucket_mode_) apply_buckets(p);
+    // PSG_SLAB_FAKE=1 (measurement only - the result is WRONG): the peer-slab probe kernel on one
+    // GPU, pretending to be rank 0 of 2 (half the keys "remote", staged into a local scratch
+    // outbox), so the N > 1 probe kernel can be profiled with ncu in a single process.
+    DevBuf fake_out, fake_cnt;
+    static const bool fake = [] {
+      const char* e = std::getenv("PSG_SLAB_FAKE");
+      return e && e[0] == '1';
+    }();
+    if (fake && bucket_mode_ && aggt_.krec && pneed.size() >= 2 && pneed.size() <= 4) {
+      std::vector<int64_t> lo(pneed.size(), INT64_MAX), hi(pneed.size(), INT64_MIN);
+      for (size_t k = 0; k < pneed.size(); ++k) {
+        long long a = LLONG_MAX, b = LLONG_MIN;
+        zone_range(psrc_.scan->paths, psrc_.proj.file_idx[psrc_.stage_refs.back()[pneed[k]].idx], a, b);
+        lo[k] = a, hi[k] = b;
+      }
+      const PackLayout L = plan_pack(lo.data(), hi.data(), static_cast<int>(pneed.size()));
+      uint64_t rows = 0;
+      for (const auto& path : psrc_.scan->paths) rows += ctx_.footers.get(path)->total_rows();
+      if (L.fits && L.bits < 64) {
+        fake_out = DevBuf(ctx_.pool, (std::max<uint64_t>(rows, 1) + kSlabChunkSlack) * 8, ctx_.compute);
+        fake_cnt = DevBuf(ctx_.pool, 16, ctx_.compute);
+        PSG_CUDA(cudaMemsetAsync(fake_cnt.p, 0, 16, ctx_.compute));
+        p.slab = 1;
+        p.nparts = 2;
+        p.self_rank = 0;
+        p.slab_cap = std::max<uint64_t>(rows, 1) + kSlabChunkSlack;
+        p.slab_cnt = fake_cnt.as<unsigned long long>();
+        p.slab_dst[1] = fake_out.as<uint64_t>();
+        p.semi_kbits = aggt_.kbits;
+        p.semi_kmin = aggt_.kmin;
+        p.semi_krange = aggt_.krange;
+        p.semi_key_reg = p.key_reg;
+        p.pack_n = static_cast<int>(pneed.size());
+        for (size_t k = 0; k < pneed.size(); ++k) {
+          p.pack_reg[k] = pm.reg_of.at(psrc_.stage_refs.back()[pneed[k]]);
+          p.pack_min[k] = L.min[k];
+          p.pack_shift[k] = L.shift[k];
+          p.pack_mask[k] = L.mask[k];
+        }
+      }
+    }
     BatchView v;
     while (pfeed->next(v)) {
       run_scan(p, v, staged_ != nullptr);

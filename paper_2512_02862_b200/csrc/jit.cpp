@@ -231,13 +231,18 @@ void emit_rank_tail(std::ostringstream& s, const ScanProgram& P) {
   s << "      }\n";
 }
 
-/// Peer-slab shuffle (P.slab, SINK_PROBE at N > 1): per-warp staging of the rows owned by other
-/// ranks in shared memory (packed word + destination), flushed 128 rows at a time: per destination
-/// ONE atomic reserves the positions in its slab region and the lanes store consecutive words
-/// over NVLink (coalesced). Per-row reservations on one counter serialised at the L2 (SF100 N=2:
-/// probe 1.7 -> 6.8 ms); per flush they are ~30x fewer. `w` indexes the warp's staging row.
-/// PSG_SLAB_DIAG (measurement only - results are wrong when set): 1 no NVLink stores, 2 remote
-/// rows dropped before staging.
+/// Peer-slab shuffle (P.slab, SINK_PROBE at N > 1): the rows owned by other ranks go into the
+/// outbox region of their destination in CHUNKS of kSlabChunk words a warp claims with one atomic
+/// (per-row reservations on one counter serialised at the L2: SF100 N=2 probe 1.7 -> 6.8 ms; a
+/// shared-memory staging buffer with per-flush reservations cost ~320 extra warp instructions per
+/// tile, profiles/r2_ncu_probe_fake.txt). The lanes of a warp with the same destination store
+/// consecutive words of the warp's current chunk; a chunk left partly filled (a new chunk was
+/// claimed, or the kernel ends) is padded with the sentinel word 1 << 63, never a packed row
+/// (slab mode requires packed rows of at most 63 bits). Chunk state per (warp, destination) lives
+/// in shared memory, updated warp-synchronously. `w` indexes the warp's state row.
+/// PSG_SLAB_DIAG (measurement only - results are wrong when set): 1 no outbox stores, 2 remote
+/// rows dropped, 8 remote rows screened through the own rank records (the one-GPU lookup
+/// footprint) instead of the global bitmap.
 int slab_diag() {
   static const int v = [] {
     const char* e = std::getenv("PSG_SLAB_DIAG");
@@ -245,24 +250,40 @@ int slab_diag() {
   }();
   return v;
 }
+constexpr int kSlabChunk = 256;
 
-void emit_slab_prologue(std::ostringstream& s, int nwarps, const std::string& w) {
-  s << "  __shared__ uint64_t s_slab[" << nwarps << "][128];\n  __shared__ unsigned char s_sdst[" << nwarps << "][128];\n"
-    << "  int sfill = 0;\n"
-    << "  auto sflush = [&]() {\n    __syncwarp();\n    if (sfill == 0) return;\n"
-    << "    const int ln = threadIdx.x & 31; const uint32_t lt = (1u << ln) - 1u;\n"
-    << "    for (int d = 0; d < P.nparts; ++d) {\n      if (d == P.self_rank) continue;\n"
-    << "      unsigned c = 0;\n      for (int i = ln; i < sfill; i += 32) c += s_sdst[" << w << "][i] == d;\n"
-    << "      const unsigned tot = __reduce_add_sync(0xffffffffu, c);\n      if (tot == 0) continue;\n"
-    << "      unsigned long long base = 0;\n"
-    << "      if (ln == 0) base = atomicAdd(P.slab_cnt + d, static_cast<unsigned long long>(tot));\n"
-    << "      base = __shfl_sync(0xffffffffu, base, 0);\n      unsigned off = 0;\n"
-    << "      for (int i0 = 0; i0 < sfill; i0 += 32) {\n        const int i = i0 + ln;\n"
-    << "        const bool mine = i < sfill && s_sdst[" << w << "][i] == d;\n"
-    << "        const unsigned b = __ballot_sync(0xffffffffu, mine);\n"
-    << "        if (mine) { const uint64_t pos = base + off + __popc(b & lt); if (pos < P.slab_cap" << ((slab_diag() & 1) ? " && pos == ~0ULL" : "")
-    << ") P.slab_dst[d][pos] = s_slab[" << w << "][i]; }\n"
-    << "        off += __popc(b);\n      }\n    }\n    sfill = 0;\n    __syncwarp();\n  };\n";
+void emit_slab_prologue(std::ostringstream& s, const ScanProgram& P, int nwarps, const std::string& w) {
+  s << "  __shared__ unsigned long long s_cbase[" << nwarps << "][" << P.nparts << "];\n"
+    << "  __shared__ unsigned s_cfill[" << nwarps << "][" << P.nparts << "];\n"
+    // warp-private state rows: each warp initialises its own (no block barrier: the warp-specialised
+    // kernel's producer warp has already left)
+    << "  for (int i = threadIdx.x & 31; i < " << P.nparts << "; i += 32) { s_cfill[" << w << "][i] = " << kSlabChunk
+    << "u; s_cbase[" << w << "][i] = ~0ULL; }\n  __syncwarp();\n"
+    // pad the rest of the chunk [from, kSlabChunk) of destination d with sentinels (lanes of `grp`)
+    << "  auto slab_pad = [&](unsigned grp, uint32_t d, unsigned long long base, unsigned from) {\n"
+    << "    if (base == ~0ULL) return;\n"
+    << "    const unsigned me = __popc(grp & ((1u << (threadIdx.x & 31)) - 1u)), n = __popc(grp);\n"
+    << "    for (unsigned i = from + me; i < " << kSlabChunk << "u; i += n) if (base + i < P.slab_cap) P.slab_dst[d][base + i] = 1ULL << 63;\n"
+    << "  };\n"
+    // append one word per lane of `on` lanes; dst per lane
+    << "  auto slab_put = [&](bool on, uint32_t d, uint64_t word) {\n"
+    << "    const unsigned grp = __match_any_sync(0xffffffffu, on ? d : 0xffffffffu);\n"
+    << "    if (on) {\n"
+    << "      const int leader = __ffs(grp) - 1; const unsigned cnt = __popc(grp);\n"
+    << "      unsigned fill = s_cfill[" << w << "][d]; unsigned long long base = s_cbase[" << w << "][d];\n"
+    << "      if (fill + cnt > " << kSlabChunk << "u) {\n"
+    << "        slab_pad(grp, d, base, fill);\n"
+    << "        if ((threadIdx.x & 31) == leader) base = atomicAdd(P.slab_cnt + d, " << kSlabChunk << "ULL);\n"
+    << "        base = __shfl_sync(grp, base, leader); fill = 0;\n      }\n"
+    << "      const unsigned long long pos = base + fill + __popc(grp & ((1u << (threadIdx.x & 31)) - 1u));\n"
+    << "      if (pos < P.slab_cap" << ((slab_diag() & 1) ? " && pos == ~0ULL" : "") << ") P.slab_dst[d][pos] = word;\n"
+    << "      __syncwarp(grp);\n"
+    << "      if ((threadIdx.x & 31) == leader) { s_cfill[" << w << "][d] = fill + cnt; s_cbase[" << w << "][d] = base; }\n"
+    << "    }\n    __syncwarp();\n  };\n"
+    // kernel end: pad every partly filled chunk of this warp
+    << "  auto slab_finish = [&]() {\n    __syncwarp();\n"
+    << "    for (uint32_t d = 0; d < " << P.nparts << "u; ++d) slab_pad(0xffffffffu, d, s_cbase[" << w << "][d], s_cfill[" << w << "][d]);\n"
+    << "  };\n";
 }
 
 /// The probe with the peer-slab shuffle: ONE dependent 16-byte lookup per row into the global
@@ -292,16 +313,9 @@ void emit_slab_probe1(std::ostringstream& s, const ScanProgram& P, Late late, co
     << "      pass = own | rem;\n";
   late();
   if (slab_diag() & 2) s << "      rem = 0;\n";
-  s << "      const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;\n"
-    << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
     << "        const bool on = (rem >> r) & 1u;\n"
-    << "        const unsigned b = __ballot_sync(0xffffffffu, on);\n"
-    << "        const int cnt = __popc(b);\n        if (cnt == 0) continue;\n"
-    << "        if (sfill + cnt > 128) sflush();\n"
-    << "        if (on) { const int pos = sfill + __popc(b & lt);\n"
-    << "          s_slab[" << w << "][pos] = " << out_value(P, 0) << ";\n"
-    << "          s_sdst[" << w << "][pos] = static_cast<unsigned char>(dst[r]); }\n"
-    << "        sfill += cnt;\n      }\n"
+    << "        if (__any_sync(0xffffffffu, on)) slab_put(on, dst[r], on ? " << out_value(P, 0) << " : 0ULL);\n      }\n"
     << "      pass = own;\n";
   emit_rank_tail(s, P);
   s << "    }\n";
@@ -319,26 +333,19 @@ void emit_slab_probe2(std::ostringstream& s, const ScanProgram& P, Late late, co
     << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bp[r] = 0; bb[r] = 0; dst[r] = 0; const uint64_t key = "
     << V(P.key_reg) << "[r];\n"
     << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
-    << "          if (d < T.krange) { const uint32_t o = part_of(key, static_cast<uint32_t>(P.nparts)); dst[r] = o;\n"
-    << "            if (o == static_cast<uint32_t>(P.self_rank)) { own |= 1u << r; bb[r] = static_cast<uint32_t>(d & 63);\n"
+    << "          if (d < T.krange) { const uint32_t o = part_of(key, " << P.nparts << "u); dst[r] = o;\n"
+    << "            if (o == " << P.self_rank << "u) { own |= 1u << r; bb[r] = static_cast<uint32_t>(d & 63);\n"
     << "              uint64_t a, b; ldg_keep_v2u64(T.krec + 2 * (d >> 6), pol_keep, a, b); bw[r] = a; bp[r] = b; }\n"
-    << "            else { rem |= 1u << r; bb[r] = static_cast<uint32_t>(d & 31); bw[r] = ldg_keep_u32(P.semi_kbits + (d >> 5), pol_keep); } } } }\n"
+    << "            else { rem |= 1u << r; " << ((slab_diag() & 8) ? "bb[r] = static_cast<uint32_t>(d & 63); uint64_t a, b; ldg_keep_v2u64(T.krec + 2 * (d >> 6), pol_keep, a, b); bw[r] = ~0ULL; bp[r] = a + b;" : "bb[r] = static_cast<uint32_t>(d & 31); bw[r] = ldg_keep_u32(P.semi_kbits + (d >> 5), pol_keep);") << " } } } }\n"
     << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0;\n"
     << "        if (!((bw[r] >> bb[r]) & 1ULL)) { own &= ~(1u << r); rem &= ~(1u << r); }\n"
     << "        else if ((own >> r) & 1u) sl[r] = bp[r] + static_cast<uint64_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n"
     << "      pass = own | rem;\n";
   late();
   if (slab_diag() & 2) s << "      rem = 0;\n";
-  s << "      const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;\n"
-    << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
     << "        const bool on = (rem >> r) & 1u;\n"
-    << "        const unsigned b = __ballot_sync(0xffffffffu, on);\n"
-    << "        const int cnt = __popc(b);\n        if (cnt == 0) continue;\n"
-    << "        if (sfill + cnt > 128) sflush();\n"
-    << "        if (on) { const int pos = sfill + __popc(b & lt);\n"
-    << "          s_slab[" << w << "][pos] = " << out_value(P, 0) << ";\n"
-    << "          s_sdst[" << w << "][pos] = static_cast<unsigned char>(dst[r]); }\n"
-    << "        sfill += cnt;\n      }\n"
+    << "        if (__any_sync(0xffffffffu, on)) slab_put(on, dst[r], on ? " << out_value(P, 0) << " : 0ULL);\n      }\n"
     << "      pass = own;\n";
   emit_rank_tail(s, P);
   s << "    }\n";
@@ -533,7 +540,7 @@ std::string jit_source(const ScanProgram& P) {
   if (glob) s << "  __shared__ unsigned long long s_gacc[" << nglob << "];\n";
   s << "  const int tid = threadIdx.x;\n  const int lane = tid & 31, warp = tid >> 5;\n  const int wrow = warp * (R * 32) + lane;\n"
     << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep; (void)wrow;\n";
-  if (P.slab) emit_slab_prologue(s, NW, "warp");
+  if (P.slab) emit_slab_prologue(s, P, NW, "warp");
   // SINK_KEYBITS row count: per lane, one atomic per warp at the end (a per-tile atomic on one
   // counter serialises at the L2)
   if (P.sink == SINK_KEYBITS) s << "  unsigned long long kb_rows = 0;\n";
@@ -774,7 +781,7 @@ std::string jit_source(const ScanProgram& P) {
   if (bscan) s << "    __syncthreads();\n";  // s_base / s_woff reuse by the next tile
   s << "    cur_col = pf_col; cur_r0 = pf_r0; cur_rows = pf_rows;\n  }\n";
   if (wstage) s << "  flush();\n";
-  if (P.slab) s << "  sflush();\n";
+  if (P.slab) s << "  slab_finish();\n";
   if (P.sink == SINK_KEYBITS)
     s << "  for (int o = 16; o > 0; o >>= 1) kb_rows += __shfl_xor_sync(0xffffffffu, kb_rows, o);\n"
       << "  if (lane == 0 && kb_rows) atomicAdd(P.kb_count, kb_rows);\n";
@@ -853,7 +860,7 @@ std::string jit_source_staged(const ScanProgram& P) {
   s << "      }\n    }\n    return;\n  }\n"
     << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep;\n"
     << "  const int cw = (warp - 1) % " << CW << ", grp = (warp - 1) / " << CW << ";\n  const int wrow = cw * (R * 32) + lane;\n";
-  if (P.slab && P.sink == SINK_PROBE) emit_slab_prologue(s, CW * NG, "warp - 1");
+  if (P.slab && P.sink == SINK_PROBE) emit_slab_prologue(s, P, CW * NG, "warp - 1");
   if (mat) {
     s << "  int fill = 0;\n  auto flush = [&]() {\n    __syncwarp();\n    if (fill == 0) return;\n"
       << "    unsigned long long base = 0;\n    if (lane == 0) base = atomicAdd(P.out_count, static_cast<unsigned long long>(fill));\n"
@@ -885,7 +892,7 @@ std::string jit_source_staged(const ScanProgram& P) {
   if (P.sink == SINK_PROBE) {
     if (P.slab) {
       emit_slab_probe(s, P, late, "warp - 1");
-      s << "  }\n  sflush();\n  __threadfence_system();  // slab stores visible to the owners before the kernel ends\n}\n";
+      s << "  }\n  slab_finish();\n  __threadfence_system();  // slab stores visible to the owners before the kernel ends\n}\n";
     } else {
       emit_rank_probe(s, P, late);
       s << "  }\n}\n";

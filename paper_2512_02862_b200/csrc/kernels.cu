@@ -754,33 +754,48 @@ __global__ void __launch_bounds__(256) k_slab_consume(AggTableDev t, SlabConsume
     const uint64_t n = min(static_cast<uint64_t>(s_n[src]), c.cap);
     if (n == 0) continue;
     if (gtid == 0) atomicAdd(c.received, static_cast<unsigned long long>(n));
-    const uint64_t* in = c.slab + static_cast<uint64_t>(src) * c.cap;
-    for (uint64_t i = gtid; i < n; i += stride) {
-      const uint64_t w = __ldcs(reinterpret_cast<const unsigned long long*>(in + i));
-      const uint64_t key = static_cast<uint64_t>(c.pmin[0]) + ((w >> c.pshift[0]) & c.pmask[0]);
-      const uint64_t d = key - static_cast<uint64_t>(t.kmin);
-      if (d >= t.krange) continue;  // (the senders' global screen guarantees membership)
-      const ulonglong2 rec = __ldg(reinterpret_cast<const ulonglong2*>(t.krec) + (d >> 6));
-      if (!((rec.x >> (d & 63)) & 1ULL)) continue;
-      const uint64_t slot = rec.y + static_cast<uint64_t>(__popcll(rec.x & ((1ULL << (d & 63)) - 1ULL)));
-      uint64_t e = slot & static_cast<uint64_t>(kBucketSlots - 1);
-      for (int k = 0; k + 1 < c.npack; ++k) {
-        const uint64_t v = static_cast<uint64_t>(c.pmin[1 + k]) + ((w >> c.pshift[1 + k]) & c.pmask[1 + k]);
-        e |= ((v - static_cast<uint64_t>(c.bmin[k])) & c.bmask[k]) << c.bshift[k];
+    const uint64_t* in = c.src_rows[src];
+    // 4 rows per thread per round: their loads (NVLink in the pull mode) and rank-record lookups
+    // are in flight together before the dependent appends
+    constexpr int U = 4;
+    for (uint64_t i0 = gtid; i0 < n; i0 += U * stride) {
+      uint64_t w[U], d[U];
+      ulonglong2 rec[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t i = i0 + u * stride;
+        w[u] = i < n ? __ldcs(reinterpret_cast<const unsigned long long*>(in + i)) : 0ULL;
       }
-      const uint64_t b = ((slot >> kBucketBits) << c.bsub_bits) | (threadIdx.x & ((1u << c.bsub_bits) - 1u));
-      if (c.diag & 4) {  // measurement only (PSG_SLAB_DIAG=4): no bucket append
-        if (e == ~0ULL) c.bkt[b] = e;
-        continue;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint64_t key = static_cast<uint64_t>(c.pmin[0]) + ((w[u] >> c.pshift[0]) & c.pmask[0]);
+        d[u] = i0 + u * stride < n && !(w[u] >> 63) ? key - static_cast<uint64_t>(t.kmin) : ~0ULL;
+        rec[u] = d[u] < t.krange ? __ldg(reinterpret_cast<const ulonglong2*>(t.krec) + (d[u] >> 6)) : make_ulonglong2(0, 0);
       }
-      const unsigned pos = atomicAdd(c.fill + b, 1u);
-      if (pos < c.bcap) {
-        c.bkt[b * c.bcap + pos] = e;
-      } else {
-        const unsigned o = atomicAdd(c.ovf_count, 1u);
-        if (o < c.ovf_cap) {
-          c.ovf[2 * o] = slot;
-          c.ovf[2 * o + 1] = e;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        // (padding of partly filled chunks: bit 63; the senders' global screen guarantees membership)
+        if (d[u] >= t.krange || !((rec[u].x >> (d[u] & 63)) & 1ULL)) continue;
+        const uint64_t slot = rec[u].y + static_cast<uint64_t>(__popcll(rec[u].x & ((1ULL << (d[u] & 63)) - 1ULL)));
+        uint64_t e = slot & static_cast<uint64_t>(kBucketSlots - 1);
+        for (int k = 0; k + 1 < c.npack; ++k) {
+          const uint64_t v = static_cast<uint64_t>(c.pmin[1 + k]) + ((w[u] >> c.pshift[1 + k]) & c.pmask[1 + k]);
+          e |= ((v - static_cast<uint64_t>(c.bmin[k])) & c.bmask[k]) << c.bshift[k];
+        }
+        const uint64_t b = ((slot >> kBucketBits) << c.bsub_bits) | (threadIdx.x & ((1u << c.bsub_bits) - 1u));
+        if (c.diag & 4) {  // measurement only (PSG_SLAB_DIAG=4): no bucket append
+          if (e == ~0ULL) c.bkt[b] = e;
+          continue;
+        }
+        const unsigned pos = atomicAdd(c.fill + b, 1u);
+        if (pos < c.bcap) {
+          c.bkt[b * c.bcap + pos] = e;
+        } else {
+          const unsigned o = atomicAdd(c.ovf_count, 1u);
+          if (o < c.ovf_cap) {
+            c.ovf[2 * o] = slot;
+            c.ovf[2 * o + 1] = e;
+          }
         }
       }
     }

@@ -106,7 +106,7 @@ void launch_own_mask(const unsigned long long* global, unsigned long long* own, 
                      int self, unsigned long long* cnt, void* stream);
 /// Peer-slab shuffle, owner side (kernels.cu k_slab_consume).
 struct SlabConsume {
-  const uint64_t* slab;                                // this rank's receive slab: region r = source r
+  const uint64_t* src_rows[kMaxSlabPeers];             // rows source r holds for this rank (peer-mapped outbox, or the local inbox)
   const unsigned long long* src_cnt[kMaxSlabPeers];    // rows source r stored here (peer-mapped; null: none)
   uint64_t cap;                                        // rows per region
   int32_t nsrc;
