@@ -1296,6 +1296,7 @@ void Execution::build_local_tables() {
           PSG_CUDA(cudaMemsetAsync(kc.p, 0, 16, ctx_.compute));
           ScanProgram kp = p;
           kp.sink = SINK_KEYBITS;
+          kp.staged_ok = 1;
           kp.key_reg = out_regs[0];
           kp.kb_bits = t->bitmap.as<uint32_t>();
           kp.kb_min = lohi[0];
@@ -2036,6 +2037,7 @@ ResultRows Execution::run(bool want_rows) {
     PSG_CUDA(cudaMemsetAsync(kb_cnt.p, 0, 16, ctx_.compute));
     ScanProgram p = bp;
     p.sink = SINK_KEYBITS;
+    p.staged_ok = 1;  // PSTO batches / staged images: 16-byte aligned chunks with tail padding
     p.key_reg = b_out[0];
     p.kb_bits = agg_kbits_.as<uint32_t>();
     p.kb_min = kb_lo;
@@ -2227,7 +2229,8 @@ ResultRows Execution::run(bool want_rows) {
       DevBuf cnts(ctx_.pool, 16, ctx_.compute);  // [own bits, global bits]
       PSG_CUDA(cudaMemsetAsync(cnts.p, 0, 16, ctx_.compute));
       if (nr > 1) {
-        semi_all = DevBuf(ctx_.pool, words64 * 8, ctx_.compute);
+        // (+1 word: the probe reads the global bitmap in aligned 16-byte chunks)
+        semi_all = DevBuf(ctx_.pool, (words64 + 1) * 8, ctx_.compute);
         PSG_NCCL(ncclAllReduce(agg_kbits_.p, semi_all.p, words64, ncclUint64, ncclSum, ctx_.nccl, ctx_.compute));
         PSG_NCCL(ncclAllReduce(kb_cnt.p, kb_cnt.p, 1, ncclUint64, ncclSum, ctx_.nccl, ctx_.compute));
         PSG_NCCL(ncclAllReduce(kb_cnt.as<unsigned long long>() + 1, kb_cnt.as<unsigned long long>() + 1, 1, ncclUint64,

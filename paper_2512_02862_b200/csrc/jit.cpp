@@ -280,10 +280,65 @@ void emit_slab_prologue(std::ostringstream& s, const ScanProgram& P, int nwarps,
     << "      __syncwarp(grp);\n"
     << "      if ((threadIdx.x & 31) == leader) { s_cfill[" << w << "][d] = fill + cnt; s_cbase[" << w << "][d] = base; }\n"
     << "    }\n    __syncwarp();\n  };\n"
-    // kernel end: pad every partly filled chunk of this warp
-    << "  auto slab_finish = [&]() {\n    __syncwarp();\n"
-    << "    for (uint32_t d = 0; d < " << P.nparts << "u; ++d) slab_pad(0xffffffffu, d, s_cbase[" << w << "][d], s_cfill[" << w << "][d]);\n"
-    << "  };\n";
+    ;
+  // two ranks: one destination, chunk state in (warp-uniform) registers, ballot instead of match
+  if (P.nparts == 2)
+    s << "  unsigned c2fill = " << kSlabChunk << "u; unsigned long long c2base = ~0ULL;\n"
+    << "  auto slab_put2 = [&](bool on, uint64_t word) {\n"
+    << "    const unsigned b = __ballot_sync(0xffffffffu, on);\n    if (!b) return;\n"
+    << "    const unsigned cnt = __popc(b);\n"
+    << "    if (c2fill + cnt > " << kSlabChunk << "u) {\n"
+    << "      slab_pad(0xffffffffu, " << 1 - P.self_rank << "u, c2base, c2fill);\n"
+    << "      unsigned long long nb = 0;\n"
+    << "      if ((threadIdx.x & 31) == 0) nb = atomicAdd(P.slab_cnt + " << 1 - P.self_rank << ", " << kSlabChunk << "ULL);\n"
+    << "      c2base = __shfl_sync(0xffffffffu, nb, 0); c2fill = 0;\n    }\n"
+    << "    const unsigned long long pos = c2base + c2fill + __popc(b & ((1u << (threadIdx.x & 31)) - 1u));\n"
+    << "    if (on && pos < P.slab_cap" << ((slab_diag() & 1) ? " && pos == ~0ULL" : "") << ") P.slab_dst[" << 1 - P.self_rank << "][pos] = word;\n"
+    << "    c2fill += cnt;\n  };\n";
+  // kernel end: pad every partly filled chunk of this warp
+  s << "  auto slab_finish = [&]() {\n    __syncwarp();\n";
+  if (P.nparts == 2) s << "    slab_pad(0xffffffffu, " << 1 - P.self_rank << "u, c2base, c2fill);\n";
+  // (chunks of the match-based put; untouched rows keep base ~0: no-op)
+  s << "    for (uint32_t d = 0; d < " << P.nparts << "u; ++d) slab_pad(0xffffffffu, d, s_cbase[" << w << "][d], s_cfill[" << w << "][d]);\n";
+  s << "  };\n";
+}
+
+/// Default peer-slab probe (PSG_SLAB_V=2: the branchy two-lookup emit_slab_probe2): branch-free -
+/// every row issues ONE 16-byte load whose base depends on its owner (own rank records, or the
+/// 16-byte chunk of the global bitmap holding its bit), so the warp does not diverge into two
+/// lookup paths; two ranks use the ballot-based register-state put.
+template <class Late>
+void emit_slab_probe3(std::ostringstream& s, const ScanProgram& P, Late late) {
+  // (slots and ranks in 32 bits: the engine caps a rank table at 2^32 keys; fewer registers at the
+  // 60-register cap of 2 x 544-thread CTAs per SM)
+  s << "    { const AggTableDev& T = P.agg; unsigned long long bw[R]; uint32_t bp[R], sl[R], bb[R], dst[R];\n"
+    << "      uint32_t own = 0, rem = 0;\n"
+    << "      const unsigned long long* gbits = reinterpret_cast<const unsigned long long*>(P.semi_kbits);\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { const uint64_t key = " << V(P.key_reg) << "[r];\n"
+    << "        const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+    << "        const bool ok = ((pass >> r) & 1u) && key != kEmptyKey && d < T.krange;\n"
+    << "        const uint32_t o = part_of(key, " << P.nparts << "u); dst[r] = o;\n"
+    << "        const bool mine = o == " << P.self_rank << "u;\n"
+    << "        uint64_t a = 0, b = 0;\n"
+    << "        if (ok) ldg_keep_v2u64(mine ? T.krec + 2 * (d >> 6) : gbits + 2 * (d >> 7), pol_keep, a, b);\n"
+    << "        bb[r] = static_cast<uint32_t>(d & 63);\n"
+    << "        bw[r] = (mine || !((d >> 6) & 1)) ? a : b; bp[r] = mine ? static_cast<uint32_t>(b) : 0u;\n"
+    << "        own |= static_cast<uint32_t>(ok && mine) << r; rem |= static_cast<uint32_t>(ok && !mine) << r; }\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+    << "        if (!((bw[r] >> bb[r]) & 1ULL)) { own &= ~(1u << r); rem &= ~(1u << r); }\n"
+    << "        sl[r] = bp[r] + static_cast<uint32_t>(__popcll(bw[r] & ((1ULL << bb[r]) - 1ULL))); }\n"
+    << "      pass = own | rem;\n";
+  late();
+  if (slab_diag() & 2) s << "      rem = 0;\n";
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+    << "        const bool on = (rem >> r) & 1u;\n";
+  if (P.nparts == 2)
+    s << "        slab_put2(on, on ? " << out_value(P, 0) << " : 0ULL);\n      }\n";
+  else
+    s << "        if (__any_sync(0xffffffffu, on)) slab_put(on, dst[r], on ? " << out_value(P, 0) << " : 0ULL);\n      }\n";
+  s << "      pass = own;\n";
+  emit_rank_tail(s, P);
+  s << "    }\n";
 }
 
 /// The probe with the peer-slab shuffle: ONE dependent 16-byte lookup per row into the global
@@ -360,12 +415,21 @@ bool slab_grec_env() {
   }();
   return v;
 }
+int slab_variant() {
+  static const int v = [] {
+    const char* e = std::getenv("PSG_SLAB_V");
+    return e ? std::atoi(e) : 3;
+  }();
+  return v;
+}
 template <class Late>
 void emit_slab_probe(std::ostringstream& s, const ScanProgram& P, Late late, const std::string& w) {
   if (P.slab_grec != nullptr && slab_grec_env())
     emit_slab_probe1(s, P, late, w);
-  else
+  else if (slab_variant() == 2)
     emit_slab_probe2(s, P, late, w);
+  else
+    emit_slab_probe3(s, P, late);
 }
 
 /// Predicate atoms: clear a row's pass bit when an atom fails.
@@ -460,6 +524,14 @@ bool staged_probe(const ScanProgram& P) {
   }();
   if (!on || !P.staged_ok || P.remote || P.unpack_n != 0 || P.n_early < 1 || P.n_early > 4 || P.n_in > kMaxIn) return false;
   if (P.sink == SINK_PROBE) return P.agg.krec != nullptr;
+  // the key-bitmap build (orders: date + customer key early, the order key late): opt-in
+  // (PSG_TMA_KB=1) - measured slower than the register kernel (SF100 N=1 orders scan 0.91 vs
+  // 0.75 ms: its chain date -> customer bitmap -> order key -> bit is short per row)
+  static const bool kb_on = [] {
+    const char* e = std::getenv("PSG_TMA_KB");
+    return e && e[0] == '1';
+  }();
+  if (P.sink == SINK_KEYBITS) return kb_on;
   // unordered warp-staged compaction (+ partition histogram, semi-join screen, packed rows):
   // opt-in (PSG_TMA_MAT=1) - the SF100 orders scan measured slower staged (0.97 vs 0.73 ms: three
   // early columns leave room for one CTA per SM)
@@ -488,6 +560,7 @@ int jit_rows(const ScanProgram& P) {
   const bool probe = P.sink == SINK_PROBE || P.sink == SINK_PROBE_GLOBAL;
   if (env == "p") return probe ? 8 : 4;
   if (env == "pm") return probe || P.sink == SINK_MATERIALIZE ? 8 : 4;
+  if (env == "pk") return probe || P.sink == SINK_KEYBITS ? 8 : 4;
   return 4;
 }
 int jit_block(const ScanProgram& P) { return 1024 / jit_rows(P); }
@@ -861,6 +934,7 @@ std::string jit_source_staged(const ScanProgram& P) {
     << "  const uint64_t pol_keep = l2_evict_last(); (void)pol_keep;\n"
     << "  const int cw = (warp - 1) % " << CW << ", grp = (warp - 1) / " << CW << ";\n  const int wrow = cw * (R * 32) + lane;\n";
   if (P.slab && P.sink == SINK_PROBE) emit_slab_prologue(s, P, CW * NG, "warp - 1");
+  if (P.sink == SINK_KEYBITS) s << "  unsigned long long kb_rows = 0;\n";
   if (mat) {
     s << "  int fill = 0;\n  auto flush = [&]() {\n    __syncwarp();\n    if (fill == 0) return;\n"
       << "    unsigned long long base = 0;\n    if (lane == 0) base = atomicAdd(P.out_count, static_cast<unsigned long long>(fill));\n"
@@ -897,6 +971,18 @@ std::string jit_source_staged(const ScanProgram& P) {
       emit_rank_probe(s, P, late);
       s << "  }\n}\n";
     }
+    return s.str();
+  }
+  if (P.sink == SINK_KEYBITS) {  // late key column for the survivors, then their bits
+    late();
+    s << "    { unsigned nset = 0;\n#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+      << "        const uint64_t d = " << V(P.key_reg) << "[r] - static_cast<uint64_t>(P.kb_min);\n"
+      << "        ++nset;\n        if (d >= P.kb_range) { atomicOr(P.kb_flag, 2u); continue; }\n"
+      << "        const uint32_t bit = 1u << (d & 31);\n"
+      << "        if (atomicOr(P.kb_bits + (d >> 5), bit) & bit) atomicOr(P.kb_flag, 1u); }\n"
+      << "      kb_rows += nset;\n    }\n  }\n"
+      << "  for (int o = 16; o > 0; o >>= 1) kb_rows += __shfl_xor_sync(0xffffffffu, kb_rows, o);\n"
+      << "  if (lane == 0 && kb_rows) atomicAdd(P.kb_count, kb_rows);\n}\n";
     return s.str();
   }
   // MATERIALIZE: screen -> late columns -> per-warp staging in shared memory, flushed 128 rows at
@@ -1156,6 +1242,10 @@ int jit_selftest(std::string& log) {
       progs.push_back(q);
       q.staged_ok = 0;  // ... in the register kernel
       progs.push_back(q);
+      q.staged_ok = 1;  // two ranks: the ballot-based put
+      q.nparts = 2;
+      q.self_rank = 1;
+      progs.push_back(q);
     }
     if (sink == SINK_PROBE) {  // consuming packed rows
       ScanProgram q = p;
@@ -1168,6 +1258,8 @@ int jit_selftest(std::string& log) {
   {
     ScanProgram p = base();  // build side straight into the key bitmap
     p.sink = SINK_KEYBITS;
+    progs.push_back(p);
+    p.staged_ok = 1;  // ... warp-specialised
     progs.push_back(p);
   }
   {
