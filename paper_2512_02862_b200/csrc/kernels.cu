@@ -883,12 +883,23 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
   for (uint64_t sub = bucket << b.sub_bits; sub < (bucket + 1) << b.sub_bits; ++sub) {
     const uint32_t n = min(b.fill[sub], b.cap);
     const uint64_t* e = b.bkt + sub * b.cap;
-    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
-      const uint64_t w = __ldcs(reinterpret_cast<const unsigned long long*>(e + i));
-      const uint32_t sl = static_cast<uint32_t>(w & (kBucketSlots - 1));
-      atomicAdd(&m.hits[sl], 1u);
-      for (int k = 0; k < nps; ++k)
-        add64_u32pair(&m.lo[k * kBucketSlots + sl], &m.hi[k * kBucketSlots + sl], (w >> b.shift[k]) & b.mask[k]);
+    // 4 entries per thread per round: their loads are in flight together before the folds
+    for (uint32_t i0 = threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {
+      uint64_t w4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t i = i0 + u * blockDim.x;
+        w4[u] = i < n ? __ldcs(reinterpret_cast<const unsigned long long*>(e + i)) : 0ULL;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (i0 + u * blockDim.x >= n) break;
+        const uint64_t w = w4[u];
+        const uint32_t sl = static_cast<uint32_t>(w & (kBucketSlots - 1));
+        atomicAdd(&m.hits[sl], 1u);
+        for (int k = 0; k < nps; ++k)
+          add64_u32pair(&m.lo[k * kBucketSlots + sl], &m.hi[k * kBucketSlots + sl], (w >> b.shift[k]) & b.mask[k]);
+      }
     }
   }
   __syncthreads();
@@ -927,25 +938,36 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
     m.pos[wbase + k * 32 + lane] = static_cast<uint16_t>(acc + __popc(flags[k] & below));
     acc += __popc(flags[k]);
   }
-  if (threadIdx.x == 0) {  // look-back: this bucket's output offset
+  if (threadIdx.x < 32) {  // warp-wide decoupled look-back: this bucket's output offset
     uint32_t total = 0;
     for (int w = 0; w < 16; ++w) total += s_warp[w];
     constexpr unsigned long long kCount = 1ULL << 62, kPrefix = 2ULL << 62, kVal = (1ULL << 62) - 1;
     unsigned long long prefix = 0;
     if (bucket == 0) {
-      atomicExch(&state[0], kPrefix | total);
+      if (lane == 0) atomicExch(&state[0], kPrefix | total);
     } else {
-      atomicExch(&state[bucket], kCount | total);
-      for (int64_t j = static_cast<int64_t>(bucket) - 1; j >= 0;) {
-        const unsigned long long v = atomicAdd(&state[j], 0ULL);
-        if ((v >> 62) == 0) continue;  // predecessor still folding (it runs: it claimed its ticket first)
-        prefix += v & kVal;
-        if ((v >> 62) == 2) break;
-        --j;
+      if (lane == 0) atomicExch(&state[bucket], kCount | total);
+      // 32 predecessors per round (one lane each, nearest first): sum back to the nearest one
+      // that has published its inclusive prefix; a round with a predecessor still folding (flag
+      // 0) before that point is re-read (it runs: it claimed its ticket first). A one-thread walk
+      // read one predecessor per L2 round trip (~600 CTAs in flight: the emit's top stall).
+      for (int64_t j = static_cast<int64_t>(bucket) - 1;;) {
+        const int64_t idx = j - lane;
+        const unsigned long long v = idx >= 0 ? atomicAdd(&state[idx], 0ULL) : kPrefix;
+        const unsigned f = static_cast<unsigned>(v >> 62);
+        const unsigned pm = __ballot_sync(0xffffffffu, f == 2), zm = __ballot_sync(0xffffffffu, f == 0);
+        const int fp = pm ? __ffs(pm) - 1 : 32;  // nearest lane holding a prefix
+        const unsigned need = fp < 31 ? (2u << fp) - 1u : 0xffffffffu;
+        if (zm & need) continue;
+        unsigned long long c = lane <= fp ? (v & kVal) : 0ULL;
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        prefix += c;
+        if (fp < 32) break;
+        j -= 32;
       }
-      atomicExch(&state[bucket], kPrefix | (prefix + total));
+      if (lane == 0) atomicExch(&state[bucket], kPrefix | (prefix + total));
     }
-    s_base = prefix;
+    if (lane == 0) s_base = prefix;
   }
   __syncthreads();
   // rows in key order: walk the key-bitmap words covering the bucket's slots
