@@ -568,6 +568,20 @@ class Execution {
   DevCols materialize_chain(const SourceDef& s, const RegMap& m, const BatchView& v, const std::vector<int>& out_regs);
   DevCols concat_cols(std::vector<DevCols>& parts, size_t ncols);
   uint64_t read_count(DevCols& c);
+  // duplicate flags of local semi-join bitmaps built optimistically (SINK_KEYBITS), [rows, flag]
+  // each: enqueue their reads before a host sync the query makes anyway, then check
+  std::vector<DevBuf> lt_flags_;
+  std::vector<uint64_t> lt_flag_host_;
+  void enqueue_lt_flags() {
+    lt_flag_host_.assign(2 * lt_flags_.size(), 0);
+    for (size_t i = 0; i < lt_flags_.size(); ++i)
+      PSG_CUDA(cudaMemcpyAsync(lt_flag_host_.data() + 2 * i, lt_flags_[i].p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+  }
+  void check_lt_flags() {  // after the sync that completed enqueue_lt_flags' copies
+    for (size_t i = 0; i < lt_flags_.size(); ++i)
+      if (lt_flag_host_[2 * i + 1] != 0) throw KeybitsRetry();
+    lt_flags_.clear();
+  }
   // event pairs around the timed (dominant) kernel launches, resolved after the query's last sync
   // (no host sync per launch)
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed_;
@@ -1309,21 +1323,17 @@ void Execution::build_local_tables() {
             feed->done();
             st_.ingest_bytes += v.bytes;
           }
-          uint64_t h[2] = {0, 0};
-          PSG_CUDA(cudaMemcpyAsync(h, kc.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
-          PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
-          if (h[1] == 0) {
-            t->unique = true;
-            std::memset(&t->dev, 0, sizeof t->dev);
-            t->dev.bitmap = t->bitmap.as<uint32_t>();
-            t->dev.bmin = lohi[0];
-            t->dev.brange = range;
-            tables.push_back(std::move(t));
-            continue;
-          }
-          // duplicates: the query re-runs with the materialising build (the replicated scan is the
-          // same on every rank, so every rank decides alike)
-          throw KeybitsRetry();
+          // optimistic: the duplicate flag is read with the query's next host read (check_lt_flags;
+          // no sync here). Duplicates re-run the query with the materialising build (the
+          // replicated scan is the same on every rank, so every rank decides alike).
+          lt_flags_.push_back(std::move(kc));
+          t->unique = true;
+          std::memset(&t->dev, 0, sizeof t->dev);
+          t->dev.bitmap = t->bitmap.as<uint32_t>();
+          t->dev.bmin = lohi[0];
+          t->dev.brange = range;
+          tables.push_back(std::move(t));
+          continue;
         }
       }
       DevCols mat = alloc_cols(out_regs.size(), std::max<uint64_t>(feed->total_rows, 1));
@@ -2241,7 +2251,9 @@ ResultRows Execution::run(bool want_rows) {
       uint64_t h[4] = {0, 0, 0, 0};
       PSG_CUDA(cudaMemcpyAsync(h, kb_cnt.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
       PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      enqueue_lt_flags();
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+      check_lt_flags();
       pt.mark("  key bitmap (all-reduce, own bits)", ctx_.compute);
       const uint64_t rows_set = h[0], flag = h[1];
       // duplicates within a rank set the flag; across ranks the SUM carried, so the global bit
@@ -2985,8 +2997,10 @@ ResultRows Execution::run(bool want_rows) {
       st_.result_bytes += total * nc * 8;
     }
   }
+  if (!lt_flags_.empty()) enqueue_lt_flags();
   PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
   PSG_CUDA(cudaGetLastError());
+  if (!lt_flags_.empty()) check_lt_flags();
   pt.mark("finalize", ctx_.compute);
   PSG_CUDA(cudaEventRecord(ev1, ctx_.compute));
   PSG_CUDA(cudaEventSynchronize(ev1));
@@ -3131,8 +3145,10 @@ ResultRows Execution::run_local() {
     st_.ingest_bytes += v.bytes;
   }
   finalize_global(out);
+  if (!lt_flags_.empty()) enqueue_lt_flags();
   PSG_CUDA(cudaEventRecord(ev1, ctx_.compute));
   PSG_CUDA(cudaEventSynchronize(ev1));
+  if (!lt_flags_.empty()) check_lt_flags();
   float dms = 0;
   PSG_CUDA(cudaEventElapsedTime(&dms, ev0, ev1));
   cudaEventDestroy(ev0);
@@ -3375,8 +3391,19 @@ ResultRows execute_plan(Ctx& ctx, const std::string& plan_json, const std::strin
 ResultRows execute_local(Ctx& ctx, const std::string& plan_json, const std::string& data_root, int mode) {
   PSG_CUDA(cudaSetDevice(ctx.device));
   if (mode < 0 || mode > 3) throw InvalidInput("unknown execution mode");
-  Execution ex(ctx, plan_json, data_root, mode, nullptr);
-  return ex.run_local();
+  // a local semi-join bitmap that found duplicate keys re-runs on the materialising path
+  try {
+    Execution ex(ctx, plan_json, data_root, mode, nullptr);
+    return ex.run_local();
+  } catch (const KeybitsRetry&) {
+    struct Flag {
+      Ctx& c;
+      ~Flag() { c.no_keybits = false; }
+    } flag{ctx};
+    ctx.no_keybits = true;
+    Execution ex(ctx, plan_json, data_root, mode, nullptr);
+    return ex.run_local();
+  }
 }
 
 Staged* stage_plan(Ctx& ctx, const std::string& plan_json, const std::string& data_root) {
