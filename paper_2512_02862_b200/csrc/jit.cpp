@@ -192,6 +192,32 @@ void emit_rank_tail(std::ostringstream& s, const ScanProgram& P);
 /// surviving rows only), then every survivor accumulates into its hot slot.
 template <class Late>
 void emit_rank_probe(std::ostringstream& s, const ScanProgram& P, Late late) {
+  // Screen first (PSG_RANK_SCREEN=0: off): test the 4-byte word of the key bitmap (19 MB vs the
+  // rank records' 37 MB at SF100), then read the rank record only for the survivors, with the late
+  // columns. SF100 N=1 A/B: probe 3.23 -> 3.19 ms.
+  static const bool screen_first = [] {
+    const char* e = std::getenv("PSG_RANK_SCREEN");
+    return !(e && e[0] == '0');
+  }();
+  if (screen_first && P.agg.krec != nullptr && P.agg.kbits != nullptr) {
+    s << "    { const AggTableDev& T = P.agg; uint32_t gw[R], bb[R], kr[R], sl[R]; unsigned long long kw[R]; uint32_t sel = 0;\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { const uint64_t key = " << V(P.key_reg) << "[r];\n"
+      << "        const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+      << "        const bool ok = ((pass >> r) & 1u) && key != kEmptyKey && d < T.krange;\n"
+      << "        bb[r] = static_cast<uint32_t>(d & 31); gw[r] = ok ? ldg_keep_u32(T.kbits + (d >> 5), pol_keep) : 0u; }\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((gw[r] >> bb[r]) & 1u) sel |= 1u << r;\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { kw[r] = 0; kr[r] = 0; if ((sel >> r) & 1u) {\n"
+      << "        const uint64_t d = " << V(P.key_reg) << "[r] - static_cast<uint64_t>(T.kmin);\n"
+      << "        uint64_t a, b; ldg_keep_v2u64(T.krec + 2 * (d >> 6), pol_keep, a, b); kw[r] = a; kr[r] = static_cast<uint32_t>(b); } }\n"
+      << "      pass = sel;\n";
+    late();
+    s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { const uint32_t d6 = static_cast<uint32_t>((" << V(P.key_reg)
+      << "[r] - static_cast<uint64_t>(T.kmin)) & 63);\n"
+      << "        sl[r] = kr[r] + static_cast<uint32_t>(__popcll(kw[r] & ((1ULL << d6) - 1ULL))); }\n";
+    emit_rank_tail(s, P);
+    s << "    }\n";
+    return;
+  }
   s << "    { const AggTableDev& T = P.agg; uint64_t sl[R]; unsigned long long bw[R]; uint64_t bp[R]; uint32_t bb[R];\n"
     << "#pragma unroll\n      for (int r = 0; r < R; ++r) { bw[r] = 0; bp[r] = 0; bb[r] = 0; const uint64_t key = " << V(P.key_reg) << "[r];\n"
     << "        if ((pass & (1u << r)) && key != kEmptyKey) { const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
@@ -415,10 +441,48 @@ bool slab_grec_env() {
   }();
   return v;
 }
+/// Screen-first peer-slab probe (default; PSG_SLAB_V=3: the one-lookup branch-free variant; SF100
+/// N=2 A/B: probe 2.34 -> 2.04 ms, query 3.66 -> 3.36 ms): every
+/// predicate-passing row tests its bit in the 4-byte word of the GLOBAL key bitmap (19 MB at SF100
+/// - half the rank records' footprint, so more of the 300 M lookups hit L2); only the ~10% that
+/// survive compute their owner, and the owned ones read their rank record (slot) together with
+/// the late columns - the extra lookup overlaps the HBM gathers.
+template <class Late>
+void emit_slab_probe4(std::ostringstream& s, const ScanProgram& P, Late late) {
+  s << "    { const AggTableDev& T = P.agg; uint32_t gw[R], bb[R], kr[R], sl[R], dst[R]; unsigned long long kw[R];\n"
+    << "      uint32_t sel = 0, own = 0, rem = 0;\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { const uint64_t key = " << V(P.key_reg) << "[r];\n"
+    << "        const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+    << "        const bool ok = ((pass >> r) & 1u) && key != kEmptyKey && d < T.krange;\n"
+    << "        bb[r] = static_cast<uint32_t>(d & 31); gw[r] = ok ? ldg_keep_u32(P.semi_kbits + (d >> 5), pol_keep) : 0u; }\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) if ((gw[r] >> bb[r]) & 1u) sel |= 1u << r;\n"
+    << "#pragma unroll\n      for (int r = 0; r < R; ++r) { dst[r] = 0; kw[r] = 0; kr[r] = 0;\n"
+    << "        if ((sel >> r) & 1u) { const uint64_t key = " << V(P.key_reg) << "[r];\n"
+    << "          const uint32_t o = part_of(key, " << P.nparts << "u); dst[r] = o;\n"
+    << "          if (o == " << P.self_rank << "u) { own |= 1u << r; const uint64_t d = key - static_cast<uint64_t>(T.kmin);\n"
+    << "            uint64_t a, b; ldg_keep_v2u64(T.krec + 2 * (d >> 6), pol_keep, a, b); kw[r] = a; kr[r] = static_cast<uint32_t>(b); }\n"
+    << "          else rem |= 1u << r; } }\n"
+    << "      pass = sel;\n";
+  late();
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { const uint32_t d6 = static_cast<uint32_t>((" << V(P.key_reg)
+    << "[r] - static_cast<uint64_t>(T.kmin)) & 63);\n"
+    << "        sl[r] = kr[r] + static_cast<uint32_t>(__popcll(kw[r] & ((1ULL << d6) - 1ULL))); }\n";
+  if (slab_diag() & 2) s << "      rem = 0;\n";
+  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+    << "        const bool on = (rem >> r) & 1u;\n";
+  if (P.nparts == 2)
+    s << "        slab_put2(on, on ? " << out_value(P, 0) << " : 0ULL);\n      }\n";
+  else
+    s << "        if (__any_sync(0xffffffffu, on)) slab_put(on, dst[r], on ? " << out_value(P, 0) << " : 0ULL);\n      }\n";
+  s << "      pass = own;\n";
+  emit_rank_tail(s, P);
+  s << "    }\n";
+}
+
 int slab_variant() {
   static const int v = [] {
     const char* e = std::getenv("PSG_SLAB_V");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 4;
   }();
   return v;
 }
@@ -428,8 +492,10 @@ void emit_slab_probe(std::ostringstream& s, const ScanProgram& P, Late late, con
     emit_slab_probe1(s, P, late, w);
   else if (slab_variant() == 2)
     emit_slab_probe2(s, P, late, w);
-  else
+  else if (slab_variant() == 3)
     emit_slab_probe3(s, P, late);
+  else
+    emit_slab_probe4(s, P, late);
 }
 
 /// Predicate atoms: clear a row's pass bit when an atom fails.
