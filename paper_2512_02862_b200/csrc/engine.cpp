@@ -2039,21 +2039,67 @@ ResultRows Execution::run(bool want_rows) {
       }
     }
   }
+  // N > 1: the local key bitmaps (and their duplicate flags) go into the symmetric heap, so every
+  // rank ORs them through NVLink (k_or_own) instead of a SUM all-reduce; the heap also holds the
+  // peer-slab outboxes when that path applies. One collective sizing (every input all-reduced).
+  bool kb_heap = false;
+  size_t kb_bits_off = 0, kb_cnt_off = 0;
+  bool slab_possible = false;
+  PackLayout slab_layout;
+  uint64_t slab_cap = 0;
+  if (kb_direct && nr > 1) {
+    const uint64_t words64 = (kb_range + 63) / 64;
+    if (!pdup && slab_env() && !ctx_.no_buckets && nr <= kMaxSlabPeers && pneed.size() >= 2 && pneed.size() <= 4 &&
+        slab_plo.size() == pneed.size()) {
+      slab_layout = plan_pack(slab_plo.data(), slab_phi.data(), static_cast<int>(pneed.size()));
+      // every row, plus one partly filled chunk per (warp, destination) of the probe kernel
+      slab_cap = std::max<uint64_t>(slab_max_rows, 1) + kSlabChunkSlack;
+      const size_t sneed = 512 + static_cast<size_t>(nr) * slab_cap * 8;
+      const bool budget_ok = plan_.memory_budget_bytes == 0 || sneed <= plan_.memory_budget_bytes / 2;
+      // (packed rows of at most 63 bits: bit 63 marks the padding of partly filled chunks)
+      slab_possible = slab_layout.fits && slab_layout.bits < 64 && budget_ok;
+    }
+    static const bool or_env = [] {  // PSG_KB_OR=0: SUM all-reduce of the rank bitmaps
+      const char* e = std::getenv("PSG_KB_OR");
+      return !(e && e[0] == '0');
+    }();
+    const size_t bneed = ((words64 * 8 + 255) & ~size_t(255)) + 256;
+    const size_t need = (or_env ? bneed : 0) + (slab_possible ? 512 + static_cast<size_t>(nr) * slab_cap * 8 + 256 : 0);
+    if (need && ensure_symmetric(need)) {
+      ctx_.symm_top = 0;
+      if (or_env) {
+        kb_bits_off = static_cast<size_t>(ctx_.symm_alloc(words64 * 8) - ctx_.symm);
+        kb_cnt_off = static_cast<size_t>(ctx_.symm_alloc(16) - ctx_.symm);
+        kb_heap = true;
+      }
+    } else {
+      slab_possible = false;
+    }
+  }
   if (kb_direct) {
     const uint64_t words64 = (kb_range + 63) / 64;
-    agg_kbits_ = DevBuf(ctx_.pool, words64 * 8, ctx_.compute);
-    kb_cnt = DevBuf(ctx_.pool, 16, ctx_.compute);
-    PSG_CUDA(cudaMemsetAsync(agg_kbits_.p, 0, words64 * 8, ctx_.compute));
-    PSG_CUDA(cudaMemsetAsync(kb_cnt.p, 0, 16, ctx_.compute));
+    uint32_t* kbits = nullptr;
+    unsigned long long* kcnt = nullptr;
+    if (kb_heap) {
+      kbits = reinterpret_cast<uint32_t*>(ctx_.symm + kb_bits_off);
+      kcnt = reinterpret_cast<unsigned long long*>(ctx_.symm + kb_cnt_off);
+    } else {
+      agg_kbits_ = DevBuf(ctx_.pool, words64 * 8, ctx_.compute);
+      kb_cnt = DevBuf(ctx_.pool, 16, ctx_.compute);
+      kbits = agg_kbits_.as<uint32_t>();
+      kcnt = kb_cnt.as<unsigned long long>();
+    }
+    PSG_CUDA(cudaMemsetAsync(kbits, 0, words64 * 8, ctx_.compute));
+    PSG_CUDA(cudaMemsetAsync(kcnt, 0, 16, ctx_.compute));
     ScanProgram p = bp;
     p.sink = SINK_KEYBITS;
     p.staged_ok = 1;  // PSTO batches / staged images: 16-byte aligned chunks with tail padding
     p.key_reg = b_out[0];
-    p.kb_bits = agg_kbits_.as<uint32_t>();
+    p.kb_bits = kbits;
     p.kb_min = kb_lo;
     p.kb_range = kb_range;
-    p.kb_count = kb_cnt.as<unsigned long long>();
-    p.kb_flag = reinterpret_cast<unsigned int*>(kb_cnt.as<unsigned long long>() + 1);
+    p.kb_count = kcnt;
+    p.kb_flag = reinterpret_cast<unsigned int*>(kcnt + 1);
     BatchView v;
     while (bfeed->next(v)) {
       run_scan(p, v, false);
@@ -2236,9 +2282,23 @@ ResultRows Execution::run(bool want_rows) {
       // the key bitmap was set by the build scan itself: N > 1 all-reduces it into the global key
       // set (semi_all) and keeps the bits this rank owns; one host read checks the key counts
       const uint64_t words64 = (kb_range + 63) / 64;
-      DevBuf cnts(ctx_.pool, 16, ctx_.compute);  // [own bits, global bits]
-      PSG_CUDA(cudaMemsetAsync(cnts.p, 0, 16, ctx_.compute));
-      if (nr > 1) {
+      DevBuf cnts(ctx_.pool, 24, ctx_.compute);  // [own bits, global bits, duplicate]
+      PSG_CUDA(cudaMemsetAsync(cnts.p, 0, 24, ctx_.compute));
+      if (nr > 1 && kb_heap) {
+        gpu_barrier();  // every rank's local bitmap and flag are complete
+        semi_all = DevBuf(ctx_.pool, (words64 + 1) * 8, ctx_.compute);
+        agg_kbits_ = DevBuf(ctx_.pool, words64 * 8, ctx_.compute);
+        OrPeers op{};
+        op.n = nr;
+        for (int r = 0; r < nr; ++r) {
+          op.bits[r] = reinterpret_cast<const unsigned long long*>(ctx_.symm_peer[r] + kb_bits_off);
+          op.flag[r] = reinterpret_cast<const unsigned int*>(ctx_.symm_peer[r] + kb_cnt_off + 8);
+        }
+        launch_or_own(op, words64, kb_lo, ctx_.rank, semi_all.as<unsigned long long>(), agg_kbits_.as<unsigned long long>(),
+                      cnts.as<unsigned long long>(), ctx_.compute);
+        // (a peer may still read this rank's local bitmap: it is rewritten only by the next query's
+        // build scan, which follows this query's collectives)
+      } else if (nr > 1) {
         // (+1 word: the probe reads the global bitmap in aligned 16-byte chunks)
         semi_all = DevBuf(ctx_.pool, (words64 + 1) * 8, ctx_.compute);
         PSG_NCCL(ncclAllReduce(agg_kbits_.p, semi_all.p, words64, ncclUint64, ncclSum, ctx_.nccl, ctx_.compute));
@@ -2248,18 +2308,28 @@ ResultRows Execution::run(bool want_rows) {
         launch_own_mask(semi_all.as<unsigned long long>(), agg_kbits_.as<unsigned long long>(), words64, kb_lo, nr,
                         ctx_.rank, cnts.as<unsigned long long>(), ctx_.compute);
       }
-      uint64_t h[4] = {0, 0, 0, 0};
-      PSG_CUDA(cudaMemcpyAsync(h, kb_cnt.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
-      PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      uint64_t h[5] = {0, 0, 0, 0, 0};
+      if (kb_heap) {
+        PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 24, cudaMemcpyDeviceToHost, ctx_.compute));
+      } else {
+        PSG_CUDA(cudaMemcpyAsync(h, kb_cnt.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+        PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      }
       enqueue_lt_flags();
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
       check_lt_flags();
-      pt.mark("  key bitmap (all-reduce, own bits)", ctx_.compute);
-      const uint64_t rows_set = h[0], flag = h[1];
-      // duplicates within a rank set the flag; across ranks the SUM carried, so the global bit
-      // count falls short of the rows that set bits
-      if (flag != 0 || rows_set == 0 || rows_set >= (1ULL << 32) || (nr > 1 && h[3] != rows_set)) throw KeybitsRetry();
-      build_rows = nr > 1 ? h[2] : rows_set;
+      pt.mark("  key bitmap (global, own bits)", ctx_.compute);
+      if (kb_heap) {
+        // the OR kernel saw every rank's flag and every overlap: identical on all ranks
+        if (h[4] != 0 || h[3] == 0 || h[3] >= (1ULL << 32)) throw KeybitsRetry();
+        build_rows = h[2];
+      } else {
+        const uint64_t rows_set = h[0], flag = h[1];
+        // duplicates within a rank set the flag; across ranks the SUM carried, so the global bit
+        // count falls short of the rows that set bits
+        if (flag != 0 || rows_set == 0 || rows_set >= (1ULL << 32) || (nr > 1 && h[3] != rows_set)) throw KeybitsRetry();
+        build_rows = nr > 1 ? h[2] : rows_set;
+      }
       krange_lo = kb_lo;
       krange = kb_range;
       bloom_words = 0;
@@ -2364,24 +2434,12 @@ ResultRows Execution::run(bool want_rows) {
     // bit-packed word stored by the probe kernel straight into the owner's receive slab over
     // NVLink (symmetric heap, one region per source rank, sized for the largest probe side), the
     // owners fold them into their buckets after a device-side barrier. PSG_SLAB=0: NCCL shuffle.
-    // (every input of these decisions is all-reduced or plan-wide: all ranks agree)
-    bool slab_cand = false;
-    PackLayout slab_layout;
-    uint64_t slab_cap = 0;
-    if (kb_direct && nr > 1 && !pdup && slab_env() && !ctx_.no_buckets && nr <= kMaxSlabPeers && pneed.size() >= 2 &&
-        pneed.size() <= 4 && slab_plo.size() == pneed.size()) {
-      slab_layout = plan_pack(slab_plo.data(), slab_phi.data(), static_cast<int>(pneed.size()));
-      // every row, plus one partly filled chunk per (warp, destination) of the probe kernel
-      slab_cap = std::max<uint64_t>(slab_max_rows, 1) + kSlabChunkSlack;
-      const size_t need = 512 + static_cast<size_t>(nr) * slab_cap * 8;
-      const bool budget_ok = plan_.memory_budget_bytes == 0 || need <= plan_.memory_budget_bytes / 2;
-      // (packed rows of at most 63 bits: bit 63 marks the padding of partly filled chunks)
-      slab_cand = slab_layout.fits && slab_layout.bits < 64 && budget_ok && ensure_symmetric(need);
-    }
+    // (every input of these decisions is all-reduced or plan-wide: all ranks agree; the heap was
+    // sized with the key bitmaps above)
+    const bool slab_cand = slab_possible && ctx_.symm_bytes > 0;
     if (rank_mode && (nr == 1 || slab_cand) && grouped_ && !pdup)
       bucket_mode_ = slab_cand ? setup_buckets(slab_plo.data() + 1, slab_phi.data() + 1, probe_rows_all) : setup_buckets();
     if (slab_cand && bucket_mode_) {
-      ctx_.symm_top = 0;
       uint8_t* cnt = ctx_.symm_alloc(static_cast<size_t>(nr) * 8);
       uint8_t* slab = ctx_.symm_alloc(static_cast<size_t>(nr) * slab_cap * 8);
       if (!cnt || !slab) throw Error(PSG_ERR_INTERNAL, "symmetric heap layout");

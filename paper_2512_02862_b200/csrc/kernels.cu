@@ -736,6 +736,77 @@ void launch_own_mask(const unsigned long long* global, unsigned long long* own, 
   k_own_mask<<<grid_for(nwords, 256), 256, 0, S(stream)>>>(global, own, nwords, kmin, nparts, self, cnt);
 }
 
+/// Global key bitmap at N > 1 without a collective: every rank's local bitmap (set by its build
+/// scan) lives in the symmetric heap, and each rank ORs all of them word by word through NVLink
+/// (16-byte loads), keeping the owned bits too. Keys two ranks both hold (duplicates: the rank
+/// table needs unique keys) show as a word whose summed popcounts exceed the popcount of the OR;
+/// with every rank's own duplicate flag (read from its heap) that gives dup, identical on every
+/// rank (same inputs), so the re-run decision needs no all-reduce. cnt[0] += own bits, cnt[1] +=
+/// global bits, cnt[2] |= dup.
+__global__ void k_or_own(OrPeers p, uint64_t nwords, int64_t kmin, int self, unsigned long long* __restrict__ global,
+                         unsigned long long* __restrict__ own, unsigned long long* cnt) {
+  unsigned long long no = 0, ng = 0;
+  bool dup = false;
+  if (blockIdx.x == 0 && threadIdx.x < p.n)
+    dup = *reinterpret_cast<const volatile unsigned int*>(p.flag[threadIdx.x]) != 0;
+  const uint64_t npairs = nwords / 2;
+  auto word = [&](uint64_t w, unsigned long long g, int s) {
+    if (s != __popcll(g)) dup = true;
+    unsigned long long m = 0, rest = g;
+    const uint64_t base = static_cast<uint64_t>(kmin) + (w << 6);
+    while (rest) {
+      const int b = __ffsll(static_cast<long long>(rest)) - 1;
+      rest &= rest - 1;
+      if (part_of(base + b, static_cast<uint32_t>(p.n)) == static_cast<uint32_t>(self)) m |= 1ULL << b;
+    }
+    global[w] = g;
+    own[w] = m;
+    no += __popcll(m);
+    ng += __popcll(g);
+  };
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < npairs;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long g0 = 0, g1 = 0;
+    int s0 = 0, s1 = 0;
+    for (int r = 0; r < p.n; ++r) {
+      const ulonglong2 x = __ldcs(reinterpret_cast<const ulonglong2*>(p.bits[r]) + i);
+      g0 |= x.x, g1 |= x.y;
+      s0 += __popcll(x.x), s1 += __popcll(x.y);
+    }
+    word(2 * i, g0, s0);
+    word(2 * i + 1, g1, s1);
+  }
+  if ((nwords & 1) && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long g = 0;
+    int sc = 0;
+    for (int r = 0; r < p.n; ++r) {
+      const unsigned long long x = p.bits[r][nwords - 1];
+      g |= x;
+      sc += __popcll(x);
+    }
+    word(nwords - 1, g, sc);
+  }
+  no = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(no));
+  ng = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(ng));
+  const unsigned anydup = __ballot_sync(0xffffffffu, dup);
+  if ((threadIdx.x & 31) == 0) {
+    if (no | ng) {
+      atomicAdd(cnt, no);
+      atomicAdd(cnt + 1, ng);
+    }
+    if (anydup) atomicOr(cnt + 2, 1ULL);
+  }
+}
+void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, unsigned long long* global,
+                   unsigned long long* own, unsigned long long* cnt, void* stream) {
+  if (nwords == 0) return;
+  count_launch();
+  int sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_or_own<<<sms * 8, 256, 0, S(stream)>>>(p, nwords, kmin, self, global, own, cnt);
+}
+
 /// Peer-slab shuffle, owner side: every packed row the other ranks stored into this rank's
 /// receive slab (region r = source r, *c.src_cnt[r] rows, read from the source's counters through
 /// NVLink after the cross-rank barrier) is unpacked, finds its slot in the rank-indexed table

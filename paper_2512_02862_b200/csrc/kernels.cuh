@@ -104,6 +104,16 @@ void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuck
 /// Own-key bitmap of a rank (N > 1) from the global one; cnt[0..1] += own / global popcounts.
 void launch_own_mask(const unsigned long long* global, unsigned long long* own, uint64_t nwords, int64_t kmin, int nparts,
                      int self, unsigned long long* cnt, void* stream);
+/// Every rank's local key bitmap (peer-mapped) and duplicate flag, for k_or_own.
+struct OrPeers {
+  const unsigned long long* bits[kMaxSlabPeers];
+  const unsigned int* flag[kMaxSlabPeers];
+  int32_t n;
+};
+/// Global (OR over ranks through NVLink) and own key bitmaps; cnt[0..2] += own bits, global bits,
+/// |= duplicate (k_or_own, kernels.cu).
+void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, unsigned long long* global,
+                   unsigned long long* own, unsigned long long* cnt, void* stream);
 /// Peer-slab shuffle, owner side (kernels.cu k_slab_consume).
 struct SlabConsume {
   const uint64_t* src_rows[kMaxSlabPeers];             // rows source r holds for this rank (peer-mapped outbox, or the local inbox)
