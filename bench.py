@@ -406,6 +406,20 @@ def main():
                           "within_budget": bool(reduce(float(bpeak)) <= bplan["memory_budget_bytes"])}
         except Exception as e:
             e2e_budget = {"error": str(e)[:200], "budget_bytes": bplan["memory_budget_bytes"]}
+    # the paper's blocking vs overlapped comparison (ExecMode, pipeline.hpp:124): the blocking mode
+    # runs the storage phase (every needed chunk into HBM) before the compute/network phase
+    e2e_modes = {"overlapped": e2e["value"]}
+    try:
+        mt = []
+        for _ in range(min(e2e_steps, 3)):
+            sync_all()
+            t = time.time()
+            r = ctx.execute_plan(plan, data_root, mode="blocking")
+            mt.append(time.time() - t)
+            del r
+        e2e_modes["blocking"] = round(reduce(statistics.mean(mt)), 4)
+    except Exception as e:
+        e2e_modes["blocking_error"] = str(e)[:200]
     e2e_block = None
     if with_block:
         e2e_block, parity_block, _, _ = e2e_run(block_root, min(e2e_steps, 10), "block codec")
@@ -515,6 +529,7 @@ def main():
             "e2e": e2e,
             "e2e_block": e2e_block,
             "e2e_budget": e2e_budget,
+            "e2e_modes": e2e_modes,
             "e2e_roofline": e2e_roof,
             "gpu_launches": int(launches),
             "clocks": clk.summary(),

@@ -2099,7 +2099,7 @@ ResultRows Execution::run(bool want_rows) {
     p.kb_min = kb_lo;
     p.kb_range = kb_range;
     p.kb_count = kcnt;
-    p.kb_flag = reinterpret_cast<unsigned int*>(kcnt + 1);
+    p.kb_flag = nullptr;  // bits by reductions; duplicates = fewer set bits than rows (checked below)
     BatchView v;
     while (bfeed->next(v)) {
       run_scan(p, v, false);
@@ -2278,12 +2278,23 @@ ResultRows Execution::run(bool want_rows) {
     long long krange_lo = 0;
     uint64_t krange = 0;
     const bool rank_ok = grouped_ && rank_env && jit_available() && !p2p;
+    auto rank_records = [&](uint64_t kwords64) {  // popcount prefix per 64-bit word + interleaved {bits, rank} records
+      DevBuf cnt(ctx_.pool, kwords64 * 4, ctx_.compute);
+      agg_krank_ = DevBuf(ctx_.pool, kwords64 * 4, ctx_.compute);
+      launch_popc64(agg_kbits_.as<unsigned long long>(), kwords64, cnt.as<uint32_t>(), ctx_.compute);
+      const size_t tb = exclusive_scan_u32(nullptr, nullptr, kwords64, nullptr, 0, ctx_.compute);
+      DevBuf tmp(ctx_.pool, tb, ctx_.compute);
+      exclusive_scan_u32(cnt.as<uint32_t>(), agg_krank_.as<uint32_t>(), kwords64, tmp.p, tb, ctx_.compute);
+      agg_krec_ = DevBuf(ctx_.pool, kwords64 * 16, ctx_.compute);
+      launch_krec_build(agg_kbits_.as<unsigned long long>(), agg_krank_.as<uint32_t>(), kwords64,
+                        agg_krec_.as<unsigned long long>(), ctx_.compute);
+    };
     if (kb_direct) {
       // the key bitmap was set by the build scan itself: N > 1 all-reduces it into the global key
       // set (semi_all) and keeps the bits this rank owns; one host read checks the key counts
       const uint64_t words64 = (kb_range + 63) / 64;
-      DevBuf cnts(ctx_.pool, 24, ctx_.compute);  // [own bits, global bits, duplicate]
-      PSG_CUDA(cudaMemsetAsync(cnts.p, 0, 24, ctx_.compute));
+      DevBuf cnts(ctx_.pool, 32, ctx_.compute);  // [own bits, global bits, overlap, summed rows]
+      PSG_CUDA(cudaMemsetAsync(cnts.p, 0, 32, ctx_.compute));
       if (nr > 1 && kb_heap) {
         gpu_barrier();  // every rank's local bitmap and flag are complete
         semi_all = DevBuf(ctx_.pool, (words64 + 1) * 8, ctx_.compute);
@@ -2292,7 +2303,7 @@ ResultRows Execution::run(bool want_rows) {
         op.n = nr;
         for (int r = 0; r < nr; ++r) {
           op.bits[r] = reinterpret_cast<const unsigned long long*>(ctx_.symm_peer[r] + kb_bits_off);
-          op.flag[r] = reinterpret_cast<const unsigned int*>(ctx_.symm_peer[r] + kb_cnt_off + 8);
+          op.rows[r] = reinterpret_cast<const unsigned long long*>(ctx_.symm_peer[r] + kb_cnt_off);
         }
         launch_or_own(op, words64, kb_lo, ctx_.rank, semi_all.as<unsigned long long>(), agg_kbits_.as<unsigned long long>(),
                       cnts.as<unsigned long long>(), ctx_.compute);
@@ -2308,27 +2319,35 @@ ResultRows Execution::run(bool want_rows) {
         launch_own_mask(semi_all.as<unsigned long long>(), agg_kbits_.as<unsigned long long>(), words64, kb_lo, nr,
                         ctx_.rank, cnts.as<unsigned long long>(), ctx_.compute);
       }
-      uint64_t h[5] = {0, 0, 0, 0, 0};
-      if (kb_heap) {
-        PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 24, cudaMemcpyDeviceToHost, ctx_.compute));
-      } else {
-        PSG_CUDA(cudaMemcpyAsync(h, kb_cnt.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
-        PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 16, cudaMemcpyDeviceToHost, ctx_.compute));
-      }
+      // the rank records of the (own) bitmap are queued before the host read: at one GPU its
+      // popcount (last prefix + last word) is the duplicate check
+      rank_records((kb_range + 63) / 64);
+      uint64_t h[6] = {0, 0, 0, 0, 0, 0};
+      uint32_t last_rank = 0;
+      PSG_CUDA(cudaMemcpyAsync(h, kb_cnt.p ? kb_cnt.p : ctx_.symm + kb_cnt_off, 16, cudaMemcpyDeviceToHost, ctx_.compute));
+      PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 32, cudaMemcpyDeviceToHost, ctx_.compute));
+      const uint64_t wl = (kb_range + 63) / 64 - 1;
+      PSG_CUDA(cudaMemcpyAsync(&last_rank, agg_krank_.as<uint32_t>() + wl, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+      uint64_t last_word = 0;
+      PSG_CUDA(cudaMemcpyAsync(&last_word, agg_kbits_.as<unsigned long long>() + wl, 8, cudaMemcpyDeviceToHost, ctx_.compute));
       enqueue_lt_flags();
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
       check_lt_flags();
       pt.mark("  key bitmap (global, own bits)", ctx_.compute);
+      const uint64_t rows_set = h[0];
       if (kb_heap) {
-        // the OR kernel saw every rank's flag and every overlap: identical on all ranks
-        if (h[4] != 0 || h[3] == 0 || h[3] >= (1ULL << 32)) throw KeybitsRetry();
+        // overlaps and the summed row counts of every rank: identical on all ranks
+        if (h[4] != 0 || h[5] != h[3] || h[3] == 0 || h[3] >= (1ULL << 32)) throw KeybitsRetry();
+        build_rows = h[2];
+      } else if (nr > 1) {
+        // (rows_set is the all-reduced sum) a repeated key left fewer bits than rows; across ranks
+        // the SUM all-reduce carried: fewer global bits than rows as well
+        if (rows_set == 0 || rows_set >= (1ULL << 32) || h[3] != rows_set) throw KeybitsRetry();
         build_rows = h[2];
       } else {
-        const uint64_t rows_set = h[0], flag = h[1];
-        // duplicates within a rank set the flag; across ranks the SUM carried, so the global bit
-        // count falls short of the rows that set bits
-        if (flag != 0 || rows_set == 0 || rows_set >= (1ULL << 32) || (nr > 1 && h[3] != rows_set)) throw KeybitsRetry();
-        build_rows = nr > 1 ? h[2] : rows_set;
+        const uint64_t bits_set = static_cast<uint64_t>(last_rank) + static_cast<uint64_t>(__builtin_popcountll(last_word));
+        if (rows_set == 0 || rows_set >= (1ULL << 32) || bits_set != rows_set) throw KeybitsRetry();
+        build_rows = rows_set;
       }
       krange_lo = kb_lo;
       krange = kb_range;
@@ -2378,20 +2397,8 @@ ResultRows Execution::run(bool want_rows) {
     }
     bool rank_mode = false;
     const uint64_t kwords64 = (krange + 63) / 64;
-    auto rank_records = [&] {  // popcount prefix per 64-bit word + interleaved {bits, rank} records
-      DevBuf cnt(ctx_.pool, kwords64 * 4, ctx_.compute);
-      agg_krank_ = DevBuf(ctx_.pool, kwords64 * 4, ctx_.compute);
-      launch_popc64(agg_kbits_.as<unsigned long long>(), kwords64, cnt.as<uint32_t>(), ctx_.compute);
-      const size_t tb = exclusive_scan_u32(nullptr, nullptr, kwords64, nullptr, 0, ctx_.compute);
-      DevBuf tmp(ctx_.pool, tb, ctx_.compute);
-      exclusive_scan_u32(cnt.as<uint32_t>(), agg_krank_.as<uint32_t>(), kwords64, tmp.p, tb, ctx_.compute);
-      agg_krec_ = DevBuf(ctx_.pool, kwords64 * 16, ctx_.compute);
-      launch_krec_build(agg_kbits_.as<unsigned long long>(), agg_krank_.as<uint32_t>(), kwords64,
-                        agg_krec_.as<unsigned long long>(), ctx_.compute);
-    };
     if (kb_direct) {
-      rank_records();
-      rank_mode = true;
+      rank_mode = true;  // (rank records queued with the key-bitmap check above)
     } else if (krange && rank_ok && krange_lo != LLONG_MIN && kwords64 < (1ULL << 32) && build_rows > 0 &&
                build_rows < (1ULL << 32)) {
       agg_kbits_ = DevBuf(ctx_.pool, kwords64 * 8, ctx_.compute);
@@ -2405,7 +2412,7 @@ ResultRows Execution::run(bool want_rows) {
       PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
       pt.mark("  key bitmap + dup check", ctx_.compute);
       if (!d) {
-        rank_records();
+        rank_records(kwords64);
         rank_mode = true;
       }
     }

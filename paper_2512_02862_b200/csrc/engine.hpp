@@ -202,6 +202,9 @@ class Ingest {
   std::mutex mu_;
   std::condition_variable cv_;
   size_t next_job_ = 0;
+  long cur_batch_ = -1;        // batch whose pieces are being handed out
+  size_t cur_ext_ = 0;         // its next extent
+  std::vector<int> pending_;   // per batch: pieces being read
   std::vector<int> slot_of_batch_;
   std::deque<int> free_slots_;
   bool stop_ = false;
@@ -214,6 +217,8 @@ class Ingest {
     int slot;
   };
   std::vector<std::unique_ptr<CopyDone>> done_args_;
+  cudaStream_t cb_stream_ = nullptr;     // slot-release host callbacks (off the copy stream)
+  std::vector<cudaEvent_t> slot_ev_;     // per pinned slot: its copy's completion
 };
 
 struct Ctx {

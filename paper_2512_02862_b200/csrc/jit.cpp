@@ -498,6 +498,23 @@ void emit_slab_probe(std::ostringstream& s, const ScanProgram& P, Late late, con
     emit_slab_probe4(s, P, late);
 }
 
+/// SINK_KEYBITS: every surviving row sets its key's bit. With kb_flag a duplicate (bit already
+/// set) or out-of-range key raises the flag (atomics with a return value: the warp waits on them);
+/// without it the bits are set by reductions (no return, nothing to wait for) and the engine
+/// detects duplicates / out-of-range keys as fewer set bits than rows (kb_count).
+void emit_keybits(std::ostringstream& s, const ScanProgram& P) {
+  s << "    { unsigned nset = 0;\n#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+    << "        const uint64_t d = " << V(P.key_reg) << "[r] - static_cast<uint64_t>(P.kb_min);\n"
+    << "        ++nset;\n";
+  if (P.kb_flag != nullptr)
+    s << "        if (d >= P.kb_range) { atomicOr(P.kb_flag, 2u); continue; }\n"
+      << "        const uint32_t bit = 1u << (d & 31);\n"
+      << "        if (atomicOr(P.kb_bits + (d >> 5), bit) & bit) atomicOr(P.kb_flag, 1u); }\n";
+  else
+    s << "        if (d < P.kb_range) atomicOr(P.kb_bits + (d >> 5), 1u << (d & 31)); }\n";
+  s << "      kb_rows += nset;\n    }\n";
+}
+
 /// Predicate atoms: clear a row's pass bit when an atom fails.
 void emit_atoms(std::ostringstream& s, const ScanProgram& P) {
   for (int a = 0; a < P.n_atoms; ++a) {
@@ -830,12 +847,7 @@ std::string jit_source(const ScanProgram& P) {
       }
       s << "    }\n";
     } else if (P.sink == SINK_KEYBITS) {  // build side straight into the key bitmap
-      s << "    { unsigned nset = 0;\n#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
-        << "        const uint64_t d = " << V(P.key_reg) << "[r] - static_cast<uint64_t>(P.kb_min);\n"
-        << "        ++nset;\n        if (d >= P.kb_range) { atomicOr(P.kb_flag, 2u); continue; }\n"
-        << "        const uint32_t bit = 1u << (d & 31);\n"
-        << "        if (atomicOr(P.kb_bits + (d >> 5), bit) & bit) atomicOr(P.kb_flag, 1u); }\n"
-        << "      kb_rows += nset;\n    }\n";
+      emit_keybits(s, P);
     } else if (P.sink == SINK_BUILD) {
       s << "    { const AggTableDev& T = P.agg;\n      uint64_t sl[R]; unsigned long long pv[R];\n"
         << "#pragma unroll\n      for (int r = 0; r < R; ++r) { sl[r] = 0; pv[r] = kEmptyKey; if (!(pass & (1u << r))) continue;\n"
@@ -1041,12 +1053,8 @@ std::string jit_source_staged(const ScanProgram& P) {
   }
   if (P.sink == SINK_KEYBITS) {  // late key column for the survivors, then their bits
     late();
-    s << "    { unsigned nset = 0;\n#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
-      << "        const uint64_t d = " << V(P.key_reg) << "[r] - static_cast<uint64_t>(P.kb_min);\n"
-      << "        ++nset;\n        if (d >= P.kb_range) { atomicOr(P.kb_flag, 2u); continue; }\n"
-      << "        const uint32_t bit = 1u << (d & 31);\n"
-      << "        if (atomicOr(P.kb_bits + (d >> 5), bit) & bit) atomicOr(P.kb_flag, 1u); }\n"
-      << "      kb_rows += nset;\n    }\n  }\n"
+    emit_keybits(s, P);
+    s << "  }\n"
       << "  for (int o = 16; o > 0; o >>= 1) kb_rows += __shfl_xor_sync(0xffffffffu, kb_rows, o);\n"
       << "  if (lane == 0 && kb_rows) atomicAdd(P.kb_count, kb_rows);\n}\n";
     return s.str();
@@ -1325,6 +1333,9 @@ int jit_selftest(std::string& log) {
     ScanProgram p = base();  // build side straight into the key bitmap
     p.sink = SINK_KEYBITS;
     progs.push_back(p);
+    p.kb_flag = reinterpret_cast<unsigned int*>(16);  // ... with the in-kernel duplicate flag
+    progs.push_back(p);
+    p.kb_flag = nullptr;
     p.staged_ok = 1;  // ... warp-specialised
     progs.push_back(p);
   }

@@ -739,16 +739,17 @@ void launch_own_mask(const unsigned long long* global, unsigned long long* own, 
 /// Global key bitmap at N > 1 without a collective: every rank's local bitmap (set by its build
 /// scan) lives in the symmetric heap, and each rank ORs all of them word by word through NVLink
 /// (16-byte loads), keeping the owned bits too. Keys two ranks both hold (duplicates: the rank
-/// table needs unique keys) show as a word whose summed popcounts exceed the popcount of the OR;
-/// with every rank's own duplicate flag (read from its heap) that gives dup, identical on every
-/// rank (same inputs), so the re-run decision needs no all-reduce. cnt[0] += own bits, cnt[1] +=
-/// global bits, cnt[2] |= dup.
+/// table needs unique keys) show as a word whose summed popcounts exceed the popcount of the OR
+/// (cnt[2]); a key repeated within a rank, or outside the range, as fewer global bits than the
+/// summed row counts of the ranks' build scans (cnt[3], read from their heaps). Identical on every
+/// rank (same inputs): the re-run decision needs no all-reduce. cnt[0] += own bits, cnt[1] +=
+/// global bits.
 __global__ void k_or_own(OrPeers p, uint64_t nwords, int64_t kmin, int self, unsigned long long* __restrict__ global,
                          unsigned long long* __restrict__ own, unsigned long long* cnt) {
   unsigned long long no = 0, ng = 0;
   bool dup = false;
-  if (blockIdx.x == 0 && threadIdx.x < p.n)
-    dup = *reinterpret_cast<const volatile unsigned int*>(p.flag[threadIdx.x]) != 0;
+  if (blockIdx.x == 0 && threadIdx.x < p.n)  // every rank's row count: sum == global bits unless keys repeat
+    atomicAdd(cnt + 3, *reinterpret_cast<const volatile unsigned long long*>(p.rows[threadIdx.x]));
   const uint64_t npairs = nwords / 2;
   auto word = [&](uint64_t w, unsigned long long g, int s) {
     if (s != __popcll(g)) dup = true;

@@ -107,11 +107,11 @@ void launch_own_mask(const unsigned long long* global, unsigned long long* own, 
 /// Every rank's local key bitmap (peer-mapped) and duplicate flag, for k_or_own.
 struct OrPeers {
   const unsigned long long* bits[kMaxSlabPeers];
-  const unsigned int* flag[kMaxSlabPeers];
+  const unsigned long long* rows[kMaxSlabPeers];  // rows that set bits (the build scan's kb_count)
   int32_t n;
 };
-/// Global (OR over ranks through NVLink) and own key bitmaps; cnt[0..2] += own bits, global bits,
-/// |= duplicate (k_or_own, kernels.cu).
+/// Global (OR over ranks through NVLink) and own key bitmaps; cnt[0..3] += own bits, global bits,
+/// |= overlap, += summed rows (k_or_own, kernels.cu).
 void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, unsigned long long* global,
                    unsigned long long* own, unsigned long long* cnt, void* stream);
 /// Peer-slab shuffle, owner side (kernels.cu k_slab_consume).
