@@ -1497,12 +1497,13 @@ bool Execution::setup_buckets(const int64_t* prange_lo, const int64_t* prange_hi
   // 2^sub_bits sub-lists per bucket (PSG_BUCKET_SUB): more distinct append counters. SF100 A/B:
   // one GPU 4.60 ms with 1 sub-list vs 4.79 with 16 (the emit walks 16 lists, the probe keeps 16x
   // more open bucket tails); N=2 4.15 vs 4.07 (the owner-side fold of the received rows, a burst
-  // of appends, 0.43 -> 0.20 ms). Default: 1 at one GPU, 16 at N > 1.
+  // of appends, 0.43 -> 0.20 ms); at N=2 4 sub-lists measured best (query 3.31 / 3.21 / 3.29 /
+  // 3.29 ms for 1 / 4 / 8 / 16). Default: 1 at one GPU, 4 at N > 1.
   static const int sub_env = [] {
     const char* e = std::getenv("PSG_BUCKET_SUB");
     return e ? std::max(1, std::atoi(e)) : 0;
   }();
-  const int sub_req = sub_env ? sub_env : (ctx_.nranks > 1 ? 16 : 1);
+  const int sub_req = sub_env ? sub_env : (ctx_.nranks > 1 ? 4 : 1);
   int sub_bits = 0;
   while ((2 << sub_bits) <= sub_req && sub_bits < 5) ++sub_bits;
   const uint64_t nsub = nb << sub_bits;

@@ -656,6 +656,9 @@ int min_blocks(const ScanProgram& P) {
     return e ? std::atoi(e) : 0;
   }();
   if (env > 0) return env;
+  // the key-bitmap build (date -> customer bitmap -> key -> bit): 8 CTAs/SM at 32 registers, no
+  // spills (SF100 N=1 query 4.44 -> 4.38 ms with every register program at 8)
+  if (P.sink == SINK_KEYBITS) return 8;
   // 6 x 256 threads: 40 registers. At 8 (32 registers) the probe/build programs spill 16-64 B
   // per thread, and the local-memory stores go through to L2 (8 GB per SF100 probe launch in the
   // ncu capture); A/B at N=1 SF100: probe kernel 4.47/4.52 -> 4.42/4.35 ms, query 7.90/7.95 ->

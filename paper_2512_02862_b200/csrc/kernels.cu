@@ -878,7 +878,12 @@ void launch_slab_consume(const AggTableDev& t, const SlabConsume& c, void* strea
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  k_slab_consume<<<sms * 4, 256, 0, S(stream)>>>(t, c);
+  // PSG_CONSUME_BPS: blocks per SM (measurement knob)
+  static const int bps = [] {
+    const char* e = std::getenv("PSG_CONSUME_BPS");
+    return e ? std::max(1, std::atoi(e)) : 4;
+  }();
+  k_slab_consume<<<sms * bps, 256, 0, S(stream)>>>(t, c);
 }
 
 /// Output column recipe of the emit kernels: kind 0 key, 1 rows, 2 probe sum idx, 3 build sum idx.
