@@ -2732,6 +2732,13 @@ ResultRows Execution::run(bool want_rows) {
       st_.ingest_bytes += v.bytes;
     }
     pt.mark("  probe + slab stores", ctx_.compute);
+    // the received rows' rank records are cold (the probe read only the owned rows' ones): warm L2
+    // while the barrier waits for the other ranks (PSG_CONSUME_PREFETCH=0: off)
+    static const bool prefetch_env = [] {
+      const char* e = std::getenv("PSG_CONSUME_PREFETCH");
+      return !(e && e[0] == '0');
+    }();
+    if (prefetch_env) launch_l2_prefetch(aggt_.krec, ((aggt_.krange + 63) / 64) * 16, ctx_.compute);
     gpu_barrier();  // every source's slab stores landed
     pt.mark("  barrier", ctx_.compute);
     SlabConsume c{};
@@ -2782,9 +2789,10 @@ ResultRows Execution::run(bool want_rows) {
       for (int b = 0; b < aggt_.nbs; ++b) p.global_float[1 + p.n_sum + b] = aggt_.bs_float[b];
     }
     if (bucket_mode_) apply_buckets(p);
-    // PSG_SLAB_FAKE=1 (measurement only - the result is WRONG): the peer-slab probe kernel on one
-    // GPU, pretending to be rank 0 of 2 (half the keys "remote", staged into a local scratch
-    // outbox), so the N > 1 probe kernel can be profiled with ncu in a single process.
+    // PSG_SLAB_FAKE=1: the peer-slab data path on one GPU, pretending to be rank 0 of 2 - half the
+    // keys "remote": packed into a local outbox by the probe kernel and folded back by the
+    // owner-side kernel - so the N > 1 kernels can be profiled with ncu and parity-tested in a
+    // single process.
     DevBuf fake_out, fake_cnt;
     static const bool fake = [] {
       const char* e = std::getenv("PSG_SLAB_FAKE");
@@ -2828,6 +2836,35 @@ ResultRows Execution::run(bool want_rows) {
       run_scan(p, v, staged_ != nullptr);
       pfeed->done();
       st_.ingest_bytes += v.bytes;
+    }
+    if (p.slab) {  // fake mode: fold the "remote" rows back in (the owner side, from the local outbox)
+      SlabConsume c{};
+      c.src_rows[1] = fake_out.as<uint64_t>();
+      c.src_cnt[1] = fake_cnt.as<unsigned long long>() + 1;
+      c.cap = p.slab_cap;
+      c.nsrc = 2;
+      c.npack = p.pack_n;
+      for (int k = 0; k < p.pack_n; ++k) {
+        c.pshift[k] = p.pack_shift[k];
+        c.pmask[k] = p.pack_mask[k];
+        c.pmin[k] = p.pack_min[k];
+      }
+      c.bkt = p.bkt;
+      c.fill = p.bkt_fill;
+      c.bcap = p.bkt_cap;
+      c.bsub_bits = p.bkt_sub_bits;
+      for (int k = 0; k < kMaxSums; ++k) {
+        c.bshift[k] = p.bkt_shift[k];
+        c.bmask[k] = p.bkt_mask[k];
+        c.bmin[k] = p.bkt_min[k];
+      }
+      c.ovf = p.bkt_ovf;
+      c.ovf_count = p.bkt_ovf_count;
+      c.ovf_cap = p.bkt_ovf_cap;
+      slab_recv_ = DevBuf(ctx_.pool, 8, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(slab_recv_.p, 0, 8, ctx_.compute));
+      c.received = slab_recv_.as<unsigned long long>();
+      launch_slab_consume(aggt_, c, ctx_.compute);
     }
   } else {
     uint64_t waves = pfeed->nbatches;

@@ -185,6 +185,14 @@ void emit_accumulate(std::ostringstream& s, const ScanProgram& P, const char* in
 
 
 void emit_rank_tail(std::ostringstream& s, const ScanProgram& P);
+/// PSG_BATCH_APPENDS=0: one bucket append (reserve, store) after the other per row.
+bool batched_appends() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_BATCH_APPENDS");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
 
 /// Rank-indexed table probe (SINK_PROBE): the key's 64-bit bitmap word and its block prefix (both
 /// L2-resident; one 16-byte {bits, rank} record when krec is set) give membership and the slot at
@@ -238,6 +246,26 @@ void emit_rank_probe(std::ostringstream& s, const ScanProgram& P, Late late) {
 /// Every row still in `pass` accumulates into its rank-table slot sl[r]: one word appended to the
 /// slot's bucket (bucketed aggregation), else atomics on the hot slot.
 void emit_rank_tail(std::ostringstream& s, const ScanProgram& P) {
+  if (P.bkt != nullptr && batched_appends()) {
+    // all R reservations first (independent atomics in flight together), then the stores: one
+    // atomic round trip per tile instead of R serialised ones (the consume profile showed the
+    // warps waiting on each append's return in turn)
+    s << "      { uint64_t ab[R]; unsigned apos[R];\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { ab[r] = 0; apos[r] = 0; if (!(pass & (1u << r))) continue;\n"
+      << "        ab[r] = ((sl[r] >> " << kBucketBits << ") << P.bkt_sub_bits) | (threadIdx.x & ((1u << P.bkt_sub_bits) - 1u));\n"
+      << "        apos[r] = atomicAdd(P.bkt_fill + ab[r], 1u); }\n"
+      << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n"
+      << "        uint64_t e = sl[r] & " << (kBucketSlots - 1) << "ULL;\n";
+    for (int k = 0; k < P.n_sum; ++k)
+      s << "        e |= ((" << V(P.sum_reg[k]) << "[r] - static_cast<uint64_t>(P.bkt_min[" << k << "])) & P.bkt_mask[" << k
+        << "]) << P.bkt_shift[" << k << "];\n";
+    s << "        if (apos[r] < P.bkt_cap) {\n"
+      << "          P.bkt[ab[r] * P.bkt_cap + apos[r]] = e;\n        } else {  // bucket full: the overflow list\n"
+      << "          const unsigned o = atomicAdd(P.bkt_ovf_count, 1u);\n"
+      << "          if (o < P.bkt_ovf_cap) { P.bkt_ovf[2 * o] = sl[r]; P.bkt_ovf[2 * o + 1] = e; }\n        }\n"
+      << "      } }\n";
+    return;
+  }
   s << "#pragma unroll\n      for (int r = 0; r < R; ++r) { if (!(pass & (1u << r))) continue;\n";
   if (P.bkt != nullptr) {  // append one word to the slot's bucket (k_bucket_emit folds it)
     s << "        const uint64_t b = ((sl[r] >> " << kBucketBits << ") << P.bkt_sub_bits) | (threadIdx.x & ((1u << P.bkt_sub_bits) - 1u));\n"

@@ -808,6 +808,24 @@ void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, un
   k_or_own<<<sms * 8, 256, 0, S(stream)>>>(p, nwords, kmin, self, global, own, cnt);
 }
 
+/// L2 warm-up of a table the next kernel reads at random (the owner-side fold's rank records: the
+/// probe kernel touched only the records of the rows this rank owned, so the received rows' records
+/// are cold and each fold lookup went to DRAM): bulk L2 prefetches of 64 KB per instruction, issued
+/// before the cross-rank barrier so they overlap the wait.
+__global__ void k_l2_prefetch(const unsigned char* p, uint64_t bytes) {
+  constexpr uint64_t kChunk = 64ull << 10;
+  for (uint64_t off = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) * kChunk; off < bytes;
+       off += static_cast<uint64_t>(gridDim.x) * blockDim.x * kChunk) {
+    const uint32_t n = static_cast<uint32_t>(min(kChunk, bytes - off)) & ~15u;
+    if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(n) : "memory");
+  }
+}
+void launch_l2_prefetch(const void* p, uint64_t bytes, void* stream) {
+  if (!p || bytes < 16) return;
+  count_launch();
+  k_l2_prefetch<<<64, 32, 0, S(stream)>>>(static_cast<const unsigned char*>(p), bytes);
+}
+
 /// Peer-slab shuffle, owner side: every packed row the other ranks stored into this rank's
 /// receive slab (region r = source r, *c.src_cnt[r] rows, read from the source's counters through
 /// NVLink after the cross-rank barrier) is unpacked, finds its slot in the rank-indexed table
@@ -844,29 +862,38 @@ __global__ void __launch_bounds__(256) k_slab_consume(AggTableDev t, SlabConsume
         d[u] = i0 + u * stride < n && !(w[u] >> 63) ? key - static_cast<uint64_t>(t.kmin) : ~0ULL;
         rec[u] = d[u] < t.krange ? __ldg(reinterpret_cast<const ulonglong2*>(t.krec) + (d[u] >> 6)) : make_ulonglong2(0, 0);
       }
+      // the U reservations in flight together, then the stores (one atomic round trip per round)
+      uint64_t slot[U], e[U], bk[U];
+      unsigned pos[U];
+      bool ok[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         // (padding of partly filled chunks: bit 63; the senders' global screen guarantees membership)
-        if (d[u] >= t.krange || !((rec[u].x >> (d[u] & 63)) & 1ULL)) continue;
-        const uint64_t slot = rec[u].y + static_cast<uint64_t>(__popcll(rec[u].x & ((1ULL << (d[u] & 63)) - 1ULL)));
-        uint64_t e = slot & static_cast<uint64_t>(kBucketSlots - 1);
+        ok[u] = d[u] < t.krange && ((rec[u].x >> (d[u] & 63)) & 1ULL);
+        slot[u] = ok[u] ? rec[u].y + static_cast<uint64_t>(__popcll(rec[u].x & ((1ULL << (d[u] & 63)) - 1ULL))) : 0;
+        e[u] = slot[u] & static_cast<uint64_t>(kBucketSlots - 1);
         for (int k = 0; k + 1 < c.npack; ++k) {
           const uint64_t v = static_cast<uint64_t>(c.pmin[1 + k]) + ((w[u] >> c.pshift[1 + k]) & c.pmask[1 + k]);
-          e |= ((v - static_cast<uint64_t>(c.bmin[k])) & c.bmask[k]) << c.bshift[k];
+          e[u] |= ((v - static_cast<uint64_t>(c.bmin[k])) & c.bmask[k]) << c.bshift[k];
         }
-        const uint64_t b = ((slot >> kBucketBits) << c.bsub_bits) | (threadIdx.x & ((1u << c.bsub_bits) - 1u));
+        bk[u] = ((slot[u] >> kBucketBits) << c.bsub_bits) | (threadIdx.x & ((1u << c.bsub_bits) - 1u));
+        pos[u] = 0;
+        if (ok[u] && !(c.diag & 4)) pos[u] = atomicAdd(c.fill + bk[u], 1u);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
         if (c.diag & 4) {  // measurement only (PSG_SLAB_DIAG=4): no bucket append
-          if (e == ~0ULL) c.bkt[b] = e;
+          if (e[u] == ~0ULL) c.bkt[bk[u]] = e[u];
           continue;
         }
-        const unsigned pos = atomicAdd(c.fill + b, 1u);
-        if (pos < c.bcap) {
-          c.bkt[b * c.bcap + pos] = e;
+        if (pos[u] < c.bcap) {
+          c.bkt[bk[u] * c.bcap + pos[u]] = e[u];
         } else {
           const unsigned o = atomicAdd(c.ovf_count, 1u);
           if (o < c.ovf_cap) {
-            c.ovf[2 * o] = slot;
-            c.ovf[2 * o + 1] = e;
+            c.ovf[2 * o] = slot[u];
+            c.ovf[2 * o + 1] = e[u];
           }
         }
       }

@@ -114,6 +114,8 @@ struct OrPeers {
 /// |= overlap, += summed rows (k_or_own, kernels.cu).
 void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, unsigned long long* global,
                    unsigned long long* own, unsigned long long* cnt, void* stream);
+/// Bulk L2 prefetch of [p, p + bytes) (16-byte aligned).
+void launch_l2_prefetch(const void* p, uint64_t bytes, void* stream);
 /// Peer-slab shuffle, owner side (kernels.cu k_slab_consume).
 struct SlabConsume {
   const uint64_t* src_rows[kMaxSlabPeers];             // rows source r holds for this rank (peer-mapped outbox, or the local inbox)

@@ -22,6 +22,7 @@ def main():
     bad = 0
     kinds = {}  # psg_stats.agg_table kind -> cases (4 = rank-indexed table)
     ovf = [0]  # rows that went through the bucket overflow list
+    fused = [0]  # cases whose shuffle ran through the peer-slab path (PSG_SLAB_FAKE at one GPU)
     with tempfile.TemporaryDirectory() as tmp:
         cache = {}
 
@@ -43,6 +44,7 @@ def main():
             s = po.summary([(res.schema, res.rows)])
             kinds[res.stats["agg_table"]] = kinds.get(res.stats["agg_table"], 0) + 1
             ovf[0] += res.stats["bucket_overflow"]
+            fused[0] += res.stats.get("shuffle_fused", 0)
             if r["plan"] == "global_agg" and r["nodes"] > 1:
                 ok = s["colsums"] == r["colsums"]
             else:
@@ -76,6 +78,7 @@ def main():
     ctx.close()
     print("AGG_TABLES", json.dumps({str(k): v for k, v in sorted(kinds.items())}))
     print("BUCKET_OVERFLOW", ovf[0])
+    print("SLAB_FUSED", fused[0])
     print("BAD", bad)
     sys.exit(1 if bad else 0)
 

@@ -112,3 +112,17 @@ def test_strided_tile_order_matches_golden():
                        text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "BAD 0" in r.stdout
+
+
+def test_peer_slab_path_on_one_gpu_matches_golden():
+    """PSG_SLAB_FAKE=1: the N>1 peer-slab data path on one GPU - the probe kernel treats half the
+    keys as another rank's (packed into the outbox in warp-claimed chunks, padding sentinels) and
+    the owner-side fold (k_slab_consume) adds them back - so the multi-GPU kernels are
+    parity-tested even on a single-GPU box; asserted to have run from psg_stats.shuffle_fused."""
+    env = dict(os.environ, PSG_SCREEN_MIN_MB="0", PSG_SLAB_FAKE="1")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "BAD 0" in r.stdout
+    n = int([x for x in r.stdout.splitlines() if x.startswith("SLAB_FUSED")][0].split()[1])
+    assert n > 0, r.stdout[-500:]
