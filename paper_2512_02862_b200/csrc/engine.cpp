@@ -2732,11 +2732,11 @@ ResultRows Execution::run(bool want_rows) {
       st_.ingest_bytes += v.bytes;
     }
     pt.mark("  probe + slab stores", ctx_.compute);
-    // the received rows' rank records are cold (the probe read only the owned rows' ones): warm L2
-    // while the barrier waits for the other ranks (PSG_CONSUME_PREFETCH=0: off)
+    // PSG_CONSUME_PREFETCH=1: warm L2 with the rank records the owner-side fold reads while the
+    // barrier waits for the other ranks (measured neutral at SF100 N=2: off)
     static const bool prefetch_env = [] {
       const char* e = std::getenv("PSG_CONSUME_PREFETCH");
-      return !(e && e[0] == '0');
+      return e && e[0] == '1';
     }();
     if (prefetch_env) launch_l2_prefetch(aggt_.krec, ((aggt_.krange + 63) / 64) * 16, ctx_.compute);
     gpu_barrier();  // every source's slab stores landed
