@@ -496,12 +496,32 @@ void emit_slab_probe4(std::ostringstream& s, const ScanProgram& P, Late late) {
     << "[r] - static_cast<uint64_t>(T.kmin)) & 63);\n"
     << "        sl[r] = kr[r] + static_cast<uint32_t>(__popcll(kw[r] & ((1ULL << d6) - 1ULL))); }\n";
   if (slab_diag() & 2) s << "      rem = 0;\n";
-  s << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
-    << "        const bool on = (rem >> r) & 1u;\n";
-  if (P.nparts == 2)
-    s << "        slab_put2(on, on ? " << out_value(P, 0) << " : 0ULL);\n      }\n";
-  else
-    s << "        if (__any_sync(0xffffffffu, on)) slab_put(on, dst[r], on ? " << out_value(P, 0) << " : 0ULL);\n      }\n";
+  if (P.nparts == 2) {
+    // two ranks: one destination, so the tile's remote rows are placed with ONE chunk check - a
+    // ballot per row slot, positions from the running count; rows past the current chunk's room
+    // go to a freshly claimed one (at most one per tile: a tile has R x 32 < kSlabChunk rows)
+    s << "      { unsigned bl[R], tot = 0; const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;\n"
+      << "#pragma unroll\n        for (int r = 0; r < R; ++r) { bl[r] = __ballot_sync(0xffffffffu, (rem >> r) & 1u); tot += __popc(bl[r]); }\n"
+      << "        if (tot) {\n"
+      << "          const unsigned room = c2base == ~0ULL ? 0u : " << kSlabChunk << "u - c2fill;\n"
+      << "          unsigned long long nb = c2base;\n"
+      << "          if (tot > room) {\n"
+      << "            if ((threadIdx.x & 31) == 0) nb = atomicAdd(P.slab_cnt + " << 1 - P.self_rank << ", " << kSlabChunk << "ULL);\n"
+      << "            nb = __shfl_sync(0xffffffffu, nb, 0);\n          }\n"
+      << "          unsigned at = 0;\n"
+      << "#pragma unroll\n          for (int r = 0; r < R; ++r) {\n"
+      << "            if ((rem >> r) & 1u) { const unsigned k = at + __popc(bl[r] & lt);\n"
+      << "              const unsigned long long pos = k < room ? c2base + c2fill + k : nb + (k - room);\n"
+      << "              if (pos < P.slab_cap" << ((slab_diag() & 1) ? " && pos == ~0ULL" : "") << ") P.slab_dst[" << 1 - P.self_rank
+      << "][pos] = " << out_value(P, 0) << "; }\n"
+      << "            at += __popc(bl[r]); }\n"
+      << "          if (tot > room) { c2base = nb; c2fill = tot - room; } else { c2fill += tot; }\n"
+      << "        }\n      }\n";
+  } else {
+    s << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
+      << "        const bool on = (rem >> r) & 1u;\n"
+      << "        if (__any_sync(0xffffffffu, on)) slab_put(on, dst[r], on ? " << out_value(P, 0) << " : 0ULL);\n      }\n";
+  }
   s << "      pass = own;\n";
   emit_rank_tail(s, P);
   s << "    }\n";
