@@ -297,6 +297,16 @@ void emit_rank_tail(std::ostringstream& s, const ScanProgram& P) {
 /// PSG_SLAB_DIAG (measurement only - results are wrong when set): 1 no outbox stores, 2 remote
 /// rows dropped, 8 remote rows screened through the own rank records (the one-GPU lookup
 /// footprint) instead of the global bitmap.
+/// PSG_TILE_PUT=1: the per-tile outbox placement also at more than two ranks (once per
+/// destination) - measured slower at N=4 (probe 1.13 -> 1.32 ms), so the per-row-slot
+/// match-based put stays the default there.
+bool tile_put_env() {
+  static const bool v = [] {
+    const char* e = std::getenv("PSG_TILE_PUT");
+    return e && e[0] == '1';
+  }();
+  return v;
+}
 int slab_diag() {
   static const int v = [] {
     const char* e = std::getenv("PSG_SLAB_DIAG");
@@ -476,7 +486,7 @@ bool slab_grec_env() {
 /// survive compute their owner, and the owned ones read their rank record (slot) together with
 /// the late columns - the extra lookup overlaps the HBM gathers.
 template <class Late>
-void emit_slab_probe4(std::ostringstream& s, const ScanProgram& P, Late late) {
+void emit_slab_probe4(std::ostringstream& s, const ScanProgram& P, Late late, const std::string& w) {
   s << "    { const AggTableDev& T = P.agg; uint32_t gw[R], bb[R], kr[R], sl[R], dst[R]; unsigned long long kw[R];\n"
     << "      uint32_t sel = 0, own = 0, rem = 0;\n"
     << "#pragma unroll\n      for (int r = 0; r < R; ++r) { const uint64_t key = " << V(P.key_reg) << "[r];\n"
@@ -517,6 +527,34 @@ void emit_slab_probe4(std::ostringstream& s, const ScanProgram& P, Late late) {
       << "            at += __popc(bl[r]); }\n"
       << "          if (tot > room) { c2base = nb; c2fill = tot - room; } else { c2fill += tot; }\n"
       << "        }\n      }\n";
+  } else if (tile_put_env()) {
+    // more ranks: the same per-tile placement once per destination (literal loop over the ranks,
+    // chunk state of the warp in shared memory)
+    s << "      { const uint32_t lt = (1u << (threadIdx.x & 31)) - 1u;\n";
+    for (int d = 0; d < P.nparts; ++d) {
+      if (d == P.self_rank) continue;
+      s << "      { unsigned bl[R], tot = 0;\n"
+        << "#pragma unroll\n        for (int r = 0; r < R; ++r) { bl[r] = __ballot_sync(0xffffffffu, ((rem >> r) & 1u) && dst[r] == " << d
+        << "u); tot += __popc(bl[r]); }\n"
+        << "        if (tot) {\n"
+        << "          unsigned cf = s_cfill[" << w << "][" << d << "]; unsigned long long cb = s_cbase[" << w << "][" << d << "];\n"
+        << "          const unsigned room = cb == ~0ULL ? 0u : " << kSlabChunk << "u - cf;\n"
+        << "          unsigned long long nb = cb;\n"
+        << "          if (tot > room) {\n"
+        << "            if ((threadIdx.x & 31) == 0) nb = atomicAdd(P.slab_cnt + " << d << ", " << kSlabChunk << "ULL);\n"
+        << "            nb = __shfl_sync(0xffffffffu, nb, 0);\n          }\n"
+        << "          unsigned at = 0;\n"
+        << "#pragma unroll\n          for (int r = 0; r < R; ++r) {\n"
+        << "            if ((bl[r] >> (threadIdx.x & 31)) & 1u) { const unsigned k = at + __popc(bl[r] & lt);\n"
+        << "              const unsigned long long pos = k < room ? cb + cf + k : nb + (k - room);\n"
+        << "              if (pos < P.slab_cap) P.slab_dst[" << d << "][pos] = " << out_value(P, 0) << "; }\n"
+        << "            at += __popc(bl[r]); }\n"
+        << "          __syncwarp();\n"
+        << "          if ((threadIdx.x & 31) == 0) { if (tot > room) { s_cbase[" << w << "][" << d << "] = nb; s_cfill[" << w << "][" << d
+        << "] = tot - room; } else { s_cfill[" << w << "][" << d << "] = cf + tot; } }\n"
+        << "          __syncwarp();\n        }\n      }\n";
+    }
+    s << "      }\n";
   } else {
     s << "#pragma unroll\n      for (int r = 0; r < R; ++r) {\n"
       << "        const bool on = (rem >> r) & 1u;\n"
@@ -543,7 +581,7 @@ void emit_slab_probe(std::ostringstream& s, const ScanProgram& P, Late late, con
   else if (slab_variant() == 3)
     emit_slab_probe3(s, P, late);
   else
-    emit_slab_probe4(s, P, late);
+    emit_slab_probe4(s, P, late, w);
 }
 
 /// SINK_KEYBITS: every surviving row sets its key's bit. With kb_flag a duplicate (bit already
