@@ -2009,16 +2009,24 @@ ResultRows Execution::run(bool want_rows) {
           zone_range(psrc_.scan->paths, psrc_.proj.file_idx[ref.idx], a, b);
         mx[3 + k] = ~a, mx[3 + np + k] = b;
       }
-      if (nr > 1) {
-        DevBuf red(ctx_.pool, (mx.size() + sm.size()) * 8, ctx_.compute);
-        long long* d = red.as<long long>();
-        PSG_CUDA(cudaMemcpyAsync(d, mx.data(), mx.size() * 8, cudaMemcpyHostToDevice, ctx_.compute));
-        PSG_CUDA(cudaMemcpyAsync(d + mx.size(), sm.data(), sm.size() * 8, cudaMemcpyHostToDevice, ctx_.compute));
-        PSG_NCCL(ncclAllReduce(d, d, mx.size(), ncclInt64, ncclMax, ctx_.nccl, ctx_.compute));
-        PSG_NCCL(ncclAllReduce(d + mx.size(), d + mx.size(), sm.size(), ncclInt64, ncclSum, ctx_.nccl, ctx_.compute));
-        PSG_CUDA(cudaMemcpyAsync(mx.data(), d, mx.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
-        PSG_CUDA(cudaMemcpyAsync(sm.data(), d + mx.size(), sm.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
+      if (nr > 1) {  // one all-gather of every rank's vector; MAX / SUM reduced on the host
+        const size_t nv = mx.size() + sm.size();
+        std::vector<long long> mine(mx);
+        mine.insert(mine.end(), sm.begin(), sm.end());
+        DevBuf in(ctx_.pool, nv * 8, ctx_.compute), all(ctx_.pool, nv * 8 * nr, ctx_.compute);
+        PSG_CUDA(cudaMemcpyAsync(in.p, mine.data(), nv * 8, cudaMemcpyHostToDevice, ctx_.compute));
+        PSG_NCCL(ncclAllGather(in.p, all.p, nv, ncclInt64, ctx_.nccl, ctx_.compute));
+        std::vector<long long> got(nv * nr);
+        PSG_CUDA(cudaMemcpyAsync(got.data(), all.p, got.size() * 8, cudaMemcpyDeviceToHost, ctx_.compute));
         PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+        for (size_t k = 0; k < mx.size(); ++k) {
+          mx[k] = got[k];
+          for (int r = 1; r < nr; ++r) mx[k] = std::max(mx[k], got[r * nv + k]);
+        }
+        for (size_t k = 0; k < sm.size(); ++k) {
+          sm[k] = 0;
+          for (int r = 0; r < nr; ++r) sm[k] += got[r * nv + mx.size() + k];
+        }
       }
       lo = ~mx[0], hi = mx[1];
       slab_max_rows = static_cast<uint64_t>(mx[2]);

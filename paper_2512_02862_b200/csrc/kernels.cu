@@ -973,15 +973,20 @@ __device__ __forceinline__ void add64_u32pair(uint32_t* lo, uint32_t* hi, uint64
 /// prefix and writes its rows. state[b] = (status << 62) | value: 1 = count, 2 = inclusive prefix.
 __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b, uint64_t nslots, uint64_t nwords,
                                                      unsigned long long* state, unsigned int* ticket,
-                                                     const uint32_t* first_word, int nc, EmitCols ec, uint64_t* out) {
+                                                     const uint32_t* first_word, int nc, EmitCols ec, uint64_t* out,
+                                                     uint64_t nbuckets) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int nps = t.nps;
   const BucketSmem m = bucket_smem(smem_raw, nps);
   __shared__ uint32_t s_warp[16];
   __shared__ uint64_t s_bucket, s_base;
+  // persistent CTAs (at most the resident count, so every claimed predecessor is running): each
+  // claims buckets from the ticket in order until none is left
+  for (;;) {
   if (threadIdx.x == 0) s_bucket = atomicAdd(ticket, 1u);
   for (int i = threadIdx.x; i < (1 + 2 * nps) * kBucketSlots; i += blockDim.x) m.hits[i] = 0;
   __syncthreads();
+  if (s_bucket >= nbuckets) return;
   const uint64_t bucket = s_bucket, s0 = bucket << kBucketBits;
   const uint64_t s_end = min(s0 + kBucketSlots, nslots);
   for (uint64_t sub = bucket << b.sub_bits; sub < (bucket + 1) << b.sub_bits; ++sub) {
@@ -1111,6 +1116,8 @@ __global__ void __launch_bounds__(512) k_bucket_emit(AggTableDev t, BucketDev b,
         for (int k = 0; k < nc; ++k) row[k] = col(k);
     }
   }
+  __syncthreads();  // smem and s_bucket are reused by the next bucket
+  }
 }
 
 void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuckets, uint64_t nslots,
@@ -1134,8 +1141,14 @@ void launch_bucket_emit(const AggTableDev& t, const BucketDev& b, uint64_t nbuck
   count_launch();
   cudaMemsetAsync(state, 0, nbuckets * sizeof(unsigned long long), S(stream));
   cudaMemsetAsync(ticket, 0, sizeof(unsigned int), S(stream));
-  k_bucket_emit<<<static_cast<unsigned>(nbuckets), 512, smem, S(stream)>>>(t, b, nslots, nwords, state, ticket, first_word,
-                                                                           nc, ec, out_rows);
+  int per_sm = 0, sms = 148, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_bucket_emit, 512, smem);
+  const int resident = sms * std::max(per_sm, 1);
+  const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(nbuckets, static_cast<uint64_t>(resident)));
+  k_bucket_emit<<<grid, 512, smem, S(stream)>>>(t, b, nslots, nwords, state, ticket, first_word, nc, ec, out_rows,
+                                                 nbuckets);
 }
 
 /// Destination histogram of n keys (partition_of, hashing.hpp:35-37): one shared atomic per
