@@ -2746,9 +2746,9 @@ ResultRows Execution::run(bool want_rows) {
     pt.mark("  probe + slab stores", ctx_.compute);
     // PSG_CONSUME_PREFETCH=1: warm L2 with the rank records the owner-side fold reads while the
     // barrier waits for the other ranks (measured neutral at SF100 N=2: off)
-    static const bool prefetch_env = [] {
+    static const bool prefetch_env = [] {  // 1: bulk L2 prefetch, 2: evict-last loads
       const char* e = std::getenv("PSG_CONSUME_PREFETCH");
-      return e && e[0] == '1';
+      return e && (e[0] == '1' || e[0] == '2');
     }();
     if (prefetch_env) launch_l2_prefetch(aggt_.krec, ((aggt_.krange + 63) / 64) * 16, ctx_.compute);
     gpu_barrier();  // every source's slab stores landed

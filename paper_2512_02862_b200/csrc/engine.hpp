@@ -86,7 +86,10 @@ class FooterCache {
 /// out of the page cache with memcpy (streaming stores) instead of pread: one kernel-side copy
 /// fewer per byte - on the bench box the page cache -> pinned -> HBM pipeline goes from 44 to
 /// 53 GB/s, the PCIe H2D rate (profiles/r2_ingest_probe2.txt). Mappings hold no data of their
-/// own; pages stay in the page cache. PSG_MMAP=0: pread.
+/// own; pages stay in the page cache. A file truncated WHILE a query copies from its mapping
+/// would fault (SIGBUS) where pread reports a short read: the stamp check at each query's start
+/// re-maps changed files, and the footer bounds every extent by the file size it was read with.
+/// PSG_MMAP=0: pread.
 struct FileMapping {
   const uint8_t* base = nullptr;
   size_t bytes = 0;

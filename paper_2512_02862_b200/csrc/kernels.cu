@@ -820,10 +820,32 @@ __global__ void k_l2_prefetch(const unsigned char* p, uint64_t bytes) {
     if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(n) : "memory");
   }
 }
+/// The same warm-up by loads that mark the lines evict-last (one 16-byte load per 128-byte line).
+__global__ void k_l2_touch(const unsigned long long* p, uint64_t lines, unsigned long long* sink) {
+  const uint64_t pol = l2_evict_last();
+  unsigned long long acc = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < lines;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t a, b;
+    ldg_keep_v2u64(p + 16 * i, pol, a, b);
+    acc ^= a ^ b;
+  }
+  if (acc == 0x9E3779B97F4A7C15ULL) *sink = acc;  // (keeps the loads)
+}
 void launch_l2_prefetch(const void* p, uint64_t bytes, void* stream) {
   if (!p || bytes < 16) return;
   count_launch();
-  k_l2_prefetch<<<64, 32, 0, S(stream)>>>(static_cast<const unsigned char*>(p), bytes);
+  static const int mode = [] {
+    const char* e = std::getenv("PSG_CONSUME_PREFETCH");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (mode == 2) {
+    static unsigned long long* sink = nullptr;
+    if (!sink) cudaMalloc(&sink, 8);
+    k_l2_touch<<<sm_count() * 8, 256, 0, S(stream)>>>(static_cast<const unsigned long long*>(p), bytes / 128, sink);
+  } else {
+    k_l2_prefetch<<<64, 32, 0, S(stream)>>>(static_cast<const unsigned char*>(p), bytes);
+  }
 }
 
 /// Peer-slab shuffle, owner side: every packed row the other ranks stored into this rank's
