@@ -64,10 +64,11 @@ for v in a.variants.split(","):
     dev = red(statistics.median(ms))
     recv = red(rb)
     total_rows = red(rows, "sum")
+    wall_s = red(statistics.median(wall))  # (every rank: a collective)
     in_bytes = (a.build_rows + a.probe_rows) * (1 + a.payload) * 8
     if rank == 0:
         print(json.dumps({"variant": v, "n_gpus": world, "streams": k, "chunk_rows": a.chunk_rows,
-                          "device_ms": round(dev, 3), "wall_s": round(red(statistics.median(wall)), 4),
+                          "device_ms": round(dev, 3), "wall_s": round(wall_s, 4),
                           "result_rows": int(total_rows), "host_syncs": syncs, "recv_bytes_per_gpu": int(recv),
                           "shuffle_gbs": round(recv / 1e9 / (dev / 1e3), 1) if recv else None,
                           "input_gbs": round(in_bytes / 1e9 / (dev / 1e3), 1),
