@@ -2723,13 +2723,14 @@ ResultRows Execution::run(bool want_rows) {
     p.slab_cap = slab_cap_;
     unsigned long long* my_cnt = reinterpret_cast<unsigned long long*>(ctx_.symm + slab_cnt_off_);
     p.slab_cnt = my_cnt;
-    // pull (default): remote rows go to this rank's OWN outbox region for their destination (local
-    // HBM stores) and the owner reads them over NVLink after the barrier - the probe kernel's peer
-    // stores measured 0.3 ms of the 2.6 ms N=2 kernel. PSG_SLAB_PUSH=1: stores into the owner's
-    // inbox through NVLink from inside the probe kernel.
+    // push (default): the probe kernel stores remote rows into the owner's inbox through NVLink,
+    // so the transfer overlaps the scan and the owner-side fold reads local HBM; PSG_SLAB_PUSH=0
+    // (pull): remote rows go to this rank's own outbox and the owner reads them over NVLink after
+    // the barrier. SF100 A/B: N=2 3.02 / 3.02 ms (the fold is bound by its appends there), N=4
+    // 2.05 / 2.11 ms (fold 0.14 / 0.18 ms: pulling from three peers is read-bound).
     static const bool push = [] {
       const char* e = std::getenv("PSG_SLAB_PUSH");
-      return e && e[0] == '1';
+      return !(e && e[0] == '0');
     }();
     for (int d = 0; d < nr; ++d)
       p.slab_dst[d] = d == ctx_.rank ? nullptr
