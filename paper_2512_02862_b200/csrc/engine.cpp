@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <functional>
+#include <initializer_list>
 #include <numeric>
 #include <cstdio>
 #include <climits>
@@ -580,6 +581,27 @@ class Execution {
   void check_lt_flags() {  // after the sync that completed enqueue_lt_flags' copies
     for (size_t i = 0; i < lt_flags_.size(); ++i)
       if (lt_flag_host_[2 * i + 1] != 0) throw KeybitsRetry();
+    lt_flags_.clear();
+  }
+  /// One gathered host read of device scalars (u32 where the flag says so) plus the pending
+  /// local-table duplicate flags: one small kernel writing mapped pinned memory and one stream
+  /// sync, then the flag check.
+  void read_words(std::initializer_list<std::pair<const void*, bool>> srcs, uint64_t* out) {
+    GatherWords g{};
+    for (const auto& [ptr, is32] : srcs) {
+      if (is32) g.w32 |= 1u << g.n;
+      g.src[g.n++] = ptr;
+    }
+    const int nw = g.n;
+    if (nw + static_cast<int>(lt_flags_.size()) > 24) throw Error(PSG_ERR_INTERNAL, "read_words: too many words");
+    for (auto& f : lt_flags_) g.src[g.n++] = f.as<unsigned long long>() + 1;
+    unsigned long long* hw = ctx_.ensure_host_words();
+    launch_gather_words(g, hw, ctx_.compute);
+    PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+    const volatile unsigned long long* v = hw;
+    for (int i = 0; i < nw; ++i) out[i] = v[i];
+    for (int i = nw; i < g.n; ++i)
+      if (v[i] != 0) throw KeybitsRetry();
     lt_flags_.clear();
   }
   // event pairs around the timed (dominant) kernel launches, resolved after the query's last sync
@@ -1568,19 +1590,19 @@ void Execution::finalize_buckets(ResultRows& out, bool want_rows) {
   DevBuf rows(ctx_.pool, std::max<uint64_t>(agg_cap_, 1) * nc * 8, ctx_.compute);
   launch_bucket_emit(aggt_, bd_, nbuckets_, agg_cap_, state.as<unsigned long long>(), ticket.as<unsigned int>(),
                      first_word.as<uint32_t>(), nc, kind.data(), idx.data(), rows.as<uint64_t>(), ctx_.compute);
-  unsigned long long last = 0, recv = 0;
-  unsigned int novf = 0;
-  PSG_CUDA(cudaMemcpyAsync(&last, state.as<unsigned long long>() + (nbuckets_ - 1), 8, cudaMemcpyDeviceToHost,
-                           ctx_.compute));
+  DevBuf o;
+  const void* ovf = bd_.ovf_count;
   if (ctx_.nranks > 1) {  // the re-run decision is collective: the largest overflow of any rank
-    DevBuf o(ctx_.pool, 4, ctx_.compute);
+    o = DevBuf(ctx_.pool, 4, ctx_.compute);
     PSG_NCCL(ncclAllReduce(bd_.ovf_count, o.p, 1, ncclUint32, ncclMax, ctx_.nccl, ctx_.compute));
-    PSG_CUDA(cudaMemcpyAsync(&novf, o.p, 4, cudaMemcpyDeviceToHost, ctx_.compute));
-  } else {
-    PSG_CUDA(cudaMemcpyAsync(&novf, bd_.ovf_count, 4, cudaMemcpyDeviceToHost, ctx_.compute));
+    ovf = o.p;
   }
-  if (slab_recv_.p) PSG_CUDA(cudaMemcpyAsync(&recv, slab_recv_.p, 8, cudaMemcpyDeviceToHost, ctx_.compute));
-  PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
+  uint64_t w[3] = {0, 0, 0};
+  const void* last_p = state.as<unsigned long long>() + (nbuckets_ - 1);
+  if (slab_recv_.p) read_words({{last_p, false}, {ovf, true}, {slab_recv_.p, false}}, w);
+  else read_words({{last_p, false}, {ovf, true}}, w);
+  const unsigned long long last = w[0], recv = w[2];
+  const uint64_t novf = w[1];
   st_.bucket_overflow = novf;
   if (slab_recv_.p) {
     st_.bytes_received += recv * 8;
@@ -2292,8 +2314,19 @@ ResultRows Execution::run(bool want_rows) {
     uint64_t krange = 0;
     const bool rank_ok = grouped_ && rank_env && jit_available() && !p2p;
     auto rank_records = [&](uint64_t kwords64) {  // popcount prefix per 64-bit word + interleaved {bits, rank} records
-      DevBuf cnt(ctx_.pool, kwords64 * 4, ctx_.compute);
       agg_krank_ = DevBuf(ctx_.pool, kwords64 * 4, ctx_.compute);
+      static const bool fused = [] {  // PSG_RANK_FUSED=0: popc64 + CUB scan + krec build (measurement knob)
+        const char* e = std::getenv("PSG_RANK_FUSED");
+        return !(e && std::string(e) == "0");
+      }();
+      if (fused && rank_tiles(kwords64) <= 16384) {  // (each tile sums the earlier tiles' counts)
+        DevBuf ts(ctx_.pool, rank_tiles(kwords64) * 4, ctx_.compute);
+        agg_krec_ = DevBuf(ctx_.pool, kwords64 * 16, ctx_.compute);
+        launch_rank_records(agg_kbits_.as<unsigned long long>(), kwords64, ts.as<uint32_t>(), agg_krank_.as<uint32_t>(),
+                            agg_krec_.as<unsigned long long>(), ctx_.compute);
+        return;
+      }
+      DevBuf cnt(ctx_.pool, kwords64 * 4, ctx_.compute);
       launch_popc64(agg_kbits_.as<unsigned long long>(), kwords64, cnt.as<uint32_t>(), ctx_.compute);
       const size_t tb = exclusive_scan_u32(nullptr, nullptr, kwords64, nullptr, 0, ctx_.compute);
       DevBuf tmp(ctx_.pool, tb, ctx_.compute);
@@ -2310,6 +2343,7 @@ ResultRows Execution::run(bool want_rows) {
       PSG_CUDA(cudaMemsetAsync(cnts.p, 0, 32, ctx_.compute));
       if (nr > 1 && kb_heap) {
         gpu_barrier();  // every rank's local bitmap and flag are complete
+        pt.mark("  barrier (rank bitmaps)", ctx_.compute);
         semi_all = DevBuf(ctx_.pool, (words64 + 1) * 8, ctx_.compute);
         agg_kbits_ = DevBuf(ctx_.pool, words64 * 8, ctx_.compute);
         OrPeers op{};
@@ -2320,6 +2354,7 @@ ResultRows Execution::run(bool want_rows) {
         }
         launch_or_own(op, words64, kb_lo, ctx_.rank, semi_all.as<unsigned long long>(), agg_kbits_.as<unsigned long long>(),
                       cnts.as<unsigned long long>(), ctx_.compute);
+        pt.mark("  NVLink OR of the rank bitmaps", ctx_.compute);
         // (a peer may still read this rank's local bitmap: it is rewritten only by the next query's
         // build scan, which follows this query's collectives)
       } else if (nr > 1) {
@@ -2335,17 +2370,15 @@ ResultRows Execution::run(bool want_rows) {
       // the rank records of the (own) bitmap are queued before the host read: at one GPU its
       // popcount (last prefix + last word) is the duplicate check
       rank_records((kb_range + 63) / 64);
-      uint64_t h[6] = {0, 0, 0, 0, 0, 0};
-      uint32_t last_rank = 0;
-      PSG_CUDA(cudaMemcpyAsync(h, kb_cnt.p ? kb_cnt.p : ctx_.symm + kb_cnt_off, 16, cudaMemcpyDeviceToHost, ctx_.compute));
-      PSG_CUDA(cudaMemcpyAsync(h + 2, cnts.p, 32, cudaMemcpyDeviceToHost, ctx_.compute));
       const uint64_t wl = (kb_range + 63) / 64 - 1;
-      PSG_CUDA(cudaMemcpyAsync(&last_rank, agg_krank_.as<uint32_t>() + wl, 4, cudaMemcpyDeviceToHost, ctx_.compute));
-      uint64_t last_word = 0;
-      PSG_CUDA(cudaMemcpyAsync(&last_word, agg_kbits_.as<unsigned long long>() + wl, 8, cudaMemcpyDeviceToHost, ctx_.compute));
-      enqueue_lt_flags();
-      PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
-      check_lt_flags();
+      const auto* kc = kb_cnt.p ? kb_cnt.as<unsigned long long>() : reinterpret_cast<const unsigned long long*>(ctx_.symm + kb_cnt_off);
+      const auto* cw = cnts.as<unsigned long long>();
+      uint64_t h[8];
+      read_words({{kc, false}, {kc + 1, false}, {cw, false}, {cw + 1, false}, {cw + 2, false}, {cw + 3, false},
+                  {agg_krank_.as<uint32_t>() + wl, true}, {agg_kbits_.as<unsigned long long>() + wl, false}},
+                 h);
+      const uint32_t last_rank = static_cast<uint32_t>(h[6]);
+      const uint64_t last_word = h[7];
       pt.mark("  key bitmap (global, own bits)", ctx_.compute);
       const uint64_t rows_set = h[0];
       if (kb_heap) {

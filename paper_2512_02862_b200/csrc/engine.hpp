@@ -258,6 +258,9 @@ struct Ctx {
     return symm + off;
   }
   void ensure_pinned(int nslots, uint64_t slot_bytes);
+  // mapped pinned words for gathered scalar host reads (launch_gather_words)
+  unsigned long long* host_words = nullptr;
+  unsigned long long* ensure_host_words();
   Timeline* timeline = nullptr;  // set for the duration of a query when PSG_TIMELINE is on
   bool no_buckets = false;       // set while a query re-runs after a bucket-overflow-list overflow
   bool no_keybits = false;       // set while a query re-runs after a key-bitmap build did not apply

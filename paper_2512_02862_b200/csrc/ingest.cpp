@@ -297,8 +297,18 @@ void Ctx::free_symmetric_heap() {
   symm_bytes = symm_top = 0;
 }
 
+unsigned long long* Ctx::ensure_host_words() {
+  if (!host_words) {
+    void* p = nullptr;
+    PSG_CUDA(cudaHostAlloc(&p, 4096, cudaHostAllocMapped));
+    host_words = static_cast<unsigned long long*>(p);
+  }
+  return host_words;
+}
+
 Ctx::~Ctx() {
   cudaSetDevice(device);
+  if (host_words) cudaFreeHost(host_words);
   for (int p = 0; p < static_cast<int>(symm_peer.size()); ++p)
     if (p != rank && symm_peer[p]) cudaIpcCloseMemHandle(symm_peer[p]);
   if (symm) cudaFree(symm);

@@ -696,6 +696,84 @@ __global__ void k_krec_build(const unsigned long long* __restrict__ bits, const 
     reinterpret_cast<ulonglong2*>(krec)[w] = v;
   }
 }
+constexpr int kRankThreads = 256, kRankIters = 8;
+constexpr uint64_t kRankTile = kRankThreads * kRankIters;  // words per CTA
+uint64_t rank_tiles(uint64_t n) { return (n + kRankTile - 1) / kRankTile; }
+__global__ void __launch_bounds__(kRankThreads) k_rank_tiles(const unsigned long long* __restrict__ bits, uint64_t n,
+                                                             uint32_t* __restrict__ tile_sums) {
+  const uint64_t base = blockIdx.x * kRankTile;
+  uint32_t c = 0;
+#pragma unroll
+  for (int it = 0; it < kRankIters; ++it) {
+    const uint64_t w = base + it * kRankThreads + threadIdx.x;
+    if (w < n) c += __popcll(bits[w]);
+  }
+  c = __reduce_add_sync(0xffffffffu, c);
+  __shared__ uint32_t ws[kRankThreads / 32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    uint32_t v = threadIdx.x < kRankThreads / 32 ? ws[threadIdx.x] : 0;
+    v = __reduce_add_sync(0xffffffffu, v);
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = v;
+  }
+}
+__global__ void __launch_bounds__(kRankThreads) k_rank_build(const unsigned long long* __restrict__ bits, uint64_t n,
+                                                             const uint32_t* __restrict__ tile_sums,
+                                                             uint32_t* __restrict__ krank,
+                                                             unsigned long long* __restrict__ krec) {
+  __shared__ uint32_t ws[kRankThreads / 32];
+  __shared__ uint32_t s_run;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  // this tile's offset: the sum of the earlier tiles' counts (<= a few thousand words, from L2)
+  uint32_t pre = 0;
+  for (uint32_t t = threadIdx.x; t < blockIdx.x; t += kRankThreads) pre += tile_sums[t];
+  pre = __reduce_add_sync(0xffffffffu, pre);
+  if (lane == 0) ws[wid] = pre;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint32_t v = 0;
+    for (int k = 0; k < kRankThreads / 32; ++k) v += ws[k];
+    s_run = v;
+  }
+  __syncthreads();
+  const uint64_t base = blockIdx.x * kRankTile;
+  for (int it = 0; it < kRankIters; ++it) {
+    const uint64_t w = base + it * kRankThreads + threadIdx.x;
+    const unsigned long long b = w < n ? bits[w] : 0ULL;
+    const uint32_t c = __popcll(b);
+    uint32_t inc = c;  // inclusive warp scan
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    if (lane == 31) ws[wid] = inc;
+    __syncthreads();
+    uint32_t wpre = 0;
+    for (int k = 0; k < wid; ++k) wpre += ws[k];
+    const uint32_t r = s_run + wpre + inc - c;
+    if (w < n) {
+      krank[w] = r;
+      ulonglong2 v;
+      v.x = b;
+      v.y = r;
+      reinterpret_cast<ulonglong2*>(krec)[w] = v;
+    }
+    __syncthreads();  // every warp has read ws and s_run
+    if (threadIdx.x == kRankThreads - 1) s_run = r + c;
+    __syncthreads();
+  }
+}
+void launch_rank_records(const unsigned long long* bits, uint64_t n, uint32_t* tile_sums, uint32_t* krank,
+                         unsigned long long* krec, void* stream) {
+  if (n == 0) return;
+  const uint64_t tiles = rank_tiles(n);
+  count_launch();
+  k_rank_tiles<<<static_cast<unsigned>(tiles), kRankThreads, 0, S(stream)>>>(bits, n, tile_sums);
+  count_launch();
+  k_rank_build<<<static_cast<unsigned>(tiles), kRankThreads, 0, S(stream)>>>(bits, n, tile_sums, krank, krec);
+}
 void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, uint64_t n, unsigned long long* krec,
                        void* stream) {
   if (n == 0) return;
@@ -806,6 +884,19 @@ void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, un
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   k_or_own<<<sms * 8, 256, 0, S(stream)>>>(p, nwords, kmin, self, global, own, cnt);
+}
+
+__global__ void k_gather_words(GatherWords g, unsigned long long* host) {
+  const int i = threadIdx.x;
+  if (i < g.n)
+    host[i] = (g.w32 >> i) & 1 ? static_cast<unsigned long long>(*static_cast<const uint32_t*>(g.src[i]))
+                               : *static_cast<const unsigned long long*>(g.src[i]);
+  __threadfence_system();
+}
+void launch_gather_words(const GatherWords& g, unsigned long long* host_mapped, void* stream) {
+  if (g.n <= 0) return;
+  count_launch();
+  k_gather_words<<<1, 32, 0, S(stream)>>>(g, host_mapped);
 }
 
 /// L2 warm-up of a table the next kernel reads at random (the owner-side fold's rank records: the

@@ -114,6 +114,15 @@ struct OrPeers {
 /// |= overlap, += summed rows (k_or_own, kernels.cu).
 void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, unsigned long long* global,
                    unsigned long long* own, unsigned long long* cnt, void* stream);
+/// Small host reads gathered into one launch: word i = *src[i] (a u32 when bit i of w32 is set)
+/// stored into mapped pinned host memory, so a batch of scalars costs one kernel and one stream
+/// sync instead of one pageable D2H copy (each a host round trip with the GPU idle) per value.
+struct GatherWords {
+  const void* src[24];
+  uint32_t w32;
+  int32_t n;
+};
+void launch_gather_words(const GatherWords& g, unsigned long long* host_mapped, void* stream);
 /// Bulk L2 prefetch of [p, p + bytes) (16-byte aligned).
 void launch_l2_prefetch(const void* p, uint64_t bytes, void* stream);
 /// Peer-slab shuffle, owner side (kernels.cu k_slab_consume).
@@ -141,6 +150,12 @@ struct SlabConsume {
   int32_t diag;                                        // PSG_SLAB_DIAG (measurement only)
 };
 void launch_slab_consume(const AggTableDev& t, const SlabConsume& c, void* stream);
+/// Rank records of a key bitmap in two launches (replaces popc64 + scan + krec_build): per-tile
+/// popcounts into tile_sums (rank_tiles(n) words), then krank[w] = the popcount of words < w and
+/// krec[w] = {bits[w], krank[w]} (the bitmap tile is re-read from L2).
+uint64_t rank_tiles(uint64_t n);
+void launch_rank_records(const unsigned long long* bits, uint64_t n, uint32_t* tile_sums, uint32_t* krank,
+                         unsigned long long* krec, void* stream);
 void launch_krec_build(const unsigned long long* bits, const uint32_t* krank, uint64_t n, unsigned long long* krec,
                        void* stream);
 void launch_part_hist(const uint64_t* keys, uint64_t n, int nparts, unsigned long long* counts, void* stream);
