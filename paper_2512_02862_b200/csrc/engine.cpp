@@ -593,14 +593,20 @@ class Execution {
       g.src[g.n++] = ptr;
     }
     const int nw = g.n;
-    if (nw + static_cast<int>(lt_flags_.size()) > 24) throw Error(PSG_ERR_INTERNAL, "read_words: too many words");
+    if (nw + static_cast<int>(lt_flags_.size()) + 1 > 24) throw Error(PSG_ERR_INTERNAL, "read_words: too many words");
+    if (barrier_err_.p) {  // a peer barrier that timed out (a rank never arrived)
+      g.w32 |= 1u << g.n;
+      g.src[g.n++] = barrier_err_.p;
+    }
+    const int nb = g.n;
     for (auto& f : lt_flags_) g.src[g.n++] = f.as<unsigned long long>() + 1;
     unsigned long long* hw = ctx_.ensure_host_words();
     launch_gather_words(g, hw, ctx_.compute);
     PSG_CUDA(cudaStreamSynchronize(ctx_.compute));
     const volatile unsigned long long* v = hw;
     for (int i = 0; i < nw; ++i) out[i] = v[i];
-    for (int i = nw; i < g.n; ++i)
+    if (nb > nw && v[nw] != 0) throw Error(PSG_ERR_NCCL, "peer barrier timed out (a rank did not arrive)");
+    for (int i = nb; i < g.n; ++i)
       if (v[i] != 0) throw KeybitsRetry();
     lt_flags_.clear();
   }
@@ -665,7 +671,7 @@ class Execution {
   };
   std::vector<std::unique_ptr<LocalTable>> bl_tables_, pl_tables_;
   // agg table
-  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, agg_krank_, agg_krec_, global_acc_, barrier_word_;
+  DevBuf agg_hot_, agg_cold_, agg_bloom_, agg_dups_, agg_kbits_, agg_krank_, agg_krec_, global_acc_, barrier_word_, barrier_err_;
   DevBuf bkt_, bkt_fill_, bkt_ovf_, bkt_ovf_count_;  // bucketed aggregation (rank table, one GPU)
   bool bucket_mode_ = false;
   BucketDev bd_{};
@@ -1720,6 +1726,7 @@ bool Execution::build_symmetric_agg_table(uint64_t max_rows, bool bloom) {
 }
 
 bool Execution::ensure_symmetric(size_t bytes) {
+  bytes += Ctx::kSymmReserve;
   if (ctx_.symm_bytes >= bytes) return true;
   if (ctx_.symm_failed) return false;
   // collective: grow every rank's heap together (1 GiB granules), re-mapping the peers' heaps
@@ -1732,6 +1739,23 @@ bool Execution::ensure_symmetric(size_t bytes) {
 /// Device-side barrier across ranks: a one-word all-reduce on the compute stream completes only
 /// after every rank's preceding kernels (including their peer-memory writes) have finished.
 void Execution::gpu_barrier() {
+  // with the symmetric heap mapped (every rank alike): flag stores through NVLink, no NCCL launch.
+  // PSG_PEER_BARRIER=0: the one-word all-reduce.
+  static const bool peer_env = [] {
+    const char* e = std::getenv("PSG_PEER_BARRIER");
+    return !(e && e[0] == '0');
+  }();
+  if (peer_env && ctx_.symm_bytes > 0 && ctx_.nranks <= kMaxSlabPeers) {
+    if (!barrier_err_.p) {
+      barrier_err_ = DevBuf(ctx_.pool, 4, ctx_.compute);
+      PSG_CUDA(cudaMemsetAsync(barrier_err_.p, 0, 4, ctx_.compute));
+    }
+    PeerFlags f{};
+    for (int r = 0; r < ctx_.nranks; ++r) f.flag[r] = ctx_.barrier_flags(r);
+    launch_peer_barrier(f, ctx_.barrier_flags(ctx_.rank), ctx_.rank, ctx_.nranks, ++ctx_.barrier_epoch,
+                        barrier_err_.as<unsigned int>(), ctx_.compute);
+    return;
+  }
   if (!barrier_word_.p) {
     barrier_word_ = DevBuf(ctx_.pool, 8, ctx_.compute);
     PSG_CUDA(cudaMemsetAsync(barrier_word_.p, 0, 8, ctx_.compute));

@@ -251,9 +251,15 @@ struct Ctx {
   void init_symmetric_heap(size_t bytes);  // collective over the NCCL communicator
   void free_symmetric_heap();              // collective (before a re-init)
   void free_symmetric_heap_local();
+  // the heap's last kSymmReserve bytes: the peer-barrier flags (one u32 per source rank)
+  static constexpr size_t kSymmReserve = 256;
+  uint32_t barrier_epoch = 0;  // last peer-barrier epoch (reset with the heap)
+  uint32_t* barrier_flags(int peer) const {
+    return reinterpret_cast<uint32_t*>(symm_peer[peer] + symm_bytes - kSymmReserve);
+  }
   uint8_t* symm_alloc(size_t bytes) {       // nullptr when the heap is exhausted
     const size_t off = (symm_top + 255) & ~size_t(255);
-    if (!symm || off + bytes > symm_bytes) return nullptr;
+    if (!symm || off + bytes + kSymmReserve > symm_bytes) return nullptr;
     symm_top = off + bytes;
     return symm + off;
   }

@@ -218,6 +218,10 @@ void Ctx::init_symmetric_heap(size_t bytes) {
   std::vector<cudaIpcMemHandle_t> all(nranks);
   bool ok = cudaMalloc(&symm, bytes) == cudaSuccess;
   if (ok) ok = cudaIpcGetMemHandle(&mine, symm) == cudaSuccess;
+  // zeroed barrier flags: ordered before the handle all-gather below, so before any peer's first
+  // barrier store into them
+  if (ok) ok = cudaMemsetAsync(symm + bytes - kSymmReserve, 0, kSymmReserve, compute) == cudaSuccess;
+  barrier_epoch = 0;
   if (!ok) {
     cudaGetLastError();
     std::memset(&mine, 0, sizeof mine);

@@ -886,6 +886,29 @@ void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, un
   k_or_own<<<sms * 8, 256, 0, S(stream)>>>(p, nwords, kmin, self, global, own, cnt);
 }
 
+__global__ void k_peer_barrier(PeerFlags f, const uint32_t* own, int self, int n, uint32_t epoch, unsigned int* err) {
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(f.flag[i] + self), "r"(epoch) : "memory");
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(own + i) : "memory");
+    if (static_cast<int32_t>(v - epoch) >= 0) break;
+    if (clock64() - t0 > (20LL << 30)) {  // ~10 s at 2 GHz: a rank never arrived
+      atomicExch(err, 1u);
+      break;
+    }
+    __nanosleep(32);
+  }
+}
+void launch_peer_barrier(const PeerFlags& f, const uint32_t* own, int self, int n, uint32_t epoch, unsigned int* err,
+                         void* stream) {
+  count_launch();
+  k_peer_barrier<<<1, 32, 0, S(stream)>>>(f, own, self, n, epoch, err);
+}
+
 __global__ void k_gather_words(GatherWords g, unsigned long long* host) {
   const int i = threadIdx.x;
   if (i < g.n)

@@ -114,6 +114,15 @@ struct OrPeers {
 /// |= overlap, += summed rows (k_or_own, kernels.cu).
 void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, unsigned long long* global,
                    unsigned long long* own, unsigned long long* cnt, void* stream);
+/// Device-side barrier over the symmetric heap (N > 1): flag[p] is peer p's flag array (one word
+/// per source rank), own this rank's. Each rank stores the epoch into every peer's slot for it
+/// (release, system scope), then waits until every slot of its own array holds the epoch
+/// (acquire); a rank missing for ~10 s sets *err instead of hanging the GPU.
+struct PeerFlags {
+  uint32_t* flag[kMaxSlabPeers];
+};
+void launch_peer_barrier(const PeerFlags& f, const uint32_t* own, int self, int n, uint32_t epoch, unsigned int* err,
+                         void* stream);
 /// Small host reads gathered into one launch: word i = *src[i] (a u32 when bit i of w32 is set)
 /// stored into mapped pinned host memory, so a batch of scalars costs one kernel and one stream
 /// sync instead of one pageable D2H copy (each a host round trip with the GPU idle) per value.
