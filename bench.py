@@ -93,17 +93,22 @@ def golden(scale):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line). One sampler per
+    job (local rank 0, every GPU of the job, `index` = "0,1,..."): a sampler per rank measurably
+    slowed the N=4 query (1.94 -> 2.00 ms median, scripts/bench_clocks_ab.sh). index None: off."""
 
     def __init__(self, index):
         self.index, self.samples, self.proc = index, [], None
 
     def __enter__(self):
+        if self.index is None:
+            return self
+        period = os.environ.get("PSG_CLOCKS_MS", "100")
         q = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", period],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
@@ -327,7 +332,7 @@ def main():
         staged.run(want_rows=False)
     sync_all()
     dev_ms, sts = [], []
-    clk = Clocks(local)
+    clk = Clocks(",".join(str(i) for i in range(world)) if local == 0 else None)
     if os.environ.get("PSG_BENCH_NO_CLOCKS") != "1":  # A/B knob: the sampler's effect on the value loop
         clk.__enter__()
     wall0 = time.time()
