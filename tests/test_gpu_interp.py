@@ -39,6 +39,17 @@ def test_rank_table_on_small_cases_matches_golden():
     assert _tables(r.stdout).get(4, 0) > 0, r.stdout[-500:]
 
 
+def test_rank_records_three_launch_path_matches_golden():
+    """PSG_RANK_FUSED=0: the rank records built by popcount + CUB scan + record build instead of
+    the two-launch tile kernels (k_rank_tiles, k_rank_build) - the same results on the small cases."""
+    env = dict(os.environ, PSG_SCREEN_MIN_MB="0", PSG_RANK_FUSED="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "golden_check.py")], env=env, capture_output=True,
+                       text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert "BAD 0" in r.stdout
+    assert _tables(r.stdout).get(4, 0) > 0, r.stdout[-500:]
+
+
 def test_bucket_overflow_list_matches_golden():
     """PSG_BUCKET_CAP=8: tiny aggregation buckets, so most matched rows go through the overflow
     list that every bucket CTA folds - results unchanged."""
