@@ -2366,6 +2366,18 @@ ResultRows Execution::run(bool want_rows) {
       DevBuf cnts(ctx_.pool, 32, ctx_.compute);  // [own bits, global bits, overlap, summed rows]
       PSG_CUDA(cudaMemsetAsync(cnts.p, 0, 32, ctx_.compute));
       if (nr > 1 && kb_heap) {
+        // the owned-bit masks of one period of words (power-of-two N): computed before the barrier,
+        // so off the critical path; PSG_OWN_TABLE=0: partition_of per set bit inside k_or_own
+        static const bool own_table_env = [] {
+          const char* e = std::getenv("PSG_OWN_TABLE");
+          return !(e && e[0] == '0');
+        }();
+        const uint32_t period = own_table_env ? own_period(nr) : 0;
+        DevBuf own_tbl;
+        if (period) {
+          own_tbl = DevBuf(ctx_.pool, static_cast<size_t>(period) * 8, ctx_.compute);
+          launch_own_table(kb_lo, nr, ctx_.rank, own_tbl.as<unsigned long long>(), ctx_.compute);
+        }
         gpu_barrier();  // every rank's local bitmap and flag are complete
         pt.mark("  barrier (rank bitmaps)", ctx_.compute);
         semi_all = DevBuf(ctx_.pool, (words64 + 1) * 8, ctx_.compute);
@@ -2377,7 +2389,8 @@ ResultRows Execution::run(bool want_rows) {
           op.rows[r] = reinterpret_cast<const unsigned long long*>(ctx_.symm_peer[r] + kb_cnt_off);
         }
         launch_or_own(op, words64, kb_lo, ctx_.rank, semi_all.as<unsigned long long>(), agg_kbits_.as<unsigned long long>(),
-                      cnts.as<unsigned long long>(), ctx_.compute);
+                      cnts.as<unsigned long long>(), ctx_.compute, period ? own_tbl.as<unsigned long long>() : nullptr,
+                      period);
         pt.mark("  NVLink OR of the rank bitmaps", ctx_.compute);
         // (a peer may still read this rank's local bitmap: it is rewritten only by the next query's
         // build scan, which follows this query's collectives)

@@ -822,8 +822,29 @@ void launch_own_mask(const unsigned long long* global, unsigned long long* own, 
 /// summed row counts of the ranks' build scans (cnt[3], read from their heaps). Identical on every
 /// rank (same inputs): the re-run decision needs no all-reduce. cnt[0] += own bits, cnt[1] +=
 /// global bits.
+uint32_t own_period(int nparts) {
+  if (nparts < 2 || (nparts & (nparts - 1)) != 0 || nparts > kMaxSlabPeers) return 0;
+  return 128u * static_cast<uint32_t>(nparts);  // 2^(13 + log2 n) keys / 64 per word
+}
+__global__ void k_own_table(int64_t kmin, int nparts, int self, uint32_t period, unsigned long long* table) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= period) return;
+  const uint64_t base = static_cast<uint64_t>(kmin) + (static_cast<uint64_t>(j) << 6);
+  unsigned long long m = 0;
+  for (int b = 0; b < 64; ++b)
+    if (part_of(base + b, static_cast<uint32_t>(nparts)) == static_cast<uint32_t>(self)) m |= 1ULL << b;
+  table[j] = m;
+}
+void launch_own_table(int64_t kmin, int nparts, int self, unsigned long long* table, void* stream) {
+  const uint32_t period = own_period(nparts);
+  if (!period) return;
+  count_launch();
+  k_own_table<<<(period + 127) / 128, 128, 0, S(stream)>>>(kmin, nparts, self, period, table);
+}
+
 __global__ void k_or_own(OrPeers p, uint64_t nwords, int64_t kmin, int self, unsigned long long* __restrict__ global,
-                         unsigned long long* __restrict__ own, unsigned long long* cnt) {
+                         unsigned long long* __restrict__ own, unsigned long long* cnt,
+                         const unsigned long long* __restrict__ table, uint32_t period) {
   unsigned long long no = 0, ng = 0;
   bool dup = false;
   if (blockIdx.x == 0 && threadIdx.x < p.n)  // every rank's row count: sum == global bits unless keys repeat
@@ -832,6 +853,10 @@ __global__ void k_or_own(OrPeers p, uint64_t nwords, int64_t kmin, int self, uns
   auto word = [&](uint64_t w, unsigned long long g, int s) {
     if (s != __popcll(g)) dup = true;
     unsigned long long m = 0, rest = g;
+    if (table) {
+      m = g & __ldg(table + (w & (period - 1)));
+      rest = 0;
+    }
     const uint64_t base = static_cast<uint64_t>(kmin) + (w << 6);
     while (rest) {
       const int b = __ffsll(static_cast<long long>(rest)) - 1;
@@ -877,13 +902,15 @@ __global__ void k_or_own(OrPeers p, uint64_t nwords, int64_t kmin, int self, uns
   }
 }
 void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, unsigned long long* global,
-                   unsigned long long* own, unsigned long long* cnt, void* stream) {
+                   unsigned long long* own, unsigned long long* cnt, void* stream, const unsigned long long* own_table,
+                   uint32_t own_period) {
   if (nwords == 0) return;
   count_launch();
   int sms = 148, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  k_or_own<<<sms * 8, 256, 0, S(stream)>>>(p, nwords, kmin, self, global, own, cnt);
+  k_or_own<<<sms * 8, 256, 0, S(stream)>>>(p, nwords, kmin, self, global, own, cnt, own_table,
+                                           own_table ? own_period : 0);
 }
 
 __global__ void k_peer_barrier(PeerFlags f, const uint32_t* own, int self, int n, uint32_t epoch, unsigned int* err) {

@@ -113,7 +113,13 @@ struct OrPeers {
 /// Global (OR over ranks through NVLink) and own key bitmaps; cnt[0..3] += own bits, global bits,
 /// |= overlap, += summed rows (k_or_own, kernels.cu).
 void launch_or_own(const OrPeers& p, uint64_t nwords, int64_t kmin, int self, unsigned long long* global,
-                   unsigned long long* own, unsigned long long* cnt, void* stream);
+                   unsigned long long* own, unsigned long long* cnt, void* stream,
+                   const unsigned long long* own_table = nullptr, uint32_t own_period = 0);
+/// Ownership masks of one period of bitmap words (power-of-two node counts): partition_of(k) =
+/// bits [13, 13 + log2 n) of k * kPartMul, which depend on k mod 2^(13 + log2 n) only, so word w's
+/// owned-bit mask is table[w mod P], P = own_period(n) words. 0: no period (n not a power of two).
+uint32_t own_period(int nparts);
+void launch_own_table(int64_t kmin, int nparts, int self, unsigned long long* table, void* stream);
 /// Device-side barrier over the symmetric heap (N > 1): flag[p] is peer p's flag array (one word
 /// per source rank), own this rank's. Each rank stores the epoch into every peer's slot for it
 /// (release, system scope), then waits until every slot of its own array holds the epoch
