@@ -82,6 +82,22 @@ def test_partition_of_matches_reference_hash():
             assert list(got) == want
 
 
+def test_partition_of_is_periodic_for_power_of_two_nodes():
+    """The invariant k_own_table / k_or_own rely on (kernels.cu): at power-of-two n the owner of
+    key k depends on k mod 2^(13 + log2 n) only, so the owned-bit mask of bitmap word w (keys
+    kmin + 64 w + b) is the mask of word w mod 128 n."""
+    rng = np.random.default_rng(7)
+    with np.errstate(over="ignore"):
+        for n in (2, 4, 8, 16):
+            period = 128 * n
+            for kmin in (0, -5, int(rng.integers(-(2**40), 2**40))):
+                ws = rng.integers(0, 10**7, size=32)
+                for w in ws:
+                    a = (np.int64(kmin) + np.int64(64 * int(w)) + np.arange(64, dtype=np.int64)).view(np.uint64)
+                    b = (np.int64(kmin) + np.int64(64 * (int(w) % period)) + np.arange(64, dtype=np.int64)).view(np.uint64)
+                    assert np.array_equal(po.partition_of(a, n), po.partition_of(b, n))
+
+
 def test_oracle_local_plans_match_reference_scan(tmp_path):
     """plan_oracle.execute_local (the Q6-analog restatement) against the reference's own
     read_blocking + predicate + sums (tests/golden/local.json), per node."""
